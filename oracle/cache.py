@@ -1,0 +1,70 @@
+"""Degree-ordered static device feature cache (oracle side).
+
+Paper: transmission abstraction §3.2 P:260-273 ("the device cache is
+initialized according to the available memory resource ... figures out which
+part of the mini-batch has been cached ... the remaining part is filtered out
+from the host"); PaGraph template = static cache with ratio r, update
+disabled; cache volume r|V|; transfer
+volume n_attr |V_i| (1-hit) (Eq.6).
+
+Readings: Q7 capacity floor(r*|V|) in IEEE double, ties by lower id
+(SPEC S:188); degree = stored CSR row length.  Q8 hit accounting per
+unique input row of F_L.  Sharded placement over G GPUs:
+owner = rank mod G, local slot = rank div G.
+"""
+from __future__ import annotations
+
+import math
+
+import numpy as np
+
+POLICY_NONE = 0
+POLICY_DEGREE = 1
+
+
+def cache_capacity(ratio: float, n: int, policy: int = POLICY_DEGREE) -> int:
+    """C = floor(ratio * |V|); policy NONE => 0."""
+    if not (0.0 <= ratio <= 1.0) or math.isnan(ratio):
+        raise ValueError("parameter error: ratio must be in [0,1]")
+    if policy == POLICY_NONE:
+        return 0
+    return int(math.floor(float(ratio) * float(n)))
+
+
+def degree_rank(indptr: np.ndarray) -> np.ndarray:
+    """rank[v] = position of v in the order (degree desc, id asc)."""
+    deg = np.diff(np.asarray(indptr, dtype=np.int64))
+    n = deg.shape[0]
+    ids = np.arange(n, dtype=np.int64)
+    order = np.lexsort((ids, -deg))  # primary -deg, secondary id
+    rank = np.empty(n, dtype=np.int64)
+    rank[order] = ids
+    return rank
+
+
+def cache_slots(indptr: np.ndarray, ratio: float, policy: int = POLICY_DEGREE,
+                world: int = 1):
+    """Per vertex: (slot, owner, local_slot).  slot = rank if rank < C else -1.
+
+    For G = world shards: owner = rank mod G, local_slot = rank div G
+    (both -1 for uncached vertices)."""
+    n = len(indptr) - 1
+    C = cache_capacity(ratio, n, policy)
+    rank = degree_rank(indptr)
+    cached = rank < C
+    slot = np.where(cached, rank, -1)
+    owner = np.where(cached, rank % world, -1)
+    local = np.where(cached, rank // world, -1)
+    return slot, owner, local
+
+
+def access_counts(slot: np.ndarray, owner: np.ndarray, rows: np.ndarray, me: int = 0):
+    """Counters over the unique rows F_L (Q8):
+    hits = #{slot >= 0}; peer = #{hit and owner != me}; host misses = rows - hits."""
+    rows = np.asarray(rows, dtype=np.int64)
+    s = slot[rows]
+    hit = s >= 0
+    hits = int(hit.sum())
+    peer = int((hit & (owner[rows] != me)).sum())
+    return dict(rows=int(rows.size), hits=hits, hits_local=hits - peer, hits_peer=peer,
+                misses_host=int(rows.size) - hits)
