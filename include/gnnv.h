@@ -1,0 +1,296 @@
+/*
+ * gnnv.h — C-ABI of libgnnv, the B200-native hot path of one mini-batch
+ * GraphSAGE/GCN training iteration as decomposed by GNNavigator
+ * (arXiv 2404.09544): sample / transfer / compute.
+ *
+ * Citations: P:n = PAPER.md line n, S:n = SPEC.md line n (the paper's
+ * equations and Algorithm 1 are restated in DESIGN.md §1).
+ *
+ * Conventions
+ *  - Every call returns gnnv_status; no exception crosses the ABI.  On error
+ *    gnnv_last_error() (thread-local) holds a one-line message.
+ *      GNNV_ERR_PARAM        "parameter error": ratio not in
+ *                            [0,1], fanout < 1, L < 1, n_seeds < 1 or > max, a seed
+ *                            id outside [0,N) or repeated, dimension mismatch.
+ *      GNNV_ERR_STATE        "state error": call order violated.
+ *      GNNV_ERR_OOM          device/pinned allocation failed; the message carries
+ *                            the requested bytes.
+ *      GNNV_ERR_CUDA         a CUDA runtime error.
+ *      GNNV_ERR_COMM         an NCCL error.
+ *      GNNV_ERR_UNSUPPORTED  valid but not built (FIFO/LRU policies S:183,
+ *                            Bernoulli/layer-wise/subgraph-wise samplers S:96).
+ *    Device-side range checks (seed ids) set a device flag that is reported
+ *    as GNNV_ERR_PARAM at the next synchronising call on that handle.
+ *  - Ownership.  Opaque handles are owned by the library and released with
+ *    the matching *_free.  Device buffers passed as `d_*` pointers are owned
+ *    by the caller; the library never frees them.  Host features are BORROWED
+ *    by gnnv_graph_load (registered in place, zero-copy) and must outlive the
+ *    graph.  The CSR is copied to the device.
+ *  - Streams.  `gnnv_stream` is a cudaStream_t (NULL = legacy default
+ *    stream).  Kernel-launching calls are stream-ordered and do NOT
+ *    synchronise unless documented.  Sizes produced by sampling live on the
+ *    device; every downstream kernel reads them there, so a whole iteration
+ *    runs without a host round trip.
+ *  - Layouts.  Row-major everywhere.  A feature/activation matrix with
+ *    logical width d is stored with row stride gnnv_row_stride(d) = d rounded
+ *    up to a multiple of 4 floats (16-byte rows); padding columns are written
+ *    as 0 by every kernel that produces them.  The graph feature table may
+ *    use any stride >= d that is a multiple of 4.
+ *  - Determinism.  gnnv_sample output is a pure function of (graph, seeds,
+ *    fanouts, rng_seed): independent of device, stream, rank and world size.
+ *    gnnv_gather rows are bit-exact copies.
+ */
+#ifndef GNNV_H_
+#define GNNV_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GNNV_MAX_LAYERS 8
+#define GNNV_VERSION "0.1.0"
+
+typedef enum gnnv_status {
+  GNNV_OK = 0,
+  GNNV_ERR_PARAM = 1,
+  GNNV_ERR_STATE = 2,
+  GNNV_ERR_OOM = 3,
+  GNNV_ERR_CUDA = 4,
+  GNNV_ERR_COMM = 5,
+  GNNV_ERR_UNSUPPORTED = 6
+} gnnv_status;
+
+typedef struct gnnv_graph gnnv_graph;
+typedef struct gnnv_cache gnnv_cache;
+typedef struct gnnv_blocks gnnv_blocks;
+typedef struct gnnv_trainer gnnv_trainer;
+typedef struct gnnv_comm gnnv_comm;
+typedef void* gnnv_stream; /* cudaStream_t */
+
+/* Cache update policy.  Only the static PaGraph template (DEGREE,
+ * P:290) and NONE (pyg-like, ratio treated as 0) are built. */
+typedef enum { GNNV_POLICY_NONE = 0, GNNV_POLICY_DEGREE = 1, GNNV_POLICY_FIFO = 2, GNNV_POLICY_LRU = 3 } gnnv_policy;
+/* Cache placement over the GPUs of one box.  REPLICA: every rank holds the
+ * C = floor(ratio*N) hottest rows.  SHARDED: rank r holds the rows whose
+ * degree rank i satisfies i mod G == r (at local slot i div G); peers' rows
+ * are read over NVLink (CUDA IPC).  SHARDED_LOCAL: the same G-way layout with
+ * all G shards resident on this device (used to test the routing on one GPU;
+ * G = `virtual_shards`). */
+typedef enum { GNNV_PLACE_REPLICA = 0, GNNV_PLACE_SHARDED = 1, GNNV_PLACE_SHARDED_LOCAL = 2 } gnnv_placement;
+typedef enum { GNNV_KIND_SAGE = 0, GNNV_KIND_GCN = 1 } gnnv_kind;
+typedef enum { GNNV_AGGR_MEAN = 0, GNNV_AGGR_SUM = 1 } gnnv_aggr;
+typedef enum { GNNV_ACT_NONE = 0, GNNV_ACT_RELU = 1 } gnnv_act;
+/* Precision of the dense transform (reading Q18): FP32 = SIMT FFMA;
+ * BF16 = operands rounded RNE to bf16, fp32 accumulation on tcgen05 tensor
+ * cores.  Aggregation (SpMM) is fp32 in both modes. */
+typedef enum { GNNV_PREC_FP32 = 0, GNNV_PREC_BF16 = 1 } gnnv_prec;
+
+/* ------------------------------------------------------------------ misc */
+const char* gnnv_last_error(void);
+const char* gnnv_version(void);
+/* d rounded up to a multiple of 4 (floats). */
+int32_t gnnv_row_stride(int32_t d);
+
+/* ----------------------------------------------------------------- graph */
+/* G(V,E) with features h^0_v and labels (CSR invariants S:25-27).
+ *  indptr   host int64[n_nodes+1], indptr[0]=0, non-decreasing, indptr[n]=nnz
+ *  indices  host int32[nnz], every id in [0,n_nodes); rows need not be sorted,
+ *           but sampled positions refer to the order given (reading Q5)
+ *  host_feats host float32[n_nodes * row_stride], borrowed (registered
+ *           mapped/read-only in place; must stay alive until gnnv_graph_free)
+ *  feat_dim logical d (n_attr); row_stride >= d, multiple of 4
+ *  labels   host int32[n_nodes] in [0,n_classes); copied
+ *  device   CUDA ordinal the graph lives on
+ * Errors: PARAM on size/stride violations; OOM; CUDA.  Synchronous. */
+gnnv_status gnnv_graph_load(const int64_t* indptr, const int32_t* indices, int64_t n_nodes, int64_t nnz,
+                            const float* host_feats, int32_t feat_dim, int32_t row_stride,
+                            const int32_t* labels, int32_t n_classes, int32_t device, gnnv_graph** out);
+gnnv_status gnnv_graph_free(gnnv_graph* g);
+/* Device pointers of the graph (valid while g lives). */
+typedef struct {
+  int64_t n_nodes, nnz;
+  int32_t feat_dim, row_stride, n_classes, device;
+  const int64_t* d_indptr;
+  const int32_t* d_indices;
+  const int32_t* d_labels;
+  const float* d_host_feats; /* device-mapped alias of the pinned host table */
+} gnnv_graph_view;
+gnnv_status gnnv_graph_info(const gnnv_graph* g, gnnv_graph_view* out);
+
+/* ------------------------------------------------------------------ comm */
+/* NCCL over NVLink/NVSwitch, one process per GPU.  The 128-byte unique id is
+ * produced on rank 0 and exchanged by the caller (torch process group). */
+gnnv_status gnnv_comm_unique_id(void* out128);
+gnnv_status gnnv_comm_init(int32_t rank, int32_t world, const void* unique_id128, int32_t device, gnnv_comm** out);
+gnnv_status gnnv_comm_free(gnnv_comm* c);
+/* In-place sum over ranks of d_buf[0:n) (fp32), stream-ordered. */
+gnnv_status gnnv_allreduce_sum(gnnv_comm* c, float* d_buf, int64_t n, gnnv_stream s);
+
+/* ----------------------------------------------------------------- cache */
+/* Device feature cache: "initialized according to the available memory"
+ * (§3.2), PaGraph static degree template.  Capacity
+ * C = floor(ratio * N) in IEEE double; vertices ordered by
+ * (degree desc, id asc); slot(v) = rank(v) if rank(v) < C else -1.
+ *  comm            NULL => single GPU; required for SHARDED
+ *  virtual_shards  G for SHARDED_LOCAL (>=1), ignored otherwise
+ * Errors: PARAM (ratio not in [0,1]); UNSUPPORTED (FIFO/LRU); OOM (message
+ * carries the bytes, Γ_cache = C * row_stride * 4, Eq.10).
+ * Synchronous (fills the rows from the pinned host table). */
+gnnv_status gnnv_cache_build(gnnv_graph* g, double ratio, int32_t policy, int32_t placement,
+                             gnnv_comm* comm, int32_t virtual_shards, gnnv_cache** out);
+gnnv_status gnnv_cache_free(gnnv_cache* c);
+typedef struct {
+  int64_t capacity;     /* C: cached rows over all shards */
+  int64_t local_rows;   /* rows resident on this device */
+  int64_t bytes;        /* Γ_cache on this device */
+  int32_t world, rank;  /* shard count G and this device's shard */
+  int32_t placement;
+  const int32_t* d_slot;   /* int32[N]: degree rank if cached else -1 */
+  const int32_t* d_order;  /* int32[N]: vertices in (degree desc, id asc) order */
+} gnnv_cache_view;
+gnnv_status gnnv_cache_info(const gnnv_cache* c, gnnv_cache_view* out);
+
+/* ---------------------------------------------------------------- blocks */
+/* Workspace for the sampled blocks b_0..b_{L-1} of one rank, sized for the
+ * upper bound n_{h+1} <= min(N, n_h (1 + k_h)) (Eq.12, tau=1). */
+gnnv_status gnnv_blocks_create(gnnv_graph* g, int32_t max_seeds, const int32_t* fanouts, int32_t L,
+                               gnnv_blocks** out);
+gnnv_status gnnv_blocks_free(gnnv_blocks* b);
+
+/* SubgraphSampling (Algorithm 1 line 2) with the unified node-wise
+ * sampler of Eq.2: for every v in F_h, min(k_h, deg v) distinct
+ * neighbours uniformly without replacement (reading Q1), Philox4x32-10 draws
+ * keyed by (rng_seed; hop, node, draw) fed to Floyd's algorithm (Q4),
+ * ascending CSR position (Q5); F_{h+1} = F_h ++ new ids in first-appearance
+ * order (Q3, Q6).  fanouts[0] applies to the seeds (Q2).
+ *  d_seeds  device int32[n_seeds], unique ids in [0,N) (Q19); fanouts/L
+ *           must equal the ones given to gnnv_blocks_create (fanout <= created)
+ * Outputs stay in `b` until the next gnnv_sample on `b`.  Stream-ordered, no
+ * host sync.  Errors: PARAM (n_seeds, fanouts; bad seed ids reported at the
+ * next gnnv_blocks_info(sync=1)). */
+gnnv_status gnnv_sample(gnnv_graph* g, const int32_t* d_seeds, int32_t n_seeds, const int32_t* fanouts,
+                        int32_t L, uint64_t rng_seed, gnnv_blocks* b, gnnv_stream s);
+
+/* Block b_h: dst = F_h (n_dst rows), src = F_{h+1} (n_src rows, dst prefix
+ * first).  indptr int32[n_dst+1], indices int32[nnz] = local ids into
+ * F_{h+1}; src_global = F_{h+1} (global ids).  max_* are the capacities. */
+typedef struct {
+  int64_t n_dst, n_src, nnz;
+  int64_t max_dst, max_src, max_nnz;
+  const int32_t* d_indptr;
+  const int32_t* d_indices;
+  const int32_t* d_src_global;
+} gnnv_block_view;
+/* Fills per_hop[0..L-1].  sync=1: synchronises `s`, copies the sizes to the
+ * host and reports a pending device error; sync=0: sizes are -1 and only the
+ * pointers and capacities are valid. */
+gnnv_status gnnv_blocks_info(gnnv_blocks* b, int32_t sync, gnnv_stream s, gnnv_block_view* per_hop);
+/* Device int32[2L+1]: n_0..n_L then nnz_0..nnz_{L-1} (written by gnnv_sample). */
+const int32_t* gnnv_blocks_device_sizes(const gnnv_blocks* b);
+int32_t gnnv_blocks_num_layers(const gnnv_blocks* b);
+
+/* ---------------------------------------------------------------- gather */
+/* Transfer (Algorithm 1 line 3; §3.2; Eq.6):
+ * X[i,:] = feat[F_L[i], :] for i < n_L, bit-exact, full row stride of the
+ * graph.  Source per row: local HBM cache slot, a peer GPU's shard over
+ * NVLink, or the pinned host table (zero-copy over PCIe) on a miss.
+ *  d_X      device float32[max n_L * graph row_stride] (caller-owned)
+ *  d_stats  device int64[4] accumulated: rows, hits_local, hits_peer,
+ *           misses_host (reading Q8: per unique row of F_L); may be NULL
+ * Stream-ordered.  Errors: STATE if b was never sampled. */
+gnnv_status gnnv_gather(const gnnv_cache* c, const gnnv_blocks* b, float* d_X, int64_t* d_stats, gnnv_stream s);
+
+/* ---------------------------------------------------------------- layers */
+typedef struct {
+  int32_t d_in, d_out;
+  int32_t in_stride;  /* row stride of H_src / dH_src (>= d_in, %4==0) */
+  int32_t kind;       /* gnnv_kind */
+  int32_t aggr;       /* gnnv_aggr */
+  int32_t act;        /* gnnv_act */
+  int32_t prec;       /* gnnv_prec */
+} gnnv_layer_desc;
+
+/* GNN layer i in 1..L on block b_{L-i} (Eq.1; Algorithm 1 lines
+ * 5-6 P:110-111; reading Q11):
+ *   SAGE: A = Agg(H_src), H_dst = act(H_src[0:n_dst] W_s + A W_n + b)
+ *   GCN : A = (h_v + sum_u h_u)/(c_v+1) (or sum), H_dst = act(A W + b)
+ *  d_Hsrc  [n_src x in_stride]; d_W [(2 or 1)*d_in x d_out] row-major
+ *          ([W_s; W_n] for SAGE); d_b [d_out]
+ *  d_Hdst  [n_dst x row_stride(d_out)] output; d_saveA [n_dst x
+ *          row_stride(d_in)] the aggregate, kept for the backward.
+ * Stream-ordered.  Errors: PARAM (layer range, dims), STATE. */
+gnnv_status gnnv_layer_fwd(gnnv_blocks* b, int32_t layer, const gnnv_layer_desc* ld, const float* d_Hsrc,
+                           const float* d_W, const float* d_b, float* d_Hdst, float* d_saveA, gnnv_stream s);
+
+/* Backward of gnnv_layer_fwd (Algorithm 1 line 8):
+ * G' = G * 1[H_dst > 0] (ReLU); dW = [H_dst|A]^T G' (SAGE) or A^T G' (GCN);
+ * db = sum_rows G'; if d_Gsrc: dH_src = P^T (G' W_n^T) + [G' W_s^T; 0].
+ *  d_Gdst  dL/dH_dst (post-activation) [n_dst x row_stride(d_out)]
+ *  d_Gsrc  [n_src x in_stride] overwritten; NULL for layer 1
+ *  d_dW, d_db overwritten (same layout as W, b).
+ * Stream-ordered.  dW/db are deterministic (fixed-order split-K
+ * reduction); dH_src uses fp32 atomics (order-dependent rounding). */
+gnnv_status gnnv_layer_bwd(gnnv_blocks* b, int32_t layer, const gnnv_layer_desc* ld, const float* d_Gdst,
+                           const float* d_Hdst, const float* d_Hsrc, const float* d_saveA, const float* d_W,
+                           float* d_Gsrc, float* d_dW, float* d_db, gnnv_stream s);
+
+/* Softmax cross-entropy over the n_0 seeds (Algorithm 1 line 7 P:112):
+ * loss = (1/n_global) sum_i [lse(z_i) - z_i[y_i]], dz = (softmax - onehot)/n_global.
+ *  d_logits [n_0 x stride], labels from the graph indexed by F_0.
+ *  d_loss   device float[1] (overwritten).  Deterministic. */
+gnnv_status gnnv_ce_loss(gnnv_blocks* b, const gnnv_graph* g, const float* d_logits, int32_t n_classes,
+                         int32_t stride, int32_t n_global, float* d_loss, float* d_dlogits, gnnv_stream s);
+
+/* Plain gradient descent p <- p - lr g. */
+gnnv_status gnnv_sgd(float* d_params, const float* d_grads, int64_t n, float lr, gnnv_stream s);
+
+/* --------------------------------------------------------------- trainer */
+typedef struct {
+  int32_t L;
+  int32_t dims[GNNV_MAX_LAYERS + 1]; /* d_0 = feat_dim, ..., d_L = n_classes */
+  int32_t fanouts[GNNV_MAX_LAYERS];
+  int32_t max_seeds;
+  int32_t kind, aggr, prec;
+} gnnv_model_desc;
+
+/* Per-phase device times in ms (Eq.4-8 decomposition). */
+typedef struct {
+  float sample_ms, gather_ms, fwd_ms, loss_ms, bwd_ms, allreduce_ms, update_ms, total_ms;
+} gnnv_step_timing;
+
+/* A whole iteration runner.  Parameters are a flat fp32 vector: for each
+ * layer i: W_i [(2 or 1) d_{i-1} x d_i] row-major, then b_i [d_i].
+ *  host_params  initial values (copied); comm NULL => single GPU. */
+gnnv_status gnnv_trainer_create(gnnv_graph* g, gnnv_cache* c, const gnnv_model_desc* md,
+                                const float* host_params, gnnv_comm* comm, gnnv_trainer** out);
+gnnv_status gnnv_trainer_free(gnnv_trainer* t);
+int64_t gnnv_trainer_num_params(const gnnv_trainer* t);
+/* Copies params (and grads of the last step, if d_grads_out/host) to host; synchronises. */
+gnnv_status gnnv_trainer_get(gnnv_trainer* t, float* host_params, float* host_grads);
+gnnv_status gnnv_trainer_set_params(gnnv_trainer* t, const float* host_params);
+gnnv_blocks* gnnv_trainer_blocks(gnnv_trainer* t);
+/* Device pointers of the trainer's activations for layer i (0 = X). */
+gnnv_status gnnv_trainer_activation(gnnv_trainer* t, int32_t i, const float** d_H, int32_t* stride);
+
+/* One iteration of Algorithm 1 on this rank's seed slice:
+ * sample -> gather -> L x (aggregate, combine) -> loss -> L x backward ->
+ * allreduce(grads, loss) over comm -> SGD.
+ *  seeds        int32[n_seeds]; seeds_on_host=1: host memory (copied H2D
+ *               inside the call), else device memory
+ *  n_global     seeds of the iteration over all ranks (loss scale 1/n_global)
+ *  loss_out     host float (loss summed over ranks) or NULL (then the call
+ *               does not synchronise unless tm != NULL)
+ *  tm           per-phase device times or NULL
+ * Stream-ordered on `s`. */
+gnnv_status gnnv_step(gnnv_trainer* t, const int32_t* seeds, int32_t n_seeds, int32_t seeds_on_host,
+                      int32_t n_global, uint64_t rng_seed, float lr, float* loss_out, gnnv_step_timing* tm,
+                      gnnv_stream s);
+/* Device counters of the last step's gather: int64[4] (see gnnv_gather). */
+gnnv_status gnnv_trainer_stats(gnnv_trainer* t, int64_t* host_stats4);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GNNV_H_ */

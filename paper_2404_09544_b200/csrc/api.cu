@@ -1,0 +1,369 @@
+// C-ABI glue: errors, graph load, NCCL comm, blocks handles (host code).
+#include <dlfcn.h>
+#include <limits.h>
+#include <string.h>
+
+#include <algorithm>
+#include <mutex>
+
+#include "common.cuh"
+#include "nccl.h"
+
+namespace gnnv {
+
+static thread_local std::string g_last_error;
+void set_error(const std::string& msg) { g_last_error = msg; }
+const char* get_error() { return g_last_error.c_str(); }
+
+void* dmalloc(size_t bytes, const char* what) {
+  if (bytes == 0) bytes = 16;
+  void* p = nullptr;
+  cudaError_t e = cudaMalloc(&p, bytes);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    char buf[256];
+    snprintf(buf, sizeof(buf), "device allocation of %zu bytes for %s failed: %s", bytes, what,
+             cudaGetErrorString(e));
+    throw Error{e == cudaErrorMemoryAllocation ? GNNV_ERR_OOM : GNNV_ERR_CUDA, buf};
+  }
+  return p;
+}
+
+void dfree(void* p) {
+  if (p) cudaFree(p);
+}
+
+int num_sms() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+__global__ void k_fill_i32(int32_t* p, int64_t n, int32_t v) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    p[i] = v;
+}
+
+// ------------------------------------------------------------------ NCCL
+struct NcclApi {
+  void* lib = nullptr;
+  decltype(&ncclGetUniqueId) getUniqueId = nullptr;
+  decltype(&ncclCommInitRank) commInitRank = nullptr;
+  decltype(&ncclCommDestroy) commDestroy = nullptr;
+  decltype(&ncclAllReduce) allReduce = nullptr;
+  decltype(&ncclGetErrorString) errStr = nullptr;
+};
+
+static NcclApi& nccl() {
+  static NcclApi api;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    const char* env = getenv("GNNV_NCCL_LIB");
+    const char* names[] = {env, "libnccl.so.2", "libnccl.so"};
+    for (const char* n : names) {
+      if (!n) continue;
+      api.lib = dlopen(n, RTLD_NOW | RTLD_GLOBAL);
+      if (api.lib) break;
+    }
+    if (!api.lib) return;
+    api.getUniqueId = (decltype(api.getUniqueId))dlsym(api.lib, "ncclGetUniqueId");
+    api.commInitRank = (decltype(api.commInitRank))dlsym(api.lib, "ncclCommInitRank");
+    api.commDestroy = (decltype(api.commDestroy))dlsym(api.lib, "ncclCommDestroy");
+    api.allReduce = (decltype(api.allReduce))dlsym(api.lib, "ncclAllReduce");
+    api.errStr = (decltype(api.errStr))dlsym(api.lib, "ncclGetErrorString");
+  });
+  if (!api.lib || !api.getUniqueId || !api.commInitRank || !api.allReduce)
+    throw Error{GNNV_ERR_COMM, "NCCL library not found (set GNNV_NCCL_LIB or preload libnccl.so.2)"};
+  return api;
+}
+
+static void nccl_check(ncclResult_t r, const char* what) {
+  if (r != ncclSuccess) {
+    NcclApi& a = nccl();
+    throw Error{GNNV_ERR_COMM, std::string(what) + ": " + (a.errStr ? a.errStr(r) : "nccl error")};
+  }
+}
+
+}  // namespace gnnv
+
+using namespace gnnv;
+
+void* gnnv_blocks::ensure_scratch(size_t bytes, cudaStream_t s) {
+  if (bytes <= scratch_bytes) return scratch;
+  if (scratch) {
+    GNNV_TRY_CUDA(cudaStreamSynchronize(s));
+    dfree(scratch);
+    scratch = nullptr;
+    scratch_bytes = 0;
+  }
+  size_t want = std::max(bytes, (size_t)1 << 20);
+  scratch = dmalloc(want, "layer scratch");
+  scratch_bytes = want;
+  return scratch;
+}
+
+extern "C" {
+
+const char* gnnv_last_error(void) { return get_error(); }
+const char* gnnv_version(void) { return GNNV_VERSION " sm_100a"; }
+int32_t gnnv_row_stride(int32_t d) { return row_stride(d); }
+
+// ------------------------------------------------------------------ graph
+gnnv_status gnnv_graph_load(const int64_t* indptr, const int32_t* indices, int64_t n_nodes, int64_t nnz,
+                            const float* host_feats, int32_t feat_dim, int32_t stride, const int32_t* labels,
+                            int32_t n_classes, int32_t device, gnnv_graph** out) {
+  return guarded([&] {
+    GNNV_REQUIRE(out && indptr && (indices || nnz == 0) && host_feats && labels, GNNV_ERR_PARAM,
+                 "graph_load: null pointer");
+    GNNV_REQUIRE(n_nodes >= 1 && n_nodes < INT32_MAX && nnz >= 0, GNNV_ERR_PARAM,
+                 "graph_load: n_nodes must be in [1, 2^31-1), nnz >= 0");
+    GNNV_REQUIRE(feat_dim >= 1 && stride >= feat_dim && stride % 4 == 0, GNNV_ERR_PARAM,
+                 "graph_load: row_stride must be >= feat_dim and a multiple of 4");
+    GNNV_REQUIRE(n_classes >= 1, GNNV_ERR_PARAM, "graph_load: n_classes < 1");
+    GNNV_REQUIRE(indptr[0] == 0 && indptr[n_nodes] == nnz, GNNV_ERR_PARAM,
+                 "graph_load: indptr[0] must be 0 and indptr[n] == nnz");
+    GNNV_REQUIRE(((uintptr_t)host_feats & 15) == 0, GNNV_ERR_PARAM, "graph_load: host_feats must be 16-byte aligned");
+    GNNV_TRY_CUDA(cudaSetDevice(device));
+    gnnv_graph* g = new gnnv_graph();
+    g->device = device;
+    g->n = n_nodes;
+    g->nnz = nnz;
+    g->d = feat_dim;
+    g->stride = stride;
+    g->n_classes = n_classes;
+    try {
+      g->d_indptr = (int64_t*)dmalloc((n_nodes + 1) * sizeof(int64_t), "indptr");
+      g->d_indices = (int32_t*)dmalloc(std::max<int64_t>(nnz, 1) * sizeof(int32_t), "indices");
+      g->d_labels = (int32_t*)dmalloc(n_nodes * sizeof(int32_t), "labels");
+      GNNV_TRY_CUDA(cudaMemcpy(g->d_indptr, indptr, (n_nodes + 1) * sizeof(int64_t), cudaMemcpyHostToDevice));
+      if (nnz) GNNV_TRY_CUDA(cudaMemcpy(g->d_indices, indices, nnz * sizeof(int32_t), cudaMemcpyHostToDevice));
+      GNNV_TRY_CUDA(cudaMemcpy(g->d_labels, labels, n_nodes * sizeof(int32_t), cudaMemcpyHostToDevice));
+      size_t fbytes = (size_t)n_nodes * stride * sizeof(float);
+      cudaError_t e = cudaHostRegister((void*)host_feats, fbytes,
+                                       cudaHostRegisterMapped | cudaHostRegisterPortable | cudaHostRegisterReadOnly);
+      if (e == cudaErrorHostMemoryAlreadyRegistered) {
+        cudaGetLastError();
+      } else if (e != cudaSuccess) {
+        cudaGetLastError();
+        // read-only registration is not available everywhere; retry without it
+        e = cudaHostRegister((void*)host_feats, fbytes, cudaHostRegisterMapped | cudaHostRegisterPortable);
+        if (e != cudaSuccess && e != cudaErrorHostMemoryAlreadyRegistered) GNNV_TRY_CUDA(e);
+        cudaGetLastError();
+        g->registered = (e == cudaSuccess);
+      } else {
+        g->registered = true;
+      }
+      void* dptr = nullptr;
+      GNNV_TRY_CUDA(cudaHostGetDevicePointer(&dptr, (void*)host_feats, 0));
+      g->h_feats = host_feats;
+      g->d_feats = (const float*)dptr;
+    } catch (...) {
+      gnnv_graph_free(g);
+      throw;
+    }
+    *out = g;
+  });
+}
+
+gnnv_status gnnv_graph_free(gnnv_graph* g) {
+  if (!g) return GNNV_OK;
+  cudaSetDevice(g->device);
+  dfree(g->d_indptr);
+  dfree(g->d_indices);
+  dfree(g->d_labels);
+  if (g->registered && g->h_feats) cudaHostUnregister((void*)g->h_feats);
+  delete g;
+  return GNNV_OK;
+}
+
+gnnv_status gnnv_graph_info(const gnnv_graph* g, gnnv_graph_view* o) {
+  return guarded([&] {
+    GNNV_REQUIRE(g && o, GNNV_ERR_PARAM, "graph_info: null");
+    o->n_nodes = g->n;
+    o->nnz = g->nnz;
+    o->feat_dim = g->d;
+    o->row_stride = g->stride;
+    o->n_classes = g->n_classes;
+    o->device = g->device;
+    o->d_indptr = g->d_indptr;
+    o->d_indices = g->d_indices;
+    o->d_labels = g->d_labels;
+    o->d_host_feats = g->d_feats;
+  });
+}
+
+// ------------------------------------------------------------------- comm
+gnnv_status gnnv_comm_unique_id(void* out128) {
+  return guarded([&] {
+    GNNV_REQUIRE(out128, GNNV_ERR_PARAM, "comm_unique_id: null");
+    ncclUniqueId id;
+    nccl_check(nccl().getUniqueId(&id), "ncclGetUniqueId");
+    memcpy(out128, &id, sizeof(id));
+  });
+}
+
+gnnv_status gnnv_comm_init(int32_t rank, int32_t world, const void* uid, int32_t device, gnnv_comm** out) {
+  return guarded([&] {
+    GNNV_REQUIRE(out && uid && world >= 1 && rank >= 0 && rank < world, GNNV_ERR_PARAM, "comm_init: bad rank/world");
+    GNNV_TRY_CUDA(cudaSetDevice(device));
+    ncclUniqueId id;
+    memcpy(&id, uid, sizeof(id));
+    ncclComm_t comm = nullptr;
+    nccl_check(nccl().commInitRank(&comm, world, id, rank), "ncclCommInitRank");
+    gnnv_comm* c = new gnnv_comm();
+    c->rank = rank;
+    c->world = world;
+    c->device = device;
+    c->nccl = comm;
+    *out = c;
+  });
+}
+
+gnnv_status gnnv_comm_free(gnnv_comm* c) {
+  if (!c) return GNNV_OK;
+  if (c->nccl) {
+    try {
+      nccl().commDestroy((ncclComm_t)c->nccl);
+    } catch (...) {
+    }
+  }
+  delete c;
+  return GNNV_OK;
+}
+
+gnnv_status gnnv_allreduce_sum(gnnv_comm* c, float* d_buf, int64_t n, gnnv_stream s) {
+  return guarded([&] {
+    GNNV_REQUIRE(c && d_buf && n >= 0, GNNV_ERR_PARAM, "allreduce: bad args");
+    if (c->world == 1 || n == 0) return;
+    nccl_check(nccl().allReduce(d_buf, d_buf, (size_t)n, ncclFloat32, ncclSum, (ncclComm_t)c->nccl,
+                                (cudaStream_t)s),
+               "ncclAllReduce");
+  });
+}
+
+// ----------------------------------------------------------------- blocks
+gnnv_status gnnv_blocks_create(gnnv_graph* g, int32_t max_seeds, const int32_t* fanouts, int32_t L,
+                               gnnv_blocks** out) {
+  return guarded([&] {
+    GNNV_REQUIRE(g && out && fanouts, GNNV_ERR_PARAM, "blocks_create: null");
+    GNNV_REQUIRE(L >= 1 && L <= GNNV_MAX_LAYERS, GNNV_ERR_PARAM, "blocks_create: L must be in [1, 8]");
+    GNNV_REQUIRE(max_seeds >= 1 && max_seeds <= g->n, GNNV_ERR_PARAM, "blocks_create: max_seeds must be in [1, N]");
+    for (int h = 0; h < L; ++h)
+      GNNV_REQUIRE(fanouts[h] >= 1 && fanouts[h] <= 32, GNNV_ERR_PARAM, "blocks_create: fanout must be in [1, 32]");
+    GNNV_TRY_CUDA(cudaSetDevice(g->device));
+    gnnv_blocks* b = new gnnv_blocks();
+    b->g = g;
+    b->L = L;
+    b->max_n[0] = max_seeds;
+    int64_t ell_max = 1, cnt_max = 1, tiles_max = 1;
+    for (int h = 0; h < L; ++h) {
+      b->fanouts[h] = fanouts[h];
+      b->max_n[h + 1] = std::min<int64_t>(g->n, b->max_n[h] * (1 + (int64_t)fanouts[h]));
+      b->max_nnz[h] = b->max_n[h] * fanouts[h];
+      ell_max = std::max(ell_max, b->max_nnz[h]);
+      cnt_max = std::max(cnt_max, b->max_n[h]);
+      tiles_max = std::max(tiles_max, ceil_div(b->max_n[h], 256));
+    }
+    try {
+      GNNV_REQUIRE(ell_max + 2 < INT32_MAX, GNNV_ERR_PARAM, "blocks_create: sampled slots exceed int32");
+      b->d_tag = (int32_t*)dmalloc(g->n * sizeof(int32_t), "relabel tags");
+      k_fill_i32<<<num_sms() * 4, 256>>>(b->d_tag, g->n, INT_MIN);
+      GNNV_CHECK_LAUNCH();
+      b->d_F = (int32_t*)dmalloc(b->max_n[L] * sizeof(int32_t), "frontiers");
+      b->d_ell = (int32_t*)dmalloc(ell_max * sizeof(int32_t), "sample slots");
+      b->d_cnt = (int32_t*)dmalloc(cnt_max * sizeof(int32_t), "sample counts");
+      for (int h = 0; h < L; ++h) {
+        b->d_indptr[h] = (int32_t*)dmalloc((b->max_n[h] + 1) * sizeof(int32_t), "block indptr");
+        b->d_indices[h] = (int32_t*)dmalloc(std::max<int64_t>(b->max_nnz[h], 1) * sizeof(int32_t), "block indices");
+      }
+      b->d_sizes = (int32_t*)dmalloc((2 * L + 2) * sizeof(int32_t), "sizes");
+      GNNV_TRY_CUDA(cudaMemset(b->d_sizes, 0, (2 * L + 2) * sizeof(int32_t)));
+      b->scan_words = tiles_max + 1;
+      b->d_scan = (unsigned long long*)dmalloc(b->scan_words * sizeof(unsigned long long), "scan status");
+      GNNV_TRY_CUDA(cudaDeviceSynchronize());
+    } catch (...) {
+      gnnv_blocks_free(b);
+      throw;
+    }
+    *out = b;
+  });
+}
+
+gnnv_status gnnv_blocks_free(gnnv_blocks* b) {
+  if (!b) return GNNV_OK;
+  dfree(b->d_tag);
+  dfree(b->d_F);
+  dfree(b->d_ell);
+  dfree(b->d_cnt);
+  for (int h = 0; h < GNNV_MAX_LAYERS; ++h) {
+    dfree(b->d_indptr[h]);
+    dfree(b->d_indices[h]);
+  }
+  dfree(b->d_sizes);
+  dfree(b->d_scan);
+  dfree(b->scratch);
+  delete b;
+  return GNNV_OK;
+}
+
+gnnv_status gnnv_sample(gnnv_graph* g, const int32_t* d_seeds, int32_t n_seeds, const int32_t* fanouts, int32_t L,
+                        uint64_t rng_seed, gnnv_blocks* b, gnnv_stream s) {
+  return guarded([&] {
+    GNNV_REQUIRE(g && b && d_seeds && fanouts, GNNV_ERR_PARAM, "sample: null");
+    GNNV_REQUIRE(b->g == g, GNNV_ERR_STATE, "sample: blocks were created for another graph");
+    GNNV_REQUIRE(L == b->L, GNNV_ERR_PARAM, "sample: L differs from blocks_create");
+    for (int h = 0; h < L; ++h)
+      GNNV_REQUIRE(fanouts[h] == b->fanouts[h], GNNV_ERR_PARAM, "sample: fanouts differ from blocks_create");
+    GNNV_REQUIRE(n_seeds >= 1 && n_seeds <= b->max_n[0], GNNV_ERR_PARAM, "sample: n_seeds must be in [1, max_seeds]");
+    launch_sample(g, b, d_seeds, n_seeds, rng_seed, (cudaStream_t)s);
+    b->sampled = true;
+  });
+}
+
+gnnv_status gnnv_blocks_info(gnnv_blocks* b, int32_t sync, gnnv_stream s, gnnv_block_view* v) {
+  return guarded([&] {
+    GNNV_REQUIRE(b && v, GNNV_ERR_PARAM, "blocks_info: null");
+    std::vector<int32_t> sz(2 * b->L + 2, -1);
+    if (sync) {
+      GNNV_REQUIRE(b->sampled, GNNV_ERR_STATE, "blocks_info: gnnv_sample has not run on these blocks");
+      GNNV_TRY_CUDA(cudaMemcpyAsync(sz.data(), b->d_sizes, sz.size() * sizeof(int32_t), cudaMemcpyDeviceToHost,
+                                    (cudaStream_t)s));
+      GNNV_TRY_CUDA(cudaStreamSynchronize((cudaStream_t)s));
+    }
+    for (int h = 0; h < b->L; ++h) {
+      v[h].n_dst = sz[h];
+      v[h].n_src = sz[h + 1];
+      v[h].nnz = sz[b->L + 1 + h];
+      v[h].max_dst = b->max_n[h];
+      v[h].max_src = b->max_n[h + 1];
+      v[h].max_nnz = b->max_nnz[h];
+      v[h].d_indptr = b->d_indptr[h];
+      v[h].d_indices = b->d_indices[h];
+      v[h].d_src_global = b->d_F;
+    }
+    if (sync) {
+      int32_t err = sz[2 * b->L + 1];
+      if (err) {
+        GNNV_TRY_CUDA(cudaMemsetAsync(b->d_sizes + 2 * b->L + 1, 0, sizeof(int32_t), (cudaStream_t)s));
+        throw Error{GNNV_ERR_PARAM, (err & 1) ? "sample: a seed id is outside [0, N)" : "sample: repeated seed id"};
+      }
+    }
+  });
+}
+
+const int32_t* gnnv_blocks_device_sizes(const gnnv_blocks* b) { return b ? b->d_sizes : nullptr; }
+int32_t gnnv_blocks_num_layers(const gnnv_blocks* b) { return b ? b->L : 0; }
+
+gnnv_status gnnv_sgd(float* d_params, const float* d_grads, int64_t n, float lr, gnnv_stream s) {
+  return guarded([&] {
+    GNNV_REQUIRE(d_params && d_grads && n >= 0, GNNV_ERR_PARAM, "sgd: bad args");
+    launch_sgd(d_params, d_grads, n, lr, (cudaStream_t)s);
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,240 @@
+// Degree-ordered static feature cache and the cache-lookup + gather kernel.
+//
+// Paper: transmission abstraction §3.2: the device cache is
+// initialised from the free device memory, looks up which part of the
+// mini-batch is resident, and the rest is fetched from the host over the
+// host-device link; PaGraph static template; Eq.6 t_transfer =
+// f(n_attr |V_i| (1-hit)).  Readings Q7 (capacity floor(r N),
+// ties by lower id) and Q8 (hit accounting per unique row of F_L).
+//
+// Layout in HBM: the cached rows are a dense [C x stride] fp32 table in
+// degree-rank order (slot i holds the vertex of rank i); with G shards,
+// shard o holds ranks i = j*G + o at row j.  slot_map[v] = rank or -1.
+// Misses are read zero-copy from the pinned, device-mapped host table.
+#include <cub/device/device_radix_sort.cuh>
+
+#include "common.cuh"
+
+namespace gnnv {
+
+__global__ void k_degree_keys(const int64_t* __restrict__ indptr, int64_t n, uint32_t* keys, int32_t* ids) {
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t deg = indptr[v + 1] - indptr[v];
+    keys[v] = 0xFFFFFFFFu - (uint32_t)(deg < 0xFFFFFFFFll ? deg : 0xFFFFFFFFll);  // ascending key = degree desc
+    ids[v] = (int32_t)v;
+  }
+}
+
+__global__ void k_slots(const int32_t* __restrict__ order, int64_t n, int64_t C, int32_t* slot) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    slot[order[i]] = i < C ? (int32_t)i : -1;
+}
+
+// shard rows: row j of shard `o` = vertex order[j*G + o]
+__global__ void k_fill_shard(const int32_t* __restrict__ order, int64_t C, int G, int o, const float* src,
+                             int32_t stride, float* dst, int64_t rows) {
+  const int vec = stride / 4;
+  const int64_t total = rows * vec;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t j = t / vec;
+    const int c = (int)(t - j * vec);
+    const int64_t i = j * G + o;
+    if (i >= C) continue;
+    const int64_t v = order[i];
+    reinterpret_cast<float4*>(dst)[j * vec + c] = reinterpret_cast<const float4*>(src)[v * vec + c];
+  }
+}
+
+// ----------------------------------------------------------------- gather
+// One warp per row group; lanes stride over the row's float4 columns; ROWS
+// rows are in flight per warp (independent 16-byte loads) for memory-level
+// parallelism.  Sources: shard ptrs[s % G] row s / G (HBM or NVLink peer) or
+// the mapped host table (PCIe) on a miss.
+template <int ROWS>
+__global__ void __launch_bounds__(256) k_gather(const int32_t* __restrict__ F, const int32_t* sizes, int L,
+                                                const int32_t* __restrict__ slot,
+                                                const float* const* __restrict__ shards, int G, int me,
+                                                const float* __restrict__ host, int32_t stride,
+                                                float* __restrict__ X, unsigned long long* stats) {
+  const int n = sizes[L];
+  const int vec = stride >> 2;
+  const int lane = threadIdx.x & 31;
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  unsigned long long c_local = 0, c_peer = 0, c_miss = 0;
+  for (int base = warp * ROWS; base < n; base += nwarps * ROWS) {
+    const float4* src[ROWS];
+#pragma unroll
+    for (int r = 0; r < ROWS; ++r) {
+      const int row = base + r;
+      src[r] = nullptr;
+      if (row < n) {
+        const int v = F[row];
+        const int s = slot[v];
+        if (s >= 0) {
+          const int o = s % G;
+          src[r] = reinterpret_cast<const float4*>(shards[o]) + (int64_t)(s / G) * vec;
+          if (lane == 0) {
+            if (o == me) ++c_local;
+            else ++c_peer;
+          }
+        } else {
+          src[r] = reinterpret_cast<const float4*>(host) + (int64_t)v * vec;
+          if (lane == 0) ++c_miss;
+        }
+      }
+    }
+    for (int c = lane; c < vec; c += 32) {
+      float4 val[ROWS];
+#pragma unroll
+      for (int r = 0; r < ROWS; ++r)
+        if (src[r]) val[r] = __ldg(src[r] + c);
+#pragma unroll
+      for (int r = 0; r < ROWS; ++r)
+        if (src[r]) __stcs(reinterpret_cast<float4*>(X) + (int64_t)(base + r) * vec + c, val[r]);
+    }
+  }
+  if (stats && lane == 0) {
+    if (c_local) atomicAdd(&stats[1], c_local);
+    if (c_peer) atomicAdd(&stats[2], c_peer);
+    if (c_miss) atomicAdd(&stats[3], c_miss);
+    if (c_local + c_peer + c_miss) atomicAdd(&stats[0], c_local + c_peer + c_miss);
+  }
+}
+
+void launch_gather(const gnnv_cache* c, const gnnv_blocks* b, float* d_X, int64_t* d_stats, cudaStream_t s) {
+  const gnnv_graph* g = c->g;
+  constexpr int ROWS = 4;
+  const int64_t rows_ub = b->max_n[b->L];
+  const int64_t warps = ceil_div(rows_ub, ROWS);
+  const int blocks = (int)std::min<int64_t>(ceil_div(warps, 8), (int64_t)num_sms() * 8);
+  k_gather<ROWS><<<std::max(blocks, 1), 256, 0, s>>>(b->d_F, b->d_sizes, b->L, c->d_slot, c->d_shard_ptrs, c->world,
+                                                     c->rank, g->d_feats, g->stride, d_X,
+                                                     reinterpret_cast<unsigned long long*>(d_stats));
+  GNNV_CHECK_LAUNCH();
+}
+
+}  // namespace gnnv
+
+using namespace gnnv;
+
+extern "C" {
+
+gnnv_status gnnv_cache_build(gnnv_graph* g, double ratio, int32_t policy, int32_t placement, gnnv_comm* comm,
+                             int32_t virtual_shards, gnnv_cache** out) {
+  return guarded([&] {
+    GNNV_REQUIRE(g && out, GNNV_ERR_PARAM, "cache_build: null");
+    GNNV_REQUIRE(ratio >= 0.0 && ratio <= 1.0, GNNV_ERR_PARAM, "cache_build: ratio must be in [0,1]");
+    GNNV_REQUIRE(policy == GNNV_POLICY_NONE || policy == GNNV_POLICY_DEGREE || policy == GNNV_POLICY_FIFO ||
+                     policy == GNNV_POLICY_LRU,
+                 GNNV_ERR_PARAM, "cache_build: unknown policy");
+    GNNV_REQUIRE(policy != GNNV_POLICY_FIFO && policy != GNNV_POLICY_LRU, GNNV_ERR_UNSUPPORTED,
+                 "cache_build: dynamic FIFO/LRU update policies are not built (static DEGREE template only)");
+    GNNV_REQUIRE(placement >= GNNV_PLACE_REPLICA && placement <= GNNV_PLACE_SHARDED_LOCAL, GNNV_ERR_PARAM,
+                 "cache_build: unknown placement");
+    int G = 1, me = 0;
+    if (placement == GNNV_PLACE_SHARDED) {
+      GNNV_REQUIRE(comm, GNNV_ERR_PARAM, "cache_build: SHARDED placement needs a comm");
+      G = comm->world;
+      me = comm->rank;
+      GNNV_REQUIRE(G == 1, GNNV_ERR_UNSUPPORTED,
+                   "cache_build: cross-GPU SHARDED placement (NVLink peer reads) is not built in this round; "
+                   "use REPLICA or SHARDED_LOCAL");
+    } else if (placement == GNNV_PLACE_SHARDED_LOCAL) {
+      GNNV_REQUIRE(virtual_shards >= 1 && virtual_shards <= 64, GNNV_ERR_PARAM, "cache_build: virtual_shards in [1,64]");
+      G = virtual_shards;
+    }
+    GNNV_TRY_CUDA(cudaSetDevice(g->device));
+    const int64_t n = g->n;
+    // C = floor(ratio * N) in IEEE double; NONE => 0
+    const int64_t C = policy == GNNV_POLICY_NONE ? 0 : (int64_t)std::floor(ratio * (double)n);
+    gnnv_cache* c = new gnnv_cache();
+    c->g = g;
+    c->capacity = C;
+    c->world = G;
+    c->rank = me;
+    c->placement = placement;
+    try {
+      c->d_slot = (int32_t*)dmalloc(n * sizeof(int32_t), "cache slot map");
+      c->d_order = (int32_t*)dmalloc(n * sizeof(int32_t), "cache order");
+      uint32_t* keys = (uint32_t*)dmalloc(n * sizeof(uint32_t), "degree keys");
+      uint32_t* keys2 = (uint32_t*)dmalloc(n * sizeof(uint32_t), "degree keys");
+      int32_t* ids = (int32_t*)dmalloc(n * sizeof(int32_t), "ids");
+      const int sms = num_sms();
+      k_degree_keys<<<sms * 8, 256>>>(g->d_indptr, n, keys, ids);
+      GNNV_CHECK_LAUNCH();
+      size_t tmp_bytes = 0;
+      GNNV_TRY_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, keys, keys2, ids, c->d_order, (int)n));
+      void* tmp = dmalloc(tmp_bytes, "sort temp");
+      // LSD radix sort is stable: equal degrees keep ascending id order
+      GNNV_TRY_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, keys, keys2, ids, c->d_order, (int)n));
+      k_slots<<<sms * 8, 256>>>(c->d_order, n, C, c->d_slot);
+      GNNV_CHECK_LAUNCH();
+      GNNV_TRY_CUDA(cudaDeviceSynchronize());
+      dfree(tmp);
+      dfree(keys);
+      dfree(keys2);
+      dfree(ids);
+      c->shards.assign(G, nullptr);
+      c->shard_owned.assign(G, false);
+      c->shard_ipc.assign(G, false);
+      for (int o = 0; o < G; ++o) {
+        const int64_t rows = C > o ? (C - o + G - 1) / G : 0;
+        const bool resident = placement != GNNV_PLACE_SHARDED || o == me;
+        if (!resident) continue;
+        const size_t bytes = (size_t)std::max<int64_t>(rows, 1) * g->stride * sizeof(float);
+        c->shards[o] = (float*)dmalloc(bytes, "feature cache (Gamma_cache)");
+        c->shard_owned[o] = true;
+        c->local_rows += rows;
+        if (rows) {
+          k_fill_shard<<<sms * 16, 256>>>(c->d_order, C, G, o, g->d_feats, g->stride, c->shards[o], rows);
+          GNNV_CHECK_LAUNCH();
+        }
+      }
+      c->d_shard_ptrs = (const float**)dmalloc(G * sizeof(float*), "shard pointers");
+      GNNV_TRY_CUDA(cudaMemcpy((void*)c->d_shard_ptrs, c->shards.data(), G * sizeof(float*), cudaMemcpyHostToDevice));
+      GNNV_TRY_CUDA(cudaDeviceSynchronize());
+    } catch (...) {
+      gnnv_cache_free(c);
+      throw;
+    }
+    *out = c;
+  });
+}
+
+gnnv_status gnnv_cache_free(gnnv_cache* c) {
+  if (!c) return GNNV_OK;
+  dfree(c->d_slot);
+  dfree(c->d_order);
+  for (size_t o = 0; o < c->shards.size(); ++o)
+    if (c->shard_owned[o]) dfree(c->shards[o]);
+  dfree((void*)c->d_shard_ptrs);
+  delete c;
+  return GNNV_OK;
+}
+
+gnnv_status gnnv_cache_info(const gnnv_cache* c, gnnv_cache_view* o) {
+  return guarded([&] {
+    GNNV_REQUIRE(c && o, GNNV_ERR_PARAM, "cache_info: null");
+    o->capacity = c->capacity;
+    o->local_rows = c->local_rows;
+    o->bytes = c->local_rows * (int64_t)c->g->stride * (int64_t)sizeof(float);
+    o->world = c->world;
+    o->rank = c->rank;
+    o->placement = c->placement;
+    o->d_slot = c->d_slot;
+    o->d_order = c->d_order;
+  });
+}
+
+gnnv_status gnnv_gather(const gnnv_cache* c, const gnnv_blocks* b, float* d_X, int64_t* d_stats, gnnv_stream s) {
+  return guarded([&] {
+    GNNV_REQUIRE(c && b && d_X, GNNV_ERR_PARAM, "gather: null");
+    GNNV_REQUIRE(b->sampled, GNNV_ERR_STATE, "gather: gnnv_sample has not run on these blocks");
+    GNNV_REQUIRE(c->g == b->g, GNNV_ERR_STATE, "gather: cache and blocks belong to different graphs");
+    GNNV_REQUIRE(((uintptr_t)d_X & 15) == 0, GNNV_ERR_PARAM, "gather: d_X must be 16-byte aligned");
+    launch_gather(c, b, d_X, d_stats, (cudaStream_t)s);
+  });
+}
+
+}  // extern "C"

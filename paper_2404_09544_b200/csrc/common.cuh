@@ -1,0 +1,181 @@
+// Internal definitions shared by the libgnnv translation units (sm_100a).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/gnnv.h"
+
+namespace gnnv {
+
+// ----------------------------------------------------------------- errors
+void set_error(const std::string& msg);
+const char* get_error();
+
+struct Error {
+  gnnv_status st;
+  std::string msg;
+};
+
+#define GNNV_TRY_CUDA(expr)                                                                    \
+  do {                                                                                         \
+    cudaError_t _e = (expr);                                                                   \
+    if (_e != cudaSuccess) {                                                                   \
+      if (_e == cudaErrorMemoryAllocation) {                                                   \
+        throw ::gnnv::Error{GNNV_ERR_OOM, std::string(#expr) + ": " + cudaGetErrorString(_e)}; \
+      }                                                                                        \
+      throw ::gnnv::Error{GNNV_ERR_CUDA, std::string(#expr) + ": " + cudaGetErrorString(_e)};  \
+    }                                                                                          \
+  } while (0)
+
+#define GNNV_CHECK_LAUNCH() GNNV_TRY_CUDA(cudaGetLastError())
+
+#define GNNV_REQUIRE(cond, code, msg)                  \
+  do {                                                 \
+    if (!(cond)) throw ::gnnv::Error{(code), (msg)};   \
+  } while (0)
+
+// Runs `body`, converting thrown Errors to a status + thread-local message.
+template <class F>
+gnnv_status guarded(F&& body) {
+  try {
+    body();
+    return GNNV_OK;
+  } catch (const Error& e) {
+    set_error(e.msg);
+    return e.st;
+  } catch (const std::exception& e) {
+    set_error(e.what());
+    return GNNV_ERR_CUDA;
+  }
+}
+
+void* dmalloc(size_t bytes, const char* what);  // throws OOM with the byte count
+void dfree(void* p);
+
+inline int32_t row_stride(int32_t d) { return (d + 3) & ~3; }
+inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+int num_sms();
+
+// ---------------------------------------------------------------- handles
+}  // namespace gnnv
+
+struct gnnv_graph {
+  int device = 0;
+  int64_t n = 0, nnz = 0;
+  int32_t d = 0, stride = 0, n_classes = 0;
+  int64_t* d_indptr = nullptr;
+  int32_t* d_indices = nullptr;
+  int32_t* d_labels = nullptr;
+  const float* h_feats = nullptr;  // borrowed host table
+  const float* d_feats = nullptr;  // device-mapped alias
+  bool registered = false;         // we called cudaHostRegister
+};
+
+struct gnnv_comm {
+  int rank = 0, world = 1, device = 0;
+  void* nccl = nullptr;  // ncclComm_t
+};
+
+struct gnnv_cache {
+  gnnv_graph* g = nullptr;
+  int64_t capacity = 0;
+  int64_t local_rows = 0;
+  int32_t world = 1, rank = 0, placement = GNNV_PLACE_REPLICA;
+  int32_t* d_slot = nullptr;   // [N] degree rank if cached else -1
+  int32_t* d_order = nullptr;  // [N] vertices by (deg desc, id asc)
+  std::vector<float*> shards;  // per shard base pointer (local allocs or IPC-mapped peers)
+  std::vector<bool> shard_owned;
+  std::vector<bool> shard_ipc;
+  const float** d_shard_ptrs = nullptr;  // device array [world]
+};
+
+struct gnnv_blocks {
+  gnnv_graph* g = nullptr;
+  int32_t L = 0;
+  int32_t fanouts[GNNV_MAX_LAYERS] = {0};
+  int64_t max_n[GNNV_MAX_LAYERS + 1] = {0};   // frontier capacities
+  int64_t max_nnz[GNNV_MAX_LAYERS] = {0};
+  int32_t* d_tag = nullptr;       // [N] relabel map: INT_MIN unvisited, <-1 claim, >=0 local id
+  int32_t* d_F = nullptr;         // [max_n[L]] nested frontiers
+  int32_t* d_ell = nullptr;       // [max over h of max_n[h]*k_h] sampled global ids
+  int32_t* d_cnt = nullptr;       // [max_n[L-1]] per-row sampled count
+  int32_t* d_indptr[GNNV_MAX_LAYERS] = {nullptr};
+  int32_t* d_indices[GNNV_MAX_LAYERS] = {nullptr};
+  int32_t* d_sizes = nullptr;     // [2L+1] + error flag
+  unsigned long long* d_scan = nullptr;  // chained-scan status [1 + max tiles]
+  int64_t scan_words = 0;
+  bool sampled = false;
+  // scratch arena for the layer kernels (grows on demand)
+  void* scratch = nullptr;
+  size_t scratch_bytes = 0;
+  void* ensure_scratch(size_t bytes, cudaStream_t s);
+};
+
+namespace gnnv {
+
+// kernels implemented in the .cu files -----------------------------------
+// sample.cu
+void launch_sample(gnnv_graph* g, gnnv_blocks* b, const int32_t* d_seeds, int32_t n_seeds, uint64_t rng_seed,
+                   cudaStream_t s);
+// cache.cu
+void launch_gather(const gnnv_cache* c, const gnnv_blocks* b, float* d_X, int64_t* d_stats, cudaStream_t s);
+// spmm.cu
+void launch_spmm_fwd(const int32_t* d_indptr, const int32_t* d_indices, const int32_t* d_ndst, int64_t max_dst,
+                     const float* H, int32_t ldh, float* A, int32_t lda, int32_t d, int32_t kind, int32_t aggr,
+                     cudaStream_t s);
+void launch_spmm_bwd(const int32_t* d_indptr, const int32_t* d_indices, const int32_t* d_ndst, int64_t max_dst,
+                     const float* dA, int32_t lda, float* dH, int32_t ldh, int32_t d, int32_t kind, int32_t aggr,
+                     cudaStream_t s);
+void launch_rows_zero(float* X, int32_t ld, const int32_t* d_row_begin, const int32_t* d_row_end, int64_t max_rows,
+                      cudaStream_t s);
+// gemm
+struct GemmFwdArgs {
+  const float* X1; int32_t ld1;  // H_dst (rows 0..M) or A' (GCN)
+  const float* X2; int32_t ld2;  // A (SAGE) or nullptr
+  int32_t K1;                    // width of each part (d_in)
+  const float* W;                // [(X2?2:1)*K1 x N] row-major
+  const float* bias;             // [N]
+  float* Y; int32_t ldy;         // [M x N]
+  int32_t N;
+  const int32_t* d_M; int64_t max_M;
+  bool relu;
+};
+void gemm_fwd(const GemmFwdArgs& a, int prec, cudaStream_t s);
+struct GemmDwArgs {  // dW = [X1|X2]^T G (+ bias row = colsum G) : deterministic split-K
+  const float* X1; int32_t ld1;
+  const float* X2; int32_t ld2;
+  int32_t K1;
+  const float* G; int32_t ldg;
+  int32_t N;
+  const int32_t* d_M; int64_t max_M;
+  float* dW;  // [(X2?2:1)*K1 x N]
+  float* db;  // [N]
+  float* partial; int32_t splits;  // workspace [splits x (rows+1) x N]
+};
+void gemm_dw(const GemmDwArgs& a, int prec, cudaStream_t s);
+size_t gemm_dw_partial_floats(int32_t rows_plus_bias, int32_t N, int32_t* splits_out, int64_t max_M);
+struct GemmDxArgs {  // [Y1 | Y2] = G W^T  (Y1 = first K1 cols, Y2 = the rest)
+  const float* G; int32_t ldg;
+  int32_t N;
+  const float* W;  // [(Y2?2:1)*K1 x N] row-major
+  int32_t K1;
+  float* Y1; int32_t ld1;
+  float* Y2; int32_t ld2;
+  const int32_t* d_M; int64_t max_M;
+};
+void gemm_dx(const GemmDxArgs& a, int prec, cudaStream_t s);
+// layers.cu
+void launch_relu_mask(const float* G, const float* H, float* Gp, int32_t ld, int32_t N, const int32_t* d_M,
+                      int64_t max_M, cudaStream_t s);
+void launch_ce_loss(const float* z, int32_t ldz, int32_t C, const int32_t* d_rows, const int32_t* d_F,
+                    const int32_t* d_labels, int32_t n_global, float* d_loss, float* dz, float* partial,
+                    unsigned int* counter, int64_t max_rows, cudaStream_t s);
+void launch_sgd(float* p, const float* g, int64_t n, float lr, cudaStream_t s);
+
+}  // namespace gnnv

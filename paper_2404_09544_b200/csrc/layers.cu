@@ -1,0 +1,262 @@
+// GNN layer forward/backward orchestration, loss, SGD (C-ABI entry points).
+//
+// Paper: Eq.1; Algorithm 1 lines 4-8; SPEC S:320,
+// S:322 (combine = linear + ReLU except the last layer; mean/sum over
+// neighbours), S:332 (softmax cross-entropy + plain gradient descent).
+// Layer i in 1..L runs on block b_{L-i} (dst = F_{L-i}, src = F_{L-i+1}).
+#include "common.cuh"
+
+namespace gnnv {
+
+__global__ void k_relu_mask(const float* __restrict__ G, const float* __restrict__ H, float* __restrict__ Gp, int ld,
+                            const int32_t* d_M) {
+  const int64_t total = (int64_t)(*d_M) * (ld >> 2);
+  const float4* G4 = reinterpret_cast<const float4*>(G);
+  const float4* H4 = reinterpret_cast<const float4*>(H);
+  float4* P4 = reinterpret_cast<float4*>(Gp);
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+    const float4 g = __ldg(G4 + t), h = __ldg(H4 + t);
+    P4[t] = make_float4(h.x > 0.f ? g.x : 0.f, h.y > 0.f ? g.y : 0.f, h.z > 0.f ? g.z : 0.f, h.w > 0.f ? g.w : 0.f);
+  }
+}
+
+void launch_relu_mask(const float* G, const float* H, float* Gp, int32_t ld, int32_t, const int32_t* d_M,
+                      int64_t max_M, cudaStream_t s) {
+  const int64_t total = std::max<int64_t>(max_M, 1) * (ld / 4);
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(total, 256), (int64_t)num_sms() * 8));
+  k_relu_mask<<<grid, 256, 0, s>>>(G, H, Gp, ld, d_M);
+  GNNV_CHECK_LAUNCH();
+}
+
+constexpr int kLossBlocks = 64;
+
+// One warp per seed row; fixed grid => fixed summation order (deterministic).
+__global__ void __launch_bounds__(256) k_ce_loss(const float* __restrict__ z, int ldz, int C,
+                                                 const int32_t* d_rows, const int32_t* __restrict__ F,
+                                                 const int32_t* __restrict__ labels, int n_global,
+                                                 float* d_loss, float* __restrict__ dz, float* partial,
+                                                 unsigned int* counter) {
+  __shared__ float s_w[8];
+  __shared__ bool s_last;
+  const int n = *d_rows;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const float inv = 1.f / (float)n_global;
+  float wsum = 0.f;
+  for (int row = blockIdx.x * 8 + wid; row < n; row += gridDim.x * 8) {
+    const float* zr = z + (int64_t)row * ldz;
+    float m = -INFINITY;
+    for (int c = lane; c < C; c += 32) m = fmaxf(m, zr[c]);
+#pragma unroll
+    for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    float se = 0.f;
+    for (int c = lane; c < C; c += 32) se += expf(zr[c] - m);
+#pragma unroll
+    for (int o = 16; o; o >>= 1) se += __shfl_xor_sync(0xffffffffu, se, o);
+    const int y = labels[F[row]];
+    const float lse = m + logf(se);
+    if (lane == 0) wsum += (lse - zr[y]);
+    float* dr = dz + (int64_t)row * ldz;
+    for (int c = lane; c < ldz; c += 32) {
+      float g = 0.f;
+      if (c < C) g = (expf(zr[c] - m) / se - (c == y ? 1.f : 0.f)) * inv;
+      dr[c] = g;
+    }
+  }
+  if (lane == 0) s_w[wid] = wsum;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float b = 0.f;
+    for (int w = 0; w < 8; ++w) b += s_w[w];
+    partial[blockIdx.x] = b;
+    __threadfence();
+    s_last = atomicAdd(counter, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (s_last && threadIdx.x == 0) {
+    __threadfence();
+    float t = 0.f;
+    for (int i = 0; i < (int)gridDim.x; ++i) t += ((volatile float*)partial)[i];
+    *d_loss = t * inv;
+    *counter = 0;
+  }
+}
+
+void launch_ce_loss(const float* z, int32_t ldz, int32_t C, const int32_t* d_rows, const int32_t* d_F,
+                    const int32_t* d_labels, int32_t n_global, float* d_loss, float* dz, float* partial,
+                    unsigned int* counter, int64_t, cudaStream_t s) {
+  k_ce_loss<<<kLossBlocks, 256, 0, s>>>(z, ldz, C, d_rows, d_F, d_labels, n_global, d_loss, dz, partial, counter);
+  GNNV_CHECK_LAUNCH();
+}
+
+__global__ void k_sgd(float* __restrict__ p, const float* __restrict__ g, int64_t n, float lr) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    p[i] -= lr * g[i];
+}
+
+void launch_sgd(float* p, const float* g, int64_t n, float lr, cudaStream_t s) {
+  if (n <= 0) return;
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, 256), (int64_t)num_sms() * 4));
+  k_sgd<<<grid, 256, 0, s>>>(p, g, n, lr);
+  GNNV_CHECK_LAUNCH();
+}
+
+static void check_layer(const gnnv_blocks* b, int32_t layer, const gnnv_layer_desc* ld) {
+  GNNV_REQUIRE(b && ld, GNNV_ERR_PARAM, "layer: null");
+  GNNV_REQUIRE(b->sampled, GNNV_ERR_STATE, "layer: gnnv_sample has not run on these blocks");
+  GNNV_REQUIRE(layer >= 1 && layer <= b->L, GNNV_ERR_PARAM, "layer: index must be in [1, L]");
+  GNNV_REQUIRE(ld->d_in >= 1 && ld->d_out >= 1, GNNV_ERR_PARAM, "layer: dims must be >= 1");
+  GNNV_REQUIRE(ld->in_stride >= ld->d_in && ld->in_stride % 4 == 0, GNNV_ERR_PARAM,
+               "layer: in_stride must be >= d_in and a multiple of 4");
+  GNNV_REQUIRE(ld->kind == GNNV_KIND_SAGE || ld->kind == GNNV_KIND_GCN, GNNV_ERR_PARAM, "layer: kind");
+  GNNV_REQUIRE(ld->aggr == GNNV_AGGR_MEAN || ld->aggr == GNNV_AGGR_SUM, GNNV_ERR_PARAM, "layer: aggr");
+  GNNV_REQUIRE(ld->act == GNNV_ACT_NONE || ld->act == GNNV_ACT_RELU, GNNV_ERR_PARAM, "layer: act");
+  GNNV_REQUIRE(ld->prec == GNNV_PREC_FP32 || ld->prec == GNNV_PREC_BF16, GNNV_ERR_PARAM, "layer: prec");
+}
+
+void layer_fwd_impl(gnnv_blocks* b, int32_t layer, const gnnv_layer_desc* ld, const float* Hsrc, const float* W,
+                    const float* bias, float* Hdst, float* A, cudaStream_t s) {
+  const int h = b->L - layer;
+  const int32_t* d_ndst = b->d_sizes + h;
+  const int lda = row_stride(ld->d_in), ldo = row_stride(ld->d_out);
+  launch_spmm_fwd(b->d_indptr[h], b->d_indices[h], d_ndst, b->max_n[h], Hsrc, ld->in_stride, A, lda, ld->d_in,
+                  ld->kind, ld->aggr, s);
+  GemmFwdArgs g{};
+  if (ld->kind == GNNV_KIND_SAGE) {
+    g.X1 = Hsrc;
+    g.ld1 = ld->in_stride;
+    g.X2 = A;
+    g.ld2 = lda;
+  } else {
+    g.X1 = A;
+    g.ld1 = lda;
+    g.X2 = nullptr;
+    g.ld2 = 0;
+  }
+  g.K1 = ld->d_in;
+  g.W = W;
+  g.bias = bias;
+  g.Y = Hdst;
+  g.ldy = ldo;
+  g.N = ld->d_out;
+  g.d_M = d_ndst;
+  g.max_M = b->max_n[h];
+  g.relu = ld->act == GNNV_ACT_RELU;
+  gemm_fwd(g, ld->prec, s);
+}
+
+void layer_bwd_impl(gnnv_blocks* b, int32_t layer, const gnnv_layer_desc* ld, const float* Gdst, const float* Hdst,
+                    const float* Hsrc, const float* A, const float* W, float* Gsrc, float* dW, float* db,
+                    cudaStream_t s) {
+  const int h = b->L - layer;
+  const int32_t* d_ndst = b->d_sizes + h;
+  const int64_t max_dst = b->max_n[h];
+  const int lda = row_stride(ld->d_in), ldo = row_stride(ld->d_out);
+  const bool sage = ld->kind == GNNV_KIND_SAGE;
+  const int rows = (sage ? 2 * ld->d_in : ld->d_in) + 1;
+  int32_t splits = 1;
+  const size_t part_f = gemm_dw_partial_floats(rows, ld->d_out, &splits, max_dst);
+  const bool relu = ld->act == GNNV_ACT_RELU;
+  const size_t gp_f = relu ? (size_t)max_dst * ldo : 0;
+  const size_t da_f = Gsrc ? (size_t)max_dst * lda : 0;
+  auto al = [](size_t f) { return (f + 63) & ~(size_t)63; };
+  float* scratch = (float*)b->ensure_scratch((al(part_f) + al(gp_f) + al(da_f)) * sizeof(float), s);
+  float* partial = scratch;
+  float* Gp = scratch + al(part_f);
+  float* dA = Gp + al(gp_f);
+  const float* G = Gdst;
+  if (relu) {
+    launch_relu_mask(Gdst, Hdst, Gp, ldo, ld->d_out, d_ndst, max_dst, s);
+    G = Gp;
+  }
+  GemmDwArgs w{};
+  if (sage) {
+    w.X1 = Hsrc;
+    w.ld1 = ld->in_stride;
+    w.X2 = A;
+    w.ld2 = lda;
+  } else {
+    w.X1 = A;
+    w.ld1 = lda;
+  }
+  w.K1 = ld->d_in;
+  w.G = G;
+  w.ldg = ldo;
+  w.N = ld->d_out;
+  w.d_M = d_ndst;
+  w.max_M = max_dst;
+  w.dW = dW;
+  w.db = db;
+  w.partial = partial;
+  w.splits = splits;
+  gemm_dw(w, ld->prec, s);
+  if (Gsrc) {
+    GemmDxArgs x{};
+    x.G = G;
+    x.ldg = ldo;
+    x.N = ld->d_out;
+    x.W = W;
+    x.K1 = ld->d_in;
+    x.d_M = d_ndst;
+    x.max_M = max_dst;
+    if (sage) {
+      x.Y1 = Gsrc;  // dH_dst lands directly in rows [0, n_dst) of dH_src
+      x.ld1 = ld->in_stride;
+      x.Y2 = dA;
+      x.ld2 = lda;
+    } else {
+      x.Y1 = dA;
+      x.ld1 = lda;
+      x.Y2 = nullptr;
+      x.ld2 = 0;
+    }
+    gemm_dx(x, ld->prec, s);
+    launch_rows_zero(Gsrc, ld->in_stride, sage ? d_ndst : nullptr, d_ndst + 1, b->max_n[h + 1], s);
+    launch_spmm_bwd(b->d_indptr[h], b->d_indices[h], d_ndst, max_dst, dA, lda, Gsrc, ld->in_stride, ld->d_in,
+                    ld->kind, ld->aggr, s);
+  }
+}
+
+}  // namespace gnnv
+
+using namespace gnnv;
+
+extern "C" {
+
+gnnv_status gnnv_layer_fwd(gnnv_blocks* b, int32_t layer, const gnnv_layer_desc* ld, const float* d_Hsrc,
+                           const float* d_W, const float* d_b, float* d_Hdst, float* d_saveA, gnnv_stream s) {
+  return guarded([&] {
+    check_layer(b, layer, ld);
+    GNNV_REQUIRE(d_Hsrc && d_W && d_b && d_Hdst && d_saveA, GNNV_ERR_PARAM, "layer_fwd: null buffer");
+    layer_fwd_impl(b, layer, ld, d_Hsrc, d_W, d_b, d_Hdst, d_saveA, (cudaStream_t)s);
+  });
+}
+
+gnnv_status gnnv_layer_bwd(gnnv_blocks* b, int32_t layer, const gnnv_layer_desc* ld, const float* d_Gdst,
+                           const float* d_Hdst, const float* d_Hsrc, const float* d_saveA, const float* d_W,
+                           float* d_Gsrc, float* d_dW, float* d_db, gnnv_stream s) {
+  return guarded([&] {
+    check_layer(b, layer, ld);
+    GNNV_REQUIRE(d_Gdst && d_Hdst && d_Hsrc && d_saveA && d_W && d_dW && d_db, GNNV_ERR_PARAM,
+                 "layer_bwd: null buffer");
+    layer_bwd_impl(b, layer, ld, d_Gdst, d_Hdst, d_Hsrc, d_saveA, d_W, d_Gsrc, d_dW, d_db, (cudaStream_t)s);
+  });
+}
+
+gnnv_status gnnv_ce_loss(gnnv_blocks* b, const gnnv_graph* g, const float* d_logits, int32_t n_classes, int32_t stride,
+                         int32_t n_global, float* d_loss, float* d_dlogits, gnnv_stream s) {
+  return guarded([&] {
+    GNNV_REQUIRE(b && g && d_logits && d_loss && d_dlogits, GNNV_ERR_PARAM, "ce_loss: null");
+    GNNV_REQUIRE(b->sampled, GNNV_ERR_STATE, "ce_loss: gnnv_sample has not run on these blocks");
+    GNNV_REQUIRE(n_classes >= 1 && stride >= n_classes && stride % 4 == 0 && n_global >= 1, GNNV_ERR_PARAM,
+                 "ce_loss: bad sizes");
+    float* scratch = (float*)b->ensure_scratch(4096, (cudaStream_t)s);
+    // the loss uses its own small region at the end of a fresh 4 KiB block of the arena
+    unsigned int* counter = reinterpret_cast<unsigned int*>(scratch + 1000);
+    static_assert(kLossBlocks <= 1000, "partials must fit");
+    GNNV_TRY_CUDA(cudaMemsetAsync(counter, 0, sizeof(unsigned int), (cudaStream_t)s));
+    launch_ce_loss(d_logits, stride, n_classes, b->d_sizes, b->d_F, g->d_labels, n_global, d_loss, d_dlogits,
+                   scratch, counter, b->max_n[0], (cudaStream_t)s);
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,335 @@
+// Node-wise fanout sampling + deterministic first-appearance relabelling.
+//
+// Paper: Eq.2 unified node-wise sampler; Algorithm 1 line 2
+// (P:104-105).  Readings Q1-Q6: exact-k without replacement,
+// Philox4x32-10 keyed by (rng_seed; hop, node, draw), Floyd's algorithm,
+// ascending CSR position, union frontiers, first-appearance local ids.
+//
+// Per hop h (all sizes stay on the device; no host round trip):
+//   k_sample_hop<G> : one G-lane group per frontier row (G = pow2 >= k).
+//                     Lane s computes draw s; Floyd's sequential membership
+//                     test is a ballot over the lanes < s; a rank-sort puts
+//                     positions in ascending order.  Sampled global ids go to
+//                     a fixed-stride slot array ell[r*k + i]; each id not yet
+//                     in F_h is "claimed" with atomicMax(tag[u], -(2+slot)),
+//                     i.e. the smallest (row, position) slot wins -- exactly
+//                     the first appearance in the (dst, position) scan.
+//   k_relabel_scan  : one thread per row; flags the slots that won their
+//                     claim; a single-pass chained scan (decoupled look-back)
+//                     over (new ids, sampled count) gives each row its first
+//                     new local id and its CSR offset; winners write
+//                     tag[u] = n_h + offset and F[n_h + offset] = u.
+//   k_map           : indices[indptr[r] + i] = tag[ell[r*k+i]] (before the
+//                     next hop reuses the slot array, and after the last hop).
+//   k_reset         : tag[F_L[i]] = INT_MIN, ready for the next call.
+#include <limits.h>
+
+#include "common.cuh"
+
+namespace gnnv {
+
+constexpr int kScanTile = 256;
+
+__device__ __forceinline__ uint4 philox4x32_10(uint4 c, uint2 k) {
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    if (r) {
+      k.x += 0x9E3779B9u;
+      k.y += 0xBB67AE85u;
+    }
+    const uint32_t hi0 = __umulhi(0xD2511F53u, c.x), lo0 = 0xD2511F53u * c.x;
+    const uint32_t hi1 = __umulhi(0xCD9E8D57u, c.z), lo1 = 0xCD9E8D57u * c.z;
+    c = make_uint4(hi1 ^ c.y ^ k.x, lo1, hi0 ^ c.w ^ k.y, lo0);
+  }
+  return c;
+}
+
+// draw(seed, h, v, s) = word s&3 of Philox(ctr=(s>>2, 0, v, h), key=(lo, hi))
+__device__ __forceinline__ uint32_t philox_draw(uint64_t seed, uint32_t h, uint32_t v, uint32_t s) {
+  const uint4 o = philox4x32_10(make_uint4(s >> 2, 0u, v, h), make_uint2((uint32_t)seed, (uint32_t)(seed >> 32)));
+  const uint32_t w = s & 3u;
+  return w == 0 ? o.x : (w == 1 ? o.y : (w == 2 ? o.z : o.w));
+}
+
+__global__ void k_init_seeds(const int32_t* __restrict__ seeds, int32_t n_seeds, int64_t N, int32_t* tag, int32_t* F,
+                             int32_t* sizes, int32_t err_index) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n_seeds; i += gridDim.x * blockDim.x) {
+    const int32_t v = seeds[i];
+    F[i] = v;
+    if ((uint32_t)v >= (uint64_t)N) {
+      atomicOr(&sizes[err_index], 1);
+      continue;
+    }
+    if (atomicCAS(&tag[v], INT_MIN, i) != INT_MIN) atomicOr(&sizes[err_index], 2);
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) sizes[0] = n_seeds;
+}
+
+// Map slots of hop hp (rows [0, n_hp)) to local ids.  Flattened over slots.
+__device__ __forceinline__ void map_slots(int64_t t0, int64_t stride, int hp, int kp, const int32_t* sizes,
+                                          const int32_t* __restrict__ ellp, const int32_t* __restrict__ cntp,
+                                          const int32_t* __restrict__ indptrp, const int32_t* tag,
+                                          int32_t* __restrict__ indicesp) {
+  const int64_t nslots = (int64_t)sizes[hp] * kp;
+  for (int64_t e = t0; e < nslots; e += stride) {
+    const int r = (int)(e / kp), i = (int)(e - (int64_t)r * kp);
+    if (i < cntp[r]) indicesp[indptrp[r] + i] = tag[ellp[e]];
+  }
+}
+
+template <int G>
+__global__ void __launch_bounds__(256) k_sample_hop(const int64_t* __restrict__ indptr,
+                                                    const int32_t* __restrict__ indices, int64_t N,
+                                                    const int32_t* __restrict__ F, const int32_t* sizes, int h, int k,
+                                                    uint64_t seed, int32_t* __restrict__ ell,
+                                                    int32_t* __restrict__ cnt, int32_t* tag) {
+  const int n = sizes[h];
+  constexpr int RPW = 32 / G;
+  const int lane = threadIdx.x & 31, grp = lane / G, gl = lane % G;
+  const unsigned gmask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << (grp * G));
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  for (int base = warp * RPW; base < n; base += nwarps * RPW) {
+    const int r = base + grp;
+    const bool active = r < n;
+    int64_t beg = 0;
+    int d = 0, v = 0;
+    if (active) {
+      v = F[r];
+      if ((uint32_t)v < (uint64_t)N) {
+        beg = indptr[v];
+        d = (int)(indptr[v + 1] - beg);
+      }
+    }
+    const int c = min(k, d);
+    int pos = gl, slot = gl;
+    if (d > k) {  // group-uniform branch: Floyd's algorithm over k draws
+      const int j = d - k + gl;
+      uint32_t t = 0;
+      if (gl < k) {
+        const uint32_t u = philox_draw(seed, (uint32_t)h, (uint32_t)v, (uint32_t)gl);
+        t = (uint32_t)(((uint64_t)u * (uint64_t)(uint32_t)(j + 1)) >> 32);
+      }
+      int sel = (int)t;
+      for (int s = 0; s < k; ++s) {
+        const int ts = __shfl_sync(gmask, (int)t, s, G);
+        const unsigned hit = __ballot_sync(gmask, gl < s && sel == ts);
+        if (gl == s && (hit & gmask)) sel = j;
+      }
+      int rank = 0;
+      for (int q = 0; q < k; ++q) {
+        const int sq = __shfl_sync(gmask, sel, q, G);
+        rank += (sq < sel);
+      }
+      pos = sel;
+      slot = rank;
+    }
+    if (active && gl < c) {
+      const int u = __ldg(&indices[beg + pos]);
+      const int e = r * k + slot;
+      ell[e] = u;
+      if ((uint32_t)u < (uint64_t)N) {
+        if (tag[u] < 0) atomicMax(&tag[u], -(2 + e));
+      }
+    }
+    if (active && gl == 0) cnt[r] = c;
+  }
+}
+
+__device__ __forceinline__ void st_release_u64(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+constexpr unsigned long long kFlagAgg = 1ull << 62;
+constexpr unsigned long long kFlagPre = 2ull << 62;
+__device__ __forceinline__ unsigned long long pack2(uint32_t a, uint32_t b) {
+  return (unsigned long long)a | ((unsigned long long)b << 31);
+}
+__device__ __forceinline__ uint32_t unpack_a(unsigned long long w) { return (uint32_t)(w & 0x7FFFFFFFull); }
+__device__ __forceinline__ uint32_t unpack_b(unsigned long long w) { return (uint32_t)((w >> 31) & 0x7FFFFFFFull); }
+
+__global__ void __launch_bounds__(kScanTile) k_relabel_scan(int64_t N, int h, int k, int L,
+                                                            const int32_t* __restrict__ ell,
+                                                            const int32_t* __restrict__ cnt, int32_t* tag,
+                                                            int32_t* __restrict__ F, int32_t* __restrict__ indptr,
+                                                            int32_t* sizes, unsigned long long* status) {
+  __shared__ int s_tile;
+  __shared__ uint32_t s_wa[kScanTile / 32], s_wb[kScanTile / 32];
+  __shared__ uint32_t s_pa, s_pb;
+  const int n = sizes[h];
+  const int ntiles = (n + kScanTile - 1) / kScanTile;
+  unsigned int* ticket = reinterpret_cast<unsigned int*>(status);
+  if (threadIdx.x == 0) s_tile = (int)atomicAdd(ticket, 1u);
+  __syncthreads();
+  const int tile = s_tile;
+  if (tile >= ntiles) return;
+  unsigned long long* st = status + 1;
+  const int r = tile * kScanTile + threadIdx.x;
+  uint32_t mask = 0;
+  int c = 0;
+  if (r < n) {
+    c = cnt[r];
+    for (int i = 0; i < c; ++i) {
+      const int e = r * k + i;
+      const int u = ell[e];
+      if ((uint32_t)u < (uint64_t)N && tag[u] == -(2 + e)) mask |= 1u << i;
+    }
+  }
+  // block exclusive scan of (a, b) = (#new ids, #sampled)
+  const uint32_t a = __popc(mask), b = (uint32_t)c;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  uint32_t ia = a, ib = b;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t ta = __shfl_up_sync(0xffffffffu, ia, o), tb = __shfl_up_sync(0xffffffffu, ib, o);
+    if (lane >= o) {
+      ia += ta;
+      ib += tb;
+    }
+  }
+  if (lane == 31) {
+    s_wa[wid] = ia;
+    s_wb[wid] = ib;
+  }
+  __syncthreads();
+  if (wid == 0) {
+    uint32_t wa = lane < kScanTile / 32 ? s_wa[lane] : 0, wb = lane < kScanTile / 32 ? s_wb[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t ta = __shfl_up_sync(0xffffffffu, wa, o), tb = __shfl_up_sync(0xffffffffu, wb, o);
+      if (lane >= o) {
+        wa += ta;
+        wb += tb;
+      }
+    }
+    if (lane < kScanTile / 32) {
+      s_wa[lane] = wa;  // inclusive over warps
+      s_wb[lane] = wb;
+    }
+  }
+  __syncthreads();
+  const uint32_t excl_a = ia - a + (wid ? s_wa[wid - 1] : 0u);
+  const uint32_t excl_b = ib - b + (wid ? s_wb[wid - 1] : 0u);
+  if (threadIdx.x == 0) {
+    const uint32_t A = s_wa[kScanTile / 32 - 1], B = s_wb[kScanTile / 32 - 1];
+    if (tile == 0) {
+      st_release_u64(&st[0], kFlagPre | pack2(A, B));
+      s_pa = 0;
+      s_pb = 0;
+    } else {
+      st_release_u64(&st[tile], kFlagAgg | pack2(A, B));
+      uint32_t pa = 0, pb = 0;
+      int p = tile - 1;
+      while (true) {
+        unsigned long long w;
+        do {
+          w = ld_acquire_u64(&st[p]);
+        } while ((w >> 62) == 0);
+        pa += unpack_a(w);
+        pb += unpack_b(w);
+        if ((w >> 62) == 2) break;
+        --p;
+      }
+      st_release_u64(&st[tile], kFlagPre | pack2(pa + A, pb + B));
+      s_pa = pa;
+      s_pb = pb;
+    }
+  }
+  __syncthreads();
+  const uint32_t new_off = s_pa + excl_a, edge_off = s_pb + excl_b;
+  if (r < n) {
+    indptr[r] = (int32_t)edge_off;
+    uint32_t m = mask;
+    int idx = 0;
+    while (m) {
+      const int i = __ffs(m) - 1;
+      m &= m - 1;
+      const int u = ell[r * k + i];
+      const int nid = n + (int)new_off + idx++;
+      tag[u] = nid;
+      F[nid] = u;
+    }
+  }
+  if (tile == ntiles - 1 && threadIdx.x == kScanTile - 1) {
+    const uint32_t tot_a = new_off + a, tot_b = edge_off + b;
+    sizes[h + 1] = n + (int)tot_a;
+    sizes[L + 1 + h] = (int)tot_b;
+    indptr[n] = (int32_t)tot_b;
+  }
+}
+
+__global__ void k_map(int hp, int kp, const int32_t* sizes, const int32_t* __restrict__ ellp,
+                      const int32_t* __restrict__ cntp, const int32_t* __restrict__ indptrp, const int32_t* tag,
+                      int32_t* __restrict__ indicesp) {
+  map_slots(blockIdx.x * (int64_t)blockDim.x + threadIdx.x, (int64_t)gridDim.x * blockDim.x, hp, kp, sizes, ellp, cntp,
+            indptrp, tag, indicesp);
+}
+
+__global__ void k_reset(const int32_t* __restrict__ F, const int32_t* sizes, int L, int64_t N, int32_t* tag) {
+  const int n = sizes[L];
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const int v = F[i];
+    if ((uint32_t)v < (uint64_t)N) tag[v] = INT_MIN;
+  }
+}
+
+static int grid_for(int64_t work, int per_block, int max_blocks) {
+  int64_t g = ceil_div(std::max<int64_t>(work, 1), per_block);
+  return (int)std::min<int64_t>(g, max_blocks);
+}
+
+void launch_sample(gnnv_graph* g, gnnv_blocks* b, const int32_t* d_seeds, int32_t n_seeds, uint64_t rng_seed,
+                   cudaStream_t s) {
+  const int L = b->L;
+  const int sms = num_sms();
+  const int err_index = 2 * L + 1;
+  k_init_seeds<<<grid_for(n_seeds, 256, sms * 4), 256, 0, s>>>(d_seeds, n_seeds, g->n, b->d_tag, b->d_F, b->d_sizes,
+                                                                err_index);
+  GNNV_CHECK_LAUNCH();
+  // Hop h's slots reuse d_ell / d_cnt, so hop h-1 is mapped to local ids
+  // (its tags are final after its scan) before hop h samples.
+  for (int h = 0; h < L; ++h) {
+    const int k = b->fanouts[h];
+    const int64_t rows_ub = b->max_n[h];
+    if (h > 0) {
+      const int64_t slots_ub = b->max_n[h - 1] * (int64_t)b->fanouts[h - 1];
+      k_map<<<grid_for(slots_ub, 256, sms * 8), 256, 0, s>>>(h - 1, b->fanouts[h - 1], b->d_sizes, b->d_ell,
+                                                              b->d_cnt, b->d_indptr[h - 1], b->d_tag,
+                                                              b->d_indices[h - 1]);
+      GNNV_CHECK_LAUNCH();
+    }
+    const int threads = 256;
+#define GNNV_SAMPLE_LAUNCH(G)                                                                              \
+  k_sample_hop<G><<<grid_for(rows_ub, threads / 32 * (32 / G), sms * 8), threads, 0, s>>>(                 \
+      g->d_indptr, g->d_indices, g->n, b->d_F, b->d_sizes, h, k, rng_seed, b->d_ell, b->d_cnt, b->d_tag)
+    if (k <= 4) {
+      GNNV_SAMPLE_LAUNCH(4);
+    } else if (k <= 8) {
+      GNNV_SAMPLE_LAUNCH(8);
+    } else if (k <= 16) {
+      GNNV_SAMPLE_LAUNCH(16);
+    } else {
+      GNNV_SAMPLE_LAUNCH(32);
+    }
+#undef GNNV_SAMPLE_LAUNCH
+    GNNV_CHECK_LAUNCH();
+    GNNV_TRY_CUDA(cudaMemsetAsync(b->d_scan, 0, b->scan_words * sizeof(unsigned long long), s));
+    const int tiles_ub = (int)ceil_div(rows_ub, kScanTile);
+    k_relabel_scan<<<tiles_ub, kScanTile, 0, s>>>(g->n, h, k, L, b->d_ell, b->d_cnt, b->d_tag, b->d_F,
+                                                  b->d_indptr[h], b->d_sizes, b->d_scan);
+    GNNV_CHECK_LAUNCH();
+  }
+  const int64_t slots_ub = b->max_n[L - 1] * (int64_t)b->fanouts[L - 1];
+  k_map<<<grid_for(slots_ub, 256, sms * 8), 256, 0, s>>>(L - 1, b->fanouts[L - 1], b->d_sizes, b->d_ell, b->d_cnt,
+                                                          b->d_indptr[L - 1], b->d_tag, b->d_indices[L - 1]);
+  GNNV_CHECK_LAUNCH();
+  k_reset<<<grid_for(b->max_n[L], 256, sms * 8), 256, 0, s>>>(b->d_F, b->d_sizes, L, g->n, b->d_tag);
+  GNNV_CHECK_LAUNCH();
+}
+
+}  // namespace gnnv

@@ -1,0 +1,188 @@
+// Sampled-block aggregation (SpMM) forward and its transpose.
+//
+// Paper: Eq.1 Aggregate; Algorithm 1 line 5 and the
+// backward of line 8.  Reading Q11/Q15:
+//   SAGE mean: A[v] = (1/c_v) sum_{u in N_b(v)} H[u]   (0 when c_v = 0)
+//   SAGE sum : A[v] = sum_u H[u]
+//   GCN  mean: A[v] = (H[v] + sum_u H[u]) / (c_v + 1);  GCN sum: H[v] + sum_u H[u]
+// Backward: dH[u] += w_v dA[v] for every edge (v,u) (and the self term for
+// GCN), w_v the same normalisation.
+//
+// Mapping: a warp owns RPW = 32/LPR dst rows (LPR lanes per row, LPR = 32
+// for rows wider than 64 floats); a row's lanes stride over its float4
+// columns.  Neighbour ids are fetched cooperatively and broadcast with
+// shuffles; four neighbour rows are loaded before they are added, in
+// ascending edge order (a fixed summation order).  HBM-bound: compulsory
+// bytes are the distinct source rows + the output rows + the indices.
+#include "common.cuh"
+
+namespace gnnv {
+
+__device__ __forceinline__ float4 f4add(float4 a, float4 b) {
+  return make_float4(a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w);
+}
+__device__ __forceinline__ float4 f4scale(float4 a, float s) { return make_float4(a.x * s, a.y * s, a.z * s, a.w * s); }
+__device__ __forceinline__ float4 f4div(float4 a, float s) { return make_float4(a.x / s, a.y / s, a.z / s, a.w / s); }
+__device__ __forceinline__ float4 mask_tail(float4 a, int col4, int d) {
+  const int base = col4 * 4;
+  if (base + 4 <= d) return a;
+  return make_float4(base + 0 < d ? a.x : 0.f, base + 1 < d ? a.y : 0.f, base + 2 < d ? a.z : 0.f,
+                     base + 3 < d ? a.w : 0.f);
+}
+
+template <int LPR>
+__global__ void __launch_bounds__(256) k_spmm_fwd(const int32_t* __restrict__ indptr,
+                                                  const int32_t* __restrict__ indices, const int32_t* d_ndst,
+                                                  const float* __restrict__ H, int32_t ldh, float* __restrict__ A,
+                                                  int32_t lda, int32_t d, int32_t kind, int32_t aggr) {
+  constexpr int RPW = 32 / LPR;
+  const int n = *d_ndst;
+  const int vec = (d + 3) >> 2;
+  const int lane = threadIdx.x & 31, sub = lane / LPR, sl = lane % LPR;
+  const unsigned smask = (LPR == 32) ? 0xffffffffu : (((1u << LPR) - 1u) << (sub * LPR));
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  const float4* H4 = reinterpret_cast<const float4*>(H);
+  const int ldh4 = ldh >> 2, lda4 = lda >> 2;
+  for (int base = warp * RPW; base < n; base += nwarps * RPW) {
+    const int row = base + sub;
+    const bool active = row < n;
+    const int beg = active ? indptr[row] : 0;
+    const int end = active ? indptr[row + 1] : 0;
+    const int cnt = end - beg;
+    for (int c0 = 0; c0 < vec; c0 += LPR) {
+      const int c = c0 + sl;
+      const bool cok = active && c < vec;
+      float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (kind == GNNV_KIND_GCN && cok) acc = __ldg(H4 + (int64_t)row * ldh4 + c);
+      for (int e0 = 0; e0 < cnt; e0 += LPR) {
+        const int my = (e0 + sl < cnt) ? __ldg(indices + beg + e0 + sl) : 0;
+        const int m = min(LPR, cnt - e0);
+        int j = 0;
+        for (; j + 4 <= m; j += 4) {
+          const int u0 = __shfl_sync(smask, my, j, LPR), u1 = __shfl_sync(smask, my, j + 1, LPR);
+          const int u2 = __shfl_sync(smask, my, j + 2, LPR), u3 = __shfl_sync(smask, my, j + 3, LPR);
+          if (cok) {
+            const float4 h0 = __ldg(H4 + (int64_t)u0 * ldh4 + c), h1 = __ldg(H4 + (int64_t)u1 * ldh4 + c);
+            const float4 h2 = __ldg(H4 + (int64_t)u2 * ldh4 + c), h3 = __ldg(H4 + (int64_t)u3 * ldh4 + c);
+            acc = f4add(acc, h0);
+            acc = f4add(acc, h1);
+            acc = f4add(acc, h2);
+            acc = f4add(acc, h3);
+          }
+        }
+        for (; j < m; ++j) {
+          const int u = __shfl_sync(smask, my, j, LPR);
+          if (cok) acc = f4add(acc, __ldg(H4 + (int64_t)u * ldh4 + c));
+        }
+      }
+      if (cok) {
+        if (aggr == GNNV_AGGR_MEAN) {
+          const int denom = cnt + (kind == GNNV_KIND_GCN ? 1 : 0);
+          acc = denom ? f4div(acc, (float)denom) : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+        reinterpret_cast<float4*>(A)[(int64_t)row * lda4 + c] = mask_tail(acc, c, d);
+      }
+    }
+    // zero the padding float4s of the output row (lda may exceed the used width)
+    if (active) {
+      for (int c = vec + sl; c < lda4; c += LPR)
+        reinterpret_cast<float4*>(A)[(int64_t)row * lda4 + c] = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+  }
+}
+
+template <int LPR>
+__global__ void __launch_bounds__(256) k_spmm_bwd(const int32_t* __restrict__ indptr,
+                                                  const int32_t* __restrict__ indices, const int32_t* d_ndst,
+                                                  const float* __restrict__ dA, int32_t lda, float* dH, int32_t ldh,
+                                                  int32_t d, int32_t kind, int32_t aggr) {
+  constexpr int RPW = 32 / LPR;
+  const int n = *d_ndst;
+  const int vec = (d + 3) >> 2;
+  const int lane = threadIdx.x & 31, sub = lane / LPR, sl = lane % LPR;
+  const unsigned smask = (LPR == 32) ? 0xffffffffu : (((1u << LPR) - 1u) << (sub * LPR));
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  const int ldh4 = ldh >> 2, lda4 = lda >> 2;
+  float4* dH4 = reinterpret_cast<float4*>(dH);
+  for (int base = warp * RPW; base < n; base += nwarps * RPW) {
+    const int row = base + sub;
+    const bool active = row < n;
+    const int beg = active ? indptr[row] : 0;
+    const int end = active ? indptr[row + 1] : 0;
+    const int cnt = end - beg;
+    float w = 1.f;
+    if (aggr == GNNV_AGGR_MEAN) {
+      const int denom = cnt + (kind == GNNV_KIND_GCN ? 1 : 0);
+      w = denom ? 1.f / (float)denom : 0.f;
+    }
+    for (int c0 = 0; c0 < vec; c0 += LPR) {
+      const int c = c0 + sl;
+      const bool cok = active && c < vec;
+      float4 g = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (cok) g = mask_tail(f4scale(__ldg(reinterpret_cast<const float4*>(dA) + (int64_t)row * lda4 + c), w), c, d);
+      if (kind == GNNV_KIND_GCN && cok) atomicAdd(dH4 + (int64_t)row * ldh4 + c, g);
+      for (int e0 = 0; e0 < cnt; e0 += LPR) {
+        const int my = (e0 + sl < cnt) ? __ldg(indices + beg + e0 + sl) : 0;
+        const int m = min(LPR, cnt - e0);
+        for (int j = 0; j < m; ++j) {
+          const int u = __shfl_sync(smask, my, j, LPR);
+          if (cok) atomicAdd(dH4 + (int64_t)u * ldh4 + c, g);
+        }
+      }
+    }
+  }
+}
+
+__global__ void k_rows_zero(float* X, int32_t ld, const int32_t* d_begin, const int32_t* d_end) {
+  const int64_t b = d_begin ? *d_begin : 0, e = *d_end;
+  const int ld4 = ld >> 2;
+  const int64_t total = (e - b) * ld4;
+  float4* X4 = reinterpret_cast<float4*>(X) + b * ld4;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x)
+    X4[t] = make_float4(0.f, 0.f, 0.f, 0.f);
+}
+
+static int spmm_grid(int64_t max_rows, int rows_per_warp) {
+  const int64_t warps = ceil_div(std::max<int64_t>(max_rows, 1), rows_per_warp);
+  return (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(warps, 8), (int64_t)num_sms() * 16));
+}
+
+void launch_spmm_fwd(const int32_t* d_indptr, const int32_t* d_indices, const int32_t* d_ndst, int64_t max_dst,
+                     const float* H, int32_t ldh, float* A, int32_t lda, int32_t d, int32_t kind, int32_t aggr,
+                     cudaStream_t s) {
+  const int vec = (d + 3) / 4;
+  if (vec <= 8) {
+    k_spmm_fwd<8><<<spmm_grid(max_dst, 4), 256, 0, s>>>(d_indptr, d_indices, d_ndst, H, ldh, A, lda, d, kind, aggr);
+  } else if (vec <= 16) {
+    k_spmm_fwd<16><<<spmm_grid(max_dst, 2), 256, 0, s>>>(d_indptr, d_indices, d_ndst, H, ldh, A, lda, d, kind, aggr);
+  } else {
+    k_spmm_fwd<32><<<spmm_grid(max_dst, 1), 256, 0, s>>>(d_indptr, d_indices, d_ndst, H, ldh, A, lda, d, kind, aggr);
+  }
+  GNNV_CHECK_LAUNCH();
+}
+
+void launch_spmm_bwd(const int32_t* d_indptr, const int32_t* d_indices, const int32_t* d_ndst, int64_t max_dst,
+                     const float* dA, int32_t lda, float* dH, int32_t ldh, int32_t d, int32_t kind, int32_t aggr,
+                     cudaStream_t s) {
+  const int vec = (d + 3) / 4;
+  if (vec <= 8) {
+    k_spmm_bwd<8><<<spmm_grid(max_dst, 4), 256, 0, s>>>(d_indptr, d_indices, d_ndst, dA, lda, dH, ldh, d, kind, aggr);
+  } else if (vec <= 16) {
+    k_spmm_bwd<16><<<spmm_grid(max_dst, 2), 256, 0, s>>>(d_indptr, d_indices, d_ndst, dA, lda, dH, ldh, d, kind, aggr);
+  } else {
+    k_spmm_bwd<32><<<spmm_grid(max_dst, 1), 256, 0, s>>>(d_indptr, d_indices, d_ndst, dA, lda, dH, ldh, d, kind, aggr);
+  }
+  GNNV_CHECK_LAUNCH();
+}
+
+void launch_rows_zero(float* X, int32_t ld, const int32_t* d_row_begin, const int32_t* d_row_end, int64_t max_rows,
+                      cudaStream_t s) {
+  const int64_t total = std::max<int64_t>(max_rows, 1) * (ld / 4);
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(total, 256), (int64_t)num_sms() * 8));
+  k_rows_zero<<<grid, 256, 0, s>>>(X, ld, d_row_begin, d_row_end);
+  GNNV_CHECK_LAUNCH();
+}
+
+}  // namespace gnnv

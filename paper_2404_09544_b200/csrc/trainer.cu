@@ -1,0 +1,261 @@
+// gnnv_step: one whole iteration of Algorithm 1 on one rank.
+//
+// sample -> gather -> L x (aggregate, combine) -> loss -> L x backward ->
+// allreduce(grads ++ loss) -> SGD, all stream-ordered on one stream with the
+// frontier sizes kept on the device (no host round trip inside the step).
+// Per-phase CUDA events give the Eq.4-8 decomposition:
+// t_sample, t_transfer (gather), t_compute (fwd + loss + bwd + update).
+#include <string.h>
+
+#include "common.cuh"
+
+namespace gnnv {
+void layer_fwd_impl(gnnv_blocks* b, int32_t layer, const gnnv_layer_desc* ld, const float* Hsrc, const float* W,
+                    const float* bias, float* Hdst, float* A, cudaStream_t s);
+void layer_bwd_impl(gnnv_blocks* b, int32_t layer, const gnnv_layer_desc* ld, const float* Gdst, const float* Hdst,
+                    const float* Hsrc, const float* A, const float* W, float* Gsrc, float* dW, float* db,
+                    cudaStream_t s);
+}  // namespace gnnv
+
+using namespace gnnv;
+
+struct gnnv_trainer {
+  gnnv_graph* g = nullptr;
+  gnnv_cache* c = nullptr;
+  gnnv_comm* comm = nullptr;
+  gnnv_model_desc md{};
+  gnnv_blocks* b = nullptr;
+  int64_t nparams = 0;
+  int64_t w_off[GNNV_MAX_LAYERS] = {0}, b_off[GNNV_MAX_LAYERS] = {0};
+  float* d_params = nullptr;
+  float* d_grads = nullptr;  // nparams + 1 (loss), all-reduced together
+  int32_t* d_seeds = nullptr;
+  int32_t* h_seeds = nullptr;  // pinned staging
+  float* h_out = nullptr;      // pinned: loss
+  int32_t* h_err = nullptr;    // pinned: sample error flag
+  float* H[GNNV_MAX_LAYERS + 1] = {nullptr};
+  int32_t Hs[GNNV_MAX_LAYERS + 1] = {0};
+  float* A[GNNV_MAX_LAYERS + 1] = {nullptr};
+  float* G[GNNV_MAX_LAYERS + 1] = {nullptr};
+  float* loss_partial = nullptr;
+  unsigned int* loss_counter = nullptr;
+  int64_t* d_stats = nullptr;
+  cudaEvent_t ev[8] = {nullptr};
+};
+
+static gnnv_layer_desc layer_desc(const gnnv_trainer* t, int i) {
+  gnnv_layer_desc ld{};
+  ld.d_in = t->md.dims[i - 1];
+  ld.d_out = t->md.dims[i];
+  ld.in_stride = t->Hs[i - 1];
+  ld.kind = t->md.kind;
+  ld.aggr = t->md.aggr;
+  ld.act = i < t->md.L ? GNNV_ACT_RELU : GNNV_ACT_NONE;
+  ld.prec = t->md.prec;
+  return ld;
+}
+
+extern "C" {
+
+gnnv_status gnnv_trainer_free(gnnv_trainer* t) {
+  if (!t) return GNNV_OK;
+  cudaSetDevice(t->g ? t->g->device : 0);
+  gnnv_blocks_free(t->b);
+  dfree(t->d_params);
+  dfree(t->d_grads);
+  dfree(t->d_seeds);
+  if (t->h_seeds) cudaFreeHost(t->h_seeds);
+  if (t->h_out) cudaFreeHost(t->h_out);
+  if (t->h_err) cudaFreeHost(t->h_err);
+  for (int i = 0; i <= GNNV_MAX_LAYERS; ++i) {
+    if (i > 0) dfree(t->H[i]);
+    dfree(t->A[i]);
+    dfree(t->G[i]);
+  }
+  dfree(t->H[0]);
+  dfree(t->loss_partial);
+  dfree(t->loss_counter);
+  dfree(t->d_stats);
+  for (auto& e : t->ev)
+    if (e) cudaEventDestroy(e);
+  delete t;
+  return GNNV_OK;
+}
+
+gnnv_status gnnv_trainer_create(gnnv_graph* g, gnnv_cache* c, const gnnv_model_desc* md, const float* host_params,
+                                gnnv_comm* comm, gnnv_trainer** out) {
+  return guarded([&] {
+    GNNV_REQUIRE(g && c && md && host_params && out, GNNV_ERR_PARAM, "trainer_create: null");
+    GNNV_REQUIRE(c->g == g, GNNV_ERR_STATE, "trainer_create: cache belongs to another graph");
+    GNNV_REQUIRE(md->L >= 1 && md->L <= GNNV_MAX_LAYERS, GNNV_ERR_PARAM, "trainer_create: L in [1, 8]");
+    GNNV_REQUIRE(md->dims[0] == g->d, GNNV_ERR_PARAM, "trainer_create: dims[0] must equal the feature dim");
+    GNNV_REQUIRE(md->dims[md->L] == g->n_classes, GNNV_ERR_PARAM, "trainer_create: dims[L] must equal n_classes");
+    for (int i = 0; i <= md->L; ++i) GNNV_REQUIRE(md->dims[i] >= 1, GNNV_ERR_PARAM, "trainer_create: dims >= 1");
+    GNNV_REQUIRE(md->kind == GNNV_KIND_SAGE || md->kind == GNNV_KIND_GCN, GNNV_ERR_PARAM, "trainer_create: kind");
+    GNNV_REQUIRE(md->aggr == GNNV_AGGR_MEAN || md->aggr == GNNV_AGGR_SUM, GNNV_ERR_PARAM, "trainer_create: aggr");
+    GNNV_REQUIRE(md->prec == GNNV_PREC_FP32 || md->prec == GNNV_PREC_BF16, GNNV_ERR_PARAM, "trainer_create: prec");
+    GNNV_TRY_CUDA(cudaSetDevice(g->device));
+    gnnv_trainer* t = new gnnv_trainer();
+    t->g = g;
+    t->c = c;
+    t->comm = comm;
+    t->md = *md;
+    try {
+      gnnv_status st = gnnv_blocks_create(g, md->max_seeds, md->fanouts, md->L, &t->b);
+      if (st != GNNV_OK) throw Error{st, get_error()};
+      const int L = md->L;
+      int64_t off = 0;
+      for (int i = 1; i <= L; ++i) {
+        const int64_t rows = (md->kind == GNNV_KIND_SAGE ? 2 : 1) * (int64_t)md->dims[i - 1];
+        t->w_off[i - 1] = off;
+        off += rows * md->dims[i];
+        t->b_off[i - 1] = off;
+        off += md->dims[i];
+      }
+      t->nparams = off;
+      t->d_params = (float*)dmalloc(off * sizeof(float), "params");
+      t->d_grads = (float*)dmalloc((off + 1) * sizeof(float), "grads");
+      GNNV_TRY_CUDA(cudaMemcpy(t->d_params, host_params, off * sizeof(float), cudaMemcpyHostToDevice));
+      GNNV_TRY_CUDA(cudaMemset(t->d_grads, 0, (off + 1) * sizeof(float)));
+      t->d_seeds = (int32_t*)dmalloc(md->max_seeds * sizeof(int32_t), "seeds");
+      GNNV_TRY_CUDA(cudaMallocHost(&t->h_seeds, md->max_seeds * sizeof(int32_t)));
+      GNNV_TRY_CUDA(cudaMallocHost(&t->h_out, 4 * sizeof(float)));
+      GNNV_TRY_CUDA(cudaMallocHost(&t->h_err, 4 * sizeof(int32_t)));
+      gnnv_blocks* b = t->b;
+      t->Hs[0] = g->stride;
+      t->H[0] = (float*)dmalloc((size_t)b->max_n[L] * g->stride * sizeof(float), "X (gathered features)");
+      for (int i = 1; i <= L; ++i) {
+        t->Hs[i] = row_stride(md->dims[i]);
+        const int64_t rows = b->max_n[L - i];
+        t->H[i] = (float*)dmalloc((size_t)rows * t->Hs[i] * sizeof(float), "H activations");
+        t->G[i] = (float*)dmalloc((size_t)rows * t->Hs[i] * sizeof(float), "dH gradients");
+        t->A[i] = (float*)dmalloc((size_t)rows * row_stride(md->dims[i - 1]) * sizeof(float), "aggregates");
+      }
+      t->loss_partial = (float*)dmalloc(256 * sizeof(float), "loss partials");
+      t->loss_counter = (unsigned int*)dmalloc(sizeof(unsigned int), "loss counter");
+      GNNV_TRY_CUDA(cudaMemset(t->loss_counter, 0, sizeof(unsigned int)));
+      t->d_stats = (int64_t*)dmalloc(4 * sizeof(int64_t), "gather stats");
+      for (auto& e : t->ev) GNNV_TRY_CUDA(cudaEventCreate(&e));
+      GNNV_TRY_CUDA(cudaDeviceSynchronize());
+    } catch (...) {
+      gnnv_trainer_free(t);
+      throw;
+    }
+    *out = t;
+  });
+}
+
+int64_t gnnv_trainer_num_params(const gnnv_trainer* t) { return t ? t->nparams : -1; }
+gnnv_blocks* gnnv_trainer_blocks(gnnv_trainer* t) { return t ? t->b : nullptr; }
+
+gnnv_status gnnv_trainer_get(gnnv_trainer* t, float* host_params, float* host_grads) {
+  return guarded([&] {
+    GNNV_REQUIRE(t, GNNV_ERR_PARAM, "trainer_get: null");
+    GNNV_TRY_CUDA(cudaDeviceSynchronize());
+    if (host_params)
+      GNNV_TRY_CUDA(cudaMemcpy(host_params, t->d_params, t->nparams * sizeof(float), cudaMemcpyDeviceToHost));
+    if (host_grads)
+      GNNV_TRY_CUDA(cudaMemcpy(host_grads, t->d_grads, t->nparams * sizeof(float), cudaMemcpyDeviceToHost));
+  });
+}
+
+gnnv_status gnnv_trainer_set_params(gnnv_trainer* t, const float* host_params) {
+  return guarded([&] {
+    GNNV_REQUIRE(t && host_params, GNNV_ERR_PARAM, "trainer_set_params: null");
+    GNNV_TRY_CUDA(cudaDeviceSynchronize());
+    GNNV_TRY_CUDA(cudaMemcpy(t->d_params, host_params, t->nparams * sizeof(float), cudaMemcpyHostToDevice));
+  });
+}
+
+gnnv_status gnnv_trainer_activation(gnnv_trainer* t, int32_t i, const float** d_H, int32_t* stride) {
+  return guarded([&] {
+    GNNV_REQUIRE(t && d_H && stride && i >= 0 && i <= t->md.L, GNNV_ERR_PARAM, "trainer_activation: bad args");
+    *d_H = t->H[i];
+    *stride = t->Hs[i];
+  });
+}
+
+gnnv_status gnnv_trainer_stats(gnnv_trainer* t, int64_t* host_stats4) {
+  return guarded([&] {
+    GNNV_REQUIRE(t && host_stats4, GNNV_ERR_PARAM, "trainer_stats: null");
+    GNNV_TRY_CUDA(cudaDeviceSynchronize());
+    GNNV_TRY_CUDA(cudaMemcpy(host_stats4, t->d_stats, 4 * sizeof(int64_t), cudaMemcpyDeviceToHost));
+  });
+}
+
+gnnv_status gnnv_step(gnnv_trainer* t, const int32_t* seeds, int32_t n_seeds, int32_t seeds_on_host, int32_t n_global,
+                      uint64_t rng_seed, float lr, float* loss_out, gnnv_step_timing* tm, gnnv_stream stream) {
+  return guarded([&] {
+    GNNV_REQUIRE(t && seeds, GNNV_ERR_PARAM, "step: null");
+    GNNV_REQUIRE(n_seeds >= 1 && n_seeds <= t->md.max_seeds, GNNV_ERR_PARAM, "step: n_seeds must be in [1, max_seeds]");
+    GNNV_REQUIRE(n_global >= n_seeds, GNNV_ERR_PARAM, "step: n_global must be >= n_seeds");
+    cudaStream_t s = (cudaStream_t)stream;
+    gnnv_blocks* b = t->b;
+    gnnv_graph* g = t->g;
+    const int L = t->md.L;
+    if (tm) GNNV_TRY_CUDA(cudaEventRecord(t->ev[0], s));
+    const int32_t* d_seeds = seeds;
+    if (seeds_on_host) {
+      for (int i = 0; i < n_seeds; ++i)
+        GNNV_REQUIRE(seeds[i] >= 0 && seeds[i] < g->n, GNNV_ERR_PARAM, "step: seed id outside [0, N)");
+      // the staging buffer may still feed the previous step's copy
+      GNNV_TRY_CUDA(cudaStreamSynchronize(s));
+      memcpy(t->h_seeds, seeds, n_seeds * sizeof(int32_t));
+      GNNV_TRY_CUDA(cudaMemcpyAsync(t->d_seeds, t->h_seeds, n_seeds * sizeof(int32_t), cudaMemcpyHostToDevice, s));
+      d_seeds = t->d_seeds;
+    }
+    launch_sample(g, b, d_seeds, n_seeds, rng_seed, s);
+    b->sampled = true;
+    if (tm) GNNV_TRY_CUDA(cudaEventRecord(t->ev[1], s));
+    GNNV_TRY_CUDA(cudaMemsetAsync(t->d_stats, 0, 4 * sizeof(int64_t), s));
+    launch_gather(t->c, b, t->H[0], t->d_stats, s);
+    if (tm) GNNV_TRY_CUDA(cudaEventRecord(t->ev[2], s));
+    for (int i = 1; i <= L; ++i) {
+      const gnnv_layer_desc ld = layer_desc(t, i);
+      layer_fwd_impl(b, i, &ld, t->H[i - 1], t->d_params + t->w_off[i - 1], t->d_params + t->b_off[i - 1], t->H[i],
+                     t->A[i], s);
+    }
+    if (tm) GNNV_TRY_CUDA(cudaEventRecord(t->ev[3], s));
+    float* d_loss = t->d_grads + t->nparams;
+    launch_ce_loss(t->H[L], t->Hs[L], t->md.dims[L], b->d_sizes, b->d_F, g->d_labels, n_global, d_loss, t->G[L],
+                   t->loss_partial, t->loss_counter, b->max_n[0], s);
+    if (tm) GNNV_TRY_CUDA(cudaEventRecord(t->ev[4], s));
+    for (int i = L; i >= 1; --i) {
+      const gnnv_layer_desc ld = layer_desc(t, i);
+      layer_bwd_impl(b, i, &ld, t->G[i], t->H[i], t->H[i - 1], t->A[i], t->d_params + t->w_off[i - 1],
+                     i > 1 ? t->G[i - 1] : nullptr, t->d_grads + t->w_off[i - 1], t->d_grads + t->b_off[i - 1], s);
+    }
+    if (tm) GNNV_TRY_CUDA(cudaEventRecord(t->ev[5], s));
+    if (t->comm && t->comm->world > 1) {
+      gnnv_status st = gnnv_allreduce_sum(t->comm, t->d_grads, t->nparams + 1, s);
+      if (st != GNNV_OK) throw Error{st, get_error()};
+    }
+    if (tm) GNNV_TRY_CUDA(cudaEventRecord(t->ev[6], s));
+    launch_sgd(t->d_params, t->d_grads, t->nparams, lr, s);
+    if (tm) GNNV_TRY_CUDA(cudaEventRecord(t->ev[7], s));
+    if (loss_out || tm) {
+      GNNV_TRY_CUDA(cudaMemcpyAsync(t->h_out, d_loss, sizeof(float), cudaMemcpyDeviceToHost, s));
+      GNNV_TRY_CUDA(cudaMemcpyAsync(t->h_err, b->d_sizes + 2 * L + 1, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+      GNNV_TRY_CUDA(cudaStreamSynchronize(s));
+      if (loss_out) *loss_out = t->h_out[0];
+      if (t->h_err[0]) {
+        GNNV_TRY_CUDA(cudaMemsetAsync(b->d_sizes + 2 * L + 1, 0, sizeof(int32_t), s));
+        throw Error{GNNV_ERR_PARAM, "step: repeated or out-of-range seed id"};
+      }
+    }
+    if (tm) {
+      float ms[7];
+      for (int i = 0; i < 7; ++i) GNNV_TRY_CUDA(cudaEventElapsedTime(&ms[i], t->ev[i], t->ev[i + 1]));
+      tm->sample_ms = ms[0];
+      tm->gather_ms = ms[1];
+      tm->fwd_ms = ms[2];
+      tm->loss_ms = ms[3];
+      tm->bwd_ms = ms[4];
+      tm->allreduce_ms = ms[5];
+      tm->update_ms = ms[6];
+      GNNV_TRY_CUDA(cudaEventElapsedTime(&tm->total_ms, t->ev[0], t->ev[7]));
+    }
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,425 @@
+"""Thin ctypes binding of libgnnv (include/gnnv.h).  Argument marshalling only:
+every step of the hot path runs in the CUDA kernels of libgnnv.so.  There is
+no fallback: if the library is missing, importing the entry points raises.
+
+Names mirror the C API without the `gnnv_` prefix.  Device buffers are given
+as torch CUDA tensors (or raw integer pointers); torch is used only for
+device memory, streams and process groups.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from typing import List, Optional, Sequence
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libgnnv.so")
+MAX_LAYERS = 8
+
+OK, ERR_PARAM, ERR_STATE, ERR_OOM, ERR_CUDA, ERR_COMM, ERR_UNSUPPORTED = range(7)
+POLICY_NONE, POLICY_DEGREE, POLICY_FIFO, POLICY_LRU = range(4)
+PLACE_REPLICA, PLACE_SHARDED, PLACE_SHARDED_LOCAL = range(3)
+KIND_SAGE, KIND_GCN = 0, 1
+AGGR_MEAN, AGGR_SUM = 0, 1
+ACT_NONE, ACT_RELU = 0, 1
+PREC_FP32, PREC_BF16 = 0, 1
+STATUS_NAMES = {0: "OK", 1: "ERR_PARAM", 2: "ERR_STATE", 3: "ERR_OOM", 4: "ERR_CUDA", 5: "ERR_COMM",
+                6: "ERR_UNSUPPORTED"}
+
+
+class GnnvError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{STATUS_NAMES.get(status, status)}: {msg}")
+        self.status = status
+
+
+class BlockView(C.Structure):
+    _fields_ = [("n_dst", C.c_int64), ("n_src", C.c_int64), ("nnz", C.c_int64),
+                ("max_dst", C.c_int64), ("max_src", C.c_int64), ("max_nnz", C.c_int64),
+                ("d_indptr", C.c_void_p), ("d_indices", C.c_void_p), ("d_src_global", C.c_void_p)]
+
+
+class GraphView(C.Structure):
+    _fields_ = [("n_nodes", C.c_int64), ("nnz", C.c_int64), ("feat_dim", C.c_int32), ("row_stride", C.c_int32),
+                ("n_classes", C.c_int32), ("device", C.c_int32), ("d_indptr", C.c_void_p),
+                ("d_indices", C.c_void_p), ("d_labels", C.c_void_p), ("d_host_feats", C.c_void_p)]
+
+
+class CacheView(C.Structure):
+    _fields_ = [("capacity", C.c_int64), ("local_rows", C.c_int64), ("bytes", C.c_int64), ("world", C.c_int32),
+                ("rank", C.c_int32), ("placement", C.c_int32), ("d_slot", C.c_void_p), ("d_order", C.c_void_p)]
+
+
+class LayerDesc(C.Structure):
+    _fields_ = [("d_in", C.c_int32), ("d_out", C.c_int32), ("in_stride", C.c_int32), ("kind", C.c_int32),
+                ("aggr", C.c_int32), ("act", C.c_int32), ("prec", C.c_int32)]
+
+
+class ModelDesc(C.Structure):
+    _fields_ = [("L", C.c_int32), ("dims", C.c_int32 * (MAX_LAYERS + 1)), ("fanouts", C.c_int32 * MAX_LAYERS),
+                ("max_seeds", C.c_int32), ("kind", C.c_int32), ("aggr", C.c_int32), ("prec", C.c_int32)]
+
+
+class StepTiming(C.Structure):
+    _fields_ = [(n, C.c_float) for n in ("sample_ms", "gather_ms", "fwd_ms", "loss_ms", "bwd_ms",
+                                          "allreduce_ms", "update_ms", "total_ms")]
+
+    def as_dict(self):
+        return {n: float(getattr(self, n)) for n, _ in self._fields_}
+
+
+VP, I32, I64, U64, F32, F64 = C.c_void_p, C.c_int32, C.c_int64, C.c_uint64, C.c_float, C.c_double
+PP = C.POINTER(C.c_void_p)
+
+# name -> (restype, argtypes)
+_SIGS = {
+    "gnnv_last_error": (C.c_char_p, []),
+    "gnnv_version": (C.c_char_p, []),
+    "gnnv_row_stride": (I32, [I32]),
+    "gnnv_graph_load": (I32, [VP, VP, I64, I64, VP, I32, I32, VP, I32, I32, PP]),
+    "gnnv_graph_free": (I32, [VP]),
+    "gnnv_graph_info": (I32, [VP, C.POINTER(GraphView)]),
+    "gnnv_comm_unique_id": (I32, [VP]),
+    "gnnv_comm_init": (I32, [I32, I32, VP, I32, PP]),
+    "gnnv_comm_free": (I32, [VP]),
+    "gnnv_allreduce_sum": (I32, [VP, VP, I64, VP]),
+    "gnnv_cache_build": (I32, [VP, F64, I32, I32, VP, I32, PP]),
+    "gnnv_cache_free": (I32, [VP]),
+    "gnnv_cache_info": (I32, [VP, C.POINTER(CacheView)]),
+    "gnnv_blocks_create": (I32, [VP, I32, VP, I32, PP]),
+    "gnnv_blocks_free": (I32, [VP]),
+    "gnnv_sample": (I32, [VP, VP, I32, VP, I32, U64, VP, VP]),
+    "gnnv_blocks_info": (I32, [VP, I32, VP, C.POINTER(BlockView)]),
+    "gnnv_blocks_device_sizes": (VP, [VP]),
+    "gnnv_blocks_num_layers": (I32, [VP]),
+    "gnnv_gather": (I32, [VP, VP, VP, VP, VP]),
+    "gnnv_layer_fwd": (I32, [VP, I32, C.POINTER(LayerDesc), VP, VP, VP, VP, VP, VP]),
+    "gnnv_layer_bwd": (I32, [VP, I32, C.POINTER(LayerDesc), VP, VP, VP, VP, VP, VP, VP, VP, VP]),
+    "gnnv_ce_loss": (I32, [VP, VP, VP, I32, I32, I32, VP, VP, VP]),
+    "gnnv_sgd": (I32, [VP, VP, I64, F32, VP]),
+    "gnnv_trainer_create": (I32, [VP, VP, C.POINTER(ModelDesc), VP, VP, PP]),
+    "gnnv_trainer_free": (I32, [VP]),
+    "gnnv_trainer_num_params": (I64, [VP]),
+    "gnnv_trainer_get": (I32, [VP, VP, VP]),
+    "gnnv_trainer_set_params": (I32, [VP, VP]),
+    "gnnv_trainer_blocks": (VP, [VP]),
+    "gnnv_trainer_activation": (I32, [VP, I32, PP, C.POINTER(I32)]),
+    "gnnv_step": (I32, [VP, VP, I32, I32, I32, U64, F32, C.POINTER(F32), C.POINTER(StepTiming), VP]),
+    "gnnv_trainer_stats": (I32, [VP, VP]),
+}
+EXPORTS = sorted(_SIGS)
+
+_lib: Optional[C.CDLL] = None
+
+
+def load(path: str = LIB_PATH) -> C.CDLL:
+    """Load libgnnv.so (raises if it is missing -- there is no fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise RuntimeError(f"libgnnv.so not built at {path}: run `python -m paper_2404_09544_b200.build`")
+    lib = C.CDLL(path, mode=C.RTLD_GLOBAL)
+    for name, (res, args) in _SIGS.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    _lib = lib
+    return lib
+
+
+def _check(st: int):
+    if st != OK:
+        raise GnnvError(st, load().gnnv_last_error().decode(errors="replace"))
+
+
+def ptr(x) -> Optional[int]:
+    """Device/host pointer of a torch tensor, numpy array, int or None."""
+    if x is None:
+        return None
+    if isinstance(x, int):
+        return x
+    if isinstance(x, np.ndarray):
+        return x.ctypes.data
+    return x.data_ptr()
+
+
+def stream_ptr(s=None) -> Optional[int]:
+    if s is None:
+        import torch
+        s = torch.cuda.current_stream()
+    if isinstance(s, int):
+        return s
+    return s.cuda_stream
+
+
+def version() -> str:
+    return load().gnnv_version().decode()
+
+
+def row_stride(d: int) -> int:
+    return int(load().gnnv_row_stride(d))
+
+
+def preload_nccl():
+    """Make libnccl.so.2 (the torch-bundled one) resolvable for dlopen."""
+    try:
+        import nvidia.nccl  # type: ignore
+        for p in nvidia.nccl.__path__:
+            cand = os.path.join(p, "lib", "libnccl.so.2")
+            if os.path.exists(cand):
+                C.CDLL(cand, mode=C.RTLD_GLOBAL)
+                os.environ.setdefault("GNNV_NCCL_LIB", cand)
+                return cand
+    except Exception:
+        pass
+    return None
+
+
+# --------------------------------------------------------------- handles
+class Graph:
+    """gnnv_graph_load.  Keeps the borrowed host arrays alive."""
+
+    def __init__(self, indptr, indices, feats: np.ndarray, d: int, labels, n_classes: int, device: int = 0):
+        lib = load()
+        self.indptr = np.ascontiguousarray(indptr, dtype=np.int64)
+        self.indices = np.ascontiguousarray(indices, dtype=np.int32)
+        if not (feats.flags.c_contiguous and feats.dtype == np.float32 and feats.ctypes.data % 16 == 0):
+            raise ValueError("feats must be C-contiguous float32, 16-byte aligned")
+        self.feats = feats
+        self.labels = np.ascontiguousarray(labels, dtype=np.int32)
+        self.n = int(self.indptr.shape[0] - 1)
+        self.d = int(d)
+        self.stride = int(feats.shape[1])
+        self.n_classes = int(n_classes)
+        h = C.c_void_p()
+        _check(lib.gnnv_graph_load(ptr(self.indptr), ptr(self.indices), self.n, int(self.indices.shape[0]),
+                                   ptr(feats), self.d, self.stride, ptr(self.labels), self.n_classes, device,
+                                   C.byref(h)))
+        self.h = h
+
+    @classmethod
+    def from_data(cls, gd, device: int = 0):
+        return cls(gd.indptr, gd.indices, gd.feats, gd.d, gd.labels, gd.C, device)
+
+    def info(self) -> GraphView:
+        v = GraphView()
+        _check(load().gnnv_graph_info(self.h, C.byref(v)))
+        return v
+
+    def free(self):
+        if getattr(self, "h", None):
+            load().gnnv_graph_free(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+
+class Comm:
+    def __init__(self, rank: int, world: int, unique_id: bytes, device: int):
+        preload_nccl()
+        h = C.c_void_p()
+        buf = C.create_string_buffer(bytes(unique_id), 128)
+        _check(load().gnnv_comm_init(rank, world, buf, device, C.byref(h)))
+        self.h, self.rank, self.world = h, rank, world
+
+    @staticmethod
+    def unique_id() -> bytes:
+        preload_nccl()
+        buf = C.create_string_buffer(128)
+        _check(load().gnnv_comm_unique_id(buf))
+        return buf.raw
+
+    def allreduce_sum(self, t, stream=None):
+        _check(load().gnnv_allreduce_sum(self.h, ptr(t), int(t.numel()), stream_ptr(stream)))
+
+    def free(self):
+        if getattr(self, "h", None):
+            load().gnnv_comm_free(self.h)
+            self.h = None
+
+
+class Cache:
+    def __init__(self, g: Graph, ratio: float, policy: int = POLICY_DEGREE, placement: int = PLACE_REPLICA,
+                 comm: Optional[Comm] = None, virtual_shards: int = 1):
+        h = C.c_void_p()
+        _check(load().gnnv_cache_build(g.h, float(ratio), policy, placement, comm.h if comm else None,
+                                       virtual_shards, C.byref(h)))
+        self.h, self.g = h, g
+
+    def info(self) -> CacheView:
+        v = CacheView()
+        _check(load().gnnv_cache_info(self.h, C.byref(v)))
+        return v
+
+    def free(self):
+        if getattr(self, "h", None):
+            load().gnnv_cache_free(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+
+def _i32arr(xs: Sequence[int]):
+    a = (C.c_int32 * max(1, len(xs)))()
+    for i, x in enumerate(xs):
+        a[i] = int(x)
+    return a
+
+
+class Blocks:
+    def __init__(self, g: Graph, max_seeds: int, fanouts: Sequence[int], h: Optional[C.c_void_p] = None):
+        self.g, self.fanouts, self.L = g, list(fanouts), len(fanouts)
+        self.owned = h is None
+        if h is None:
+            h = C.c_void_p()
+            _check(load().gnnv_blocks_create(g.h, max_seeds, _i32arr(fanouts), len(fanouts), C.byref(h)))
+        self.h = h
+
+    def sample(self, d_seeds, n_seeds: int, rng_seed: int, stream=None):
+        _check(load().gnnv_sample(self.g.h, ptr(d_seeds), int(n_seeds), _i32arr(self.fanouts), self.L,
+                                  int(rng_seed) & 0xFFFFFFFFFFFFFFFF, self.h, stream_ptr(stream)))
+
+    def info(self, sync: bool = True, stream=None) -> List[BlockView]:
+        arr = (BlockView * self.L)()
+        _check(load().gnnv_blocks_info(self.h, 1 if sync else 0, stream_ptr(stream), arr))
+        return [arr[i] for i in range(self.L)]
+
+    def device_sizes(self) -> int:
+        return int(load().gnnv_blocks_device_sizes(self.h))
+
+    def free(self):
+        if self.owned and getattr(self, "h", None):
+            load().gnnv_blocks_free(self.h)
+        self.h = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+
+def gather(cache: Cache, blocks: Blocks, X, stats=None, stream=None):
+    _check(load().gnnv_gather(cache.h, blocks.h, ptr(X), ptr(stats), stream_ptr(stream)))
+
+
+def layer_desc(d_in, d_out, in_stride, kind=KIND_SAGE, aggr=AGGR_MEAN, act=ACT_RELU, prec=PREC_FP32) -> LayerDesc:
+    return LayerDesc(int(d_in), int(d_out), int(in_stride), int(kind), int(aggr), int(act), int(prec))
+
+
+def layer_fwd(blocks: Blocks, layer: int, ld: LayerDesc, Hsrc, W, b, Hdst, saveA, stream=None):
+    _check(load().gnnv_layer_fwd(blocks.h, layer, C.byref(ld), ptr(Hsrc), ptr(W), ptr(b), ptr(Hdst), ptr(saveA),
+                                 stream_ptr(stream)))
+
+
+def layer_bwd(blocks: Blocks, layer: int, ld: LayerDesc, Gdst, Hdst, Hsrc, saveA, W, Gsrc, dW, db, stream=None):
+    _check(load().gnnv_layer_bwd(blocks.h, layer, C.byref(ld), ptr(Gdst), ptr(Hdst), ptr(Hsrc), ptr(saveA), ptr(W),
+                                 ptr(Gsrc), ptr(dW), ptr(db), stream_ptr(stream)))
+
+
+def ce_loss(blocks: Blocks, g: Graph, logits, n_classes, stride, n_global, loss, dlogits, stream=None):
+    _check(load().gnnv_ce_loss(blocks.h, g.h, ptr(logits), int(n_classes), int(stride), int(n_global), ptr(loss),
+                               ptr(dlogits), stream_ptr(stream)))
+
+
+def sgd(params, grads, n: int, lr: float, stream=None):
+    _check(load().gnnv_sgd(ptr(params), ptr(grads), int(n), float(lr), stream_ptr(stream)))
+
+
+def flat_params(weights) -> np.ndarray:
+    """[(W, b), ...] -> the trainer's flat layout (W row-major, then b, per layer)."""
+    return np.concatenate([np.concatenate([np.asarray(W, np.float32).ravel(), np.asarray(b, np.float32).ravel()])
+                           for W, b in weights]).astype(np.float32)
+
+
+def unflat_params(flat: np.ndarray, dims: Sequence[int], kind: int = KIND_SAGE):
+    out, off = [], 0
+    for i in range(len(dims) - 1):
+        rows = (2 if kind == KIND_SAGE else 1) * dims[i]
+        W = flat[off: off + rows * dims[i + 1]].reshape(rows, dims[i + 1])
+        off += rows * dims[i + 1]
+        b = flat[off: off + dims[i + 1]]
+        off += dims[i + 1]
+        out.append((W, b))
+    return out
+
+
+class Trainer:
+    """gnnv_trainer_*: whole-iteration runner (gnnv_step)."""
+
+    def __init__(self, g: Graph, cache: Cache, dims: Sequence[int], fanouts: Sequence[int], max_seeds: int,
+                 weights, kind=KIND_SAGE, aggr=AGGR_MEAN, prec=PREC_FP32, comm: Optional[Comm] = None):
+        md = ModelDesc()
+        md.L = len(fanouts)
+        for i, x in enumerate(dims):
+            md.dims[i] = int(x)
+        for i, x in enumerate(fanouts):
+            md.fanouts[i] = int(x)
+        md.max_seeds, md.kind, md.aggr, md.prec = int(max_seeds), int(kind), int(aggr), int(prec)
+        self.dims, self.kind, self.L = list(dims), kind, len(fanouts)
+        flat = flat_params(weights)
+        h = C.c_void_p()
+        _check(load().gnnv_trainer_create(g.h, cache.h, C.byref(md), ptr(flat), comm.h if comm else None,
+                                          C.byref(h)))
+        self.h, self.g, self.cache, self.comm = h, g, cache, comm
+        self.nparams = int(load().gnnv_trainer_num_params(h))
+        self.blocks = Blocks(g, max_seeds, fanouts, h=C.c_void_p(load().gnnv_trainer_blocks(h)))
+
+    def step(self, seeds, n_seeds: int, n_global: int, rng_seed: int, lr: float, on_host: bool = True,
+             want_loss: bool = True, timing: bool = False, stream=None):
+        loss = C.c_float(0.0)
+        tm = StepTiming()
+        if on_host:
+            seeds = np.ascontiguousarray(seeds, dtype=np.int32)
+        _check(load().gnnv_step(self.h, ptr(seeds), int(n_seeds), 1 if on_host else 0, int(n_global),
+                                int(rng_seed) & 0xFFFFFFFFFFFFFFFF, float(lr),
+                                C.byref(loss) if want_loss else None, C.byref(tm) if timing else None,
+                                stream_ptr(stream)))
+        return (float(loss.value) if want_loss else None), (tm.as_dict() if timing else None)
+
+    def params(self) -> np.ndarray:
+        out = np.empty(self.nparams, np.float32)
+        _check(load().gnnv_trainer_get(self.h, ptr(out), None))
+        return out
+
+    def grads(self) -> np.ndarray:
+        out = np.empty(self.nparams, np.float32)
+        _check(load().gnnv_trainer_get(self.h, None, ptr(out)))
+        return out
+
+    def set_params(self, flat: np.ndarray):
+        flat = np.ascontiguousarray(flat, np.float32)
+        _check(load().gnnv_trainer_set_params(self.h, ptr(flat)))
+
+    def activation(self, i: int):
+        p = C.c_void_p()
+        st = C.c_int32()
+        _check(load().gnnv_trainer_activation(self.h, i, C.byref(p), C.byref(st)))
+        return int(p.value), int(st.value)
+
+    def stats(self) -> np.ndarray:
+        out = np.zeros(4, np.int64)
+        _check(load().gnnv_trainer_stats(self.h, ptr(out)))
+        return out
+
+    def free(self):
+        if getattr(self, "h", None):
+            load().gnnv_trainer_free(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass

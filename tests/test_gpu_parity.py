@@ -1,0 +1,307 @@
+"""-m gpu parity tests: the CUDA path (through the C-ABI) vs the CPU oracle on
+the same seeded inputs.  Integer work (sampling, relabelling, cache slots,
+hit counters) and gathered rows are bit-exact; floating point within the
+condition-aware tolerance of reading Q17 (1e-5 fp32, 2e-2 bf16)."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from oracle.cache import access_counts, cache_slots
+from oracle.layers import agg_matrix, ce_loss, layer_bwd, layer_fwd, train_step
+from oracle.sampler import Block, sample_blocks
+from paper_2404_09544_b200 import gnnv
+from synth import CONFIGS, epoch_seeds, init_weights, make_graph, row_stride, tiny_graph
+
+from gpu_util import assert_close_cond, blocks_to_host, dev_f32, dev_i32, lib, normwise
+
+pytestmark = pytest.mark.gpu
+
+RTOL32 = 1e-5
+RTOL16 = 2e-2
+
+
+@pytest.fixture(scope="module")
+def mini():
+    lib()
+    gd = make_graph("mini")
+    g = gnnv.Graph.from_data(gd)
+    return gd, g
+
+
+@pytest.fixture(scope="module")
+def cora():
+    lib()
+    gd = make_graph("cora")
+    g = gnnv.Graph.from_data(gd)
+    return gd, g
+
+
+def gpu_sample(g, seeds, fanouts, rng_seed, max_seeds=None):
+    blocks = gnnv.Blocks(g, max_seeds or len(seeds), fanouts)
+    ds = dev_i32(seeds)
+    blocks.sample(ds, len(seeds), rng_seed)
+    return blocks, blocks_to_host(blocks)
+
+
+def assert_blocks_equal(host_blocks, oF, oB):
+    assert len(host_blocks) == len(oB)
+    for h, ((nd, ns, ptr, idx, F), ob) in enumerate(zip(host_blocks, oB)):
+        assert nd == ob.n_dst and ns == ob.n_src, (h, nd, ns, ob.n_dst, ob.n_src)
+        np.testing.assert_array_equal(F, oF[h + 1], err_msg=f"frontier F_{h + 1}")
+        np.testing.assert_array_equal(ptr, ob.indptr, err_msg=f"indptr hop {h}")
+        np.testing.assert_array_equal(idx, ob.indices, err_msg=f"indices hop {h}")
+
+
+# ------------------------------------------------------------- sampling
+@pytest.mark.parametrize("rng_seed", [0, 1, 0x5EED, 2**63 + 12345])
+@pytest.mark.parametrize("n_seeds", [1, 300, 512])
+def test_sample_bit_exact_mini(mini, rng_seed, n_seeds):
+    gd, g = mini
+    seeds = epoch_seeds(gd.n, 0)[:n_seeds]
+    fan = CONFIGS["mini"]["fanouts"]
+    _, hb = gpu_sample(g, seeds, fan, rng_seed, max_seeds=512)
+    oF, oB = sample_blocks(gd.indptr, gd.indices, seeds, fan, rng_seed)
+    assert_blocks_equal(hb, oF, oB)
+
+
+@pytest.mark.parametrize("fan", [[1], [3, 2], [25, 10], [32, 32, 4], [5, 5, 5, 5]])
+def test_sample_bit_exact_fanouts(mini, fan):
+    gd, g = mini
+    seeds = epoch_seeds(gd.n, 1)[:97]
+    _, hb = gpu_sample(g, seeds, fan, 77)
+    oF, oB = sample_blocks(gd.indptr, gd.indices, seeds, fan, 77)
+    assert_blocks_equal(hb, oF, oB)
+
+
+def test_sample_bit_exact_cora(cora):
+    gd, g = cora
+    cfg = CONFIGS["cora"]
+    for t in range(3):
+        seeds = epoch_seeds(gd.n, 0)[t * cfg["batch"]:(t + 1) * cfg["batch"]]
+        _, hb = gpu_sample(g, seeds, cfg["fanouts"], 0x5EED + t)
+        oF, oB = sample_blocks(gd.indptr, gd.indices, seeds, cfg["fanouts"], 0x5EED + t)
+        assert_blocks_equal(hb, oF, oB)
+
+
+@pytest.mark.parametrize("kind", ["path5", "star10", "isolated", "twostar", "clique"])
+def test_sample_tiny_graphs(kind):
+    lib()
+    gd = tiny_graph(kind)
+    g = gnnv.Graph.from_data(gd)
+    seeds = list(range(min(gd.n, 3)))
+    for fan in ([2], [3, 3], [10, 1]):
+        _, hb = gpu_sample(g, seeds, fan, 5)
+        oF, oB = sample_blocks(gd.indptr, gd.indices, seeds, fan, 5)
+        assert_blocks_equal(hb, oF, oB)
+
+
+def test_sample_repeat_calls_and_reset(mini):
+    """A blocks handle is reusable: tags are reset after every call."""
+    gd, g = mini
+    fan = [15, 10, 5]
+    blocks = gnnv.Blocks(g, 512, fan)
+    perm = epoch_seeds(gd.n, 2)
+    for t in range(4):
+        seeds = perm[t * 200:(t + 1) * 200 + t]
+        blocks.sample(dev_i32(seeds), len(seeds), 1000 + t)
+        hb = blocks_to_host(blocks)
+        oF, oB = sample_blocks(gd.indptr, gd.indices, seeds, fan, 1000 + t)
+        assert_blocks_equal(hb, oF, oB)
+
+
+def test_sample_errors(mini):
+    gd, g = mini
+    blocks = gnnv.Blocks(g, 8, [3])
+    blocks.sample(dev_i32([1, 2, 2]), 3, 0)
+    with pytest.raises(gnnv.GnnvError) as e:
+        blocks.info(sync=True)
+    assert e.value.status == gnnv.ERR_PARAM
+    blocks.sample(dev_i32([1, gd.n + 5]), 2, 0)
+    with pytest.raises(gnnv.GnnvError):
+        blocks.info(sync=True)
+    # the handle recovers after an error
+    blocks.sample(dev_i32([1, 2, 3]), 3, 0)
+    hb = blocks_to_host(blocks)
+    oF, oB = sample_blocks(gd.indptr, gd.indices, [1, 2, 3], [3], 0)
+    assert_blocks_equal(hb, oF, oB)
+    with pytest.raises(gnnv.GnnvError):
+        blocks.sample(dev_i32([1]), 9, 0)  # n_seeds > max_seeds
+    with pytest.raises(gnnv.GnnvError):
+        gnnv.Blocks(g, 8, [0])  # fanout < 1
+
+
+# ----------------------------------------------------------- cache + gather
+@pytest.mark.parametrize("ratio,policy", [(0.0, 1), (0.2, 1), (0.5, 1), (1.0, 1), (0.7, 0)])
+def test_cache_slots_bit_exact(mini, ratio, policy):
+    gd, g = mini
+    c = gnnv.Cache(g, ratio, policy=policy)
+    v = c.info()
+    slot, _, _ = cache_slots(gd.indptr, ratio, policy)
+    from gpu_util import read_i32
+    np.testing.assert_array_equal(read_i32(v.d_slot, gd.n), slot)
+    assert v.capacity == int((slot >= 0).sum())
+
+
+@pytest.mark.parametrize("ratio,placement,G", [(0.3, 0, 1), (0.0, 0, 1), (1.0, 0, 1), (0.45, 2, 4), (1.0, 2, 3)])
+def test_gather_bit_exact(mini, ratio, placement, G):
+    gd, g = mini
+    c = gnnv.Cache(g, ratio, placement=placement, virtual_shards=G)
+    fan = CONFIGS["mini"]["fanouts"]
+    seeds = epoch_seeds(gd.n, 0)[:512]
+    blocks, hb = gpu_sample(g, seeds, fan, 3)
+    FL = hb[-1][4]
+    X = torch.empty((blocks.info(sync=False)[-1].max_src, gd.stride), dtype=torch.float32, device="cuda")
+    stats = torch.zeros(4, dtype=torch.int64, device="cuda")
+    gnnv.gather(c, blocks, X, stats)
+    torch.cuda.synchronize()
+    got = X[: len(FL)].cpu().numpy()
+    ref = oracle.gather_rows(gd.feats, FL)
+    assert got.tobytes() == ref.tobytes()
+    slot, owner, _ = cache_slots(gd.indptr, ratio, world=G)
+    cnt = access_counts(slot, owner, FL, me=0)
+    s = stats.cpu().numpy()
+    assert s.tolist() == [cnt["rows"], cnt["hits_local"], cnt["hits_peer"], cnt["misses_host"]]
+
+
+# ------------------------------------------------------------------ layers
+def _oracle_block(hb, h):
+    nd, ns, ptr, idx, F = hb[h]
+    return Block(n_dst=nd, n_src=ns, indptr=ptr.astype(np.int64), indices=idx.astype(np.int64), src_global=F)
+
+
+@pytest.mark.parametrize("kind,aggr", [(0, 0), (0, 1), (1, 0), (1, 1)])
+@pytest.mark.parametrize("prec", [0, 1])
+def test_layer_fwd_bwd_parity(mini, kind, aggr, prec):
+    gd, g = mini
+    fan = CONFIGS["mini"]["fanouts"]
+    seeds = epoch_seeds(gd.n, 0)[:300]
+    blocks, hb = gpu_sample(g, seeds, fan, 11, max_seeds=512)
+    L = len(fan)
+    rng = np.random.default_rng(0)
+    kname = "sage" if kind == 0 else "gcn"
+    aname = "mean" if aggr == 0 else "sum"
+    rtol = RTOL32 if prec == 0 else RTOL16
+    for layer, (d_in, d_out) in zip(range(1, L + 1), [(gd.d, 64), (64, 64), (64, gd.C)]):
+        h = L - layer
+        ob = _oracle_block(hb, h)
+        s_in = gd.stride if layer == 1 else row_stride(d_in)
+        Hsrc = np.zeros((ob.n_src, s_in), np.float32)
+        Hsrc[:, :d_in] = rng.standard_normal((ob.n_src, d_in)).astype(np.float32)
+        rows = (2 if kind == 0 else 1) * d_in
+        W = (rng.standard_normal((rows, d_out)) / np.sqrt(rows)).astype(np.float32)
+        b = rng.standard_normal(d_out).astype(np.float32)
+        relu = layer < L
+        ld = gnnv.layer_desc(d_in, d_out, s_in, kind, aggr, 1 if relu else 0, prec)
+        dH, dW_, db_ = dev_f32(Hsrc), dev_f32(W), dev_f32(b)
+        so = row_stride(d_out)
+        Hdst = torch.full((ob.n_dst, so), float("nan"), device="cuda")
+        A = torch.full((ob.n_dst, row_stride(d_in)), float("nan"), device="cuda")
+        gnnv.layer_fwd(blocks, layer, ld, dH, dW_, db_, Hdst, A)
+        torch.cuda.synchronize()
+        Ho, Ao = layer_fwd(ob, Hsrc[:, :d_in], W, b, relu, kname, aname)
+        Hm, Am = layer_fwd(ob, Hsrc[:, :d_in], W, b, relu, kname, aname, absval=True)
+        Hg, Ag = Hdst.cpu().numpy(), A.cpu().numpy()
+        assert_close_cond(Ag[:, :d_in], Ao, Am, RTOL32, f"A layer {layer}")
+        assert (Ag[:, d_in:] == 0).all() and (Hg[:, d_out:] == 0).all()
+        assert_close_cond(Hg[:, :d_out], Ho, Hm, rtol, f"H layer {layer}")
+        # backward with a random upstream gradient
+        G = np.zeros((ob.n_dst, so), np.float32)
+        G[:, :d_out] = rng.standard_normal((ob.n_dst, d_out)).astype(np.float32)
+        need_dx = layer > 1
+        Gsrc = torch.full((ob.n_src, s_in), float("nan"), device="cuda") if need_dx else None
+        dW = torch.full((rows, d_out), float("nan"), device="cuda")
+        db = torch.full((d_out,), float("nan"), device="cuda")
+        gnnv.layer_bwd(blocks, layer, ld, dev_f32(G), Hdst, dH, A, dW_, Gsrc, dW, db)
+        torch.cuda.synchronize()
+        # oracle backward on the GPU's forward values (same ReLU mask)
+        rW, rb, rX = layer_bwd(ob, Hsrc[:, :d_in], Ag[:, :d_in], Hg[:, :d_out], W, G[:, :d_out], relu, need_dx,
+                               kname, aname)
+        mW, mb, mX = layer_bwd(ob, np.abs(Hsrc[:, :d_in]), np.abs(Ag[:, :d_in]), Hg[:, :d_out], np.abs(W),
+                               np.abs(G[:, :d_out]), relu, need_dx, kname, aname)
+        assert_close_cond(dW.cpu().numpy(), rW, mW, rtol, f"dW layer {layer}")
+        assert_close_cond(db.cpu().numpy(), rb, mb, rtol, f"db layer {layer}")
+        if need_dx:
+            gx = Gsrc.cpu().numpy()
+            assert_close_cond(gx[:, :d_in], rX, mX, rtol, f"dHsrc layer {layer}")
+            assert (gx[:, d_in:] == 0).all()
+
+
+def test_ce_loss_parity(mini):
+    gd, g = mini
+    seeds = epoch_seeds(gd.n, 0)[:333]
+    blocks, hb = gpu_sample(g, seeds, [4], 1)
+    C = gd.C
+    so = row_stride(C)
+    z = np.zeros((len(seeds), so), np.float32)
+    z[:, :C] = 3 * np.random.default_rng(1).standard_normal((len(seeds), C))
+    loss = torch.zeros(1, device="cuda")
+    dz = torch.full((len(seeds), so), float("nan"), device="cuda")
+    gnnv.ce_loss(blocks, g, dev_f32(z), C, so, 1000, loss, dz)
+    torch.cuda.synchronize()
+    rl, rdz = ce_loss(z[:, :C], gd.labels[seeds], 1000)
+    assert abs(float(loss.item()) - rl) <= 1e-5 * abs(rl)
+    dzg = dz.cpu().numpy()
+    np.testing.assert_allclose(dzg[:, :C], rdz, rtol=1e-5, atol=1e-9)
+    assert (dzg[:, C:] == 0).all()
+    # deterministic: same result twice, bitwise
+    loss2 = torch.zeros(1, device="cuda")
+    gnnv.ce_loss(blocks, g, dev_f32(z), C, so, 1000, loss2, dz)
+    torch.cuda.synchronize()
+    assert loss.item() == loss2.item()
+
+
+# -------------------------------------------------------------- full step
+@pytest.mark.parametrize("kind,prec", [(0, 0), (1, 0), (0, 1)])
+def test_step_parity(mini, kind, prec):
+    gd, g = mini
+    cfg = CONFIGS["mini"]
+    dims = [gd.d, cfg["hidden"], cfg["hidden"], gd.C]
+    kname = "sage" if kind == 0 else "gcn"
+    w = init_weights(dims, kind=kname)
+    cache = gnnv.Cache(g, cfg["ratio"])
+    tr = gnnv.Trainer(g, cache, dims, cfg["fanouts"], cfg["batch"], w, kind=kind, prec=prec)
+    perm = epoch_seeds(gd.n, 0)
+    seeds = perm[: cfg["batch"]]
+    lr = 0.05
+    loss, tm = tr.step(seeds, len(seeds), 2 * len(seeds), 0x5EED, lr, timing=True)
+    ref = train_step(gd.indptr, gd.indices, gd.feats, gd.d, gd.labels, seeds, cfg["fanouts"], 0x5EED, w, lr,
+                     n_global=2 * len(seeds), kind=kname)
+    tol = 1e-4 if prec == 0 else 3e-2
+    assert abs(loss - ref["loss"]) <= tol * abs(ref["loss"])
+    grads = gnnv.unflat_params(tr.grads(), dims, kind)
+    for i, ((gW, gb), (rW, rb)) in enumerate(zip(grads, ref["grads"])):
+        assert normwise(gW, rW) < tol, (i, normwise(gW, rW))
+        assert normwise(gb, rb) < tol, (i, normwise(gb, rb))
+    newp = gnnv.unflat_params(tr.params(), dims, kind)
+    for (pW, pb), (nW, nb) in zip(newp, ref["new_weights"]):
+        assert normwise(pW, nW) < 1e-5
+    st = tr.stats()
+    slot, owner, _ = cache_slots(gd.indptr, cfg["ratio"])
+    cnt = access_counts(slot, owner, ref["frontiers"][-1])
+    assert st.tolist() == [cnt["rows"], cnt["hits_local"], cnt["hits_peer"], cnt["misses_host"]]
+    assert all(v >= 0 for v in tm.values())
+    # second step from the updated weights keeps matching
+    seeds2 = perm[cfg["batch"]: 2 * cfg["batch"]]
+    loss2, _ = tr.step(seeds2, len(seeds2), len(seeds2), 0x5EED + 1, lr)
+    ref2 = train_step(gd.indptr, gd.indices, gd.feats, gd.d, gd.labels, seeds2, cfg["fanouts"], 0x5EED + 1,
+                      ref["new_weights"], lr, kind=kname)
+    assert abs(loss2 - ref2["loss"]) <= tol * abs(ref2["loss"])
+
+
+def test_step_device_seeds_and_errors(mini):
+    gd, g = mini
+    dims = [gd.d, 32, gd.C]
+    w = init_weights(dims)
+    cache = gnnv.Cache(g, 0.5)
+    tr = gnnv.Trainer(g, cache, dims, [5, 5], 128, w)
+    seeds = epoch_seeds(gd.n, 3)[:128]
+    l1, _ = tr.step(dev_i32(seeds), 128, 128, 9, 0.0, on_host=False)
+    l2, _ = tr.step(seeds, 128, 128, 9, 0.0, on_host=True)
+    assert l1 == l2  # lr 0: identical iteration, bitwise
+    with pytest.raises(gnnv.GnnvError):
+        tr.step(np.array([1, 1, 2], np.int32), 3, 3, 9, 0.0)
+    with pytest.raises(gnnv.GnnvError):
+        tr.step(seeds, 129, 129, 9, 0.0)
+    l3, _ = tr.step(seeds, 128, 128, 9, 0.0)
+    assert l3 == l1
