@@ -287,6 +287,18 @@ gnnv_status gnnv_trainer_activation(gnnv_trainer* t, int32_t i, const float** d_
 gnnv_status gnnv_step(gnnv_trainer* t, const int32_t* seeds, int32_t n_seeds, int32_t seeds_on_host,
                       int32_t n_global, uint64_t rng_seed, float lr, float* loss_out, gnnv_step_timing* tm,
                       gnnv_stream s);
+/* Fine-grained timeline: with on=1 every gnnv_step records CUDA events on its
+ * stream around each kernel group (sample, gather, spmm_fwd.l<i>,
+ * gemm_fwd.l<i>, loss, relu_mask.l<i>, gemm_dw.l<i>, gemm_dx.l<i>,
+ * spmm_bwd.l<i>, allreduce, sgd) without synchronising.  _read synchronises
+ * the device and returns the per-name totals since the last read/enable. */
+typedef struct {
+  char name[32];
+  double total_ms;
+  int32_t count;
+} gnnv_segment;
+gnnv_status gnnv_trainer_timeline(gnnv_trainer* t, int32_t on);
+gnnv_status gnnv_trainer_timeline_read(gnnv_trainer* t, gnnv_segment* out, int32_t cap, int32_t* n_out);
 /* Device counters of the last step's gather: int64[4] (see gnnv_gather). */
 gnnv_status gnnv_trainer_stats(gnnv_trainer* t, int64_t* host_stats4);
 

@@ -119,6 +119,34 @@ struct gnnv_blocks {
 
 namespace gnnv {
 
+// Named segments of a step, bracketed by CUDA events on the step's stream
+// and read back after the timed region (no sync inside a step).  Segment j
+// runs from mark j to mark j+1.
+struct Timeline {
+  bool on = false;
+  std::vector<cudaEvent_t> pool;
+  size_t used = 0;
+  std::vector<std::pair<std::string, cudaEvent_t>> marks;
+  void mark(cudaStream_t s, const std::string& name) {
+    if (!on) return;
+    if (used == pool.size()) {
+      cudaEvent_t e;
+      GNNV_TRY_CUDA(cudaEventCreate(&e));
+      pool.push_back(e);
+    }
+    cudaEvent_t e = pool[used++];
+    GNNV_TRY_CUDA(cudaEventRecord(e, s));
+    marks.emplace_back(name, e);
+  }
+  void clear() {
+    used = 0;
+    marks.clear();
+  }
+  ~Timeline() {
+    for (auto e : pool) cudaEventDestroy(e);
+  }
+};
+
 // kernels implemented in the .cu files -----------------------------------
 // sample.cu
 void launch_sample(gnnv_graph* g, gnnv_blocks* b, const int32_t* d_seeds, int32_t n_seeds, uint64_t rng_seed,

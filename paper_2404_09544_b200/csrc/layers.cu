@@ -114,7 +114,9 @@ static void check_layer(const gnnv_blocks* b, int32_t layer, const gnnv_layer_de
 }
 
 void layer_fwd_impl(gnnv_blocks* b, int32_t layer, const gnnv_layer_desc* ld, const float* Hsrc, const float* W,
-                    const float* bias, float* Hdst, float* A, cudaStream_t s) {
+                    const float* bias, float* Hdst, float* A, cudaStream_t s, Timeline* tl) {
+  const std::string sfx = ".l" + std::to_string(layer);
+  if (tl) tl->mark(s, "spmm_fwd" + sfx);
   const int h = b->L - layer;
   const int32_t* d_ndst = b->d_sizes + h;
   const int lda = row_stride(ld->d_in), ldo = row_stride(ld->d_out);
@@ -141,12 +143,14 @@ void layer_fwd_impl(gnnv_blocks* b, int32_t layer, const gnnv_layer_desc* ld, co
   g.d_M = d_ndst;
   g.max_M = b->max_n[h];
   g.relu = ld->act == GNNV_ACT_RELU;
+  if (tl) tl->mark(s, "gemm_fwd" + sfx);
   gemm_fwd(g, ld->prec, s);
 }
 
 void layer_bwd_impl(gnnv_blocks* b, int32_t layer, const gnnv_layer_desc* ld, const float* Gdst, const float* Hdst,
                     const float* Hsrc, const float* A, const float* W, float* Gsrc, float* dW, float* db,
-                    cudaStream_t s) {
+                    cudaStream_t s, Timeline* tl) {
+  const std::string sfx = ".l" + std::to_string(layer);
   const int h = b->L - layer;
   const int32_t* d_ndst = b->d_sizes + h;
   const int64_t max_dst = b->max_n[h];
@@ -165,6 +169,7 @@ void layer_bwd_impl(gnnv_blocks* b, int32_t layer, const gnnv_layer_desc* ld, co
   float* dA = Gp + al(gp_f);
   const float* G = Gdst;
   if (relu) {
+    if (tl) tl->mark(s, "relu_mask" + sfx);
     launch_relu_mask(Gdst, Hdst, Gp, ldo, ld->d_out, d_ndst, max_dst, s);
     G = Gp;
   }
@@ -188,6 +193,7 @@ void layer_bwd_impl(gnnv_blocks* b, int32_t layer, const gnnv_layer_desc* ld, co
   w.db = db;
   w.partial = partial;
   w.splits = splits;
+  if (tl) tl->mark(s, "gemm_dw" + sfx);
   gemm_dw(w, ld->prec, s);
   if (Gsrc) {
     GemmDxArgs x{};
@@ -209,7 +215,9 @@ void layer_bwd_impl(gnnv_blocks* b, int32_t layer, const gnnv_layer_desc* ld, co
       x.Y2 = nullptr;
       x.ld2 = 0;
     }
+    if (tl) tl->mark(s, "gemm_dx" + sfx);
     gemm_dx(x, ld->prec, s);
+    if (tl) tl->mark(s, "spmm_bwd" + sfx);
     launch_rows_zero(Gsrc, ld->in_stride, sage ? d_ndst : nullptr, d_ndst + 1, b->max_n[h + 1], s);
     launch_spmm_bwd(b->d_indptr[h], b->d_indices[h], d_ndst, max_dst, dA, lda, Gsrc, ld->in_stride, ld->d_in,
                     ld->kind, ld->aggr, s);
@@ -227,7 +235,7 @@ gnnv_status gnnv_layer_fwd(gnnv_blocks* b, int32_t layer, const gnnv_layer_desc*
   return guarded([&] {
     check_layer(b, layer, ld);
     GNNV_REQUIRE(d_Hsrc && d_W && d_b && d_Hdst && d_saveA, GNNV_ERR_PARAM, "layer_fwd: null buffer");
-    layer_fwd_impl(b, layer, ld, d_Hsrc, d_W, d_b, d_Hdst, d_saveA, (cudaStream_t)s);
+    layer_fwd_impl(b, layer, ld, d_Hsrc, d_W, d_b, d_Hdst, d_saveA, (cudaStream_t)s, nullptr);
   });
 }
 
@@ -238,7 +246,7 @@ gnnv_status gnnv_layer_bwd(gnnv_blocks* b, int32_t layer, const gnnv_layer_desc*
     check_layer(b, layer, ld);
     GNNV_REQUIRE(d_Gdst && d_Hdst && d_Hsrc && d_saveA && d_W && d_dW && d_db, GNNV_ERR_PARAM,
                  "layer_bwd: null buffer");
-    layer_bwd_impl(b, layer, ld, d_Gdst, d_Hdst, d_Hsrc, d_saveA, d_W, d_Gsrc, d_dW, d_db, (cudaStream_t)s);
+    layer_bwd_impl(b, layer, ld, d_Gdst, d_Hdst, d_Hsrc, d_saveA, d_W, d_Gsrc, d_dW, d_db, (cudaStream_t)s, nullptr);
   });
 }
 

@@ -11,10 +11,10 @@
 
 namespace gnnv {
 void layer_fwd_impl(gnnv_blocks* b, int32_t layer, const gnnv_layer_desc* ld, const float* Hsrc, const float* W,
-                    const float* bias, float* Hdst, float* A, cudaStream_t s);
+                    const float* bias, float* Hdst, float* A, cudaStream_t s, Timeline* tl);
 void layer_bwd_impl(gnnv_blocks* b, int32_t layer, const gnnv_layer_desc* ld, const float* Gdst, const float* Hdst,
                     const float* Hsrc, const float* A, const float* W, float* Gsrc, float* dW, float* db,
-                    cudaStream_t s);
+                    cudaStream_t s, Timeline* tl);
 }  // namespace gnnv
 
 using namespace gnnv;
@@ -41,6 +41,7 @@ struct gnnv_trainer {
   unsigned int* loss_counter = nullptr;
   int64_t* d_stats = nullptr;
   cudaEvent_t ev[8] = {nullptr};
+  Timeline tl;
 };
 
 static gnnv_layer_desc layer_desc(const gnnv_trainer* t, int i) {
@@ -175,6 +176,42 @@ gnnv_status gnnv_trainer_activation(gnnv_trainer* t, int32_t i, const float** d_
   });
 }
 
+gnnv_status gnnv_trainer_timeline(gnnv_trainer* t, int32_t on) {
+  return guarded([&] {
+    GNNV_REQUIRE(t, GNNV_ERR_PARAM, "trainer_timeline: null");
+    GNNV_TRY_CUDA(cudaDeviceSynchronize());
+    t->tl.clear();
+    t->tl.on = on != 0;
+  });
+}
+
+gnnv_status gnnv_trainer_timeline_read(gnnv_trainer* t, gnnv_segment* out, int32_t cap, int32_t* n_out) {
+  return guarded([&] {
+    GNNV_REQUIRE(t && n_out && (out || cap == 0), GNNV_ERR_PARAM, "trainer_timeline_read: null");
+    GNNV_TRY_CUDA(cudaDeviceSynchronize());
+    std::vector<gnnv_segment> segs;
+    auto& m = t->tl.marks;
+    for (size_t j = 0; j + 1 < m.size(); ++j) {
+      if (m[j].first == "end") continue;
+      float ms = 0.f;
+      GNNV_TRY_CUDA(cudaEventElapsedTime(&ms, m[j].second, m[j + 1].second));
+      size_t k = 0;
+      for (; k < segs.size(); ++k)
+        if (m[j].first == segs[k].name) break;
+      if (k == segs.size()) {
+        gnnv_segment sg{};
+        strncpy(sg.name, m[j].first.c_str(), sizeof(sg.name) - 1);
+        segs.push_back(sg);
+      }
+      segs[k].total_ms += ms;
+      segs[k].count += 1;
+    }
+    t->tl.clear();
+    *n_out = (int32_t)segs.size();
+    for (int32_t i = 0; i < cap && i < (int32_t)segs.size(); ++i) out[i] = segs[i];
+  });
+}
+
 gnnv_status gnnv_trainer_stats(gnnv_trainer* t, int64_t* host_stats4) {
   return guarded([&] {
     GNNV_REQUIRE(t && host_stats4, GNNV_ERR_PARAM, "trainer_stats: null");
@@ -193,6 +230,7 @@ gnnv_status gnnv_step(gnnv_trainer* t, const int32_t* seeds, int32_t n_seeds, in
     gnnv_blocks* b = t->b;
     gnnv_graph* g = t->g;
     const int L = t->md.L;
+    Timeline* tl = t->tl.on ? &t->tl : nullptr;
     if (tm) GNNV_TRY_CUDA(cudaEventRecord(t->ev[0], s));
     const int32_t* d_seeds = seeds;
     if (seeds_on_host) {
@@ -201,37 +239,44 @@ gnnv_status gnnv_step(gnnv_trainer* t, const int32_t* seeds, int32_t n_seeds, in
       // the staging buffer may still feed the previous step's copy
       GNNV_TRY_CUDA(cudaStreamSynchronize(s));
       memcpy(t->h_seeds, seeds, n_seeds * sizeof(int32_t));
+      if (tl) tl->mark(s, "h2d_seeds");
       GNNV_TRY_CUDA(cudaMemcpyAsync(t->d_seeds, t->h_seeds, n_seeds * sizeof(int32_t), cudaMemcpyHostToDevice, s));
       d_seeds = t->d_seeds;
     }
+    if (tl) tl->mark(s, "sample");
     launch_sample(g, b, d_seeds, n_seeds, rng_seed, s);
     b->sampled = true;
-    if (tm) GNNV_TRY_CUDA(cudaEventRecord(t->ev[1], s));
     GNNV_TRY_CUDA(cudaMemsetAsync(t->d_stats, 0, 4 * sizeof(int64_t), s));
+    if (tm) GNNV_TRY_CUDA(cudaEventRecord(t->ev[1], s));
+    if (tl) tl->mark(s, "gather");
     launch_gather(t->c, b, t->H[0], t->d_stats, s);
     if (tm) GNNV_TRY_CUDA(cudaEventRecord(t->ev[2], s));
     for (int i = 1; i <= L; ++i) {
       const gnnv_layer_desc ld = layer_desc(t, i);
       layer_fwd_impl(b, i, &ld, t->H[i - 1], t->d_params + t->w_off[i - 1], t->d_params + t->b_off[i - 1], t->H[i],
-                     t->A[i], s);
+                     t->A[i], s, tl);
     }
     if (tm) GNNV_TRY_CUDA(cudaEventRecord(t->ev[3], s));
     float* d_loss = t->d_grads + t->nparams;
+    if (tl) tl->mark(s, "loss");
     launch_ce_loss(t->H[L], t->Hs[L], t->md.dims[L], b->d_sizes, b->d_F, g->d_labels, n_global, d_loss, t->G[L],
                    t->loss_partial, t->loss_counter, b->max_n[0], s);
     if (tm) GNNV_TRY_CUDA(cudaEventRecord(t->ev[4], s));
     for (int i = L; i >= 1; --i) {
       const gnnv_layer_desc ld = layer_desc(t, i);
       layer_bwd_impl(b, i, &ld, t->G[i], t->H[i], t->H[i - 1], t->A[i], t->d_params + t->w_off[i - 1],
-                     i > 1 ? t->G[i - 1] : nullptr, t->d_grads + t->w_off[i - 1], t->d_grads + t->b_off[i - 1], s);
+                     i > 1 ? t->G[i - 1] : nullptr, t->d_grads + t->w_off[i - 1], t->d_grads + t->b_off[i - 1], s, tl);
     }
     if (tm) GNNV_TRY_CUDA(cudaEventRecord(t->ev[5], s));
+    if (tl) tl->mark(s, "allreduce");
     if (t->comm && t->comm->world > 1) {
       gnnv_status st = gnnv_allreduce_sum(t->comm, t->d_grads, t->nparams + 1, s);
       if (st != GNNV_OK) throw Error{st, get_error()};
     }
     if (tm) GNNV_TRY_CUDA(cudaEventRecord(t->ev[6], s));
+    if (tl) tl->mark(s, "sgd");
     launch_sgd(t->d_params, t->d_grads, t->nparams, lr, s);
+    if (tl) tl->mark(s, "end");
     if (tm) GNNV_TRY_CUDA(cudaEventRecord(t->ev[7], s));
     if (loss_out || tm) {
       GNNV_TRY_CUDA(cudaMemcpyAsync(t->h_out, d_loss, sizeof(float), cudaMemcpyDeviceToHost, s));

@@ -70,6 +70,10 @@ class StepTiming(C.Structure):
         return {n: float(getattr(self, n)) for n, _ in self._fields_}
 
 
+class Segment(C.Structure):
+    _fields_ = [("name", C.c_char * 32), ("total_ms", C.c_double), ("count", C.c_int32)]
+
+
 VP, I32, I64, U64, F32, F64 = C.c_void_p, C.c_int32, C.c_int64, C.c_uint64, C.c_float, C.c_double
 PP = C.POINTER(C.c_void_p)
 
@@ -108,6 +112,8 @@ _SIGS = {
     "gnnv_trainer_activation": (I32, [VP, I32, PP, C.POINTER(I32)]),
     "gnnv_step": (I32, [VP, VP, I32, I32, I32, U64, F32, C.POINTER(F32), C.POINTER(StepTiming), VP]),
     "gnnv_trainer_stats": (I32, [VP, VP]),
+    "gnnv_trainer_timeline": (I32, [VP, I32]),
+    "gnnv_trainer_timeline_read": (I32, [VP, C.POINTER(Segment), I32, C.POINTER(I32)]),
 }
 EXPORTS = sorted(_SIGS)
 
@@ -407,6 +413,16 @@ class Trainer:
         st = C.c_int32()
         _check(load().gnnv_trainer_activation(self.h, i, C.byref(p), C.byref(st)))
         return int(p.value), int(st.value)
+
+    def timeline(self, on: bool):
+        _check(load().gnnv_trainer_timeline(self.h, 1 if on else 0))
+
+    def timeline_read(self):
+        """{name: (total_ms, count)} since the last read (synchronises)."""
+        arr = (Segment * 256)()
+        n = C.c_int32()
+        _check(load().gnnv_trainer_timeline_read(self.h, arr, 256, C.byref(n)))
+        return {arr[i].name.decode(): (float(arr[i].total_ms), int(arr[i].count)) for i in range(min(n.value, 256))}
 
     def stats(self) -> np.ndarray:
         out = np.zeros(4, np.int64)
