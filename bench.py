@@ -1,0 +1,446 @@
+#!/usr/bin/env python
+"""Benchmark: sampled-GraphSAGE training iterations (GNNavigator hot path) on B200.
+
+One step = one whole iteration of Algorithm 1 per rank:
+sample -> gather (degree cache) -> 3 x (SpMM aggregate + dense transform) ->
+softmax-CE loss -> backward -> NCCL all-reduce -> SGD, through the libgnnv
+C-ABI (gnnv_step).  Workload: the ogbn-products-shaped synthetic graph
+(BASELINE.json configs[3]: 2.45M nodes, 61.9M CSR edges, d=100, 47 classes,
+fanouts [15,10,5], 4096 seeds per rank, cache ratio 1.0 replicated).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...
+
+Prints ONE JSON line on rank 0 (see DESIGN.md §6 for every field).
+`--impl reference` times the CPU oracle (oracle/) on the same workload: the
+paper ships no code, so the oracle is this tier's reference arm.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+METRIC = "sampled-GraphSAGE seeds/sec"
+UNIT = "seeds/s"
+FP32_SIMT_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12  # 148 SMs x 128 FP32 lanes x FMA x 1.965 GHz (guide)
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=100)
+    p.add_argument("--warmup", type=int, default=10)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--config", default="products")
+    p.add_argument("--prec", default="fp32", choices=["fp32", "bf16"])
+    p.add_argument("--kind", default="sage", choices=["sage", "gcn"])
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--cpu-baseline-seeds", type=int, default=0, help="seeds in the oracle sample (0 = one batch)")
+    p.add_argument("--ratio", type=float, default=None)
+    return p.parse_args()
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def load_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        pk = json.load(open(path))
+        return dict(hbm=float(pk["hbm_gbs"]), bf16=float(pk["bf16_tflops"]),
+                    bf16_sust=float(pk["bf16_tflops_sustained"]), src="measured (MEASURED_PEAKS.json)")
+    except Exception:
+        return dict(hbm=6650.0, bf16=1590.0, bf16_sust=1400.0, src="fallback (B200_PROFILING.md)")
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.th = threading.Thread(target=self._read, daemon=True)
+            self.th.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        time.sleep(0.15)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        self.th.join(timeout=1)
+        sm, mx, pw, reasons = [], [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx.append(float(f[2]))
+                pw.append(float(f[3]))
+            except ValueError:
+                continue
+            for n, v in zip(names, f[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "power_w_max": max(pw) if pw else None, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def d2d(dst, src_ptr: int, nbytes: int):
+    """Device-to-device copy from a raw libgnnv pointer into a torch tensor."""
+    import ctypes
+
+    rt = ctypes.CDLL("libcudart.so.12")
+    rc = rt.cudaMemcpy(ctypes.c_void_p(dst.data_ptr()), ctypes.c_void_p(int(src_ptr)), ctypes.c_size_t(nbytes), 3)
+    if rc != 0:
+        raise RuntimeError(f"cudaMemcpy failed: {rc}")
+
+
+def cpu_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def oracle_run(gd, cfg, seeds_list, rng_seeds, weights, lr, kind):
+    """Times the oracle (oracle.layers.train_step) on the given seed slices."""
+    from oracle.layers import train_step
+
+    t0 = time.perf_counter()
+    n = 0
+    for seeds, rs in zip(seeds_list, rng_seeds):
+        out = train_step(gd.indptr, gd.indices, gd.feats, gd.d, gd.labels, seeds, cfg["fanouts"], rs, weights,
+                         lr, n_global=len(seeds), kind=kind)
+        weights = out["new_weights"]
+        n += len(seeds)
+    return n, time.perf_counter() - t0
+
+
+def blas_threads():
+    try:
+        from threadpoolctl import threadpool_info
+
+        info = threadpool_info()
+        return max([i.get("num_threads", 1) for i in info] or [1])
+    except Exception:
+        return cpu_cores()
+
+
+def run_reference(args):
+    """--impl reference: the CPU oracle on this workload (rank 0 only)."""
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    from synth import BASE_RNG_SEED, CONFIGS, epoch_seeds, init_weights, make_graph
+
+    cfg = CONFIGS[args.config]
+    gd = make_graph(cfg)
+    dims = [gd.d] + [cfg["hidden"]] * (len(cfg["fanouts"]) - 1) + [gd.C]
+    w = init_weights(dims, kind=args.kind)
+    perm = epoch_seeds(gd.n, 0)
+    # a bounded sample of the batch per reference step, sized so that the
+    # whole --steps/--warmup run stays near two minutes of CPU time
+    probe = min(256, cfg["batch"])
+    _, tp = oracle_run(gd, cfg, [perm[-probe:]], [BASE_RNG_SEED - 1], w, 0.01, args.kind)
+    budget = 120.0 / max(1, args.steps + args.warmup)
+    sub = int(max(16, min(cfg["batch"], budget / max(tp / probe, 1e-9))))
+    seeds = [perm[i * sub:(i + 1) * sub] for i in range(args.warmup + args.steps)]
+    rs = [BASE_RNG_SEED + i for i in range(len(seeds))]
+    oracle_run(gd, cfg, seeds[: args.warmup], rs[: args.warmup], w, 0.01, args.kind)
+    n, t = oracle_run(gd, cfg, seeds[args.warmup:], rs[args.warmup:], w, 0.01, args.kind)
+    value = n / t
+    ms = 1000.0 * t / max(1, args.steps)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": cfg["name"], "n_nodes": gd.n, "nnz": gd.nnz, "d": gd.d, "classes": gd.C,
+                   "fanouts": cfg["fanouts"], "seeds_per_step": sub, "kind": args.kind},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": blas_threads(), "kind": "oracle",
+                         "sample": f"{args.steps} oracle iterations of {sub} seeds each (of a {cfg['batch']}-seed "
+                                   f"batch) on the {cfg['name']}-shaped graph, host CPU, float64"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def algorithmic(seg: str, sizes, cfg, dims, stride, prec, peaks):
+    """(bound, amount per launch, unit, peak) for a timeline segment.
+
+    sizes: dict of per-step averages (n[h], nnz[h], U[h] distinct referenced
+    src rows per block, hits/misses).  Formulas: DESIGN.md §5 / SURVEY §8(d)."""
+    L = len(cfg["fanouts"])
+    n, nnz, U = sizes["n"], sizes["nnz"], sizes["U"]
+    name, _, lay = seg.partition(".l")
+    if name == "gather":
+        rowb = stride * 4
+        by = sizes["hits"] * rowb + n[L] * rowb + n[L] * 8
+        return "hbm", by, "GB/s", peaks["hbm"]
+    if name == "sample":
+        by = sum(n[h] * 16 + nnz[h] * 12 for h in range(L))
+        return "hbm", by, "GB/s", peaks["hbm"]
+    i = int(lay) if lay else 0
+    h = L - i
+    d_in, d_out = dims[i - 1], dims[i]
+    K = 2 * d_in
+    if name == "spmm_fwd":
+        by = U[h] * d_in * 4 + n[h] * ((d_in + 3) & ~3) * 4 + nnz[h] * 4 + (n[h] + 1) * 4
+        return "hbm", by, "GB/s", peaks["hbm"]
+    if name == "spmm_bwd":
+        by = n[h] * d_in * 4 + 2 * U[h] * d_in * 4 + nnz[h] * 4 + n[h + 1] * ((d_in + 3) & ~3) * 4
+        return "hbm", by, "GB/s", peaks["hbm"]
+    if name == "relu_mask":
+        return "hbm", 3 * n[h] * ((d_out + 3) & ~3) * 4, "GB/s", peaks["hbm"]
+    if name in ("gemm_fwd", "gemm_dx"):
+        fl = 2.0 * n[h] * K * d_out
+    elif name == "gemm_dw":
+        fl = 2.0 * n[h] * (K + 1) * d_out
+    else:
+        return None
+    if prec == "bf16":
+        return "tensor", fl, "TFLOP/s", peaks["bf16_sust"]
+    return "alu", fl, "TFLOP/s", FP32_SIMT_TFLOPS
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+    import torch
+    import torch.distributed as dist
+
+    from paper_2404_09544_b200 import gnnv
+    from synth import BASE_RNG_SEED, CONFIGS, epoch_seeds, init_weights, make_graph
+
+    rank, world, local = dist_env()
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    cfg = dict(CONFIGS[args.config])
+    if args.ratio is not None:
+        cfg["ratio"] = args.ratio
+    t_gen = time.perf_counter()
+    gd = make_graph(cfg)
+    t_gen = time.perf_counter() - t_gen
+    gnnv.load()
+    comm = None
+    if world > 1:
+        obj = [gnnv.Comm.unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        comm = gnnv.Comm(rank, world, obj[0], local)
+    g = gnnv.Graph.from_data(gd, device=local)
+    cache = gnnv.Cache(g, cfg["ratio"])
+    dims = [gd.d] + [cfg["hidden"]] * (len(cfg["fanouts"]) - 1) + [gd.C]
+    kind = gnnv.KIND_SAGE if args.kind == "sage" else gnnv.KIND_GCN
+    prec = gnnv.PREC_BF16 if args.prec == "bf16" else gnnv.PREC_FP32
+    w = init_weights(dims, kind=args.kind)
+    B = cfg["batch"]
+    tr = gnnv.Trainer(g, cache, dims, cfg["fanouts"], B, w, kind=kind, prec=prec, comm=comm)
+    stream = torch.cuda.current_stream()
+    lr = 0.01
+    # seeds of global iteration t: perm[t*G*B:(t+1)*G*B], rank r takes the r-th B-slice
+    perm = epoch_seeds(gd.n, 0)
+    iters_per_epoch = math.ceil(gd.n / (world * B))
+    d_perm = torch.as_tensor(perm).cuda()
+
+    def seeds_of(t):
+        t = t % iters_per_epoch
+        lo = t * world * B + rank * B
+        hi = min(gd.n, lo + B)
+        return lo, max(lo, hi)
+
+    def step_device(t):
+        lo, hi = seeds_of(t)
+        if hi <= lo:
+            lo, hi = 0, B
+        nb = hi - lo
+        tr.step(d_perm[lo:hi].data_ptr(), nb, world * B, BASE_RNG_SEED + t, lr, on_host=False, want_loss=False,
+                stream=stream)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    for t in range(args.warmup):
+        step_device(t)
+    barrier()
+    # ---------------------------------------------------------- timed region
+    t0_steps = args.warmup
+    tr.timeline(True)
+    clocks = ClockSampler(local)
+    clocks.start()
+    launches0 = gnnv.launch_count()
+    barrier()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for t in range(t0_steps, t0_steps + args.steps):
+        step_device(t)
+    ev1.record(stream)
+    barrier()
+    launches = gnnv.launch_count() - launches0
+    clk = clocks.stop()
+    ms_total = max_over_ranks(ev0.elapsed_time(ev1))
+    segs = tr.timeline_read()
+    tr.timeline(False)
+    ms_per_step = ms_total / args.steps
+    value = world * B * args.steps / (ms_total / 1000.0)
+    # ------------------------------------------------------- e2e (host I/O)
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t_e2e0 = time.perf_counter()
+    e0.record(stream)
+    loss = None
+    for t in range(t0_steps, t0_steps + args.steps):
+        lo, hi = seeds_of(t)
+        host_seeds = perm[lo:hi]
+        loss, _ = tr.step(host_seeds, len(host_seeds), world * B, BASE_RNG_SEED + t, lr, on_host=True,
+                          want_loss=True, stream=stream)
+    e1.record(stream)
+    barrier()
+    wall_e2e = time.perf_counter() - t_e2e0
+    ms_e2e = max_over_ranks(e0.elapsed_time(e1))
+    value_e2e = world * B * args.steps / (ms_e2e / 1000.0)
+    # ------------------------------------------- sizes of the timed steps
+    nsz = min(args.steps, 8)
+    blk = gnnv.Blocks(g, B, cfg["fanouts"])
+    L = len(cfg["fanouts"])
+    acc = {"n": np.zeros(L + 1), "nnz": np.zeros(L), "U": np.zeros(L), "hits": 0.0, "misses": 0.0}
+    cv = cache.info()
+    slot_map = torch.empty(gd.n, dtype=torch.int32, device="cuda")
+    d2d(slot_map, cv.d_slot, 4 * gd.n)
+    for t in range(t0_steps, t0_steps + nsz):
+        lo, hi = seeds_of(t)
+        blk.sample(d_perm[lo:hi].data_ptr(), hi - lo, BASE_RNG_SEED + t, stream=stream)
+        views = blk.info(sync=True, stream=stream)
+        for h, v in enumerate(views):
+            acc["n"][h] += v.n_dst
+            acc["nnz"][h] += v.nnz
+            if v.nnz:
+                idx = torch.empty(int(v.nnz), dtype=torch.int32, device="cuda")
+                d2d(idx, v.d_indices, 4 * int(v.nnz))
+                acc["U"][h] += int(torch.unique(idx).numel())
+        nL = int(views[-1].n_src)
+        acc["n"][L] += nL
+        FL = torch.empty(nL, dtype=torch.int32, device="cuda")
+        d2d(FL, views[-1].d_src_global, 4 * nL)
+        hit = int((slot_map[FL.long()] >= 0).sum().item())
+        acc["hits"] += hit
+        acc["misses"] += nL - hit
+    sizes = {k: (v / nsz) for k, v in acc.items()}
+    peaks = load_peaks()
+    # dominant kernel segment of the timed region
+    seg_ms = {k: v[0] / max(1, v[1]) for k, v in segs.items()}
+    seg_tot = {k: v[0] for k, v in segs.items()}
+    ranked = sorted(seg_tot.items(), key=lambda kv: -kv[1])
+    roofline = None
+    rooflines = {}
+    for name, tot in ranked:
+        a = algorithmic(name, sizes, cfg, dims, gd.stride, args.prec, peaks)
+        if a is None:
+            continue
+        bound, amount, unit, peak = a
+        avg_ms = seg_ms[name]
+        achieved = amount / (avg_ms / 1000.0) / (1e9 if unit == "GB/s" else 1e12)
+        r = {"kernel": name, "bound": bound, "achieved": achieved, "peak": peak, "unit": unit,
+             "frac": achieved / peak, "traffic": None, "avg_ms": avg_ms,
+             "share_of_step": tot / max(1e-9, sum(seg_tot.values())),
+             "algorithmic_per_launch": amount}
+        rooflines[name] = r
+        if roofline is None:
+            roofline = r
+    # -------------------------------------------------------- CPU baseline
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        ns = args.cpu_baseline_seeds or B
+        lo, hi = seeds_of(t0_steps)
+        n_done, tcpu = oracle_run(gd, cfg, [perm[lo:lo + ns]], [BASE_RNG_SEED + t0_steps], w, lr, args.kind)
+        cpu = {"value": n_done / tcpu, "unit": UNIT, "cores": blas_threads(), "kind": "oracle",
+               "sample": f"1 oracle iteration of {ns} seeds (sample+gather+fwd+loss+bwd+SGD, float64) on the "
+                         f"{cfg['name']}-shaped graph; {tcpu:.1f} s"}
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32" if args.prec == "fp32" else "f32+bf16gemm", "data": "synthetic",
+            "config": {"workload": cfg["name"], "n_nodes": gd.n, "nnz": gd.nnz, "d": gd.d, "classes": gd.C,
+                       "fanouts": cfg["fanouts"], "batch_per_rank": B, "global_batch": world * B,
+                       "cache_ratio": cfg["ratio"], "placement": "replica", "kind": args.kind,
+                       "hidden": cfg["hidden"], "gemm_precision": args.prec,
+                       "l2": "inputs > L2 (feature table %.0f MB, gathered X %.0f MB per step)" % (
+                           gd.n * gd.stride * 4 / 1e6, sizes["n"][L] * gd.stride * 4 / 1e6),
+                       "parallelism": f"dp{world}"},
+            "epoch_s": iters_per_epoch * ms_per_step / 1000.0,
+            "iters_per_epoch": iters_per_epoch,
+            "clocks": clk,
+            "gpu_launches": int(launches),
+            "roofline": roofline,
+            "rooflines": rooflines,
+            "phases_ms_per_step": {k: v[0] / args.steps for k, v in sorted(segs.items(), key=lambda kv: -kv[1][0])},
+            "sizes_per_step": {"frontier": [round(x) for x in sizes["n"]], "edges": [round(x) for x in sizes["nnz"]],
+                               "distinct_src": [round(x) for x in sizes["U"]], "cache_hits": sizes["hits"],
+                               "cache_misses": sizes["misses"]},
+            "e2e": {"value": value_e2e, "unit": UNIT, "h2d_bytes_per_step": B * 4, "d2h_bytes_per_step": 8,
+                    "ms_per_step": ms_e2e / args.steps, "wall_s": wall_e2e, "last_loss": loss},
+            "cpu_baseline": cpu,
+            "peaks": peaks["src"],
+            "graph_gen_s": t_gen,
+        }
+        print(json.dumps(line), flush=True)
+    tr.free()
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -90,6 +90,8 @@ typedef enum { GNNV_PREC_FP32 = 0, GNNV_PREC_BF16 = 1 } gnnv_prec;
 /* ------------------------------------------------------------------ misc */
 const char* gnnv_last_error(void);
 const char* gnnv_version(void);
+/* Number of kernels libgnnv has launched in this process (monotonic). */
+uint64_t gnnv_launch_count(void);
 /* d rounded up to a multiple of 4 (floats). */
 int32_t gnnv_row_stride(int32_t d);
 

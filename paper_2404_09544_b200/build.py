@@ -55,9 +55,9 @@ def _sources():
 def _digest(debug: bool) -> str:
     h = hashlib.sha256()
     for p in _sources() + sorted(glob.glob(os.path.join(CSRC, "*.cuh"))) + [os.path.join(ROOT, "include", "gnnv.h")]:
-        h.update(p.encode())
+        h.update(os.path.relpath(p, ROOT).encode())
         h.update(open(p, "rb").read())
-    h.update(" ".join(_flags(debug)).encode())
+    h.update(" ".join(f for f in _flags(debug) if not f.startswith("-I")).encode())
     return h.hexdigest()
 
 

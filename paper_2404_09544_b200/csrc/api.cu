@@ -4,6 +4,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <atomic>
 #include <mutex>
 
 #include "common.cuh"
@@ -12,6 +13,8 @@
 namespace gnnv {
 
 static thread_local std::string g_last_error;
+static std::atomic<unsigned long long> g_launches{0};
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 void set_error(const std::string& msg) { g_last_error = msg; }
 const char* get_error() { return g_last_error.c_str(); }
 
@@ -111,6 +114,7 @@ extern "C" {
 
 const char* gnnv_last_error(void) { return get_error(); }
 const char* gnnv_version(void) { return GNNV_VERSION " sm_100a"; }
+uint64_t gnnv_launch_count(void) { return g_launches.load(); }
 int32_t gnnv_row_stride(int32_t d) { return row_stride(d); }
 
 // ------------------------------------------------------------------ graph

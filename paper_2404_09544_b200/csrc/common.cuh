@@ -32,7 +32,14 @@ struct Error {
     }                                                                                          \
   } while (0)
 
-#define GNNV_CHECK_LAUNCH() GNNV_TRY_CUDA(cudaGetLastError())
+// Every kernel launch site ends with GNNV_CHECK_LAUNCH(), which also counts
+// the launch (gnnv_launch_count(), used by bench.py's gpu_launches).
+void count_launch();
+#define GNNV_CHECK_LAUNCH()          \
+  do {                               \
+    ::gnnv::count_launch();          \
+    GNNV_TRY_CUDA(cudaGetLastError()); \
+  } while (0)
 
 #define GNNV_REQUIRE(cond, code, msg)                  \
   do {                                                 \

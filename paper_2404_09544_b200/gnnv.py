@@ -82,6 +82,7 @@ _SIGS = {
     "gnnv_last_error": (C.c_char_p, []),
     "gnnv_version": (C.c_char_p, []),
     "gnnv_row_stride": (I32, [I32]),
+    "gnnv_launch_count": (U64, []),
     "gnnv_graph_load": (I32, [VP, VP, I64, I64, VP, I32, I32, VP, I32, I32, PP]),
     "gnnv_graph_free": (I32, [VP]),
     "gnnv_graph_info": (I32, [VP, C.POINTER(GraphView)]),
@@ -163,6 +164,10 @@ def stream_ptr(s=None) -> Optional[int]:
 
 def version() -> str:
     return load().gnnv_version().decode()
+
+
+def launch_count() -> int:
+    return int(load().gnnv_launch_count())
 
 
 def row_stride(d: int) -> int:

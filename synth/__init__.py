@@ -7,6 +7,7 @@ both `oracle/` and `paper_2404_09544_b200/` may import it, neither imports
 the other.
 """
 from .graphs import (  # noqa: F401
+    BASE_RNG_SEED,
     CONFIGS,
     GraphData,
     chung_lu_graph,

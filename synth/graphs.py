@@ -88,13 +88,45 @@ def csr_from_edges(n: int, src: np.ndarray, dst: np.ndarray):
     src = np.asarray(src, dtype=np.int64)
     dst = np.asarray(dst, dtype=np.int64)
     key = src * np.int64(n) + dst
-    key.sort(kind="stable")
+    key.sort()
     rows = key // n
     cols = (key - rows * n).astype(np.int32)
     counts = np.bincount(rows, minlength=n).astype(np.int64)
     indptr = np.zeros(n + 1, dtype=np.int64)
     np.cumsum(counts, out=indptr[1:])
     return indptr, cols
+
+
+_U_BITS = 38  # resolution of the uniform draws (2^-38, far below the smallest cdf step)
+_IDX_BITS = 25
+_IDX_MASK = (1 << _IDX_BITS) - 1
+
+
+def _inverse_cdf(cdf: np.ndarray, rng: np.random.Generator, count: int) -> np.ndarray:
+    """count draws of an index i with P(i) = cdf[i] - cdf[i-1].
+
+    u = U38 / 2^38 with U38 uniform 38-bit integers; the queries are sorted
+    (packed with their position into one int64 key, a fast integer sort) so
+    that searchsorted walks the cdf sequentially."""
+    assert count <= _IDX_MASK
+    u = rng.integers(0, 1 << _U_BITS, size=count, dtype=np.int64)
+    key = (u << _IDX_BITS) | np.arange(count, dtype=np.int64)
+    key.sort()
+    pos = key & _IDX_MASK
+    us = (key >> _IDX_BITS).astype(np.float64) * (1.0 / (1 << _U_BITS))
+    out = np.empty(count, dtype=np.int64)
+    out[pos] = np.searchsorted(cdf, us, side="right")
+    return out
+
+
+def _sorted_unique(k: np.ndarray) -> np.ndarray:
+    k = np.sort(k)
+    if k.size == 0:
+        return k
+    keep = np.empty(k.size, dtype=bool)
+    keep[0] = True
+    np.not_equal(k[1:], k[:-1], out=keep[1:])
+    return k[keep]
 
 
 def chung_lu_graph(n: int, nnz: int, beta: float, seed: int = GRAPH_SEED):
@@ -111,16 +143,16 @@ def chung_lu_graph(n: int, nnz: int, beta: float, seed: int = GRAPH_SEED):
     keys = np.empty(0, dtype=np.int64)
     while keys.shape[0] < m:
         need = m - keys.shape[0]
-        batch = int(need * 1.05) + 64
-        a = np.searchsorted(cdf, rng.random(batch), side="right")
-        b = np.searchsorted(cdf, rng.random(batch), side="right")
+        batch = min(int(need * 1.05) + 64, _IDX_MASK)
+        a = _inverse_cdf(cdf, rng, batch)
+        b = _inverse_cdf(cdf, rng, batch)
         np.minimum(a, n - 1, out=a)
         np.minimum(b, n - 1, out=b)
-        lo = np.minimum(a, b).astype(np.int64)
-        hi = np.maximum(a, b).astype(np.int64)
+        lo = np.minimum(a, b)
+        hi = np.maximum(a, b)
         ok = lo != hi
         k = lo[ok] * np.int64(n) + hi[ok]
-        keys = np.unique(np.concatenate([keys, k]))
+        keys = _sorted_unique(np.concatenate([keys, k]))
     if keys.shape[0] > m:
         keep = rng.choice(keys.shape[0], m, replace=False)
         keys = keys[np.sort(keep)]
