@@ -305,3 +305,52 @@ def test_step_device_seeds_and_errors(mini):
         tr.step(seeds, 129, 129, 9, 0.0)
     l3, _ = tr.step(seeds, 128, 128, 9, 0.0)
     assert l3 == l1
+
+
+@pytest.mark.parametrize("prec", [0, 1])
+@pytest.mark.parametrize("d_in,d_out,kind", [(1433, 256, 0), (256, 256, 0), (256, 47, 0), (602, 41, 0),
+                                             (128, 40, 1), (100, 256, 0), (7, 13, 0), (256, 172, 1)])
+def test_layer_shapes(mini, prec, d_in, d_out, kind):
+    """GEMM shape sweep (all config widths, ragged K/N, both precisions) on a
+    real sampled block; layer 2 of the mini blocks (so dX is exercised)."""
+    gd, g = mini
+    seeds = epoch_seeds(gd.n, 5)[:257]
+    blocks, hb = gpu_sample(g, seeds, [7, 6], 21, max_seeds=512)
+    layer, L = 2, 2
+    ob = _oracle_block(hb, L - layer)
+    rng = np.random.default_rng(d_in * 7 + d_out)
+    s_in = row_stride(d_in)
+    Hsrc = np.zeros((ob.n_src, s_in), np.float32)
+    Hsrc[:, :d_in] = rng.standard_normal((ob.n_src, d_in)).astype(np.float32)
+    rows = (2 if kind == 0 else 1) * d_in
+    W = (rng.standard_normal((rows, d_out)) / np.sqrt(rows)).astype(np.float32)
+    b = rng.standard_normal(d_out).astype(np.float32)
+    kname = "sage" if kind == 0 else "gcn"
+    ld = gnnv.layer_desc(d_in, d_out, s_in, kind, 0, 1, prec)
+    so = row_stride(d_out)
+    dH, dW_, db_ = dev_f32(Hsrc), dev_f32(W), dev_f32(b)
+    Hdst = torch.full((ob.n_dst, so), float("nan"), device="cuda")
+    A = torch.full((ob.n_dst, s_in), float("nan"), device="cuda")
+    gnnv.layer_fwd(blocks, layer, ld, dH, dW_, db_, Hdst, A)
+    torch.cuda.synchronize()
+    rtol = RTOL32 if prec == 0 else RTOL16
+    Ho, Ao = layer_fwd(ob, Hsrc[:, :d_in], W, b, True, kname)
+    Hm, _ = layer_fwd(ob, Hsrc[:, :d_in], W, b, True, kname, absval=True)
+    Hg, Ag = Hdst.cpu().numpy(), A.cpu().numpy()
+    assert_close_cond(Hg[:, :d_out], Ho, Hm, rtol, "H")
+    assert (Hg[:, d_out:] == 0).all()
+    G = np.zeros((ob.n_dst, so), np.float32)
+    G[:, :d_out] = rng.standard_normal((ob.n_dst, d_out)).astype(np.float32)
+    Gsrc = torch.full((ob.n_src, s_in), float("nan"), device="cuda")
+    dW = torch.full((rows, d_out), float("nan"), device="cuda")
+    db = torch.full((d_out,), float("nan"), device="cuda")
+    gnnv.layer_bwd(blocks, layer, ld, dev_f32(G), Hdst, dH, A, dW_, Gsrc, dW, db)
+    torch.cuda.synchronize()
+    rW, rb, rX = layer_bwd(ob, Hsrc[:, :d_in], Ag[:, :d_in], Hg[:, :d_out], W, G[:, :d_out], True, True, kname)
+    mW, mb, mX = layer_bwd(ob, np.abs(Hsrc[:, :d_in]), np.abs(Ag[:, :d_in]), Hg[:, :d_out], np.abs(W),
+                           np.abs(G[:, :d_out]), True, True, kname)
+    assert_close_cond(dW.cpu().numpy(), rW, mW, rtol, "dW")
+    assert_close_cond(db.cpu().numpy(), rb, mb, rtol, "db")
+    gx = Gsrc.cpu().numpy()
+    assert_close_cond(gx[:, :d_in], rX, mX, rtol, "dHsrc")
+    assert (gx[:, d_in:] == 0).all()
