@@ -44,7 +44,7 @@ def parse():
     p.add_argument("--warmup", type=int, default=10)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--config", default="products")
-    p.add_argument("--prec", default="fp32", choices=["fp32", "bf16"])
+    p.add_argument("--prec", default="tf32", choices=["fp32", "bf16", "tf32"])
     p.add_argument("--kind", default="sage", choices=["sage", "gcn"])
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-baseline-seeds", type=int, default=0, help="seeds in the oracle sample (0 = one batch)")
@@ -230,15 +230,25 @@ def algorithmic(seg: str, sizes, cfg, dims, stride, prec, peaks):
         return "hbm", by, "GB/s", peaks["hbm"]
     if name == "relu_mask":
         return "hbm", 3 * n[h] * ((d_out + 3) & ~3) * 4, "GB/s", peaks["hbm"]
-    if name in ("gemm_fwd", "gemm_dx"):
+    ld_in, ld_out = (d_in + 3) & ~3, (d_out + 3) & ~3
+    if name == "gemm_fwd":
         fl = 2.0 * n[h] * K * d_out
+        by = n[h] * K * 4 + n[h] * ld_out * 4
+    elif name == "gemm_dx":
+        fl = 2.0 * n[h] * K * d_out
+        by = n[h] * d_out * 4 + n[h] * 2 * ld_in * 4
     elif name == "gemm_dw":
         fl = 2.0 * n[h] * (K + 1) * d_out
+        by = n[h] * K * 4 + n[h] * d_out * 4
     else:
         return None
-    if prec == "bf16":
-        return "tensor", fl, "TFLOP/s", peaks["bf16_sust"]
-    return "alu", fl, "TFLOP/s", FP32_SIMT_TFLOPS
+    if prec == "fp32":
+        return "alu", fl, "TFLOP/s", FP32_SIMT_TFLOPS
+    # tensor-core modes: the binding roof is the larger of the two times
+    tpeak = peaks["bf16_sust"] * (0.5 if prec == "tf32" else 1.0)  # tf32 = 1/2 bf16 rate (guide)
+    if by / (peaks["hbm"] * 1e9) >= fl / (tpeak * 1e12):
+        return "hbm", by, "GB/s", peaks["hbm"]
+    return "tensor", fl, "TFLOP/s", tpeak
 
 
 def main():
@@ -274,7 +284,7 @@ def main():
     cache = gnnv.Cache(g, cfg["ratio"])
     dims = [gd.d] + [cfg["hidden"]] * (len(cfg["fanouts"]) - 1) + [gd.C]
     kind = gnnv.KIND_SAGE if args.kind == "sage" else gnnv.KIND_GCN
-    prec = gnnv.PREC_BF16 if args.prec == "bf16" else gnnv.PREC_FP32
+    prec = {"fp32": gnnv.PREC_FP32, "bf16": gnnv.PREC_BF16, "tf32": gnnv.PREC_TF32}[args.prec]
     w = init_weights(dims, kind=args.kind)
     B = cfg["batch"]
     tr = gnnv.Trainer(g, cache, dims, cfg["fanouts"], B, w, kind=kind, prec=prec, comm=comm)
@@ -411,7 +421,7 @@ def main():
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f32" if args.prec == "fp32" else "f32+bf16gemm", "data": "synthetic",
+            "vs_baseline": None, "dtype": {"fp32": "f32", "bf16": "f32+bf16gemm", "tf32": "f32+tf32gemm"}[args.prec], "data": "synthetic",
             "config": {"workload": cfg["name"], "n_nodes": gd.n, "nnz": gd.nnz, "d": gd.d, "classes": gd.C,
                        "fanouts": cfg["fanouts"], "batch_per_rank": B, "global_batch": world * B,
                        "cache_ratio": cfg["ratio"], "placement": "replica", "kind": args.kind,

@@ -82,10 +82,14 @@ typedef enum { GNNV_PLACE_REPLICA = 0, GNNV_PLACE_SHARDED = 1, GNNV_PLACE_SHARDE
 typedef enum { GNNV_KIND_SAGE = 0, GNNV_KIND_GCN = 1 } gnnv_kind;
 typedef enum { GNNV_AGGR_MEAN = 0, GNNV_AGGR_SUM = 1 } gnnv_aggr;
 typedef enum { GNNV_ACT_NONE = 0, GNNV_ACT_RELU = 1 } gnnv_act;
-/* Precision of the dense transform (reading Q18): FP32 = SIMT FFMA;
- * BF16 = operands rounded RNE to bf16, fp32 accumulation on tcgen05 tensor
- * cores.  Aggregation (SpMM) is fp32 in both modes. */
-typedef enum { GNNV_PREC_FP32 = 0, GNNV_PREC_BF16 = 1 } gnnv_prec;
+/* Precision of the dense transform (reading Q18): FP32 = SIMT FFMA (parity
+ * mode); BF16 = operands rounded RNE to bf16 by the producer warps, fp32
+ * accumulation on tcgen05; TF32 = fp32 operands fed by TMA straight to
+ * tcgen05 kind::tf32 (10-bit mantissa, fp32 accumulation) -- the
+ * throughput mode, since these GEMMs are HBM-bound on fp32 activations.
+ * Aggregation (SpMM) is fp32 in every mode.  Tensor-core modes support
+ * d_out <= 252 (fwd) / 256 (dW). */
+typedef enum { GNNV_PREC_FP32 = 0, GNNV_PREC_BF16 = 1, GNNV_PREC_TF32 = 2 } gnnv_prec;
 
 /* ------------------------------------------------------------------ misc */
 const char* gnnv_last_error(void);

@@ -240,17 +240,27 @@ bool gemm_fwd_tc(const GemmFwdArgs& a, cudaStream_t s);
 bool gemm_dx_tc(const GemmDxArgs& a, cudaStream_t s);
 bool gemm_dw_tc(const GemmDwArgs& a, cudaStream_t s);
 
+bool gemm_fwd_tma(const GemmFwdArgs& a, cudaStream_t s);
+bool gemm_dx_tma(const GemmDxArgs& a, cudaStream_t s);
+bool gemm_dw_tma(const GemmDwArgs& a, cudaStream_t s);
+
+// Precision dispatch.  A tensor-core path that does not handle a shape is an
+// error, never a silent fall back to another precision.
 void gemm_fwd(const GemmFwdArgs& a, int prec, cudaStream_t s) {
-  if (prec == GNNV_PREC_BF16 && gemm_fwd_tc(a, s)) return;
-  gemm_fwd_simt(a, s);
+  if (prec == GNNV_PREC_FP32) return gemm_fwd_simt(a, s);
+  const bool ok = prec == GNNV_PREC_TF32 ? gemm_fwd_tma(a, s) : gemm_fwd_tc(a, s);
+  GNNV_REQUIRE(ok, GNNV_ERR_UNSUPPORTED, "tensor-core fwd GEMM: d_out > 252 is not supported");
 }
 void gemm_dx(const GemmDxArgs& a, int prec, cudaStream_t s) {
-  if (prec == GNNV_PREC_BF16 && gemm_dx_tc(a, s)) return;
-  gemm_dx_simt(a, s);
+  if (prec == GNNV_PREC_FP32) return gemm_dx_simt(a, s);
+  const bool ok = prec == GNNV_PREC_TF32 ? gemm_dx_tma(a, s) : gemm_dx_tc(a, s);
+  GNNV_REQUIRE(ok, GNNV_ERR_UNSUPPORTED, "tensor-core dX GEMM: unsupported shape");
 }
+// For TF32 this computes dW only; db comes from k_mask_colsum (layers.cu).
 void gemm_dw(const GemmDwArgs& a, int prec, cudaStream_t s) {
-  if (prec == GNNV_PREC_BF16 && gemm_dw_tc(a, s)) return;
-  gemm_dw_simt(a, s);
+  if (prec == GNNV_PREC_FP32) return gemm_dw_simt(a, s);
+  const bool ok = prec == GNNV_PREC_TF32 ? gemm_dw_tma(a, s) : gemm_dw_tc(a, s);
+  GNNV_REQUIRE(ok, GNNV_ERR_UNSUPPORTED, "tensor-core dW GEMM: d_out > 256 is not supported");
 }
 
 }  // namespace gnnv

@@ -1,0 +1,618 @@
+// Dense transform of the GNN layer on tcgen05 with TMA-fed fp32 operands
+// (kind::tf32, fp32 accumulation in TMEM) -- the GNNV_PREC_TF32 path.
+//
+// Paper: Eq.1 Combine; Algorithm 1 lines 6 and 8.
+//
+// Why tf32 + TMA: at hidden 256 the layer GEMMs have low arithmetic
+// intensity against fp32 activations (e.g. products layer 1: 50 GFLOP on
+// 0.9 GB), so they are HBM-bound on B200 even at tf32 rates (~1.1 PF dense).
+// Feeding the fp32 activations to the tensor cores as tf32 removes every
+// conversion pass: TMA writes the tiles straight into the UMMA canonical
+// 128B-swizzled layout and the MMA consumes them in place.
+//
+//   fwd : Y = act([X1 | X2] W + b)   A = activations, K-major (TMA box 128 x 32)
+//                                     B = W^T, K-major (prep image [Npad x K'])
+//   dX  : [Y1 | Y2] = G W^T           A = G, K-major; B = W rows, K-major image
+//   dW  : dW = [X1 | X2]^T G'         both operands MN-major (TMA box 32 x 32:
+//                                     32 graph rows x 32 features), reduction over
+//                                     graph rows split across CTAs; db = colsum(G')
+//                                     is a separate deterministic kernel
+//
+// Warp roles (192 threads): warp 0 = TMA producer (one elected thread),
+// warp 1 = TMEM owner + MMA issuer (one elected thread), warps 2-5 = epilogue
+// (tcgen05.ld lanes 32*(warp%4) .. +31).  fwd/dX are persistent over output
+// tiles with two TMEM accumulators (epilogue of tile t overlaps the mainloop
+// of tile t+1); dW owns one (i-tile group, row split) per CTA.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include "common.cuh"
+
+namespace gnnv {
+namespace tma {
+
+constexpr int BM = 128;     // MMA M
+constexpr int BKB = 128;    // bytes of K per stage row (32 fp32 = one 128B swizzle atom row)
+constexpr int BK = 32;      // fp32 elements of K per stage
+constexpr int NTHREADS = 192;
+constexpr int FWD_STAGES = 4;
+constexpr int DW_STAGES = 3;
+constexpr int DW_MT = 2;    // 128-row i-tiles per dW CTA
+constexpr int MODE_FWD = 0, MODE_DX = 1, MODE_DW = 2;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t c) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(c) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_tx(uint64_t* b, uint32_t tx) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(tx) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+  asm volatile(
+      "{\n.reg .pred p;\nW_%=:\nmbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n@!p bra W_%=;\n}\n" ::"r"(
+          smem_u32(b)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tc_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          smem_u32(dst)),
+      "l"(map), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void tma_prefetch(const CUtensorMap* map) {
+  asm volatile("prefetch.tensormap [%0];" ::"l"(map) : "memory");
+}
+
+// SW128 descriptors (layout type 2, sm100 version 1).
+//  K-major : rows of 128B (32 tf32 of K), 8-row atoms 1024B apart (SBO);
+//            the K step inside the atom moves the start address by 32B.
+//  MN-major: 128B rows hold 32 consecutive M (or N) for one k; 8 k-rows form
+//            a 1024B atom (SBO); 32-wide M/N blocks are LBO apart.
+__device__ __forceinline__ uint64_t desc_sw128(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFFu) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFFu) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)2 << 61;
+  return d;
+}
+// kind::tf32 instruction descriptor: D=f32, A=B=tf32, M=128, N, majors.
+__device__ __forceinline__ uint32_t idesc_tf32(uint32_t n, bool a_mn, bool b_mn) {
+  return (1u << 4) | (2u << 7) | (2u << 10) | ((a_mn ? 1u : 0u) << 15) | ((b_mn ? 1u : 0u) << 16) | ((n >> 3) << 17) |
+         ((uint32_t)(BM >> 4) << 24);
+}
+__device__ __forceinline__ void mma_tf32(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\ntcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(
+          d),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+struct Params {
+  CUtensorMap ta1, ta2, tb;
+  int two;      // A has a second source (SAGE [H_dst | A])
+  int nkb1;     // fwd: K blocks served by X1 (ceil(K1/32)); dw: 32-col blocks of X1
+  int nkb;      // fwd/dx: K blocks in total
+  int BN;       // N per tile (fwd/dx: mult of 16; dw: mult of 32)
+  int n_ntiles; // dx
+  const int32_t* dM;
+  // fwd epilogue
+  float* Y;
+  int ldy, N;
+  const float* bias;
+  int relu;
+  // dx epilogue
+  float *Y1, *Y2;
+  int ld1, ld2;
+  // dw
+  float* partial;
+  int splits, rows_p, ablocks;  // ablocks: valid 32-wide i blocks (X1 then X2)
+};
+
+template <int MODE>
+__global__ void __launch_bounds__(NTHREADS, 1) k_tma_gemm(const __grid_constant__ Params p) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+  constexpr int S = MODE == MODE_DW ? DW_STAGES : FWD_STAGES;
+  constexpr int MT = MODE == MODE_DW ? DW_MT : 1;
+  const int BN = p.BN;
+  // per-stage bytes
+  const int a_bytes = MODE == MODE_DW ? MT * 4 * (BK * BKB) : BM * BKB;  // dw: MT x 4 boxes of 32 rows
+  const int b_bytes = MODE == MODE_DW ? (BN / 32) * (BK * BKB) : BN * BKB;
+  const int stage_bytes = a_bytes + b_bytes;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + (size_t)S * stage_bytes);
+  uint64_t* full = bars;
+  uint64_t* empty = bars + S;
+  uint64_t* fixb = bars + 2 * S;      // dw: tail rows zeroed
+  uint64_t* tfull = bars + 3 * S;     // 2 accumulators
+  uint64_t* tempty = bars + 3 * S + 2;
+  uint32_t* s_tmem = reinterpret_cast<uint32_t*>(bars + 3 * S + 4);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int M = *p.dM;
+
+  // work decomposition
+  int ntiles = 0, tiles_m = 0, kb0 = 0, kb1 = 0;
+  if (MODE == MODE_DW) {
+    const int nkbm = (M + BK - 1) / BK;
+    const int per = (nkbm + p.splits - 1) / p.splits;
+    kb0 = min(nkbm, (int)blockIdx.x * per);
+    kb1 = min(nkbm, kb0 + per);
+  } else {
+    tiles_m = (M + BM - 1) / BM;
+    ntiles = tiles_m * (MODE == MODE_DX ? p.n_ntiles : 1);
+    if ((int)blockIdx.x >= ntiles) return;  // block-uniform
+  }
+  const uint32_t acc_cols = (uint32_t)(MT * BN);
+  uint32_t ncols = 32;
+  const uint32_t need = MODE == MODE_DW ? acc_cols : 2 * acc_cols;
+  while (ncols < need) ncols <<= 1;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+      mbar_init(&fixb[s], 128);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 128);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&p.ta1);
+    if (p.two) tma_prefetch(&p.ta2);
+    tma_prefetch(&p.tb);
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(s_tmem)),
+                 "r"(ncols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_before();
+  __syncthreads();
+  tc_after();
+  const uint32_t tmem = *s_tmem;
+
+  if (MODE != MODE_DW) {
+    // ======================= persistent fwd / dX =======================
+    if (warp == 0) {
+      if (lane == 0) {
+        int it = 0;
+        for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+          const int mt = MODE == MODE_DX ? tile / p.n_ntiles : tile;
+          const int nt = MODE == MODE_DX ? tile % p.n_ntiles : 0;
+          for (int kb = 0; kb < p.nkb; ++kb, ++it) {
+            const int s = it % S;
+            if (it >= S) mbar_wait(&empty[s], ((it / S) & 1) ^ 1);
+            uint8_t* sa = smem + (size_t)s * stage_bytes;
+            uint8_t* sb = sa + a_bytes;
+            mbar_arrive_tx(&full[s], (uint32_t)stage_bytes);
+            if (MODE == MODE_FWD && kb >= p.nkb1) tma_load_2d(sa, &p.ta2, (kb - p.nkb1) * BK, mt * BM, &full[s]);
+            else tma_load_2d(sa, &p.ta1, kb * BK, mt * BM, &full[s]);
+            tma_load_2d(sb, &p.tb, kb * BK, nt * BN, &full[s]);
+          }
+        }
+      }
+    } else if (warp == 1) {
+      if (lane == 0) {
+        const uint32_t idesc = idesc_tf32((uint32_t)BN, false, false);
+        int it = 0, lt = 0;
+        for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++lt) {
+          const int acc = lt & 1;
+          if (lt >= 2) mbar_wait(&tempty[acc], ((lt >> 1) & 1) ^ 1);
+          tc_after();
+          for (int kb = 0; kb < p.nkb; ++kb, ++it) {
+            const int s = it % S;
+            mbar_wait(&full[s], (it / S) & 1);
+            tc_after();
+            const uint32_t a0 = smem_u32(smem + (size_t)s * stage_bytes);
+            const uint32_t b0 = a0 + a_bytes;
+#pragma unroll
+            for (int k = 0; k < BK / 8; ++k) {
+              mma_tf32(tmem + (uint32_t)(acc * BN), desc_sw128(a0 + k * 32, 16, 1024), desc_sw128(b0 + k * 32, 16, 1024),
+                       idesc, (kb > 0 || k > 0) ? 1u : 0u);
+            }
+            mma_commit(&empty[s]);
+          }
+          mma_commit(&tfull[acc]);
+        }
+      }
+      __syncwarp();
+    } else {
+      const int q = warp & 3;  // TMEM lane quarter of this warp
+      const int row = q * 32 + lane;
+      int lt = 0;
+      for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++lt) {
+        const int acc = lt & 1;
+        const int mt = MODE == MODE_DX ? tile / p.n_ntiles : tile;
+        const int nt = MODE == MODE_DX ? tile % p.n_ntiles : 0;
+        mbar_wait(&tfull[acc], (lt >> 1) & 1);
+        tc_after();
+        const int64_t m = (int64_t)mt * BM + row;
+        for (int c = 0; c < BN; c += 16) {
+          float v[16];
+          tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN + c), v);
+          if (m < M) {
+            if (MODE == MODE_FWD) {
+#pragma unroll
+              for (int j = 0; j < 16; j += 4) {
+                const int n = c + j;
+                if (n < p.ldy) {
+                  float o[4];
+#pragma unroll
+                  for (int e = 0; e < 4; ++e) {
+                    const int nn = n + e;
+                    float x = 0.f;
+                    if (nn < p.N) {
+                      x = v[j + e] + __ldg(p.bias + nn);
+                      if (p.relu) x = fmaxf(x, 0.f);
+                    }
+                    o[e] = x;
+                  }
+                  *reinterpret_cast<float4*>(p.Y + m * p.ldy + n) = make_float4(o[0], o[1], o[2], o[3]);
+                }
+              }
+            } else {
+#pragma unroll
+              for (int j = 0; j < 16; j += 4) {
+                const int col = nt * BN + c + j;
+                const float4 o = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+                if (col < p.ld1) *reinterpret_cast<float4*>(p.Y1 + m * p.ld1 + col) = o;
+                else if (p.Y2 && col - p.ld1 < p.ld2) *reinterpret_cast<float4*>(p.Y2 + m * p.ld2 + (col - p.ld1)) = o;
+              }
+            }
+          }
+        }
+        tc_before();
+        mbar_arrive(&tempty[acc]);
+      }
+    }
+  } else {
+    // =============================== dW ===============================
+    const int nkb = kb1 - kb0;
+    const int ig = blockIdx.y;  // i-tile group
+    if (warp == 0) {
+      if (lane == 0) {
+        for (int i = 0; i < nkb; ++i) {
+          const int s = i % S;
+          if (i >= S) mbar_wait(&empty[s], ((i / S) & 1) ^ 1);
+          uint8_t* sa = smem + (size_t)s * stage_bytes;
+          uint8_t* sb = sa + a_bytes;
+          const int row = (kb0 + i) * BK;
+          uint32_t bytes = (uint32_t)b_bytes;
+          for (int mt = 0; mt < MT; ++mt)
+            for (int cb = 0; cb < 4; ++cb)
+              if ((ig * MT + mt) * 4 + cb < p.ablocks) bytes += BK * BKB;
+          mbar_arrive_tx(&full[s], bytes);
+          for (int mt = 0; mt < MT; ++mt) {
+            for (int cb = 0; cb < 4; ++cb) {
+              const int blk = (ig * MT + mt) * 4 + cb;  // 32-wide i block
+              if (blk >= p.ablocks) continue;
+              uint8_t* dst = sa + (mt * 4 + cb) * (BK * BKB);
+              if (blk < p.nkb1) tma_load_2d(dst, &p.ta1, blk * 32, row, &full[s]);
+              else tma_load_2d(dst, &p.ta2, (blk - p.nkb1) * 32, row, &full[s]);
+            }
+          }
+          for (int cb = 0; cb < BN / 32; ++cb) tma_load_2d(sb + cb * (BK * BKB), &p.tb, cb * 32, row, &full[s]);
+        }
+      }
+    } else if (warp == 1) {
+      if (lane == 0) {
+        const uint32_t idesc = idesc_tf32((uint32_t)BN, true, true);
+        for (int i = 0; i < nkb; ++i) {
+          const int s = i % S;
+          mbar_wait(&fixb[s], (i / S) & 1);
+          tc_after();
+          const uint32_t a0 = smem_u32(smem + (size_t)s * stage_bytes);
+          const uint32_t b0 = a0 + a_bytes;
+#pragma unroll
+          for (int mt = 0; mt < MT; ++mt) {
+#pragma unroll
+            for (int k = 0; k < BK / 8; ++k) {
+              // k-th group of 8 graph rows = one 1024B atom row block
+              mma_tf32(tmem + (uint32_t)(mt * BN), desc_sw128(a0 + mt * 4 * (BK * BKB) + k * 1024, BK * BKB, 1024),
+                       desc_sw128(b0 + k * 1024, BK * BKB, 1024), idesc, (i > 0 || k > 0) ? 1u : 0u);
+            }
+          }
+          mma_commit(&empty[s]);
+        }
+        if (nkb > 0) mma_commit(&tfull[0]);
+        else mbar_arrive(&tfull[0]);
+      }
+      __syncwarp();
+    } else {
+      const int t = threadIdx.x - 64;  // 0..127
+      // A blocks that TMA never writes (i beyond the valid range) must be 0
+      for (int s = 0; s < S; ++s) {
+        uint8_t* sa = smem + (size_t)s * stage_bytes;
+        for (int mt = 0; mt < MT; ++mt)
+          for (int cb = 0; cb < 4; ++cb)
+            if ((ig * MT + mt) * 4 + cb >= p.ablocks) {
+              uint4* z = reinterpret_cast<uint4*>(sa + (mt * 4 + cb) * (BK * BKB));
+              for (int j = t; j < BK * BKB / 16; j += 128) z[j] = make_uint4(0, 0, 0, 0);
+            }
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      // tail: graph rows >= M inside the last block hold stale data -> zero
+      for (int i = 0; i < nkb; ++i) {
+        const int s = i % S;
+        mbar_wait(&full[s], (i / S) & 1);
+        const int row0 = (kb0 + i) * BK;
+        const int valid = M - row0;
+        if (valid < BK) {
+          uint8_t* sa = smem + (size_t)s * stage_bytes;
+          const int nblocks = MT * 4 + BN / 32;
+          const int chunks = (BK - valid) * (BKB / 16);  // 16B chunks per block to clear
+          for (int j = t; j < nblocks * chunks; j += 128) {
+            const int blk = j / chunks, r = j % chunks;
+            uint4* z = reinterpret_cast<uint4*>(sa + blk * (BK * BKB) + valid * BKB) + r;
+            *z = make_uint4(0, 0, 0, 0);
+          }
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        }
+        mbar_arrive(&fixb[s]);
+      }
+      mbar_wait(&tfull[0], 0);
+      tc_after();
+      const int q = warp & 3;
+      const int row = q * 32 + lane;
+      for (int mt = 0; mt < MT; ++mt) {
+        const int irow = (ig * MT + mt) * BM + row;
+        float* dst = p.partial + ((int64_t)blockIdx.x * p.rows_p + irow) * BN;
+        for (int c = 0; c < BN; c += 16) {
+          float v[16];
+          if (nkb > 0) {
+            tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(mt * BN + c), v);
+          } else {
+#pragma unroll
+            for (int j = 0; j < 16; ++j) v[j] = 0.f;
+          }
+#pragma unroll
+          for (int j = 0; j < 16; j += 4)
+            *reinterpret_cast<float4*>(dst + c + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+        }
+      }
+    }
+  }
+  tc_before();
+  __syncthreads();
+  if (warp == 1) {
+    __syncwarp();
+    tc_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(ncols) : "memory");
+  }
+}
+
+// --------------------------------------------------------- prep kernels
+// fwd B image: Bt[n][k'] (Npad x Kp, fp32, K-major), k' = kb*32 + c over
+// [X1 blocks | X2 blocks]: k' < 32*nkb1 -> W row k' (valid < K1), else
+// W row K1 + (k' - 32*nkb1) (valid < K1).
+__global__ void k_bt_fwd(const float* __restrict__ W, int K1, int nkb1, int two, int N, int Npad, int Kp, float* Bt) {
+  const int total = Npad * Kp;
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < total; t += gridDim.x * blockDim.x) {
+    const int n = t / Kp, kp = t - n * Kp;
+    int k = -1;
+    if (kp < 32 * nkb1) {
+      if (kp < K1) k = kp;
+    } else if (two) {
+      const int kk = kp - 32 * nkb1;
+      if (kk < K1) k = K1 + kk;
+    }
+    Bt[t] = (k >= 0 && n < N) ? W[(int64_t)k * N + n] : 0.f;
+  }
+}
+// dX B image: Bd[j][k] (NCpad x Kp): j over [0, ld1) -> W row j (< K1),
+// [ld1, ld1+ld2) -> W row K1 + (j - ld1); k < N.
+__global__ void k_bt_dx(const float* __restrict__ W, int K1, int ld1, int ld2, int two, int N, int NCpad, int Kp,
+                        float* Bd) {
+  const int total = NCpad * Kp;
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < total; t += gridDim.x * blockDim.x) {
+    const int j = t / Kp, k = t - j * Kp;
+    int r = -1;
+    if (j < ld1) {
+      if (j < K1) r = j;
+    } else if (two && j - ld1 < ld2 && j - ld1 < K1) {
+      r = K1 + (j - ld1);
+    }
+    Bd[t] = (r >= 0 && k < N) ? W[(int64_t)r * N + k] : 0.f;
+  }
+}
+// dW: partial[split][i'][n] -> dW[k][n] with i' = k (X1) or 32*nkb1 + (k-K1) (X2)
+__global__ void k_dw_reduce_tma(const float* __restrict__ partial, int splits, int rows_p, int BN, int K1, int nkb1,
+                                int Ktot, int N, float* dW) {
+  const int total = Ktot * N;
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < total; t += gridDim.x * blockDim.x) {
+    const int k = t / N, n = t - k * N;
+    const int ip = k < K1 ? k : 32 * nkb1 + (k - K1);
+    float s = 0.f;
+    for (int z = 0; z < splits; ++z) s += partial[((int64_t)z * rows_p + ip) * BN + n];
+    dW[t] = s;
+  }
+}
+
+// ------------------------------------------------------ host helpers
+static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    GNNV_TRY_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
+    GNNV_REQUIRE(p && q == cudaDriverEntryPointSuccess, GNNV_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+    fn = (PFN_cuTensorMapEncodeTiled_v12000)p;
+  }
+  return fn;
+}
+
+// 2-D fp32 row-major tensor [rows x cols] with row stride ld (floats); box
+// [box_rows x 32 cols], 128B swizzle, out-of-range elements read as zero.
+static CUtensorMap make_map(const float* base, int64_t rows, int64_t cols, int64_t ld, int box_rows) {
+  CUtensorMap m;
+  const cuuint64_t dims[2] = {(cuuint64_t)std::max<int64_t>(cols, 1), (cuuint64_t)std::max<int64_t>(rows, 1)};
+  const cuuint64_t strides[1] = {(cuuint64_t)ld * sizeof(float)};
+  const cuuint32_t box[2] = {32, (cuuint32_t)box_rows};
+  const cuuint32_t estr[2] = {1, 1};
+  CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void*)base, dims, strides, box, estr,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  GNNV_REQUIRE(r == CUDA_SUCCESS, GNNV_ERR_CUDA, "cuTensorMapEncodeTiled failed (alignment/stride)");
+  return m;
+}
+
+struct Arena {
+  void* buf = nullptr;
+  size_t cap = 0;
+  void* get(size_t bytes, cudaStream_t s) {
+    if (bytes > cap) {
+      if (buf) {
+        GNNV_TRY_CUDA(cudaStreamSynchronize(s));
+        dfree(buf);
+      }
+      cap = std::max(bytes, (size_t)4 << 20);
+      buf = dmalloc(cap, "tf32 GEMM workspace");
+    }
+    return buf;
+  }
+};
+static Arena g_img, g_part;
+
+static size_t smem_bytes(int mode, int BN) {
+  const int S = mode == MODE_DW ? DW_STAGES : FWD_STAGES;
+  const int a = mode == MODE_DW ? DW_MT * 4 * BK * BKB : BM * BKB;
+  const int b = mode == MODE_DW ? (BN / 32) * BK * BKB : BN * BKB;
+  return (size_t)S * (a + b) + 8 * (3 * S + 4) + 16 + 1024;
+}
+
+template <int MODE>
+static void launch(const Params& p, dim3 grid, cudaStream_t s) {
+  static bool set = false;
+  if (!set) {
+    GNNV_TRY_CUDA(cudaFuncSetAttribute(k_tma_gemm<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    set = true;
+  }
+  k_tma_gemm<MODE><<<grid, NTHREADS, smem_bytes(MODE, p.BN), s>>>(p);
+  GNNV_CHECK_LAUNCH();
+}
+
+static int rup(int x, int m) { return (x + m - 1) / m * m; }
+
+}  // namespace tma
+
+bool gemm_fwd_tma(const GemmFwdArgs& a, cudaStream_t s) {
+  using namespace tma;
+  const int BN = rup(a.ldy, 16);
+  if (BN > 256) return false;
+  const int nkb1 = (a.K1 + BK - 1) / BK;
+  const int nkb = a.X2 ? 2 * nkb1 : nkb1;
+  const int Kp = nkb * BK;
+  float* Bt = (float*)g_img.get((size_t)BN * Kp * sizeof(float), s);
+  k_bt_fwd<<<std::min(1024, (BN * Kp + 255) / 256), 256, 0, s>>>(a.W, a.K1, nkb1, a.X2 ? 1 : 0, a.N, BN, Kp, Bt);
+  GNNV_CHECK_LAUNCH();
+  Params p{};
+  p.ta1 = make_map(a.X1, a.max_M, a.K1, a.ld1, BM);
+  p.ta2 = a.X2 ? make_map(a.X2, a.max_M, a.K1, a.ld2, BM) : p.ta1;
+  p.tb = make_map(Bt, BN, Kp, Kp, BN);
+  p.two = a.X2 ? 1 : 0;
+  p.nkb1 = nkb1;
+  p.nkb = nkb;
+  p.BN = BN;
+  p.n_ntiles = 1;
+  p.dM = a.d_M;
+  p.Y = a.Y;
+  p.ldy = a.ldy;
+  p.N = a.N;
+  p.bias = a.bias;
+  p.relu = a.relu ? 1 : 0;
+  const int64_t tiles = ceil_div(std::max<int64_t>(a.max_M, 1), BM);
+  launch<MODE_FWD>(p, dim3((unsigned)std::min<int64_t>(tiles, num_sms())), s);
+  return true;
+}
+
+bool gemm_dx_tma(const GemmDxArgs& a, cudaStream_t s) {
+  using namespace tma;
+  const int NC = a.Y2 ? a.ld1 + a.ld2 : a.ld1;
+  const int ntl = (NC + 255) / 256;
+  const int BN = rup((NC + ntl - 1) / ntl, 16);
+  const int nkb = (a.N + BK - 1) / BK;
+  const int Kp = nkb * BK;
+  const int NCpad = ntl * BN;
+  float* Bd = (float*)g_img.get((size_t)NCpad * Kp * sizeof(float), s);
+  k_bt_dx<<<std::min(1024, (NCpad * Kp + 255) / 256), 256, 0, s>>>(a.W, a.K1, a.ld1, a.ld2, a.Y2 ? 1 : 0, a.N, NCpad,
+                                                                    Kp, Bd);
+  GNNV_CHECK_LAUNCH();
+  Params p{};
+  p.ta1 = make_map(a.G, a.max_M, a.N, a.ldg, BM);
+  p.ta2 = p.ta1;
+  p.tb = make_map(Bd, NCpad, Kp, Kp, BN);
+  p.nkb1 = nkb;
+  p.nkb = nkb;
+  p.BN = BN;
+  p.n_ntiles = ntl;
+  p.dM = a.d_M;
+  p.Y1 = a.Y1;
+  p.Y2 = a.Y2;
+  p.ld1 = a.ld1;
+  p.ld2 = a.ld2;
+  const int64_t tiles = ceil_div(std::max<int64_t>(a.max_M, 1), BM) * ntl;
+  launch<MODE_DX>(p, dim3((unsigned)std::min<int64_t>(tiles, num_sms())), s);
+  return true;
+}
+
+// dW only (db comes from the column-sum kernel).
+bool gemm_dw_tma(const GemmDwArgs& a, cudaStream_t s) {
+  using namespace tma;
+  const int BN = rup(a.N, 32);
+  if (BN * DW_MT > 512) return false;
+  const int nkb1 = (a.K1 + 31) / 32;
+  const int ablocks = a.X2 ? 2 * nkb1 : nkb1;
+  const int rows_p = rup(ablocks * 32, BM * DW_MT);
+  const int igroups = rows_p / (BM * DW_MT);
+  const int64_t nkbm = ceil_div(std::max<int64_t>(a.max_M, 1), BK);
+  const int splits = (int)std::max<int64_t>(1, std::min<int64_t>(nkbm, (int64_t)num_sms() / igroups));
+  float* partial = (float*)g_part.get((size_t)splits * rows_p * BN * sizeof(float), s);
+  Params p{};
+  p.ta1 = make_map(a.X1, a.max_M, a.K1, a.ld1, BK);
+  p.ta2 = a.X2 ? make_map(a.X2, a.max_M, a.K1, a.ld2, BK) : p.ta1;
+  p.tb = make_map(a.G, a.max_M, a.N, a.ldg, BK);
+  p.two = a.X2 ? 1 : 0;
+  p.nkb1 = nkb1;
+  p.BN = BN;
+  p.dM = a.d_M;
+  p.partial = partial;
+  p.splits = splits;
+  p.rows_p = rows_p;
+  p.ablocks = ablocks;
+  launch<MODE_DW>(p, dim3((unsigned)splits, (unsigned)igroups), s);
+  const int Ktot = a.X2 ? 2 * a.K1 : a.K1;
+  k_dw_reduce_tma<<<std::min(1024, (Ktot * a.N + 255) / 256), 256, 0, s>>>(partial, splits, rows_p, BN, a.K1, nkb1,
+                                                                          Ktot, a.N, a.dW);
+  GNNV_CHECK_LAUNCH();
+  return true;
+}
+
+}  // namespace gnnv

@@ -28,6 +28,62 @@ void launch_relu_mask(const float* G, const float* H, float* Gp, int32_t ld, int
   GNNV_CHECK_LAUNCH();
 }
 
+// G' = G * 1[H > 0] (if H) written to Gp, plus per-block column sums of G'
+// (db).  Fixed grid, contiguous row ranges, fixed in-block order: the
+// bias gradient is deterministic.
+constexpr int kColBlocks = 296;
+__global__ void __launch_bounds__(256) k_mask_colsum(const float* __restrict__ G, const float* __restrict__ H,
+                                                     float* __restrict__ Gp, int ld, const int32_t* d_M,
+                                                     float* __restrict__ partial) {
+  __shared__ float4 s_acc[256];
+  const int M = *d_M;
+  const int ld4 = ld >> 2;
+  const int groups = max(1, (int)blockDim.x / ld4);
+  const int rg = threadIdx.x / ld4, c4 = threadIdx.x - rg * ld4;
+  const int per = (M + gridDim.x - 1) / gridDim.x;
+  const int r0 = min(M, (int)blockIdx.x * per), r1 = min(M, r0 + per);
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (rg < groups && c4 < ld4) {
+    const float4* G4 = reinterpret_cast<const float4*>(G);
+    const float4* H4 = reinterpret_cast<const float4*>(H);
+    float4* P4 = reinterpret_cast<float4*>(Gp);
+    for (int r = r0 + rg; r < r1; r += groups) {
+      const int64_t i = (int64_t)r * ld4 + c4;
+      float4 g = __ldg(G4 + i);
+      if (H) {
+        const float4 h = __ldg(H4 + i);
+        g = make_float4(h.x > 0.f ? g.x : 0.f, h.y > 0.f ? g.y : 0.f, h.z > 0.f ? g.z : 0.f, h.w > 0.f ? g.w : 0.f);
+        P4[i] = g;
+      }
+      acc.x += g.x;
+      acc.y += g.y;
+      acc.z += g.z;
+      acc.w += g.w;
+    }
+  }
+  s_acc[threadIdx.x] = acc;
+  __syncthreads();
+  if (rg == 0 && c4 < ld4) {
+    float4 t = s_acc[c4];
+    for (int q = 1; q < groups; ++q) {
+      const float4 u = s_acc[q * ld4 + c4];
+      t.x += u.x;
+      t.y += u.y;
+      t.z += u.z;
+      t.w += u.w;
+    }
+    reinterpret_cast<float4*>(partial)[(int64_t)blockIdx.x * ld4 + c4] = t;
+  }
+}
+
+__global__ void k_colsum_reduce(const float* __restrict__ partial, int blocks, int ld, int N, float* db) {
+  for (int n = blockIdx.x * blockDim.x + threadIdx.x; n < N; n += gridDim.x * blockDim.x) {
+    float s = 0.f;
+    for (int b = 0; b < blocks; ++b) s += partial[(int64_t)b * ld + n];
+    db[n] = s;
+  }
+}
+
 constexpr int kLossBlocks = 64;
 
 // One warp per seed row; fixed grid => fixed summation order (deterministic).
@@ -110,7 +166,8 @@ static void check_layer(const gnnv_blocks* b, int32_t layer, const gnnv_layer_de
   GNNV_REQUIRE(ld->kind == GNNV_KIND_SAGE || ld->kind == GNNV_KIND_GCN, GNNV_ERR_PARAM, "layer: kind");
   GNNV_REQUIRE(ld->aggr == GNNV_AGGR_MEAN || ld->aggr == GNNV_AGGR_SUM, GNNV_ERR_PARAM, "layer: aggr");
   GNNV_REQUIRE(ld->act == GNNV_ACT_NONE || ld->act == GNNV_ACT_RELU, GNNV_ERR_PARAM, "layer: act");
-  GNNV_REQUIRE(ld->prec == GNNV_PREC_FP32 || ld->prec == GNNV_PREC_BF16, GNNV_ERR_PARAM, "layer: prec");
+  GNNV_REQUIRE(ld->prec == GNNV_PREC_FP32 || ld->prec == GNNV_PREC_BF16 || ld->prec == GNNV_PREC_TF32, GNNV_ERR_PARAM,
+               "layer: prec");
 }
 
 void layer_fwd_impl(gnnv_blocks* b, int32_t layer, const gnnv_layer_desc* ld, const float* Hsrc, const float* W,
@@ -160,15 +217,26 @@ void layer_bwd_impl(gnnv_blocks* b, int32_t layer, const gnnv_layer_desc* ld, co
   int32_t splits = 1;
   const size_t part_f = gemm_dw_partial_floats(rows, ld->d_out, &splits, max_dst);
   const bool relu = ld->act == GNNV_ACT_RELU;
+  const bool tf32 = ld->prec == GNNV_PREC_TF32;
   const size_t gp_f = relu ? (size_t)max_dst * ldo : 0;
   const size_t da_f = Gsrc ? (size_t)max_dst * lda : 0;
+  const size_t cs_f = tf32 ? (size_t)kColBlocks * ldo : 0;
   auto al = [](size_t f) { return (f + 63) & ~(size_t)63; };
-  float* scratch = (float*)b->ensure_scratch((al(part_f) + al(gp_f) + al(da_f)) * sizeof(float), s);
+  float* scratch = (float*)b->ensure_scratch((al(part_f) + al(gp_f) + al(da_f) + al(cs_f)) * sizeof(float), s);
   float* partial = scratch;
   float* Gp = scratch + al(part_f);
   float* dA = Gp + al(gp_f);
+  float* colpart = dA + al(da_f);
   const float* G = Gdst;
-  if (relu) {
+  if (tf32) {
+    // masked gradient + deterministic column sums (db) in one pass
+    if (tl) tl->mark(s, "relu_mask" + sfx);
+    k_mask_colsum<<<kColBlocks, 256, 0, s>>>(Gdst, relu ? Hdst : nullptr, Gp, ldo, d_ndst, colpart);
+    GNNV_CHECK_LAUNCH();
+    k_colsum_reduce<<<1, 256, 0, s>>>(colpart, kColBlocks, ldo, ld->d_out, db);
+    GNNV_CHECK_LAUNCH();
+    if (relu) G = Gp;
+  } else if (relu) {
     if (tl) tl->mark(s, "relu_mask" + sfx);
     launch_relu_mask(Gdst, Hdst, Gp, ldo, ld->d_out, d_ndst, max_dst, s);
     G = Gp;

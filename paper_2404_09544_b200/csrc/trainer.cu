@@ -94,7 +94,7 @@ gnnv_status gnnv_trainer_create(gnnv_graph* g, gnnv_cache* c, const gnnv_model_d
     for (int i = 0; i <= md->L; ++i) GNNV_REQUIRE(md->dims[i] >= 1, GNNV_ERR_PARAM, "trainer_create: dims >= 1");
     GNNV_REQUIRE(md->kind == GNNV_KIND_SAGE || md->kind == GNNV_KIND_GCN, GNNV_ERR_PARAM, "trainer_create: kind");
     GNNV_REQUIRE(md->aggr == GNNV_AGGR_MEAN || md->aggr == GNNV_AGGR_SUM, GNNV_ERR_PARAM, "trainer_create: aggr");
-    GNNV_REQUIRE(md->prec == GNNV_PREC_FP32 || md->prec == GNNV_PREC_BF16, GNNV_ERR_PARAM, "trainer_create: prec");
+    GNNV_REQUIRE(md->prec >= GNNV_PREC_FP32 && md->prec <= GNNV_PREC_TF32, GNNV_ERR_PARAM, "trainer_create: prec");
     GNNV_TRY_CUDA(cudaSetDevice(g->device));
     gnnv_trainer* t = new gnnv_trainer();
     t->g = g;

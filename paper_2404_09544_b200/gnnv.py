@@ -24,7 +24,7 @@ PLACE_REPLICA, PLACE_SHARDED, PLACE_SHARDED_LOCAL = range(3)
 KIND_SAGE, KIND_GCN = 0, 1
 AGGR_MEAN, AGGR_SUM = 0, 1
 ACT_NONE, ACT_RELU = 0, 1
-PREC_FP32, PREC_BF16 = 0, 1
+PREC_FP32, PREC_BF16, PREC_TF32 = 0, 1, 2
 STATUS_NAMES = {0: "OK", 1: "ERR_PARAM", 2: "ERR_STATE", 3: "ERR_OOM", 4: "ERR_CUDA", 5: "ERR_COMM",
                 6: "ERR_UNSUPPORTED"}
 

@@ -37,6 +37,17 @@ def read_i32(p, n):
     return out.cpu().numpy()
 
 
+def read_f32(p, rows, stride):
+    """Copy a [rows x stride] fp32 matrix from a raw device pointer."""
+    out = torch.empty((int(rows), int(stride)), dtype=torch.float32, device="cuda")
+    if rows:
+        torch.cuda.synchronize()
+        res = _cudart().cudaMemcpy(ctypes.c_void_p(out.data_ptr()), ctypes.c_void_p(int(p)),
+                                   ctypes.c_size_t(int(rows) * int(stride) * 4), 3)
+        assert int(res) == 0, res
+    return out.cpu().numpy()
+
+
 _rt = None
 
 
