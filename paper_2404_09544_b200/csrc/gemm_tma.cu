@@ -382,6 +382,24 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_tma_gemm(const __grid_constant_
       tc_after();
       const int q = warp & 3;
       const int row = q * 32 + lane;
+#ifdef GNNV_DEBUG_DW
+      if (blockIdx.x == 0 && blockIdx.y == 0 && t == 0) {
+        const float* sa = reinterpret_cast<const float*>(smem);
+        const float* sb = reinterpret_cast<const float*>(smem + a_bytes);
+        printf("DW dbg M=%d kb0=%d kb1=%d nkb=%d BN=%d ablocks=%d nkb1=%d splits=%d\n", M, kb0, kb1, nkb, BN,
+               p.ablocks, p.nkb1, p.splits);
+        printf("A[0..7] %f %f %f %f %f %f %f %f\n", sa[0], sa[1], sa[2], sa[3], sa[4], sa[5], sa[6], sa[7]);
+        printf("B[0..7] %f %f %f %f %f %f %f %f\n", sb[0], sb[1], sb[2], sb[3], sb[4], sb[5], sb[6], sb[7]);
+      }
+      if (blockIdx.x == 0 && blockIdx.y == 0 && (t == 0 || t == 32)) {
+        float v[16];
+        tmem_ld16(tmem + ((uint32_t)(q * 32) << 16), v);
+        printf("TMEM row %d: %f %f %f %f\n", row, v[0], v[1], v[2], v[3]);
+      } else if (blockIdx.x == 0 && blockIdx.y == 0) {
+        float v[16];
+        tmem_ld16(tmem + ((uint32_t)(q * 32) << 16), v);
+      }
+#endif
       for (int mt = 0; mt < MT; ++mt) {
         const int irow = (ig * MT + mt) * BM + row;
         float* dst = p.partial + ((int64_t)blockIdx.x * p.rows_p + irow) * BN;
