@@ -13,10 +13,15 @@
 //   fwd : Y = act([X1 | X2] W + b)   A = activations, K-major (TMA box 128 x 32)
 //                                     B = W^T, K-major (prep image [Npad x K'])
 //   dX  : [Y1 | Y2] = G W^T           A = G, K-major; B = W rows, K-major image
-//   dW  : dW = [X1 | X2]^T G'         both operands MN-major (TMA box 32 x 32:
-//                                     32 graph rows x 32 features), reduction over
-//                                     graph rows split across CTAs; db = colsum(G')
-//                                     is a separate deterministic kernel
+//   dW  : dW = [X1 | X2]^T G'         operands arrive MN-major (TMA boxes of 32
+//                                     graph rows x 32 features); kind::tf32 only
+//                                     takes K-major operands (tools/umma_probe.cu:
+//                                     an MN-major tf32 operand yields zeros), so
+//                                     the 4 epilogue warps transpose each staged
+//                                     box into a K-major SW128 tile (and zero the
+//                                     stale tail rows) before the MMA.  Reduction
+//                                     over graph rows is split across CTAs;
+//                                     db = colsum(G') is a separate kernel
 //
 // Warp roles (192 threads): warp 0 = TMA producer (one elected thread),
 // warp 1 = TMEM owner + MMA issuer (one elected thread), warps 2-5 = epilogue
@@ -36,7 +41,7 @@ constexpr int BKB = 128;    // bytes of K per stage row (32 fp32 = one 128B swiz
 constexpr int BK = 32;      // fp32 elements of K per stage
 constexpr int NTHREADS = 192;
 constexpr int FWD_STAGES = 4;
-constexpr int DW_STAGES = 3;
+constexpr int DW_STAGES = 2;
 constexpr int DW_MT = 2;    // 128-row i-tiles per dW CTA
 constexpr int MODE_FWD = 0, MODE_DX = 1, MODE_DW = 2;
 
@@ -144,10 +149,13 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_tma_gemm(const __grid_constant_
   const int a_bytes = MODE == MODE_DW ? MT * 4 * (BK * BKB) : BM * BKB;  // dw: MT x 4 boxes of 32 rows
   const int b_bytes = MODE == MODE_DW ? (BN / 32) * (BK * BKB) : BN * BKB;
   const int stage_bytes = a_bytes + b_bytes;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + (size_t)S * stage_bytes);
+  // dW only: K-major tf32 tile the transposers build from the staged boxes
+  const int k_bytes = MODE == MODE_DW ? MT * BM * BKB + BN * BKB : 0;
+  uint8_t* kbuf = smem + (size_t)S * stage_bytes;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(kbuf + k_bytes);
   uint64_t* full = bars;
   uint64_t* empty = bars + S;
-  uint64_t* fixb = bars + 2 * S;      // dw: tail rows zeroed
+  uint64_t* fixb = bars + 2 * S;      // dw: [0] K-major tile ready, [1] K-major tile free
   uint64_t* tfull = bars + 3 * S;     // 2 accumulators
   uint64_t* tempty = bars + 3 * S + 2;
   uint32_t* s_tmem = reinterpret_cast<uint32_t*>(bars + 3 * S + 4);
@@ -174,9 +182,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_tma_gemm(const __grid_constant_
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
-      mbar_init(&fixb[s], 128);
+      mbar_init(&empty[s], MODE == MODE_DW ? 128 : 1);  // dW: released by the transposers
     }
+    mbar_init(&fixb[0], 128);
+    mbar_init(&fixb[1], 1);
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
       mbar_init(&tempty[a], 128);
@@ -323,83 +332,70 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_tma_gemm(const __grid_constant_
         }
       }
     } else if (warp == 1) {
+      // kind::tf32 accepts K-major operands only (an MN-major tf32 operand
+      // yields zeros on sm_100a -- tools/umma_probe.cu), so the MMA reads the
+      // K-major tile the transposer warps build from each staged stage.
       if (lane == 0) {
-        const uint32_t idesc = idesc_tf32((uint32_t)BN, true, true);
+        const uint32_t idesc = idesc_tf32((uint32_t)BN, false, false);
+        const uint32_t ka = smem_u32(kbuf), kb = ka + MT * BM * BKB;
         for (int i = 0; i < nkb; ++i) {
-          const int s = i % S;
-          mbar_wait(&fixb[s], (i / S) & 1);
+          mbar_wait(&fixb[0], i & 1);
           tc_after();
-          const uint32_t a0 = smem_u32(smem + (size_t)s * stage_bytes);
-          const uint32_t b0 = a0 + a_bytes;
 #pragma unroll
           for (int mt = 0; mt < MT; ++mt) {
 #pragma unroll
             for (int k = 0; k < BK / 8; ++k) {
-              // k-th group of 8 graph rows = one 1024B atom row block
-              mma_tf32(tmem + (uint32_t)(mt * BN), desc_sw128(a0 + mt * 4 * (BK * BKB) + k * 1024, BK * BKB, 1024),
-                       desc_sw128(b0 + k * 1024, BK * BKB, 1024), idesc, (i > 0 || k > 0) ? 1u : 0u);
+              mma_tf32(tmem + (uint32_t)(mt * BN), desc_sw128(ka + mt * BM * BKB + k * 32, 16, 1024),
+                       desc_sw128(kb + k * 32, 16, 1024), idesc, (i > 0 || k > 0) ? 1u : 0u);
             }
           }
-          mma_commit(&empty[s]);
+          mma_commit(&fixb[1]);
         }
         if (nkb > 0) mma_commit(&tfull[0]);
         else mbar_arrive(&tfull[0]);
       }
       __syncwarp();
     } else {
-      const int t = threadIdx.x - 64;  // 0..127
-      // A blocks that TMA never writes (i beyond the valid range) must be 0
-      for (int s = 0; s < S; ++s) {
-        uint8_t* sa = smem + (size_t)s * stage_bytes;
-        for (int mt = 0; mt < MT; ++mt)
-          for (int cb = 0; cb < 4; ++cb)
-            if ((ig * MT + mt) * 4 + cb >= p.ablocks) {
-              uint4* z = reinterpret_cast<uint4*>(sa + (mt * 4 + cb) * (BK * BKB));
-              for (int j = t; j < BK * BKB / 16; j += 128) z[j] = make_uint4(0, 0, 0, 0);
-            }
-      }
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      // tail: graph rows >= M inside the last block hold stale data -> zero
+      // ---- transposers: staged MN boxes [32 graph rows x 32 cols] -> K-major
+      // rows (one row per feature / output column, 32 graph rows of K).
+      // Lane l reads column l of the box row by row (conflict-free 128B row
+      // reads) and writes its K-major row as 8 swizzled 16B chunks.  Graph
+      // rows >= M (stale tail) and features beyond the operand are zero.
+      const int tw = warp - 2;  // 0..3
+      const int nboxes = MT * 4 + BN / 32;
       for (int i = 0; i < nkb; ++i) {
         const int s = i % S;
         mbar_wait(&full[s], (i / S) & 1);
-        const int row0 = (kb0 + i) * BK;
-        const int valid = M - row0;
-        if (valid < BK) {
-          uint8_t* sa = smem + (size_t)s * stage_bytes;
-          const int nblocks = MT * 4 + BN / 32;
-          const int chunks = (BK - valid) * (BKB / 16);  // 16B chunks per block to clear
-          for (int j = t; j < nblocks * chunks; j += 128) {
-            const int blk = j / chunks, r = j % chunks;
-            uint4* z = reinterpret_cast<uint4*>(sa + blk * (BK * BKB) + valid * BKB) + r;
-            *z = make_uint4(0, 0, 0, 0);
+        if (i > 0) mbar_wait(&fixb[1], (i - 1) & 1);  // MMA done with the K-major tile
+        const int valid = min(BK, M - (kb0 + i) * BK);
+        const uint8_t* st = smem + (size_t)s * stage_bytes;
+        for (int bx = tw; bx < nboxes; bx += 4) {
+          const bool is_a = bx < MT * 4;
+          const bool loaded = !is_a || ((ig * MT + bx / 4) * 4 + bx % 4 < p.ablocks);
+          const uint8_t* src =
+              st + (is_a ? (size_t)bx * (BK * BKB) : (size_t)a_bytes + (size_t)(bx - MT * 4) * (BK * BKB));
+          float x[32];
+#pragma unroll
+          for (int r = 0; r < 32; ++r) {
+            const uint32_t off = r * BKB + ((((lane >> 2) ^ (r & 7))) << 4) + (lane & 3) * 4;
+            x[r] = (loaded && r < valid) ? *reinterpret_cast<const float*>(src + off) : 0.f;
           }
-          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          // destination K-major row
+          const int krow = is_a ? (bx / 4) * BM + (bx % 4) * 32 + lane : (bx - MT * 4) * 32 + lane;
+          uint8_t* drow = kbuf + (is_a ? 0 : MT * BM * BKB) + (size_t)krow * BKB;
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            *reinterpret_cast<float4*>(drow + ((j ^ (krow & 7)) << 4)) =
+                make_float4(x[4 * j], x[4 * j + 1], x[4 * j + 2], x[4 * j + 3]);
         }
-        mbar_arrive(&fixb[s]);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_arrive(&empty[s]);    // staging stage s may be refilled
+        mbar_arrive(&fixb[0]);     // K-major tile ready for the MMA
       }
       mbar_wait(&tfull[0], 0);
       tc_after();
       const int q = warp & 3;
       const int row = q * 32 + lane;
-#ifdef GNNV_DEBUG_DW
-      if (blockIdx.x == 0 && blockIdx.y == 0 && t == 0) {
-        const float* sa = reinterpret_cast<const float*>(smem);
-        const float* sb = reinterpret_cast<const float*>(smem + a_bytes);
-        printf("DW dbg M=%d kb0=%d kb1=%d nkb=%d BN=%d ablocks=%d nkb1=%d splits=%d\n", M, kb0, kb1, nkb, BN,
-               p.ablocks, p.nkb1, p.splits);
-        printf("A[0..7] %f %f %f %f %f %f %f %f\n", sa[0], sa[1], sa[2], sa[3], sa[4], sa[5], sa[6], sa[7]);
-        printf("B[0..7] %f %f %f %f %f %f %f %f\n", sb[0], sb[1], sb[2], sb[3], sb[4], sb[5], sb[6], sb[7]);
-      }
-      if (blockIdx.x == 0 && blockIdx.y == 0 && (t == 0 || t == 32)) {
-        float v[16];
-        tmem_ld16(tmem + ((uint32_t)(q * 32) << 16), v);
-        printf("TMEM row %d: %f %f %f %f\n", row, v[0], v[1], v[2], v[3]);
-      } else if (blockIdx.x == 0 && blockIdx.y == 0) {
-        float v[16];
-        tmem_ld16(tmem + ((uint32_t)(q * 32) << 16), v);
-      }
-#endif
       for (int mt = 0; mt < MT; ++mt) {
         const int irow = (ig * MT + mt) * BM + row;
         float* dst = p.partial + ((int64_t)blockIdx.x * p.rows_p + irow) * BN;
@@ -523,7 +519,8 @@ static size_t smem_bytes(int mode, int BN) {
   const int S = mode == MODE_DW ? DW_STAGES : FWD_STAGES;
   const int a = mode == MODE_DW ? DW_MT * 4 * BK * BKB : BM * BKB;
   const int b = mode == MODE_DW ? (BN / 32) * BK * BKB : BN * BKB;
-  return (size_t)S * (a + b) + 8 * (3 * S + 4) + 16 + 1024;
+  const int k = mode == MODE_DW ? DW_MT * BM * BKB + BN * BKB : 0;
+  return (size_t)S * (a + b) + k + 8 * (3 * S + 4) + 16 + 1024;
 }
 
 template <int MODE>
