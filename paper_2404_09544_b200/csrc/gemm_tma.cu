@@ -39,10 +39,13 @@ namespace tma {
 constexpr int BM = 128;     // MMA M
 constexpr int BKB = 128;    // bytes of K per stage row (32 fp32 = one 128B swizzle atom row)
 constexpr int BK = 32;      // fp32 elements of K per stage
-constexpr int NTHREADS = 192;
+constexpr int NE = 8;       // epilogue / transposer warps
+constexpr int NTHREADS = 64 + 32 * NE;
 constexpr int FWD_STAGES = 4;
-constexpr int DW_STAGES = 2;
+constexpr int DW_STAGES = 3;
 constexpr int DW_MT = 2;    // 128-row i-tiles per dW CTA
+constexpr int DW_KR = 16;   // graph rows per dW k-block
+constexpr int DW_BOX = DW_KR * BKB;  // one staged [16 x 32] fp32 box
 constexpr int MODE_FWD = 0, MODE_DX = 1, MODE_DW = 2;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -76,18 +79,16 @@ __device__ __forceinline__ void tma_prefetch(const CUtensorMap* map) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(map) : "memory");
 }
 
-// SW128 descriptors (layout type 2, sm100 version 1).
-//  K-major : rows of 128B (32 tf32 of K), 8-row atoms 1024B apart (SBO);
-//            the K step inside the atom moves the start address by 32B.
-//  MN-major: 128B rows hold 32 consecutive M (or N) for one k; 8 k-rows form
-//            a 1024B atom (SBO); 32-wide M/N blocks are LBO apart.
-__device__ __forceinline__ uint64_t desc_sw128(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+// K-major swizzled descriptors (sm100 version 1).  SW128: rows of 128B
+// (32 tf32 of K), 8-row atoms 1024B apart (SBO); SW64: rows of 64B, 8-row
+// atoms of 512B.  The K step of 8 tf32 moves the start address by 32B.
+__device__ __forceinline__ uint64_t desc_sw(uint32_t saddr, uint32_t sbo, uint32_t layout) {
   uint64_t d = 0;
   d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
-  d |= (uint64_t)((lbo >> 4) & 0x3FFFu) << 16;
+  d |= (uint64_t)1 << 16;  // LBO (unused for swizzled K-major)
   d |= (uint64_t)((sbo >> 4) & 0x3FFFu) << 32;
   d |= (uint64_t)1 << 46;
-  d |= (uint64_t)2 << 61;
+  d |= (uint64_t)layout << 61;  // 2 = SWIZZLE_128B, 4 = SWIZZLE_64B
   return d;
 }
 // kind::tf32 instruction descriptor: D=f32, A=B=tf32, M=128, N, majors.
@@ -108,13 +109,30 @@ __device__ __forceinline__ void mma_commit(uint64_t* bar) {
 __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
   uint32_t r[16];
   asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n"
+      "tcgen05.wait::ld.sync.aligned;"
       : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
         "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
-      : "r"(taddr));
-  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      : "r"(taddr)
+      : "memory");
 #pragma unroll
   for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
+  uint32_t r[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,"
+      "%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"
+      "tcgen05.wait::ld.sync.aligned;"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]),
+        "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+        "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr)
+      : "memory");
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
 }
 
 struct Params {
@@ -141,54 +159,54 @@ struct Params {
 template <int MODE>
 __global__ void __launch_bounds__(NTHREADS, 1) k_tma_gemm(const __grid_constant__ Params p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
+  __shared__ float s_bias[256];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
   constexpr int S = MODE == MODE_DW ? DW_STAGES : FWD_STAGES;
   constexpr int MT = MODE == MODE_DW ? DW_MT : 1;
   const int BN = p.BN;
-  // per-stage bytes
-  const int a_bytes = MODE == MODE_DW ? MT * 4 * (BK * BKB) : BM * BKB;  // dw: MT x 4 boxes of 32 rows
-  const int b_bytes = MODE == MODE_DW ? (BN / 32) * (BK * BKB) : BN * BKB;
+  // fwd/dX stage: A [128 rows x 128B] + B [BN rows x 128B] (K-major SW128).
+  // dW stage: MN boxes of [16 graph rows x 32 cols] (2 KB): MT*4 of A, BN/32 of G.
+  const int a_bytes = MODE == MODE_DW ? MT * 4 * DW_BOX : BM * BKB;
+  const int b_bytes = MODE == MODE_DW ? (BN / 32) * DW_BOX : BN * BKB;
   const int stage_bytes = a_bytes + b_bytes;
-  // dW only: K-major tf32 tile the transposers build from the staged boxes
-  const int k_bytes = MODE == MODE_DW ? MT * BM * BKB + BN * BKB : 0;
+  // dW: two K-major SW64 tiles (64B rows = 16 tf32 of K) built by the transposers
+  const int kt_bytes = MODE == MODE_DW ? (MT * BM + BN) * 64 : 0;
   uint8_t* kbuf = smem + (size_t)S * stage_bytes;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(kbuf + k_bytes);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(kbuf + 2 * kt_bytes);
   uint64_t* full = bars;
   uint64_t* empty = bars + S;
-  uint64_t* fixb = bars + 2 * S;      // dw: [0] K-major tile ready, [1] K-major tile free
-  uint64_t* tfull = bars + 3 * S;     // 2 accumulators
-  uint64_t* tempty = bars + 3 * S + 2;
-  uint32_t* s_tmem = reinterpret_cast<uint32_t*>(bars + 3 * S + 4);
+  uint64_t* kready = bars + 2 * S;  // dW: K-major tile b ready
+  uint64_t* kfree = kready + 2;     // dW: MMA finished reading tile b
+  uint64_t* tfull = kfree + 2;      // fwd/dX: two TMEM accumulators
+  uint64_t* tempty = tfull + 2;
+  uint32_t* s_tmem = reinterpret_cast<uint32_t*>(tempty + 2);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int M = *p.dM;
 
-  // work decomposition
-  int ntiles = 0, tiles_m = 0, kb0 = 0, kb1 = 0;
+  int ntiles = 0, kb0 = 0, kb1 = 0;
   if (MODE == MODE_DW) {
-    const int nkbm = (M + BK - 1) / BK;
+    const int nkbm = (M + DW_KR - 1) / DW_KR;
     const int per = (nkbm + p.splits - 1) / p.splits;
     kb0 = min(nkbm, (int)blockIdx.x * per);
     kb1 = min(nkbm, kb0 + per);
   } else {
-    tiles_m = (M + BM - 1) / BM;
-    ntiles = tiles_m * (MODE == MODE_DX ? p.n_ntiles : 1);
+    ntiles = ((M + BM - 1) / BM) * (MODE == MODE_DX ? p.n_ntiles : 1);
     if ((int)blockIdx.x >= ntiles) return;  // block-uniform
   }
-  const uint32_t acc_cols = (uint32_t)(MT * BN);
   uint32_t ncols = 32;
-  const uint32_t need = MODE == MODE_DW ? acc_cols : 2 * acc_cols;
+  const uint32_t need = (uint32_t)(MT * BN) * (MODE == MODE_DW ? 1u : 2u);
   while (ncols < need) ncols <<= 1;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], MODE == MODE_DW ? 128 : 1);  // dW: released by the transposers
+      mbar_init(&empty[s], MODE == MODE_DW ? NE * 32 : 1);  // dW: released by the transposers
     }
-    mbar_init(&fixb[0], 128);
-    mbar_init(&fixb[1], 1);
-    for (int a = 0; a < 2; ++a) {
-      mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 128);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&kready[b], NE * 32);
+      mbar_init(&kfree[b], 1);
+      mbar_init(&tfull[b], 1);
+      mbar_init(&tempty[b], NE * 32);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -202,6 +220,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_tma_gemm(const __grid_constant_
                  "r"(ncols)
                  : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  if (MODE == MODE_FWD && warp >= 2) {
+    for (int i = threadIdx.x - 64; i < BN; i += NE * 32) s_bias[i] = i < p.N ? __ldg(p.bias + i) : 0.f;
   }
   tc_before();
   __syncthreads();
@@ -244,7 +265,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_tma_gemm(const __grid_constant_
             const uint32_t b0 = a0 + a_bytes;
 #pragma unroll
             for (int k = 0; k < BK / 8; ++k) {
-              mma_tf32(tmem + (uint32_t)(acc * BN), desc_sw128(a0 + k * 32, 16, 1024), desc_sw128(b0 + k * 32, 16, 1024),
+              mma_tf32(tmem + (uint32_t)(acc * BN), desc_sw(a0 + k * 32, 1024, 2), desc_sw(b0 + k * 32, 1024, 2),
                        idesc, (kb > 0 || k > 0) ? 1u : 0u);
             }
             mma_commit(&empty[s]);
@@ -254,7 +275,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_tma_gemm(const __grid_constant_
       }
       __syncwarp();
     } else {
-      const int q = warp & 3;  // TMEM lane quarter of this warp
+      // 8 epilogue warps: lane quarter q = warp & 3 (tcgen05.ld restriction),
+      // 32-column chunks interleaved between the two warps of a quarter.
+      const int q = warp & 3;
+      const int half = (warp - 2) >> 2;
       const int row = q * 32 + lane;
       int lt = 0;
       for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++lt) {
@@ -264,32 +288,33 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_tma_gemm(const __grid_constant_
         mbar_wait(&tfull[acc], (lt >> 1) & 1);
         tc_after();
         const int64_t m = (int64_t)mt * BM + row;
-        for (int c = 0; c < BN; c += 16) {
-          float v[16];
-          tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN + c), v);
+        const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN);
+        for (int c = half * 32; c < BN; c += 64) {
+          float v[32];
+          const int w = min(32, BN - c);
+          if (w == 32) tmem_ld32(tbase + c, v);
+          else tmem_ld16(tbase + c, v);
           if (m < M) {
             if (MODE == MODE_FWD) {
+              float* yrow = p.Y + m * p.ldy;
 #pragma unroll
-              for (int j = 0; j < 16; j += 4) {
+              for (int j = 0; j < 32; j += 4) {
                 const int n = c + j;
-                if (n < p.ldy) {
+                if (j < w && n < p.ldy) {
                   float o[4];
 #pragma unroll
                   for (int e = 0; e < 4; ++e) {
-                    const int nn = n + e;
-                    float x = 0.f;
-                    if (nn < p.N) {
-                      x = v[j + e] + __ldg(p.bias + nn);
-                      if (p.relu) x = fmaxf(x, 0.f);
-                    }
-                    o[e] = x;
+                    float x = v[j + e] + s_bias[n + e];
+                    if (p.relu) x = fmaxf(x, 0.f);
+                    o[e] = (n + e < p.N) ? x : 0.f;
                   }
-                  *reinterpret_cast<float4*>(p.Y + m * p.ldy + n) = make_float4(o[0], o[1], o[2], o[3]);
+                  *reinterpret_cast<float4*>(yrow + n) = make_float4(o[0], o[1], o[2], o[3]);
                 }
               }
             } else {
 #pragma unroll
-              for (int j = 0; j < 16; j += 4) {
+              for (int j = 0; j < 32; j += 4) {
+                if (j >= w) break;
                 const int col = nt * BN + c + j;
                 const float4 o = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
                 if (col < p.ld1) *reinterpret_cast<float4*>(p.Y1 + m * p.ld1 + col) = o;
@@ -306,109 +331,105 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_tma_gemm(const __grid_constant_
     // =============================== dW ===============================
     const int nkb = kb1 - kb0;
     const int ig = blockIdx.y;  // i-tile group
+    const int nboxes = MT * 4 + BN / 32;
     if (warp == 0) {
       if (lane == 0) {
         for (int i = 0; i < nkb; ++i) {
           const int s = i % S;
           if (i >= S) mbar_wait(&empty[s], ((i / S) & 1) ^ 1);
           uint8_t* sa = smem + (size_t)s * stage_bytes;
-          uint8_t* sb = sa + a_bytes;
-          const int row = (kb0 + i) * BK;
+          const int row = (kb0 + i) * DW_KR;
           uint32_t bytes = (uint32_t)b_bytes;
-          for (int mt = 0; mt < MT; ++mt)
-            for (int cb = 0; cb < 4; ++cb)
-              if ((ig * MT + mt) * 4 + cb < p.ablocks) bytes += BK * BKB;
+          for (int bx = 0; bx < MT * 4; ++bx)
+            if (ig * MT * 4 + bx < p.ablocks) bytes += DW_BOX;
           mbar_arrive_tx(&full[s], bytes);
-          for (int mt = 0; mt < MT; ++mt) {
-            for (int cb = 0; cb < 4; ++cb) {
-              const int blk = (ig * MT + mt) * 4 + cb;  // 32-wide i block
-              if (blk >= p.ablocks) continue;
-              uint8_t* dst = sa + (mt * 4 + cb) * (BK * BKB);
-              if (blk < p.nkb1) tma_load_2d(dst, &p.ta1, blk * 32, row, &full[s]);
-              else tma_load_2d(dst, &p.ta2, (blk - p.nkb1) * 32, row, &full[s]);
-            }
+          for (int bx = 0; bx < MT * 4; ++bx) {
+            const int blk = ig * MT * 4 + bx;  // 32-wide i block
+            if (blk >= p.ablocks) continue;
+            if (blk < p.nkb1) tma_load_2d(sa + bx * DW_BOX, &p.ta1, blk * 32, row, &full[s]);
+            else tma_load_2d(sa + bx * DW_BOX, &p.ta2, (blk - p.nkb1) * 32, row, &full[s]);
           }
-          for (int cb = 0; cb < BN / 32; ++cb) tma_load_2d(sb + cb * (BK * BKB), &p.tb, cb * 32, row, &full[s]);
+          for (int cb = 0; cb < BN / 32; ++cb) tma_load_2d(sa + a_bytes + cb * DW_BOX, &p.tb, cb * 32, row, &full[s]);
         }
       }
     } else if (warp == 1) {
       // kind::tf32 accepts K-major operands only (an MN-major tf32 operand
       // yields zeros on sm_100a -- tools/umma_probe.cu), so the MMA reads the
-      // K-major tile the transposer warps build from each staged stage.
+      // K-major tiles the transposer warps build from each staged block.
       if (lane == 0) {
         const uint32_t idesc = idesc_tf32((uint32_t)BN, false, false);
-        const uint32_t ka = smem_u32(kbuf), kb = ka + MT * BM * BKB;
         for (int i = 0; i < nkb; ++i) {
-          mbar_wait(&fixb[0], i & 1);
+          const int b = i & 1;
+          mbar_wait(&kready[b], (i >> 1) & 1);
           tc_after();
+          const uint32_t ka = smem_u32(kbuf + (size_t)b * kt_bytes), kbb = ka + MT * BM * 64;
 #pragma unroll
           for (int mt = 0; mt < MT; ++mt) {
 #pragma unroll
-            for (int k = 0; k < BK / 8; ++k) {
-              mma_tf32(tmem + (uint32_t)(mt * BN), desc_sw128(ka + mt * BM * BKB + k * 32, 16, 1024),
-                       desc_sw128(kb + k * 32, 16, 1024), idesc, (i > 0 || k > 0) ? 1u : 0u);
+            for (int k = 0; k < DW_KR / 8; ++k) {
+              mma_tf32(tmem + (uint32_t)(mt * BN), desc_sw(ka + mt * BM * 64 + k * 32, 512, 4),
+                       desc_sw(kbb + k * 32, 512, 4), idesc, (i > 0 || k > 0) ? 1u : 0u);
             }
           }
-          mma_commit(&fixb[1]);
+          mma_commit(&kfree[b]);
         }
         if (nkb > 0) mma_commit(&tfull[0]);
         else mbar_arrive(&tfull[0]);
       }
       __syncwarp();
     } else {
-      // ---- transposers: staged MN boxes [32 graph rows x 32 cols] -> K-major
-      // rows (one row per feature / output column, 32 graph rows of K).
+      // ---- transposers: staged MN box [16 graph rows x 32 cols] -> 32 K-major
+      // SW64 rows (one per feature / output column, 16 graph rows of K).
       // Lane l reads column l of the box row by row (conflict-free 128B row
-      // reads) and writes its K-major row as 8 swizzled 16B chunks.  Graph
-      // rows >= M (stale tail) and features beyond the operand are zero.
-      const int tw = warp - 2;  // 0..3
-      const int nboxes = MT * 4 + BN / 32;
+      // reads) and writes its 64B row as 4 swizzled 16B chunks.  Graph rows
+      // >= M (stale tail) and features beyond the operand are written as 0.
+      const int tw = warp - 2;  // 0..NE-1
       for (int i = 0; i < nkb; ++i) {
-        const int s = i % S;
+        const int s = i % S, b = i & 1;
         mbar_wait(&full[s], (i / S) & 1);
-        if (i > 0) mbar_wait(&fixb[1], (i - 1) & 1);  // MMA done with the K-major tile
-        const int valid = min(BK, M - (kb0 + i) * BK);
+        if (i >= 2) mbar_wait(&kfree[b], ((i >> 1) - 1) & 1);  // MMA done with tile b
+        const int valid = min(DW_KR, M - (kb0 + i) * DW_KR);
         const uint8_t* st = smem + (size_t)s * stage_bytes;
-        for (int bx = tw; bx < nboxes; bx += 4) {
+        uint8_t* kt = kbuf + (size_t)b * kt_bytes;
+        for (int bx = tw; bx < nboxes; bx += NE) {
           const bool is_a = bx < MT * 4;
-          const bool loaded = !is_a || ((ig * MT + bx / 4) * 4 + bx % 4 < p.ablocks);
-          const uint8_t* src =
-              st + (is_a ? (size_t)bx * (BK * BKB) : (size_t)a_bytes + (size_t)(bx - MT * 4) * (BK * BKB));
-          float x[32];
+          const bool loaded = !is_a || (ig * MT * 4 + bx < p.ablocks);
+          const uint8_t* src = st + (is_a ? (size_t)bx * DW_BOX : (size_t)a_bytes + (size_t)(bx - MT * 4) * DW_BOX);
+          float x[DW_KR];
 #pragma unroll
-          for (int r = 0; r < 32; ++r) {
-            const uint32_t off = r * BKB + ((((lane >> 2) ^ (r & 7))) << 4) + (lane & 3) * 4;
+          for (int r = 0; r < DW_KR; ++r) {
+            const uint32_t off = r * BKB + (((lane >> 2) ^ (r & 7)) << 4) + (lane & 3) * 4;
             x[r] = (loaded && r < valid) ? *reinterpret_cast<const float*>(src + off) : 0.f;
           }
-          // destination K-major row
-          const int krow = is_a ? (bx / 4) * BM + (bx % 4) * 32 + lane : (bx - MT * 4) * 32 + lane;
-          uint8_t* drow = kbuf + (is_a ? 0 : MT * BM * BKB) + (size_t)krow * BKB;
+          const int krow = is_a ? bx * 32 + lane : (bx - MT * 4) * 32 + lane;
+          uint8_t* drow = kt + (is_a ? 0 : MT * BM * 64) + (size_t)krow * 64;
 #pragma unroll
-          for (int j = 0; j < 8; ++j)
-            *reinterpret_cast<float4*>(drow + ((j ^ (krow & 7)) << 4)) =
+          for (int j = 0; j < 4; ++j)
+            *reinterpret_cast<float4*>(drow + ((j ^ ((krow >> 1) & 3)) << 4)) =
                 make_float4(x[4 * j], x[4 * j + 1], x[4 * j + 2], x[4 * j + 3]);
         }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        mbar_arrive(&empty[s]);    // staging stage s may be refilled
-        mbar_arrive(&fixb[0]);     // K-major tile ready for the MMA
+        mbar_arrive(&empty[s]);   // staging stage s may be refilled
+        mbar_arrive(&kready[b]);  // K-major tile b ready for the MMA
       }
       mbar_wait(&tfull[0], 0);
       tc_after();
       const int q = warp & 3;
+      const int half = (warp - 2) >> 2;
       const int row = q * 32 + lane;
       for (int mt = 0; mt < MT; ++mt) {
         const int irow = (ig * MT + mt) * BM + row;
         float* dst = p.partial + ((int64_t)blockIdx.x * p.rows_p + irow) * BN;
-        for (int c = 0; c < BN; c += 16) {
-          float v[16];
+        for (int c = half * 32; c < BN; c += 64) {
+          float v[32];
           if (nkb > 0) {
-            tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(mt * BN + c), v);
+            tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(mt * BN + c), v);
           } else {
 #pragma unroll
-            for (int j = 0; j < 16; ++j) v[j] = 0.f;
+            for (int j = 0; j < 32; ++j) v[j] = 0.f;
           }
 #pragma unroll
-          for (int j = 0; j < 16; j += 4)
+          for (int j = 0; j < 32; j += 4)
             *reinterpret_cast<float4*>(dst + c + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
         }
       }
@@ -517,10 +538,10 @@ static Arena g_img, g_part;
 
 static size_t smem_bytes(int mode, int BN) {
   const int S = mode == MODE_DW ? DW_STAGES : FWD_STAGES;
-  const int a = mode == MODE_DW ? DW_MT * 4 * BK * BKB : BM * BKB;
-  const int b = mode == MODE_DW ? (BN / 32) * BK * BKB : BN * BKB;
-  const int k = mode == MODE_DW ? DW_MT * BM * BKB + BN * BKB : 0;
-  return (size_t)S * (a + b) + k + 8 * (3 * S + 4) + 16 + 1024;
+  const int a = mode == MODE_DW ? DW_MT * 4 * DW_BOX : BM * BKB;
+  const int b = mode == MODE_DW ? (BN / 32) * DW_BOX : BN * BKB;
+  const int k = mode == MODE_DW ? 2 * (DW_MT * BM + BN) * 64 : 0;
+  return (size_t)S * (a + b) + k + 8 * (2 * S + 8) + 16 + 1024;
 }
 
 template <int MODE>
@@ -607,13 +628,13 @@ bool gemm_dw_tma(const GemmDwArgs& a, cudaStream_t s) {
   const int ablocks = a.X2 ? 2 * nkb1 : nkb1;
   const int rows_p = rup(ablocks * 32, BM * DW_MT);
   const int igroups = rows_p / (BM * DW_MT);
-  const int64_t nkbm = ceil_div(std::max<int64_t>(a.max_M, 1), BK);
+  const int64_t nkbm = ceil_div(std::max<int64_t>(a.max_M, 1), DW_KR);
   const int splits = (int)std::max<int64_t>(1, std::min<int64_t>(nkbm, (int64_t)num_sms() / igroups));
   float* partial = (float*)g_part.get((size_t)splits * rows_p * BN * sizeof(float), s);
   Params p{};
-  p.ta1 = make_map(a.X1, a.max_M, a.K1, a.ld1, BK);
-  p.ta2 = a.X2 ? make_map(a.X2, a.max_M, a.K1, a.ld2, BK) : p.ta1;
-  p.tb = make_map(a.G, a.max_M, a.N, a.ldg, BK);
+  p.ta1 = make_map(a.X1, a.max_M, a.K1, a.ld1, DW_KR);
+  p.ta2 = a.X2 ? make_map(a.X2, a.max_M, a.K1, a.ld2, DW_KR) : p.ta1;
+  p.tb = make_map(a.G, a.max_M, a.N, a.ldg, DW_KR);
   p.two = a.X2 ? 1 : 0;
   p.nkb1 = nkb1;
   p.BN = BN;

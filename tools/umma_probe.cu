@@ -29,6 +29,18 @@ __device__ uint32_t off_kmajor(int mn, int k, int esz) {
   const int chunk = byte >> 4, in = byte & 15;
   return (uint32_t)(mn * 128 + ((chunk ^ (mn & 7)) << 4) + in);
 }
+// K-major SWIZZLE_64B: 64B rows (16 tf32), 8-row atoms of 512B, chunk ^= (row>>1)&3
+__device__ uint32_t off_kmajor64(int mn, int k, int esz) {
+  const int byte = k * esz;
+  const int chunk = byte >> 4, in = byte & 15;
+  return (uint32_t)(mn * 64 + ((chunk ^ ((mn >> 1) & 3)) << 4) + in);
+}
+// K-major SWIZZLE_NONE: core matrices 8 rows x 16B; [kchunk][rowgroup][8][16B]
+__device__ uint32_t off_knone(int mn, int k, int esz, int M) {
+  const int byte = k * esz;
+  const int chunk = byte >> 4, in = byte & 15;
+  return (uint32_t)(chunk * (M * 16) + mn * 16 + in);
+}
 __device__ uint32_t off_mnmajor(int mn, int k, int esz, int mnblk_bytes, int kgrp_bytes) {
   const int per_row = 128 / esz;  // MN elements per 128B row
   const int blk = mn / per_row, r = mn % per_row;
@@ -38,7 +50,7 @@ __device__ uint32_t off_mnmajor(int mn, int k, int esz, int mnblk_bytes, int kgr
   return (uint32_t)(blk * mnblk_bytes + kg * kgrp_bytes + krow * 128 + ((chunk ^ krow) << 4) + in);
 }
 
-__global__ void probe(int kind /*0 tf32, 1 bf16*/, int a_mn, int b_mn, uint32_t lbo_a, uint32_t sbo_a, uint32_t lbo_b,
+__global__ void probe(int kind /*0 tf32, 1 bf16*/, int a_mn, int b_mn, int klay /*0 sw128 1 sw64 2 none*/, uint32_t lbo_a, uint32_t sbo_a, uint32_t lbo_b,
                       uint32_t sbo_b, float* out) {
   extern __shared__ __align__(1024) uint8_t sm[];
   uint8_t* base = (uint8_t*)(((uintptr_t)sm + 1023) & ~(uintptr_t)1023);
@@ -52,13 +64,15 @@ __global__ void probe(int kind /*0 tf32, 1 bf16*/, int a_mn, int b_mn, uint32_t 
   __syncthreads();
   for (int i = threadIdx.x; i < 128 * K; i += blockDim.x) {
     const int m = i / K, k = i % K;
-    const uint32_t o = a_mn ? off_mnmajor(m, k, esz, lbo_a, sbo_a) : off_kmajor(m, k, esz) + (k * esz / 128) * 0;
+    const uint32_t o = a_mn ? off_mnmajor(m, k, esz, lbo_a, sbo_a)
+                            : (klay == 0 ? off_kmajor(m, k, esz) : klay == 1 ? off_kmajor64(m, k, esz) : off_knone(m, k, esz, 128));
     if (kind == 0) *(float*)(sA + o) = Aval(m, k);
     else *(__nv_bfloat16*)(sA + o) = __float2bfloat16(Aval(m, k));
   }
   for (int i = threadIdx.x; i < 32 * K; i += blockDim.x) {
     const int n = i / K, k = i % K;
-    const uint32_t o = b_mn ? off_mnmajor(n, k, esz, lbo_b, sbo_b) : off_kmajor(n, k, esz);
+    const uint32_t o = b_mn ? off_mnmajor(n, k, esz, lbo_b, sbo_b)
+                            : (klay == 0 ? off_kmajor(n, k, esz) : klay == 1 ? off_kmajor64(n, k, esz) : off_knone(n, k, esz, 32));
     if (kind == 0) *(float*)(sB + o) = Bval(n, k);
     else *(__nv_bfloat16*)(sB + o) = __float2bfloat16(Bval(n, k));
   }
@@ -79,8 +93,11 @@ __global__ void probe(int kind /*0 tf32, 1 bf16*/, int a_mn, int b_mn, uint32_t 
     const uint32_t fmt = kind == 0 ? 2u : 1u;
     const uint32_t idesc = (1u << 4) | (fmt << 7) | (fmt << 10) | ((uint32_t)a_mn << 15) | ((uint32_t)b_mn << 16) |
                            ((32u >> 3) << 17) | ((128u >> 4) << 24);
-    const uint64_t ad = desc(su32(sA), a_mn ? lbo_a : 16, a_mn ? sbo_a : 1024, 2);
-    const uint64_t bd = desc(su32(sB), b_mn ? lbo_b : 16, b_mn ? sbo_b : 1024, 2);
+    const uint32_t lay = klay == 0 ? 2u : klay == 1 ? 4u : 0u;
+    const uint64_t ad = a_mn ? desc(su32(sA), lbo_a, sbo_a, 2)
+                             : desc(su32(sA), klay == 2 ? 128 * 16 : 16, klay == 0 ? 1024 : klay == 1 ? 512 : 128, lay);
+    const uint64_t bd = b_mn ? desc(su32(sB), lbo_b, sbo_b, 2)
+                             : desc(su32(sB), klay == 2 ? 32 * 16 : 16, klay == 0 ? 1024 : klay == 1 ? 512 : 128, lay);
     if (kind == 0)
       asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, 0, 0;\ntcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(t),
                    "l"(ad), "l"(bd), "r"(idesc));
@@ -112,22 +129,24 @@ int main() {
   cudaFuncSetAttribute(probe, cudaFuncAttributeMaxDynamicSharedMemorySize, 140 * 1024);
   struct V {
     const char* name;
-    int kind, amn, bmn;
+    int kind, amn, bmn, klay;
     uint32_t la, sa, lb, sb;
   } vs[] = {
-      {"tf32 K/K", 0, 0, 0, 0, 0, 0, 0},
-      {"tf32 MN/MN lbo=mnblk sbo=kgrp", 0, 1, 1, 4096, 1024, 4096, 1024},
-      {"tf32 MN/MN lbo=kgrp sbo=mnblk", 0, 1, 1, 1024, 4096, 1024, 4096},
-      {"tf32 MN/K  lbo=mnblk sbo=kgrp", 0, 1, 0, 4096, 1024, 0, 0},
-      {"tf32 K/MN  lbo=mnblk sbo=kgrp", 0, 0, 1, 0, 0, 4096, 1024},
-      {"bf16 K/K", 1, 0, 0, 0, 0, 0, 0},
-      {"bf16 MN/MN lbo=mnblk sbo=kgrp", 1, 1, 1, 8192, 1024, 8192, 1024},
-      {"bf16 MN/MN lbo=kgrp sbo=mnblk", 1, 1, 1, 1024, 8192, 1024, 8192},
+      {"tf32 K/K sw128", 0, 0, 0, 0, 0, 0, 0, 0},
+      {"tf32 K/K sw64", 0, 0, 0, 1, 0, 0, 0, 0},
+      {"tf32 K/K none", 0, 0, 0, 2, 0, 0, 0, 0},
+      {"tf32 MN/MN lbo=mnblk sbo=kgrp", 0, 1, 1, 0, 4096, 1024, 4096, 1024},
+      {"tf32 MN/MN lbo=kgrp sbo=mnblk", 0, 1, 1, 0, 1024, 4096, 1024, 4096},
+      {"tf32 MN/K  lbo=mnblk sbo=kgrp", 0, 1, 0, 0, 4096, 1024, 0, 0},
+      {"tf32 K/MN  lbo=mnblk sbo=kgrp", 0, 0, 1, 0, 0, 0, 4096, 1024},
+      {"bf16 K/K", 1, 0, 0, 0, 0, 0, 0, 0},
+      {"bf16 MN/MN lbo=mnblk sbo=kgrp", 1, 1, 1, 0, 8192, 1024, 8192, 1024},
+      {"bf16 MN/MN lbo=kgrp sbo=mnblk", 1, 1, 1, 0, 1024, 8192, 1024, 8192},
   };
   float h[128 * 32];
   for (auto& v : vs) {
     cudaMemset(d, 0, sizeof(h));
-    probe<<<1, 128, 140 * 1024>>>(v.kind, v.amn, v.bmn, v.la, v.sa, v.lb, v.sb, d);
+    probe<<<1, 128, 140 * 1024>>>(v.kind, v.amn, v.bmn, v.klay, v.la, v.sa, v.lb, v.sb, d);
     cudaError_t e = cudaDeviceSynchronize();
     cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost);
     const int K = v.kind == 0 ? 8 : 16;
