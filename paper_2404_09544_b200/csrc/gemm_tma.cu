@@ -546,12 +546,13 @@ static size_t smem_bytes(int mode, int BN) {
 
 template <int MODE>
 static void launch(const Params& p, dim3 grid, cudaStream_t s) {
-  static bool set = false;
-  if (!set) {
-    GNNV_TRY_CUDA(cudaFuncSetAttribute(k_tma_gemm<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-    set = true;
+  static size_t attr = 0;  // dynamic smem opt-in, raised to the largest request seen
+  const size_t bytes = smem_bytes(MODE, p.BN);
+  if (bytes > attr) {
+    GNNV_TRY_CUDA(cudaFuncSetAttribute(k_tma_gemm<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+    attr = bytes;
   }
-  k_tma_gemm<MODE><<<grid, NTHREADS, smem_bytes(MODE, p.BN), s>>>(p);
+  k_tma_gemm<MODE><<<grid, NTHREADS, bytes, s>>>(p);
   GNNV_CHECK_LAUNCH();
 }
 
