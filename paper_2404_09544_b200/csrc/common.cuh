@@ -192,6 +192,7 @@ struct GemmDwArgs {  // dW = [X1|X2]^T G (+ bias row = colsum G) : deterministic
   float* dW;  // [(X2?2:1)*K1 x N]
   float* db;  // [N]
   float* partial; int32_t splits;  // workspace [splits x (rows+1) x N]
+  const float* Hmask;  // TF32 only: fuse G' = G * 1[Hmask > 0] and db (NULL: G is final, db elsewhere)
 };
 void gemm_dw(const GemmDwArgs& a, int prec, cudaStream_t s);
 size_t gemm_dw_partial_floats(int32_t rows_plus_bias, int32_t N, int32_t* splits_out, int64_t max_M);

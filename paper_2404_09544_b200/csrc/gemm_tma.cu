@@ -154,6 +154,10 @@ struct Params {
   // dw
   float* partial;
   int splits, rows_p, ablocks;  // ablocks: valid 32-wide i blocks (X1 then X2)
+  // dw with a fused ReLU mask: G' = G * 1[H > 0] and db partials per split
+  CUtensorMap th;
+  int mask;
+  float* dbpart;  // [splits][BN]
 };
 
 template <int MODE>
@@ -167,7 +171,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_tma_gemm(const __grid_constant_
   // fwd/dX stage: A [128 rows x 128B] + B [BN rows x 128B] (K-major SW128).
   // dW stage: MN boxes of [16 graph rows x 32 cols] (2 KB): MT*4 of A, BN/32 of G.
   const int a_bytes = MODE == MODE_DW ? MT * 4 * DW_BOX : BM * BKB;
-  const int b_bytes = MODE == MODE_DW ? (BN / 32) * DW_BOX : BN * BKB;
+  // dW with fused mask: the H boxes follow the G boxes in the stage
+  const int b_bytes = MODE == MODE_DW ? (BN / 32) * DW_BOX * (p.mask ? 2 : 1) : BN * BKB;
   const int stage_bytes = a_bytes + b_bytes;
   // dW: two K-major SW64 tiles (64B rows = 16 tf32 of K) built by the transposers
   const int kt_bytes = MODE == MODE_DW ? (MT * BM + BN) * 64 : 0;
@@ -350,6 +355,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_tma_gemm(const __grid_constant_
             else tma_load_2d(sa + bx * DW_BOX, &p.ta2, (blk - p.nkb1) * 32, row, &full[s]);
           }
           for (int cb = 0; cb < BN / 32; ++cb) tma_load_2d(sa + a_bytes + cb * DW_BOX, &p.tb, cb * 32, row, &full[s]);
+          if (p.mask)
+            for (int cb = 0; cb < BN / 32; ++cb)
+              tma_load_2d(sa + a_bytes + (BN / 32 + cb) * DW_BOX, &p.th, cb * 32, row, &full[s]);
         }
       }
     } else if (warp == 1) {
@@ -383,7 +391,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_tma_gemm(const __grid_constant_
       // Lane l reads column l of the box row by row (conflict-free 128B row
       // reads) and writes its 64B row as 4 swizzled 16B chunks.  Graph rows
       // >= M (stale tail) and features beyond the operand are written as 0.
+      // With p.mask the G boxes are multiplied by 1[H > 0] (H box staged next
+      // to them) and each lane keeps the column sum of its G' column (db).
       const int tw = warp - 2;  // 0..NE-1
+      float dbacc[2] = {0.f, 0.f};  // G' column sums of this warp's (<= 2) G boxes
       for (int i = 0; i < nkb; ++i) {
         const int s = i % S, b = i & 1;
         mbar_wait(&full[s], (i / S) & 1);
@@ -391,7 +402,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_tma_gemm(const __grid_constant_
         const int valid = min(DW_KR, M - (kb0 + i) * DW_KR);
         const uint8_t* st = smem + (size_t)s * stage_bytes;
         uint8_t* kt = kbuf + (size_t)b * kt_bytes;
-        for (int bx = tw; bx < nboxes; bx += NE) {
+        for (int bx = tw, jb = 0; bx < nboxes; bx += NE, ++jb) {
           const bool is_a = bx < MT * 4;
           const bool loaded = !is_a || (ig * MT * 4 + bx < p.ablocks);
           const uint8_t* src = st + (is_a ? (size_t)bx * DW_BOX : (size_t)a_bytes + (size_t)(bx - MT * 4) * DW_BOX);
@@ -400,6 +411,17 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_tma_gemm(const __grid_constant_
           for (int r = 0; r < DW_KR; ++r) {
             const uint32_t off = r * BKB + (((lane >> 2) ^ (r & 7)) << 4) + (lane & 3) * 4;
             x[r] = (loaded && r < valid) ? *reinterpret_cast<const float*>(src + off) : 0.f;
+          }
+          if (!is_a && p.mask) {
+            const uint8_t* hsrc = src + (BN / 32) * DW_BOX;
+            float acc = 0.f;
+#pragma unroll
+            for (int r = 0; r < DW_KR; ++r) {
+              const uint32_t off = r * BKB + (((lane >> 2) ^ (r & 7)) << 4) + (lane & 3) * 4;
+              if (!(r < valid && *reinterpret_cast<const float*>(hsrc + off) > 0.f)) x[r] = 0.f;
+              acc += x[r];
+            }
+            dbacc[jb & 1] += acc;
           }
           const int krow = is_a ? bx * 32 + lane : (bx - MT * 4) * 32 + lane;
           uint8_t* drow = kt + (is_a ? 0 : MT * BM * 64) + (size_t)krow * 64;
@@ -411,6 +433,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_tma_gemm(const __grid_constant_
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         mbar_arrive(&empty[s]);   // staging stage s may be refilled
         mbar_arrive(&kready[b]);  // K-major tile b ready for the MMA
+      }
+      if (p.mask && ig == 0) {
+        for (int bx = tw, jb = 0; bx < nboxes; bx += NE, ++jb)
+          if (bx >= MT * 4) p.dbpart[(int64_t)blockIdx.x * BN + (bx - MT * 4) * 32 + lane] = dbacc[jb & 1];
       }
       mbar_wait(&tfull[0], 0);
       tc_after();
@@ -536,10 +562,10 @@ struct Arena {
 };
 static Arena g_img, g_part;
 
-static size_t smem_bytes(int mode, int BN) {
+static size_t smem_bytes(int mode, int BN, int mask) {
   const int S = mode == MODE_DW ? DW_STAGES : FWD_STAGES;
   const int a = mode == MODE_DW ? DW_MT * 4 * DW_BOX : BM * BKB;
-  const int b = mode == MODE_DW ? (BN / 32) * DW_BOX : BN * BKB;
+  const int b = mode == MODE_DW ? (BN / 32) * DW_BOX * (mask ? 2 : 1) : BN * BKB;
   const int k = mode == MODE_DW ? 2 * (DW_MT * BM + BN) * 64 : 0;
   return (size_t)S * (a + b) + k + 8 * (2 * S + 8) + 16 + 1024;
 }
@@ -547,7 +573,7 @@ static size_t smem_bytes(int mode, int BN) {
 template <int MODE>
 static void launch(const Params& p, dim3 grid, cudaStream_t s) {
   static size_t attr = 0;  // dynamic smem opt-in, raised to the largest request seen
-  const size_t bytes = smem_bytes(MODE, p.BN);
+  const size_t bytes = smem_bytes(MODE, p.BN, p.mask);
   if (bytes > attr) {
     GNNV_TRY_CUDA(cudaFuncSetAttribute(k_tma_gemm<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
     attr = bytes;
@@ -620,7 +646,16 @@ bool gemm_dx_tma(const GemmDxArgs& a, cudaStream_t s) {
   return true;
 }
 
-// dW only (db comes from the column-sum kernel).
+__global__ void k_db_reduce_tma(const float* __restrict__ dbpart, int splits, int BN, int N, float* db) {
+  for (int n = blockIdx.x * blockDim.x + threadIdx.x; n < N; n += gridDim.x * blockDim.x) {
+    float s = 0.f;
+    for (int z = 0; z < splits; ++z) s += dbpart[(int64_t)z * BN + n];
+    db[n] = s;
+  }
+}
+
+// dW; with a.Hmask also the fused ReLU mask and db (else db comes from the
+// column-sum kernel in layers.cu).
 bool gemm_dw_tma(const GemmDwArgs& a, cudaStream_t s) {
   using namespace tma;
   const int BN = rup(a.N, 32);
@@ -631,8 +666,14 @@ bool gemm_dw_tma(const GemmDwArgs& a, cudaStream_t s) {
   const int igroups = rows_p / (BM * DW_MT);
   const int64_t nkbm = ceil_div(std::max<int64_t>(a.max_M, 1), DW_KR);
   const int splits = (int)std::max<int64_t>(1, std::min<int64_t>(nkbm, (int64_t)num_sms() / igroups));
-  float* partial = (float*)g_part.get((size_t)splits * rows_p * BN * sizeof(float), s);
+  const size_t part_f = (size_t)splits * rows_p * BN;
+  float* partial = (float*)g_part.get((part_f + (size_t)splits * BN) * sizeof(float), s);
   Params p{};
+  if (a.Hmask) {
+    p.mask = 1;
+    p.th = make_map(a.Hmask, a.max_M, a.N, a.ldg, DW_KR);
+    p.dbpart = partial + part_f;
+  }
   p.ta1 = make_map(a.X1, a.max_M, a.K1, a.ld1, DW_KR);
   p.ta2 = a.X2 ? make_map(a.X2, a.max_M, a.K1, a.ld2, DW_KR) : p.ta1;
   p.tb = make_map(a.G, a.max_M, a.N, a.ldg, DW_KR);
@@ -649,6 +690,10 @@ bool gemm_dw_tma(const GemmDwArgs& a, cudaStream_t s) {
   k_dw_reduce_tma<<<std::min(1024, (Ktot * a.N + 255) / 256), 256, 0, s>>>(partial, splits, rows_p, BN, a.K1, nkb1,
                                                                           Ktot, a.N, a.dW);
   GNNV_CHECK_LAUNCH();
+  if (a.Hmask) {
+    k_db_reduce_tma<<<1, 256, 0, s>>>(p.dbpart, splits, BN, a.N, a.db);
+    GNNV_CHECK_LAUNCH();
+  }
   return true;
 }
 

@@ -228,7 +228,10 @@ void layer_bwd_impl(gnnv_blocks* b, int32_t layer, const gnnv_layer_desc* ld, co
   float* dA = Gp + al(gp_f);
   float* colpart = dA + al(da_f);
   const float* G = Gdst;
-  if (tf32) {
+  // TF32 without dX (layer 1): the dW kernel applies the ReLU mask and sums
+  // db itself, so G' is never materialised.
+  const bool fuse_mask = tf32 && relu && !Gsrc;
+  if (tf32 && !fuse_mask) {
     // masked gradient + deterministic column sums (db) in one pass
     if (tl) tl->mark(s, "relu_mask" + sfx);
     k_mask_colsum<<<kColBlocks, 256, 0, s>>>(Gdst, relu ? Hdst : nullptr, Gp, ldo, d_ndst, colpart);
@@ -261,6 +264,7 @@ void layer_bwd_impl(gnnv_blocks* b, int32_t layer, const gnnv_layer_desc* ld, co
   w.db = db;
   w.partial = partial;
   w.splits = splits;
+  w.Hmask = fuse_mask ? Hdst : nullptr;
   if (tl) tl->mark(s, "gemm_dw" + sfx);
   gemm_dw(w, ld->prec, s);
   if (Gsrc) {
