@@ -239,7 +239,7 @@ void layer_bwd_impl(gnnv_blocks* b, int32_t layer, const gnnv_layer_desc* ld, co
     k_colsum_reduce<<<1, 256, 0, s>>>(colpart, kColBlocks, ldo, ld->d_out, db);
     GNNV_CHECK_LAUNCH();
     if (relu) G = Gp;
-  } else if (relu) {
+  } else if (relu && !tf32) {
     if (tl) tl->mark(s, "relu_mask" + sfx);
     launch_relu_mask(Gdst, Hdst, Gp, ldo, ld->d_out, d_ndst, max_dst, s);
     G = Gp;
