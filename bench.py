@@ -291,23 +291,22 @@ def main():
     stream = torch.cuda.current_stream()
     lr = 0.01
     # seeds of global iteration t: perm[t*G*B:(t+1)*G*B], rank r takes the r-th B-slice
+    from paper_2404_09544_b200.partition import global_batch, iters_per_epoch as _ipe, rank_slice
+
     perm = epoch_seeds(gd.n, 0)
-    iters_per_epoch = math.ceil(gd.n / (world * B))
+    iters_per_epoch = _ipe(gd.n, world, B)
     d_perm = torch.as_tensor(perm).cuda()
 
     def seeds_of(t):
-        t = t % iters_per_epoch
-        lo = t * world * B + rank * B
-        hi = min(gd.n, lo + B)
-        return lo, max(lo, hi)
+        lo, hi = rank_slice(t, rank, world, B, gd.n)
+        if hi <= lo:  # an empty trailing slice of a partial last iteration
+            lo, hi = 0, B
+        return lo, hi
 
     def step_device(t):
         lo, hi = seeds_of(t)
-        if hi <= lo:
-            lo, hi = 0, B
-        nb = hi - lo
-        tr.step(d_perm[lo:hi].data_ptr(), nb, world * B, BASE_RNG_SEED + t, lr, on_host=False, want_loss=False,
-                stream=stream)
+        tr.step(d_perm[lo:hi].data_ptr(), hi - lo, max(hi - lo, global_batch(t, world, B, gd.n)), BASE_RNG_SEED + t, lr,
+                on_host=False, want_loss=False, stream=stream)
 
     def barrier():
         if world > 1:
@@ -353,7 +352,8 @@ def main():
     for t in range(t0_steps, t0_steps + args.steps):
         lo, hi = seeds_of(t)
         host_seeds = perm[lo:hi]
-        loss, _ = tr.step(host_seeds, len(host_seeds), world * B, BASE_RNG_SEED + t, lr, on_host=True,
+        loss, _ = tr.step(host_seeds, len(host_seeds), max(len(host_seeds), global_batch(t, world, B, gd.n)),
+                          BASE_RNG_SEED + t, lr, on_host=True,
                           want_loss=True, stream=stream)
     e1.record(stream)
     barrier()
