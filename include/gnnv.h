@@ -249,6 +249,21 @@ gnnv_status gnnv_layer_bwd(gnnv_blocks* b, int32_t layer, const gnnv_layer_desc*
 gnnv_status gnnv_ce_loss(gnnv_blocks* b, const gnnv_graph* g, const float* d_logits, int32_t n_classes,
                          int32_t stride, int32_t n_global, float* d_loss, float* d_dlogits, gnnv_stream s);
 
+/* The layer's dense products on their own (host-side M), for kernel tests
+ * and micro-benchmarks.  Layouts as in gnnv_layer_fwd/bwd:
+ *  fwd: Y[M x ldy] = act([X1 | X2] W + b), X2 may be NULL (K = K1)
+ *  dx : [Y1 | Y2] = G W^T, G [M x ldg] with N columns, Y2 may be NULL
+ *  dw : dW = [X1 | X2]^T G (+ db = colsum(G) if d_db), deterministic
+ * prec: gnnv_prec.  Stream-ordered. */
+gnnv_status gnnv_dense_fwd(const float* d_X1, int32_t ld1, const float* d_X2, int32_t ld2, int32_t K1,
+                           const float* d_W, const float* d_b, float* d_Y, int32_t ldy, int32_t N, int64_t M,
+                           int32_t relu, int32_t prec, gnnv_stream s);
+gnnv_status gnnv_dense_dx(const float* d_G, int32_t ldg, int32_t N, const float* d_W, int32_t K1, float* d_Y1,
+                          int32_t ld1, float* d_Y2, int32_t ld2, int64_t M, int32_t prec, gnnv_stream s);
+gnnv_status gnnv_dense_dw(const float* d_X1, int32_t ld1, const float* d_X2, int32_t ld2, int32_t K1,
+                          const float* d_G, int32_t ldg, int32_t N, int64_t M, float* d_dW, float* d_db,
+                          int32_t prec, gnnv_stream s);
+
 /* Plain gradient descent p <- p - lr g. */
 gnnv_status gnnv_sgd(float* d_params, const float* d_grads, int64_t n, float lr, gnnv_stream s);
 

@@ -158,7 +158,17 @@ struct Params {
   CUtensorMap th;
   int mask;
   float* dbpart;  // [splits][BN]
+  int dbg;        // micro-benchmark switches (GNNV_DEBUG_GEMM): 1 = no epilogue stores, 2 = no MMA
 };
+
+static int debug_flags() {
+  static int f = -1;
+  if (f < 0) {
+    const char* e = getenv("GNNV_DEBUG_GEMM");
+    f = e ? atoi(e) : 0;
+  }
+  return f;
+}
 
 template <int MODE>
 __global__ void __launch_bounds__(NTHREADS, 1) k_tma_gemm(const __grid_constant__ Params p) {
@@ -270,7 +280,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_tma_gemm(const __grid_constant_
             const uint32_t b0 = a0 + a_bytes;
 #pragma unroll
             for (int k = 0; k < BK / 8; ++k) {
-              mma_tf32(tmem + (uint32_t)(acc * BN), desc_sw(a0 + k * 32, 1024, 2), desc_sw(b0 + k * 32, 1024, 2),
+              if (!(p.dbg & 2))
+                mma_tf32(tmem + (uint32_t)(acc * BN), desc_sw(a0 + k * 32, 1024, 2), desc_sw(b0 + k * 32, 1024, 2),
                        idesc, (kb > 0 || k > 0) ? 1u : 0u);
             }
             mma_commit(&empty[s]);
@@ -299,7 +310,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_tma_gemm(const __grid_constant_
           const int w = min(32, BN - c);
           if (w == 32) tmem_ld32(tbase + c, v);
           else tmem_ld16(tbase + c, v);
-          if (m < M) {
+          if (m < M && !(p.dbg & 1)) {
             if (MODE == MODE_FWD) {
               float* yrow = p.Y + m * p.ldy;
 #pragma unroll
@@ -612,6 +623,7 @@ bool gemm_fwd_tma(const GemmFwdArgs& a, cudaStream_t s) {
   p.bias = a.bias;
   p.relu = a.relu ? 1 : 0;
   const int64_t tiles = ceil_div(std::max<int64_t>(a.max_M, 1), BM);
+  p.dbg = debug_flags();
   launch<MODE_FWD>(p, dim3((unsigned)std::min<int64_t>(tiles, num_sms())), s);
   return true;
 }
@@ -642,6 +654,7 @@ bool gemm_dx_tma(const GemmDxArgs& a, cudaStream_t s) {
   p.ld1 = a.ld1;
   p.ld2 = a.ld2;
   const int64_t tiles = ceil_div(std::max<int64_t>(a.max_M, 1), BM) * ntl;
+  p.dbg = debug_flags();
   launch<MODE_DX>(p, dim3((unsigned)std::min<int64_t>(tiles, num_sms())), s);
   return true;
 }
@@ -685,6 +698,7 @@ bool gemm_dw_tma(const GemmDwArgs& a, cudaStream_t s) {
   p.splits = splits;
   p.rows_p = rows_p;
   p.ablocks = ablocks;
+  p.dbg = debug_flags();
   launch<MODE_DW>(p, dim3((unsigned)splits, (unsigned)igroups), s);
   const int Ktot = a.X2 ? 2 * a.K1 : a.K1;
   k_dw_reduce_tma<<<std::min(1024, (Ktot * a.N + 255) / 256), 256, 0, s>>>(partial, splits, rows_p, BN, a.K1, nkb1,

@@ -322,6 +322,129 @@ gnnv_status gnnv_layer_bwd(gnnv_blocks* b, int32_t layer, const gnnv_layer_desc*
   });
 }
 
+}  // extern "C"
+
+namespace {
+// device-side row counts for the dense entry points: a ring of slots filled
+// in stream order (the kernels read M from the device, like in a step)
+const int32_t* device_count(int64_t M, cudaStream_t s) {
+  static int32_t* ring = nullptr;
+  static int slot = 0;
+  constexpr int kSlots = 1024;
+  if (!ring) ring = (int32_t*)gnnv::dmalloc(kSlots * sizeof(int32_t), "dense row counts");
+  int32_t* p = ring + (slot++ % kSlots);
+  const int32_t v = (int32_t)M;
+  GNNV_TRY_CUDA(cudaMemcpyAsync(p, &v, sizeof(v), cudaMemcpyHostToDevice, s));
+  return p;
+}
+float* dense_scratch(size_t floats, cudaStream_t s) {
+  static float* buf = nullptr;
+  static size_t cap = 0;
+  if (floats > cap) {
+    if (buf) {
+      GNNV_TRY_CUDA(cudaStreamSynchronize(s));
+      gnnv::dfree(buf);
+    }
+    cap = std::max(floats, (size_t)1 << 20);
+    buf = (float*)gnnv::dmalloc(cap * sizeof(float), "dense scratch");
+  }
+  return buf;
+}
+}  // namespace
+
+extern "C" {
+
+gnnv_status gnnv_dense_fwd(const float* X1, int32_t ld1, const float* X2, int32_t ld2, int32_t K1, const float* W,
+                           const float* b, float* Y, int32_t ldy, int32_t N, int64_t M, int32_t relu, int32_t prec,
+                           gnnv_stream st) {
+  return guarded([&] {
+    GNNV_REQUIRE(X1 && W && b && Y && K1 >= 1 && N >= 1 && M >= 1 && M < INT32_MAX, GNNV_ERR_PARAM, "dense_fwd: args");
+    GNNV_REQUIRE(ld1 >= K1 && ld1 % 4 == 0 && (!X2 || (ld2 >= K1 && ld2 % 4 == 0)) && ldy >= N && ldy % 4 == 0,
+                 GNNV_ERR_PARAM, "dense_fwd: strides");
+    GNNV_REQUIRE(prec >= GNNV_PREC_FP32 && prec <= GNNV_PREC_TF32, GNNV_ERR_PARAM, "dense_fwd: prec");
+    cudaStream_t s = (cudaStream_t)st;
+    GemmFwdArgs g{};
+    g.X1 = X1;
+    g.ld1 = ld1;
+    g.X2 = X2;
+    g.ld2 = ld2;
+    g.K1 = K1;
+    g.W = W;
+    g.bias = b;
+    g.Y = Y;
+    g.ldy = ldy;
+    g.N = N;
+    g.d_M = device_count(M, s);
+    g.max_M = M;
+    g.relu = relu != 0;
+    gemm_fwd(g, prec, s);
+  });
+}
+
+gnnv_status gnnv_dense_dx(const float* G, int32_t ldg, int32_t N, const float* W, int32_t K1, float* Y1, int32_t ld1,
+                          float* Y2, int32_t ld2, int64_t M, int32_t prec, gnnv_stream st) {
+  return guarded([&] {
+    GNNV_REQUIRE(G && W && Y1 && K1 >= 1 && N >= 1 && M >= 1 && M < INT32_MAX, GNNV_ERR_PARAM, "dense_dx: args");
+    GNNV_REQUIRE(ldg >= N && ldg % 4 == 0 && ld1 >= K1 && ld1 % 4 == 0 && (!Y2 || (ld2 >= K1 && ld2 % 4 == 0)),
+                 GNNV_ERR_PARAM, "dense_dx: strides");
+    GNNV_REQUIRE(prec >= GNNV_PREC_FP32 && prec <= GNNV_PREC_TF32, GNNV_ERR_PARAM, "dense_dx: prec");
+    cudaStream_t s = (cudaStream_t)st;
+    GemmDxArgs x{};
+    x.G = G;
+    x.ldg = ldg;
+    x.N = N;
+    x.W = W;
+    x.K1 = K1;
+    x.Y1 = Y1;
+    x.ld1 = ld1;
+    x.Y2 = Y2;
+    x.ld2 = ld2;
+    x.d_M = device_count(M, s);
+    x.max_M = M;
+    gemm_dx(x, prec, s);
+  });
+}
+
+gnnv_status gnnv_dense_dw(const float* X1, int32_t ld1, const float* X2, int32_t ld2, int32_t K1, const float* G,
+                          int32_t ldg, int32_t N, int64_t M, float* dW, float* db, int32_t prec, gnnv_stream st) {
+  return guarded([&] {
+    GNNV_REQUIRE(X1 && G && dW && K1 >= 1 && N >= 1 && M >= 1 && M < INT32_MAX, GNNV_ERR_PARAM, "dense_dw: args");
+    GNNV_REQUIRE(ld1 >= K1 && ld1 % 4 == 0 && (!X2 || (ld2 >= K1 && ld2 % 4 == 0)) && ldg >= N && ldg % 4 == 0,
+                 GNNV_ERR_PARAM, "dense_dw: strides");
+    GNNV_REQUIRE(prec >= GNNV_PREC_FP32 && prec <= GNNV_PREC_TF32, GNNV_ERR_PARAM, "dense_dw: prec");
+    cudaStream_t s = (cudaStream_t)st;
+    const int rows = (X2 ? 2 * K1 : K1) + 1;
+    int32_t splits = 1;
+    const size_t part_f = gemm_dw_partial_floats(rows, N, &splits, M);
+    const size_t cs_f = (size_t)kColBlocks * ldg;
+    float* scratch = dense_scratch(part_f + cs_f + N, s);
+    float* db_out = db ? db : scratch + part_f + cs_f;
+    GemmDwArgs w{};
+    w.X1 = X1;
+    w.ld1 = ld1;
+    w.X2 = X2;
+    w.ld2 = ld2;
+    w.K1 = K1;
+    w.G = G;
+    w.ldg = ldg;
+    w.N = N;
+    w.d_M = device_count(M, s);
+    w.max_M = M;
+    w.dW = dW;
+    w.db = db_out;
+    w.partial = scratch;
+    w.splits = splits;
+    if (prec == GNNV_PREC_TF32) {
+      float* colpart = scratch + part_f;
+      k_mask_colsum<<<kColBlocks, 256, 0, s>>>(G, nullptr, nullptr, ldg, w.d_M, colpart);
+      GNNV_CHECK_LAUNCH();
+      k_colsum_reduce<<<1, 256, 0, s>>>(colpart, kColBlocks, ldg, N, db_out);
+      GNNV_CHECK_LAUNCH();
+    }
+    gemm_dw(w, prec, s);
+  });
+}
+
 gnnv_status gnnv_ce_loss(gnnv_blocks* b, const gnnv_graph* g, const float* d_logits, int32_t n_classes, int32_t stride,
                          int32_t n_global, float* d_loss, float* d_dlogits, gnnv_stream s) {
   return guarded([&] {

@@ -104,6 +104,9 @@ _SIGS = {
     "gnnv_layer_bwd": (I32, [VP, I32, C.POINTER(LayerDesc), VP, VP, VP, VP, VP, VP, VP, VP, VP]),
     "gnnv_ce_loss": (I32, [VP, VP, VP, I32, I32, I32, VP, VP, VP]),
     "gnnv_sgd": (I32, [VP, VP, I64, F32, VP]),
+    "gnnv_dense_fwd": (I32, [VP, I32, VP, I32, I32, VP, VP, VP, I32, I32, I64, I32, I32, VP]),
+    "gnnv_dense_dx": (I32, [VP, I32, I32, VP, I32, VP, I32, VP, I32, I64, I32, VP]),
+    "gnnv_dense_dw": (I32, [VP, I32, VP, I32, I32, VP, I32, I32, I64, VP, VP, I32, VP]),
     "gnnv_trainer_create": (I32, [VP, VP, C.POINTER(ModelDesc), VP, VP, PP]),
     "gnnv_trainer_free": (I32, [VP]),
     "gnnv_trainer_num_params": (I64, [VP]),
@@ -342,6 +345,21 @@ def layer_bwd(blocks: Blocks, layer: int, ld: LayerDesc, Gdst, Hdst, Hsrc, saveA
 def ce_loss(blocks: Blocks, g: Graph, logits, n_classes, stride, n_global, loss, dlogits, stream=None):
     _check(load().gnnv_ce_loss(blocks.h, g.h, ptr(logits), int(n_classes), int(stride), int(n_global), ptr(loss),
                                ptr(dlogits), stream_ptr(stream)))
+
+
+def dense_fwd(X1, ld1, X2, ld2, K1, W, b, Y, ldy, N, M, relu=True, prec=PREC_TF32, stream=None):
+    _check(load().gnnv_dense_fwd(ptr(X1), ld1, ptr(X2), ld2, K1, ptr(W), ptr(b), ptr(Y), ldy, N, int(M),
+                                 1 if relu else 0, prec, stream_ptr(stream)))
+
+
+def dense_dx(G, ldg, N, W, K1, Y1, ld1, Y2, ld2, M, prec=PREC_TF32, stream=None):
+    _check(load().gnnv_dense_dx(ptr(G), ldg, N, ptr(W), K1, ptr(Y1), ld1, ptr(Y2), ld2, int(M), prec,
+                                stream_ptr(stream)))
+
+
+def dense_dw(X1, ld1, X2, ld2, K1, G, ldg, N, M, dW, db=None, prec=PREC_TF32, stream=None):
+    _check(load().gnnv_dense_dw(ptr(X1), ld1, ptr(X2), ld2, K1, ptr(G), ldg, N, int(M), ptr(dW), ptr(db), prec,
+                                stream_ptr(stream)))
 
 
 def sgd(params, grads, n: int, lr: float, stream=None):
