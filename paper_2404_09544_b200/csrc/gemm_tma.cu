@@ -45,7 +45,6 @@ constexpr int FWD_STAGES = 4;
 constexpr int DW_STAGES = 3;
 constexpr int DW_MT = 2;    // 128-row i-tiles per dW CTA
 constexpr int DW_KR = 16;   // graph rows per dW k-block
-constexpr int DW_BOX = DW_KR * BKB;  // one staged [16 x 32] fp32 box
 constexpr int MODE_FWD = 0, MODE_DX = 1, MODE_DW = 2;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -74,6 +73,14 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, i
           smem_u32(dst)),
       "l"(map), "r"(c0), "r"(c1), "r"(smem_u32(bar))
       : "memory");
+}
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void* src, int c0, int c1) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(map), "r"(c0),
+               "r"(c1), "r"(smem_u32(src))
+               : "memory");
+}
+__device__ __forceinline__ void st_shared_v4(uint32_t addr, float a, float b, float c, float d) {
+  asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "f"(a), "f"(b), "f"(c), "f"(d) : "memory");
 }
 __device__ __forceinline__ void tma_prefetch(const CUtensorMap* map) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(map) : "memory");
@@ -137,6 +144,7 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
 
 struct Params {
   CUtensorMap ta1, ta2, tb;
+  CUtensorMap ty1, ty2;  // fwd/dX outputs (TMA stores, SW128 boxes of 32 x 32)
   int two;      // A has a second source (SAGE [H_dst | A])
   int nkb1;     // fwd: K blocks served by X1 (ceil(K1/32)); dw: 32-col blocks of X1
   int nkb;      // fwd/dx: K blocks in total
@@ -178,16 +186,20 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_tma_gemm(const __grid_constant_
   constexpr int S = MODE == MODE_DW ? DW_STAGES : FWD_STAGES;
   constexpr int MT = MODE == MODE_DW ? DW_MT : 1;
   const int BN = p.BN;
-  // fwd/dX stage: A [128 rows x 128B] + B [BN rows x 128B] (K-major SW128).
-  // dW stage: MN boxes of [16 graph rows x 32 cols] (2 KB): MT*4 of A, BN/32 of G.
-  const int a_bytes = MODE == MODE_DW ? MT * 4 * DW_BOX : BM * BKB;
-  // dW with fused mask: the H boxes follow the G boxes in the stage
-  const int b_bytes = MODE == MODE_DW ? (BN / 32) * DW_BOX * (p.mask ? 2 : 1) : BN * BKB;
+  // fwd/dX stage: A [128 rows x 128B] + B [BN rows x 128B] (K-major SW128 boxes).
+  // dW stage (unswizzled row-major boxes of DW_KR graph rows): MT A tiles of
+  // [16 x 128] fp32, then G [16 x BN], then (fused mask) H [16 x BN].
+  const int a_bytes = MODE == MODE_DW ? MT * DW_KR * BM * 4 : BM * BKB;
+  const int g_bytes = MODE == MODE_DW ? DW_KR * BN * 4 : BN * BKB;
+  const int b_bytes = MODE == MODE_DW ? g_bytes * (p.mask ? 2 : 1) : g_bytes;
   const int stage_bytes = a_bytes + b_bytes;
-  // dW: two K-major SW64 tiles (64B rows = 16 tf32 of K) built by the transposers
+  // dW: two K-major SW64 tiles (64B rows = 16 tf32 of K) built by the transposers;
+  // fwd/dX: one 4 KB SW128 output staging buffer per epilogue warp (TMA store)
   const int kt_bytes = MODE == MODE_DW ? (MT * BM + BN) * 64 : 0;
   uint8_t* kbuf = smem + (size_t)S * stage_bytes;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(kbuf + 2 * kt_bytes);
+  uint8_t* obuf = kbuf;
+  const int extra = MODE == MODE_DW ? 2 * kt_bytes : NE * 4096;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(kbuf + extra);
   uint64_t* full = bars;
   uint64_t* empty = bars + S;
   uint64_t* kready = bars + 2 * S;  // dW: K-major tile b ready
@@ -282,7 +294,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_tma_gemm(const __grid_constant_
             for (int k = 0; k < BK / 8; ++k) {
               if (!(p.dbg & 2))
                 mma_tf32(tmem + (uint32_t)(acc * BN), desc_sw(a0 + k * 32, 1024, 2), desc_sw(b0 + k * 32, 1024, 2),
-                       idesc, (kb > 0 || k > 0) ? 1u : 0u);
+                         idesc, (kb > 0 || k > 0) ? 1u : 0u);
             }
             mma_commit(&empty[s]);
           }
@@ -291,11 +303,14 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_tma_gemm(const __grid_constant_
       }
       __syncwarp();
     } else {
-      // 8 epilogue warps: lane quarter q = warp & 3 (tcgen05.ld restriction),
-      // 32-column chunks interleaved between the two warps of a quarter.
+      // 8 epilogue warps: TMEM lane quarter q = warp & 3 (tcgen05.ld
+      // restriction), 32-column chunks interleaved between the two warps of a
+      // quarter.  Each chunk (32 rows x 32 cols) goes through a 128B-swizzled
+      // 4 KB smem buffer and one TMA store: coalesced full-line writes.
       const int q = warp & 3;
       const int half = (warp - 2) >> 2;
-      const int row = q * 32 + lane;
+      uint8_t* ob = obuf + (warp - 2) * 4096;
+      const uint32_t ob_u32 = smem_u32(ob);
       int lt = 0;
       for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++lt) {
         const int acc = lt & 1;
@@ -303,51 +318,55 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_tma_gemm(const __grid_constant_
         const int nt = MODE == MODE_DX ? tile % p.n_ntiles : 0;
         mbar_wait(&tfull[acc], (lt >> 1) & 1);
         tc_after();
-        const int64_t m = (int64_t)mt * BM + row;
+        const int row0 = mt * BM + q * 32;
         const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN);
         for (int c = half * 32; c < BN; c += 64) {
           float v[32];
-          const int w = min(32, BN - c);
-          if (w == 32) tmem_ld32(tbase + c, v);
-          else tmem_ld16(tbase + c, v);
-          if (m < M && !(p.dbg & 1)) {
-            if (MODE == MODE_FWD) {
-              float* yrow = p.Y + m * p.ldy;
+          if (BN - c >= 32) tmem_ld32(tbase + c, v);
+          else {
+            tmem_ld16(tbase + c, v);
 #pragma unroll
-              for (int j = 0; j < 32; j += 4) {
-                const int n = c + j;
-                if (j < w && n < p.ldy) {
-                  float o[4];
+            for (int j = 16; j < 32; ++j) v[j] = 0.f;
+          }
+          if (MODE == MODE_FWD) {
 #pragma unroll
-                  for (int e = 0; e < 4; ++e) {
-                    float x = v[j + e] + s_bias[n + e];
-                    if (p.relu) x = fmaxf(x, 0.f);
-                    o[e] = (n + e < p.N) ? x : 0.f;
-                  }
-                  *reinterpret_cast<float4*>(yrow + n) = make_float4(o[0], o[1], o[2], o[3]);
-                }
-              }
-            } else {
-#pragma unroll
-              for (int j = 0; j < 32; j += 4) {
-                if (j >= w) break;
-                const int col = nt * BN + c + j;
-                const float4 o = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
-                if (col < p.ld1) *reinterpret_cast<float4*>(p.Y1 + m * p.ld1 + col) = o;
-                else if (p.Y2 && col - p.ld1 < p.ld2) *reinterpret_cast<float4*>(p.Y2 + m * p.ld2 + (col - p.ld1)) = o;
-              }
+            for (int j = 0; j < 32; ++j) {
+              const int n = c + j;
+              float x = v[j] + (n < BN ? s_bias[n] : 0.f);
+              if (p.relu) x = fmaxf(x, 0.f);
+              v[j] = n < p.N ? x : 0.f;
             }
+          }
+          // the previous TMA store from this buffer must have read it
+          if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+          __syncwarp();
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            st_shared_v4(ob_u32 + lane * 128 + ((j ^ (lane & 7)) << 4), v[4 * j], v[4 * j + 1], v[4 * j + 2],
+                         v[4 * j + 3]);
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          __syncwarp();
+          if (lane == 0 && !(p.dbg & 1)) {
+            if (MODE == MODE_FWD) {
+              tma_store_2d(&p.ty1, ob, c, row0);
+            } else {
+              const int j0 = nt * BN + c;
+              if (j0 < p.ld1) tma_store_2d(&p.ty1, ob, j0, row0);
+              if (p.Y2 && j0 + 32 > p.ld1) tma_store_2d(&p.ty2, ob, j0 - p.ld1, row0);
+            }
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
           }
         }
         tc_before();
         mbar_arrive(&tempty[acc]);
       }
+      if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
     }
   } else {
     // =============================== dW ===============================
     const int nkb = kb1 - kb0;
     const int ig = blockIdx.y;  // i-tile group
-    const int nboxes = MT * 4 + BN / 32;
+    const int ngroups = MT * 4 + BN / 32;  // 32-column transposer work units
     if (warp == 0) {
       if (lane == 0) {
         for (int i = 0; i < nkb; ++i) {
@@ -356,19 +375,18 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_tma_gemm(const __grid_constant_
           uint8_t* sa = smem + (size_t)s * stage_bytes;
           const int row = (kb0 + i) * DW_KR;
           uint32_t bytes = (uint32_t)b_bytes;
-          for (int bx = 0; bx < MT * 4; ++bx)
-            if (ig * MT * 4 + bx < p.ablocks) bytes += DW_BOX;
+          for (int mt = 0; mt < MT; ++mt)
+            if ((ig * MT + mt) * 4 < p.ablocks) bytes += DW_KR * BM * 4;
           mbar_arrive_tx(&full[s], bytes);
-          for (int bx = 0; bx < MT * 4; ++bx) {
-            const int blk = ig * MT * 4 + bx;  // 32-wide i block
+          for (int mt = 0; mt < MT; ++mt) {
+            const int blk = (ig * MT + mt) * 4;  // first 32-wide i block of this 128-row tile
             if (blk >= p.ablocks) continue;
-            if (blk < p.nkb1) tma_load_2d(sa + bx * DW_BOX, &p.ta1, blk * 32, row, &full[s]);
-            else tma_load_2d(sa + bx * DW_BOX, &p.ta2, (blk - p.nkb1) * 32, row, &full[s]);
+            uint8_t* dst = sa + mt * (DW_KR * BM * 4);
+            if (blk < p.nkb1) tma_load_2d(dst, &p.ta1, blk * 32, row, &full[s]);
+            else tma_load_2d(dst, &p.ta2, (blk - p.nkb1) * 32, row, &full[s]);
           }
-          for (int cb = 0; cb < BN / 32; ++cb) tma_load_2d(sa + a_bytes + cb * DW_BOX, &p.tb, cb * 32, row, &full[s]);
-          if (p.mask)
-            for (int cb = 0; cb < BN / 32; ++cb)
-              tma_load_2d(sa + a_bytes + (BN / 32 + cb) * DW_BOX, &p.th, cb * 32, row, &full[s]);
+          tma_load_2d(sa + a_bytes, &p.tb, 0, row, &full[s]);
+          if (p.mask) tma_load_2d(sa + a_bytes + g_bytes, &p.th, 0, row, &full[s]);
         }
       }
     } else if (warp == 1) {
@@ -386,8 +404,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_tma_gemm(const __grid_constant_
           for (int mt = 0; mt < MT; ++mt) {
 #pragma unroll
             for (int k = 0; k < DW_KR / 8; ++k) {
-              mma_tf32(tmem + (uint32_t)(mt * BN), desc_sw(ka + mt * BM * 64 + k * 32, 512, 4),
-                       desc_sw(kbb + k * 32, 512, 4), idesc, (i > 0 || k > 0) ? 1u : 0u);
+              if (!(p.dbg & 2))
+                mma_tf32(tmem + (uint32_t)(mt * BN), desc_sw(ka + mt * BM * 64 + k * 32, 512, 4),
+                         desc_sw(kbb + k * 32, 512, 4), idesc, (i > 0 || k > 0) ? 1u : 0u);
             }
           }
           mma_commit(&kfree[b]);
@@ -397,15 +416,15 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_tma_gemm(const __grid_constant_
       }
       __syncwarp();
     } else {
-      // ---- transposers: staged MN box [16 graph rows x 32 cols] -> 32 K-major
-      // SW64 rows (one per feature / output column, 16 graph rows of K).
-      // Lane l reads column l of the box row by row (conflict-free 128B row
-      // reads) and writes its 64B row as 4 swizzled 16B chunks.  Graph rows
-      // >= M (stale tail) and features beyond the operand are written as 0.
-      // With p.mask the G boxes are multiplied by 1[H > 0] (H box staged next
-      // to them) and each lane keeps the column sum of its G' column (db).
+      // ---- transposers: a 32-column group of a staged [16 x cols] box -> 32
+      // K-major SW64 rows (one per feature / output column, 16 graph rows of
+      // K).  Lane l reads column l row by row (consecutive floats: no bank
+      // conflicts) and writes its 64B row as 4 swizzled 16B chunks.  Graph
+      // rows >= M (stale tail) and features beyond the operand become 0.  With
+      // p.mask the G group is multiplied by 1[H > 0] (H staged after G) and
+      // each lane keeps the column sum of its G' column (db).
       const int tw = warp - 2;  // 0..NE-1
-      float dbacc[2] = {0.f, 0.f};  // G' column sums of this warp's (<= 2) G boxes
+      float dbacc[2] = {0.f, 0.f};
       for (int i = 0; i < nkb; ++i) {
         const int s = i % S, b = i & 1;
         mbar_wait(&full[s], (i / S) & 1);
@@ -413,41 +432,52 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_tma_gemm(const __grid_constant_
         const int valid = min(DW_KR, M - (kb0 + i) * DW_KR);
         const uint8_t* st = smem + (size_t)s * stage_bytes;
         uint8_t* kt = kbuf + (size_t)b * kt_bytes;
-        for (int bx = tw, jb = 0; bx < nboxes; bx += NE, ++jb) {
-          const bool is_a = bx < MT * 4;
-          const bool loaded = !is_a || (ig * MT * 4 + bx < p.ablocks);
-          const uint8_t* src = st + (is_a ? (size_t)bx * DW_BOX : (size_t)a_bytes + (size_t)(bx - MT * 4) * DW_BOX);
+#pragma unroll
+        for (int jb = 0; jb < 2; ++jb) {
+          const int gx = tw + jb * NE;
+          if (gx >= ngroups) break;
+          const bool is_a = gx < MT * 4;
+          const bool loaded = !is_a || ((ig * MT + gx / 4) * 4 < p.ablocks);
+          const float* src;
+          int ld;
+          if (is_a) {
+            src = reinterpret_cast<const float*>(st + (gx / 4) * (DW_KR * BM * 4)) + (gx % 4) * 32 + lane;
+            ld = BM;
+          } else {
+            src = reinterpret_cast<const float*>(st + a_bytes) + (gx - MT * 4) * 32 + lane;
+            ld = BN;
+          }
           float x[DW_KR];
 #pragma unroll
-          for (int r = 0; r < DW_KR; ++r) {
-            const uint32_t off = r * BKB + (((lane >> 2) ^ (r & 7)) << 4) + (lane & 3) * 4;
-            x[r] = (loaded && r < valid) ? *reinterpret_cast<const float*>(src + off) : 0.f;
-          }
+          for (int r = 0; r < DW_KR; ++r) x[r] = (loaded && r < valid) ? src[r * ld] : 0.f;
           if (!is_a && p.mask) {
-            const uint8_t* hsrc = src + (BN / 32) * DW_BOX;
+            const float* hs = src + DW_KR * BN;
             float acc = 0.f;
 #pragma unroll
             for (int r = 0; r < DW_KR; ++r) {
-              const uint32_t off = r * BKB + (((lane >> 2) ^ (r & 7)) << 4) + (lane & 3) * 4;
-              if (!(r < valid && *reinterpret_cast<const float*>(hsrc + off) > 0.f)) x[r] = 0.f;
+              if (!(r < valid && hs[r * ld] > 0.f)) x[r] = 0.f;
               acc += x[r];
             }
-            dbacc[jb & 1] += acc;
+            if (jb == 0) dbacc[0] += acc;
+            else dbacc[1] += acc;
           }
-          const int krow = is_a ? bx * 32 + lane : (bx - MT * 4) * 32 + lane;
-          uint8_t* drow = kt + (is_a ? 0 : MT * BM * 64) + (size_t)krow * 64;
+          const int krow = is_a ? gx * 32 + lane : (gx - MT * 4) * 32 + lane;
+          const uint32_t drow = smem_u32(kt + (is_a ? 0 : MT * BM * 64) + (size_t)krow * 64);
 #pragma unroll
           for (int j = 0; j < 4; ++j)
-            *reinterpret_cast<float4*>(drow + ((j ^ ((krow >> 1) & 3)) << 4)) =
-                make_float4(x[4 * j], x[4 * j + 1], x[4 * j + 2], x[4 * j + 3]);
+            st_shared_v4(drow + ((j ^ ((krow >> 1) & 3)) << 4), x[4 * j], x[4 * j + 1], x[4 * j + 2], x[4 * j + 3]);
         }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         mbar_arrive(&empty[s]);   // staging stage s may be refilled
         mbar_arrive(&kready[b]);  // K-major tile b ready for the MMA
       }
       if (p.mask && ig == 0) {
-        for (int bx = tw, jb = 0; bx < nboxes; bx += NE, ++jb)
-          if (bx >= MT * 4) p.dbpart[(int64_t)blockIdx.x * BN + (bx - MT * 4) * 32 + lane] = dbacc[jb & 1];
+#pragma unroll
+        for (int jb = 0; jb < 2; ++jb) {
+          const int gx = tw + jb * NE;
+          if (gx >= MT * 4 && gx < ngroups)
+            p.dbpart[(int64_t)blockIdx.x * BN + (gx - MT * 4) * 32 + lane] = jb == 0 ? dbacc[0] : dbacc[1];
+        }
       }
       mbar_wait(&tfull[0], 0);
       tc_after();
@@ -543,15 +573,17 @@ static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 
 // 2-D fp32 row-major tensor [rows x cols] with row stride ld (floats); box
 // [box_rows x 32 cols], 128B swizzle, out-of-range elements read as zero.
-static CUtensorMap make_map(const float* base, int64_t rows, int64_t cols, int64_t ld, int box_rows) {
+static CUtensorMap make_map(const float* base, int64_t rows, int64_t cols, int64_t ld, int box_rows,
+                            int box_cols = 32, bool swizzle = true) {
   CUtensorMap m;
   const cuuint64_t dims[2] = {(cuuint64_t)std::max<int64_t>(cols, 1), (cuuint64_t)std::max<int64_t>(rows, 1)};
   const cuuint64_t strides[1] = {(cuuint64_t)ld * sizeof(float)};
-  const cuuint32_t box[2] = {32, (cuuint32_t)box_rows};
+  const cuuint32_t box[2] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows};
   const cuuint32_t estr[2] = {1, 1};
   CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void*)base, dims, strides, box, estr,
-                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                           CU_TENSOR_MAP_INTERLEAVE_NONE,
+                           swizzle ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   GNNV_REQUIRE(r == CUDA_SUCCESS, GNNV_ERR_CUDA, "cuTensorMapEncodeTiled failed (alignment/stride)");
   return m;
 }
@@ -575,9 +607,9 @@ static Arena g_img, g_part;
 
 static size_t smem_bytes(int mode, int BN, int mask) {
   const int S = mode == MODE_DW ? DW_STAGES : FWD_STAGES;
-  const int a = mode == MODE_DW ? DW_MT * 4 * DW_BOX : BM * BKB;
-  const int b = mode == MODE_DW ? (BN / 32) * DW_BOX * (mask ? 2 : 1) : BN * BKB;
-  const int k = mode == MODE_DW ? 2 * (DW_MT * BM + BN) * 64 : 0;
+  const int a = mode == MODE_DW ? DW_MT * DW_KR * BM * 4 : BM * BKB;
+  const int b = mode == MODE_DW ? DW_KR * BN * 4 * (mask ? 2 : 1) : BN * BKB;
+  const int k = mode == MODE_DW ? 2 * (DW_MT * BM + BN) * 64 : NE * 4096;
   return (size_t)S * (a + b) + k + 8 * (2 * S + 8) + 16 + 1024;
 }
 
@@ -622,6 +654,7 @@ bool gemm_fwd_tma(const GemmFwdArgs& a, cudaStream_t s) {
   p.N = a.N;
   p.bias = a.bias;
   p.relu = a.relu ? 1 : 0;
+  p.ty1 = make_map(a.Y, a.max_M, a.ldy, a.ldy, 32);
   const int64_t tiles = ceil_div(std::max<int64_t>(a.max_M, 1), BM);
   p.dbg = debug_flags();
   launch<MODE_FWD>(p, dim3((unsigned)std::min<int64_t>(tiles, num_sms())), s);
@@ -653,6 +686,8 @@ bool gemm_dx_tma(const GemmDxArgs& a, cudaStream_t s) {
   p.Y2 = a.Y2;
   p.ld1 = a.ld1;
   p.ld2 = a.ld2;
+  p.ty1 = make_map(a.Y1, a.max_M, a.ld1, a.ld1, 32);
+  p.ty2 = a.Y2 ? make_map(a.Y2, a.max_M, a.ld2, a.ld2, 32) : p.ty1;
   const int64_t tiles = ceil_div(std::max<int64_t>(a.max_M, 1), BM) * ntl;
   p.dbg = debug_flags();
   launch<MODE_DX>(p, dim3((unsigned)std::min<int64_t>(tiles, num_sms())), s);
@@ -673,7 +708,7 @@ bool gemm_dw_tma(const GemmDwArgs& a, cudaStream_t s) {
   using namespace tma;
   const int BN = rup(a.N, 32);
   if (BN * DW_MT > 512) return false;
-  const int nkb1 = (a.K1 + 31) / 32;
+  const int nkb1 = (a.K1 + 127) / 128 * 4;  // 32-col blocks per source, whole 128-col tiles
   const int ablocks = a.X2 ? 2 * nkb1 : nkb1;
   const int rows_p = rup(ablocks * 32, BM * DW_MT);
   const int igroups = rows_p / (BM * DW_MT);
@@ -684,12 +719,12 @@ bool gemm_dw_tma(const GemmDwArgs& a, cudaStream_t s) {
   Params p{};
   if (a.Hmask) {
     p.mask = 1;
-    p.th = make_map(a.Hmask, a.max_M, a.N, a.ldg, DW_KR);
+    p.th = make_map(a.Hmask, a.max_M, a.N, a.ldg, DW_KR, BN, false);
     p.dbpart = partial + part_f;
   }
-  p.ta1 = make_map(a.X1, a.max_M, a.K1, a.ld1, DW_KR);
-  p.ta2 = a.X2 ? make_map(a.X2, a.max_M, a.K1, a.ld2, DW_KR) : p.ta1;
-  p.tb = make_map(a.G, a.max_M, a.N, a.ldg, DW_KR);
+  p.ta1 = make_map(a.X1, a.max_M, a.K1, a.ld1, DW_KR, BM, false);
+  p.ta2 = a.X2 ? make_map(a.X2, a.max_M, a.K1, a.ld2, DW_KR, BM, false) : p.ta1;
+  p.tb = make_map(a.G, a.max_M, a.N, a.ldg, DW_KR, BN, false);
   p.two = a.X2 ? 1 : 0;
   p.nkb1 = nkb1;
   p.BN = BN;
