@@ -218,7 +218,14 @@ typedef struct {
   int32_t prec;       /* gnnv_prec */
 } gnnv_layer_desc;
 
-/* GNN layer i in 1..L on block b_{L-i} (Eq.1; Algorithm 1 lines
+/* Buffer sizing for the layer calls: the row counts live on the device (the
+ * step never synchronises), so every activation / gradient buffer passed
+ * below must be allocated for the CAPACITY rows of its block
+ * (gnnv_block_view.max_dst / max_src, available with sync=0).  Rows beyond
+ * the actual counts may be read (and ignored); outputs are written for the
+ * actual rows only, except dH_src rows beyond n_src which are unspecified.
+ *
+ * GNN layer i in 1..L on block b_{L-i} (Eq.1; Algorithm 1 lines
  * 5-6 P:110-111; reading Q11):
  *   SAGE: A = Agg(H_src), H_dst = act(H_src[0:n_dst] W_s + A W_n + b)
  *   GCN : A = (h_v + sum_u h_u)/(c_v+1) (or sum), H_dst = act(A W + b)

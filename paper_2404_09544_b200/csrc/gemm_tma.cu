@@ -337,6 +337,25 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_tma_gemm(const __grid_constant_
               v[j] = n < p.N ? x : 0.f;
             }
           }
+          if (row0 + 32 > M) {
+            // ragged last chunk: plain stores of the rows < M only (the TMA
+            // map spans the row capacity, which may exceed the caller's rows)
+            const int64_t m = (int64_t)row0 + lane;
+            if (m < M && !(p.dbg & 1)) {
+#pragma unroll
+              for (int j = 0; j < 32; j += 4) {
+                const float4 o = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+                if (MODE == MODE_FWD) {
+                  if (c + j < p.ldy) *reinterpret_cast<float4*>(p.Y + m * p.ldy + c + j) = o;
+                } else {
+                  const int col = nt * BN + c + j;
+                  if (col < p.ld1) *reinterpret_cast<float4*>(p.Y1 + m * p.ld1 + col) = o;
+                  else if (p.Y2 && col - p.ld1 < p.ld2) *reinterpret_cast<float4*>(p.Y2 + m * p.ld2 + (col - p.ld1)) = o;
+                }
+              }
+            }
+            continue;
+          }
           // the previous TMA store from this buffer must have read it
           if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
           __syncwarp();

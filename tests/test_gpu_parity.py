@@ -169,6 +169,14 @@ def test_gather_bit_exact(mini, ratio, placement, G):
 
 
 # ------------------------------------------------------------------ layers
+def padded(arr, cap):
+    """Device copy of `arr` in a buffer of `cap` rows (capacity-sized, as the
+    layer API requires); the rows beyond are NaN and must never matter."""
+    t = torch.full((int(cap), arr.shape[1]), float("nan"), device="cuda")
+    t[: arr.shape[0]] = torch.as_tensor(np.ascontiguousarray(arr, dtype=np.float32)).cuda()
+    return t
+
+
 def _oracle_block(hb, h):
     nd, ns, ptr, idx, F = hb[h]
     return Block(n_dst=nd, n_src=ns, indptr=ptr.astype(np.int64), indices=idx.astype(np.int64), src_global=F)
@@ -197,15 +205,18 @@ def test_layer_fwd_bwd_parity(mini, kind, aggr, prec):
         b = rng.standard_normal(d_out).astype(np.float32)
         relu = layer < L
         ld = gnnv.layer_desc(d_in, d_out, s_in, kind, aggr, 1 if relu else 0, prec)
-        dH, dW_, db_ = dev_f32(Hsrc), dev_f32(W), dev_f32(b)
+        view = blocks.info(sync=False)[h]
+        cap_dst, cap_src = view.max_dst, view.max_src
+        dH, dW_, db_ = padded(Hsrc, cap_src), dev_f32(W), dev_f32(b)
         so = row_stride(d_out)
-        Hdst = torch.full((ob.n_dst, so), float("nan"), device="cuda")
-        A = torch.full((ob.n_dst, row_stride(d_in)), float("nan"), device="cuda")
+        Hdst = torch.full((cap_dst, so), float("nan"), device="cuda")
+        A = torch.full((cap_dst, row_stride(d_in)), float("nan"), device="cuda")
         gnnv.layer_fwd(blocks, layer, ld, dH, dW_, db_, Hdst, A)
         torch.cuda.synchronize()
         Ho, Ao = layer_fwd(ob, Hsrc[:, :d_in], W, b, relu, kname, aname)
         Hm, Am = layer_fwd(ob, Hsrc[:, :d_in], W, b, relu, kname, aname, absval=True)
-        Hg, Ag = Hdst.cpu().numpy(), A.cpu().numpy()
+        Hg, Ag = Hdst[: ob.n_dst].cpu().numpy(), A[: ob.n_dst].cpu().numpy()
+        assert torch.isnan(Hdst[ob.n_dst:]).all() and torch.isnan(A[ob.n_dst:]).all()  # rows >= n_dst untouched
         assert_close_cond(Ag[:, :d_in], Ao, Am, RTOL32, f"A layer {layer}")
         assert (Ag[:, d_in:] == 0).all() and (Hg[:, d_out:] == 0).all()
         assert_close_cond(Hg[:, :d_out], Ho, Hm, rtol, f"H layer {layer}")
@@ -213,11 +224,13 @@ def test_layer_fwd_bwd_parity(mini, kind, aggr, prec):
         G = np.zeros((ob.n_dst, so), np.float32)
         G[:, :d_out] = rng.standard_normal((ob.n_dst, d_out)).astype(np.float32)
         need_dx = layer > 1
-        Gsrc = torch.full((ob.n_src, s_in), float("nan"), device="cuda") if need_dx else None
+        Gsrc = torch.full((cap_src, s_in), float("nan"), device="cuda") if need_dx else None
         dW = torch.full((rows, d_out), float("nan"), device="cuda")
         db = torch.full((d_out,), float("nan"), device="cuda")
-        gnnv.layer_bwd(blocks, layer, ld, dev_f32(G), Hdst, dH, A, dW_, Gsrc, dW, db)
+        gnnv.layer_bwd(blocks, layer, ld, padded(G, cap_dst), Hdst, dH, A, dW_, Gsrc, dW, db)
         torch.cuda.synchronize()
+        if need_dx:
+            Gsrc = Gsrc[: ob.n_src]
         # oracle backward on the GPU's forward values (same ReLU mask)
         rW, rb, rX = layer_bwd(ob, Hsrc[:, :d_in], Ag[:, :d_in], Hg[:, :d_out], W, G[:, :d_out], relu, need_dx,
                                kname, aname)
@@ -356,24 +369,28 @@ def test_layer_shapes(mini, prec, d_in, d_out, kind):
     kname = "sage" if kind == 0 else "gcn"
     ld = gnnv.layer_desc(d_in, d_out, s_in, kind, 0, 1, prec)
     so = row_stride(d_out)
-    dH, dW_, db_ = dev_f32(Hsrc), dev_f32(W), dev_f32(b)
-    Hdst = torch.full((ob.n_dst, so), float("nan"), device="cuda")
-    A = torch.full((ob.n_dst, s_in), float("nan"), device="cuda")
+    view = blocks.info(sync=False)[L - layer]
+    cap_dst, cap_src = view.max_dst, view.max_src
+    dH, dW_, db_ = padded(Hsrc, cap_src), dev_f32(W), dev_f32(b)
+    Hdst = torch.full((cap_dst, so), float("nan"), device="cuda")
+    A = torch.full((cap_dst, s_in), float("nan"), device="cuda")
     gnnv.layer_fwd(blocks, layer, ld, dH, dW_, db_, Hdst, A)
     torch.cuda.synchronize()
     rtol = RTOL[prec]
     Ho, Ao = layer_fwd(ob, Hsrc[:, :d_in], W, b, True, kname)
     Hm, _ = layer_fwd(ob, Hsrc[:, :d_in], W, b, True, kname, absval=True)
-    Hg, Ag = Hdst.cpu().numpy(), A.cpu().numpy()
+    Hg, Ag = Hdst[: ob.n_dst].cpu().numpy(), A[: ob.n_dst].cpu().numpy()
     assert_close_cond(Hg[:, :d_out], Ho, Hm, rtol, "H")
     assert (Hg[:, d_out:] == 0).all()
+    assert torch.isnan(Hdst[ob.n_dst:]).all()
     G = np.zeros((ob.n_dst, so), np.float32)
     G[:, :d_out] = rng.standard_normal((ob.n_dst, d_out)).astype(np.float32)
-    Gsrc = torch.full((ob.n_src, s_in), float("nan"), device="cuda")
+    Gsrc = torch.full((cap_src, s_in), float("nan"), device="cuda")
     dW = torch.full((rows, d_out), float("nan"), device="cuda")
     db = torch.full((d_out,), float("nan"), device="cuda")
-    gnnv.layer_bwd(blocks, layer, ld, dev_f32(G), Hdst, dH, A, dW_, Gsrc, dW, db)
+    gnnv.layer_bwd(blocks, layer, ld, padded(G, cap_dst), Hdst, dH, A, dW_, Gsrc, dW, db)
     torch.cuda.synchronize()
+    Gsrc = Gsrc[: ob.n_src]
     rW, rb, rX = layer_bwd(ob, Hsrc[:, :d_in], Ag[:, :d_in], Hg[:, :d_out], W, G[:, :d_out], True, True, kname)
     mW, mb, mX = layer_bwd(ob, np.abs(Hsrc[:, :d_in]), np.abs(Ag[:, :d_in]), Hg[:, :d_out], np.abs(W),
                            np.abs(G[:, :d_out]), True, True, kname)
