@@ -337,9 +337,11 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_tma_gemm(const __grid_constant_
               v[j] = n < p.N ? x : 0.f;
             }
           }
-          if (row0 + 32 > M) {
+          const int j0 = nt * BN + c;  // dX: column in the [Y1 | Y2] space
+          if (row0 + 32 > M || (MODE == MODE_DX && j0 < p.ld1 && j0 + 32 > p.ld1)) {
             // ragged last chunk: plain stores of the rows < M only (the TMA
-            // map spans the row capacity, which may exceed the caller's rows)
+            // map spans the row capacity, which may exceed the caller's rows);
+            // a dX chunk straddling Y1 | Y2 also takes this path
             const int64_t m = (int64_t)row0 + lane;
             if (m < M && !(p.dbg & 1)) {
 #pragma unroll
@@ -368,10 +370,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_tma_gemm(const __grid_constant_
           if (lane == 0 && !(p.dbg & 1)) {
             if (MODE == MODE_FWD) {
               tma_store_2d(&p.ty1, ob, c, row0);
-            } else {
-              const int j0 = nt * BN + c;
-              if (j0 < p.ld1) tma_store_2d(&p.ty1, ob, j0, row0);
-              if (p.Y2 && j0 + 32 > p.ld1) tma_store_2d(&p.ty2, ob, j0 - p.ld1, row0);
+            } else if (j0 < p.ld1) {
+              tma_store_2d(&p.ty1, ob, j0, row0);
+            } else if (p.Y2) {
+              tma_store_2d(&p.ty2, ob, j0 - p.ld1, row0);
             }
             asm volatile("cp.async.bulk.commit_group;" ::: "memory");
           }
@@ -684,7 +686,7 @@ bool gemm_dx_tma(const GemmDxArgs& a, cudaStream_t s) {
   using namespace tma;
   const int NC = a.Y2 ? a.ld1 + a.ld2 : a.ld1;
   const int ntl = (NC + 255) / 256;
-  const int BN = rup((NC + ntl - 1) / ntl, 16);
+  const int BN = rup((NC + ntl - 1) / ntl, 32);  // whole 32-column epilogue chunks
   const int nkb = (a.N + BK - 1) / BK;
   const int Kp = nkb * BK;
   const int NCpad = ntl * BN;
