@@ -46,11 +46,13 @@ __global__ void k_fill_shard(const int32_t* __restrict__ order, int64_t C, int G
 }
 
 // ----------------------------------------------------------------- gather
-// One warp per row group; lanes stride over the row's float4 columns; ROWS
-// rows are in flight per warp (independent 16-byte loads) for memory-level
-// parallelism.  Sources: shard ptrs[s % G] row s / G (HBM or NVLink peer) or
-// the mapped host table (PCIe) on a miss.
-template <int ROWS>
+// A warp owns 32 consecutive rows of F_L: lane i resolves row base+i's
+// source (F -> slot -> shard pointer, or the mapped host row on a miss) in
+// one round of parallel loads, then the warp copies the rows RU at a time
+// with the lanes striding over float4 columns and all RU loads issued before
+// the stores (memory-level parallelism for 400-2400 B rows).  Sources: shard
+// ptrs[s % G] row s / G (HBM or NVLink peer) or the pinned host table (PCIe).
+template <int RU>
 __global__ void __launch_bounds__(256) k_gather(const int32_t* __restrict__ F, const int32_t* sizes, int L,
                                                 const int32_t* __restrict__ slot,
                                                 const float* const* __restrict__ shards, int G, int me,
@@ -62,36 +64,40 @@ __global__ void __launch_bounds__(256) k_gather(const int32_t* __restrict__ F, c
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int nwarps = (gridDim.x * blockDim.x) >> 5;
   unsigned long long c_local = 0, c_peer = 0, c_miss = 0;
-  for (int base = warp * ROWS; base < n; base += nwarps * ROWS) {
-    const float4* src[ROWS];
-#pragma unroll
-    for (int r = 0; r < ROWS; ++r) {
-      const int row = base + r;
-      src[r] = nullptr;
-      if (row < n) {
-        const int v = F[row];
-        const int s = slot[v];
-        if (s >= 0) {
-          const int o = s % G;
-          src[r] = reinterpret_cast<const float4*>(shards[o]) + (int64_t)(s / G) * vec;
-          if (lane == 0) {
-            if (o == me) ++c_local;
-            else ++c_peer;
-          }
-        } else {
-          src[r] = reinterpret_cast<const float4*>(host) + (int64_t)v * vec;
-          if (lane == 0) ++c_miss;
-        }
+  for (int base = warp * 32; base < n; base += nwarps * 32) {
+    const int row = base + lane;
+    const float4* src = nullptr;
+    int kind = -1;  // 0 local, 1 peer, 2 host
+    if (row < n) {
+      const int v = F[row];
+      const int s = slot[v];
+      if (s >= 0) {
+        const int o = s % G;
+        src = reinterpret_cast<const float4*>(shards[o]) + (int64_t)(s / G) * vec;
+        kind = o == me ? 0 : 1;
+      } else {
+        src = reinterpret_cast<const float4*>(host) + (int64_t)v * vec;
+        kind = 2;
       }
     }
-    for (int c = lane; c < vec; c += 32) {
-      float4 val[ROWS];
+    c_local += __popc(__ballot_sync(0xffffffffu, kind == 0));
+    c_peer += __popc(__ballot_sync(0xffffffffu, kind == 1));
+    c_miss += __popc(__ballot_sync(0xffffffffu, kind == 2));
+    const int nrows = min(32, n - base);
+    const uint64_t my = reinterpret_cast<uint64_t>(src);
+    for (int r0 = 0; r0 < nrows; r0 += RU) {
+      const float4* ps[RU];
 #pragma unroll
-      for (int r = 0; r < ROWS; ++r)
-        if (src[r]) val[r] = __ldg(src[r] + c);
+      for (int j = 0; j < RU; ++j) ps[j] = reinterpret_cast<const float4*>(__shfl_sync(0xffffffffu, my, r0 + j));
+      for (int c = lane; c < vec; c += 32) {
+        float4 val[RU];
 #pragma unroll
-      for (int r = 0; r < ROWS; ++r)
-        if (src[r]) __stcs(reinterpret_cast<float4*>(X) + (int64_t)(base + r) * vec + c, val[r]);
+        for (int j = 0; j < RU; ++j)
+          if (r0 + j < nrows) val[j] = __ldg(ps[j] + c);
+#pragma unroll
+        for (int j = 0; j < RU; ++j)
+          if (r0 + j < nrows) __stcs(reinterpret_cast<float4*>(X) + (int64_t)(base + r0 + j) * vec + c, val[j]);
+      }
     }
   }
   if (stats && lane == 0) {
@@ -104,13 +110,13 @@ __global__ void __launch_bounds__(256) k_gather(const int32_t* __restrict__ F, c
 
 void launch_gather(const gnnv_cache* c, const gnnv_blocks* b, float* d_X, int64_t* d_stats, cudaStream_t s) {
   const gnnv_graph* g = c->g;
-  constexpr int ROWS = 4;
+  constexpr int RU = 8;
   const int64_t rows_ub = b->max_n[b->L];
-  const int64_t warps = ceil_div(rows_ub, ROWS);
+  const int64_t warps = ceil_div(rows_ub, 32);
   const int blocks = (int)std::min<int64_t>(ceil_div(warps, 8), (int64_t)num_sms() * 8);
-  k_gather<ROWS><<<std::max(blocks, 1), 256, 0, s>>>(b->d_F, b->d_sizes, b->L, c->d_slot, c->d_shard_ptrs, c->world,
-                                                     c->rank, g->d_feats, g->stride, d_X,
-                                                     reinterpret_cast<unsigned long long*>(d_stats));
+  k_gather<RU><<<std::max(blocks, 1), 256, 0, s>>>(b->d_F, b->d_sizes, b->L, c->d_slot, c->d_shard_ptrs, c->world,
+                                                   c->rank, g->d_feats, g->stride, d_X,
+                                                   reinterpret_cast<unsigned long long*>(d_stats));
   GNNV_CHECK_LAUNCH();
 }
 

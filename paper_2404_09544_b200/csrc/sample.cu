@@ -89,18 +89,38 @@ __global__ void __launch_bounds__(256) k_sample_hop(const int64_t* __restrict__ 
   const unsigned gmask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << (grp * G));
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int nwarps = (gridDim.x * blockDim.x) >> 5;
-  for (int base = warp * RPW; base < n; base += nwarps * RPW) {
+  const int stride = nwarps * RPW;
+  // software pipeline over this group's rows r, r+stride, ...: F two rows
+  // ahead and indptr one row ahead, so a row's dependent metadata loads are
+  // in flight while the previous row is processed
+  auto loadF = [&](int row) { return row < n ? F[row] : -1; };
+  auto loadDeg = [&](int v, int64_t& beg, int& d) {
+    beg = 0;
+    d = 0;
+    if ((uint32_t)v < (uint64_t)N) {
+      beg = indptr[v];
+      d = (int)(indptr[v + 1] - beg);
+    }
+  };
+  int v_cur = loadF(warp * RPW + grp);
+  int v_nxt = loadF(warp * RPW + grp + stride);
+  int64_t beg_cur;
+  int d_cur;
+  loadDeg(v_cur, beg_cur, d_cur);
+  for (int base = warp * RPW; base < n; base += stride) {
     const int r = base + grp;
     const bool active = r < n;
-    int64_t beg = 0;
-    int d = 0, v = 0;
-    if (active) {
-      v = F[r];
-      if ((uint32_t)v < (uint64_t)N) {
-        beg = indptr[v];
-        d = (int)(indptr[v + 1] - beg);
-      }
-    }
+    int64_t beg_nxt;
+    int d_nxt;
+    loadDeg(v_nxt, beg_nxt, d_nxt);
+    const int v_nn = loadF(r + 2 * stride);
+    const int v = active ? v_cur : 0;
+    const int64_t beg = beg_cur;
+    const int d = active ? d_cur : 0;
+    v_cur = v_nxt;
+    beg_cur = beg_nxt;
+    d_cur = d_nxt;
+    v_nxt = v_nn;
     const int c = min(k, d);
     int pos = gl, slot = gl;
     if (d > k) {  // group-uniform branch: Floyd's algorithm over k draws
@@ -170,16 +190,31 @@ __global__ void __launch_bounds__(kScanTile) k_relabel_scan(int64_t N, int h, in
   if (tile >= ntiles) return;
   unsigned long long* st = status + 1;
   const int r = tile * kScanTile + threadIdx.x;
-  uint32_t mask = 0;
-  int c = 0;
-  if (r < n) {
-    c = cnt[r];
-    for (int i = 0; i < c; ++i) {
-      const int e = r * k + i;
-      const int u = ell[e];
-      if ((uint32_t)u < (uint64_t)N && tag[u] == -(2 + e)) mask |= 1u << i;
+  // winners of the claim, computed slot-parallel over the tile (independent
+  // ell -> tag load pairs in flight) and collected as per-row bit masks
+  __shared__ uint32_t s_mask[kScanTile];
+  __shared__ int s_cnt[kScanTile];
+  const int r0 = tile * kScanTile;
+  const int rows = min(kScanTile, n - r0);
+  s_mask[threadIdx.x] = 0;
+  s_cnt[threadIdx.x] = threadIdx.x < rows ? cnt[r0 + threadIdx.x] : 0;
+  __syncthreads();
+  {
+    const int nslots = rows * k;
+    const int e0 = r0 * k;
+#pragma unroll 4
+    for (int j = threadIdx.x; j < nslots; j += kScanTile) {
+      const int rl = j / k, i = j - rl * k;
+      if (i < s_cnt[rl]) {
+        const int e = e0 + j;
+        const int u = ell[e];
+        if ((uint32_t)u < (uint64_t)N && tag[u] == -(2 + e)) atomicOr(&s_mask[rl], 1u << i);
+      }
     }
   }
+  __syncthreads();
+  const uint32_t mask = s_mask[threadIdx.x];
+  const int c = s_cnt[threadIdx.x];
   // block exclusive scan of (a, b) = (#new ids, #sampled)
   const uint32_t a = __popc(mask), b = (uint32_t)c;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -215,29 +250,45 @@ __global__ void __launch_bounds__(kScanTile) k_relabel_scan(int64_t N, int h, in
   __syncthreads();
   const uint32_t excl_a = ia - a + (wid ? s_wa[wid - 1] : 0u);
   const uint32_t excl_b = ib - b + (wid ? s_wb[wid - 1] : 0u);
-  if (threadIdx.x == 0) {
+  if (wid == 0) {
+    // decoupled look-back, one warp: lane j inspects predecessor tile-1-j
     const uint32_t A = s_wa[kScanTile / 32 - 1], B = s_wb[kScanTile / 32 - 1];
     if (tile == 0) {
-      st_release_u64(&st[0], kFlagPre | pack2(A, B));
-      s_pa = 0;
-      s_pb = 0;
+      if (lane == 0) {
+        st_release_u64(&st[0], kFlagPre | pack2(A, B));
+        s_pa = 0;
+        s_pb = 0;
+      }
     } else {
-      st_release_u64(&st[tile], kFlagAgg | pack2(A, B));
+      if (lane == 0) st_release_u64(&st[tile], kFlagAgg | pack2(A, B));
       uint32_t pa = 0, pb = 0;
       int p = tile - 1;
       while (true) {
-        unsigned long long w;
-        do {
-          w = ld_acquire_u64(&st[p]);
-        } while ((w >> 62) == 0);
-        pa += unpack_a(w);
-        pb += unpack_b(w);
-        if ((w >> 62) == 2) break;
-        --p;
+        const int q = p - lane;
+        unsigned long long w = kFlagPre;  // before tile 0: an inclusive zero
+        if (q >= 0) {
+          do {
+            w = ld_acquire_u64(&st[q]);
+          } while ((w >> 62) == 0);
+        }
+        const unsigned pre = __ballot_sync(0xffffffffu, (w >> 62) == 2);
+        const int stop = pre ? __ffs(pre) - 1 : 31;  // nearest inclusive prefix in the window
+        uint32_t va = lane <= stop ? unpack_a(w) : 0u, vb = lane <= stop ? unpack_b(w) : 0u;
+#pragma unroll
+        for (int o = 16; o; o >>= 1) {
+          va += __shfl_xor_sync(0xffffffffu, va, o);
+          vb += __shfl_xor_sync(0xffffffffu, vb, o);
+        }
+        pa += va;
+        pb += vb;
+        if (pre) break;
+        p -= 32;
       }
-      st_release_u64(&st[tile], kFlagPre | pack2(pa + A, pb + B));
-      s_pa = pa;
-      s_pb = pb;
+      if (lane == 0) {
+        st_release_u64(&st[tile], kFlagPre | pack2(pa + A, pb + B));
+        s_pa = pa;
+        s_pb = pb;
+      }
     }
   }
   __syncthreads();
