@@ -167,6 +167,10 @@ void launch_spmm_fwd(const int32_t* d_indptr, const int32_t* d_indices, const in
 void launch_spmm_bwd(const int32_t* d_indptr, const int32_t* d_indices, const int32_t* d_ndst, int64_t max_dst,
                      const float* dA, int32_t lda, float* dH, int32_t ldh, int32_t d, int32_t kind, int32_t aggr,
                      cudaStream_t s);
+size_t spmm_bwd_csc_scratch_bytes(int64_t max_dst, int64_t max_src, int64_t max_nnz);
+void launch_spmm_bwd_csc(const int32_t* d_indptr, const int32_t* d_indices, const int32_t* d_ndst, const int32_t* d_nsrc,
+                         int64_t max_dst, int64_t max_src, int64_t max_nnz, const float* dA, int32_t lda, float* dH,
+                         int32_t ldh, int32_t d, int32_t kind, int32_t aggr, void* scratch, cudaStream_t s);
 void launch_rows_zero(float* X, int32_t ld, const int32_t* d_row_begin, const int32_t* d_row_end, int64_t max_rows,
                       cudaStream_t s);
 // gemm

@@ -89,38 +89,18 @@ __global__ void __launch_bounds__(256) k_sample_hop(const int64_t* __restrict__ 
   const unsigned gmask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << (grp * G));
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int nwarps = (gridDim.x * blockDim.x) >> 5;
-  const int stride = nwarps * RPW;
-  // software pipeline over this group's rows r, r+stride, ...: F two rows
-  // ahead and indptr one row ahead, so a row's dependent metadata loads are
-  // in flight while the previous row is processed
-  auto loadF = [&](int row) { return row < n ? F[row] : -1; };
-  auto loadDeg = [&](int v, int64_t& beg, int& d) {
-    beg = 0;
-    d = 0;
-    if ((uint32_t)v < (uint64_t)N) {
-      beg = indptr[v];
-      d = (int)(indptr[v + 1] - beg);
-    }
-  };
-  int v_cur = loadF(warp * RPW + grp);
-  int v_nxt = loadF(warp * RPW + grp + stride);
-  int64_t beg_cur;
-  int d_cur;
-  loadDeg(v_cur, beg_cur, d_cur);
-  for (int base = warp * RPW; base < n; base += stride) {
+  for (int base = warp * RPW; base < n; base += nwarps * RPW) {
     const int r = base + grp;
     const bool active = r < n;
-    int64_t beg_nxt;
-    int d_nxt;
-    loadDeg(v_nxt, beg_nxt, d_nxt);
-    const int v_nn = loadF(r + 2 * stride);
-    const int v = active ? v_cur : 0;
-    const int64_t beg = beg_cur;
-    const int d = active ? d_cur : 0;
-    v_cur = v_nxt;
-    beg_cur = beg_nxt;
-    d_cur = d_nxt;
-    v_nxt = v_nn;
+    int64_t beg = 0;
+    int d = 0, v = 0;
+    if (active) {
+      v = F[r];
+      if ((uint32_t)v < (uint64_t)N) {
+        beg = indptr[v];
+        d = (int)(indptr[v + 1] - beg);
+      }
+    }
     const int c = min(k, d);
     int pos = gl, slot = gl;
     if (d > k) {  // group-uniform branch: Floyd's algorithm over k draws
