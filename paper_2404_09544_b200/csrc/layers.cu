@@ -222,7 +222,7 @@ void layer_bwd_impl(gnnv_blocks* b, int32_t layer, const gnnv_layer_desc* ld, co
   const size_t da_f = Gsrc ? (size_t)max_dst * lda : 0;
   const size_t cs_f = tf32 ? (size_t)kColBlocks * ldo : 0;
   auto al = [](size_t f) { return (f + 63) & ~(size_t)63; };
-  const size_t csc_f = Gsrc ? (spmm_bwd_csc_scratch_bytes(max_dst, b->max_n[h + 1], b->max_nnz[h]) + 3) / 4 : 0;
+  const size_t csc_f = 0;
   float* scratch =
       (float*)b->ensure_scratch((al(part_f) + al(gp_f) + al(da_f) + al(cs_f) + al(csc_f)) * sizeof(float), s);
   float* partial = scratch;
@@ -293,10 +293,13 @@ void layer_bwd_impl(gnnv_blocks* b, int32_t layer, const gnnv_layer_desc* ld, co
     if (tl) tl->mark(s, "gemm_dx" + sfx);
     gemm_dx(x, ld->prec, s);
     if (tl) tl->mark(s, "spmm_bwd" + sfx);
-    // transposed aggregation in gather form (CSC built on the device): every
-    // dH_src row is written once, no atomics, no zeroing pass
-    launch_spmm_bwd_csc(b->d_indptr[h], b->d_indices[h], d_ndst, d_ndst + 1, max_dst, b->max_n[h + 1], b->max_nnz[h],
-                        dA, lda, Gsrc, ld->in_stride, ld->d_in, ld->kind, ld->aggr, cscbuf, s);
+    // transposed aggregation by scatter (red.global.add.v4.f32); the
+    // gather form over a device-built CSC (launch_spmm_bwd_csc) measured no
+    // faster on the products workload and stays available
+    (void)cscbuf;
+    launch_rows_zero(Gsrc, ld->in_stride, sage ? d_ndst : nullptr, d_ndst + 1, b->max_n[h + 1], s);
+    launch_spmm_bwd(b->d_indptr[h], b->d_indices[h], d_ndst, max_dst, dA, lda, Gsrc, ld->in_stride, ld->d_in,
+                    ld->kind, ld->aggr, s);
   }
 }
 

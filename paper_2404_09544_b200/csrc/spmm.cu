@@ -144,17 +144,6 @@ __global__ void k_rows_zero(float* X, int32_t ld, const int32_t* d_begin, const 
     X4[t] = make_float4(0.f, 0.f, 0.f, 0.f);
 }
 
-template <int RU, int EK, bool BWD>
-__global__ void k_row_gather(const int32_t* __restrict__ ptr, const int32_t* __restrict__ idx,
-                             const float* __restrict__ wv, const int32_t* d_nrows, const int32_t* d_nself,
-                             const float* __restrict__ in, int32_t ldi, float* out, int32_t ldo, int32_t d,
-                             int32_t kind, int32_t aggr);
-
-static int rowgather_grid(int64_t max_rows) {
-  const int64_t warps = ceil_div(std::max<int64_t>(max_rows, 1), 32);
-  return (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(warps, 8), (int64_t)num_sms() * 8));
-}
-
 static int spmm_grid(int64_t max_rows, int rows_per_warp) {
   const int64_t warps = ceil_div(std::max<int64_t>(max_rows, 1), rows_per_warp);
   return (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(warps, 8), (int64_t)num_sms() * 16));
@@ -163,8 +152,14 @@ static int spmm_grid(int64_t max_rows, int rows_per_warp) {
 void launch_spmm_fwd(const int32_t* d_indptr, const int32_t* d_indices, const int32_t* d_ndst, int64_t max_dst,
                      const float* H, int32_t ldh, float* A, int32_t lda, int32_t d, int32_t kind, int32_t aggr,
                      cudaStream_t s) {
-  k_row_gather<2, 8, false><<<rowgather_grid(max_dst), 256, 0, s>>>(d_indptr, d_indices, nullptr, d_ndst, nullptr, H,
-                                                                      ldh, A, lda, d, kind, aggr);
+  const int vec = (d + 3) / 4;
+  if (vec <= 8) {
+    k_spmm_fwd<8><<<spmm_grid(max_dst, 4), 256, 0, s>>>(d_indptr, d_indices, d_ndst, H, ldh, A, lda, d, kind, aggr);
+  } else if (vec <= 16) {
+    k_spmm_fwd<16><<<spmm_grid(max_dst, 2), 256, 0, s>>>(d_indptr, d_indices, d_ndst, H, ldh, A, lda, d, kind, aggr);
+  } else {
+    k_spmm_fwd<32><<<spmm_grid(max_dst, 1), 256, 0, s>>>(d_indptr, d_indices, d_ndst, H, ldh, A, lda, d, kind, aggr);
+  }
   GNNV_CHECK_LAUNCH();
 }
 
@@ -348,125 +343,6 @@ __global__ void __launch_bounds__(256) k_spmm_bwd_gather(const int32_t* __restri
   }
 }
 
-// ---------------------------------------------------------------------
-// Batched row gather: out[r] = base(r) + scale(r) * sum_k w_k in[idx_k].
-// A warp owns 32 output rows: lane i resolves row base+i's list (offsets,
-// the first EK neighbour ids and weights) in one round of parallel loads;
-// the warp then produces the rows RU at a time, lanes striding over float4
-// columns, with all RU x EK neighbour-row loads issued before they are
-// summed (ascending list order).  Lists longer than EK continue from
-// memory.  Used for the forward (CSR, per-row mean scale, GCN self term)
-// and for the gather-form backward (CSC, per-edge weights w_v, SAGE base =
-// the dH_dst row already in `out`, GCN base = w_u dA[u]).
-template <int RU, int EK, bool BWD>
-__global__ void __launch_bounds__(256) k_row_gather(const int32_t* __restrict__ ptr, const int32_t* __restrict__ idx,
-                                                    const float* __restrict__ wv, const int32_t* d_nrows,
-                                                    const int32_t* d_nself, const float* __restrict__ in, int32_t ldi,
-                                                    float* out, int32_t ldo, int32_t d, int32_t kind, int32_t aggr) {
-  const int n = *d_nrows;
-  const int nself = d_nself ? *d_nself : 0;
-  const int vec = (d + 3) >> 2, ldi4 = ldi >> 2, ldo4 = ldo >> 2;
-  const int lane = threadIdx.x & 31;
-  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int nwarps = (gridDim.x * blockDim.x) >> 5;
-  const float4* in4 = reinterpret_cast<const float4*>(in);
-  float4* out4 = reinterpret_cast<float4*>(out);
-  for (int base = warp * 32; base < n; base += nwarps * 32) {
-    const int row = base + lane;
-    const bool act = row < n;
-    const int beg = act ? ptr[row] : 0;
-    const int cnt = act ? ptr[row + 1] - beg : 0;
-    int e[EK];
-    float w[EK];
-#pragma unroll
-    for (int k = 0; k < EK; ++k) e[k] = k < cnt ? __ldg(idx + beg + k) : 0;
-#pragma unroll
-    for (int k = 0; k < EK; ++k) w[k] = BWD ? (k < cnt ? __ldg(wv + e[k]) : 0.f) : 1.f;
-    // forward: mean scale of the row; backward GCN: the self weight
-    float rs = 1.f;
-    if (!BWD && aggr == GNNV_AGGR_MEAN) {
-      const int denom = cnt + (kind == GNNV_KIND_GCN ? 1 : 0);
-      rs = denom ? 1.f / (float)denom : 0.f;
-    }
-    if (BWD && kind == GNNV_KIND_GCN) rs = (act && row < nself) ? __ldg(wv + row) : 0.f;
-    const int nrows = min(32, n - base);
-    for (int r0 = 0; r0 < nrows; r0 += RU) {
-      int cj[RU], bj[RU];
-      float sj[RU];
-#pragma unroll
-      for (int j = 0; j < RU; ++j) {
-        cj[j] = __shfl_sync(0xffffffffu, cnt, (r0 + j) & 31);
-        bj[j] = __shfl_sync(0xffffffffu, beg, (r0 + j) & 31);
-        sj[j] = __shfl_sync(0xffffffffu, rs, (r0 + j) & 31);
-        if (r0 + j >= nrows) cj[j] = -1;
-      }
-      int ej[RU][EK];
-      float wj[RU][EK];
-#pragma unroll
-      for (int j = 0; j < RU; ++j)
-#pragma unroll
-        for (int k = 0; k < EK; ++k) {
-          ej[j][k] = __shfl_sync(0xffffffffu, e[k], (r0 + j) & 31);
-          wj[j][k] = BWD ? __shfl_sync(0xffffffffu, w[k], (r0 + j) & 31) : 1.f;
-        }
-      for (int c = lane; c < ldo4; c += 32) {
-        const bool cv = c < vec;
-        float4 acc[RU];
-#pragma unroll
-        for (int j = 0; j < RU; ++j) {
-          acc[j] = make_float4(0.f, 0.f, 0.f, 0.f);
-          const int r = base + r0 + j;
-          if (cj[j] >= 0 && cv) {
-            if (!BWD && kind == GNNV_KIND_GCN) acc[j] = __ldg(in4 + (int64_t)r * ldi4 + c);
-            if (BWD && r < nself) {
-              if (kind == GNNV_KIND_GCN) acc[j] = f4scale(__ldg(in4 + (int64_t)r * ldi4 + c), sj[j]);
-              else acc[j] = out4[(int64_t)r * ldo4 + c];
-            }
-          }
-        }
-        float4 val[RU][EK];
-#pragma unroll
-        for (int j = 0; j < RU; ++j)
-#pragma unroll
-          for (int k = 0; k < EK; ++k)
-            val[j][k] = (k < cj[j] && cv) ? __ldg(in4 + (int64_t)ej[j][k] * ldi4 + c) : make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll
-        for (int j = 0; j < RU; ++j) {
-#pragma unroll
-          for (int k = 0; k < EK; ++k) {
-            if (k < cj[j]) {
-              acc[j].x = fmaf(wj[j][k], val[j][k].x, acc[j].x);
-              acc[j].y = fmaf(wj[j][k], val[j][k].y, acc[j].y);
-              acc[j].z = fmaf(wj[j][k], val[j][k].z, acc[j].z);
-              acc[j].w = fmaf(wj[j][k], val[j][k].w, acc[j].w);
-            }
-          }
-          for (int k = EK; k < cj[j]; ++k) {  // long lists
-            const int u = __ldg(idx + bj[j] + k);
-            const float ww = BWD ? __ldg(wv + u) : 1.f;
-            if (cv) {
-              const float4 g = __ldg(in4 + (int64_t)u * ldi4 + c);
-              acc[j].x = fmaf(ww, g.x, acc[j].x);
-              acc[j].y = fmaf(ww, g.y, acc[j].y);
-              acc[j].z = fmaf(ww, g.z, acc[j].z);
-              acc[j].w = fmaf(ww, g.w, acc[j].w);
-            }
-          }
-        }
-#pragma unroll
-        for (int j = 0; j < RU; ++j) {
-          if (cj[j] < 0) continue;
-          const int r = base + r0 + j;
-          float4 o = acc[j];
-          if (!BWD && aggr == GNNV_AGGR_MEAN) o = f4scale(o, sj[j]);
-          o = cv ? mask_tail(o, c, d) : make_float4(0.f, 0.f, 0.f, 0.f);
-          out4[(int64_t)r * ldo4 + c] = o;
-        }
-      }
-    }
-  }
-}
-
 size_t spmm_bwd_csc_scratch_bytes(int64_t max_dst, int64_t max_src, int64_t max_nnz) {
   const int64_t tiles = ceil_div(std::max<int64_t>(max_src, 1), kCscTile) + 1;
   return (size_t)(max_src * 4 + (max_src + 1) * 4 + max_nnz * 4 + max_dst * 4 + tiles * 8 + 256);
@@ -496,8 +372,17 @@ void launch_spmm_bwd_csc(const int32_t* d_indptr, const int32_t* d_indices, cons
   GNNV_CHECK_LAUNCH();
   k_csc_fill<<<sms * 8, 256, 0, s>>>(d_indptr, d_indices, d_ndst, colptr, colcnt, cscv);
   GNNV_CHECK_LAUNCH();
-  k_row_gather<4, 4, true><<<rowgather_grid(max_src), 256, 0, s>>>(colptr, cscv, wv, d_nsrc, d_ndst, dA, lda, dH,
-                                                                     ldh, d, kind, aggr);
+  const int vec = (ldh + 3) / 4;
+  if (vec <= 8) {
+    k_spmm_bwd_gather<8><<<spmm_grid(max_src, 4), 256, 0, s>>>(colptr, cscv, wv, d_ndst, d_nsrc, dA, lda, dH, ldh, d,
+                                                               kind);
+  } else if (vec <= 16) {
+    k_spmm_bwd_gather<16><<<spmm_grid(max_src, 2), 256, 0, s>>>(colptr, cscv, wv, d_ndst, d_nsrc, dA, lda, dH, ldh, d,
+                                                                kind);
+  } else {
+    k_spmm_bwd_gather<32><<<spmm_grid(max_src, 1), 256, 0, s>>>(colptr, cscv, wv, d_ndst, d_nsrc, dA, lda, dH, ldh, d,
+                                                                kind);
+  }
   GNNV_CHECK_LAUNCH();
 }
 
