@@ -49,6 +49,8 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-baseline-seeds", type=int, default=0, help="seeds in the oracle sample (0 = one batch)")
     p.add_argument("--ratio", type=float, default=None)
+    p.add_argument("--no-pipeline", action="store_true",
+                   help="disable the Eq.4 overlap of next-batch sample+gather with compute")
     return p.parse_args()
 
 
@@ -211,6 +213,8 @@ def algorithmic(seg: str, sizes, cfg, dims, stride, prec, peaks):
     L = len(cfg["fanouts"])
     n, nnz, U = sizes["n"], sizes["nnz"], sizes["U"]
     name, _, lay = seg.partition(".l")
+    if name.startswith("pf_"):  # the prefetch stream's sample / gather
+        name = name[3:]
     if name == "gather":
         rowb = stride * 4
         by = sizes["hits"] * rowb + n[L] * rowb + n[L] * 8
@@ -303,10 +307,35 @@ def main():
             lo, hi = 0, B
         return lo, hi
 
-    def step_device(t):
+    pipeline = not args.no_pipeline
+    pending = {"t": None}
+
+    def batch(t, host):
         lo, hi = seeds_of(t)
-        tr.step(d_perm[lo:hi].data_ptr(), hi - lo, max(hi - lo, global_batch(t, world, B, gd.n)), BASE_RNG_SEED + t, lr,
-                on_host=False, want_loss=False, stream=stream)
+        return (perm[lo:hi] if host else d_perm[lo:hi].data_ptr()), hi - lo
+
+    def run(t, host=False, want_loss=False):
+        """One step; with the Eq.4 pipeline the next batch's sample + gather
+        is enqueued on the side stream right after this step's compute."""
+        seeds, n = batch(t, host)
+        if pipeline and pending["t"] != t:
+            tr.prefetch(seeds, n, BASE_RNG_SEED + t, on_host=host, stream=stream)
+        tr.step(seeds, n, max(n, global_batch(t, world, B, gd.n)), BASE_RNG_SEED + t, lr, on_host=host,
+                want_loss=False, stream=stream)
+        pending["t"] = None
+        if pipeline:
+            s2, n2 = batch(t + 1, host)
+            tr.prefetch(s2, n2, BASE_RNG_SEED + t + 1, on_host=host, stream=stream)
+            pending["t"] = t + 1
+        return tr.read_loss(stream=stream) if want_loss else None
+
+    def drain():
+        if pending["t"] is not None:  # consume the trailing prefetch (untimed)
+            run(pending["t"])
+            torch.cuda.synchronize()
+
+    def step_device(t):
+        run(t)
 
     def barrier():
         if world > 1:
@@ -344,22 +373,22 @@ def main():
     ms_per_step = ms_total / args.steps
     value = world * B * args.steps / (ms_total / 1000.0)
     # ------------------------------------------------------- e2e (host I/O)
+    # host seeds copied in (inside the prefetch / step call) and the loss read
+    # back every step through the public API
+    drain()
     barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     t_e2e0 = time.perf_counter()
     e0.record(stream)
     loss = None
     for t in range(t0_steps, t0_steps + args.steps):
-        lo, hi = seeds_of(t)
-        host_seeds = perm[lo:hi]
-        loss, _ = tr.step(host_seeds, len(host_seeds), max(len(host_seeds), global_batch(t, world, B, gd.n)),
-                          BASE_RNG_SEED + t, lr, on_host=True,
-                          want_loss=True, stream=stream)
+        loss = run(t, host=True, want_loss=True)
     e1.record(stream)
     barrier()
     wall_e2e = time.perf_counter() - t_e2e0
     ms_e2e = max_over_ranks(e0.elapsed_time(e1))
     value_e2e = world * B * args.steps / (ms_e2e / 1000.0)
+    drain()
     # ------------------------------------------- sizes of the timed steps
     nsz = min(args.steps, 8)
     blk = gnnv.Blocks(g, B, cfg["fanouts"])
@@ -428,7 +457,8 @@ def main():
                        "hidden": cfg["hidden"], "gemm_precision": args.prec,
                        "l2": "inputs > L2 (feature table %.0f MB, gathered X %.0f MB per step)" % (
                            gd.n * gd.stride * 4 / 1e6, sizes["n"][L] * gd.stride * 4 / 1e6),
-                       "parallelism": f"dp{world}"},
+                       "parallelism": f"dp{world}",
+                       "pipeline": "eq4-overlap (next batch sample+gather on a side stream)" if pipeline else "off"},
             "epoch_s": iters_per_epoch * ms_per_step / 1000.0,
             "iters_per_epoch": iters_per_epoch,
             "clocks": clk,

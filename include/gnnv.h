@@ -327,6 +327,19 @@ typedef struct {
 } gnnv_segment;
 gnnv_status gnnv_trainer_timeline(gnnv_trainer* t, int32_t on);
 gnnv_status gnnv_trainer_timeline_read(gnnv_trainer* t, gnnv_segment* out, int32_t cap, int32_t* n_out);
+/* Eq.4 pipelining (T = n_iter max(t_sample + t_transfer,
+ * t_replace + t_compute)): enqueue the sampling and the gather of the NEXT
+ * step on the trainer's side stream, into a second buffer set, so that they
+ * overlap the current step's compute.  The next gnnv_step trains on this
+ * batch (its seeds/n_seeds/rng_seed must match; it waits for the prefetch on
+ * its stream).  At most one prefetch may be pending (else STATE).  The second
+ * buffer set is allocated on the first call (synchronises once). */
+gnnv_status gnnv_trainer_prefetch(gnnv_trainer* t, const int32_t* seeds, int32_t n_seeds, int32_t seeds_on_host,
+                                  uint64_t rng_seed, gnnv_stream s);
+/* Loss of the last step (summed over ranks) to the host; synchronises `s`
+ * and reports a pending seed error.  Lets a pipelined loop enqueue the next
+ * prefetch before blocking on the loss. */
+gnnv_status gnnv_trainer_read_loss(gnnv_trainer* t, float* loss_out, gnnv_stream s);
 /* Device counters of the last step's gather: int64[4] (see gnnv_gather). */
 gnnv_status gnnv_trainer_stats(gnnv_trainer* t, int64_t* host_stats4);
 

@@ -42,6 +42,22 @@ struct gnnv_trainer {
   int64_t* d_stats = nullptr;
   cudaEvent_t ev[8] = {nullptr};
   Timeline tl;
+  // Eq.4 pipeline: sample + gather of step t+1 on a side stream
+  // into the other buffer set while step t computes.  bb[cur] / X[cur] are
+  // the current step's blocks and gathered features (b == bb[cur], H[0] ==
+  // X[cur]).
+  gnnv_blocks* bb[2] = {nullptr, nullptr};
+  float* X[2] = {nullptr, nullptr};
+  int32_t* d_seedsb[2] = {nullptr, nullptr};
+  int32_t* h_seedsb[2] = {nullptr, nullptr};
+  int64_t* d_statsb[2] = {nullptr, nullptr};
+  int cur = 0;
+  bool pending = false;
+  int pend_n = 0;
+  uint64_t pend_rng = 0;
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_ready[2] = {nullptr, nullptr}, ev_free[2] = {nullptr, nullptr}, ev_in = nullptr;
+  Timeline tl_side;
 };
 
 static gnnv_layer_desc layer_desc(const gnnv_trainer* t, int i) {
@@ -61,22 +77,29 @@ extern "C" {
 gnnv_status gnnv_trainer_free(gnnv_trainer* t) {
   if (!t) return GNNV_OK;
   cudaSetDevice(t->g ? t->g->device : 0);
-  gnnv_blocks_free(t->b);
+  if (t->side) cudaStreamSynchronize(t->side);
+  for (int k = 0; k < 2; ++k) {
+    gnnv_blocks_free(t->bb[k]);
+    dfree(t->X[k]);
+    dfree(t->d_seedsb[k]);
+    if (t->h_seedsb[k]) cudaFreeHost(t->h_seedsb[k]);
+    dfree(t->d_statsb[k]);
+    if (t->ev_ready[k]) cudaEventDestroy(t->ev_ready[k]);
+    if (t->ev_free[k]) cudaEventDestroy(t->ev_free[k]);
+  }
+  if (t->ev_in) cudaEventDestroy(t->ev_in);
+  if (t->side) cudaStreamDestroy(t->side);
   dfree(t->d_params);
   dfree(t->d_grads);
-  dfree(t->d_seeds);
-  if (t->h_seeds) cudaFreeHost(t->h_seeds);
   if (t->h_out) cudaFreeHost(t->h_out);
   if (t->h_err) cudaFreeHost(t->h_err);
-  for (int i = 0; i <= GNNV_MAX_LAYERS; ++i) {
-    if (i > 0) dfree(t->H[i]);
+  for (int i = 1; i <= GNNV_MAX_LAYERS; ++i) {
+    dfree(t->H[i]);
     dfree(t->A[i]);
     dfree(t->G[i]);
   }
-  dfree(t->H[0]);
   dfree(t->loss_partial);
   dfree(t->loss_counter);
-  dfree(t->d_stats);
   for (auto& e : t->ev)
     if (e) cudaEventDestroy(e);
   delete t;
@@ -136,7 +159,19 @@ gnnv_status gnnv_trainer_create(gnnv_graph* g, gnnv_cache* c, const gnnv_model_d
       t->loss_counter = (unsigned int*)dmalloc(sizeof(unsigned int), "loss counter");
       GNNV_TRY_CUDA(cudaMemset(t->loss_counter, 0, sizeof(unsigned int)));
       t->d_stats = (int64_t*)dmalloc(4 * sizeof(int64_t), "gather stats");
+      GNNV_TRY_CUDA(cudaMemset(t->d_stats, 0, 4 * sizeof(int64_t)));
       for (auto& e : t->ev) GNNV_TRY_CUDA(cudaEventCreate(&e));
+      // buffer set 0; set 1 is allocated by the first gnnv_trainer_prefetch
+      t->bb[0] = t->b;
+      t->X[0] = t->H[0];
+      t->d_seedsb[0] = t->d_seeds;
+      t->h_seedsb[0] = t->h_seeds;
+      t->d_statsb[0] = t->d_stats;
+      for (int k = 0; k < 2; ++k) {
+        GNNV_TRY_CUDA(cudaEventCreateWithFlags(&t->ev_ready[k], cudaEventDisableTiming));
+        GNNV_TRY_CUDA(cudaEventCreateWithFlags(&t->ev_free[k], cudaEventDisableTiming));
+      }
+      GNNV_TRY_CUDA(cudaEventCreateWithFlags(&t->ev_in, cudaEventDisableTiming));
       GNNV_TRY_CUDA(cudaDeviceSynchronize());
     } catch (...) {
       gnnv_trainer_free(t);
@@ -181,7 +216,9 @@ gnnv_status gnnv_trainer_timeline(gnnv_trainer* t, int32_t on) {
     GNNV_REQUIRE(t, GNNV_ERR_PARAM, "trainer_timeline: null");
     GNNV_TRY_CUDA(cudaDeviceSynchronize());
     t->tl.clear();
+    t->tl_side.clear();
     t->tl.on = on != 0;
+    t->tl_side.on = on != 0;
   });
 }
 
@@ -190,25 +227,45 @@ gnnv_status gnnv_trainer_timeline_read(gnnv_trainer* t, gnnv_segment* out, int32
     GNNV_REQUIRE(t && n_out && (out || cap == 0), GNNV_ERR_PARAM, "trainer_timeline_read: null");
     GNNV_TRY_CUDA(cudaDeviceSynchronize());
     std::vector<gnnv_segment> segs;
-    auto& m = t->tl.marks;
-    for (size_t j = 0; j + 1 < m.size(); ++j) {
-      if (m[j].first == "end") continue;
-      float ms = 0.f;
-      GNNV_TRY_CUDA(cudaEventElapsedTime(&ms, m[j].second, m[j + 1].second));
-      size_t k = 0;
-      for (; k < segs.size(); ++k)
-        if (m[j].first == segs[k].name) break;
-      if (k == segs.size()) {
-        gnnv_segment sg{};
-        strncpy(sg.name, m[j].first.c_str(), sizeof(sg.name) - 1);
-        segs.push_back(sg);
+    // main-stream segments, then the prefetch stream's (pf_*): each timeline
+    // is a chain of consecutive marks on its own stream
+    for (Timeline* tlp : {&t->tl, &t->tl_side}) {
+      auto& m = tlp->marks;
+      for (size_t j = 0; j + 1 < m.size(); ++j) {
+        if (m[j].first == "end") continue;
+        float ms = 0.f;
+        GNNV_TRY_CUDA(cudaEventElapsedTime(&ms, m[j].second, m[j + 1].second));
+        size_t k = 0;
+        for (; k < segs.size(); ++k)
+          if (m[j].first == segs[k].name) break;
+        if (k == segs.size()) {
+          gnnv_segment sg{};
+          strncpy(sg.name, m[j].first.c_str(), sizeof(sg.name) - 1);
+          segs.push_back(sg);
+        }
+        segs[k].total_ms += ms;
+        segs[k].count += 1;
       }
-      segs[k].total_ms += ms;
-      segs[k].count += 1;
+      tlp->clear();
     }
-    t->tl.clear();
     *n_out = (int32_t)segs.size();
     for (int32_t i = 0; i < cap && i < (int32_t)segs.size(); ++i) out[i] = segs[i];
+  });
+}
+
+gnnv_status gnnv_trainer_read_loss(gnnv_trainer* t, float* loss_out, gnnv_stream stream) {
+  return guarded([&] {
+    GNNV_REQUIRE(t && loss_out, GNNV_ERR_PARAM, "read_loss: null");
+    cudaStream_t s = (cudaStream_t)stream;
+    const int L = t->md.L;
+    GNNV_TRY_CUDA(cudaMemcpyAsync(t->h_out, t->d_grads + t->nparams, sizeof(float), cudaMemcpyDeviceToHost, s));
+    GNNV_TRY_CUDA(cudaMemcpyAsync(t->h_err, t->b->d_sizes + 2 * L + 1, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    GNNV_TRY_CUDA(cudaStreamSynchronize(s));
+    *loss_out = t->h_out[0];
+    if (t->h_err[0]) {
+      GNNV_TRY_CUDA(cudaMemsetAsync(t->b->d_sizes + 2 * L + 1, 0, sizeof(int32_t), s));
+      throw Error{GNNV_ERR_PARAM, "step: repeated or out-of-range seed id"};
+    }
   });
 }
 
@@ -220,6 +277,71 @@ gnnv_status gnnv_trainer_stats(gnnv_trainer* t, int64_t* host_stats4) {
   });
 }
 
+static void select_buffers(gnnv_trainer* t, int k) {
+  t->cur = k;
+  t->b = t->bb[k];
+  t->H[0] = t->X[k];
+  t->d_seeds = t->d_seedsb[k];
+  t->h_seeds = t->h_seedsb[k];
+  t->d_stats = t->d_statsb[k];
+}
+
+// Stage host seeds (validated) or take device seeds; returns device pointer.
+static const int32_t* stage_seeds(gnnv_trainer* t, int k, const int32_t* seeds, int32_t n_seeds, int32_t on_host,
+                                  cudaStream_t s, Timeline* tl) {
+  if (!on_host) return seeds;
+  for (int i = 0; i < n_seeds; ++i)
+    GNNV_REQUIRE(seeds[i] >= 0 && seeds[i] < t->g->n, GNNV_ERR_PARAM, "step: seed id outside [0, N)");
+  // the staging buffer may still feed a previous copy on this stream
+  GNNV_TRY_CUDA(cudaStreamSynchronize(s));
+  memcpy(t->h_seedsb[k], seeds, n_seeds * sizeof(int32_t));
+  if (tl) tl->mark(s, "h2d_seeds");
+  GNNV_TRY_CUDA(
+      cudaMemcpyAsync(t->d_seedsb[k], t->h_seedsb[k], n_seeds * sizeof(int32_t), cudaMemcpyHostToDevice, s));
+  return t->d_seedsb[k];
+}
+
+gnnv_status gnnv_trainer_prefetch(gnnv_trainer* t, const int32_t* seeds, int32_t n_seeds, int32_t seeds_on_host,
+                                  uint64_t rng_seed, gnnv_stream stream) {
+  return guarded([&] {
+    GNNV_REQUIRE(t && seeds, GNNV_ERR_PARAM, "prefetch: null");
+    GNNV_REQUIRE(!t->pending, GNNV_ERR_STATE, "prefetch: a prefetched batch is already pending");
+    GNNV_REQUIRE(n_seeds >= 1 && n_seeds <= t->md.max_seeds, GNNV_ERR_PARAM,
+                 "prefetch: n_seeds must be in [1, max_seeds]");
+    gnnv_graph* g = t->g;
+    const int k = t->cur ^ 1;
+    if (!t->bb[k]) {  // first use: the second buffer set
+      GNNV_TRY_CUDA(cudaDeviceSynchronize());
+      gnnv_status st = gnnv_blocks_create(g, t->md.max_seeds, t->md.fanouts, t->md.L, &t->bb[k]);
+      if (st != GNNV_OK) throw Error{st, get_error()};
+      t->X[k] = (float*)dmalloc((size_t)t->bb[k]->max_n[t->md.L] * g->stride * sizeof(float), "X (prefetch)");
+      t->d_seedsb[k] = (int32_t*)dmalloc(t->md.max_seeds * sizeof(int32_t), "seeds (prefetch)");
+      GNNV_TRY_CUDA(cudaMallocHost(&t->h_seedsb[k], t->md.max_seeds * sizeof(int32_t)));
+      t->d_statsb[k] = (int64_t*)dmalloc(4 * sizeof(int64_t), "gather stats (prefetch)");
+      if (!t->side) GNNV_TRY_CUDA(cudaStreamCreateWithFlags(&t->side, cudaStreamNonBlocking));
+    }
+    cudaStream_t s = (cudaStream_t)stream;
+    // order after the caller's stream (device seeds) and after the step
+    // that last computed on buffer set k
+    GNNV_TRY_CUDA(cudaEventRecord(t->ev_in, s));
+    GNNV_TRY_CUDA(cudaStreamWaitEvent(t->side, t->ev_in, 0));
+    GNNV_TRY_CUDA(cudaStreamWaitEvent(t->side, t->ev_free[k], 0));
+    Timeline* tl = t->tl.on ? &t->tl_side : nullptr;
+    const int32_t* d_seeds = stage_seeds(t, k, seeds, n_seeds, seeds_on_host, t->side, tl);
+    if (tl) tl->mark(t->side, "pf_sample");
+    launch_sample(g, t->bb[k], d_seeds, n_seeds, rng_seed, t->side);
+    t->bb[k]->sampled = true;
+    GNNV_TRY_CUDA(cudaMemsetAsync(t->d_statsb[k], 0, 4 * sizeof(int64_t), t->side));
+    if (tl) tl->mark(t->side, "pf_gather");
+    launch_gather(t->c, t->bb[k], t->X[k], t->d_statsb[k], t->side);
+    if (tl) tl->mark(t->side, "end");
+    GNNV_TRY_CUDA(cudaEventRecord(t->ev_ready[k], t->side));
+    t->pending = true;
+    t->pend_n = n_seeds;
+    t->pend_rng = rng_seed;
+  });
+}
+
 gnnv_status gnnv_step(gnnv_trainer* t, const int32_t* seeds, int32_t n_seeds, int32_t seeds_on_host, int32_t n_global,
                       uint64_t rng_seed, float lr, float* loss_out, gnnv_step_timing* tm, gnnv_stream stream) {
   return guarded([&] {
@@ -227,30 +349,32 @@ gnnv_status gnnv_step(gnnv_trainer* t, const int32_t* seeds, int32_t n_seeds, in
     GNNV_REQUIRE(n_seeds >= 1 && n_seeds <= t->md.max_seeds, GNNV_ERR_PARAM, "step: n_seeds must be in [1, max_seeds]");
     GNNV_REQUIRE(n_global >= n_seeds, GNNV_ERR_PARAM, "step: n_global must be >= n_seeds");
     cudaStream_t s = (cudaStream_t)stream;
-    gnnv_blocks* b = t->b;
     gnnv_graph* g = t->g;
     const int L = t->md.L;
     Timeline* tl = t->tl.on ? &t->tl : nullptr;
     if (tm) GNNV_TRY_CUDA(cudaEventRecord(t->ev[0], s));
-    const int32_t* d_seeds = seeds;
-    if (seeds_on_host) {
-      for (int i = 0; i < n_seeds; ++i)
-        GNNV_REQUIRE(seeds[i] >= 0 && seeds[i] < g->n, GNNV_ERR_PARAM, "step: seed id outside [0, N)");
-      // the staging buffer may still feed the previous step's copy
-      GNNV_TRY_CUDA(cudaStreamSynchronize(s));
-      memcpy(t->h_seeds, seeds, n_seeds * sizeof(int32_t));
-      if (tl) tl->mark(s, "h2d_seeds");
-      GNNV_TRY_CUDA(cudaMemcpyAsync(t->d_seeds, t->h_seeds, n_seeds * sizeof(int32_t), cudaMemcpyHostToDevice, s));
-      d_seeds = t->d_seeds;
+    if (t->pending) {
+      // the batch was sampled and gathered by gnnv_trainer_prefetch
+      GNNV_REQUIRE(n_seeds == t->pend_n && rng_seed == t->pend_rng, GNNV_ERR_STATE,
+                   "step: seeds/rng_seed differ from the pending prefetch");
+      select_buffers(t, t->cur ^ 1);
+      t->pending = false;
+      if (tl) tl->mark(s, "wait_prefetch");
+      GNNV_TRY_CUDA(cudaStreamWaitEvent(s, t->ev_ready[t->cur], 0));
+      if (tm) GNNV_TRY_CUDA(cudaEventRecord(t->ev[1], s));
+      if (tm) GNNV_TRY_CUDA(cudaEventRecord(t->ev[2], s));
+    } else {
+      const int32_t* d_seeds = stage_seeds(t, t->cur, seeds, n_seeds, seeds_on_host, s, tl);
+      if (tl) tl->mark(s, "sample");
+      launch_sample(g, t->b, d_seeds, n_seeds, rng_seed, s);
+      t->b->sampled = true;
+      GNNV_TRY_CUDA(cudaMemsetAsync(t->d_stats, 0, 4 * sizeof(int64_t), s));
+      if (tm) GNNV_TRY_CUDA(cudaEventRecord(t->ev[1], s));
+      if (tl) tl->mark(s, "gather");
+      launch_gather(t->c, t->b, t->H[0], t->d_stats, s);
+      if (tm) GNNV_TRY_CUDA(cudaEventRecord(t->ev[2], s));
     }
-    if (tl) tl->mark(s, "sample");
-    launch_sample(g, b, d_seeds, n_seeds, rng_seed, s);
-    b->sampled = true;
-    GNNV_TRY_CUDA(cudaMemsetAsync(t->d_stats, 0, 4 * sizeof(int64_t), s));
-    if (tm) GNNV_TRY_CUDA(cudaEventRecord(t->ev[1], s));
-    if (tl) tl->mark(s, "gather");
-    launch_gather(t->c, b, t->H[0], t->d_stats, s);
-    if (tm) GNNV_TRY_CUDA(cudaEventRecord(t->ev[2], s));
+    gnnv_blocks* b = t->b;
     for (int i = 1; i <= L; ++i) {
       const gnnv_layer_desc ld = layer_desc(t, i);
       layer_fwd_impl(b, i, &ld, t->H[i - 1], t->d_params + t->w_off[i - 1], t->d_params + t->b_off[i - 1], t->H[i],
@@ -277,6 +401,7 @@ gnnv_status gnnv_step(gnnv_trainer* t, const int32_t* seeds, int32_t n_seeds, in
     if (tl) tl->mark(s, "sgd");
     launch_sgd(t->d_params, t->d_grads, t->nparams, lr, s);
     if (tl) tl->mark(s, "end");
+    GNNV_TRY_CUDA(cudaEventRecord(t->ev_free[t->cur], s));  // buffer set may be refilled
     if (tm) GNNV_TRY_CUDA(cudaEventRecord(t->ev[7], s));
     if (loss_out || tm) {
       GNNV_TRY_CUDA(cudaMemcpyAsync(t->h_out, d_loss, sizeof(float), cudaMemcpyDeviceToHost, s));

@@ -116,6 +116,8 @@ _SIGS = {
     "gnnv_trainer_activation": (I32, [VP, I32, PP, C.POINTER(I32)]),
     "gnnv_step": (I32, [VP, VP, I32, I32, I32, U64, F32, C.POINTER(F32), C.POINTER(StepTiming), VP]),
     "gnnv_trainer_stats": (I32, [VP, VP]),
+    "gnnv_trainer_prefetch": (I32, [VP, VP, I32, I32, U64, VP]),
+    "gnnv_trainer_read_loss": (I32, [VP, C.POINTER(F32), VP]),
     "gnnv_trainer_timeline": (I32, [VP, I32]),
     "gnnv_trainer_timeline_read": (I32, [VP, C.POINTER(Segment), I32, C.POINTER(I32)]),
 }
@@ -416,6 +418,18 @@ class Trainer:
                                 C.byref(loss) if want_loss else None, C.byref(tm) if timing else None,
                                 stream_ptr(stream)))
         return (float(loss.value) if want_loss else None), (tm.as_dict() if timing else None)
+
+    def prefetch(self, seeds, n_seeds: int, rng_seed: int, on_host: bool = True, stream=None):
+        """Sample + gather the next step's batch on the side stream (Eq.4 overlap)."""
+        if on_host:
+            seeds = np.ascontiguousarray(seeds, dtype=np.int32)
+        _check(load().gnnv_trainer_prefetch(self.h, ptr(seeds), int(n_seeds), 1 if on_host else 0,
+                                            int(rng_seed) & 0xFFFFFFFFFFFFFFFF, stream_ptr(stream)))
+
+    def read_loss(self, stream=None) -> float:
+        out = C.c_float(0.0)
+        _check(load().gnnv_trainer_read_loss(self.h, C.byref(out), stream_ptr(stream)))
+        return float(out.value)
 
     def params(self) -> np.ndarray:
         out = np.empty(self.nparams, np.float32)

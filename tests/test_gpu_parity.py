@@ -399,3 +399,33 @@ def test_layer_shapes(mini, prec, d_in, d_out, kind):
     gx = Gsrc.cpu().numpy()
     assert_close_cond(gx[:, :d_in], rX, mX, rtol, "dHsrc")
     assert (gx[:, d_in:] == 0).all()
+
+
+def test_pipelined_steps_match_sequential(mini):
+    """Eq.4 pipeline: prefetching sample+gather of step t+1 on the side stream
+    changes nothing in the results (losses bitwise, parameters to fp32
+    rounding of the atomic backward)."""
+    gd, g = mini
+    cfg = CONFIGS["mini"]
+    dims = [gd.d, cfg["hidden"], cfg["hidden"], gd.C]
+    w = init_weights(dims)
+    cache = gnnv.Cache(g, cfg["ratio"])
+    B = cfg["batch"]
+    perm = epoch_seeds(gd.n, 0)
+    batches = [perm[i * B:(i + 1) * B] for i in range(5)]
+    seq = gnnv.Trainer(g, cache, dims, cfg["fanouts"], B, w, prec=2)
+    l_seq = [seq.step(bt, B, B, 100 + i, 0.05)[0] for i, bt in enumerate(batches)]
+    pip = gnnv.Trainer(g, cache, dims, cfg["fanouts"], B, w, prec=2)
+    pip.prefetch(batches[0], B, 100)
+    l_pip = []
+    for i, bt in enumerate(batches):
+        pip.step(bt, B, B, 100 + i, 0.05, want_loss=False)
+        if i + 1 < len(batches):
+            pip.prefetch(batches[i + 1], B, 101 + i)
+        l_pip.append(pip.read_loss())
+    assert l_seq[0] == l_pip[0]
+    np.testing.assert_allclose(l_pip, l_seq, rtol=1e-5)
+    assert normwise(pip.params(), seq.params()) < 1e-5
+    with pytest.raises(gnnv.GnnvError):  # one pending prefetch at a time
+        pip.prefetch(batches[0], B, 7)
+        pip.prefetch(batches[1], B, 8)
