@@ -314,7 +314,7 @@ def main():
         lo, hi = seeds_of(t)
         return (perm[lo:hi] if host else d_perm[lo:hi].data_ptr()), hi - lo
 
-    def run(t, host=False, want_loss=False):
+    def run(t, host=False, want_loss=False, prefetch_next=True):
         """One step; with the Eq.4 pipeline the next batch's sample + gather
         is enqueued on the side stream right after this step's compute."""
         seeds, n = batch(t, host)
@@ -323,7 +323,7 @@ def main():
         tr.step(seeds, n, max(n, global_batch(t, world, B, gd.n)), BASE_RNG_SEED + t, lr, on_host=host,
                 want_loss=False, stream=stream)
         pending["t"] = None
-        if pipeline:
+        if pipeline and prefetch_next:
             s2, n2 = batch(t + 1, host)
             tr.prefetch(s2, n2, BASE_RNG_SEED + t + 1, on_host=host, stream=stream)
             pending["t"] = t + 1
@@ -331,7 +331,7 @@ def main():
 
     def drain():
         if pending["t"] is not None:  # consume the trailing prefetch (untimed)
-            run(pending["t"])
+            run(pending["t"], prefetch_next=False)
             torch.cuda.synchronize()
 
     def step_device(t):
