@@ -309,6 +309,9 @@ def main():
 
     pipeline = not args.no_pipeline
     pending = {"t": None}
+    # device seeds live in d_perm (ready before the loop): the prefetch is
+    # ordered after this idle stream, not after the step in flight
+    pf_stream = torch.cuda.Stream()
 
     def batch(t, host):
         lo, hi = seeds_of(t)
@@ -319,13 +322,13 @@ def main():
         is enqueued on the side stream right after this step's compute."""
         seeds, n = batch(t, host)
         if pipeline and pending["t"] != t:
-            tr.prefetch(seeds, n, BASE_RNG_SEED + t, on_host=host, stream=stream)
+            tr.prefetch(seeds, n, BASE_RNG_SEED + t, on_host=host, stream=pf_stream)
         tr.step(seeds, n, max(n, global_batch(t, world, B, gd.n)), BASE_RNG_SEED + t, lr, on_host=host,
                 want_loss=False, stream=stream)
         pending["t"] = None
         if pipeline and prefetch_next:
             s2, n2 = batch(t + 1, host)
-            tr.prefetch(s2, n2, BASE_RNG_SEED + t + 1, on_host=host, stream=stream)
+            tr.prefetch(s2, n2, BASE_RNG_SEED + t + 1, on_host=host, stream=pf_stream)
             pending["t"] = t + 1
         return tr.read_loss(stream=stream) if want_loss else None
 

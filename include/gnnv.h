@@ -333,7 +333,13 @@ gnnv_status gnnv_trainer_timeline_read(gnnv_trainer* t, gnnv_segment* out, int32
  * overlap the current step's compute.  The next gnnv_step trains on this
  * batch (its seeds/n_seeds/rng_seed must match; it waits for the prefetch on
  * its stream).  At most one prefetch may be pending (else STATE).  The second
- * buffer set is allocated on the first call (synchronises once). */
+ * buffer set is allocated on the first call (synchronises once).
+ * Ordering: the prefetch waits for the step that last used its buffer set
+ * (two steps back) and, for DEVICE seeds, for the work already enqueued on
+ * `s` -- pass the stream that produced the seeds, not the step stream, or the
+ * prefetch serialises behind the step in flight.  HOST seeds are copied to a
+ * pinned staging buffer (the host waits only for the previous copy out of
+ * that buffer) and impose no stream dependency. */
 gnnv_status gnnv_trainer_prefetch(gnnv_trainer* t, const int32_t* seeds, int32_t n_seeds, int32_t seeds_on_host,
                                   uint64_t rng_seed, gnnv_stream s);
 /* Loss of the last step (summed over ranks) to the host; synchronises `s`

@@ -57,6 +57,8 @@ struct gnnv_trainer {
   uint64_t pend_rng = 0;
   cudaStream_t side = nullptr;
   cudaEvent_t ev_ready[2] = {nullptr, nullptr}, ev_free[2] = {nullptr, nullptr}, ev_in = nullptr;
+  cudaEvent_t ev_h2d[2] = {nullptr, nullptr};  // last copy out of h_seedsb[k]
+  bool h2d_used[2] = {false, false};
   Timeline tl_side;
 };
 
@@ -86,6 +88,7 @@ gnnv_status gnnv_trainer_free(gnnv_trainer* t) {
     dfree(t->d_statsb[k]);
     if (t->ev_ready[k]) cudaEventDestroy(t->ev_ready[k]);
     if (t->ev_free[k]) cudaEventDestroy(t->ev_free[k]);
+    if (t->ev_h2d[k]) cudaEventDestroy(t->ev_h2d[k]);
   }
   if (t->ev_in) cudaEventDestroy(t->ev_in);
   if (t->side) cudaStreamDestroy(t->side);
@@ -170,6 +173,7 @@ gnnv_status gnnv_trainer_create(gnnv_graph* g, gnnv_cache* c, const gnnv_model_d
       for (int k = 0; k < 2; ++k) {
         GNNV_TRY_CUDA(cudaEventCreateWithFlags(&t->ev_ready[k], cudaEventDisableTiming));
         GNNV_TRY_CUDA(cudaEventCreateWithFlags(&t->ev_free[k], cudaEventDisableTiming));
+        GNNV_TRY_CUDA(cudaEventCreateWithFlags(&t->ev_h2d[k], cudaEventDisableTiming));
       }
       GNNV_TRY_CUDA(cudaEventCreateWithFlags(&t->ev_in, cudaEventDisableTiming));
       GNNV_TRY_CUDA(cudaDeviceSynchronize());
@@ -292,12 +296,16 @@ static const int32_t* stage_seeds(gnnv_trainer* t, int k, const int32_t* seeds, 
   if (!on_host) return seeds;
   for (int i = 0; i < n_seeds; ++i)
     GNNV_REQUIRE(seeds[i] >= 0 && seeds[i] < t->g->n, GNNV_ERR_PARAM, "step: seed id outside [0, N)");
-  // the staging buffer may still feed a previous copy on this stream
-  GNNV_TRY_CUDA(cudaStreamSynchronize(s));
+  // the staging buffer may still feed the previous copy out of it; wait for
+  // that copy only (not for the stream), so a prefetch never blocks the host
+  // on the step in flight
+  if (t->h2d_used[k]) GNNV_TRY_CUDA(cudaEventSynchronize(t->ev_h2d[k]));
   memcpy(t->h_seedsb[k], seeds, n_seeds * sizeof(int32_t));
   if (tl) tl->mark(s, "h2d_seeds");
   GNNV_TRY_CUDA(
       cudaMemcpyAsync(t->d_seedsb[k], t->h_seedsb[k], n_seeds * sizeof(int32_t), cudaMemcpyHostToDevice, s));
+  GNNV_TRY_CUDA(cudaEventRecord(t->ev_h2d[k], s));
+  t->h2d_used[k] = true;
   return t->d_seedsb[k];
 }
 
@@ -321,10 +329,15 @@ gnnv_status gnnv_trainer_prefetch(gnnv_trainer* t, const int32_t* seeds, int32_t
       if (!t->side) GNNV_TRY_CUDA(cudaStreamCreateWithFlags(&t->side, cudaStreamNonBlocking));
     }
     cudaStream_t s = (cudaStream_t)stream;
-    // order after the caller's stream (device seeds) and after the step
-    // that last computed on buffer set k
-    GNNV_TRY_CUDA(cudaEventRecord(t->ev_in, s));
-    GNNV_TRY_CUDA(cudaStreamWaitEvent(t->side, t->ev_in, 0));
+    // order after the step that last computed on buffer set k and, for
+    // device seeds, after the work already enqueued on the caller's stream
+    // (pass the stream that produced the seeds, not the step stream, to let
+    // the prefetch overlap the step in flight).  Host seeds carry no device
+    // dependency.
+    if (!seeds_on_host) {
+      GNNV_TRY_CUDA(cudaEventRecord(t->ev_in, s));
+      GNNV_TRY_CUDA(cudaStreamWaitEvent(t->side, t->ev_in, 0));
+    }
     GNNV_TRY_CUDA(cudaStreamWaitEvent(t->side, t->ev_free[k], 0));
     Timeline* tl = t->tl.on ? &t->tl_side : nullptr;
     const int32_t* d_seeds = stage_seeds(t, k, seeds, n_seeds, seeds_on_host, t->side, tl);

@@ -429,3 +429,22 @@ def test_pipelined_steps_match_sequential(mini):
     with pytest.raises(gnnv.GnnvError):  # one pending prefetch at a time
         pip.prefetch(batches[0], B, 7)
         pip.prefetch(batches[1], B, 8)
+
+    # device seeds, prefetches ordered on their own stream, no host sync
+    # between steps: the overlapped schedule still yields the same losses
+    import torch
+    dev = torch.as_tensor(np.concatenate(batches)).cuda()
+    torch.cuda.synchronize()
+    pf = torch.cuda.Stream()
+    main = torch.cuda.current_stream()
+    dv = gnnv.Trainer(g, cache, dims, cfg["fanouts"], B, w, prec=2)
+    losses = []
+    dv.prefetch(dev[0:B].data_ptr(), B, 100, on_host=False, stream=pf)
+    for i in range(len(batches)):
+        dv.step(dev[i * B:(i + 1) * B].data_ptr(), B, B, 100 + i, 0.05, on_host=False, want_loss=False,
+                stream=main)
+        if i + 1 < len(batches):
+            dv.prefetch(dev[(i + 1) * B:(i + 2) * B].data_ptr(), B, 101 + i, on_host=False, stream=pf)
+        losses.append(dv.read_loss(stream=main))
+    np.testing.assert_allclose(losses, l_seq, rtol=1e-5)
+    assert normwise(dv.params(), seq.params()) < 1e-5
