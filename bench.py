@@ -292,7 +292,10 @@ def main():
     w = init_weights(dims, kind=args.kind)
     B = cfg["batch"]
     tr = gnnv.Trainer(g, cache, dims, cfg["fanouts"], B, w, kind=kind, prec=prec, comm=comm)
-    stream = torch.cuda.current_stream()
+    # the step runs on a high-priority stream; the trainer's prefetch stream
+    # has the lowest priority (Eq.4 overlap without delaying the step)
+    stream = torch.cuda.Stream(priority=-1)
+    torch.cuda.set_stream(stream)
     lr = 0.01
     # seeds of global iteration t: perm[t*G*B:(t+1)*G*B], rank r takes the r-th B-slice
     from paper_2404_09544_b200.partition import global_batch, iters_per_epoch as _ipe, rank_slice
@@ -424,6 +427,9 @@ def main():
     seg_ms = {k: v[0] / max(1, v[1]) for k, v in segs.items()}
     seg_tot = {k: v[0] for k, v in segs.items()}
     ranked = sorted(seg_tot.items(), key=lambda kv: -kv[1])
+    # main-stream segments tile the step; pf_* run on the side stream,
+    # overlapped with them (Eq.4), so they are not on the critical path
+    main_tot = sum(v for k, v in seg_tot.items() if not k.startswith("pf_"))
     roofline = None
     rooflines = {}
     for name, tot in ranked:
@@ -435,10 +441,12 @@ def main():
         achieved = amount / (avg_ms / 1000.0) / (1e9 if unit == "GB/s" else 1e12)
         r = {"kernel": name, "bound": bound, "achieved": achieved, "peak": peak, "unit": unit,
              "frac": achieved / peak, "traffic": None, "avg_ms": avg_ms,
-             "share_of_step": tot / max(1e-9, sum(seg_tot.values())),
+             "share_of_step": tot / max(1e-9, main_tot),
              "algorithmic_per_launch": amount}
+        if name.startswith("pf_"):
+            r["overlapped"] = True
         rooflines[name] = r
-        if roofline is None:
+        if roofline is None and not name.startswith("pf_"):
             roofline = r
     # -------------------------------------------------------- CPU baseline
     cpu = None

@@ -298,8 +298,12 @@ int64_t gnnv_trainer_num_params(const gnnv_trainer* t);
 /* Copies params (and grads of the last step, if d_grads_out/host) to host; synchronises. */
 gnnv_status gnnv_trainer_get(gnnv_trainer* t, float* host_params, float* host_grads);
 gnnv_status gnnv_trainer_set_params(gnnv_trainer* t, const float* host_params);
+/* Blocks of the last step (borrowed, do not free).  With gnnv_trainer_prefetch
+ * the trainer alternates between two buffer sets, so query again after every
+ * step. */
 gnnv_blocks* gnnv_trainer_blocks(gnnv_trainer* t);
-/* Device pointers of the trainer's activations for layer i (0 = X). */
+/* Device pointers of the trainer's activations for layer i (0 = X) of the
+ * last step (same buffer-set caveat). */
 gnnv_status gnnv_trainer_activation(gnnv_trainer* t, int32_t i, const float** d_H, int32_t* stride);
 
 /* One iteration of Algorithm 1 on this rank's seed slice:

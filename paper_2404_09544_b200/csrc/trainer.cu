@@ -326,7 +326,13 @@ gnnv_status gnnv_trainer_prefetch(gnnv_trainer* t, const int32_t* seeds, int32_t
       t->d_seedsb[k] = (int32_t*)dmalloc(t->md.max_seeds * sizeof(int32_t), "seeds (prefetch)");
       GNNV_TRY_CUDA(cudaMallocHost(&t->h_seedsb[k], t->md.max_seeds * sizeof(int32_t)));
       t->d_statsb[k] = (int64_t*)dmalloc(4 * sizeof(int64_t), "gather stats (prefetch)");
-      if (!t->side) GNNV_TRY_CUDA(cudaStreamCreateWithFlags(&t->side, cudaStreamNonBlocking));
+      if (!t->side) {
+        // lowest priority: the prefetch fills the SMs the step leaves idle
+        // instead of delaying the step's (often small-grid) kernels
+        int lo = 0, hi = 0;
+        GNNV_TRY_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+        GNNV_TRY_CUDA(cudaStreamCreateWithPriority(&t->side, cudaStreamNonBlocking, lo));
+      }
     }
     cudaStream_t s = (cudaStream_t)stream;
     // order after the step that last computed on buffer set k and, for

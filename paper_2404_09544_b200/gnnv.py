@@ -405,7 +405,13 @@ class Trainer:
                                           C.byref(h)))
         self.h, self.g, self.cache, self.comm = h, g, cache, comm
         self.nparams = int(load().gnnv_trainer_num_params(h))
-        self.blocks = Blocks(g, max_seeds, fanouts, h=C.c_void_p(load().gnnv_trainer_blocks(h)))
+        self._max_seeds, self._fanouts = max_seeds, list(fanouts)
+
+    @property
+    def blocks(self) -> "Blocks":
+        """The blocks of the last step (borrowed; with the Eq.4 prefetch the
+        trainer alternates between two buffer sets)."""
+        return Blocks(self.g, self._max_seeds, self._fanouts, h=C.c_void_p(load().gnnv_trainer_blocks(self.h)))
 
     def step(self, seeds, n_seeds: int, n_global: int, rng_seed: int, lr: float, on_host: bool = True,
              want_loss: bool = True, timing: bool = False, stream=None):
