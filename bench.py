@@ -230,7 +230,10 @@ def algorithmic(seg: str, sizes, cfg, dims, stride, prec, peaks):
         by = U[h] * d_in * 4 + n[h] * ((d_in + 3) & ~3) * 4 + nnz[h] * 4 + (n[h] + 1) * 4
         return "hbm", by, "GB/s", peaks["hbm"]
     if name == "spmm_bwd":
-        by = n[h] * d_in * 4 + 2 * U[h] * d_in * 4 + nnz[h] * 4 + n[h + 1] * ((d_in + 3) & ~3) * 4
+        # dA read, block CSR + owner masks read, every dH_src row written once,
+        # and the n_dst rows the dX GEMM wrote read back for accumulation
+        ld = (d_in + 3) & ~3
+        by = n[h] * d_in * 4 + nnz[h] * 4 + (n[h] + 1) * 8 + n[h + 1] * ld * 4 + n[h] * ld * 4
         return "hbm", by, "GB/s", peaks["hbm"]
     if name == "relu_mask":
         return "hbm", 3 * n[h] * ((d_out + 3) & ~3) * 4, "GB/s", peaks["hbm"]

@@ -284,6 +284,7 @@ gnnv_status gnnv_blocks_create(gnnv_graph* g, int32_t max_seeds, const int32_t* 
       for (int h = 0; h < L; ++h) {
         b->d_indptr[h] = (int32_t*)dmalloc((b->max_n[h] + 1) * sizeof(int32_t), "block indptr");
         b->d_indices[h] = (int32_t*)dmalloc(std::max<int64_t>(b->max_nnz[h], 1) * sizeof(int32_t), "block indices");
+        b->d_own[h] = (uint32_t*)dmalloc(b->max_n[h] * sizeof(uint32_t), "block owner masks");
       }
       b->d_sizes = (int32_t*)dmalloc((2 * L + 2) * sizeof(int32_t), "sizes");
       GNNV_TRY_CUDA(cudaMemset(b->d_sizes, 0, (2 * L + 2) * sizeof(int32_t)));
@@ -307,6 +308,7 @@ gnnv_status gnnv_blocks_free(gnnv_blocks* b) {
   for (int h = 0; h < GNNV_MAX_LAYERS; ++h) {
     dfree(b->d_indptr[h]);
     dfree(b->d_indices[h]);
+    dfree(b->d_own[h]);
   }
   dfree(b->d_sizes);
   dfree(b->d_scan);

@@ -117,6 +117,7 @@ struct gnnv_blocks {
   int32_t* d_sizes = nullptr;     // [2L+1] + error flag
   unsigned long long* d_scan = nullptr;  // chained-scan status [1 + max tiles]
   int64_t scan_words = 0;
+  uint32_t* d_own[GNNV_MAX_LAYERS] = {nullptr};  // [max_n[h]] owner-edge bit mask per dst row
   bool sampled = false;
   // scratch arena for the layer kernels (grows on demand)
   void* scratch = nullptr;
@@ -164,15 +165,10 @@ void launch_gather(const gnnv_cache* c, const gnnv_blocks* b, float* d_X, int64_
 void launch_spmm_fwd(const int32_t* d_indptr, const int32_t* d_indices, const int32_t* d_ndst, int64_t max_dst,
                      const float* H, int32_t ldh, float* A, int32_t lda, int32_t d, int32_t kind, int32_t aggr,
                      cudaStream_t s);
-void launch_spmm_bwd(const int32_t* d_indptr, const int32_t* d_indices, const int32_t* d_ndst, int64_t max_dst,
-                     const float* dA, int32_t lda, float* dH, int32_t ldh, int32_t d, int32_t kind, int32_t aggr,
-                     cudaStream_t s);
-size_t spmm_bwd_csc_scratch_bytes(int64_t max_dst, int64_t max_src, int64_t max_nnz);
-void launch_spmm_bwd_csc(const int32_t* d_indptr, const int32_t* d_indices, const int32_t* d_ndst, const int32_t* d_nsrc,
-                         int64_t max_dst, int64_t max_src, int64_t max_nnz, const float* dA, int32_t lda, float* dH,
-                         int32_t ldh, int32_t d, int32_t kind, int32_t aggr, void* scratch, cudaStream_t s);
-void launch_rows_zero(float* X, int32_t ld, const int32_t* d_row_begin, const int32_t* d_row_end, int64_t max_rows,
-                      cudaStream_t s);
+void launch_spmm_bwd(const int32_t* d_indptr, const int32_t* d_indices, const uint32_t* d_own, const int32_t* d_ndst,
+                     int64_t max_dst, const float* dA, int32_t lda, float* dH, int32_t ldh, int32_t d, int32_t kind,
+                     int32_t aggr, cudaStream_t s);
+void launch_colsum_reduce(const float* partial, int blocks, int ld, int N, float* out, cudaStream_t s);
 // gemm
 struct GemmFwdArgs {
   const float* X1; int32_t ld1;  // H_dst (rows 0..M) or A' (GCN)

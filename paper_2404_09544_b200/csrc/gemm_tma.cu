@@ -566,16 +566,24 @@ __global__ void k_bt_dx(const float* __restrict__ W, int K1, int ld1, int ld2, i
     Bd[t] = (r >= 0 && k < N) ? W[(int64_t)r * N + k] : 0.f;
   }
 }
-// dW: partial[split][i'][n] -> dW[k][n] with i' = k (X1) or 32*nkb1 + (k-K1) (X2)
-__global__ void k_dw_reduce_tma(const float* __restrict__ partial, int splits, int rows_p, int BN, int K1, int nkb1,
-                                int Ktot, int N, float* dW) {
-  const int total = Ktot * N;
-  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < total; t += gridDim.x * blockDim.x) {
-    const int k = t / N, n = t - k * N;
-    const int ip = k < K1 ? k : 32 * nkb1 + (k - K1);
-    float s = 0.f;
-    for (int z = 0; z < splits; ++z) s += partial[((int64_t)z * rows_p + ip) * BN + n];
-    dW[t] = s;
+// dW: partial[split][i'][n] -> dW[k][n] with i' = k (X1) or 32*nkb1 + (k-K1)
+// (X2).  Block (32, 8) = 32 columns x 8 split-groups of one k row, fixed
+// summation order; grid (ceil(N/32), Ktot).
+__global__ void __launch_bounds__(256) k_dw_reduce_tma(const float* __restrict__ partial, int splits, int rows_p,
+                                                       int BN, int K1, int nkb1, int N, float* dW) {
+  __shared__ float sh[8][33];
+  const int k = blockIdx.y, n = blockIdx.x * 32 + threadIdx.x;
+  const int ip = k < K1 ? k : 32 * nkb1 + (k - K1);
+  float acc = 0.f;
+  if (n < N)
+    for (int z = threadIdx.y; z < splits; z += 8) acc += partial[((int64_t)z * rows_p + ip) * BN + n];
+  sh[threadIdx.y][threadIdx.x] = acc;
+  __syncthreads();
+  if (threadIdx.y == 0 && n < N) {
+    float t = 0.f;
+#pragma unroll
+    for (int y = 0; y < 8; ++y) t += sh[y][threadIdx.x];
+    dW[(int64_t)k * N + n] = t;
   }
 }
 
@@ -715,13 +723,6 @@ bool gemm_dx_tma(const GemmDxArgs& a, cudaStream_t s) {
   return true;
 }
 
-__global__ void k_db_reduce_tma(const float* __restrict__ dbpart, int splits, int BN, int N, float* db) {
-  for (int n = blockIdx.x * blockDim.x + threadIdx.x; n < N; n += gridDim.x * blockDim.x) {
-    float s = 0.f;
-    for (int z = 0; z < splits; ++z) s += dbpart[(int64_t)z * BN + n];
-    db[n] = s;
-  }
-}
 
 // dW; with a.Hmask also the fused ReLU mask and db (else db comes from the
 // column-sum kernel in layers.cu).
@@ -757,13 +758,10 @@ bool gemm_dw_tma(const GemmDwArgs& a, cudaStream_t s) {
   p.dbg = debug_flags();
   launch<MODE_DW>(p, dim3((unsigned)splits, (unsigned)igroups), s);
   const int Ktot = a.X2 ? 2 * a.K1 : a.K1;
-  k_dw_reduce_tma<<<std::min(1024, (Ktot * a.N + 255) / 256), 256, 0, s>>>(partial, splits, rows_p, BN, a.K1, nkb1,
-                                                                          Ktot, a.N, a.dW);
+  k_dw_reduce_tma<<<dim3((a.N + 31) / 32, Ktot), dim3(32, 8), 0, s>>>(partial, splits, rows_p, BN, a.K1, nkb1, a.N,
+                                                                       a.dW);
   GNNV_CHECK_LAUNCH();
-  if (a.Hmask) {
-    k_db_reduce_tma<<<1, 256, 0, s>>>(p.dbpart, splits, BN, a.N, a.db);
-    GNNV_CHECK_LAUNCH();
-  }
+  if (a.Hmask) launch_colsum_reduce(p.dbpart, splits, BN, a.N, a.db, s);
   return true;
 }
 

@@ -76,15 +76,31 @@ __global__ void __launch_bounds__(256) k_mask_colsum(const float* __restrict__ G
   }
 }
 
-__global__ void k_colsum_reduce(const float* __restrict__ partial, int blocks, int ld, int N, float* db) {
-  for (int n = blockIdx.x * blockDim.x + threadIdx.x; n < N; n += gridDim.x * blockDim.x) {
-    float s = 0.f;
-    for (int b = 0; b < blocks; ++b) s += partial[(int64_t)b * ld + n];
-    db[n] = s;
+// out[n] = sum_b partial[b*ld + n], n < N: 32 columns x 8 part-groups per
+// block, fixed order (deterministic); block (32, 8), grid ceil(N/32).
+__global__ void __launch_bounds__(256) k_colsum_reduce(const float* __restrict__ partial, int blocks, int ld, int N,
+                                                       float* db) {
+  __shared__ float s[8][33];
+  const int n = blockIdx.x * 32 + threadIdx.x;
+  float acc = 0.f;
+  if (n < N)
+    for (int b = threadIdx.y; b < blocks; b += 8) acc += partial[(int64_t)b * ld + n];
+  s[threadIdx.y][threadIdx.x] = acc;
+  __syncthreads();
+  if (threadIdx.y == 0 && n < N) {
+    float t = 0.f;
+#pragma unroll
+    for (int y = 0; y < 8; ++y) t += s[y][threadIdx.x];
+    db[n] = t;
   }
 }
 
-constexpr int kLossBlocks = 64;
+void launch_colsum_reduce(const float* partial, int blocks, int ld, int N, float* out, cudaStream_t s) {
+  k_colsum_reduce<<<(N + 31) / 32, dim3(32, 8), 0, s>>>(partial, blocks, ld, N, out);
+  GNNV_CHECK_LAUNCH();
+}
+
+constexpr int kLossBlocks = 256;  // <= the trainer's 256 partials
 
 // One warp per seed row; fixed grid => fixed summation order (deterministic).
 __global__ void __launch_bounds__(256) k_ce_loss(const float* __restrict__ z, int ldz, int C,
@@ -128,12 +144,21 @@ __global__ void __launch_bounds__(256) k_ce_loss(const float* __restrict__ z, in
     s_last = atomicAdd(counter, 1u) == gridDim.x - 1;
   }
   __syncthreads();
-  if (s_last && threadIdx.x == 0) {
+  if (s_last) {  // block-uniform: the last block reduces the partials (fixed tree)
+    __shared__ float s_r[256];
     __threadfence();
     float t = 0.f;
-    for (int i = 0; i < (int)gridDim.x; ++i) t += ((volatile float*)partial)[i];
-    *d_loss = t * inv;
-    *counter = 0;
+    for (int i = threadIdx.x; i < (int)gridDim.x; i += blockDim.x) t += ((volatile float*)partial)[i];
+    s_r[threadIdx.x] = t;
+    __syncthreads();
+    for (int o = 128; o; o >>= 1) {
+      if ((int)threadIdx.x < o) s_r[threadIdx.x] += s_r[threadIdx.x + o];
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+      *d_loss = s_r[0] * inv;
+      *counter = 0;
+    }
   }
 }
 
@@ -222,14 +247,12 @@ void layer_bwd_impl(gnnv_blocks* b, int32_t layer, const gnnv_layer_desc* ld, co
   const size_t da_f = Gsrc ? (size_t)max_dst * lda : 0;
   const size_t cs_f = tf32 ? (size_t)kColBlocks * ldo : 0;
   auto al = [](size_t f) { return (f + 63) & ~(size_t)63; };
-  const size_t csc_f = 0;
   float* scratch =
-      (float*)b->ensure_scratch((al(part_f) + al(gp_f) + al(da_f) + al(cs_f) + al(csc_f)) * sizeof(float), s);
+      (float*)b->ensure_scratch((al(part_f) + al(gp_f) + al(da_f) + al(cs_f)) * sizeof(float), s);
   float* partial = scratch;
   float* Gp = scratch + al(part_f);
   float* dA = Gp + al(gp_f);
   float* colpart = dA + al(da_f);
-  float* cscbuf = colpart + al(cs_f);
   const float* G = Gdst;
   // TF32 without dX (layer 1): the dW kernel applies the ReLU mask and sums
   // db itself, so G' is never materialised.
@@ -239,8 +262,7 @@ void layer_bwd_impl(gnnv_blocks* b, int32_t layer, const gnnv_layer_desc* ld, co
     if (tl) tl->mark(s, "relu_mask" + sfx);
     k_mask_colsum<<<kColBlocks, 256, 0, s>>>(Gdst, relu ? Hdst : nullptr, Gp, ldo, d_ndst, colpart);
     GNNV_CHECK_LAUNCH();
-    k_colsum_reduce<<<1, 256, 0, s>>>(colpart, kColBlocks, ldo, ld->d_out, db);
-    GNNV_CHECK_LAUNCH();
+    launch_colsum_reduce(colpart, kColBlocks, ldo, ld->d_out, db, s);
     if (relu) G = Gp;
   } else if (relu && !tf32) {
     if (tl) tl->mark(s, "relu_mask" + sfx);
@@ -293,13 +315,10 @@ void layer_bwd_impl(gnnv_blocks* b, int32_t layer, const gnnv_layer_desc* ld, co
     if (tl) tl->mark(s, "gemm_dx" + sfx);
     gemm_dx(x, ld->prec, s);
     if (tl) tl->mark(s, "spmm_bwd" + sfx);
-    // transposed aggregation by scatter (red.global.add.v4.f32); the
-    // gather form over a device-built CSC (launch_spmm_bwd_csc) measured no
-    // faster on the products workload and stays available
-    (void)cscbuf;
-    launch_rows_zero(Gsrc, ld->in_stride, sage ? d_ndst : nullptr, d_ndst + 1, b->max_n[h + 1], s);
-    launch_spmm_bwd(b->d_indptr[h], b->d_indices[h], d_ndst, max_dst, dA, lda, Gsrc, ld->in_stride, ld->d_in,
-                    ld->kind, ld->aggr, s);
+    // transposed aggregation pushed from the dst rows: owner edges store,
+    // the rest add atomically -- no zeroing pass over dH_src
+    launch_spmm_bwd(b->d_indptr[h], b->d_indices[h], b->d_own[h], d_ndst, max_dst, dA, lda, Gsrc, ld->in_stride,
+                    ld->d_in, ld->kind, ld->aggr, s);
   }
 }
 
@@ -445,8 +464,7 @@ gnnv_status gnnv_dense_dw(const float* X1, int32_t ld1, const float* X2, int32_t
       float* colpart = scratch + part_f;
       k_mask_colsum<<<kColBlocks, 256, 0, s>>>(G, nullptr, nullptr, ldg, w.d_M, colpart);
       GNNV_CHECK_LAUNCH();
-      k_colsum_reduce<<<1, 256, 0, s>>>(colpart, kColBlocks, ldg, N, db_out);
-      GNNV_CHECK_LAUNCH();
+      launch_colsum_reduce(colpart, kColBlocks, ldg, N, db_out, s);
     }
     gemm_dw(w, prec, s);
   });

@@ -18,7 +18,10 @@
 //                     claim; a single-pass chained scan (decoupled look-back)
 //                     over (new ids, sampled count) gives each row its first
 //                     new local id and its CSR offset; winners write
-//                     tag[u] = n_h + offset and F[n_h + offset] = u.
+//                     tag[u] = n_h + offset and F[n_h + offset] = u; the
+//                     row's winner mask is kept as own[r] (bit i = edge
+//                     indptr[r]+i discovered its src id), which the backward
+//                     aggregation uses to write rows without atomics.
 //   k_map           : indices[indptr[r] + i] = tag[ell[r*k+i]] (before the
 //                     next hop reuses the slot array, and after the last hop).
 //   k_reset         : tag[F_L[i]] = INT_MIN, ready for the next call.
@@ -157,7 +160,8 @@ __global__ void __launch_bounds__(kScanTile) k_relabel_scan(int64_t N, int h, in
                                                             const int32_t* __restrict__ ell,
                                                             const int32_t* __restrict__ cnt, int32_t* tag,
                                                             int32_t* __restrict__ F, int32_t* __restrict__ indptr,
-                                                            int32_t* sizes, unsigned long long* status) {
+                                                            uint32_t* __restrict__ own, int32_t* sizes,
+                                                            unsigned long long* status) {
   __shared__ int s_tile;
   __shared__ uint32_t s_wa[kScanTile / 32], s_wb[kScanTile / 32];
   __shared__ uint32_t s_pa, s_pb;
@@ -275,6 +279,7 @@ __global__ void __launch_bounds__(kScanTile) k_relabel_scan(int64_t N, int h, in
   const uint32_t new_off = s_pa + excl_a, edge_off = s_pb + excl_b;
   if (r < n) {
     indptr[r] = (int32_t)edge_off;
+    own[r] = mask;  // edges that discovered a new src id (owner edges)
     uint32_t m = mask;
     int idx = 0;
     while (m) {
@@ -309,9 +314,11 @@ __global__ void k_reset(const int32_t* __restrict__ F, const int32_t* sizes, int
   }
 }
 
-static int grid_for(int64_t work, int per_block, int max_blocks) {
+// One work item per thread / row group (no grid-stride caps): short-lived
+// blocks let the step's higher-priority kernels interleave with a prefetch.
+static int grid_for(int64_t work, int per_block, int /*max_blocks*/) {
   int64_t g = ceil_div(std::max<int64_t>(work, 1), per_block);
-  return (int)std::min<int64_t>(g, max_blocks);
+  return (int)std::min<int64_t>(g, INT32_MAX);
 }
 
 void launch_sample(gnnv_graph* g, gnnv_blocks* b, const int32_t* d_seeds, int32_t n_seeds, uint64_t rng_seed,
@@ -352,7 +359,7 @@ void launch_sample(gnnv_graph* g, gnnv_blocks* b, const int32_t* d_seeds, int32_
     GNNV_TRY_CUDA(cudaMemsetAsync(b->d_scan, 0, b->scan_words * sizeof(unsigned long long), s));
     const int tiles_ub = (int)ceil_div(rows_ub, kScanTile);
     k_relabel_scan<<<tiles_ub, kScanTile, 0, s>>>(g->n, h, k, L, b->d_ell, b->d_cnt, b->d_tag, b->d_F,
-                                                  b->d_indptr[h], b->d_sizes, b->d_scan);
+                                                  b->d_indptr[h], b->d_own[h], b->d_sizes, b->d_scan);
     GNNV_CHECK_LAUNCH();
   }
   const int64_t slots_ub = b->max_n[L - 1] * (int64_t)b->fanouts[L - 1];
