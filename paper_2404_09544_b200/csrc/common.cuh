@@ -180,8 +180,16 @@ struct GemmFwdArgs {
   int32_t N;
   const int32_t* d_M; int64_t max_M;
   bool relu;
+  // TF32 with relu: also write the ReLU mask as bits, bits[m*mask_ld + n/32]
+  // bit n%32 = (Y[m][n] > 0), for a later fused dW (NULL: none)
+  uint32_t* mask_bits = nullptr;
+  int32_t mask_ld = 0;
 };
 void gemm_fwd(const GemmFwdArgs& a, int prec, cudaStream_t s);
+// words per row of a ReLU bit mask over N columns (16-byte rows for TMA)
+inline int32_t mask_words(int32_t N) { return ((N + 31) / 32 + 3) / 4 * 4; }
+void launch_relu_bits(const float* H, int32_t ldh, int32_t N, const int32_t* d_M, int64_t max_M, uint32_t* bits,
+                      int32_t bits_ld, cudaStream_t s);
 struct GemmDwArgs {  // dW = [X1|X2]^T G (+ bias row = colsum G) : deterministic split-K
   const float* X1; int32_t ld1;
   const float* X2; int32_t ld2;
@@ -192,7 +200,10 @@ struct GemmDwArgs {  // dW = [X1|X2]^T G (+ bias row = colsum G) : deterministic
   float* dW;  // [(X2?2:1)*K1 x N]
   float* db;  // [N]
   float* partial; int32_t splits;  // workspace [splits x (rows+1) x N]
-  const float* Hmask;  // TF32 only: fuse G' = G * 1[Hmask > 0] and db (NULL: G is final, db elsewhere)
+  // TF32 only: fuse G' = G * mask and db, mask = the ReLU bits of the
+  // layer's output (see GemmFwdArgs::mask_bits); NULL: G is final, db elsewhere
+  const uint32_t* mask_bits = nullptr;
+  int32_t mask_ld = 0;
 };
 void gemm_dw(const GemmDwArgs& a, int prec, cudaStream_t s);
 size_t gemm_dw_partial_floats(int32_t rows_plus_bias, int32_t N, int32_t* splits_out, int64_t max_M);

@@ -162,10 +162,14 @@ struct Params {
   // dw
   float* partial;
   int splits, rows_p, ablocks;  // ablocks: valid 32-wide i blocks (X1 then X2)
-  // dw with a fused ReLU mask: G' = G * 1[H > 0] and db partials per split
+  // dw with a fused ReLU mask: G' = G * bit and db partials per split; th =
+  // the [M x nwp] uint32 bit mask (TMA box DW_KR x nwp)
   CUtensorMap th;
-  int mask;
+  int mask, nwp;
   float* dbpart;  // [splits][BN]
+  // fwd with relu: bit mask output (NULL: none)
+  uint32_t* bits;
+  int bits_ld;
   int dbg;        // micro-benchmark switches (GNNV_DEBUG_GEMM): 1 = no epilogue stores, 2 = no MMA
 };
 
@@ -191,12 +195,12 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_tma_gemm(const __grid_constant_
   // [16 x 128] fp32, then G [16 x BN], then (fused mask) H [16 x BN].
   const int a_bytes = MODE == MODE_DW ? MT * DW_KR * BM * 4 : BM * BKB;
   const int g_bytes = MODE == MODE_DW ? DW_KR * BN * 4 : BN * BKB;
-  const int b_bytes = MODE == MODE_DW ? g_bytes * (p.mask ? 2 : 1) : g_bytes;
+  const int b_bytes = MODE == MODE_DW ? g_bytes + (p.mask ? DW_KR * p.nwp * 4 : 0) : g_bytes;
   const int stage_bytes = a_bytes + b_bytes;
   // dW: two K-major SW64 tiles (64B rows = 16 tf32 of K) built by the transposers;
   // fwd/dX: one 4 KB SW128 output staging buffer per epilogue warp (TMA store)
   const int kt_bytes = MODE == MODE_DW ? (MT * BM + BN) * 64 : 0;
-  uint8_t* kbuf = smem + (size_t)S * stage_bytes;
+  uint8_t* kbuf = smem + (((size_t)S * stage_bytes + 1023) & ~(size_t)1023);  // swizzle-atom aligned
   uint8_t* obuf = kbuf;
   const int extra = MODE == MODE_DW ? 2 * kt_bytes : NE * 4096;
   uint64_t* bars = reinterpret_cast<uint64_t*>(kbuf + extra);
@@ -329,13 +333,16 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_tma_gemm(const __grid_constant_
             for (int j = 16; j < 32; ++j) v[j] = 0.f;
           }
           if (MODE == MODE_FWD) {
+            uint32_t bits = 0;
 #pragma unroll
             for (int j = 0; j < 32; ++j) {
               const int n = c + j;
               float x = v[j] + (n < BN ? s_bias[n] : 0.f);
               if (p.relu) x = fmaxf(x, 0.f);
               v[j] = n < p.N ? x : 0.f;
+              bits |= (v[j] > 0.f ? 1u : 0u) << j;
             }
+            if (p.bits && row0 + lane < M && !(p.dbg & 1)) p.bits[(int64_t)(row0 + lane) * p.bits_ld + (c >> 5)] = bits;
           }
           const int j0 = nt * BN + c;  // dX: column in the [Y1 | Y2] space
           if (row0 + 32 > M || (MODE == MODE_DX && j0 < p.ld1 && j0 + 32 > p.ld1)) {
@@ -439,13 +446,17 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_tma_gemm(const __grid_constant_
     } else {
       // ---- transposers: a 32-column group of a staged [16 x cols] box -> 32
       // K-major SW64 rows (one per feature / output column, 16 graph rows of
-      // K).  Lane l reads column l row by row (consecutive floats: no bank
-      // conflicts) and writes its 64B row as 4 swizzled 16B chunks.  Graph
-      // rows >= M (stale tail) and features beyond the operand become 0.  With
-      // p.mask the G group is multiplied by 1[H > 0] (H staged after G) and
-      // each lane keeps the column sum of its G' column (db).
+      // K).  Lane (rq, cq) = (lane / 8, lane % 8) owns the 4 x 4 block rows
+      // 4rq.., columns 4cq..: four LDS.128 along the staged rows, a register
+      // transpose, and four STS.128 into the K-major rows (one 16-byte chunk
+      // of 4 graph rows each) -- 8 shared-memory instructions per lane for
+      // 16 elements.  Graph rows >= M (stale tail) and features beyond the
+      // operand become 0.  With p.mask the G group is multiplied by its ReLU
+      // bits (one staged word per graph row) and each lane keeps the column
+      // sums of its 4 G' columns (db), reduced over rq at the end.
       const int tw = warp - 2;  // 0..NE-1
-      float dbacc[2] = {0.f, 0.f};
+      const int rq = lane >> 3, cq = lane & 7;
+      float dbacc[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
       for (int i = 0; i < nkb; ++i) {
         const int s = i % S, b = i & 1;
         mbar_wait(&full[s], (i / S) & 1);
@@ -462,31 +473,47 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_tma_gemm(const __grid_constant_
           const float* src;
           int ld;
           if (is_a) {
-            src = reinterpret_cast<const float*>(st + (gx / 4) * (DW_KR * BM * 4)) + (gx % 4) * 32 + lane;
+            src = reinterpret_cast<const float*>(st + (gx / 4) * (DW_KR * BM * 4)) + (gx % 4) * 32 + 4 * cq;
             ld = BM;
           } else {
-            src = reinterpret_cast<const float*>(st + a_bytes) + (gx - MT * 4) * 32 + lane;
+            src = reinterpret_cast<const float*>(st + a_bytes) + (gx - MT * 4) * 32 + 4 * cq;
             ld = BN;
           }
-          float x[DW_KR];
+          float4 x[4];
 #pragma unroll
-          for (int r = 0; r < DW_KR; ++r) x[r] = (loaded && r < valid) ? src[r * ld] : 0.f;
-          if (!is_a && p.mask) {
-            const float* hs = src + DW_KR * BN;
-            float acc = 0.f;
-#pragma unroll
-            for (int r = 0; r < DW_KR; ++r) {
-              if (!(r < valid && hs[r * ld] > 0.f)) x[r] = 0.f;
-              acc += x[r];
-            }
-            if (jb == 0) dbacc[0] += acc;
-            else dbacc[1] += acc;
+          for (int j = 0; j < 4; ++j) {
+            const int r = 4 * rq + j;
+            x[j] = (loaded && r < valid) ? *reinterpret_cast<const float4*>(src + r * ld)
+                                         : make_float4(0.f, 0.f, 0.f, 0.f);
           }
-          const int krow = is_a ? gx * 32 + lane : (gx - MT * 4) * 32 + lane;
-          const uint32_t drow = smem_u32(kt + (is_a ? 0 : MT * BM * 64) + (size_t)krow * 64);
+          if (!is_a && p.mask) {
+            const uint32_t* wb = reinterpret_cast<const uint32_t*>(st + a_bytes + g_bytes) + (gx - MT * 4);
 #pragma unroll
-          for (int j = 0; j < 4; ++j)
-            st_shared_v4(drow + ((j ^ ((krow >> 1) & 3)) << 4), x[4 * j], x[4 * j + 1], x[4 * j + 2], x[4 * j + 3]);
+            for (int j = 0; j < 4; ++j) {
+              const uint32_t w = wb[(4 * rq + j) * p.nwp] >> (4 * cq);
+              if (!(w & 1u)) x[j].x = 0.f;
+              if (!(w & 2u)) x[j].y = 0.f;
+              if (!(w & 4u)) x[j].z = 0.f;
+              if (!(w & 8u)) x[j].w = 0.f;
+              dbacc[jb][0] += x[j].x;
+              dbacc[jb][1] += x[j].y;
+              dbacc[jb][2] += x[j].z;
+              dbacc[jb][3] += x[j].w;
+            }
+          }
+          const int krow0 = (is_a ? gx * 32 : MT * BM + (gx - MT * 4) * 32) + 4 * cq;
+          const uint32_t kt_u32 = smem_u32(kt);
+#define GNNV_KROW_STORE(ci, comp)                                                                        \
+  {                                                                                                      \
+    const int krow = krow0 + (ci);                                                                       \
+    st_shared_v4(kt_u32 + (uint32_t)krow * 64 + ((rq ^ ((krow >> 1) & 3)) << 4), x[0].comp, x[1].comp, \
+                 x[2].comp, x[3].comp);                                                                  \
+  }
+          GNNV_KROW_STORE(0, x)
+          GNNV_KROW_STORE(1, y)
+          GNNV_KROW_STORE(2, z)
+          GNNV_KROW_STORE(3, w)
+#undef GNNV_KROW_STORE
         }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         mbar_arrive(&empty[s]);   // staging stage s may be refilled
@@ -496,8 +523,17 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_tma_gemm(const __grid_constant_
 #pragma unroll
         for (int jb = 0; jb < 2; ++jb) {
           const int gx = tw + jb * NE;
-          if (gx >= MT * 4 && gx < ngroups)
-            p.dbpart[(int64_t)blockIdx.x * BN + (gx - MT * 4) * 32 + lane] = jb == 0 ? dbacc[0] : dbacc[1];
+#pragma unroll
+          for (int ci = 0; ci < 4; ++ci) {
+            float v = dbacc[jb][ci];
+            v += __shfl_xor_sync(0xffffffffu, v, 8);
+            v += __shfl_xor_sync(0xffffffffu, v, 16);
+            dbacc[jb][ci] = v;
+          }
+          if (gx >= MT * 4 && gx < ngroups && rq == 0) {
+            float* o = p.dbpart + (int64_t)blockIdx.x * BN + (gx - MT * 4) * 32 + 4 * cq;
+            *reinterpret_cast<float4*>(o) = make_float4(dbacc[jb][0], dbacc[jb][1], dbacc[jb][2], dbacc[jb][3]);
+          }
         }
       }
       mbar_wait(&tfull[0], 0);
@@ -634,18 +670,18 @@ struct Arena {
 };
 static Arena g_img, g_part;
 
-static size_t smem_bytes(int mode, int BN, int mask) {
+static size_t smem_bytes(int mode, int BN, int mask, int nwp) {
   const int S = mode == MODE_DW ? DW_STAGES : FWD_STAGES;
   const int a = mode == MODE_DW ? DW_MT * DW_KR * BM * 4 : BM * BKB;
-  const int b = mode == MODE_DW ? DW_KR * BN * 4 * (mask ? 2 : 1) : BN * BKB;
+  const int b = mode == MODE_DW ? DW_KR * BN * 4 + (mask ? DW_KR * nwp * 4 : 0) : BN * BKB;
   const int k = mode == MODE_DW ? 2 * (DW_MT * BM + BN) * 64 : NE * 4096;
-  return (size_t)S * (a + b) + k + 8 * (2 * S + 8) + 16 + 1024;
+  return (((size_t)S * (a + b) + 1023) & ~(size_t)1023) + k + 8 * (2 * S + 8) + 16 + 1024;
 }
 
 template <int MODE>
 static void launch(const Params& p, dim3 grid, cudaStream_t s) {
   static size_t attr = 0;  // dynamic smem opt-in, raised to the largest request seen
-  const size_t bytes = smem_bytes(MODE, p.BN, p.mask);
+  const size_t bytes = smem_bytes(MODE, p.BN, p.mask, p.nwp);
   if (bytes > attr) {
     GNNV_TRY_CUDA(cudaFuncSetAttribute(k_tma_gemm<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
     attr = bytes;
@@ -684,6 +720,8 @@ bool gemm_fwd_tma(const GemmFwdArgs& a, cudaStream_t s) {
   p.bias = a.bias;
   p.relu = a.relu ? 1 : 0;
   p.ty1 = make_map(a.Y, a.max_M, a.ldy, a.ldy, 32);
+  p.bits = a.relu ? a.mask_bits : nullptr;
+  p.bits_ld = a.mask_ld;
   const int64_t tiles = ceil_div(std::max<int64_t>(a.max_M, 1), BM);
   p.dbg = debug_flags();
   launch<MODE_FWD>(p, dim3((unsigned)std::min<int64_t>(tiles, num_sms())), s);
@@ -724,7 +762,7 @@ bool gemm_dx_tma(const GemmDxArgs& a, cudaStream_t s) {
 }
 
 
-// dW; with a.Hmask also the fused ReLU mask and db (else db comes from the
+// dW; with a.mask_bits also the fused ReLU mask and db (else db comes from the
 // column-sum kernel in layers.cu).
 bool gemm_dw_tma(const GemmDwArgs& a, cudaStream_t s) {
   using namespace tma;
@@ -739,9 +777,12 @@ bool gemm_dw_tma(const GemmDwArgs& a, cudaStream_t s) {
   const size_t part_f = (size_t)splits * rows_p * BN;
   float* partial = (float*)g_part.get((part_f + (size_t)splits * BN) * sizeof(float), s);
   Params p{};
-  if (a.Hmask) {
+  if (a.mask_bits) {
+    GNNV_REQUIRE(a.mask_ld == mask_words(a.N), GNNV_ERR_PARAM, "dW: mask bits row stride");
     p.mask = 1;
-    p.th = make_map(a.Hmask, a.max_M, a.N, a.ldg, DW_KR, BN, false);
+    p.nwp = a.mask_ld;
+    p.th = make_map(reinterpret_cast<const float*>(a.mask_bits), a.max_M, a.mask_ld, a.mask_ld, DW_KR, a.mask_ld,
+                    false);
     p.dbpart = partial + part_f;
   }
   p.ta1 = make_map(a.X1, a.max_M, a.K1, a.ld1, DW_KR, BM, false);
@@ -761,7 +802,7 @@ bool gemm_dw_tma(const GemmDwArgs& a, cudaStream_t s) {
   k_dw_reduce_tma<<<dim3((a.N + 31) / 32, Ktot), dim3(32, 8), 0, s>>>(partial, splits, rows_p, BN, a.K1, nkb1, a.N,
                                                                        a.dW);
   GNNV_CHECK_LAUNCH();
-  if (a.Hmask) launch_colsum_reduce(p.dbpart, splits, BN, a.N, a.db, s);
+  if (a.mask_bits) launch_colsum_reduce(p.dbpart, splits, BN, a.N, a.db, s);
   return true;
 }
 

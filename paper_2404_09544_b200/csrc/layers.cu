@@ -28,6 +28,31 @@ void launch_relu_mask(const float* G, const float* H, float* Gp, int32_t ld, int
   GNNV_CHECK_LAUNCH();
 }
 
+// bits[m*bits_ld + n/32] bit n%32 = (H[m][n] > 0): one warp per (row, word)
+__global__ void k_relu_bits(const float* __restrict__ H, int32_t ldh, int32_t N, const int32_t* d_M, uint32_t* bits,
+                            int32_t bits_ld) {
+  const int64_t M = *d_M;
+  const int lane = threadIdx.x & 31;
+  const int64_t total = M * bits_ld;
+  for (int64_t t = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; t < total;
+       t += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    const int64_t m = t / bits_ld;
+    const int wd = (int)(t - m * bits_ld);
+    const int n = wd * 32 + lane;
+    const bool on = n < N && H[m * ldh + n] > 0.f;
+    const uint32_t w = __ballot_sync(0xffffffffu, on);
+    if (lane == 0) bits[t] = w;
+  }
+}
+
+void launch_relu_bits(const float* H, int32_t ldh, int32_t N, const int32_t* d_M, int64_t max_M, uint32_t* bits,
+                      int32_t bits_ld, cudaStream_t s) {
+  const int64_t warps = std::max<int64_t>(max_M, 1) * bits_ld;
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(warps, 8), (int64_t)num_sms() * 16));
+  k_relu_bits<<<grid, 256, 0, s>>>(H, ldh, N, d_M, bits, bits_ld);
+  GNNV_CHECK_LAUNCH();
+}
+
 // G' = G * 1[H > 0] (if H) written to Gp, plus per-block column sums of G'
 // (db).  Fixed grid, contiguous row ranges, fixed in-block order: the
 // bias gradient is deterministic.
@@ -196,7 +221,7 @@ static void check_layer(const gnnv_blocks* b, int32_t layer, const gnnv_layer_de
 }
 
 void layer_fwd_impl(gnnv_blocks* b, int32_t layer, const gnnv_layer_desc* ld, const float* Hsrc, const float* W,
-                    const float* bias, float* Hdst, float* A, cudaStream_t s, Timeline* tl) {
+                    const float* bias, float* Hdst, float* A, cudaStream_t s, Timeline* tl, uint32_t* mask_bits) {
   const std::string sfx = ".l" + std::to_string(layer);
   if (tl) tl->mark(s, "spmm_fwd" + sfx);
   const int h = b->L - layer;
@@ -225,13 +250,17 @@ void layer_fwd_impl(gnnv_blocks* b, int32_t layer, const gnnv_layer_desc* ld, co
   g.d_M = d_ndst;
   g.max_M = b->max_n[h];
   g.relu = ld->act == GNNV_ACT_RELU;
+  if (mask_bits && g.relu && ld->prec == GNNV_PREC_TF32) {
+    g.mask_bits = mask_bits;
+    g.mask_ld = mask_words(ld->d_out);
+  }
   if (tl) tl->mark(s, "gemm_fwd" + sfx);
   gemm_fwd(g, ld->prec, s);
 }
 
 void layer_bwd_impl(gnnv_blocks* b, int32_t layer, const gnnv_layer_desc* ld, const float* Gdst, const float* Hdst,
                     const float* Hsrc, const float* A, const float* W, float* Gsrc, float* dW, float* db,
-                    cudaStream_t s, Timeline* tl) {
+                    cudaStream_t s, Timeline* tl, const uint32_t* mask_bits) {
   const std::string sfx = ".l" + std::to_string(layer);
   const int h = b->L - layer;
   const int32_t* d_ndst = b->d_sizes + h;
@@ -246,17 +275,26 @@ void layer_bwd_impl(gnnv_blocks* b, int32_t layer, const gnnv_layer_desc* ld, co
   const size_t gp_f = relu ? (size_t)max_dst * ldo : 0;
   const size_t da_f = Gsrc ? (size_t)max_dst * lda : 0;
   const size_t cs_f = tf32 ? (size_t)kColBlocks * ldo : 0;
+  // TF32 without dX (layer 1): the dW kernel applies the ReLU mask (as bits:
+  // from the forward epilogue, else derived from H here) and sums db
+  // itself, so G' is never materialised.
+  const bool fuse_mask = tf32 && relu && !Gsrc;
+  const int mwords = mask_words(ld->d_out);
+  const size_t mb_f = (fuse_mask && !mask_bits) ? (size_t)max_dst * mwords : 0;
   auto al = [](size_t f) { return (f + 63) & ~(size_t)63; };
   float* scratch =
-      (float*)b->ensure_scratch((al(part_f) + al(gp_f) + al(da_f) + al(cs_f)) * sizeof(float), s);
+      (float*)b->ensure_scratch((al(part_f) + al(gp_f) + al(da_f) + al(cs_f) + al(mb_f)) * sizeof(float), s);
   float* partial = scratch;
   float* Gp = scratch + al(part_f);
   float* dA = Gp + al(gp_f);
   float* colpart = dA + al(da_f);
   const float* G = Gdst;
-  // TF32 without dX (layer 1): the dW kernel applies the ReLU mask and sums
-  // db itself, so G' is never materialised.
-  const bool fuse_mask = tf32 && relu && !Gsrc;
+  if (fuse_mask && !mask_bits) {
+    uint32_t* mb = reinterpret_cast<uint32_t*>(colpart + al(cs_f));
+    if (tl) tl->mark(s, "relu_bits" + sfx);
+    launch_relu_bits(Hdst, ldo, ld->d_out, d_ndst, max_dst, mb, mwords, s);
+    mask_bits = mb;
+  }
   if (tf32 && !fuse_mask) {
     // masked gradient + deterministic column sums (db) in one pass
     if (tl) tl->mark(s, "relu_mask" + sfx);
@@ -289,7 +327,10 @@ void layer_bwd_impl(gnnv_blocks* b, int32_t layer, const gnnv_layer_desc* ld, co
   w.db = db;
   w.partial = partial;
   w.splits = splits;
-  w.Hmask = fuse_mask ? Hdst : nullptr;
+  if (fuse_mask) {
+    w.mask_bits = mask_bits;
+    w.mask_ld = mwords;
+  }
   if (tl) tl->mark(s, "gemm_dw" + sfx);
   gemm_dw(w, ld->prec, s);
   if (Gsrc) {
@@ -333,7 +374,7 @@ gnnv_status gnnv_layer_fwd(gnnv_blocks* b, int32_t layer, const gnnv_layer_desc*
   return guarded([&] {
     check_layer(b, layer, ld);
     GNNV_REQUIRE(d_Hsrc && d_W && d_b && d_Hdst && d_saveA, GNNV_ERR_PARAM, "layer_fwd: null buffer");
-    layer_fwd_impl(b, layer, ld, d_Hsrc, d_W, d_b, d_Hdst, d_saveA, (cudaStream_t)s, nullptr);
+    layer_fwd_impl(b, layer, ld, d_Hsrc, d_W, d_b, d_Hdst, d_saveA, (cudaStream_t)s, nullptr, nullptr);
   });
 }
 
@@ -344,7 +385,8 @@ gnnv_status gnnv_layer_bwd(gnnv_blocks* b, int32_t layer, const gnnv_layer_desc*
     check_layer(b, layer, ld);
     GNNV_REQUIRE(d_Gdst && d_Hdst && d_Hsrc && d_saveA && d_W && d_dW && d_db, GNNV_ERR_PARAM,
                  "layer_bwd: null buffer");
-    layer_bwd_impl(b, layer, ld, d_Gdst, d_Hdst, d_Hsrc, d_saveA, d_W, d_Gsrc, d_dW, d_db, (cudaStream_t)s, nullptr);
+    layer_bwd_impl(b, layer, ld, d_Gdst, d_Hdst, d_Hsrc, d_saveA, d_W, d_Gsrc, d_dW, d_db, (cudaStream_t)s, nullptr,
+                   nullptr);
   });
 }
 
