@@ -42,7 +42,7 @@ constexpr int BK = 32;      // fp32 elements of K per stage
 constexpr int NE = 8;       // epilogue / transposer warps
 constexpr int NTHREADS = 64 + 32 * NE;
 constexpr int FWD_STAGES = 4;
-constexpr int DW_STAGES = 3;
+constexpr int DW_STAGES = 4;
 constexpr int DW_MT = 2;    // 128-row i-tiles per dW CTA
 constexpr int DW_KR = 16;   // graph rows per dW k-block
 constexpr int MODE_FWD = 0, MODE_DX = 1, MODE_DW = 2;
@@ -59,7 +59,7 @@ __device__ __forceinline__ void mbar_arrive_tx(uint64_t* b, uint32_t tx) {
 }
 __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
   asm volatile(
-      "{\n.reg .pred p;\nW_%=:\nmbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n@!p bra W_%=;\n}\n" ::"r"(
+      "{\n.reg .pred p;\nW_%=:\nmbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, 1000000;\n@!p bra W_%=;\n}\n" ::"r"(
           smem_u32(b)),
       "r"(parity)
       : "memory");
