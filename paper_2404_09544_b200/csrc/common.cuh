@@ -167,7 +167,7 @@ void launch_spmm_fwd(const int32_t* d_indptr, const int32_t* d_indices, const in
                      cudaStream_t s);
 void launch_spmm_bwd(const int32_t* d_indptr, const int32_t* d_indices, const uint32_t* d_own, const int32_t* d_ndst,
                      int64_t max_dst, const float* dA, int32_t lda, float* dH, int32_t ldh, int32_t d, int32_t kind,
-                     int32_t aggr, cudaStream_t s);
+                     int32_t aggr, const uint32_t* bits, int32_t bits_ld, cudaStream_t s);
 void launch_colsum_reduce(const float* partial, int blocks, int ld, int N, float* out, cudaStream_t s);
 // gemm
 struct GemmFwdArgs {
@@ -204,6 +204,7 @@ struct GemmDwArgs {  // dW = [X1|X2]^T G (+ bias row = colsum G) : deterministic
   // layer's output (see GemmFwdArgs::mask_bits); NULL: G is final, db elsewhere
   const uint32_t* mask_bits = nullptr;
   int32_t mask_ld = 0;
+  bool db_fused = false;  // TF32 only: db = colsum(G) computed by the dW kernel (G final)
 };
 void gemm_dw(const GemmDwArgs& a, int prec, cudaStream_t s);
 size_t gemm_dw_partial_floats(int32_t rows_plus_bias, int32_t N, int32_t* splits_out, int64_t max_M);
@@ -215,6 +216,9 @@ struct GemmDxArgs {  // [Y1 | Y2] = G W^T  (Y1 = first K1 cols, Y2 = the rest)
   float* Y1; int32_t ld1;
   float* Y2; int32_t ld2;
   const int32_t* d_M; int64_t max_M;
+  // TF32 only: Y1 *= ReLU bits of the previous layer (NULL: none)
+  const uint32_t* y1_bits = nullptr;
+  int32_t y1_bits_ld = 0;
 };
 void gemm_dx(const GemmDxArgs& a, int prec, cudaStream_t s);
 // layers.cu

@@ -170,6 +170,12 @@ struct Params {
   // fwd with relu: bit mask output (NULL: none)
   uint32_t* bits;
   int bits_ld;
+  // dX: multiply the Y1 columns by a ReLU bit mask (the previous layer's),
+  // ybits[m*ybits_ld + col/32] (NULL: none)
+  const uint32_t* ybits;
+  int ybits_ld;
+  // dW: also the column sums of G (db) without a mask (G already masked)
+  int dbsum;
   int dbg;        // micro-benchmark switches (GNNV_DEBUG_GEMM): 1 = no epilogue stores, 2 = no MMA
 };
 
@@ -345,6 +351,14 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_tma_gemm(const __grid_constant_
             if (p.bits && row0 + lane < M && !(p.dbg & 1)) p.bits[(int64_t)(row0 + lane) * p.bits_ld + (c >> 5)] = bits;
           }
           const int j0 = nt * BN + c;  // dX: column in the [Y1 | Y2] space
+          if (MODE == MODE_DX && p.ybits && j0 < p.ld1) {
+            // G_src = (G W_s^T) * relu'(H_src): chunks are 32-aligned, one word
+            const int64_t m = (int64_t)row0 + lane;
+            const uint32_t wv = m < M ? __ldg(p.ybits + m * p.ybits_ld + (j0 >> 5)) : 0u;
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+              if (j0 + j < p.ld1 && !((wv >> j) & 1u)) v[j] = 0.f;
+          }
           if (row0 + 32 > M || (MODE == MODE_DX && j0 < p.ld1 && j0 + 32 > p.ld1)) {
             // ragged last chunk: plain stores of the rows < M only (the TMA
             // map spans the row capacity, which may exceed the caller's rows);
@@ -495,6 +509,11 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_tma_gemm(const __grid_constant_
               if (!(w & 2u)) x[j].y = 0.f;
               if (!(w & 4u)) x[j].z = 0.f;
               if (!(w & 8u)) x[j].w = 0.f;
+            }
+          }
+          if (!is_a && (p.mask || p.dbsum)) {
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
               dbacc[jb][0] += x[j].x;
               dbacc[jb][1] += x[j].y;
               dbacc[jb][2] += x[j].z;
@@ -519,7 +538,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_tma_gemm(const __grid_constant_
         mbar_arrive(&empty[s]);   // staging stage s may be refilled
         mbar_arrive(&kready[b]);  // K-major tile b ready for the MMA
       }
-      if (p.mask && ig == 0) {
+      if ((p.mask || p.dbsum) && ig == 0) {
 #pragma unroll
         for (int jb = 0; jb < 2; ++jb) {
           const int gx = tw + jb * NE;
@@ -610,10 +629,22 @@ __global__ void __launch_bounds__(256) k_dw_reduce_tma(const float* __restrict__
   __shared__ float sh[8][33];
   const int k = blockIdx.y, n = blockIdx.x * 32 + threadIdx.x;
   const int ip = k < K1 ? k : 32 * nkb1 + (k - K1);
-  float acc = 0.f;
-  if (n < N)
-    for (int z = threadIdx.y; z < splits; z += 8) acc += partial[((int64_t)z * rows_p + ip) * BN + n];
-  sh[threadIdx.y][threadIdx.x] = acc;
+  // four independent loads in flight per thread (a fixed association
+  // order: the result stays deterministic)
+  float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+  if (n < N) {
+    const float* src = partial + (int64_t)ip * BN + n;
+    const int64_t zs = (int64_t)rows_p * BN;
+    int z = threadIdx.y;
+    for (; z + 24 < splits; z += 32) {
+      a0 += src[z * zs];
+      a1 += src[(z + 8) * zs];
+      a2 += src[(z + 16) * zs];
+      a3 += src[(z + 24) * zs];
+    }
+    for (; z < splits; z += 8) a0 += src[z * zs];
+  }
+  sh[threadIdx.y][threadIdx.x] = (a0 + a1) + (a2 + a3);
   __syncthreads();
   if (threadIdx.y == 0 && n < N) {
     float t = 0.f;
@@ -755,6 +786,8 @@ bool gemm_dx_tma(const GemmDxArgs& a, cudaStream_t s) {
   p.ld2 = a.ld2;
   p.ty1 = make_map(a.Y1, a.max_M, a.ld1, a.ld1, 32);
   p.ty2 = a.Y2 ? make_map(a.Y2, a.max_M, a.ld2, a.ld2, 32) : p.ty1;
+  p.ybits = a.y1_bits;
+  p.ybits_ld = a.y1_bits_ld;
   const int64_t tiles = ceil_div(std::max<int64_t>(a.max_M, 1), BM) * ntl;
   p.dbg = debug_flags();
   launch<MODE_DX>(p, dim3((unsigned)std::min<int64_t>(tiles, num_sms())), s);
@@ -784,6 +817,9 @@ bool gemm_dw_tma(const GemmDwArgs& a, cudaStream_t s) {
     p.th = make_map(reinterpret_cast<const float*>(a.mask_bits), a.max_M, a.mask_ld, a.mask_ld, DW_KR, a.mask_ld,
                     false);
     p.dbpart = partial + part_f;
+  } else if (a.db_fused) {
+    p.dbsum = 1;
+    p.dbpart = partial + part_f;
   }
   p.ta1 = make_map(a.X1, a.max_M, a.K1, a.ld1, DW_KR, BM, false);
   p.ta2 = a.X2 ? make_map(a.X2, a.max_M, a.K1, a.ld2, DW_KR, BM, false) : p.ta1;
@@ -802,7 +838,7 @@ bool gemm_dw_tma(const GemmDwArgs& a, cudaStream_t s) {
   k_dw_reduce_tma<<<dim3((a.N + 31) / 32, Ktot), dim3(32, 8), 0, s>>>(partial, splits, rows_p, BN, a.K1, nkb1, a.N,
                                                                        a.dW);
   GNNV_CHECK_LAUNCH();
-  if (a.mask_bits) launch_colsum_reduce(p.dbpart, splits, BN, a.N, a.db, s);
+  if (a.mask_bits || a.db_fused) launch_colsum_reduce(p.dbpart, splits, BN, a.N, a.db, s);
   return true;
 }
 

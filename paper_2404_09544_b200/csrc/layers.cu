@@ -107,10 +107,18 @@ __global__ void __launch_bounds__(256) k_colsum_reduce(const float* __restrict__
                                                        float* db) {
   __shared__ float s[8][33];
   const int n = blockIdx.x * 32 + threadIdx.x;
-  float acc = 0.f;
-  if (n < N)
-    for (int b = threadIdx.y; b < blocks; b += 8) acc += partial[(int64_t)b * ld + n];
-  s[threadIdx.y][threadIdx.x] = acc;
+  float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;  // 4 loads in flight, fixed order
+  if (n < N) {
+    int b = threadIdx.y;
+    for (; b + 24 < blocks; b += 32) {
+      a0 += partial[(int64_t)b * ld + n];
+      a1 += partial[(int64_t)(b + 8) * ld + n];
+      a2 += partial[(int64_t)(b + 16) * ld + n];
+      a3 += partial[(int64_t)(b + 24) * ld + n];
+    }
+    for (; b < blocks; b += 8) a0 += partial[(int64_t)b * ld + n];
+  }
+  s[threadIdx.y][threadIdx.x] = (a0 + a1) + (a2 + a3);
   __syncthreads();
   if (threadIdx.y == 0 && n < N) {
     float t = 0.f;
@@ -260,7 +268,8 @@ void layer_fwd_impl(gnnv_blocks* b, int32_t layer, const gnnv_layer_desc* ld, co
 
 void layer_bwd_impl(gnnv_blocks* b, int32_t layer, const gnnv_layer_desc* ld, const float* Gdst, const float* Hdst,
                     const float* Hsrc, const float* A, const float* W, float* Gsrc, float* dW, float* db,
-                    cudaStream_t s, Timeline* tl, const uint32_t* mask_bits) {
+                    cudaStream_t s, Timeline* tl, const uint32_t* mask_bits, bool g_masked,
+                    const uint32_t* src_bits, int32_t src_bits_ld) {
   const std::string sfx = ".l" + std::to_string(layer);
   const int h = b->L - layer;
   const int32_t* d_ndst = b->d_sizes + h;
@@ -275,10 +284,14 @@ void layer_bwd_impl(gnnv_blocks* b, int32_t layer, const gnnv_layer_desc* ld, co
   const size_t gp_f = relu ? (size_t)max_dst * ldo : 0;
   const size_t da_f = Gsrc ? (size_t)max_dst * lda : 0;
   const size_t cs_f = tf32 ? (size_t)kColBlocks * ldo : 0;
-  // TF32 without dX (layer 1): the dW kernel applies the ReLU mask (as bits:
-  // from the forward epilogue, else derived from H here) and sums db
-  // itself, so G' is never materialised.
-  const bool fuse_mask = tf32 && relu && !Gsrc;
+  // g_masked: Gdst already carries this layer's ReLU derivative (the trainer
+  // applies it where Gdst is produced: the next layer's dX epilogue and
+  // backward aggregation, from the forward's bit mask), so TF32 only needs
+  // db = colsum(G), fused into the dW kernel.  Otherwise the mask is applied
+  // here: TF32 without dX (layer 1) fuses it into dW (bits derived from H),
+  // other TF32 layers use the mask + column-sum pass.
+  const bool need_mask = relu && !g_masked;
+  const bool fuse_mask = tf32 && need_mask && !Gsrc;
   const int mwords = mask_words(ld->d_out);
   const size_t mb_f = (fuse_mask && !mask_bits) ? (size_t)max_dst * mwords : 0;
   auto al = [](size_t f) { return (f + 63) & ~(size_t)63; };
@@ -295,14 +308,14 @@ void layer_bwd_impl(gnnv_blocks* b, int32_t layer, const gnnv_layer_desc* ld, co
     launch_relu_bits(Hdst, ldo, ld->d_out, d_ndst, max_dst, mb, mwords, s);
     mask_bits = mb;
   }
-  if (tf32 && !fuse_mask) {
+  if (tf32 && need_mask && !fuse_mask) {
     // masked gradient + deterministic column sums (db) in one pass
     if (tl) tl->mark(s, "relu_mask" + sfx);
-    k_mask_colsum<<<kColBlocks, 256, 0, s>>>(Gdst, relu ? Hdst : nullptr, Gp, ldo, d_ndst, colpart);
+    k_mask_colsum<<<kColBlocks, 256, 0, s>>>(Gdst, Hdst, Gp, ldo, d_ndst, colpart);
     GNNV_CHECK_LAUNCH();
     launch_colsum_reduce(colpart, kColBlocks, ldo, ld->d_out, db, s);
-    if (relu) G = Gp;
-  } else if (relu && !tf32) {
+    G = Gp;
+  } else if (need_mask && !tf32) {
     if (tl) tl->mark(s, "relu_mask" + sfx);
     launch_relu_mask(Gdst, Hdst, Gp, ldo, ld->d_out, d_ndst, max_dst, s);
     G = Gp;
@@ -331,6 +344,7 @@ void layer_bwd_impl(gnnv_blocks* b, int32_t layer, const gnnv_layer_desc* ld, co
     w.mask_bits = mask_bits;
     w.mask_ld = mwords;
   }
+  w.db_fused = tf32 && !need_mask;
   if (tl) tl->mark(s, "gemm_dw" + sfx);
   gemm_dw(w, ld->prec, s);
   if (Gsrc) {
@@ -345,6 +359,10 @@ void layer_bwd_impl(gnnv_blocks* b, int32_t layer, const gnnv_layer_desc* ld, co
     if (sage) {
       x.Y1 = Gsrc;  // dH_dst lands directly in rows [0, n_dst) of dH_src
       x.ld1 = ld->in_stride;
+      if (tf32) {
+        x.y1_bits = src_bits;
+        x.y1_bits_ld = src_bits_ld;
+      }
       x.Y2 = dA;
       x.ld2 = lda;
     } else {
@@ -359,7 +377,7 @@ void layer_bwd_impl(gnnv_blocks* b, int32_t layer, const gnnv_layer_desc* ld, co
     // transposed aggregation pushed from the dst rows: owner edges store,
     // the rest add atomically -- no zeroing pass over dH_src
     launch_spmm_bwd(b->d_indptr[h], b->d_indices[h], b->d_own[h], d_ndst, max_dst, dA, lda, Gsrc, ld->in_stride,
-                    ld->d_in, ld->kind, ld->aggr, s);
+                    ld->d_in, ld->kind, ld->aggr, tf32 ? src_bits : nullptr, src_bits_ld, s);
   }
 }
 
@@ -386,7 +404,7 @@ gnnv_status gnnv_layer_bwd(gnnv_blocks* b, int32_t layer, const gnnv_layer_desc*
     GNNV_REQUIRE(d_Gdst && d_Hdst && d_Hsrc && d_saveA && d_W && d_dW && d_db, GNNV_ERR_PARAM,
                  "layer_bwd: null buffer");
     layer_bwd_impl(b, layer, ld, d_Gdst, d_Hdst, d_Hsrc, d_saveA, d_W, d_Gsrc, d_dW, d_db, (cudaStream_t)s, nullptr,
-                   nullptr);
+                   nullptr, false, nullptr, 0);
   });
 }
 

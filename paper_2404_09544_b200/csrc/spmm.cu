@@ -108,7 +108,8 @@ __global__ void __launch_bounds__(256) k_spmm_bwd(const int32_t* __restrict__ in
                                                   const int32_t* __restrict__ indices,
                                                   const uint32_t* __restrict__ own, const int32_t* d_ndst,
                                                   const float* __restrict__ dA, int32_t lda, float* dH, int32_t ldh,
-                                                  int32_t d, int32_t kind, int32_t aggr, int32_t phase) {
+                                                  int32_t d, int32_t kind, int32_t aggr, int32_t phase,
+                                                  const uint32_t* __restrict__ bits, int32_t bits_ld) {
   constexpr int RPW = 32 / LPR;
   const int n = *d_ndst;
   const int vec = (d + 3) >> 2;
@@ -120,6 +121,13 @@ __global__ void __launch_bounds__(256) k_spmm_bwd(const int32_t* __restrict__ in
   const int cols = phase == 1 ? ldh4 : vec;  // phase 1 also writes the padding
   float4* dH4 = reinterpret_cast<float4*>(dH);
   const bool gcn = kind == GNNV_KIND_GCN;
+  // optional ReLU mask of dH's rows (the previous layer's output bits):
+  // dH[u] = relu'(H[u]) * sum, applied to every contribution
+  auto masked = [&](float4 g, int64_t u, int c) {
+    if (!bits) return g;
+    const uint32_t w = __ldg(bits + u * bits_ld + (c >> 3)) >> ((c & 7) * 4);
+    return make_float4(w & 1u ? g.x : 0.f, w & 2u ? g.y : 0.f, w & 4u ? g.z : 0.f, w & 8u ? g.w : 0.f);
+  };
   for (int base = warp * RPW; base < n; base += nwarps * RPW) {
     const int row = base + sub;
     const bool active = row < n;
@@ -141,15 +149,16 @@ __global__ void __launch_bounds__(256) k_spmm_bwd(const int32_t* __restrict__ in
       float4 g = make_float4(0.f, 0.f, 0.f, 0.f);
       if (cok && c < vec)
         g = mask_tail(f4scale(__ldg(reinterpret_cast<const float4*>(dA) + (int64_t)row * lda4 + c), w), c, d);
-      if (phase == 1 && gcn && cok) dH4[(int64_t)row * ldh4 + c] = g;
+      if (phase == 1 && gcn && cok) dH4[(int64_t)row * ldh4 + c] = c < vec ? masked(g, row, c) : g;
       for (int e0 = 0; e0 < cnt; e0 += LPR) {
         const int my = (e0 + sl < cnt) ? __ldg(indices + beg + e0 + sl) : 0;
         const int m = min(LPR, cnt - e0);
         for (int j = 0; j < m; ++j) {
           const int u = __shfl_sync(smask, my, j, LPR);
           if (cok && ((todo >> (e0 + j)) & 1u)) {
-            if (phase == 1) dH4[(int64_t)u * ldh4 + c] = g;
-            else atomicAdd(dH4 + (int64_t)u * ldh4 + c, g);
+            const float4 gm = c < vec ? masked(g, u, c) : g;
+            if (phase == 1) dH4[(int64_t)u * ldh4 + c] = gm;
+            else atomicAdd(dH4 + (int64_t)u * ldh4 + c, gm);
           }
         }
       }
@@ -178,18 +187,18 @@ void launch_spmm_fwd(const int32_t* d_indptr, const int32_t* d_indices, const in
 
 void launch_spmm_bwd(const int32_t* d_indptr, const int32_t* d_indices, const uint32_t* d_own, const int32_t* d_ndst,
                      int64_t max_dst, const float* dA, int32_t lda, float* dH, int32_t ldh, int32_t d, int32_t kind,
-                     int32_t aggr, cudaStream_t s) {
+                     int32_t aggr, const uint32_t* bits, int32_t bits_ld, cudaStream_t s) {
   const int ldh4 = ldh / 4;
   for (int phase = 1; phase <= 2; ++phase) {
     if (ldh4 <= 8) {
       k_spmm_bwd<8><<<spmm_grid(max_dst, 4), 256, 0, s>>>(d_indptr, d_indices, d_own, d_ndst, dA, lda, dH, ldh, d, kind,
-                                                          aggr, phase);
+                                                          aggr, phase, bits, bits_ld);
     } else if (ldh4 <= 16) {
       k_spmm_bwd<16><<<spmm_grid(max_dst, 2), 256, 0, s>>>(d_indptr, d_indices, d_own, d_ndst, dA, lda, dH, ldh, d,
-                                                           kind, aggr, phase);
+                                                           kind, aggr, phase, bits, bits_ld);
     } else {
       k_spmm_bwd<32><<<spmm_grid(max_dst, 1), 256, 0, s>>>(d_indptr, d_indices, d_own, d_ndst, dA, lda, dH, ldh, d,
-                                                           kind, aggr, phase);
+                                                           kind, aggr, phase, bits, bits_ld);
     }
     GNNV_CHECK_LAUNCH();
   }

@@ -14,7 +14,8 @@ void layer_fwd_impl(gnnv_blocks* b, int32_t layer, const gnnv_layer_desc* ld, co
                     const float* bias, float* Hdst, float* A, cudaStream_t s, Timeline* tl, uint32_t* mask_bits);
 void layer_bwd_impl(gnnv_blocks* b, int32_t layer, const gnnv_layer_desc* ld, const float* Gdst, const float* Hdst,
                     const float* Hsrc, const float* A, const float* W, float* Gsrc, float* dW, float* db,
-                    cudaStream_t s, Timeline* tl, const uint32_t* mask_bits);
+                    cudaStream_t s, Timeline* tl, const uint32_t* mask_bits, bool g_masked,
+                    const uint32_t* src_bits, int32_t src_bits_ld);
 }  // namespace gnnv
 
 using namespace gnnv;
@@ -37,7 +38,9 @@ struct gnnv_trainer {
   int32_t Hs[GNNV_MAX_LAYERS + 1] = {0};
   float* A[GNNV_MAX_LAYERS + 1] = {nullptr};
   float* G[GNNV_MAX_LAYERS + 1] = {nullptr};
-  uint32_t* mask1 = nullptr;  // ReLU bits of layer 1's output (fused into its dW)
+  // TF32: ReLU bits of each hidden layer's output (written by its forward
+  // epilogue; the backward masks dH where it is produced)
+  uint32_t* mbits[GNNV_MAX_LAYERS + 1] = {nullptr};
   float* loss_partial = nullptr;
   unsigned int* loss_counter = nullptr;
   int64_t* d_stats = nullptr;
@@ -102,7 +105,7 @@ gnnv_status gnnv_trainer_free(gnnv_trainer* t) {
     dfree(t->A[i]);
     dfree(t->G[i]);
   }
-  dfree(t->mask1);
+  for (auto* m : t->mbits) dfree(m);
   dfree(t->loss_partial);
   dfree(t->loss_counter);
   for (auto& e : t->ev)
@@ -160,9 +163,10 @@ gnnv_status gnnv_trainer_create(gnnv_graph* g, gnnv_cache* c, const gnnv_model_d
         t->G[i] = (float*)dmalloc((size_t)rows * t->Hs[i] * sizeof(float), "dH gradients");
         t->A[i] = (float*)dmalloc((size_t)rows * row_stride(md->dims[i - 1]) * sizeof(float), "aggregates");
       }
-      if (L > 1 && md->prec == GNNV_PREC_TF32)
-        t->mask1 = (uint32_t*)dmalloc((size_t)b->max_n[L - 1] * mask_words(md->dims[1]) * sizeof(uint32_t),
-                                      "layer-1 ReLU bits");
+      if (md->prec == GNNV_PREC_TF32)
+        for (int i = 1; i < L; ++i)
+          t->mbits[i] = (uint32_t*)dmalloc((size_t)b->max_n[L - i] * mask_words(md->dims[i]) * sizeof(uint32_t),
+                                           "ReLU bits");
       t->loss_partial = (float*)dmalloc(256 * sizeof(float), "loss partials");
       t->loss_counter = (unsigned int*)dmalloc(sizeof(unsigned int), "loss counter");
       GNNV_TRY_CUDA(cudaMemset(t->loss_counter, 0, sizeof(unsigned int)));
@@ -402,7 +406,7 @@ gnnv_status gnnv_step(gnnv_trainer* t, const int32_t* seeds, int32_t n_seeds, in
     for (int i = 1; i <= L; ++i) {
       const gnnv_layer_desc ld = layer_desc(t, i);
       layer_fwd_impl(b, i, &ld, t->H[i - 1], t->d_params + t->w_off[i - 1], t->d_params + t->b_off[i - 1], t->H[i],
-                     t->A[i], s, tl, i == 1 ? t->mask1 : nullptr);
+                     t->A[i], s, tl, t->mbits[i]);
     }
     if (tm) GNNV_TRY_CUDA(cudaEventRecord(t->ev[3], s));
     float* d_loss = t->d_grads + t->nparams;
@@ -414,7 +418,7 @@ gnnv_status gnnv_step(gnnv_trainer* t, const int32_t* seeds, int32_t n_seeds, in
       const gnnv_layer_desc ld = layer_desc(t, i);
       layer_bwd_impl(b, i, &ld, t->G[i], t->H[i], t->H[i - 1], t->A[i], t->d_params + t->w_off[i - 1],
                      i > 1 ? t->G[i - 1] : nullptr, t->d_grads + t->w_off[i - 1], t->d_grads + t->b_off[i - 1], s, tl,
-                     i == 1 ? t->mask1 : nullptr);
+                     t->mbits[i], t->mbits[i] != nullptr, t->mbits[i - 1], mask_words(t->md.dims[i - 1]));
     }
     if (tm) GNNV_TRY_CUDA(cudaEventRecord(t->ev[5], s));
     if (tl) tl->mark(s, "allreduce");
