@@ -14,14 +14,16 @@
 //                     in F_h is "claimed" with atomicMax(tag[u], -(2+slot)),
 //                     i.e. the smallest (row, position) slot wins -- exactly
 //                     the first appearance in the (dst, position) scan.
-//   k_relabel_scan  : one thread per row; flags the slots that won their
-//                     claim; a single-pass chained scan (decoupled look-back)
-//                     over (new ids, sampled count) gives each row its first
-//                     new local id and its CSR offset; winners write
-//                     tag[u] = n_h + offset and F[n_h + offset] = u; the
-//                     row's winner mask is kept as own[r] (bit i = edge
-//                     indptr[r]+i discovered its src id), which the backward
-//                     aggregation uses to write rows without atomics.
+//   k_sample_hop_tpr: the same for k <= 8 with one thread per row (more rows
+//                     in flight per warp); bit-identical.
+//   k_winners       : slot-parallel over the hop: slot e won iff tag[u] still
+//                     holds -(2+e); winners collected as per-row bit masks
+//                     own[r] (kept: the backward's owner-edge masks).
+//   k_relabel_scan  : one thread per row; a single-pass chained scan
+//                     (decoupled look-back) over (new ids, sampled count)
+//                     gives each row its first new local id and its CSR
+//                     offset; winners write tag[u] = n_h + offset + rank and
+//                     F[n_h + offset + rank] = u (slot-parallel).
 //   k_map           : indices[indptr[r] + i] = tag[ell[r*k+i]] (before the
 //                     next hop reuses the slot array, and after the last hop).
 //   k_reset         : tag[F_L[i]] = INT_MIN, ready for the next call.
@@ -85,7 +87,7 @@ __global__ void __launch_bounds__(256) k_sample_hop(const int64_t* __restrict__ 
                                                     const int32_t* __restrict__ indices, int64_t N,
                                                     const int32_t* __restrict__ F, const int32_t* sizes, int h, int k,
                                                     uint64_t seed, int32_t* __restrict__ ell,
-                                                    int32_t* __restrict__ cnt, int32_t* tag) {
+                                                    int32_t* __restrict__ cnt, int32_t* tag, uint32_t* own) {
   const int n = sizes[h];
   constexpr int RPW = 32 / G;
   const int lane = threadIdx.x & 31, grp = lane / G, gl = lane % G;
@@ -135,7 +137,98 @@ __global__ void __launch_bounds__(256) k_sample_hop(const int64_t* __restrict__ 
         if (tag[u] < 0) atomicMax(&tag[u], -(2 + e));
       }
     }
-    if (active && gl == 0) cnt[r] = c;
+    if (active && gl == 0) {
+      cnt[r] = c;
+      own[r] = 0u;
+    }
+  }
+}
+
+// Thread-per-row variant for small fanouts (k <= KMAX): the same draws and
+// the same Floyd recurrence as k_sample_hop, evaluated sequentially by one
+// thread per frontier row (4 draws per Philox call), so a warp keeps 32
+// independent rows' dependent loads (F -> indptr -> indices -> tag) in
+// flight instead of 32/G.  Bit-identical output.
+template <int KMAX>
+__global__ void __launch_bounds__(256) k_sample_hop_tpr(const int64_t* __restrict__ indptr,
+                                                        const int32_t* __restrict__ indices, int64_t N,
+                                                        const int32_t* __restrict__ F, const int32_t* sizes, int h,
+                                                        int k, uint64_t seed, int32_t* __restrict__ ell,
+                                                        int32_t* __restrict__ cnt, int32_t* tag, uint32_t* own) {
+  const int n = sizes[h];
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  const int v = F[r];
+  int64_t beg = 0;
+  int d = 0;
+  if ((uint32_t)v < (uint64_t)N) {
+    beg = indptr[v];
+    d = (int)(indptr[v + 1] - beg);
+  }
+  const int c = min(k, d);
+  int pos[KMAX];
+#pragma unroll
+  for (int i = 0; i < KMAX; ++i) pos[i] = i;
+  if (d > k) {
+    const uint2 key = make_uint2((uint32_t)seed, (uint32_t)(seed >> 32));
+    uint4 o = make_uint4(0u, 0u, 0u, 0u);
+#pragma unroll
+    for (int s = 0; s < KMAX; ++s) {
+      if (s < k) {
+        if ((s & 3) == 0) o = philox4x32_10(make_uint4((uint32_t)s >> 2, 0u, (uint32_t)v, (uint32_t)h), key);
+        const uint32_t u = (s & 3) == 0 ? o.x : ((s & 3) == 1 ? o.y : ((s & 3) == 2 ? o.z : o.w));
+        const int j = d - k + s;
+        const int t = (int)(((uint64_t)u * (uint64_t)(uint32_t)(j + 1)) >> 32);
+        bool hit = false;
+#pragma unroll
+        for (int q = 0; q < KMAX; ++q)
+          if (q < s) hit |= pos[q] == t;
+        pos[s] = hit ? j : t;
+      } else {
+        pos[s] = INT_MAX;
+      }
+    }
+    // ascending positions (odd-even transposition network on registers)
+#pragma unroll
+    for (int pass = 0; pass < KMAX; ++pass) {
+#pragma unroll
+      for (int q = pass & 1; q + 1 < KMAX; q += 2) {
+        const int a = pos[q], b = pos[q + 1];
+        pos[q] = min(a, b);
+        pos[q + 1] = max(a, b);
+      }
+    }
+  }
+  int u[KMAX];
+#pragma unroll
+  for (int i = 0; i < KMAX; ++i) u[i] = i < c ? __ldg(&indices[beg + pos[i]]) : 0;
+#pragma unroll
+  for (int i = 0; i < KMAX; ++i) {
+    if (i < c) {
+      const int e = r * k + i;
+      ell[e] = u[i];
+      if ((uint32_t)u[i] < (uint64_t)N && tag[u[i]] < 0) atomicMax(&tag[u[i]], -(2 + e));
+    }
+  }
+  cnt[r] = c;
+  own[r] = 0u;
+}
+
+// Winners of hop h's claims, slot-parallel over the whole hop: slot e of
+// row r won iff tag[u] still holds its claim code -(2+e) (the smallest slot
+// claiming u).  own[r] |= bit i; own[r] was zeroed by the sample kernel.
+// The mask doubles as the backward's owner-edge mask (bit i = edge
+// indptr[r]+i discovered its src id).
+__global__ void k_winners(int64_t N, int h, int k, const int32_t* sizes, const int32_t* __restrict__ ell,
+                          const int32_t* __restrict__ cnt, const int32_t* tag, uint32_t* own) {
+  const int64_t nslots = (int64_t)sizes[h] * k;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < nslots;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int r = (int)(e / k), i = (int)(e - (int64_t)r * k);
+    if (i < __ldg(cnt + r)) {
+      const int u = __ldg(ell + e);
+      if ((uint32_t)u < (uint64_t)N && tag[u] == -(2 + (int)e)) atomicOr(&own[r], 1u << i);
+    }
   }
 }
 
@@ -174,31 +267,14 @@ __global__ void __launch_bounds__(kScanTile) k_relabel_scan(int64_t N, int h, in
   if (tile >= ntiles) return;
   unsigned long long* st = status + 1;
   const int r = tile * kScanTile + threadIdx.x;
-  // winners of the claim, computed slot-parallel over the tile (independent
-  // ell -> tag load pairs in flight) and collected as per-row bit masks
+  // winners of the claim (k_winners) as per-row bit masks
   __shared__ uint32_t s_mask[kScanTile];
-  __shared__ int s_cnt[kScanTile];
   const int r0 = tile * kScanTile;
   const int rows = min(kScanTile, n - r0);
-  s_mask[threadIdx.x] = 0;
-  s_cnt[threadIdx.x] = threadIdx.x < rows ? cnt[r0 + threadIdx.x] : 0;
-  __syncthreads();
-  {
-    const int nslots = rows * k;
-    const int e0 = r0 * k;
-#pragma unroll 4
-    for (int j = threadIdx.x; j < nslots; j += kScanTile) {
-      const int rl = j / k, i = j - rl * k;
-      if (i < s_cnt[rl]) {
-        const int e = e0 + j;
-        const int u = ell[e];
-        if ((uint32_t)u < (uint64_t)N && tag[u] == -(2 + e)) atomicOr(&s_mask[rl], 1u << i);
-      }
-    }
-  }
+  s_mask[threadIdx.x] = threadIdx.x < rows ? own[r0 + threadIdx.x] : 0u;
+  const int c = threadIdx.x < rows ? cnt[r0 + threadIdx.x] : 0;
   __syncthreads();
   const uint32_t mask = s_mask[threadIdx.x];
-  const int c = s_cnt[threadIdx.x];
   // block exclusive scan of (a, b) = (#new ids, #sampled)
   const uint32_t a = __popc(mask), b = (uint32_t)c;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -277,18 +353,23 @@ __global__ void __launch_bounds__(kScanTile) k_relabel_scan(int64_t N, int h, in
   }
   __syncthreads();
   const uint32_t new_off = s_pa + excl_a, edge_off = s_pb + excl_b;
-  if (r < n) {
-    indptr[r] = (int32_t)edge_off;
-    own[r] = mask;  // edges that discovered a new src id (owner edges)
-    uint32_t m = mask;
-    int idx = 0;
-    while (m) {
-      const int i = __ffs(m) - 1;
-      m &= m - 1;
-      const int u = ell[r * k + i];
-      const int nid = n + (int)new_off + idx++;
-      tag[u] = nid;
-      F[nid] = u;
+  if (r < n) indptr[r] = (int32_t)edge_off;
+  __shared__ uint32_t s_off[kScanTile];
+  s_off[threadIdx.x] = new_off;
+  __syncthreads();
+  // winners get their local ids slot-parallel: row offset + rank of the
+  // slot among the row's winners (no per-row serial chain)
+  {
+    const int nslots = rows * k;
+    for (int j = threadIdx.x; j < nslots; j += kScanTile) {
+      const int rl = j / k, i = j - rl * k;
+      const uint32_t m = s_mask[rl];
+      if ((m >> i) & 1u) {
+        const int u = ell[r0 * k + j];
+        const int nid = n + (int)s_off[rl] + __popc(m & ((1u << i) - 1u));
+        tag[u] = nid;
+        F[nid] = u;
+      }
     }
   }
   if (tile == ntiles - 1 && threadIdx.x == kScanTile - 1) {
@@ -344,11 +425,13 @@ void launch_sample(gnnv_graph* g, gnnv_blocks* b, const int32_t* d_seeds, int32_
     const int threads = 256;
 #define GNNV_SAMPLE_LAUNCH(G)                                                                              \
   k_sample_hop<G><<<grid_for(rows_ub, threads / 32 * (32 / G), sms * 8), threads, 0, s>>>(                 \
-      g->d_indptr, g->d_indices, g->n, b->d_F, b->d_sizes, h, k, rng_seed, b->d_ell, b->d_cnt, b->d_tag)
+      g->d_indptr, g->d_indices, g->n, b->d_F, b->d_sizes, h, k, rng_seed, b->d_ell, b->d_cnt, b->d_tag, b->d_own[h])
     if (k <= 4) {
-      GNNV_SAMPLE_LAUNCH(4);
+      k_sample_hop_tpr<4><<<grid_for(rows_ub, threads, 0), threads, 0, s>>>(
+          g->d_indptr, g->d_indices, g->n, b->d_F, b->d_sizes, h, k, rng_seed, b->d_ell, b->d_cnt, b->d_tag, b->d_own[h]);
     } else if (k <= 8) {
-      GNNV_SAMPLE_LAUNCH(8);
+      k_sample_hop_tpr<8><<<grid_for(rows_ub, threads, 0), threads, 0, s>>>(
+          g->d_indptr, g->d_indices, g->n, b->d_F, b->d_sizes, h, k, rng_seed, b->d_ell, b->d_cnt, b->d_tag, b->d_own[h]);
     } else if (k <= 16) {
       GNNV_SAMPLE_LAUNCH(16);
     } else {
@@ -358,6 +441,9 @@ void launch_sample(gnnv_graph* g, gnnv_blocks* b, const int32_t* d_seeds, int32_
     GNNV_CHECK_LAUNCH();
     GNNV_TRY_CUDA(cudaMemsetAsync(b->d_scan, 0, b->scan_words * sizeof(unsigned long long), s));
     const int tiles_ub = (int)ceil_div(rows_ub, kScanTile);
+    k_winners<<<grid_for(rows_ub * k, 256, 0), 256, 0, s>>>(g->n, h, k, b->d_sizes, b->d_ell, b->d_cnt, b->d_tag,
+                                                             b->d_own[h]);
+    GNNV_CHECK_LAUNCH();
     k_relabel_scan<<<tiles_ub, kScanTile, 0, s>>>(g->n, h, k, L, b->d_ell, b->d_cnt, b->d_tag, b->d_F,
                                                   b->d_indptr[h], b->d_own[h], b->d_sizes, b->d_scan);
     GNNV_CHECK_LAUNCH();
