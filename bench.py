@@ -49,6 +49,8 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-baseline-seeds", type=int, default=0, help="seeds in the oracle sample (0 = one batch)")
     p.add_argument("--ratio", type=float, default=None)
+    p.add_argument("--placement", default="replica", choices=["replica", "sharded"],
+                   help="feature cache across ranks: replicated, or sharded over the GPUs' HBM (NVLink peer reads)")
     p.add_argument("--no-pipeline", action="store_true",
                    help="disable the Eq.4 overlap of next-batch sample+gather with compute")
     return p.parse_args()
@@ -288,7 +290,8 @@ def main():
         dist.broadcast_object_list(obj, src=0)
         comm = gnnv.Comm(rank, world, obj[0], local)
     g = gnnv.Graph.from_data(gd, device=local)
-    cache = gnnv.Cache(g, cfg["ratio"])
+    placement = gnnv.PLACE_SHARDED if args.placement == "sharded" else gnnv.PLACE_REPLICA
+    cache = gnnv.Cache(g, cfg["ratio"], placement=placement, comm=comm)
     dims = [gd.d] + [cfg["hidden"]] * (len(cfg["fanouts"]) - 1) + [gd.C]
     kind = gnnv.KIND_SAGE if args.kind == "sage" else gnnv.KIND_GCN
     prec = {"fp32": gnnv.PREC_FP32, "bf16": gnnv.PREC_BF16, "tf32": gnnv.PREC_TF32}[args.prec]
@@ -467,7 +470,7 @@ def main():
             "vs_baseline": None, "dtype": {"fp32": "f32", "bf16": "f32+bf16gemm", "tf32": "f32+tf32gemm"}[args.prec], "data": "synthetic",
             "config": {"workload": cfg["name"], "n_nodes": gd.n, "nnz": gd.nnz, "d": gd.d, "classes": gd.C,
                        "fanouts": cfg["fanouts"], "batch_per_rank": B, "global_batch": world * B,
-                       "cache_ratio": cfg["ratio"], "placement": "replica", "kind": args.kind,
+                       "cache_ratio": cfg["ratio"], "placement": args.placement, "kind": args.kind,
                        "hidden": cfg["hidden"], "gemm_precision": args.prec,
                        "l2": "inputs > L2 (feature table %.0f MB, gathered X %.0f MB per step)" % (
                            gd.n * gd.stride * 4 / 1e6, sizes["n"][L] * gd.stride * 4 / 1e6),

@@ -127,7 +127,10 @@ gnnv_status gnnv_graph_info(const gnnv_graph* g, gnnv_graph_view* out);
 
 /* ------------------------------------------------------------------ comm */
 /* NCCL over NVLink/NVSwitch, one process per GPU.  The 128-byte unique id is
- * produced on rank 0 and exchanged by the caller (torch process group). */
+ * produced on rank 0 and exchanged by the caller (torch process group).
+ * unique_id128 == NULL creates a host-only comm (rank/world only, no NCCL):
+ * gnnv_allreduce_sum then fails with STATE for world > 1, and a SHARDED
+ * cache needs gnnv_cache_open_peers. */
 gnnv_status gnnv_comm_unique_id(void* out128);
 gnnv_status gnnv_comm_init(int32_t rank, int32_t world, const void* unique_id128, int32_t device, gnnv_comm** out);
 gnnv_status gnnv_comm_free(gnnv_comm* c);
@@ -139,7 +142,7 @@ gnnv_status gnnv_allreduce_sum(gnnv_comm* c, float* d_buf, int64_t n, gnnv_strea
  * (§3.2), PaGraph static degree template.  Capacity
  * C = floor(ratio * N) in IEEE double; vertices ordered by
  * (degree desc, id asc); slot(v) = rank(v) if rank(v) < C else -1.
- *  comm            NULL => single GPU; required for SHARDED
+ *  comm            NULL => single GPU (SHARDED then has one shard)
  *  virtual_shards  G for SHARDED_LOCAL (>=1), ignored otherwise
  * Errors: PARAM (ratio not in [0,1]); UNSUPPORTED (FIFO/LRU); OOM (message
  * carries the bytes, Γ_cache = C * row_stride * 4, Eq.10).
@@ -147,6 +150,18 @@ gnnv_status gnnv_allreduce_sum(gnnv_comm* c, float* d_buf, int64_t n, gnnv_strea
 gnnv_status gnnv_cache_build(gnnv_graph* g, double ratio, int32_t policy, int32_t placement,
                              gnnv_comm* comm, int32_t virtual_shards, gnnv_cache** out);
 gnnv_status gnnv_cache_free(gnnv_cache* c);
+/* SHARDED across GPUs (north_star: "the feature cache is sharded across the
+ * GPUs' HBM and read peer-to-peer over NVLink"): rank r holds
+ * the rows of degree rank i = j*G + r at row j, and the gather kernel reads
+ * the other ranks' rows in place through CUDA IPC mappings (one-sided
+ * NVLink loads, no collective on the data path).  With an NCCL comm,
+ * gnnv_cache_build exchanges the IPC handles itself (all-gather, collective
+ * over all ranks).  With a host-only comm the caller all-gathers the 64-byte
+ * handles of gnnv_cache_ipc_handle (rank order, world * 64 bytes) and passes
+ * them to gnnv_cache_open_peers; gnnv_gather / trainer creation fail with
+ * STATE until then.  Both synchronous; STATE unless placement is SHARDED. */
+gnnv_status gnnv_cache_ipc_handle(const gnnv_cache* c, void* out64);
+gnnv_status gnnv_cache_open_peers(gnnv_cache* c, const void* handles);
 typedef struct {
   int64_t capacity;     /* C: cached rows over all shards */
   int64_t local_rows;   /* rows resident on this device */

@@ -59,6 +59,7 @@ struct NcclApi {
   decltype(&ncclCommInitRank) commInitRank = nullptr;
   decltype(&ncclCommDestroy) commDestroy = nullptr;
   decltype(&ncclAllReduce) allReduce = nullptr;
+  decltype(&ncclAllGather) allGather = nullptr;
   decltype(&ncclGetErrorString) errStr = nullptr;
 };
 
@@ -78,9 +79,10 @@ static NcclApi& nccl() {
     api.commInitRank = (decltype(api.commInitRank))dlsym(api.lib, "ncclCommInitRank");
     api.commDestroy = (decltype(api.commDestroy))dlsym(api.lib, "ncclCommDestroy");
     api.allReduce = (decltype(api.allReduce))dlsym(api.lib, "ncclAllReduce");
+    api.allGather = (decltype(api.allGather))dlsym(api.lib, "ncclAllGather");
     api.errStr = (decltype(api.errStr))dlsym(api.lib, "ncclGetErrorString");
   });
-  if (!api.lib || !api.getUniqueId || !api.commInitRank || !api.allReduce)
+  if (!api.lib || !api.getUniqueId || !api.commInitRank || !api.allReduce || !api.allGather)
     throw Error{GNNV_ERR_COMM, "NCCL library not found (set GNNV_NCCL_LIB or preload libnccl.so.2)"};
   return api;
 }
@@ -213,12 +215,14 @@ gnnv_status gnnv_comm_unique_id(void* out128) {
 
 gnnv_status gnnv_comm_init(int32_t rank, int32_t world, const void* uid, int32_t device, gnnv_comm** out) {
   return guarded([&] {
-    GNNV_REQUIRE(out && uid && world >= 1 && rank >= 0 && rank < world, GNNV_ERR_PARAM, "comm_init: bad rank/world");
+    GNNV_REQUIRE(out && world >= 1 && rank >= 0 && rank < world, GNNV_ERR_PARAM, "comm_init: bad rank/world");
     GNNV_TRY_CUDA(cudaSetDevice(device));
-    ncclUniqueId id;
-    memcpy(&id, uid, sizeof(id));
     ncclComm_t comm = nullptr;
-    nccl_check(nccl().commInitRank(&comm, world, id, rank), "ncclCommInitRank");
+    if (uid) {  // NULL: a host-only comm (rank/world; the caller exchanges data)
+      ncclUniqueId id;
+      memcpy(&id, uid, sizeof(id));
+      nccl_check(nccl().commInitRank(&comm, world, id, rank), "ncclCommInitRank");
+    }
     gnnv_comm* c = new gnnv_comm();
     c->rank = rank;
     c->world = world;
@@ -244,11 +248,35 @@ gnnv_status gnnv_allreduce_sum(gnnv_comm* c, float* d_buf, int64_t n, gnnv_strea
   return guarded([&] {
     GNNV_REQUIRE(c && d_buf && n >= 0, GNNV_ERR_PARAM, "allreduce: bad args");
     if (c->world == 1 || n == 0) return;
+    GNNV_REQUIRE(c->nccl, GNNV_ERR_STATE, "allreduce: host-only comm (created without an NCCL id)");
     nccl_check(nccl().allReduce(d_buf, d_buf, (size_t)n, ncclFloat32, ncclSum, (ncclComm_t)c->nccl,
                                 (cudaStream_t)s),
                "ncclAllReduce");
   });
 }
+
+}  // extern "C"
+
+namespace gnnv {
+// all-gather `bytes` per rank through NCCL (synchronous; setup path only)
+void comm_allgather_bytes(gnnv_comm* c, const void* mine, void* all, size_t bytes) {
+  GNNV_REQUIRE(c && c->nccl, GNNV_ERR_STATE, "allgather: host-only comm");
+  char* d = (char*)dmalloc(bytes * (c->world + 1), "allgather buffer");
+  cudaStream_t s = nullptr;
+  try {
+    GNNV_TRY_CUDA(cudaMemcpy(d, mine, bytes, cudaMemcpyHostToDevice));
+    nccl_check(nccl().allGather(d, d + bytes, bytes, ncclChar, (ncclComm_t)c->nccl, s), "ncclAllGather");
+    GNNV_TRY_CUDA(cudaStreamSynchronize(s));
+    GNNV_TRY_CUDA(cudaMemcpy(all, d + bytes, bytes * c->world, cudaMemcpyDeviceToHost));
+  } catch (...) {
+    dfree(d);
+    throw;
+  }
+  dfree(d);
+}
+}  // namespace gnnv
+
+extern "C" {
 
 // ----------------------------------------------------------------- blocks
 gnnv_status gnnv_blocks_create(gnnv_graph* g, int32_t max_seeds, const int32_t* fanouts, int32_t L,

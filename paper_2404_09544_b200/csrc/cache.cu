@@ -11,6 +11,8 @@
 // degree-rank order (slot i holds the vertex of rank i); with G shards,
 // shard o holds ranks i = j*G + o at row j.  slot_map[v] = rank or -1.
 // Misses are read zero-copy from the pinned, device-mapped host table.
+#include <string.h>
+
 #include <cub/device/device_radix_sort.cuh>
 
 #include "common.cuh"
@@ -122,9 +124,45 @@ void launch_gather(const gnnv_cache* c, const gnnv_blocks* b, float* d_X, int64_
 
 }  // namespace gnnv
 
+namespace gnnv {
+static void open_peers(gnnv_cache* c, const cudaIpcMemHandle_t* handles) {
+  for (int o = 0; o < c->world; ++o) {
+    if (o == c->rank || c->shards[o]) continue;
+    void* p = nullptr;
+    GNNV_TRY_CUDA(cudaIpcOpenMemHandle(&p, handles[o], cudaIpcMemLazyEnablePeerAccess));
+    c->shards[o] = (float*)p;
+    c->shard_ipc[o] = true;
+  }
+  GNNV_TRY_CUDA(cudaMemcpy((void*)c->d_shard_ptrs, c->shards.data(), c->world * sizeof(float*),
+                           cudaMemcpyHostToDevice));
+  c->peers_ready = true;
+}
+}  // namespace gnnv
+
 using namespace gnnv;
 
 extern "C" {
+
+gnnv_status gnnv_cache_ipc_handle(const gnnv_cache* c, void* out64) {
+  return guarded([&] {
+    GNNV_REQUIRE(c && out64, GNNV_ERR_PARAM, "cache_ipc_handle: null");
+    GNNV_REQUIRE(c->placement == GNNV_PLACE_SHARDED, GNNV_ERR_STATE, "cache_ipc_handle: placement is not SHARDED");
+    GNNV_TRY_CUDA(cudaSetDevice(c->g->device));
+    cudaIpcMemHandle_t h;
+    GNNV_TRY_CUDA(cudaIpcGetMemHandle(&h, c->shards[c->rank]));
+    static_assert(sizeof(h) == 64, "cudaIpcMemHandle_t is 64 bytes");
+    memcpy(out64, &h, sizeof(h));
+  });
+}
+
+gnnv_status gnnv_cache_open_peers(gnnv_cache* c, const void* handles) {
+  return guarded([&] {
+    GNNV_REQUIRE(c && handles, GNNV_ERR_PARAM, "cache_open_peers: null");
+    GNNV_REQUIRE(c->placement == GNNV_PLACE_SHARDED, GNNV_ERR_STATE, "cache_open_peers: placement is not SHARDED");
+    GNNV_TRY_CUDA(cudaSetDevice(c->g->device));
+    open_peers(c, static_cast<const cudaIpcMemHandle_t*>(handles));
+  });
+}
 
 gnnv_status gnnv_cache_build(gnnv_graph* g, double ratio, int32_t policy, int32_t placement, gnnv_comm* comm,
                              int32_t virtual_shards, gnnv_cache** out) {
@@ -140,12 +178,10 @@ gnnv_status gnnv_cache_build(gnnv_graph* g, double ratio, int32_t policy, int32_
                  "cache_build: unknown placement");
     int G = 1, me = 0;
     if (placement == GNNV_PLACE_SHARDED) {
-      GNNV_REQUIRE(comm, GNNV_ERR_PARAM, "cache_build: SHARDED placement needs a comm");
-      G = comm->world;
-      me = comm->rank;
-      GNNV_REQUIRE(G == 1, GNNV_ERR_UNSUPPORTED,
-                   "cache_build: cross-GPU SHARDED placement (NVLink peer reads) is not built in this round; "
-                   "use REPLICA or SHARDED_LOCAL");
+      if (comm) {  // no comm: one rank, one shard
+        G = comm->world;
+        me = comm->rank;
+      }
     } else if (placement == GNNV_PLACE_SHARDED_LOCAL) {
       GNNV_REQUIRE(virtual_shards >= 1 && virtual_shards <= 64, GNNV_ERR_PARAM, "cache_build: virtual_shards in [1,64]");
       G = virtual_shards;
@@ -200,6 +236,19 @@ gnnv_status gnnv_cache_build(gnnv_graph* g, double ratio, int32_t policy, int32_
       c->d_shard_ptrs = (const float**)dmalloc(G * sizeof(float*), "shard pointers");
       GNNV_TRY_CUDA(cudaMemcpy((void*)c->d_shard_ptrs, c->shards.data(), G * sizeof(float*), cudaMemcpyHostToDevice));
       GNNV_TRY_CUDA(cudaDeviceSynchronize());
+      if (placement == GNNV_PLACE_SHARDED && G > 1) {
+        // peers' shards are read in place over NVLink: export this rank's
+        // shard as a CUDA IPC handle, all-gather the handles (NCCL), map the
+        // others.  A host-only comm leaves this to gnnv_cache_open_peers.
+        c->peers_ready = false;
+        if (comm->nccl) {
+          std::vector<cudaIpcMemHandle_t> all(G);
+          cudaIpcMemHandle_t mine;
+          GNNV_TRY_CUDA(cudaIpcGetMemHandle(&mine, c->shards[me]));
+          comm_allgather_bytes(comm, &mine, all.data(), sizeof(mine));
+          open_peers(c, all.data());
+        }
+      }
     } catch (...) {
       gnnv_cache_free(c);
       throw;
@@ -212,8 +261,10 @@ gnnv_status gnnv_cache_free(gnnv_cache* c) {
   if (!c) return GNNV_OK;
   dfree(c->d_slot);
   dfree(c->d_order);
-  for (size_t o = 0; o < c->shards.size(); ++o)
+  for (size_t o = 0; o < c->shards.size(); ++o) {
     if (c->shard_owned[o]) dfree(c->shards[o]);
+    if (c->shard_ipc[o]) cudaIpcCloseMemHandle(c->shards[o]);
+  }
   dfree((void*)c->d_shard_ptrs);
   delete c;
   return GNNV_OK;
@@ -239,6 +290,7 @@ gnnv_status gnnv_gather(const gnnv_cache* c, const gnnv_blocks* b, float* d_X, i
     GNNV_REQUIRE(b->sampled, GNNV_ERR_STATE, "gather: gnnv_sample has not run on these blocks");
     GNNV_REQUIRE(c->g == b->g, GNNV_ERR_STATE, "gather: cache and blocks belong to different graphs");
     GNNV_REQUIRE(((uintptr_t)d_X & 15) == 0, GNNV_ERR_PARAM, "gather: d_X must be 16-byte aligned");
+    GNNV_REQUIRE(c->peers_ready, GNNV_ERR_STATE, "gather: SHARDED peers not mapped (gnnv_cache_open_peers)");
     launch_gather(c, b, d_X, d_stats, (cudaStream_t)s);
   });
 }

@@ -89,6 +89,9 @@ struct gnnv_comm {
   void* nccl = nullptr;  // ncclComm_t
 };
 
+namespace gnnv {
+void comm_allgather_bytes(gnnv_comm* c, const void* mine, void* all, size_t bytes);
+}
 struct gnnv_cache {
   gnnv_graph* g = nullptr;
   int64_t capacity = 0;
@@ -100,6 +103,7 @@ struct gnnv_cache {
   std::vector<bool> shard_owned;
   std::vector<bool> shard_ipc;
   const float** d_shard_ptrs = nullptr;  // device array [world]
+  bool peers_ready = true;               // SHARDED: every peer's shard mapped
 };
 
 struct gnnv_blocks {

@@ -118,6 +118,7 @@ gnnv_status gnnv_trainer_create(gnnv_graph* g, gnnv_cache* c, const gnnv_model_d
                                 gnnv_comm* comm, gnnv_trainer** out) {
   return guarded([&] {
     GNNV_REQUIRE(g && c && md && host_params && out, GNNV_ERR_PARAM, "trainer_create: null");
+    GNNV_REQUIRE(c->peers_ready, GNNV_ERR_STATE, "trainer_create: SHARDED cache peers not mapped");
     GNNV_REQUIRE(c->g == g, GNNV_ERR_STATE, "trainer_create: cache belongs to another graph");
     GNNV_REQUIRE(md->L >= 1 && md->L <= GNNV_MAX_LAYERS, GNNV_ERR_PARAM, "trainer_create: L in [1, 8]");
     GNNV_REQUIRE(md->dims[0] == g->d, GNNV_ERR_PARAM, "trainer_create: dims[0] must equal the feature dim");

@@ -91,6 +91,8 @@ _SIGS = {
     "gnnv_comm_free": (I32, [VP]),
     "gnnv_allreduce_sum": (I32, [VP, VP, I64, VP]),
     "gnnv_cache_build": (I32, [VP, F64, I32, I32, VP, I32, PP]),
+    "gnnv_cache_ipc_handle": (I32, [VP, VP]),
+    "gnnv_cache_open_peers": (I32, [VP, VP]),
     "gnnv_cache_free": (I32, [VP]),
     "gnnv_cache_info": (I32, [VP, C.POINTER(CacheView)]),
     "gnnv_blocks_create": (I32, [VP, I32, VP, I32, PP]),
@@ -238,10 +240,14 @@ class Graph:
 
 
 class Comm:
-    def __init__(self, rank: int, world: int, unique_id: bytes, device: int):
-        preload_nccl()
+    def __init__(self, rank: int, world: int, unique_id: Optional[bytes], device: int):
+        """unique_id None: a host-only comm (no NCCL; see gnnv_comm_init)."""
         h = C.c_void_p()
-        buf = C.create_string_buffer(bytes(unique_id), 128)
+        if unique_id is None:
+            buf = None
+        else:
+            preload_nccl()
+            buf = C.create_string_buffer(bytes(unique_id), 128)
         _check(load().gnnv_comm_init(rank, world, buf, device, C.byref(h)))
         self.h, self.rank, self.world = h, rank, world
 
@@ -273,6 +279,17 @@ class Cache:
         v = CacheView()
         _check(load().gnnv_cache_info(self.h, C.byref(v)))
         return v
+
+    def ipc_handle(self) -> bytes:
+        """SHARDED: this rank's 64-byte CUDA IPC handle of its shard."""
+        buf = C.create_string_buffer(64)
+        _check(load().gnnv_cache_ipc_handle(self.h, buf))
+        return buf.raw
+
+    def open_peers(self, handles: Sequence[bytes]):
+        """SHARDED with a host-only comm: map the other ranks' shards."""
+        blob = b"".join(bytes(h) for h in handles)
+        _check(load().gnnv_cache_open_peers(self.h, C.create_string_buffer(blob, len(blob))))
 
     def free(self):
         if getattr(self, "h", None):
