@@ -73,6 +73,19 @@ def load_peaks():
         return dict(hbm=6650.0, bf16=1590.0, bf16_sust=1400.0, src="fallback (B200_PROFILING.md)")
 
 
+def load_traffic(workload: str):
+    """Per-segment DRAM bytes of one step from the committed ncu capture
+    (tools/ncu_traffic.py -> profiles/r01_ncu_traffic.json), or {}."""
+    path = os.path.join(ROOT, "profiles", "r01_ncu_traffic.json")
+    try:
+        d = json.load(open(path))
+        if d.get("workload") == workload:
+            return {k: v["dram_bytes"] for k, v in d["segments"].items()}
+    except Exception:
+        pass
+    return {}
+
+
 class ClockSampler:
     """nvidia-smi clocks + throttle reasons sampled during the timed region."""
 
@@ -429,6 +442,7 @@ def main():
         acc["misses"] += nL - hit
     sizes = {k: (v / nsz) for k, v in acc.items()}
     peaks = load_peaks()
+    traffic = load_traffic(f"{cfg['name']}/{args.prec}")
     # dominant kernel segment of the timed region
     seg_ms = {k: v[0] / max(1, v[1]) for k, v in segs.items()}
     seg_tot = {k: v[0] for k, v in segs.items()}
@@ -446,7 +460,8 @@ def main():
         avg_ms = seg_ms[name]
         achieved = amount / (avg_ms / 1000.0) / (1e9 if unit == "GB/s" else 1e12)
         r = {"kernel": name, "bound": bound, "achieved": achieved, "peak": peak, "unit": unit,
-             "frac": achieved / peak, "traffic": None, "avg_ms": avg_ms,
+             "frac": achieved / peak, "traffic": traffic.get(name[3:] if name.startswith("pf_") else name),
+             "avg_ms": avg_ms,
              "share_of_step": tot / max(1e-9, main_tot),
              "algorithmic_per_launch": amount}
         if name.startswith("pf_"):
