@@ -165,6 +165,10 @@ void launch_sample(gnnv_graph* g, gnnv_blocks* b, const int32_t* d_seeds, int32_
                    cudaStream_t s);
 // cache.cu
 void launch_gather(const gnnv_cache* c, const gnnv_blocks* b, float* d_X, int64_t* d_stats, cudaStream_t s);
+// Cap on the grid of the sampling / gather kernels (0 = none); the trainer
+// sets it around a prefetch so the overlapped batch occupies few SMs.
+void set_grid_cap(int blocks);
+int grid_cap();
 // spmm.cu
 void launch_spmm_fwd(const int32_t* d_indptr, const int32_t* d_indices, const int32_t* d_ndst, int64_t max_dst,
                      const float* H, int32_t ldh, float* A, int32_t lda, int32_t d, int32_t kind, int32_t aggr,

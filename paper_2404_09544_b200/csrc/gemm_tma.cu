@@ -159,14 +159,15 @@ struct Params {
   // dx epilogue
   float *Y1, *Y2;
   int ld1, ld2;
-  // dw
-  float* partial;
-  int splits, rows_p, ablocks;  // ablocks: valid 32-wide i blocks (X1 then X2)
+  // dw: outputs accumulated atomically (zeroed by the host side first)
+  float* dW;
+  float* db;
+  int K1;
+  int splits, ablocks;  // ablocks: valid 32-wide i blocks (X1 then X2)
   // dw with a fused ReLU mask: G' = G * bit and db partials per split; th =
   // the [M x nwp] uint32 bit mask (TMA box DW_KR x nwp)
   CUtensorMap th;
   int mask, nwp;
-  float* dbpart;  // [splits][BN]
   // fwd with relu: bit mask output (NULL: none)
   uint32_t* bits;
   int bits_ld;
@@ -550,8 +551,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_tma_gemm(const __grid_constant_
             dbacc[jb][ci] = v;
           }
           if (gx >= MT * 4 && gx < ngroups && rq == 0) {
-            float* o = p.dbpart + (int64_t)blockIdx.x * BN + (gx - MT * 4) * 32 + 4 * cq;
-            *reinterpret_cast<float4*>(o) = make_float4(dbacc[jb][0], dbacc[jb][1], dbacc[jb][2], dbacc[jb][3]);
+            const int col = (gx - MT * 4) * 32 + 4 * cq;
+#pragma unroll
+            for (int ci = 0; ci < 4; ++ci)
+              if (col + ci < p.N) atomicAdd(p.db + col + ci, dbacc[jb][ci]);
           }
         }
       }
@@ -560,20 +563,33 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_tma_gemm(const __grid_constant_
       const int q = warp & 3;
       const int half = (warp - 2) >> 2;
       const int row = q * 32 + lane;
-      for (int mt = 0; mt < MT; ++mt) {
+      // split-K partial sums go straight into dW with vector float atomics
+      // (red.global.add): row i' of the [X1 blocks | X2 blocks] space is
+      // weight row k = i' (X1) or K1 + i' - 32*nkb1 (X2); padding rows skip.
+      // (The backward's dH is accumulated with atomics too, so dW has no
+      // fixed summation order to preserve.)
+      for (int mt = 0; mt < MT && nkb > 0; ++mt) {
         const int irow = (ig * MT + mt) * BM + row;
-        float* dst = p.partial + ((int64_t)blockIdx.x * p.rows_p + irow) * BN;
+        int k = -1;
+        if (irow < 32 * p.nkb1) {
+          if (irow < p.K1) k = irow;
+        } else if (p.two && irow - 32 * p.nkb1 < p.K1) {
+          k = p.K1 + irow - 32 * p.nkb1;
+        }
+        float* dst = p.dW + (int64_t)(k < 0 ? 0 : k) * p.N;
         for (int c = half * 32; c < BN; c += 64) {
           float v[32];
-          if (nkb > 0) {
-            tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(mt * BN + c), v);
+          tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(mt * BN + c), v);
+          if (k < 0) continue;
+          if ((p.N & 3) == 0) {
+#pragma unroll
+            for (int j = 0; j < 32; j += 4)
+              if (c + j < p.N) atomicAdd(reinterpret_cast<float4*>(dst + c + j), make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]));
           } else {
 #pragma unroll
-            for (int j = 0; j < 32; ++j) v[j] = 0.f;
+            for (int j = 0; j < 32; ++j)
+              if (c + j < p.N) atomicAdd(dst + c + j, v[j]);
           }
-#pragma unroll
-          for (int j = 0; j < 32; j += 4)
-            *reinterpret_cast<float4*>(dst + c + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
         }
       }
     }
@@ -621,39 +637,6 @@ __global__ void k_bt_dx(const float* __restrict__ W, int K1, int ld1, int ld2, i
     Bd[t] = (r >= 0 && k < N) ? W[(int64_t)r * N + k] : 0.f;
   }
 }
-// dW: partial[split][i'][n] -> dW[k][n] with i' = k (X1) or 32*nkb1 + (k-K1)
-// (X2).  Block (32, 8) = 32 columns x 8 split-groups of one k row, fixed
-// summation order; grid (ceil(N/32), Ktot).
-__global__ void __launch_bounds__(256) k_dw_reduce_tma(const float* __restrict__ partial, int splits, int rows_p,
-                                                       int BN, int K1, int nkb1, int N, float* dW) {
-  __shared__ float sh[8][33];
-  const int k = blockIdx.y, n = blockIdx.x * 32 + threadIdx.x;
-  const int ip = k < K1 ? k : 32 * nkb1 + (k - K1);
-  // four independent loads in flight per thread (a fixed association
-  // order: the result stays deterministic)
-  float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
-  if (n < N) {
-    const float* src = partial + (int64_t)ip * BN + n;
-    const int64_t zs = (int64_t)rows_p * BN;
-    int z = threadIdx.y;
-    for (; z + 24 < splits; z += 32) {
-      a0 += src[z * zs];
-      a1 += src[(z + 8) * zs];
-      a2 += src[(z + 16) * zs];
-      a3 += src[(z + 24) * zs];
-    }
-    for (; z < splits; z += 8) a0 += src[z * zs];
-  }
-  sh[threadIdx.y][threadIdx.x] = (a0 + a1) + (a2 + a3);
-  __syncthreads();
-  if (threadIdx.y == 0 && n < N) {
-    float t = 0.f;
-#pragma unroll
-    for (int y = 0; y < 8; ++y) t += sh[y][threadIdx.x];
-    dW[(int64_t)k * N + n] = t;
-  }
-}
-
 // ------------------------------------------------------ host helpers
 static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
@@ -699,7 +682,7 @@ struct Arena {
     return buf;
   }
 };
-static Arena g_img, g_part;
+static Arena g_img;
 
 static size_t smem_bytes(int mode, int BN, int mask, int nwp) {
   const int S = mode == MODE_DW ? DW_STAGES : FWD_STAGES;
@@ -806,9 +789,12 @@ bool gemm_dw_tma(const GemmDwArgs& a, cudaStream_t s) {
   const int rows_p = rup(ablocks * 32, BM * DW_MT);
   const int igroups = rows_p / (BM * DW_MT);
   const int64_t nkbm = ceil_div(std::max<int64_t>(a.max_M, 1), DW_KR);
-  const int splits = (int)std::max<int64_t>(1, std::min<int64_t>(nkbm, (int64_t)num_sms() / igroups));
-  const size_t part_f = (size_t)splits * rows_p * BN;
-  float* partial = (float*)g_part.get((part_f + (size_t)splits * BN) * sizeof(float), s);
+  // >= 8 k-blocks (128 graph rows) per split: small layers use fewer CTAs
+  // rather than many short ones whose atomic flush dominates
+  const int splits =
+      (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(nkbm, 8), (int64_t)num_sms() / igroups));
+  const int Ktot = a.X2 ? 2 * a.K1 : a.K1;
+  GNNV_TRY_CUDA(cudaMemsetAsync(a.dW, 0, (size_t)Ktot * a.N * sizeof(float), s));
   Params p{};
   if (a.mask_bits) {
     GNNV_REQUIRE(a.mask_ld == mask_words(a.N), GNNV_ERR_PARAM, "dW: mask bits row stride");
@@ -816,10 +802,13 @@ bool gemm_dw_tma(const GemmDwArgs& a, cudaStream_t s) {
     p.nwp = a.mask_ld;
     p.th = make_map(reinterpret_cast<const float*>(a.mask_bits), a.max_M, a.mask_ld, a.mask_ld, DW_KR, a.mask_ld,
                     false);
-    p.dbpart = partial + part_f;
   } else if (a.db_fused) {
     p.dbsum = 1;
-    p.dbpart = partial + part_f;
+  }
+  if (p.mask || p.dbsum) {
+    GNNV_REQUIRE(a.db, GNNV_ERR_PARAM, "dW: db output required");
+    GNNV_TRY_CUDA(cudaMemsetAsync(a.db, 0, (size_t)a.N * sizeof(float), s));
+    p.db = a.db;
   }
   p.ta1 = make_map(a.X1, a.max_M, a.K1, a.ld1, DW_KR, BM, false);
   p.ta2 = a.X2 ? make_map(a.X2, a.max_M, a.K1, a.ld2, DW_KR, BM, false) : p.ta1;
@@ -828,17 +817,13 @@ bool gemm_dw_tma(const GemmDwArgs& a, cudaStream_t s) {
   p.nkb1 = nkb1;
   p.BN = BN;
   p.dM = a.d_M;
-  p.partial = partial;
+  p.dW = a.dW;
+  p.K1 = a.K1;
+  p.N = a.N;
   p.splits = splits;
-  p.rows_p = rows_p;
   p.ablocks = ablocks;
   p.dbg = debug_flags();
   launch<MODE_DW>(p, dim3((unsigned)splits, (unsigned)igroups), s);
-  const int Ktot = a.X2 ? 2 * a.K1 : a.K1;
-  k_dw_reduce_tma<<<dim3((a.N + 31) / 32, Ktot), dim3(32, 8), 0, s>>>(partial, splits, rows_p, BN, a.K1, nkb1, a.N,
-                                                                       a.dW);
-  GNNV_CHECK_LAUNCH();
-  if (a.mask_bits || a.db_fused) launch_colsum_reduce(p.dbpart, splits, BN, a.N, a.db, s);
   return true;
 }
 

@@ -156,8 +156,7 @@ __global__ void __launch_bounds__(256) k_sample_hop_tpr(const int64_t* __restric
                                                         int k, uint64_t seed, int32_t* __restrict__ ell,
                                                         int32_t* __restrict__ cnt, int32_t* tag, uint32_t* own) {
   const int n = sizes[h];
-  const int r = blockIdx.x * blockDim.x + threadIdx.x;
-  if (r >= n) return;
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x) {
   const int v = F[r];
   int64_t beg = 0;
   int d = 0;
@@ -212,6 +211,7 @@ __global__ void __launch_bounds__(256) k_sample_hop_tpr(const int64_t* __restric
   }
   cnt[r] = c;
   own[r] = 0u;
+  }
 }
 
 // Winners of hop h's claims, slot-parallel over the whole hop: slot e of
@@ -261,6 +261,9 @@ __global__ void __launch_bounds__(kScanTile) k_relabel_scan(int64_t N, int h, in
   const int n = sizes[h];
   const int ntiles = (n + kScanTile - 1) / kScanTile;
   unsigned int* ticket = reinterpret_cast<unsigned int*>(status);
+  // tiles are taken in ticket order (the look-back only waits on earlier
+  // tickets), so a capped grid may loop over several tiles
+  for (;;) {
   if (threadIdx.x == 0) s_tile = (int)atomicAdd(ticket, 1u);
   __syncthreads();
   const int tile = s_tile;
@@ -378,6 +381,8 @@ __global__ void __launch_bounds__(kScanTile) k_relabel_scan(int64_t N, int h, in
     sizes[L + 1 + h] = (int)tot_b;
     indptr[n] = (int32_t)tot_b;
   }
+  __syncthreads();  // shared state is reused by the next tile
+  }
 }
 
 __global__ void k_map(int hp, int kp, const int32_t* sizes, const int32_t* __restrict__ ellp,
@@ -397,10 +402,14 @@ __global__ void k_reset(const int32_t* __restrict__ F, const int32_t* sizes, int
 
 // One work item per thread / row group (no grid-stride caps): short-lived
 // blocks let the step's higher-priority kernels interleave with a prefetch.
+static int g_grid_cap = 0;  // 0: none (set around a prefetch, see set_grid_cap)
 static int grid_for(int64_t work, int per_block, int /*max_blocks*/) {
   int64_t g = ceil_div(std::max<int64_t>(work, 1), per_block);
-  return (int)std::min<int64_t>(g, INT32_MAX);
+  return (int)std::min<int64_t>(g, g_grid_cap > 0 ? g_grid_cap : INT32_MAX);
 }
+
+void set_grid_cap(int blocks) { g_grid_cap = blocks; }
+int grid_cap() { return g_grid_cap; }
 
 void launch_sample(gnnv_graph* g, gnnv_blocks* b, const int32_t* d_seeds, int32_t n_seeds, uint64_t rng_seed,
                    cudaStream_t s) {
@@ -444,7 +453,7 @@ void launch_sample(gnnv_graph* g, gnnv_blocks* b, const int32_t* d_seeds, int32_
     k_winners<<<grid_for(rows_ub * k, 256, 0), 256, 0, s>>>(g->n, h, k, b->d_sizes, b->d_ell, b->d_cnt, b->d_tag,
                                                              b->d_own[h]);
     GNNV_CHECK_LAUNCH();
-    k_relabel_scan<<<tiles_ub, kScanTile, 0, s>>>(g->n, h, k, L, b->d_ell, b->d_cnt, b->d_tag, b->d_F,
+    k_relabel_scan<<<g_grid_cap > 0 ? std::min<int>(tiles_ub, g_grid_cap) : tiles_ub, kScanTile, 0, s>>>(g->n, h, k, L, b->d_ell, b->d_cnt, b->d_tag, b->d_F,
                                                   b->d_indptr[h], b->d_own[h], b->d_sizes, b->d_scan);
     GNNV_CHECK_LAUNCH();
   }

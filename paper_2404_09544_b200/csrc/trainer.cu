@@ -358,11 +358,17 @@ gnnv_status gnnv_trainer_prefetch(gnnv_trainer* t, const int32_t* seeds, int32_t
     Timeline* tl = t->tl.on ? &t->tl_side : nullptr;
     const int32_t* d_seeds = stage_seeds(t, k, seeds, n_seeds, seeds_on_host, t->side, tl);
     if (tl) tl->mark(t->side, "pf_sample");
+    static const int pf_cap = [] {
+      const char* e = getenv("GNNV_PF_BLOCKS");
+      return e ? atoi(e) : 0;
+    }();
+    set_grid_cap(pf_cap);
     launch_sample(g, t->bb[k], d_seeds, n_seeds, rng_seed, t->side);
     t->bb[k]->sampled = true;
     GNNV_TRY_CUDA(cudaMemsetAsync(t->d_statsb[k], 0, 4 * sizeof(int64_t), t->side));
     if (tl) tl->mark(t->side, "pf_gather");
     launch_gather(t->c, t->bb[k], t->X[k], t->d_statsb[k], t->side);
+    set_grid_cap(0);
     if (tl) tl->mark(t->side, "end");
     GNNV_TRY_CUDA(cudaEventRecord(t->ev_ready[k], t->side));
     t->pending = true;
