@@ -70,15 +70,47 @@ __global__ void k_init_seeds(const int32_t* __restrict__ seeds, int32_t n_seeds,
   if (blockIdx.x == 0 && threadIdx.x == 0) sizes[0] = n_seeds;
 }
 
+// Four consecutive slots per thread: one 16-byte load of their sampled ids,
+// then four independent tag lookups in flight (the slot passes are chains of
+// dependent random loads; more of them per thread means fewer waves).
+__device__ __forceinline__ void load4(const int32_t* __restrict__ a, int64_t e0, int64_t n, int* v) {
+  if (e0 + 3 < n) {
+    const int4 q = __ldg(reinterpret_cast<const int4*>(a + e0));
+    v[0] = q.x;
+    v[1] = q.y;
+    v[2] = q.z;
+    v[3] = q.w;
+  } else {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) v[j] = e0 + j < n ? __ldg(a + e0 + j) : -1;
+  }
+}
+
 // Map slots of hop hp (rows [0, n_hp)) to local ids.  Flattened over slots.
 __device__ __forceinline__ void map_slots(int64_t t0, int64_t stride, int hp, int kp, const int32_t* sizes,
                                           const int32_t* __restrict__ ellp, const int32_t* __restrict__ cntp,
                                           const int32_t* __restrict__ indptrp, const int32_t* tag,
                                           int32_t* __restrict__ indicesp) {
   const int64_t nslots = (int64_t)sizes[hp] * kp;
-  for (int64_t e = t0; e < nslots; e += stride) {
-    const int r = (int)(e / kp), i = (int)(e - (int64_t)r * kp);
-    if (i < cntp[r]) indicesp[indptrp[r] + i] = tag[ellp[e]];
+  for (int64_t e0 = 4 * t0; e0 < nslots; e0 += 4 * stride) {
+    int u[4], t[4], dst[4];
+    load4(ellp, e0, nslots, u);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int64_t e = e0 + j;
+      dst[j] = -1;
+      t[j] = 0;
+      if (e < nslots) {
+        const int r = (int)(e / kp), i = (int)(e - (int64_t)r * kp);
+        if (i < __ldg(cntp + r)) {
+          dst[j] = __ldg(indptrp + r) + i;
+          t[j] = tag[u[j]];
+        }
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      if (dst[j] >= 0) indicesp[dst[j]] = t[j];
   }
 }
 
@@ -222,13 +254,22 @@ __global__ void __launch_bounds__(256) k_sample_hop_tpr(const int64_t* __restric
 __global__ void k_winners(int64_t N, int h, int k, const int32_t* sizes, const int32_t* __restrict__ ell,
                           const int32_t* __restrict__ cnt, const int32_t* tag, uint32_t* own) {
   const int64_t nslots = (int64_t)sizes[h] * k;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < nslots;
-       e += (int64_t)gridDim.x * blockDim.x) {
-    const int r = (int)(e / k), i = (int)(e - (int64_t)r * k);
-    if (i < __ldg(cnt + r)) {
-      const int u = __ldg(ell + e);
-      if ((uint32_t)u < (uint64_t)N && tag[u] == -(2 + (int)e)) atomicOr(&own[r], 1u << i);
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t e0 = 4 * (blockIdx.x * (int64_t)blockDim.x + threadIdx.x); e0 < nslots; e0 += 4 * stride) {
+    int u[4], t[4], r[4], i[4];
+    bool ok[4];
+    load4(ell, e0, nslots, u);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int64_t e = e0 + j;
+      r[j] = (int)(e / k);
+      i[j] = (int)(e - (int64_t)r[j] * k);
+      ok[j] = e < nslots && i[j] < __ldg(cnt + r[j]) && (uint32_t)u[j] < (uint64_t)N;
+      t[j] = ok[j] ? tag[u[j]] : 0;
     }
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      if (ok[j] && t[j] == -(2 + (int)(e0 + j))) atomicOr(&own[r[j]], 1u << i[j]);
   }
 }
 
@@ -393,10 +434,14 @@ __global__ void k_map(int hp, int kp, const int32_t* sizes, const int32_t* __res
 }
 
 __global__ void k_reset(const int32_t* __restrict__ F, const int32_t* sizes, int L, int64_t N, int32_t* tag) {
-  const int n = sizes[L];
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-    const int v = F[i];
-    if ((uint32_t)v < (uint64_t)N) tag[v] = INT_MIN;
+  const int64_t n = sizes[L];
+  for (int64_t i0 = 4 * (blockIdx.x * (int64_t)blockDim.x + threadIdx.x); i0 < n;
+       i0 += 4 * (int64_t)gridDim.x * blockDim.x) {
+    int v[4];
+    load4(F, i0, n, v);
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      if ((uint32_t)v[j] < (uint64_t)N) tag[v[j]] = INT_MIN;
   }
 }
 
@@ -426,7 +471,7 @@ void launch_sample(gnnv_graph* g, gnnv_blocks* b, const int32_t* d_seeds, int32_
     const int64_t rows_ub = b->max_n[h];
     if (h > 0) {
       const int64_t slots_ub = b->max_n[h - 1] * (int64_t)b->fanouts[h - 1];
-      k_map<<<grid_for(slots_ub, 256, sms * 8), 256, 0, s>>>(h - 1, b->fanouts[h - 1], b->d_sizes, b->d_ell,
+      k_map<<<grid_for(slots_ub, 1024, sms * 8), 256, 0, s>>>(h - 1, b->fanouts[h - 1], b->d_sizes, b->d_ell,
                                                               b->d_cnt, b->d_indptr[h - 1], b->d_tag,
                                                               b->d_indices[h - 1]);
       GNNV_CHECK_LAUNCH();
@@ -441,8 +486,11 @@ void launch_sample(gnnv_graph* g, gnnv_blocks* b, const int32_t* d_seeds, int32_
     } else if (k <= 8) {
       k_sample_hop_tpr<8><<<grid_for(rows_ub, threads, 0), threads, 0, s>>>(
           g->d_indptr, g->d_indices, g->n, b->d_F, b->d_sizes, h, k, rng_seed, b->d_ell, b->d_cnt, b->d_tag, b->d_own[h]);
+    } else if (k <= 16 && rows_ub < 16384) {
+      GNNV_SAMPLE_LAUNCH(16);  // few rows: lanes per row beat rows per thread
     } else if (k <= 16) {
-      GNNV_SAMPLE_LAUNCH(16);
+      k_sample_hop_tpr<16><<<grid_for(rows_ub, threads, 0), threads, 0, s>>>(
+          g->d_indptr, g->d_indices, g->n, b->d_F, b->d_sizes, h, k, rng_seed, b->d_ell, b->d_cnt, b->d_tag, b->d_own[h]);
     } else {
       GNNV_SAMPLE_LAUNCH(32);
     }
@@ -450,7 +498,7 @@ void launch_sample(gnnv_graph* g, gnnv_blocks* b, const int32_t* d_seeds, int32_
     GNNV_CHECK_LAUNCH();
     GNNV_TRY_CUDA(cudaMemsetAsync(b->d_scan, 0, b->scan_words * sizeof(unsigned long long), s));
     const int tiles_ub = (int)ceil_div(rows_ub, kScanTile);
-    k_winners<<<grid_for(rows_ub * k, 256, 0), 256, 0, s>>>(g->n, h, k, b->d_sizes, b->d_ell, b->d_cnt, b->d_tag,
+    k_winners<<<grid_for(rows_ub * k, 1024, 0), 256, 0, s>>>(g->n, h, k, b->d_sizes, b->d_ell, b->d_cnt, b->d_tag,
                                                              b->d_own[h]);
     GNNV_CHECK_LAUNCH();
     k_relabel_scan<<<g_grid_cap > 0 ? std::min<int>(tiles_ub, g_grid_cap) : tiles_ub, kScanTile, 0, s>>>(g->n, h, k, L, b->d_ell, b->d_cnt, b->d_tag, b->d_F,
@@ -458,10 +506,10 @@ void launch_sample(gnnv_graph* g, gnnv_blocks* b, const int32_t* d_seeds, int32_
     GNNV_CHECK_LAUNCH();
   }
   const int64_t slots_ub = b->max_n[L - 1] * (int64_t)b->fanouts[L - 1];
-  k_map<<<grid_for(slots_ub, 256, sms * 8), 256, 0, s>>>(L - 1, b->fanouts[L - 1], b->d_sizes, b->d_ell, b->d_cnt,
+  k_map<<<grid_for(slots_ub, 1024, sms * 8), 256, 0, s>>>(L - 1, b->fanouts[L - 1], b->d_sizes, b->d_ell, b->d_cnt,
                                                           b->d_indptr[L - 1], b->d_tag, b->d_indices[L - 1]);
   GNNV_CHECK_LAUNCH();
-  k_reset<<<grid_for(b->max_n[L], 256, sms * 8), 256, 0, s>>>(b->d_F, b->d_sizes, L, g->n, b->d_tag);
+  k_reset<<<grid_for(b->max_n[L], 1024, sms * 8), 256, 0, s>>>(b->d_F, b->d_sizes, L, g->n, b->d_tag);
   GNNV_CHECK_LAUNCH();
 }
 

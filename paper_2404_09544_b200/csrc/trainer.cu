@@ -5,6 +5,7 @@
 // frontier sizes kept on the device (no host round trip inside the step).
 // Per-phase CUDA events give the Eq.4-8 decomposition:
 // t_sample, t_transfer (gather), t_compute (fwd + loss + bwd + update).
+#include <cuda.h>
 #include <string.h>
 
 #include "common.cuh"
@@ -76,6 +77,52 @@ static gnnv_layer_desc layer_desc(const gnnv_trainer* t, int i) {
   ld.act = i < t->md.L ? GNNV_ACT_RELU : GNNV_ACT_NONE;
   ld.prec = t->md.prec;
   return ld;
+}
+
+// The prefetch (side) stream.  Lowest priority, so that the prefetch fills
+// the SMs the step leaves idle.  With GNNV_PF_SMS=n (n > 0) the stream
+// belongs to a green context confined to n SMs (driver API, CUDA 12.4+):
+// the prefetch then never occupies more than n SMs, and the step's
+// persistent GEMM CTAs do not wait for SMs drained of prefetch blocks.
+template <typename F>
+static F drv(const char* name) {
+  void* p = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  GNNV_TRY_CUDA(cudaGetDriverEntryPoint(name, &p, cudaEnableDefault, &q));
+  GNNV_REQUIRE(p && q == cudaDriverEntryPointSuccess, GNNV_ERR_CUDA, std::string("driver entry point ") + name);
+  return reinterpret_cast<F>(p);
+}
+
+static cudaStream_t make_side_stream(int device) {
+  int lo = 0, hi = 0;
+  GNNV_TRY_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+  const char* e = getenv("GNNV_PF_SMS");
+  const int sms = e ? atoi(e) : 0;
+  if (sms > 0) {
+    auto getdev = drv<CUresult (*)(CUdevice*, int)>("cuDeviceGet");
+    auto getres = drv<CUresult (*)(CUdevice, CUdevResource*, CUdevResourceType)>("cuDeviceGetDevResource");
+    auto split = drv<CUresult (*)(CUdevResource*, unsigned*, const CUdevResource*, CUdevResource*, unsigned, unsigned)>(
+        "cuDevSmResourceSplitByCount");
+    auto gendesc = drv<CUresult (*)(CUdevResourceDesc*, CUdevResource*, unsigned)>("cuDevResourceGenerateDesc");
+    auto create = drv<CUresult (*)(CUgreenCtx*, CUdevResourceDesc, CUdevice, unsigned)>("cuGreenCtxCreate");
+    auto mkstream = drv<CUresult (*)(CUstream*, CUgreenCtx, unsigned, int)>("cuGreenCtxStreamCreate");
+    CUdevice dev;
+    CUdevResource all, part, rest;
+    unsigned n = 1;
+    CUdevResourceDesc desc;
+    CUgreenCtx gc;
+    CUstream st;
+    GNNV_REQUIRE(getdev(&dev, device) == CUDA_SUCCESS && getres(dev, &all, CU_DEV_RESOURCE_TYPE_SM) == CUDA_SUCCESS &&
+                     split(&part, &n, &all, &rest, 0, (unsigned)sms) == CUDA_SUCCESS && n == 1 &&
+                     gendesc(&desc, &part, 1) == CUDA_SUCCESS &&
+                     create(&gc, desc, dev, CU_GREEN_CTX_DEFAULT_STREAM) == CUDA_SUCCESS &&
+                     mkstream(&st, gc, CU_STREAM_NON_BLOCKING, lo) == CUDA_SUCCESS,
+                 GNNV_ERR_CUDA, "green context for the prefetch stream");
+    return (cudaStream_t)st;
+  }
+  cudaStream_t st;
+  GNNV_TRY_CUDA(cudaStreamCreateWithPriority(&st, cudaStreamNonBlocking, lo));
+  return st;
 }
 
 extern "C" {
@@ -336,13 +383,7 @@ gnnv_status gnnv_trainer_prefetch(gnnv_trainer* t, const int32_t* seeds, int32_t
       t->d_seedsb[k] = (int32_t*)dmalloc(t->md.max_seeds * sizeof(int32_t), "seeds (prefetch)");
       GNNV_TRY_CUDA(cudaMallocHost(&t->h_seedsb[k], t->md.max_seeds * sizeof(int32_t)));
       t->d_statsb[k] = (int64_t*)dmalloc(4 * sizeof(int64_t), "gather stats (prefetch)");
-      if (!t->side) {
-        // lowest priority: the prefetch fills the SMs the step leaves idle
-        // instead of delaying the step's (often small-grid) kernels
-        int lo = 0, hi = 0;
-        GNNV_TRY_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
-        GNNV_TRY_CUDA(cudaStreamCreateWithPriority(&t->side, cudaStreamNonBlocking, lo));
-      }
+      if (!t->side) t->side = make_side_stream(g->device);
     }
     cudaStream_t s = (cudaStream_t)stream;
     // order after the step that last computed on buffer set k and, for
