@@ -85,13 +85,19 @@ class GraphData:
 
 def csr_from_edges(n: int, src: np.ndarray, dst: np.ndarray):
     """Directed edge list -> CSR (rows sorted by neighbour id, duplicates kept)."""
-    src = np.asarray(src, dtype=np.int64)
-    dst = np.asarray(dst, dtype=np.int64)
-    key = src * np.int64(n) + dst
+    key = np.asarray(src, dtype=np.int64) * np.int64(n)
+    key += np.asarray(dst, dtype=np.int64)
+    return csr_from_keys(n, key)
+
+
+def csr_from_keys(n: int, key: np.ndarray):
+    """CSR from packed directed edge keys src*n + dst (sorted in place)."""
     key.sort()
     rows = key // n
     cols = (key - rows * n).astype(np.int32)
+    del key
     counts = np.bincount(rows, minlength=n).astype(np.int64)
+    del rows
     indptr = np.zeros(n + 1, dtype=np.int64)
     np.cumsum(counts, out=indptr[1:])
     return indptr, cols
@@ -129,6 +135,32 @@ def _sorted_unique(k: np.ndarray) -> np.ndarray:
     return k[keep]
 
 
+def _chung_lu_keys_large(n: int, m: int, cdf: np.ndarray, rng: np.random.Generator) -> np.ndarray:
+    """The same edge draws for m beyond one draw batch (papers100M-sized):
+    candidates are drawn in batches of at most _IDX_MASK and de-duplicated
+    with ONE sort over all of them, instead of a sort per batch; the caller's
+    loop then tops up any shortfall."""
+    chunks = []
+    total = int(m * 1.05) + 64
+    done = 0
+    while done < total:
+        batch = min(total - done, _IDX_MASK)
+        a = _inverse_cdf(cdf, rng, batch)
+        b = _inverse_cdf(cdf, rng, batch)
+        np.minimum(a, n - 1, out=a)
+        np.minimum(b, n - 1, out=b)
+        lo = np.minimum(a, b)
+        hi = np.maximum(a, b)
+        del a, b
+        ok = lo != hi
+        chunks.append(lo[ok] * np.int64(n) + hi[ok])
+        del lo, hi, ok
+        done += batch
+    keys = np.concatenate(chunks)
+    del chunks
+    return _sorted_unique(keys)
+
+
 def chung_lu_graph(n: int, nnz: int, beta: float, seed: int = GRAPH_SEED):
     """Undirected simple Chung-Lu graph with exactly nnz (even) CSR entries."""
     if nnz % 2:
@@ -140,7 +172,11 @@ def chung_lu_graph(n: int, nnz: int, beta: float, seed: int = GRAPH_SEED):
     w = np.arange(1, n + 1, dtype=np.float64) ** (-float(beta))
     cdf = np.cumsum(w)
     cdf /= cdf[-1]
-    keys = np.empty(0, dtype=np.int64)
+    del w
+    if m > _IDX_MASK:
+        keys = _chung_lu_keys_large(n, m, cdf, rng)
+    else:
+        keys = np.empty(0, dtype=np.int64)
     while keys.shape[0] < m:
         need = m - keys.shape[0]
         batch = min(int(need * 1.05) + 64, _IDX_MASK)
@@ -158,12 +194,14 @@ def chung_lu_graph(n: int, nnz: int, beta: float, seed: int = GRAPH_SEED):
         keys = keys[np.sort(keep)]
     lo = keys // n
     hi = keys - lo * n
+    del keys
     perm = rng.permutation(n).astype(np.int64)
     lo = perm[lo]
     hi = perm[hi]
-    src = np.concatenate([lo, hi])
-    dst = np.concatenate([hi, lo])
-    return csr_from_edges(n, src, dst)
+    del perm
+    key = np.concatenate([lo * np.int64(n) + hi, hi * np.int64(n) + lo])
+    del lo, hi
+    return csr_from_keys(n, key)
 
 
 def make_features(n: int, d: int, seed: int = FEAT_SEED, stride: Optional[int] = None) -> np.ndarray:

@@ -1,0 +1,65 @@
+"""-m gpu, opt-in (GNNV_PAPERS100M=1): parity on the papers100M-shaped graph,
+BASELINE.json configs[4] (111M nodes, 1.6B CSR entries, 128-d, fanouts
+[15,10,5], batch 8192).  Generating the graph takes minutes and ~100 GB of
+host memory, so the default suite skips it; the committed run log is
+profiles/r01_papers100m_pytest.log.
+
+One rank's batch, in the bench launch configuration (Trainer, Eq.4
+prefetch, tf32): blocks, frontiers, every gathered row and the hit counters
+bit-exact against the oracle; the loss finite.  The cache is the full
+table replicated on the one GPU of the box (the 8-GPU sharded placement is
+exercised by tests/test_gpu_sharded.py).
+"""
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from oracle.cache import access_counts, cache_slots
+from oracle.sampler import sample_blocks
+from paper_2404_09544_b200 import gnnv
+from synth import BASE_RNG_SEED, CONFIGS, epoch_seeds, init_weights, make_graph
+
+from gpu_util import blocks_to_host, lib, read_f32
+
+pytestmark = [
+    pytest.mark.gpu,
+    pytest.mark.skipif(os.environ.get("GNNV_PAPERS100M") != "1", reason="opt-in: GNNV_PAPERS100M=1 (minutes, ~100 GB)"),
+]
+
+
+def test_papers100m_batch_bit_exact():
+    lib()
+    cfg = CONFIGS["papers100m"]
+    gd = make_graph("papers100m")
+    g = gnnv.Graph.from_data(gd)
+    cache = gnnv.Cache(g, cfg["ratio"])
+    dims = [gd.d] + [cfg["hidden"]] * (len(cfg["fanouts"]) - 1) + [gd.C]
+    B = cfg["batch"]
+    tr = gnnv.Trainer(g, cache, dims, cfg["fanouts"], B, init_weights(dims), prec=gnnv.PREC_TF32)
+    seeds = epoch_seeds(gd.n, 0)[:B]
+    rs = BASE_RNG_SEED + 1
+    d_seeds = torch.as_tensor(seeds.astype(np.int32)).cuda()
+    pf, main = torch.cuda.Stream(), torch.cuda.Stream(priority=-1)
+    torch.cuda.synchronize()
+    tr.prefetch(d_seeds.data_ptr(), B, rs, on_host=False, stream=pf)
+    tr.step(d_seeds.data_ptr(), B, B, rs, 0.01, on_host=False, want_loss=False, stream=main)
+    loss = tr.read_loss(stream=main)
+    assert np.isfinite(loss)
+    F, blocks = sample_blocks(gd.indptr, gd.indices, seeds, cfg["fanouts"], rs)
+    hb = blocks_to_host(tr.blocks)
+    for h, ((nd, ns, ptr, idx, Fg), ob) in enumerate(zip(hb, blocks)):
+        assert (nd, ns) == (ob.n_dst, ob.n_src)
+        np.testing.assert_array_equal(Fg, F[h + 1])
+        np.testing.assert_array_equal(ptr, ob.indptr)
+        np.testing.assert_array_equal(idx, ob.indices)
+    FL = F[-1]
+    p0, s0 = tr.activation(0)
+    X = read_f32(p0, len(FL), s0)
+    assert X.tobytes() == oracle.gather_rows(gd.feats, FL).tobytes()
+    slot, owner, _ = cache_slots(gd.indptr, cfg["ratio"])
+    cnt = access_counts(slot, owner, FL)
+    assert tr.stats().tolist() == [cnt["rows"], cnt["hits_local"], cnt["hits_peer"], cnt["misses_host"]]
+    print(f"papers100m: frontiers {[len(f) for f in F]}, edges {[b.nnz for b in blocks]}, loss {loss:.5f}")
