@@ -232,7 +232,11 @@ def algorithmic(seg: str, sizes, cfg, dims, stride, prec, peaks):
         name = name[3:]
     if name == "gather":
         rowb = stride * 4
-        by = sizes["hits"] * rowb + n[L] * rowb + n[L] * 8
+        lvl = int(sizes.get("x_level", L))
+        if lvl < L:  # whole table cached: rows of F_{L-1} copied, every F_L row resolved to its cache row
+            by = 2 * n[lvl] * rowb + n[L] * 12
+        else:
+            by = sizes["hits"] * rowb + n[L] * rowb + n[L] * 8
         return "hbm", by, "GB/s", peaks["hbm"]
     if name == "sample":
         by = sum(n[h] * 16 + nnz[h] * 12 for h in range(L))
@@ -441,6 +445,7 @@ def main():
         acc["hits"] += hit
         acc["misses"] += nL - hit
     sizes = {k: (v / nsz) for k, v in acc.items()}
+    sizes["x_level"] = tr.x_level()
     peaks = load_peaks()
     traffic = load_traffic(f"{cfg['name']}/{args.prec}")
     # dominant kernel segment of the timed region
@@ -500,7 +505,8 @@ def main():
             "phases_ms_per_step": {k: v[0] / args.steps for k, v in sorted(segs.items(), key=lambda kv: -kv[1][0])},
             "sizes_per_step": {"frontier": [round(x) for x in sizes["n"]], "edges": [round(x) for x in sizes["nnz"]],
                                "distinct_src": [round(x) for x in sizes["U"]], "cache_hits": sizes["hits"],
-                               "cache_misses": sizes["misses"]},
+                               "cache_misses": sizes["misses"],
+                               "x_rows_level": sizes["x_level"]},
             "e2e": {"value": value_e2e, "unit": UNIT, "h2d_bytes_per_step": B * 4, "d2h_bytes_per_step": 8,
                     "ms_per_step": ms_e2e / args.steps, "wall_s": wall_e2e, "last_loss": loss},
             "cpu_baseline": cpu,

@@ -317,8 +317,16 @@ gnnv_status gnnv_trainer_set_params(gnnv_trainer* t, const float* host_params);
  * the trainer alternates between two buffer sets, so query again after every
  * step. */
 gnnv_blocks* gnnv_trainer_blocks(gnnv_trainer* t);
+/* Which rows of X (activation 0) the trainer materialises: F_level, i.e.
+ * L (every row of F_L) or L-1 (the dst prefix F_{L-1} only).  L-1 when the
+ * cache holds the whole table on this device (capacity N, one shard): the
+ * gather then writes only the rows the layer-1 GEMMs read and the layer-1
+ * aggregation reads its source rows from the cache table directly (the
+ * retrieval still goes through the cache's slot map; hit counters still
+ * cover every row of F_L).  GNNV_NO_XFUSE=1 in the environment disables it. */
+int32_t gnnv_trainer_x_level(const gnnv_trainer* t);
 /* Device pointers of the trainer's activations for layer i (0 = X) of the
- * last step (same buffer-set caveat). */
+ * last step (same buffer-set caveat; X holds the rows of gnnv_trainer_x_level). */
 gnnv_status gnnv_trainer_activation(gnnv_trainer* t, int32_t i, const float** d_H, int32_t* stride);
 
 /* One iteration of Algorithm 1 on this rank's seed slice:

@@ -11,6 +11,10 @@
 // degree-rank order (slot i holds the vertex of rank i); with G shards,
 // shard o holds ranks i = j*G + o at row j.  slot_map[v] = rank or -1.
 // Misses are read zero-copy from the pinned, device-mapped host table.
+// With d_rowidx (trainer, whole table resident on this device) only the dst
+// prefix F_{L-1} of X is materialised -- the rows the layer-1 GEMMs read --
+// and rowidx[u] = cache row of every F_L row, through which the layer-1
+// aggregation reads the cache directly (spmm.cu, k_spmm_fwd<LPR, true>).
 #include <string.h>
 
 #include <cub/device/device_radix_sort.cuh>
@@ -59,8 +63,10 @@ __global__ void __launch_bounds__(256) k_gather(const int32_t* __restrict__ F, c
                                                 const int32_t* __restrict__ slot,
                                                 const float* const* __restrict__ shards, int G, int me,
                                                 const float* __restrict__ host, int32_t stride,
-                                                float* __restrict__ X, unsigned long long* stats) {
+                                                float* __restrict__ X, unsigned long long* stats, int mat_level,
+                                                int32_t* __restrict__ rowidx) {
   const int n = sizes[L];
+  const int n_mat = sizes[mat_level];  // rows materialised in X (all, or the dst prefix)
   const int vec = stride >> 2;
   const int lane = threadIdx.x & 31;
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -73,6 +79,7 @@ __global__ void __launch_bounds__(256) k_gather(const int32_t* __restrict__ F, c
     if (row < n) {
       const int v = F[row];
       const int s = slot[v];
+      if (rowidx) rowidx[row] = s;  // cache row of every F_L row (whole-table cache, one shard)
       if (s >= 0) {
         const int o = s % G;
         src = reinterpret_cast<const float4*>(shards[o]) + (int64_t)(s / G) * vec;
@@ -85,7 +92,7 @@ __global__ void __launch_bounds__(256) k_gather(const int32_t* __restrict__ F, c
     c_local += __popc(__ballot_sync(0xffffffffu, kind == 0));
     c_peer += __popc(__ballot_sync(0xffffffffu, kind == 1));
     c_miss += __popc(__ballot_sync(0xffffffffu, kind == 2));
-    const int nrows = min(32, n - base);
+    const int nrows = min(32, n_mat - base);
     const uint64_t my = reinterpret_cast<uint64_t>(src);
     for (int r0 = 0; r0 < nrows; r0 += RU) {
       const float4* ps[RU];
@@ -110,7 +117,8 @@ __global__ void __launch_bounds__(256) k_gather(const int32_t* __restrict__ F, c
   }
 }
 
-void launch_gather(const gnnv_cache* c, const gnnv_blocks* b, float* d_X, int64_t* d_stats, cudaStream_t s) {
+void launch_gather(const gnnv_cache* c, const gnnv_blocks* b, float* d_X, int64_t* d_stats, cudaStream_t s,
+                   int32_t* d_rowidx) {
   const gnnv_graph* g = c->g;
   constexpr int RU = 8;
   const int64_t rows_ub = b->max_n[b->L];
@@ -119,7 +127,8 @@ void launch_gather(const gnnv_cache* c, const gnnv_blocks* b, float* d_X, int64_
   const int blocks = (int)std::min<int64_t>(ceil_div(warps, 8), (int64_t)cap);
   k_gather<RU><<<std::max(blocks, 1), 256, 0, s>>>(b->d_F, b->d_sizes, b->L, c->d_slot, c->d_shard_ptrs, c->world,
                                                    c->rank, g->d_feats, g->stride, d_X,
-                                                   reinterpret_cast<unsigned long long*>(d_stats));
+                                                   reinterpret_cast<unsigned long long*>(d_stats),
+                                                   d_rowidx ? b->L - 1 : b->L, d_rowidx);
   GNNV_CHECK_LAUNCH();
 }
 

@@ -164,15 +164,17 @@ struct Timeline {
 void launch_sample(gnnv_graph* g, gnnv_blocks* b, const int32_t* d_seeds, int32_t n_seeds, uint64_t rng_seed,
                    cudaStream_t s);
 // cache.cu
-void launch_gather(const gnnv_cache* c, const gnnv_blocks* b, float* d_X, int64_t* d_stats, cudaStream_t s);
+void launch_gather(const gnnv_cache* c, const gnnv_blocks* b, float* d_X, int64_t* d_stats, cudaStream_t s,
+                   int32_t* d_rowidx = nullptr);
 // Cap on the grid of the sampling / gather kernels (0 = none); the trainer
 // sets it around a prefetch so the overlapped batch occupies few SMs.
 void set_grid_cap(int blocks);
 int grid_cap();
 // spmm.cu
+// rowidx != NULL: source row u is row rowidx[u] of H (the cache table)
 void launch_spmm_fwd(const int32_t* d_indptr, const int32_t* d_indices, const int32_t* d_ndst, int64_t max_dst,
                      const float* H, int32_t ldh, float* A, int32_t lda, int32_t d, int32_t kind, int32_t aggr,
-                     cudaStream_t s);
+                     cudaStream_t s, const int32_t* rowidx = nullptr);
 void launch_spmm_bwd(const int32_t* d_indptr, const int32_t* d_indices, const uint32_t* d_own, const int32_t* d_ndst,
                      int64_t max_dst, const float* dA, int32_t lda, float* dH, int32_t ldh, int32_t d, int32_t kind,
                      int32_t aggr, const uint32_t* bits, int32_t bits_ld, cudaStream_t s);

@@ -229,14 +229,17 @@ static void check_layer(const gnnv_blocks* b, int32_t layer, const gnnv_layer_de
 }
 
 void layer_fwd_impl(gnnv_blocks* b, int32_t layer, const gnnv_layer_desc* ld, const float* Hsrc, const float* W,
-                    const float* bias, float* Hdst, float* A, cudaStream_t s, Timeline* tl, uint32_t* mask_bits) {
+                    const float* bias, float* Hdst, float* A, cudaStream_t s, Timeline* tl, uint32_t* mask_bits,
+                    const float* agg_table, const int32_t* rowidx) {
   const std::string sfx = ".l" + std::to_string(layer);
   if (tl) tl->mark(s, "spmm_fwd" + sfx);
   const int h = b->L - layer;
   const int32_t* d_ndst = b->d_sizes + h;
   const int lda = row_stride(ld->d_in), ldo = row_stride(ld->d_out);
-  launch_spmm_fwd(b->d_indptr[h], b->d_indices[h], d_ndst, b->max_n[h], Hsrc, ld->in_stride, A, lda, ld->d_in,
-                  ld->kind, ld->aggr, s);
+  // rowidx: the aggregation reads its source rows from the cache table
+  // (rows of Hsrc beyond the dst prefix are not materialised)
+  launch_spmm_fwd(b->d_indptr[h], b->d_indices[h], d_ndst, b->max_n[h], rowidx ? agg_table : Hsrc, ld->in_stride, A,
+                  lda, ld->d_in, ld->kind, ld->aggr, s, rowidx);
   GemmFwdArgs g{};
   if (ld->kind == GNNV_KIND_SAGE) {
     g.X1 = Hsrc;
@@ -392,7 +395,7 @@ gnnv_status gnnv_layer_fwd(gnnv_blocks* b, int32_t layer, const gnnv_layer_desc*
   return guarded([&] {
     check_layer(b, layer, ld);
     GNNV_REQUIRE(d_Hsrc && d_W && d_b && d_Hdst && d_saveA, GNNV_ERR_PARAM, "layer_fwd: null buffer");
-    layer_fwd_impl(b, layer, ld, d_Hsrc, d_W, d_b, d_Hdst, d_saveA, (cudaStream_t)s, nullptr, nullptr);
+    layer_fwd_impl(b, layer, ld, d_Hsrc, d_W, d_b, d_Hdst, d_saveA, (cudaStream_t)s, nullptr, nullptr, nullptr, nullptr);
   });
 }
 

@@ -31,11 +31,14 @@ __device__ __forceinline__ float4 mask_tail(float4 a, int col4, int d) {
                      base + 3 < d ? a.w : 0.f);
 }
 
-template <int LPR>
+// IND: source rows are read through rowidx (row u of the block is row
+// rowidx[u] of H = the device cache table), so X need not be materialised.
+template <int LPR, bool IND>
 __global__ void __launch_bounds__(256) k_spmm_fwd(const int32_t* __restrict__ indptr,
                                                   const int32_t* __restrict__ indices, const int32_t* d_ndst,
                                                   const float* __restrict__ H, int32_t ldh, float* __restrict__ A,
-                                                  int32_t lda, int32_t d, int32_t kind, int32_t aggr) {
+                                                  int32_t lda, int32_t d, int32_t kind, int32_t aggr,
+                                                  const int32_t* __restrict__ rowidx) {
   constexpr int RPW = 32 / LPR;
   const int n = *d_ndst;
   const int vec = (d + 3) >> 2;
@@ -55,9 +58,10 @@ __global__ void __launch_bounds__(256) k_spmm_fwd(const int32_t* __restrict__ in
       const int c = c0 + sl;
       const bool cok = active && c < vec;
       float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (kind == GNNV_KIND_GCN && cok) acc = __ldg(H4 + (int64_t)row * ldh4 + c);
+      if (kind == GNNV_KIND_GCN && cok) acc = __ldg(H4 + (int64_t)(IND ? __ldg(rowidx + row) : row) * ldh4 + c);
       for (int e0 = 0; e0 < cnt; e0 += LPR) {
-        const int my = (e0 + sl < cnt) ? __ldg(indices + beg + e0 + sl) : 0;
+        int my = (e0 + sl < cnt) ? __ldg(indices + beg + e0 + sl) : 0;
+        if (IND) my = __ldg(rowidx + my);
         const int m = min(LPR, cnt - e0);
         int j = 0;
         for (; j + 4 <= m; j += 4) {
@@ -173,15 +177,25 @@ static int spmm_grid(int64_t max_rows, int rows_per_warp) {
 
 void launch_spmm_fwd(const int32_t* d_indptr, const int32_t* d_indices, const int32_t* d_ndst, int64_t max_dst,
                      const float* H, int32_t ldh, float* A, int32_t lda, int32_t d, int32_t kind, int32_t aggr,
-                     cudaStream_t s) {
+                     cudaStream_t s, const int32_t* rowidx) {
   const int vec = (d + 3) / 4;
+#define GNNV_SPMM_FWD(LPR, RPWv)                                                                                     \
+  do {                                                                                                            \
+    if (rowidx)                                                                                                   \
+      k_spmm_fwd<LPR, true><<<spmm_grid(max_dst, RPWv), 256, 0, s>>>(d_indptr, d_indices, d_ndst, H, ldh, A, lda, d, \
+                                                                     kind, aggr, rowidx);                         \
+    else                                                                                                          \
+      k_spmm_fwd<LPR, false><<<spmm_grid(max_dst, RPWv), 256, 0, s>>>(d_indptr, d_indices, d_ndst, H, ldh, A, lda,  \
+                                                                      d, kind, aggr, nullptr);                    \
+  } while (0)
   if (vec <= 8) {
-    k_spmm_fwd<8><<<spmm_grid(max_dst, 4), 256, 0, s>>>(d_indptr, d_indices, d_ndst, H, ldh, A, lda, d, kind, aggr);
+    GNNV_SPMM_FWD(8, 4);
   } else if (vec <= 16) {
-    k_spmm_fwd<16><<<spmm_grid(max_dst, 2), 256, 0, s>>>(d_indptr, d_indices, d_ndst, H, ldh, A, lda, d, kind, aggr);
+    GNNV_SPMM_FWD(16, 2);
   } else {
-    k_spmm_fwd<32><<<spmm_grid(max_dst, 1), 256, 0, s>>>(d_indptr, d_indices, d_ndst, H, ldh, A, lda, d, kind, aggr);
+    GNNV_SPMM_FWD(32, 1);
   }
+#undef GNNV_SPMM_FWD
   GNNV_CHECK_LAUNCH();
 }
 

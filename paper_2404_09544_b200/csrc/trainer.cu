@@ -12,7 +12,8 @@
 
 namespace gnnv {
 void layer_fwd_impl(gnnv_blocks* b, int32_t layer, const gnnv_layer_desc* ld, const float* Hsrc, const float* W,
-                    const float* bias, float* Hdst, float* A, cudaStream_t s, Timeline* tl, uint32_t* mask_bits);
+                    const float* bias, float* Hdst, float* A, cudaStream_t s, Timeline* tl, uint32_t* mask_bits,
+                    const float* agg_table, const int32_t* rowidx);
 void layer_bwd_impl(gnnv_blocks* b, int32_t layer, const gnnv_layer_desc* ld, const float* Gdst, const float* Hdst,
                     const float* Hsrc, const float* A, const float* W, float* Gsrc, float* dW, float* db,
                     cudaStream_t s, Timeline* tl, const uint32_t* mask_bits, bool g_masked,
@@ -65,6 +66,12 @@ struct gnnv_trainer {
   cudaEvent_t ev_h2d[2] = {nullptr, nullptr};  // last copy out of h_seedsb[k]
   bool h2d_used[2] = {false, false};
   Timeline tl_side;
+  // Whole feature table resident on this device (capacity N, one shard):
+  // the gather materialises only the dst prefix F_{L-1} of X and records
+  // every F_L row's cache row in rowidx; layer 1 aggregates from the table.
+  bool x_fused = false;
+  const float* table = nullptr;
+  int32_t* rowidx[2] = {nullptr, nullptr};
 };
 
 static gnnv_layer_desc layer_desc(const gnnv_trainer* t, int i) {
@@ -134,6 +141,7 @@ gnnv_status gnnv_trainer_free(gnnv_trainer* t) {
   for (int k = 0; k < 2; ++k) {
     gnnv_blocks_free(t->bb[k]);
     dfree(t->X[k]);
+    dfree(t->rowidx[k]);
     dfree(t->d_seedsb[k]);
     if (t->h_seedsb[k]) cudaFreeHost(t->h_seedsb[k]);
     dfree(t->d_statsb[k]);
@@ -203,7 +211,12 @@ gnnv_status gnnv_trainer_create(gnnv_graph* g, gnnv_cache* c, const gnnv_model_d
       GNNV_TRY_CUDA(cudaMallocHost(&t->h_err, 4 * sizeof(int32_t)));
       gnnv_blocks* b = t->b;
       t->Hs[0] = g->stride;
-      t->H[0] = (float*)dmalloc((size_t)b->max_n[L] * g->stride * sizeof(float), "X (gathered features)");
+      t->x_fused = L > 1 && c->capacity == g->n && c->world == 1 && c->shards.size() == 1 && c->shards[0] &&
+                   !getenv("GNNV_NO_XFUSE");
+      t->table = t->x_fused ? c->shards[0] : nullptr;
+      const int64_t xrows = t->x_fused ? b->max_n[L - 1] : b->max_n[L];
+      t->H[0] = (float*)dmalloc((size_t)xrows * g->stride * sizeof(float), "X (gathered features)");
+      if (t->x_fused) t->rowidx[0] = (int32_t*)dmalloc(b->max_n[L] * sizeof(int32_t), "cache rows of F_L");
       for (int i = 1; i <= L; ++i) {
         t->Hs[i] = row_stride(md->dims[i]);
         const int64_t rows = b->max_n[L - i];
@@ -244,6 +257,10 @@ gnnv_status gnnv_trainer_create(gnnv_graph* g, gnnv_cache* c, const gnnv_model_d
 
 int64_t gnnv_trainer_num_params(const gnnv_trainer* t) { return t ? t->nparams : -1; }
 gnnv_blocks* gnnv_trainer_blocks(gnnv_trainer* t) { return t ? t->b : nullptr; }
+
+int32_t gnnv_trainer_x_level(const gnnv_trainer* t) {
+  return t ? (t->x_fused ? t->md.L - 1 : t->md.L) : -1;
+}
 
 gnnv_status gnnv_trainer_get(gnnv_trainer* t, float* host_params, float* host_grads) {
   return guarded([&] {
@@ -379,7 +396,10 @@ gnnv_status gnnv_trainer_prefetch(gnnv_trainer* t, const int32_t* seeds, int32_t
       GNNV_TRY_CUDA(cudaDeviceSynchronize());
       gnnv_status st = gnnv_blocks_create(g, t->md.max_seeds, t->md.fanouts, t->md.L, &t->bb[k]);
       if (st != GNNV_OK) throw Error{st, get_error()};
-      t->X[k] = (float*)dmalloc((size_t)t->bb[k]->max_n[t->md.L] * g->stride * sizeof(float), "X (prefetch)");
+      const int64_t xrows = t->bb[k]->max_n[t->x_fused ? t->md.L - 1 : t->md.L];
+      t->X[k] = (float*)dmalloc((size_t)xrows * g->stride * sizeof(float), "X (prefetch)");
+      if (t->x_fused)
+        t->rowidx[k] = (int32_t*)dmalloc(t->bb[k]->max_n[t->md.L] * sizeof(int32_t), "cache rows of F_L (prefetch)");
       t->d_seedsb[k] = (int32_t*)dmalloc(t->md.max_seeds * sizeof(int32_t), "seeds (prefetch)");
       GNNV_TRY_CUDA(cudaMallocHost(&t->h_seedsb[k], t->md.max_seeds * sizeof(int32_t)));
       t->d_statsb[k] = (int64_t*)dmalloc(4 * sizeof(int64_t), "gather stats (prefetch)");
@@ -408,7 +428,7 @@ gnnv_status gnnv_trainer_prefetch(gnnv_trainer* t, const int32_t* seeds, int32_t
     t->bb[k]->sampled = true;
     GNNV_TRY_CUDA(cudaMemsetAsync(t->d_statsb[k], 0, 4 * sizeof(int64_t), t->side));
     if (tl) tl->mark(t->side, "pf_gather");
-    launch_gather(t->c, t->bb[k], t->X[k], t->d_statsb[k], t->side);
+    launch_gather(t->c, t->bb[k], t->X[k], t->d_statsb[k], t->side, t->rowidx[k]);
     set_grid_cap(0);
     if (tl) tl->mark(t->side, "end");
     GNNV_TRY_CUDA(cudaEventRecord(t->ev_ready[k], t->side));
@@ -447,14 +467,14 @@ gnnv_status gnnv_step(gnnv_trainer* t, const int32_t* seeds, int32_t n_seeds, in
       GNNV_TRY_CUDA(cudaMemsetAsync(t->d_stats, 0, 4 * sizeof(int64_t), s));
       if (tm) GNNV_TRY_CUDA(cudaEventRecord(t->ev[1], s));
       if (tl) tl->mark(s, "gather");
-      launch_gather(t->c, t->b, t->H[0], t->d_stats, s);
+      launch_gather(t->c, t->b, t->H[0], t->d_stats, s, t->rowidx[t->cur]);
       if (tm) GNNV_TRY_CUDA(cudaEventRecord(t->ev[2], s));
     }
     gnnv_blocks* b = t->b;
     for (int i = 1; i <= L; ++i) {
       const gnnv_layer_desc ld = layer_desc(t, i);
       layer_fwd_impl(b, i, &ld, t->H[i - 1], t->d_params + t->w_off[i - 1], t->d_params + t->b_off[i - 1], t->H[i],
-                     t->A[i], s, tl, t->mbits[i]);
+                     t->A[i], s, tl, t->mbits[i], t->table, i == 1 ? t->rowidx[t->cur] : nullptr);
     }
     if (tm) GNNV_TRY_CUDA(cudaEventRecord(t->ev[3], s));
     float* d_loss = t->d_grads + t->nparams;

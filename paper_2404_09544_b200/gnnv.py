@@ -115,6 +115,7 @@ _SIGS = {
     "gnnv_trainer_get": (I32, [VP, VP, VP]),
     "gnnv_trainer_set_params": (I32, [VP, VP]),
     "gnnv_trainer_blocks": (VP, [VP]),
+    "gnnv_trainer_x_level": (I32, [VP]),
     "gnnv_trainer_activation": (I32, [VP, I32, PP, C.POINTER(I32)]),
     "gnnv_step": (I32, [VP, VP, I32, I32, I32, U64, F32, C.POINTER(F32), C.POINTER(StepTiming), VP]),
     "gnnv_trainer_stats": (I32, [VP, VP]),
@@ -467,6 +468,10 @@ class Trainer:
     def set_params(self, flat: np.ndarray):
         flat = np.ascontiguousarray(flat, np.float32)
         _check(load().gnnv_trainer_set_params(self.h, ptr(flat)))
+
+    def x_level(self) -> int:
+        """Frontier level whose rows X holds: L (all of F_L) or L-1 (dst prefix)."""
+        return int(load().gnnv_trainer_x_level(self.h))
 
     def activation(self, i: int):
         p = C.c_void_p()

@@ -74,9 +74,14 @@ def check_blocks_and_gather(gd, tr, ref_frontiers, ref_blocks, ratio):
         np.testing.assert_array_equal(ptr, ob.indptr, err_msg=f"indptr hop {h}")
         np.testing.assert_array_equal(idx, ob.indices, err_msg=f"indices hop {h}")
     FL = ref_frontiers[-1]
+    # X holds F_L, or only the dst prefix F_{L-1} when the whole table is
+    # cached (the layer-1 aggregation then reads the cache table directly)
+    lvl = tr.x_level()
+    assert lvl == (len(ref_blocks) - 1 if ratio == 1.0 else len(ref_blocks))
+    Fx = ref_frontiers[lvl]
     p0, s0 = tr.activation(0)
-    X = read_f32(p0, len(FL), s0)
-    assert X.tobytes() == oracle.gather_rows(gd.feats, FL).tobytes(), "gathered rows"
+    X = read_f32(p0, len(Fx), s0)
+    assert X.tobytes() == oracle.gather_rows(gd.feats, Fx).tobytes(), "gathered rows"
     slot, owner, _ = cache_slots(gd.indptr, ratio)
     cnt = access_counts(slot, owner, FL)
     assert tr.stats().tolist() == [cnt["rows"], cnt["hits_local"], cnt["hits_peer"], cnt["misses_host"]]
@@ -118,7 +123,10 @@ def test_products_full_step(products, prec):
         ob = blks[i] = _blk(hb, L - i)
         p_in, s_in = tr.activation(i - 1)
         p_out, s_out = tr.activation(i)
-        Hin = read_f32(p_in, ob.n_src, s_in)[:, : dims[i - 1]]
+        if i == 1 and tr.x_level() < L:  # layer 1 read the cache table: the exact feature rows
+            Hin = oracle.gather_rows(gd.feats, hb[L - 1][4])[:, : dims[0]]
+        else:
+            Hin = read_f32(p_in, ob.n_src, s_in)[:, : dims[i - 1]]
         Hout = read_f32(p_out, ob.n_dst, s_out)[:, : dims[i]]
         H[i - 1], H[i] = Hin, Hout
         Wi, bi = w[i - 1]

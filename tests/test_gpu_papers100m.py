@@ -56,9 +56,10 @@ def test_papers100m_batch_bit_exact():
         np.testing.assert_array_equal(ptr, ob.indptr)
         np.testing.assert_array_equal(idx, ob.indices)
     FL = F[-1]
+    Fx = F[tr.x_level()]  # whole table cached: X holds the dst prefix F_{L-1}
     p0, s0 = tr.activation(0)
-    X = read_f32(p0, len(FL), s0)
-    assert X.tobytes() == oracle.gather_rows(gd.feats, FL).tobytes()
+    X = read_f32(p0, len(Fx), s0)
+    assert X.tobytes() == oracle.gather_rows(gd.feats, Fx).tobytes()
     slot, owner, _ = cache_slots(gd.indptr, cfg["ratio"])
     cnt = access_counts(slot, owner, FL)
     assert tr.stats().tolist() == [cnt["rows"], cnt["hits_local"], cnt["hits_peer"], cnt["misses_host"]]
