@@ -46,7 +46,7 @@ def timeit(fn, reps=10):
     return ts[len(ts) // 2]
 
 
-for prec, pname in [(gnnv.PREC_TF32, "tf32"), (gnnv.PREC_BF16, "bf16")]:
+for prec, pname in [(gnnv.PREC_TF32, "tf32"), (gnnv.PREC_FP32, "fp32")]:
     t_fwd = timeit(lambda: gnnv.dense_fwd(X1, ld_in, X2, ld_in, d_in, W, b, Y, ld_out, d_out, M, True, prec))
     by = M * 2 * d_in * 4 + M * ld_out * 4
     print(f"{pname} fwd  M={M} K={2*d_in} N={d_out}: {t_fwd*1e3:8.1f} us  {by/t_fwd/1e6:7.0f} GB/s")
