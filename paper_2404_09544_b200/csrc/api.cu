@@ -15,6 +15,12 @@ namespace gnnv {
 static thread_local std::string g_last_error;
 static std::atomic<unsigned long long> g_launches{0};
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+static thread_local bool t_pdl_off = false;
+void set_pdl(bool on) { t_pdl_off = !on; }
+bool pdl_enabled() {
+  static const bool on = getenv("GNNV_NO_PDL") == nullptr;
+  return on && !t_pdl_off;
+}
 void set_error(const std::string& msg) { g_last_error = msg; }
 const char* get_error() { return g_last_error.c_str(); }
 

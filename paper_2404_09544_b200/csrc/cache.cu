@@ -24,6 +24,7 @@
 namespace gnnv {
 
 __global__ void k_degree_keys(const int64_t* __restrict__ indptr, int64_t n, uint32_t* keys, int32_t* ids) {
+  GNNV_PDL_ENTRY();
   for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x) {
     const int64_t deg = indptr[v + 1] - indptr[v];
     keys[v] = 0xFFFFFFFFu - (uint32_t)(deg < 0xFFFFFFFFll ? deg : 0xFFFFFFFFll);  // ascending key = degree desc
@@ -32,6 +33,7 @@ __global__ void k_degree_keys(const int64_t* __restrict__ indptr, int64_t n, uin
 }
 
 __global__ void k_slots(const int32_t* __restrict__ order, int64_t n, int64_t C, int32_t* slot) {
+  GNNV_PDL_ENTRY();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     slot[order[i]] = i < C ? (int32_t)i : -1;
 }
@@ -39,6 +41,7 @@ __global__ void k_slots(const int32_t* __restrict__ order, int64_t n, int64_t C,
 // shard rows: row j of shard `o` = vertex order[j*G + o]
 __global__ void k_fill_shard(const int32_t* __restrict__ order, int64_t C, int G, int o, const float* src,
                              int32_t stride, float* dst, int64_t rows) {
+  GNNV_PDL_ENTRY();
   const int vec = stride / 4;
   const int64_t total = rows * vec;
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
@@ -65,6 +68,7 @@ __global__ void __launch_bounds__(256) k_gather(const int32_t* __restrict__ F, c
                                                 const float* __restrict__ host, int32_t stride,
                                                 float* __restrict__ X, unsigned long long* stats, int mat_level,
                                                 int32_t* __restrict__ rowidx) {
+  GNNV_PDL_ENTRY();
   const int n = sizes[L];
   const int n_mat = sizes[mat_level];  // rows materialised in X (all, or the dst prefix)
   const int vec = stride >> 2;
@@ -125,7 +129,7 @@ void launch_gather(const gnnv_cache* c, const gnnv_blocks* b, float* d_X, int64_
   const int64_t warps = ceil_div(rows_ub, 32);
   const int cap = grid_cap() > 0 ? grid_cap() : num_sms() * 8;
   const int blocks = (int)std::min<int64_t>(ceil_div(warps, 8), (int64_t)cap);
-  k_gather<RU><<<std::max(blocks, 1), 256, 0, s>>>(b->d_F, b->d_sizes, b->L, c->d_slot, c->d_shard_ptrs, c->world,
+  launch_k(k_gather<RU>, std::max(blocks, 1), 256, 0, s, b->d_F, b->d_sizes, b->L, c->d_slot, c->d_shard_ptrs, c->world,
                                                    c->rank, g->d_feats, g->stride, d_X,
                                                    reinterpret_cast<unsigned long long*>(d_stats),
                                                    d_rowidx ? b->L - 1 : b->L, d_rowidx);

@@ -6,6 +6,7 @@
 #include <stdio.h>
 
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "../../include/gnnv.h"
@@ -40,6 +41,39 @@ void count_launch();
     ::gnnv::count_launch();          \
     GNNV_TRY_CUDA(cudaGetLastError()); \
   } while (0)
+
+// Programmatic dependent launch (PDL): every kernel of the step starts with
+// GNNV_PDL_ENTRY() -- it lets the next kernel in the stream be scheduled as
+// soon as all of this kernel's CTAs are running, then waits for its own
+// predecessor to complete (griddepcontrol.wait; a no-op without a
+// programmatic dependency).  launch_k() launches with the PDL attribute, so
+// launch latency and CTA rasterisation overlap the predecessor's tail.
+// GNNV_NO_PDL=1 disables the attribute.
+#define GNNV_PDL_ENTRY()                                          \
+  do {                                                            \
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); \
+    asm volatile("griddepcontrol.wait;" ::: "memory");            \
+  } while (0)
+bool pdl_enabled();
+// off around the Eq.4 prefetch: its kernels would otherwise park waiting CTAs
+// on the SMs the concurrent step needs
+void set_pdl(bool on);
+template <typename... KArgs, typename... Args>
+inline void launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  if (pdl_enabled()) {
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+  }
+  GNNV_TRY_CUDA(cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...));
+}
 
 #define GNNV_REQUIRE(cond, code, msg)                  \
   do {                                                 \

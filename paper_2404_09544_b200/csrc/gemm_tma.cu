@@ -191,6 +191,7 @@ static int debug_flags() {
 
 template <int MODE>
 __global__ void __launch_bounds__(NTHREADS, 1) k_tma_gemm(const __grid_constant__ Params p) {
+  GNNV_PDL_ENTRY();
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   __shared__ float s_bias[256];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
@@ -608,6 +609,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_tma_gemm(const __grid_constant_
 // [X1 blocks | X2 blocks]: k' < 32*nkb1 -> W row k' (valid < K1), else
 // W row K1 + (k' - 32*nkb1) (valid < K1).
 __global__ void k_bt_fwd(const float* __restrict__ W, int K1, int nkb1, int two, int N, int Npad, int Kp, float* Bt) {
+  GNNV_PDL_ENTRY();
   const int total = Npad * Kp;
   for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < total; t += gridDim.x * blockDim.x) {
     const int n = t / Kp, kp = t - n * Kp;
@@ -625,6 +627,7 @@ __global__ void k_bt_fwd(const float* __restrict__ W, int K1, int nkb1, int two,
 // [ld1, ld1+ld2) -> W row K1 + (j - ld1); k < N.
 __global__ void k_bt_dx(const float* __restrict__ W, int K1, int ld1, int ld2, int two, int N, int NCpad, int Kp,
                         float* Bd) {
+  GNNV_PDL_ENTRY();
   const int total = NCpad * Kp;
   for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < total; t += gridDim.x * blockDim.x) {
     const int j = t / Kp, k = t - j * Kp;
@@ -700,7 +703,7 @@ static void launch(const Params& p, dim3 grid, cudaStream_t s) {
     GNNV_TRY_CUDA(cudaFuncSetAttribute(k_tma_gemm<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
     attr = bytes;
   }
-  k_tma_gemm<MODE><<<grid, NTHREADS, bytes, s>>>(p);
+  launch_k(k_tma_gemm<MODE>, grid, NTHREADS, bytes, s, p);
   GNNV_CHECK_LAUNCH();
 }
 
@@ -716,7 +719,7 @@ bool gemm_fwd_tma(const GemmFwdArgs& a, cudaStream_t s) {
   const int nkb = a.X2 ? 2 * nkb1 : nkb1;
   const int Kp = nkb * BK;
   float* Bt = (float*)g_img.get((size_t)BN * Kp * sizeof(float), s);
-  k_bt_fwd<<<std::min(1024, (BN * Kp + 255) / 256), 256, 0, s>>>(a.W, a.K1, nkb1, a.X2 ? 1 : 0, a.N, BN, Kp, Bt);
+  launch_k(k_bt_fwd, std::min(1024, (BN * Kp + 255) / 256), 256, 0, s, a.W, a.K1, nkb1, a.X2 ? 1 : 0, a.N, BN, Kp, Bt);
   GNNV_CHECK_LAUNCH();
   Params p{};
   p.ta1 = make_map(a.X1, a.max_M, a.K1, a.ld1, BM);
@@ -751,7 +754,7 @@ bool gemm_dx_tma(const GemmDxArgs& a, cudaStream_t s) {
   const int Kp = nkb * BK;
   const int NCpad = ntl * BN;
   float* Bd = (float*)g_img.get((size_t)NCpad * Kp * sizeof(float), s);
-  k_bt_dx<<<std::min(1024, (NCpad * Kp + 255) / 256), 256, 0, s>>>(a.W, a.K1, a.ld1, a.ld2, a.Y2 ? 1 : 0, a.N, NCpad,
+  launch_k(k_bt_dx, std::min(1024, (NCpad * Kp + 255) / 256), 256, 0, s, a.W, a.K1, a.ld1, a.ld2, a.Y2 ? 1 : 0, a.N, NCpad,
                                                                     Kp, Bd);
   GNNV_CHECK_LAUNCH();
   Params p{};

@@ -10,6 +10,7 @@ namespace gnnv {
 
 __global__ void k_relu_mask(const float* __restrict__ G, const float* __restrict__ H, float* __restrict__ Gp, int ld,
                             const int32_t* d_M) {
+  GNNV_PDL_ENTRY();
   const int64_t total = (int64_t)(*d_M) * (ld >> 2);
   const float4* G4 = reinterpret_cast<const float4*>(G);
   const float4* H4 = reinterpret_cast<const float4*>(H);
@@ -24,13 +25,14 @@ void launch_relu_mask(const float* G, const float* H, float* Gp, int32_t ld, int
                       int64_t max_M, cudaStream_t s) {
   const int64_t total = std::max<int64_t>(max_M, 1) * (ld / 4);
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(total, 256), (int64_t)num_sms() * 8));
-  k_relu_mask<<<grid, 256, 0, s>>>(G, H, Gp, ld, d_M);
+  launch_k(k_relu_mask, grid, 256, 0, s, G, H, Gp, ld, d_M);
   GNNV_CHECK_LAUNCH();
 }
 
 // bits[m*bits_ld + n/32] bit n%32 = (H[m][n] > 0): one warp per (row, word)
 __global__ void k_relu_bits(const float* __restrict__ H, int32_t ldh, int32_t N, const int32_t* d_M, uint32_t* bits,
                             int32_t bits_ld) {
+  GNNV_PDL_ENTRY();
   const int64_t M = *d_M;
   const int lane = threadIdx.x & 31;
   const int64_t total = M * bits_ld;
@@ -49,7 +51,7 @@ void launch_relu_bits(const float* H, int32_t ldh, int32_t N, const int32_t* d_M
                       int32_t bits_ld, cudaStream_t s) {
   const int64_t warps = std::max<int64_t>(max_M, 1) * bits_ld;
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(warps, 8), (int64_t)num_sms() * 16));
-  k_relu_bits<<<grid, 256, 0, s>>>(H, ldh, N, d_M, bits, bits_ld);
+  launch_k(k_relu_bits, grid, 256, 0, s, H, ldh, N, d_M, bits, bits_ld);
   GNNV_CHECK_LAUNCH();
 }
 
@@ -60,6 +62,7 @@ constexpr int kColBlocks = 296;
 __global__ void __launch_bounds__(256) k_mask_colsum(const float* __restrict__ G, const float* __restrict__ H,
                                                      float* __restrict__ Gp, int ld, const int32_t* d_M,
                                                      float* __restrict__ partial) {
+  GNNV_PDL_ENTRY();
   __shared__ float4 s_acc[256];
   const int M = *d_M;
   const int ld4 = ld >> 2;
@@ -105,6 +108,7 @@ __global__ void __launch_bounds__(256) k_mask_colsum(const float* __restrict__ G
 // block, fixed order (deterministic); block (32, 8), grid ceil(N/32).
 __global__ void __launch_bounds__(256) k_colsum_reduce(const float* __restrict__ partial, int blocks, int ld, int N,
                                                        float* db) {
+  GNNV_PDL_ENTRY();
   __shared__ float s[8][33];
   const int n = blockIdx.x * 32 + threadIdx.x;
   float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;  // 4 loads in flight, fixed order
@@ -129,7 +133,7 @@ __global__ void __launch_bounds__(256) k_colsum_reduce(const float* __restrict__
 }
 
 void launch_colsum_reduce(const float* partial, int blocks, int ld, int N, float* out, cudaStream_t s) {
-  k_colsum_reduce<<<(N + 31) / 32, dim3(32, 8), 0, s>>>(partial, blocks, ld, N, out);
+  launch_k(k_colsum_reduce, (N + 31) / 32, dim3(32, 8), 0, s, partial, blocks, ld, N, out);
   GNNV_CHECK_LAUNCH();
 }
 
@@ -141,6 +145,7 @@ __global__ void __launch_bounds__(256) k_ce_loss(const float* __restrict__ z, in
                                                  const int32_t* __restrict__ labels, int n_global,
                                                  float* d_loss, float* __restrict__ dz, float* partial,
                                                  unsigned int* counter) {
+  GNNV_PDL_ENTRY();
   __shared__ float s_w[8];
   __shared__ bool s_last;
   const int n = *d_rows;
@@ -198,11 +203,12 @@ __global__ void __launch_bounds__(256) k_ce_loss(const float* __restrict__ z, in
 void launch_ce_loss(const float* z, int32_t ldz, int32_t C, const int32_t* d_rows, const int32_t* d_F,
                     const int32_t* d_labels, int32_t n_global, float* d_loss, float* dz, float* partial,
                     unsigned int* counter, int64_t, cudaStream_t s) {
-  k_ce_loss<<<kLossBlocks, 256, 0, s>>>(z, ldz, C, d_rows, d_F, d_labels, n_global, d_loss, dz, partial, counter);
+  launch_k(k_ce_loss, kLossBlocks, 256, 0, s, z, ldz, C, d_rows, d_F, d_labels, n_global, d_loss, dz, partial, counter);
   GNNV_CHECK_LAUNCH();
 }
 
 __global__ void k_sgd(float* __restrict__ p, const float* __restrict__ g, int64_t n, float lr) {
+  GNNV_PDL_ENTRY();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     p[i] -= lr * g[i];
 }
@@ -210,7 +216,7 @@ __global__ void k_sgd(float* __restrict__ p, const float* __restrict__ g, int64_
 void launch_sgd(float* p, const float* g, int64_t n, float lr, cudaStream_t s) {
   if (n <= 0) return;
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, 256), (int64_t)num_sms() * 4));
-  k_sgd<<<grid, 256, 0, s>>>(p, g, n, lr);
+  launch_k(k_sgd, grid, 256, 0, s, p, g, n, lr);
   GNNV_CHECK_LAUNCH();
 }
 
@@ -314,7 +320,7 @@ void layer_bwd_impl(gnnv_blocks* b, int32_t layer, const gnnv_layer_desc* ld, co
   if (tf32 && need_mask && !fuse_mask) {
     // masked gradient + deterministic column sums (db) in one pass
     if (tl) tl->mark(s, "relu_mask" + sfx);
-    k_mask_colsum<<<kColBlocks, 256, 0, s>>>(Gdst, Hdst, Gp, ldo, d_ndst, colpart);
+    launch_k(k_mask_colsum, kColBlocks, 256, 0, s, Gdst, Hdst, Gp, ldo, d_ndst, colpart);
     GNNV_CHECK_LAUNCH();
     launch_colsum_reduce(colpart, kColBlocks, ldo, ld->d_out, db, s);
     G = Gp;
@@ -525,7 +531,7 @@ gnnv_status gnnv_dense_dw(const float* X1, int32_t ld1, const float* X2, int32_t
     w.splits = splits;
     if (prec == GNNV_PREC_TF32) {
       float* colpart = scratch + part_f;
-      k_mask_colsum<<<kColBlocks, 256, 0, s>>>(G, nullptr, nullptr, ldg, w.d_M, colpart);
+      launch_k(k_mask_colsum, kColBlocks, 256, 0, s, G, nullptr, nullptr, ldg, w.d_M, colpart);
       GNNV_CHECK_LAUNCH();
       launch_colsum_reduce(colpart, kColBlocks, ldg, N, db_out, s);
     }

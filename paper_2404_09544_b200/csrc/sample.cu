@@ -58,6 +58,7 @@ __device__ __forceinline__ uint32_t philox_draw(uint64_t seed, uint32_t h, uint3
 
 __global__ void k_init_seeds(const int32_t* __restrict__ seeds, int32_t n_seeds, int64_t N, int32_t* tag, int32_t* F,
                              int32_t* sizes, int32_t err_index) {
+  GNNV_PDL_ENTRY();
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n_seeds; i += gridDim.x * blockDim.x) {
     const int32_t v = seeds[i];
     F[i] = v;
@@ -120,6 +121,7 @@ __global__ void __launch_bounds__(256) k_sample_hop(const int64_t* __restrict__ 
                                                     const int32_t* __restrict__ F, const int32_t* sizes, int h, int k,
                                                     uint64_t seed, int32_t* __restrict__ ell,
                                                     int32_t* __restrict__ cnt, int32_t* tag, uint32_t* own) {
+  GNNV_PDL_ENTRY();
   const int n = sizes[h];
   constexpr int RPW = 32 / G;
   const int lane = threadIdx.x & 31, grp = lane / G, gl = lane % G;
@@ -187,6 +189,7 @@ __global__ void __launch_bounds__(256) k_sample_hop_tpr(const int64_t* __restric
                                                         const int32_t* __restrict__ F, const int32_t* sizes, int h,
                                                         int k, uint64_t seed, int32_t* __restrict__ ell,
                                                         int32_t* __restrict__ cnt, int32_t* tag, uint32_t* own) {
+  GNNV_PDL_ENTRY();
   const int n = sizes[h];
   for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x) {
   const int v = F[r];
@@ -253,6 +256,7 @@ __global__ void __launch_bounds__(256) k_sample_hop_tpr(const int64_t* __restric
 // indptr[r]+i discovered its src id).
 __global__ void k_winners(int64_t N, int h, int k, const int32_t* sizes, const int32_t* __restrict__ ell,
                           const int32_t* __restrict__ cnt, const int32_t* tag, uint32_t* own) {
+  GNNV_PDL_ENTRY();
   const int64_t nslots = (int64_t)sizes[h] * k;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t e0 = 4 * (blockIdx.x * (int64_t)blockDim.x + threadIdx.x); e0 < nslots; e0 += 4 * stride) {
@@ -296,6 +300,7 @@ __global__ void __launch_bounds__(kScanTile) k_relabel_scan(int64_t N, int h, in
                                                             int32_t* __restrict__ F, int32_t* __restrict__ indptr,
                                                             uint32_t* __restrict__ own, int32_t* sizes,
                                                             unsigned long long* status) {
+  GNNV_PDL_ENTRY();
   __shared__ int s_tile;
   __shared__ uint32_t s_wa[kScanTile / 32], s_wb[kScanTile / 32];
   __shared__ uint32_t s_pa, s_pb;
@@ -429,11 +434,13 @@ __global__ void __launch_bounds__(kScanTile) k_relabel_scan(int64_t N, int h, in
 __global__ void k_map(int hp, int kp, const int32_t* sizes, const int32_t* __restrict__ ellp,
                       const int32_t* __restrict__ cntp, const int32_t* __restrict__ indptrp, const int32_t* tag,
                       int32_t* __restrict__ indicesp) {
+  GNNV_PDL_ENTRY();
   map_slots(blockIdx.x * (int64_t)blockDim.x + threadIdx.x, (int64_t)gridDim.x * blockDim.x, hp, kp, sizes, ellp, cntp,
             indptrp, tag, indicesp);
 }
 
 __global__ void k_reset(const int32_t* __restrict__ F, const int32_t* sizes, int L, int64_t N, int32_t* tag) {
+  GNNV_PDL_ENTRY();
   const int64_t n = sizes[L];
   for (int64_t i0 = 4 * (blockIdx.x * (int64_t)blockDim.x + threadIdx.x); i0 < n;
        i0 += 4 * (int64_t)gridDim.x * blockDim.x) {
@@ -461,7 +468,7 @@ void launch_sample(gnnv_graph* g, gnnv_blocks* b, const int32_t* d_seeds, int32_
   const int L = b->L;
   const int sms = num_sms();
   const int err_index = 2 * L + 1;
-  k_init_seeds<<<grid_for(n_seeds, 256, sms * 4), 256, 0, s>>>(d_seeds, n_seeds, g->n, b->d_tag, b->d_F, b->d_sizes,
+  launch_k(k_init_seeds, grid_for(n_seeds, 256, sms * 4), 256, 0, s, d_seeds, n_seeds, g->n, b->d_tag, b->d_F, b->d_sizes,
                                                                 err_index);
   GNNV_CHECK_LAUNCH();
   // Hop h's slots reuse d_ell / d_cnt, so hop h-1 is mapped to local ids
@@ -471,25 +478,25 @@ void launch_sample(gnnv_graph* g, gnnv_blocks* b, const int32_t* d_seeds, int32_
     const int64_t rows_ub = b->max_n[h];
     if (h > 0) {
       const int64_t slots_ub = b->max_n[h - 1] * (int64_t)b->fanouts[h - 1];
-      k_map<<<grid_for(slots_ub, 1024, sms * 8), 256, 0, s>>>(h - 1, b->fanouts[h - 1], b->d_sizes, b->d_ell,
+      launch_k(k_map, grid_for(slots_ub, 1024, sms * 8), 256, 0, s, h - 1, b->fanouts[h - 1], b->d_sizes, b->d_ell,
                                                               b->d_cnt, b->d_indptr[h - 1], b->d_tag,
                                                               b->d_indices[h - 1]);
       GNNV_CHECK_LAUNCH();
     }
     const int threads = 256;
 #define GNNV_SAMPLE_LAUNCH(G)                                                                              \
-  k_sample_hop<G><<<grid_for(rows_ub, threads / 32 * (32 / G), sms * 8), threads, 0, s>>>(                 \
+  launch_k(k_sample_hop<G>, grid_for(rows_ub, threads / 32 * (32 / G), sms * 8), threads, 0, s,                  \
       g->d_indptr, g->d_indices, g->n, b->d_F, b->d_sizes, h, k, rng_seed, b->d_ell, b->d_cnt, b->d_tag, b->d_own[h])
     if (k <= 4) {
-      k_sample_hop_tpr<4><<<grid_for(rows_ub, threads, 0), threads, 0, s>>>(
+      launch_k(k_sample_hop_tpr<4>, grid_for(rows_ub, threads, 0), threads, 0, s, 
           g->d_indptr, g->d_indices, g->n, b->d_F, b->d_sizes, h, k, rng_seed, b->d_ell, b->d_cnt, b->d_tag, b->d_own[h]);
     } else if (k <= 8) {
-      k_sample_hop_tpr<8><<<grid_for(rows_ub, threads, 0), threads, 0, s>>>(
+      launch_k(k_sample_hop_tpr<8>, grid_for(rows_ub, threads, 0), threads, 0, s, 
           g->d_indptr, g->d_indices, g->n, b->d_F, b->d_sizes, h, k, rng_seed, b->d_ell, b->d_cnt, b->d_tag, b->d_own[h]);
     } else if (k <= 16 && rows_ub < 16384) {
       GNNV_SAMPLE_LAUNCH(16);  // few rows: lanes per row beat rows per thread
     } else if (k <= 16) {
-      k_sample_hop_tpr<16><<<grid_for(rows_ub, threads, 0), threads, 0, s>>>(
+      launch_k(k_sample_hop_tpr<16>, grid_for(rows_ub, threads, 0), threads, 0, s, 
           g->d_indptr, g->d_indices, g->n, b->d_F, b->d_sizes, h, k, rng_seed, b->d_ell, b->d_cnt, b->d_tag, b->d_own[h]);
     } else {
       GNNV_SAMPLE_LAUNCH(32);
@@ -498,18 +505,18 @@ void launch_sample(gnnv_graph* g, gnnv_blocks* b, const int32_t* d_seeds, int32_
     GNNV_CHECK_LAUNCH();
     GNNV_TRY_CUDA(cudaMemsetAsync(b->d_scan, 0, b->scan_words * sizeof(unsigned long long), s));
     const int tiles_ub = (int)ceil_div(rows_ub, kScanTile);
-    k_winners<<<grid_for(rows_ub * k, 1024, 0), 256, 0, s>>>(g->n, h, k, b->d_sizes, b->d_ell, b->d_cnt, b->d_tag,
+    launch_k(k_winners, grid_for(rows_ub * k, 1024, 0), 256, 0, s, g->n, h, k, b->d_sizes, b->d_ell, b->d_cnt, b->d_tag,
                                                              b->d_own[h]);
     GNNV_CHECK_LAUNCH();
-    k_relabel_scan<<<g_grid_cap > 0 ? std::min<int>(tiles_ub, g_grid_cap) : tiles_ub, kScanTile, 0, s>>>(g->n, h, k, L, b->d_ell, b->d_cnt, b->d_tag, b->d_F,
+    launch_k(k_relabel_scan, g_grid_cap > 0 ? std::min<int>(tiles_ub, g_grid_cap) : tiles_ub, kScanTile, 0, s, g->n, h, k, L, b->d_ell, b->d_cnt, b->d_tag, b->d_F,
                                                   b->d_indptr[h], b->d_own[h], b->d_sizes, b->d_scan);
     GNNV_CHECK_LAUNCH();
   }
   const int64_t slots_ub = b->max_n[L - 1] * (int64_t)b->fanouts[L - 1];
-  k_map<<<grid_for(slots_ub, 1024, sms * 8), 256, 0, s>>>(L - 1, b->fanouts[L - 1], b->d_sizes, b->d_ell, b->d_cnt,
+  launch_k(k_map, grid_for(slots_ub, 1024, sms * 8), 256, 0, s, L - 1, b->fanouts[L - 1], b->d_sizes, b->d_ell, b->d_cnt,
                                                           b->d_indptr[L - 1], b->d_tag, b->d_indices[L - 1]);
   GNNV_CHECK_LAUNCH();
-  k_reset<<<grid_for(b->max_n[L], 1024, sms * 8), 256, 0, s>>>(b->d_F, b->d_sizes, L, g->n, b->d_tag);
+  launch_k(k_reset, grid_for(b->max_n[L], 1024, sms * 8), 256, 0, s, b->d_F, b->d_sizes, L, g->n, b->d_tag);
   GNNV_CHECK_LAUNCH();
 }
 

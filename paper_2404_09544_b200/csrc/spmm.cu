@@ -39,6 +39,7 @@ __global__ void __launch_bounds__(256) k_spmm_fwd(const int32_t* __restrict__ in
                                                   const float* __restrict__ H, int32_t ldh, float* __restrict__ A,
                                                   int32_t lda, int32_t d, int32_t kind, int32_t aggr,
                                                   const int32_t* __restrict__ rowidx) {
+  GNNV_PDL_ENTRY();
   constexpr int RPW = 32 / LPR;
   const int n = *d_ndst;
   const int vec = (d + 3) >> 2;
@@ -114,6 +115,7 @@ __global__ void __launch_bounds__(256) k_spmm_bwd(const int32_t* __restrict__ in
                                                   const float* __restrict__ dA, int32_t lda, float* dH, int32_t ldh,
                                                   int32_t d, int32_t kind, int32_t aggr, int32_t phase,
                                                   const uint32_t* __restrict__ bits, int32_t bits_ld) {
+  GNNV_PDL_ENTRY();
   constexpr int RPW = 32 / LPR;
   const int n = *d_ndst;
   const int vec = (d + 3) >> 2;
@@ -182,10 +184,10 @@ void launch_spmm_fwd(const int32_t* d_indptr, const int32_t* d_indices, const in
 #define GNNV_SPMM_FWD(LPR, RPWv)                                                                                     \
   do {                                                                                                            \
     if (rowidx)                                                                                                   \
-      k_spmm_fwd<LPR, true><<<spmm_grid(max_dst, RPWv), 256, 0, s>>>(d_indptr, d_indices, d_ndst, H, ldh, A, lda, d, \
+      launch_k(k_spmm_fwd<LPR, true>, spmm_grid(max_dst, RPWv), 256, 0, s, d_indptr, d_indices, d_ndst, H, ldh, A, lda, d, \
                                                                      kind, aggr, rowidx);                         \
     else                                                                                                          \
-      k_spmm_fwd<LPR, false><<<spmm_grid(max_dst, RPWv), 256, 0, s>>>(d_indptr, d_indices, d_ndst, H, ldh, A, lda,  \
+      launch_k(k_spmm_fwd<LPR, false>, spmm_grid(max_dst, RPWv), 256, 0, s, d_indptr, d_indices, d_ndst, H, ldh, A, lda,  \
                                                                       d, kind, aggr, nullptr);                    \
   } while (0)
   if (vec <= 8) {
@@ -205,13 +207,13 @@ void launch_spmm_bwd(const int32_t* d_indptr, const int32_t* d_indices, const ui
   const int ldh4 = ldh / 4;
   for (int phase = 1; phase <= 2; ++phase) {
     if (ldh4 <= 8) {
-      k_spmm_bwd<8><<<spmm_grid(max_dst, 4), 256, 0, s>>>(d_indptr, d_indices, d_own, d_ndst, dA, lda, dH, ldh, d, kind,
+      launch_k(k_spmm_bwd<8>, spmm_grid(max_dst, 4), 256, 0, s, d_indptr, d_indices, d_own, d_ndst, dA, lda, dH, ldh, d, kind,
                                                           aggr, phase, bits, bits_ld);
     } else if (ldh4 <= 16) {
-      k_spmm_bwd<16><<<spmm_grid(max_dst, 2), 256, 0, s>>>(d_indptr, d_indices, d_own, d_ndst, dA, lda, dH, ldh, d,
+      launch_k(k_spmm_bwd<16>, spmm_grid(max_dst, 2), 256, 0, s, d_indptr, d_indices, d_own, d_ndst, dA, lda, dH, ldh, d,
                                                            kind, aggr, phase, bits, bits_ld);
     } else {
-      k_spmm_bwd<32><<<spmm_grid(max_dst, 1), 256, 0, s>>>(d_indptr, d_indices, d_own, d_ndst, dA, lda, dH, ldh, d,
+      launch_k(k_spmm_bwd<32>, spmm_grid(max_dst, 1), 256, 0, s, d_indptr, d_indices, d_own, d_ndst, dA, lda, dH, ldh, d,
                                                            kind, aggr, phase, bits, bits_ld);
     }
     GNNV_CHECK_LAUNCH();

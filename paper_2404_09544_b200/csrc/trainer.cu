@@ -424,12 +424,14 @@ gnnv_status gnnv_trainer_prefetch(gnnv_trainer* t, const int32_t* seeds, int32_t
       return e ? atoi(e) : 0;
     }();
     set_grid_cap(pf_cap);
+    set_pdl(false);
     launch_sample(g, t->bb[k], d_seeds, n_seeds, rng_seed, t->side);
     t->bb[k]->sampled = true;
     GNNV_TRY_CUDA(cudaMemsetAsync(t->d_statsb[k], 0, 4 * sizeof(int64_t), t->side));
     if (tl) tl->mark(t->side, "pf_gather");
     launch_gather(t->c, t->bb[k], t->X[k], t->d_statsb[k], t->side, t->rowidx[k]);
     set_grid_cap(0);
+    set_pdl(true);
     if (tl) tl->mark(t->side, "end");
     GNNV_TRY_CUDA(cudaEventRecord(t->ev_ready[k], t->side));
     t->pending = true;
