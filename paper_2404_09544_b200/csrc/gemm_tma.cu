@@ -239,13 +239,13 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_tma_gemm(const __grid_constant_
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], MODE == MODE_DW ? NE * 32 : 1);  // dW: released by the transposers
+      mbar_init(&empty[s], MODE == MODE_DW ? NE : 1);  // dW: released by the transposer warps (one arrive each)
     }
     for (int b = 0; b < 2; ++b) {
-      mbar_init(&kready[b], NE * 32);
+      mbar_init(&kready[b], NE);
       mbar_init(&kfree[b], 1);
       mbar_init(&tfull[b], 1);
-      mbar_init(&tempty[b], NE * 32);
+      mbar_init(&tempty[b], NE);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -402,7 +402,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_tma_gemm(const __grid_constant_
           }
         }
         tc_before();
-        mbar_arrive(&tempty[acc]);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[acc]);  // one arrive per epilogue warp
       }
       if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
     }
@@ -536,9 +537,12 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_tma_gemm(const __grid_constant_
           GNNV_KROW_STORE(3, w)
 #undef GNNV_KROW_STORE
         }
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        mbar_arrive(&empty[s]);   // staging stage s may be refilled
-        mbar_arrive(&kready[b]);  // K-major tile b ready for the MMA
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // every writer, then one arrive per warp
+        __syncwarp();
+        if (lane == 0) {
+          mbar_arrive(&empty[s]);   // staging stage s may be refilled
+          mbar_arrive(&kready[b]);  // K-major tile b ready for the MMA
+        }
       }
       if ((p.mask || p.dbsum) && ig == 0) {
 #pragma unroll
