@@ -19,7 +19,7 @@ Readings:
 from __future__ import annotations
 
 import dataclasses
-from typing import List, Sequence
+from typing import List, Optional, Sequence
 
 import numpy as np
 
@@ -75,6 +75,68 @@ def sample_hop_positions(deg: np.ndarray, nodes: np.ndarray, k: int, hop: int,
     return out
 
 
+def locality_weight(bias: float) -> int:
+    """Selection weight of a cached neighbour for locality bias b (NEXT-2):
+    SPEC's p(eta) = 1 + 4 b eta (the paper says only that the
+    probability is "a function of data locality").  Reading Q26:
+    b is a multiple of 1/4, so the weight W = 1 + 4b is an integer in 1..5
+    and the draw is exact integer arithmetic."""
+    w = 1.0 + 4.0 * float(bias)
+    if not (0.0 <= bias <= 1.0) or abs(w - round(w)) > 1e-12:
+        raise ValueError("parameter error: locality bias must be in {0, 0.25, 0.5, 0.75, 1}")
+    return int(round(w))
+
+
+def successive_positions(d: int, k: int, cached: Sequence[bool], ts: Sequence[int], W: int) -> List[int]:
+    """Weighted sampling without replacement, successive form (reading Q26):
+    cached neighbours weigh W, the others 1; at draw s the remaining weight is
+    T = W c + m (c cached, m uncached left) and the 32-bit draw u_s picks
+    t = floor(u_s T / 2^32); t < W c selects the (t div W)-th remaining cached
+    neighbour, else the (t - W c)-th remaining uncached one, "remaining" in
+    ascending CSR position.  Positions returned ascending.  d <= k: all."""
+    if d <= k:
+        return list(range(d))
+    cpos = [p for p in range(d) if cached[p]]
+    upos = [p for p in range(d) if not cached[p]]
+    taken = {0: [], 1: []}  # class -> ranks taken (sorted)
+    lists = {0: cpos, 1: upos}
+    out = []
+    for s in range(k):
+        c = len(cpos) - len(taken[0])
+        m = len(upos) - len(taken[1])
+        T = W * c + m
+        t = (int(ts[s]) * T) >> 32
+        if t < W * c:
+            cls, j = 0, t // W
+        else:
+            cls, j = 1, t - W * c
+        r = j
+        for x in taken[cls]:  # j-th rank not yet taken
+            if x <= r:
+                r += 1
+        taken[cls] = sorted(taken[cls] + [r])
+        out.append(lists[cls][r])
+    return sorted(out)
+
+
+def sample_hop_positions_biased(indptr: np.ndarray, indices: np.ndarray, nodes: np.ndarray, k: int, hop: int,
+                                rng_seed: int, cached_mask: np.ndarray, W: int) -> List[np.ndarray]:
+    """Locality-biased node-wise sampling of one hop (NEXT-2, reading Q26):
+    per node, the same Philox draws (rng_seed; hop, node, s) as the unbiased
+    sampler, fed to successive_positions with cached_mask[neighbour]."""
+    out = []
+    for v in np.asarray(nodes, dtype=np.int64).tolist():
+        b, e = int(indptr[v]), int(indptr[v + 1])
+        d = e - b
+        if d <= k:
+            out.append(np.arange(d, dtype=np.int64))
+            continue
+        ts = [int(x) for x in draw(rng_seed, hop, np.full(k, v, dtype=np.int64), np.arange(k))]
+        flags = cached_mask[np.asarray(indices[b:e], dtype=np.int64)]
+        out.append(np.asarray(successive_positions(d, k, flags.tolist(), ts, W), dtype=np.int64))
+    return out
+
+
 @dataclasses.dataclass
 class Block:
     """Sampled block b_h: dst = F_h (n_dst rows), src = F_{h+1} (n_src rows).
@@ -121,7 +183,8 @@ def relabel(frontier: np.ndarray, rows: List[np.ndarray]):
 
 
 def sample_blocks(indptr: np.ndarray, indices: np.ndarray, seeds: Sequence[int],
-                  fanouts: Sequence[int], rng_seed: int):
+                  fanouts: Sequence[int], rng_seed: int, cached_mask: Optional[np.ndarray] = None,
+                  locality_bias: float = 0.0):
     """SubgraphSampling (Algorithm 1 line 2) for L = len(fanouts) hops.
 
     Returns (frontiers [F_0..F_L], blocks [b_0..b_{L-1}]).
@@ -138,8 +201,12 @@ def sample_blocks(indptr: np.ndarray, indices: np.ndarray, seeds: Sequence[int],
     F = seeds
     frontiers = [F]
     blocks = []
+    W = locality_weight(locality_bias)
     for h, k in enumerate(fanouts):
-        pos = sample_hop_positions(deg_all[F], F, int(k), h, rng_seed)
+        if W > 1:  # NEXT-2: locality-biased (cached neighbours weigh W)
+            pos = sample_hop_positions_biased(indptr, indices, F, int(k), h, rng_seed, cached_mask, W)
+        else:
+            pos = sample_hop_positions(deg_all[F], F, int(k), h, rng_seed)
         rows = [np.asarray(indices[indptr[v] + p], dtype=np.int64) for v, p in zip(F.tolist(), pos)]
         F_next, bptr, bidx = relabel(F, rows)
         blocks.append(Block(n_dst=len(F), n_src=len(F_next), indptr=bptr, indices=bidx,
