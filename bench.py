@@ -49,6 +49,8 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-baseline-seeds", type=int, default=0, help="seeds in the oracle sample (0 = one batch)")
     p.add_argument("--ratio", type=float, default=None)
+    p.add_argument("--locality-bias", type=float, default=0.0,
+                   help="NEXT-2 locality-biased sampling: cached neighbours weigh 1 + 4*bias (bias in 0, .25, .5, .75, 1)")
     p.add_argument("--placement", default="replica", choices=["replica", "sharded"],
                    help="feature cache across ranks: replicated, or sharded over the GPUs' HBM (NVLink peer reads)")
     p.add_argument("--no-pipeline", action="store_true",
@@ -315,6 +317,7 @@ def main():
     w = init_weights(dims, kind=args.kind)
     B = cfg["batch"]
     tr = gnnv.Trainer(g, cache, dims, cfg["fanouts"], B, w, kind=kind, prec=prec, comm=comm)
+    tr.set_locality(args.locality_bias)
     # the step runs on a high-priority stream; the trainer's prefetch stream
     # has the lowest priority (Eq.4 overlap without delaying the step)
     stream = torch.cuda.Stream(priority=-1)
@@ -421,6 +424,7 @@ def main():
     # ------------------------------------------- sizes of the timed steps
     nsz = min(args.steps, 8)
     blk = gnnv.Blocks(g, B, cfg["fanouts"])
+    blk.set_locality(cache, args.locality_bias)
     L = len(cfg["fanouts"])
     acc = {"n": np.zeros(L + 1), "nnz": np.zeros(L), "U": np.zeros(L), "hits": 0.0, "misses": 0.0}
     cv = cache.info()
@@ -491,6 +495,7 @@ def main():
             "config": {"workload": cfg["name"], "n_nodes": gd.n, "nnz": gd.nnz, "d": gd.d, "classes": gd.C,
                        "fanouts": cfg["fanouts"], "batch_per_rank": B, "global_batch": world * B,
                        "cache_ratio": cfg["ratio"], "placement": args.placement, "kind": args.kind,
+                       "locality_bias": args.locality_bias,
                        "hidden": cfg["hidden"], "gemm_precision": args.prec,
                        "l2": "inputs > L2 (feature table %.0f MB, gathered X %.0f MB per step)" % (
                            gd.n * gd.stride * 4 / 1e6, sizes["n"][L] * gd.stride * 4 / 1e6),

@@ -179,6 +179,17 @@ gnnv_status gnnv_cache_info(const gnnv_cache* c, gnnv_cache_view* out);
 gnnv_status gnnv_blocks_create(gnnv_graph* g, int32_t max_seeds, const int32_t* fanouts, int32_t L,
                                gnnv_blocks** out);
 gnnv_status gnnv_blocks_free(gnnv_blocks* b);
+/* Locality-biased sampling (the 2PGraph template,
+ * selection probability "a function of data locality"):
+ * subsequent gnnv_sample calls on b draw each node's min(k, deg) neighbours
+ * by successive weighted sampling without replacement, cached neighbours
+ * (slot of c >= 0) weighing `weight` = 1 + 4b and the others 1 (SPEC
+ * S:123; reading Q26: b in {0, 1/4, 1/2, 3/4, 1}, so weight is an
+ * integer 1..5 and the draws are exact integer arithmetic on the same
+ * Philox words as the unbiased sampler).  weight 1 restores the unbiased
+ * Floyd sampler.  c must outlive the blocks' use.  PARAM on a bad weight
+ * or a missing cache; STATE if c belongs to another graph. */
+gnnv_status gnnv_blocks_set_locality(gnnv_blocks* b, const gnnv_cache* c, int32_t weight);
 
 /* SubgraphSampling (Algorithm 1 line 2) with the unified node-wise
  * sampler of Eq.2: for every v in F_h, min(k_h, deg v) distinct
@@ -352,6 +363,9 @@ typedef struct {
   double total_ms;
   int32_t count;
 } gnnv_segment;
+/* The trainer's sampler locality weight (gnnv_blocks_set_locality with the
+ * trainer's cache; both buffer sets).  STATE while a prefetch is pending. */
+gnnv_status gnnv_trainer_set_locality(gnnv_trainer* t, int32_t weight);
 gnnv_status gnnv_trainer_timeline(gnnv_trainer* t, int32_t on);
 gnnv_status gnnv_trainer_timeline_read(gnnv_trainer* t, gnnv_segment* out, int32_t cap, int32_t* n_out);
 /* Eq.4 pipelining (T = n_iter max(t_sample + t_transfer,

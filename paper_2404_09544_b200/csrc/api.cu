@@ -333,6 +333,17 @@ gnnv_status gnnv_blocks_create(gnnv_graph* g, int32_t max_seeds, const int32_t* 
   });
 }
 
+gnnv_status gnnv_blocks_set_locality(gnnv_blocks* b, const gnnv_cache* c, int32_t weight) {
+  return guarded([&] {
+    GNNV_REQUIRE(b, GNNV_ERR_PARAM, "blocks_set_locality: null");
+    GNNV_REQUIRE(weight >= 1 && weight <= 5, GNNV_ERR_PARAM, "blocks_set_locality: weight must be 1 + 4b in 1..5");
+    GNNV_REQUIRE(weight == 1 || c, GNNV_ERR_PARAM, "blocks_set_locality: a biased sampler needs the cache");
+    GNNV_REQUIRE(!c || c->g == b->g, GNNV_ERR_STATE, "blocks_set_locality: cache of another graph");
+    b->loc_w = weight;
+    b->loc_slot = weight > 1 ? c->d_slot : nullptr;
+  });
+}
+
 gnnv_status gnnv_blocks_free(gnnv_blocks* b) {
   if (!b) return GNNV_OK;
   dfree(b->d_tag);

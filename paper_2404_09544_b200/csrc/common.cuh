@@ -157,6 +157,10 @@ struct gnnv_blocks {
   int64_t scan_words = 0;
   uint32_t* d_own[GNNV_MAX_LAYERS] = {nullptr};  // [max_n[h]] owner-edge bit mask per dst row
   bool sampled = false;
+  // NEXT-2 locality bias: cached neighbours (slot[u] >= 0) weigh loc_w
+  // (= 1 + 4b, 1 = unbiased); see gnnv_blocks_set_locality
+  const int32_t* loc_slot = nullptr;
+  int32_t loc_w = 1;
   // scratch arena for the layer kernels (grows on demand)
   void* scratch = nullptr;
   size_t scratch_bytes = 0;

@@ -277,6 +277,122 @@ __global__ void k_winners(int64_t N, int h, int k, const int32_t* sizes, const i
   }
 }
 
+// NEXT-2: locality-biased node-wise sampling (reading Q26).  One warp per
+// frontier row.  Cached neighbours (slot[u] >= 0) weigh W, the others 1;
+// the k picks are successive weighted draws without replacement made in
+// RANK space (class, rank within the class in ascending CSR position) from
+// the same Philox draws as the unbiased sampler: at draw s the remaining
+// weight is T = W c + m and t = floor(u_s T / 2^32) selects the (t div W)-th
+// remaining cached or the (t - W c)-th remaining uncached neighbour.  Two
+// warp sweeps over the adjacency (ballots of the cached flags) count c and
+// map the picked ranks to positions (__fns = n-th set bit); positions are
+// then sorted ascending.  Bit-identical to oracle.sampler.successive_positions.
+__global__ void __launch_bounds__(256) k_sample_hop_biased(const int64_t* __restrict__ indptr,
+                                                           const int32_t* __restrict__ indices, int64_t N,
+                                                           const int32_t* __restrict__ F, const int32_t* sizes, int h,
+                                                           int k, uint64_t seed, const int32_t* __restrict__ slot,
+                                                           int W, int32_t* __restrict__ ell, int32_t* __restrict__ cnt,
+                                                           int32_t* tag, uint32_t* own) {
+  GNNV_PDL_ENTRY();
+  __shared__ int s_tc[8][32], s_tu[8][32], s_pos[8][32];
+  __shared__ uint32_t s_draw[8][32];
+  __shared__ int s_n[8][2];
+  const int n = sizes[h];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  int* tc = s_tc[wib];
+  int* tu = s_tu[wib];
+  int* spos = s_pos[wib];
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  for (int r = warp; r < n; r += nwarps) {
+    const int v = F[r];
+    int64_t beg = 0;
+    int d = 0;
+    if ((uint32_t)v < (uint64_t)N) {
+      beg = indptr[v];
+      d = (int)(indptr[v + 1] - beg);
+    }
+    const int c = min(k, d);
+    int pos = lane;
+    if (d > k) {
+      int cc = 0;
+      for (int p0 = 0; p0 < d; p0 += 32) {
+        const int p = p0 + lane;
+        const bool f = p < d && __ldg(slot + __ldg(indices + beg + p)) >= 0;
+        cc += __popc(__ballot_sync(0xffffffffu, f));
+      }
+      const int mm = d - cc;
+      if (lane < k) s_draw[wib][lane] = philox_draw(seed, (uint32_t)h, (uint32_t)v, (uint32_t)lane);
+      __syncwarp();
+      if (lane == 0) {
+        int nC = 0, nU = 0;
+        for (int s = 0; s < k; ++s) {
+          const uint32_t crem = (uint32_t)(cc - nC), urem = (uint32_t)(mm - nU);
+          const uint32_t T = (uint32_t)W * crem + urem;
+          const uint32_t t = (uint32_t)(((uint64_t)s_draw[wib][s] * T) >> 32);
+          const bool isc = t < (uint32_t)W * crem;
+          int* tk = isc ? tc : tu;
+          const int nt = isc ? nC : nU;
+          int rnk = (int)(isc ? t / (uint32_t)W : t - (uint32_t)W * crem);
+          int ins = 0;
+          while (ins < nt && tk[ins] <= rnk) {  // the j-th rank not yet taken
+            ++rnk;
+            ++ins;
+          }
+          for (int q = nt; q > ins; --q) tk[q] = tk[q - 1];
+          tk[ins] = rnk;
+          if (isc) ++nC;
+          else ++nU;
+        }
+        s_n[wib][0] = nC;
+        s_n[wib][1] = nU;
+      }
+      __syncwarp();
+      const int nC = s_n[wib][0], nU = s_n[wib][1];
+      int iC = 0, iU = 0, cb = 0, ub = 0;
+      for (int p0 = 0; p0 < d && (iC < nC || iU < nU); p0 += 32) {
+        const int p = p0 + lane;
+        const bool valid = p < d;
+        const bool f = valid && __ldg(slot + __ldg(indices + beg + p)) >= 0;
+        const unsigned bc = __ballot_sync(0xffffffffu, f), bu = __ballot_sync(0xffffffffu, valid && !f);
+        const int nc = __popc(bc), nu = __popc(bu);
+        while (iC < nC && tc[iC] < cb + nc) {
+          const int ln = (int)__fns(bc, 0, tc[iC] - cb + 1);
+          if (lane == 0) spos[iC] = p0 + ln;
+          ++iC;
+        }
+        while (iU < nU && tu[iU] < ub + nu) {
+          const int ln = (int)__fns(bu, 0, tu[iU] - ub + 1);
+          if (lane == 0) spos[nC + iU] = p0 + ln;
+          ++iU;
+        }
+        cb += nc;
+        ub += nu;
+      }
+      __syncwarp();
+      // ascending positions: rank of this lane's position among the k
+      const int mine = lane < k ? spos[lane] : INT_MAX;
+      int rank = 0;
+      for (int q = 0; q < k; ++q) rank += spos[q] < mine;
+      __syncwarp();
+      if (lane < k) spos[rank] = mine;
+      __syncwarp();
+      pos = lane < k ? spos[lane] : 0;
+      __syncwarp();
+    }
+    if (lane < c) {
+      const int u = __ldg(&indices[beg + pos]);
+      const int e = r * k + lane;
+      ell[e] = u;
+      if ((uint32_t)u < (uint64_t)N && tag[u] < 0) atomicMax(&tag[u], -(2 + e));
+    }
+    if (lane == 0) {
+      cnt[r] = c;
+      own[r] = 0u;
+    }
+  }
+}
+
 __device__ __forceinline__ void st_release_u64(unsigned long long* p, unsigned long long v) {
   asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
@@ -487,7 +603,10 @@ void launch_sample(gnnv_graph* g, gnnv_blocks* b, const int32_t* d_seeds, int32_
 #define GNNV_SAMPLE_LAUNCH(G)                                                                              \
   launch_k(k_sample_hop<G>, grid_for(rows_ub, threads / 32 * (32 / G), sms * 8), threads, 0, s,                  \
       g->d_indptr, g->d_indices, g->n, b->d_F, b->d_sizes, h, k, rng_seed, b->d_ell, b->d_cnt, b->d_tag, b->d_own[h])
-    if (k <= 4) {
+    if (b->loc_w > 1) {
+      launch_k(k_sample_hop_biased, grid_for(rows_ub, 8, 0), 256, 0, s, g->d_indptr, g->d_indices, g->n, b->d_F,
+               b->d_sizes, h, k, rng_seed, b->loc_slot, (int)b->loc_w, b->d_ell, b->d_cnt, b->d_tag, b->d_own[h]);
+    } else if (k <= 4) {
       launch_k(k_sample_hop_tpr<4>, grid_for(rows_ub, threads, 0), threads, 0, s, 
           g->d_indptr, g->d_indices, g->n, b->d_F, b->d_sizes, h, k, rng_seed, b->d_ell, b->d_cnt, b->d_tag, b->d_own[h]);
     } else if (k <= 8) {

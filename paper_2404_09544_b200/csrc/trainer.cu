@@ -69,6 +69,7 @@ struct gnnv_trainer {
   // Whole feature table resident on this device (capacity N, one shard):
   // the gather materialises only the dst prefix F_{L-1} of X and records
   // every F_L row's cache row in rowidx; layer 1 aggregates from the table.
+  int32_t loc_w = 1;  // NEXT-2 locality weight for both buffer sets
   bool x_fused = false;
   const float* table = nullptr;
   int32_t* rowidx[2] = {nullptr, nullptr};
@@ -289,6 +290,19 @@ gnnv_status gnnv_trainer_activation(gnnv_trainer* t, int32_t i, const float** d_
   });
 }
 
+gnnv_status gnnv_trainer_set_locality(gnnv_trainer* t, int32_t weight) {
+  return guarded([&] {
+    GNNV_REQUIRE(t, GNNV_ERR_PARAM, "trainer_set_locality: null");
+    GNNV_REQUIRE(!t->pending, GNNV_ERR_STATE, "trainer_set_locality: a prefetched batch is pending");
+    for (int k = 0; k < 2; ++k) {
+      if (!t->bb[k]) continue;
+      gnnv_status st = gnnv_blocks_set_locality(t->bb[k], t->c, weight);
+      if (st != GNNV_OK) throw Error{st, get_error()};
+    }
+    t->loc_w = weight;
+  });
+}
+
 gnnv_status gnnv_trainer_timeline(gnnv_trainer* t, int32_t on) {
   return guarded([&] {
     GNNV_REQUIRE(t, GNNV_ERR_PARAM, "trainer_timeline: null");
@@ -395,6 +409,8 @@ gnnv_status gnnv_trainer_prefetch(gnnv_trainer* t, const int32_t* seeds, int32_t
     if (!t->bb[k]) {  // first use: the second buffer set
       GNNV_TRY_CUDA(cudaDeviceSynchronize());
       gnnv_status st = gnnv_blocks_create(g, t->md.max_seeds, t->md.fanouts, t->md.L, &t->bb[k]);
+      if (st != GNNV_OK) throw Error{st, get_error()};
+      st = gnnv_blocks_set_locality(t->bb[k], t->c, t->loc_w);
       if (st != GNNV_OK) throw Error{st, get_error()};
       const int64_t xrows = t->bb[k]->max_n[t->x_fused ? t->md.L - 1 : t->md.L];
       t->X[k] = (float*)dmalloc((size_t)xrows * g->stride * sizeof(float), "X (prefetch)");

@@ -116,6 +116,8 @@ _SIGS = {
     "gnnv_trainer_set_params": (I32, [VP, VP]),
     "gnnv_trainer_blocks": (VP, [VP]),
     "gnnv_trainer_x_level": (I32, [VP]),
+    "gnnv_trainer_set_locality": (I32, [VP, I32]),
+    "gnnv_blocks_set_locality": (I32, [VP, VP, I32]),
     "gnnv_trainer_activation": (I32, [VP, I32, PP, C.POINTER(I32)]),
     "gnnv_step": (I32, [VP, VP, I32, I32, I32, U64, F32, C.POINTER(F32), C.POINTER(StepTiming), VP]),
     "gnnv_trainer_stats": (I32, [VP, VP]),
@@ -176,6 +178,14 @@ def version() -> str:
 
 def launch_count() -> int:
     return int(load().gnnv_launch_count())
+
+
+def locality_weight(bias: float) -> int:
+    """1 + 4 bias for bias in {0, 0.25, 0.5, 0.75, 1} (reading Q26)."""
+    w = 1.0 + 4.0 * float(bias)
+    if not (0.0 <= bias <= 1.0) or abs(w - round(w)) > 1e-12:
+        raise GnnvError(ERR_PARAM, "locality bias must be in {0, 0.25, 0.5, 0.75, 1}")
+    return int(round(w))
 
 
 def row_stride(d: int) -> int:
@@ -324,6 +334,10 @@ class Blocks:
         _check(load().gnnv_sample(self.g.h, ptr(d_seeds), int(n_seeds), _i32arr(self.fanouts), self.L,
                                   int(rng_seed) & 0xFFFFFFFFFFFFFFFF, self.h, stream_ptr(stream)))
 
+    def set_locality(self, cache: Optional["Cache"], bias: float):
+        """Locality-biased sampling (NEXT-2): cached neighbours weigh 1 + 4 bias."""
+        _check(load().gnnv_blocks_set_locality(self.h, cache.h if cache else None, locality_weight(bias)))
+
     def info(self, sync: bool = True, stream=None) -> List[BlockView]:
         arr = (BlockView * self.L)()
         _check(load().gnnv_blocks_info(self.h, 1 if sync else 0, stream_ptr(stream), arr))
@@ -468,6 +482,10 @@ class Trainer:
     def set_params(self, flat: np.ndarray):
         flat = np.ascontiguousarray(flat, np.float32)
         _check(load().gnnv_trainer_set_params(self.h, ptr(flat)))
+
+    def set_locality(self, bias: float):
+        """Locality-biased sampling (NEXT-2) for the trainer's batches."""
+        _check(load().gnnv_trainer_set_locality(self.h, locality_weight(bias)))
 
     def x_level(self) -> int:
         """Frontier level whose rows X holds: L (all of F_L) or L-1 (dst prefix)."""

@@ -448,3 +448,45 @@ def test_pipelined_steps_match_sequential(mini):
         losses.append(dv.read_loss(stream=main))
     np.testing.assert_allclose(losses, l_seq, rtol=1e-5)
     assert normwise(dv.params(), seq.params()) < 1e-5
+
+
+# ------------------------------------------- locality-biased sampling (NEXT-2)
+@pytest.mark.parametrize("bias", [0.25, 0.5, 1.0])
+@pytest.mark.parametrize("fan", [[15, 10, 5], [5, 3], [32, 2]])
+def test_biased_sampling_bit_exact(mini, bias, fan):
+    gd, g = mini
+    cache = gnnv.Cache(g, 0.3)
+    slot, _, _ = cache_slots(gd.indptr, 0.3)
+    seeds = epoch_seeds(gd.n, 1)[:300]
+    blocks = gnnv.Blocks(g, 512, fan)
+    blocks.set_locality(cache, bias)
+    blocks.sample(dev_i32(seeds), len(seeds), 77)
+    hb = blocks_to_host(blocks)
+    oF, oB = sample_blocks(gd.indptr, gd.indices, seeds, fan, 77, slot >= 0, bias)
+    assert_blocks_equal(hb, oF, oB)
+
+
+def test_biased_trainer_raises_hit_rate(mini):
+    """The trainer's locality knob: blocks equal the oracle's biased blocks,
+    and the host-miss count falls as the bias grows (the point of NEXT-2)."""
+    gd, g = mini
+    cfg = CONFIGS["mini"]
+    dims = [gd.d, cfg["hidden"], cfg["hidden"], gd.C]
+    cache = gnnv.Cache(g, 0.2)
+    slot, owner, _ = cache_slots(gd.indptr, 0.2)
+    seeds = epoch_seeds(gd.n, 0)[: cfg["batch"]]
+    misses = []
+    for bias in (0.0, 0.5, 1.0):
+        tr = gnnv.Trainer(g, cache, dims, cfg["fanouts"], cfg["batch"], init_weights(dims), prec=2)
+        tr.set_locality(bias)
+        tr.step(seeds, len(seeds), len(seeds), 5, 0.01)
+        oF, oB = sample_blocks(gd.indptr, gd.indices, seeds, cfg["fanouts"], 5, slot >= 0, bias)
+        assert_blocks_equal(blocks_to_host(tr.blocks), oF, oB)
+        cnt = access_counts(slot, owner, oF[-1])
+        st = tr.stats().tolist()
+        assert st == [cnt["rows"], cnt["hits_local"], cnt["hits_peer"], cnt["misses_host"]]
+        misses.append(st[3] / st[0])
+        tr.free()
+    assert misses[0] > misses[1] > misses[2], misses
+    with pytest.raises(gnnv.GnnvError):
+        gnnv.locality_weight(0.3)
