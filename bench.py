@@ -49,6 +49,8 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-baseline-seeds", type=int, default=0, help="seeds in the oracle sample (0 = one batch)")
     p.add_argument("--ratio", type=float, default=None)
+    p.add_argument("--policy", default="degree", choices=["degree", "fifo", "lru", "none"],
+                   help="cache policy: static degree template, or dynamic FIFO/LRU admission (NEXT-3)")
     p.add_argument("--locality-bias", type=float, default=0.0,
                    help="NEXT-2 locality-biased sampling: cached neighbours weigh 1 + 4*bias (bias in 0, .25, .5, .75, 1)")
     p.add_argument("--placement", default="replica", choices=["replica", "sharded"],
@@ -331,7 +333,9 @@ def main():
         comm = gnnv.Comm(rank, world, obj[0], local)
     g = gnnv.Graph.from_data(gd, device=local)
     placement = gnnv.PLACE_SHARDED if args.placement == "sharded" else gnnv.PLACE_REPLICA
-    cache = gnnv.Cache(g, cfg["ratio"], placement=placement, comm=comm)
+    policy = {"none": gnnv.POLICY_NONE, "degree": gnnv.POLICY_DEGREE, "fifo": gnnv.POLICY_FIFO,
+              "lru": gnnv.POLICY_LRU}[args.policy]
+    cache = gnnv.Cache(g, cfg["ratio"], policy=policy, placement=placement, comm=comm)
     dims = [gd.d] + [cfg["hidden"]] * (len(cfg["fanouts"]) - 1) + [gd.C]
     kind = gnnv.KIND_SAGE if args.kind == "sage" else gnnv.KIND_GCN
     prec = {"fp32": gnnv.PREC_FP32, "bf16": gnnv.PREC_BF16, "tf32": gnnv.PREC_TF32}[args.prec]
@@ -410,6 +414,7 @@ def main():
     tr.timeline(True)
     clocks = ClockSampler(local)
     clocks.start()
+    dyn0 = cache.counters() if args.policy in ("fifo", "lru") else None
     launches0 = gnnv.launch_count()
     barrier()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -419,6 +424,13 @@ def main():
     ev1.record(stream)
     barrier()
     launches = gnnv.launch_count() - launches0
+    # dynamic cache: hit rate of the batches gathered during the timed region
+    # (prefetches included), from the cache's own cumulative counters
+    dyn = None
+    if dyn0 is not None:
+        d1 = cache.counters() - dyn0
+        dyn = {"hits": int(d1[0]), "misses": int(d1[1]), "replaced": int(d1[2]),
+               "hit_rate": float(d1[0]) / max(1, int(d1[0] + d1[1]))}
     clk = clocks.stop()
     ms_total = max_over_ranks(ev0.elapsed_time(ev1))
     segs = tr.timeline_read()
@@ -475,7 +487,8 @@ def main():
     if sizes["misses"] > 0:
         peaks["host"] = measure_host_link()
     # the committed capture is of the default configuration only
-    default_cfg = args.ratio is None and args.locality_bias == 0 and args.placement == "replica" and args.kind == "sage"
+    default_cfg = (args.ratio is None and args.locality_bias == 0 and args.placement == "replica"
+                   and args.kind == "sage" and args.policy == "degree")
     traffic = load_traffic(f"{cfg['name']}/{args.prec}") if default_cfg else {}
     # dominant kernel segment of the timed region
     seg_ms = {k: v[0] / max(1, v[1]) for k, v in segs.items()}
@@ -520,7 +533,7 @@ def main():
             "config": {"workload": cfg["name"], "n_nodes": gd.n, "nnz": gd.nnz, "d": gd.d, "classes": gd.C,
                        "fanouts": cfg["fanouts"], "batch_per_rank": B, "global_batch": world * B,
                        "cache_ratio": cfg["ratio"], "placement": args.placement, "kind": args.kind,
-                       "locality_bias": args.locality_bias,
+                       "locality_bias": args.locality_bias, "cache_policy": args.policy,
                        "hidden": cfg["hidden"], "gemm_precision": args.prec,
                        "l2": "inputs > L2 (feature table %.0f MB, gathered X %.0f MB per step)" % (
                            gd.n * gd.stride * 4 / 1e6, sizes["n"][L] * gd.stride * 4 / 1e6),
@@ -539,6 +552,7 @@ def main():
                                "x_rows_level": sizes["x_level"]},
             "e2e": {"value": value_e2e, "unit": UNIT, "h2d_bytes_per_step": B * 4, "d2h_bytes_per_step": 8,
                     "ms_per_step": ms_e2e / args.steps, "wall_s": wall_e2e, "last_loss": loss},
+            "dynamic_cache": dyn,
             "cpu_baseline": cpu,
             "peaks": peaks["src"] + (f"; host link {peaks['host']:.1f} GB/s measured (pinned H2D copy)"
                                      if peaks.get("host") else ""),

@@ -69,8 +69,10 @@ typedef struct gnnv_trainer gnnv_trainer;
 typedef struct gnnv_comm gnnv_comm;
 typedef void* gnnv_stream; /* cudaStream_t */
 
-/* Cache update policy.  Only the static PaGraph template (DEGREE,
- * P:290) and NONE (pyg-like, ratio treated as 0) are built. */
+/* Cache update policy: NONE (pyg-like, ratio treated as 0);
+ * DEGREE = the static PaGraph template; FIFO / LRU = dynamic caches
+ * that start empty and admit every miss (gnnv_cache_update; SURVEY §8(f)
+ * NEXT-3, reading Q27). */
 typedef enum { GNNV_POLICY_NONE = 0, GNNV_POLICY_DEGREE = 1, GNNV_POLICY_FIFO = 2, GNNV_POLICY_LRU = 3 } gnnv_policy;
 /* Cache placement over the GPUs of one box.  REPLICA: every rank holds the
  * C = floor(ratio*N) hottest rows.  SHARDED: rank r holds the rows whose
@@ -144,7 +146,7 @@ gnnv_status gnnv_allreduce_sum(gnnv_comm* c, float* d_buf, int64_t n, gnnv_strea
  * (degree desc, id asc); slot(v) = rank(v) if rank(v) < C else -1.
  *  comm            NULL => single GPU (SHARDED then has one shard)
  *  virtual_shards  G for SHARDED_LOCAL (>=1), ignored otherwise
- * Errors: PARAM (ratio not in [0,1]); UNSUPPORTED (FIFO/LRU); OOM (message
+ * Errors: PARAM (ratio not in [0,1]); UNSUPPORTED (FIFO/LRU across GPUs); OOM (message
  * carries the bytes, Γ_cache = C * row_stride * 4, Eq.10).
  * Synchronous (fills the rows from the pinned host table). */
 gnnv_status gnnv_cache_build(gnnv_graph* g, double ratio, int32_t policy, int32_t placement,
@@ -160,6 +162,23 @@ gnnv_status gnnv_cache_free(gnnv_cache* c);
  * handles of gnnv_cache_ipc_handle (rank order, world * 64 bytes) and passes
  * them to gnnv_cache_open_peers; gnnv_gather / trainer creation fail with
  * STATE until then.  Both synchronous; STATE unless placement is SHARDED. */
+/* Dynamic caches (policy FIFO / LRU, one device; NEXT-3): SPEC's
+ * access_batch for the batch sampled in b whose rows were
+ * gathered into d_X (all n_L rows, row stride = the graph's): LRU stamps the
+ * hits with the batch index; the misses are admitted in ascending F_L order,
+ * each into a free slot (lowest first) or evicting the resident with the
+ * smallest key -- (last access, admission order) for LRU, admission order
+ * for FIFO (Eq.5's "replaced stale data"); their rows are copied
+ * from d_X.  Call once per gathered batch, in batch order (the trainer does,
+ * after each gather, on the gather's stream).  Stream-ordered, no sync.
+ * STATE for a static cache or unsampled blocks. */
+gnnv_status gnnv_cache_update(gnnv_cache* c, const gnnv_blocks* b, const float* d_X, gnnv_stream s);
+/* Cumulative counters of a dynamic cache: int64[4] = hits, misses, replaced
+ * (evictions), admitted; zeros for a static cache.  Synchronises. */
+gnnv_status gnnv_cache_counters(const gnnv_cache* c, int64_t* host4);
+/* Device pointer to the slot -> vertex table (int32[capacity], -1 free) of
+ * a dynamic cache (valid while c lives).  STATE for a static cache. */
+gnnv_status gnnv_cache_owners(const gnnv_cache* c, const int32_t** d_owner);
 gnnv_status gnnv_cache_ipc_handle(const gnnv_cache* c, void* out64);
 gnnv_status gnnv_cache_open_peers(gnnv_cache* c, const void* handles);
 typedef struct {

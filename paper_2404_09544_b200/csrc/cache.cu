@@ -18,6 +18,8 @@
 #include <string.h>
 
 #include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_select.cuh>
+#include <cub/iterator/counting_input_iterator.cuh>
 
 #include "common.cuh"
 
@@ -151,6 +153,138 @@ static void open_peers(gnnv_cache* c, const cudaIpcMemHandle_t* handles) {
                            cudaMemcpyHostToDevice));
   c->peers_ready = true;
 }
+// ------------------------------------------------ dynamic cache (NEXT-3)
+// access_batch of SPEC S:203-210 with all-miss admission (reading Q27), as
+// one pass per batch after its gather:
+//   k_dyn_hits   : LRU stamps the batch's hits with t; flags the misses
+//   DeviceSelect : the miss rows, ascending (the admission order)
+//   k_dyn_keys   : victim order of all C slots -- free slots first (by
+//                  index), then (stamp, seq) for LRU / seq for FIFO
+//   RadixSort    : slots sorted by key
+//   k_dyn_admit  : miss i takes slot sorted[i mod C] (only the last C misses
+//                  of a batch larger than C survive, as in the sequential
+//                  rule), evicts its owner, copies its row from X
+//   k_dyn_close  : counters (replaced = max(0, M - free slots)), seq += M
+__global__ void k_dyn_hits(const int32_t* __restrict__ F, const int32_t* sizes, int L, int64_t cap,
+                           const int32_t* __restrict__ slot, int32_t* stamp, int32_t t, int lru,
+                           int32_t* __restrict__ mflag) {
+  GNNV_PDL_ENTRY();
+  const int n = sizes[L];
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < cap; r += (int64_t)gridDim.x * blockDim.x) {
+    int f = 0;
+    if (r < n) {
+      const int s = slot[F[r]];
+      if (s >= 0) {
+        if (lru) stamp[s] = t;
+      } else {
+        f = 1;
+      }
+    }
+    mflag[r] = f;
+  }
+}
+
+__global__ void k_dyn_keys(int64_t C, const int32_t* __restrict__ owner, const int32_t* __restrict__ stamp,
+                           const int64_t* __restrict__ seq, int lru, unsigned long long* keys, int32_t* idx) {
+  GNNV_PDL_ENTRY();
+  for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < C; s += (int64_t)gridDim.x * blockDim.x) {
+    unsigned long long k;
+    if (owner[s] < 0) {
+      k = (unsigned long long)s;  // free: lowest index first
+    } else if (lru) {
+      k = ((unsigned long long)(stamp[s] + 1) << 40) | (unsigned long long)seq[s];
+    } else {
+      k = (1ull << 62) | (unsigned long long)seq[s];
+    }
+    keys[s] = k;
+    idx[s] = (int32_t)s;
+  }
+}
+
+__global__ void k_dyn_admit(int64_t C, const int32_t* __restrict__ miss, const int64_t* ctr,
+                            const int32_t* __restrict__ vslot, const int32_t* __restrict__ F, int32_t* slot,
+                            int32_t* owner, int32_t* stamp, int64_t* seq, int32_t t, const float* __restrict__ X,
+                            float* __restrict__ cache, int32_t stride) {
+  GNNV_PDL_ENTRY();
+  const int64_t M = ctr[5], base = ctr[4];
+  const int64_t first = M > C ? M - C : 0;
+  const int lane = threadIdx.x & 31;
+  const int vec = stride >> 2;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t i = first + warp; i < M; i += nwarps) {
+    const int r = miss[i];
+    const int v = F[r];
+    const int s = vslot[i % C];
+    if (lane == 0) {
+      const int old = owner[s];
+      if (old >= 0) slot[old] = -1;
+      owner[s] = v;
+      slot[v] = s;
+      stamp[s] = t;
+      seq[s] = base + i;
+    }
+    const float4* src = reinterpret_cast<const float4*>(X) + (int64_t)r * vec;
+    float4* dst = reinterpret_cast<float4*>(cache) + (int64_t)s * vec;
+    for (int c = lane; c < vec; c += 32) dst[c] = __ldg(src + c);
+  }
+}
+
+__global__ void k_dyn_close(int64_t* ctr, const int32_t* sizes, int L, int64_t C) {
+  // ctr: 0 hits, 1 misses, 2 replaced, 3 admitted, 4 seq_next, 5 M, 6 occupied
+  // all-miss admission fills the free slots first: M misses evict
+  // max(0, M - free) residents and leave min(C, occupied + M) occupied
+  const int64_t M = ctr[5], n = sizes[L], fr = C - ctr[6];
+  ctr[0] += n - M;
+  ctr[1] += M;
+  if (C > 0) {
+    ctr[2] += M > fr ? M - fr : 0;
+    ctr[3] += M;
+    ctr[4] += M;
+    ctr[6] = ctr[6] + M < C ? ctr[6] + M : C;
+  }
+}
+
+void launch_cache_update(gnnv_cache* c, const gnnv_blocks* b, const float* d_X, cudaStream_t s) {
+  const int L = b->L;
+  const int64_t cap = b->max_n[L];
+  const int64_t C = c->capacity;
+  const int sms = num_sms();
+  if (cap > c->miss_cap) {  // grow the miss buffers (setup-time synchronisation)
+    GNNV_TRY_CUDA(cudaStreamSynchronize(s));
+    dfree(c->d_miss);
+    dfree(c->d_mflag);
+    dfree(c->d_sel_tmp);
+    c->d_miss = (int32_t*)dmalloc(cap * sizeof(int32_t), "cache miss rows");
+    c->d_mflag = (int32_t*)dmalloc(cap * sizeof(int32_t), "cache miss flags");
+    c->sel_tmp_bytes = 0;
+    cub::CountingInputIterator<int32_t> it(0);
+    GNNV_TRY_CUDA(cub::DeviceSelect::Flagged(nullptr, c->sel_tmp_bytes, it, c->d_mflag, c->d_miss,
+                                             static_cast<int64_t*>(nullptr), (int)cap));
+    c->d_sel_tmp = dmalloc(c->sel_tmp_bytes, "cache select temp");
+    c->miss_cap = cap;
+  }
+  launch_k(k_dyn_hits, (int)std::min<int64_t>(ceil_div(cap, 256), sms * 8), 256, 0, s, b->d_F, b->d_sizes, L, cap,
+           c->d_slot, c->d_stamp, c->step, c->policy == GNNV_POLICY_LRU ? 1 : 0, c->d_mflag);
+  GNNV_CHECK_LAUNCH();
+  cub::CountingInputIterator<int32_t> it(0);
+  GNNV_TRY_CUDA(cub::DeviceSelect::Flagged(c->d_sel_tmp, c->sel_tmp_bytes, it, c->d_mflag, c->d_miss, c->d_ctr + 5,
+                                           (int)cap, s));
+  if (C > 0) {
+    launch_k(k_dyn_keys, (int)std::min<int64_t>(ceil_div(C, 256), sms * 8), 256, 0, s, C, c->d_owner, c->d_stamp,
+             c->d_seq, c->policy == GNNV_POLICY_LRU ? 1 : 0, c->d_keys, c->d_vidx);
+    GNNV_CHECK_LAUNCH();
+    GNNV_TRY_CUDA(cub::DeviceRadixSort::SortPairs(c->d_sort_tmp, c->sort_tmp_bytes, c->d_keys, c->d_keys + C,
+                                                  c->d_vidx, c->d_vidx + C, (int)C, 0, 64, s));
+    launch_k(k_dyn_admit, sms * 8, 256, 0, s, C, c->d_miss, c->d_ctr, c->d_vidx + C, b->d_F, c->d_slot, c->d_owner,
+             c->d_stamp, c->d_seq, c->step, d_X, c->shards[0], c->g->stride);
+    GNNV_CHECK_LAUNCH();
+  }
+  k_dyn_close<<<1, 1, 0, s>>>(c->d_ctr, b->d_sizes, L, C);
+  GNNV_CHECK_LAUNCH();
+  ++c->step;
+}
+
 }  // namespace gnnv
 
 using namespace gnnv;
@@ -186,8 +320,9 @@ gnnv_status gnnv_cache_build(gnnv_graph* g, double ratio, int32_t policy, int32_
     GNNV_REQUIRE(policy == GNNV_POLICY_NONE || policy == GNNV_POLICY_DEGREE || policy == GNNV_POLICY_FIFO ||
                      policy == GNNV_POLICY_LRU,
                  GNNV_ERR_PARAM, "cache_build: unknown policy");
-    GNNV_REQUIRE(policy != GNNV_POLICY_FIFO && policy != GNNV_POLICY_LRU, GNNV_ERR_UNSUPPORTED,
-                 "cache_build: dynamic FIFO/LRU update policies are not built (static DEGREE template only)");
+    const bool dynamic = policy == GNNV_POLICY_FIFO || policy == GNNV_POLICY_LRU;
+    GNNV_REQUIRE(!dynamic || placement == GNNV_PLACE_REPLICA || (placement == GNNV_PLACE_SHARDED && !comm),
+                 GNNV_ERR_UNSUPPORTED, "cache_build: dynamic FIFO/LRU caches are built for one device (REPLICA)");
     GNNV_REQUIRE(placement >= GNNV_PLACE_REPLICA && placement <= GNNV_PLACE_SHARDED_LOCAL, GNNV_ERR_PARAM,
                  "cache_build: unknown placement");
     int G = 1, me = 0;
@@ -210,6 +345,8 @@ gnnv_status gnnv_cache_build(gnnv_graph* g, double ratio, int32_t policy, int32_
     c->world = G;
     c->rank = me;
     c->placement = placement;
+    c->policy = policy;
+    c->dynamic = dynamic;
     try {
       c->d_slot = (int32_t*)dmalloc(n * sizeof(int32_t), "cache slot map");
       c->d_order = (int32_t*)dmalloc(n * sizeof(int32_t), "cache order");
@@ -224,7 +361,7 @@ gnnv_status gnnv_cache_build(gnnv_graph* g, double ratio, int32_t policy, int32_
       void* tmp = dmalloc(tmp_bytes, "sort temp");
       // LSD radix sort is stable: equal degrees keep ascending id order
       GNNV_TRY_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, keys, keys2, ids, c->d_order, (int)n));
-      k_slots<<<sms * 8, 256>>>(c->d_order, n, C, c->d_slot);
+      k_slots<<<sms * 8, 256>>>(c->d_order, n, dynamic ? 0 : C, c->d_slot);  // dynamic: starts empty
       GNNV_CHECK_LAUNCH();
       GNNV_TRY_CUDA(cudaDeviceSynchronize());
       dfree(tmp);
@@ -242,10 +379,26 @@ gnnv_status gnnv_cache_build(gnnv_graph* g, double ratio, int32_t policy, int32_
         c->shards[o] = (float*)dmalloc(bytes, "feature cache (Gamma_cache)");
         c->shard_owned[o] = true;
         c->local_rows += rows;
-        if (rows) {
+        if (rows && !dynamic) {
           k_fill_shard<<<sms * 16, 256>>>(c->d_order, C, G, o, g->d_feats, g->stride, c->shards[o], rows);
           GNNV_CHECK_LAUNCH();
         }
+      }
+      if (dynamic) {
+        const int64_t Cs = std::max<int64_t>(C, 1);
+        c->d_owner = (int32_t*)dmalloc(Cs * sizeof(int32_t), "cache owners");
+        c->d_stamp = (int32_t*)dmalloc(Cs * sizeof(int32_t), "cache stamps");
+        c->d_seq = (int64_t*)dmalloc(Cs * sizeof(int64_t), "cache sequence numbers");
+        c->d_keys = (unsigned long long*)dmalloc(2 * Cs * sizeof(unsigned long long), "cache victim keys");
+        c->d_vidx = (int32_t*)dmalloc(2 * Cs * sizeof(int32_t), "cache victim order");
+        c->d_ctr = (int64_t*)dmalloc(8 * sizeof(int64_t), "cache counters");
+        GNNV_TRY_CUDA(cudaMemset(c->d_owner, 0xFF, Cs * sizeof(int32_t)));
+        GNNV_TRY_CUDA(cudaMemset(c->d_stamp, 0xFF, Cs * sizeof(int32_t)));
+        GNNV_TRY_CUDA(cudaMemset(c->d_seq, 0xFF, Cs * sizeof(int64_t)));
+        GNNV_TRY_CUDA(cudaMemset(c->d_ctr, 0, 8 * sizeof(int64_t)));
+        GNNV_TRY_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, c->sort_tmp_bytes, c->d_keys, c->d_keys + Cs,
+                                                      c->d_vidx, c->d_vidx + Cs, (int)Cs));
+        c->d_sort_tmp = dmalloc(c->sort_tmp_bytes, "cache victim sort temp");
       }
       c->d_shard_ptrs = (const float**)dmalloc(G * sizeof(float*), "shard pointers");
       GNNV_TRY_CUDA(cudaMemcpy((void*)c->d_shard_ptrs, c->shards.data(), G * sizeof(float*), cudaMemcpyHostToDevice));
@@ -280,6 +433,16 @@ gnnv_status gnnv_cache_free(gnnv_cache* c) {
     if (c->shard_ipc[o]) cudaIpcCloseMemHandle(c->shards[o]);
   }
   dfree((void*)c->d_shard_ptrs);
+  dfree(c->d_owner);
+  dfree(c->d_stamp);
+  dfree(c->d_seq);
+  dfree(c->d_keys);
+  dfree(c->d_vidx);
+  dfree(c->d_sort_tmp);
+  dfree(c->d_miss);
+  dfree(c->d_mflag);
+  dfree(c->d_sel_tmp);
+  dfree(c->d_ctr);
   delete c;
   return GNNV_OK;
 }
@@ -295,6 +458,34 @@ gnnv_status gnnv_cache_info(const gnnv_cache* c, gnnv_cache_view* o) {
     o->placement = c->placement;
     o->d_slot = c->d_slot;
     o->d_order = c->d_order;
+  });
+}
+
+gnnv_status gnnv_cache_update(gnnv_cache* c, const gnnv_blocks* b, const float* d_X, gnnv_stream s) {
+  return guarded([&] {
+    GNNV_REQUIRE(c && b && d_X, GNNV_ERR_PARAM, "cache_update: null");
+    GNNV_REQUIRE(c->dynamic, GNNV_ERR_STATE, "cache_update: the cache's policy is static (FIFO/LRU only)");
+    GNNV_REQUIRE(b->sampled, GNNV_ERR_STATE, "cache_update: gnnv_sample has not run on these blocks");
+    GNNV_REQUIRE(c->g == b->g, GNNV_ERR_STATE, "cache_update: cache and blocks belong to different graphs");
+    launch_cache_update(c, b, d_X, (cudaStream_t)s);
+  });
+}
+
+gnnv_status gnnv_cache_counters(const gnnv_cache* c, int64_t* host4) {
+  return guarded([&] {
+    GNNV_REQUIRE(c && host4, GNNV_ERR_PARAM, "cache_counters: null");
+    for (int i = 0; i < 4; ++i) host4[i] = 0;
+    if (!c->dynamic) return;
+    GNNV_TRY_CUDA(cudaDeviceSynchronize());
+    GNNV_TRY_CUDA(cudaMemcpy(host4, c->d_ctr, 4 * sizeof(int64_t), cudaMemcpyDeviceToHost));
+  });
+}
+
+gnnv_status gnnv_cache_owners(const gnnv_cache* c, const int32_t** d_owner) {
+  return guarded([&] {
+    GNNV_REQUIRE(c && d_owner, GNNV_ERR_PARAM, "cache_owners: null");
+    GNNV_REQUIRE(c->dynamic, GNNV_ERR_STATE, "cache_owners: static cache");
+    *d_owner = c->d_owner;
   });
 }
 

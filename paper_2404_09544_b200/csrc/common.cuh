@@ -138,6 +138,24 @@ struct gnnv_cache {
   std::vector<bool> shard_ipc;
   const float** d_shard_ptrs = nullptr;  // device array [world]
   bool peers_ready = true;               // SHARDED: every peer's shard mapped
+  // NEXT-3 dynamic cache (policy FIFO / LRU): starts empty, the misses of
+  // every batch are admitted by gnnv_cache_update (cache.cu)
+  int32_t policy = GNNV_POLICY_DEGREE;
+  bool dynamic = false;
+  int32_t step = 0;                        // batch index t (LRU stamps)
+  int32_t* d_owner = nullptr;              // [C] vertex in slot, -1 free
+  int32_t* d_stamp = nullptr;              // [C] last-access batch (LRU)
+  int64_t* d_seq = nullptr;                // [C] admission sequence number
+  unsigned long long* d_keys = nullptr;    // [2C] victim-order keys
+  int32_t* d_vidx = nullptr;               // [2C] slots sorted by key
+  void* d_sort_tmp = nullptr;
+  size_t sort_tmp_bytes = 0;
+  int32_t* d_miss = nullptr;               // [miss_cap] miss rows of the batch (ascending)
+  int32_t* d_mflag = nullptr;              // [miss_cap]
+  int64_t miss_cap = 0;
+  void* d_sel_tmp = nullptr;
+  size_t sel_tmp_bytes = 0;
+  int64_t* d_ctr = nullptr;                // [6] hits, misses, replaced, admitted, seq_next, n_miss
 };
 
 struct gnnv_blocks {
@@ -202,6 +220,7 @@ struct Timeline {
 void launch_sample(gnnv_graph* g, gnnv_blocks* b, const int32_t* d_seeds, int32_t n_seeds, uint64_t rng_seed,
                    cudaStream_t s);
 // cache.cu
+void launch_cache_update(gnnv_cache* c, const gnnv_blocks* b, const float* d_X, cudaStream_t s);
 void launch_gather(const gnnv_cache* c, const gnnv_blocks* b, float* d_X, int64_t* d_stats, cudaStream_t s,
                    int32_t* d_rowidx = nullptr);
 // Cap on the grid of the sampling / gather kernels (0 = none); the trainer

@@ -212,8 +212,8 @@ gnnv_status gnnv_trainer_create(gnnv_graph* g, gnnv_cache* c, const gnnv_model_d
       GNNV_TRY_CUDA(cudaMallocHost(&t->h_err, 4 * sizeof(int32_t)));
       gnnv_blocks* b = t->b;
       t->Hs[0] = g->stride;
-      t->x_fused = L > 1 && c->capacity == g->n && c->world == 1 && c->shards.size() == 1 && c->shards[0] &&
-                   !getenv("GNNV_NO_XFUSE");
+      t->x_fused = L > 1 && !c->dynamic && c->capacity == g->n && c->world == 1 && c->shards.size() == 1 &&
+                   c->shards[0] && !getenv("GNNV_NO_XFUSE");
       t->table = t->x_fused ? c->shards[0] : nullptr;
       const int64_t xrows = t->x_fused ? b->max_n[L - 1] : b->max_n[L];
       t->H[0] = (float*)dmalloc((size_t)xrows * g->stride * sizeof(float), "X (gathered features)");
@@ -446,6 +446,7 @@ gnnv_status gnnv_trainer_prefetch(gnnv_trainer* t, const int32_t* seeds, int32_t
     GNNV_TRY_CUDA(cudaMemsetAsync(t->d_statsb[k], 0, 4 * sizeof(int64_t), t->side));
     if (tl) tl->mark(t->side, "pf_gather");
     launch_gather(t->c, t->bb[k], t->X[k], t->d_statsb[k], t->side, t->rowidx[k]);
+    if (t->c->dynamic) launch_cache_update(t->c, t->bb[k], t->X[k], t->side);  // NEXT-3 admission
     set_grid_cap(0);
     set_pdl(true);
     if (tl) tl->mark(t->side, "end");
@@ -486,6 +487,7 @@ gnnv_status gnnv_step(gnnv_trainer* t, const int32_t* seeds, int32_t n_seeds, in
       if (tm) GNNV_TRY_CUDA(cudaEventRecord(t->ev[1], s));
       if (tl) tl->mark(s, "gather");
       launch_gather(t->c, t->b, t->H[0], t->d_stats, s, t->rowidx[t->cur]);
+      if (t->c->dynamic) launch_cache_update(t->c, t->b, t->H[0], s);  // NEXT-3 admission
       if (tm) GNNV_TRY_CUDA(cudaEventRecord(t->ev[2], s));
     }
     gnnv_blocks* b = t->b;

@@ -92,6 +92,9 @@ _SIGS = {
     "gnnv_allreduce_sum": (I32, [VP, VP, I64, VP]),
     "gnnv_cache_build": (I32, [VP, F64, I32, I32, VP, I32, PP]),
     "gnnv_cache_ipc_handle": (I32, [VP, VP]),
+    "gnnv_cache_update": (I32, [VP, VP, VP, VP]),
+    "gnnv_cache_counters": (I32, [VP, VP]),
+    "gnnv_cache_owners": (I32, [VP, PP]),
     "gnnv_cache_open_peers": (I32, [VP, VP]),
     "gnnv_cache_free": (I32, [VP]),
     "gnnv_cache_info": (I32, [VP, C.POINTER(CacheView)]),
@@ -290,6 +293,21 @@ class Cache:
         v = CacheView()
         _check(load().gnnv_cache_info(self.h, C.byref(v)))
         return v
+
+    def update(self, blocks: "Blocks", X, stream=None):
+        """Dynamic cache: admit the misses of the batch gathered into X."""
+        _check(load().gnnv_cache_update(self.h, blocks.h, ptr(X), stream_ptr(stream)))
+
+    def counters(self) -> np.ndarray:
+        """Dynamic cache: cumulative (hits, misses, replaced, admitted)."""
+        out = np.zeros(4, np.int64)
+        _check(load().gnnv_cache_counters(self.h, ptr(out)))
+        return out
+
+    def owners_ptr(self) -> int:
+        p = C.c_void_p()
+        _check(load().gnnv_cache_owners(self.h, C.byref(p)))
+        return int(p.value)
 
     def ipc_handle(self) -> bytes:
         """SHARDED: this rank's 64-byte CUDA IPC handle of its shard."""

@@ -490,3 +490,71 @@ def test_biased_trainer_raises_hit_rate(mini):
     assert misses[0] > misses[1] > misses[2], misses
     with pytest.raises(gnnv.GnnvError):
         gnnv.locality_weight(0.3)
+
+
+# ------------------------------------------------- dynamic cache (NEXT-3)
+@pytest.mark.parametrize("policy", [2, 3])  # FIFO, LRU
+@pytest.mark.parametrize("ratio", [0.1, 0.01])
+def test_dynamic_cache_bit_exact(mini, policy, ratio):
+    """Batch after batch: gathered rows (hits now come from rows the cache
+    admitted earlier), the slot map, the slot owners and the cumulative
+    (hits, misses, replaced, admitted) equal the oracle's sequential
+    simulation of SPEC's access_batch."""
+    from gpu_util import read_i32
+    from oracle.cache import DynamicCache
+
+    gd, g = mini
+    fan = [10, 5]
+    cache = gnnv.Cache(g, ratio, policy=policy)
+    C = int(np.floor(ratio * gd.n))
+    ref = DynamicCache(gd.n, C, policy)
+    perm = epoch_seeds(gd.n, 2)
+    blocks = gnnv.Blocks(g, 400, fan)
+    for t in range(6):
+        seeds = perm[(t % 3) * 400:(t % 3 + 1) * 400]  # batches repeat: later ones hit admitted rows
+        blocks.sample(dev_i32(seeds), len(seeds), 40 + (t % 3))
+        views = blocks.info()
+        X = torch.empty((views[-1].max_src, gd.stride), dtype=torch.float32, device="cuda")
+        stats = torch.zeros(4, dtype=torch.int64, device="cuda")
+        gnnv.gather(cache, blocks, X, stats)
+        cache.update(blocks, X)
+        torch.cuda.synchronize()
+        FL = blocks_to_host(blocks)[-1][4]
+        assert X[: len(FL)].cpu().numpy().tobytes() == oracle.gather_rows(gd.feats, FL).tobytes()
+        out = ref.access_batch(FL)
+        s = stats.cpu().tolist()
+        assert s[0] == out["rows"] and s[1] == out["hits"] and s[3] == out["misses"], (t, s, out)
+        np.testing.assert_array_equal(read_i32(cache.info().d_slot, gd.n), ref.slot)
+        if C:
+            np.testing.assert_array_equal(read_i32(cache.owners_ptr(), C), ref.owner)
+        assert cache.counters().tolist() == [ref.hits, ref.misses, ref.replaced, ref.misses if C else 0]
+
+
+def test_dynamic_cache_trainer_pipelined(mini):
+    """The trainer admits each batch's misses after its gather (also when
+    the gather is a prefetch on the side stream): per-step hit counters equal
+    the oracle's sequence."""
+    from oracle.cache import DynamicCache
+
+    gd, g = mini
+    cfg = CONFIGS["mini"]
+    dims = [gd.d, cfg["hidden"], cfg["hidden"], gd.C]
+    B = cfg["batch"]
+    cache = gnnv.Cache(g, 0.1, policy=3)
+    ref = DynamicCache(gd.n, int(np.floor(0.1 * gd.n)), 3)
+    tr = gnnv.Trainer(g, cache, dims, cfg["fanouts"], B, init_weights(dims), prec=2)
+    perm = epoch_seeds(gd.n, 0)
+    batches = [perm[(i % 2) * B:(i % 2 + 1) * B] for i in range(5)]
+    tr.prefetch(batches[0], B, 200)
+    for i in range(5):
+        tr.step(batches[i], B, B, 200 + i, 0.01, want_loss=False)
+        st = tr.stats().tolist()  # this step's batch (the stats of its buffer set)
+        if i + 1 < 5:
+            tr.prefetch(batches[i + 1], B, 201 + i)
+        tr.read_loss()
+        oF, _ = sample_blocks(gd.indptr, gd.indices, batches[i], cfg["fanouts"], 200 + i)
+        out = ref.access_batch(oF[-1])
+        assert st == [out["rows"], out["hits"], 0, out["misses"]], (i, st, out)
+    tr.free()
+    torch.cuda.synchronize()
+    assert cache.counters().tolist()[:3] == [ref.hits, ref.misses, ref.replaced]
