@@ -446,7 +446,10 @@ gnnv_status gnnv_trainer_prefetch(gnnv_trainer* t, const int32_t* seeds, int32_t
     GNNV_TRY_CUDA(cudaMemsetAsync(t->d_statsb[k], 0, 4 * sizeof(int64_t), t->side));
     if (tl) tl->mark(t->side, "pf_gather");
     launch_gather(t->c, t->bb[k], t->X[k], t->d_statsb[k], t->side, t->rowidx[k]);
-    if (t->c->dynamic) launch_cache_update(t->c, t->bb[k], t->X[k], t->side);  // NEXT-3 admission
+    if (t->c->dynamic) {  // NEXT-3 admission
+      if (tl) tl->mark(t->side, "pf_replace");
+      launch_cache_update(t->c, t->bb[k], t->X[k], t->side);
+    }
     set_grid_cap(0);
     set_pdl(true);
     if (tl) tl->mark(t->side, "end");
@@ -487,7 +490,10 @@ gnnv_status gnnv_step(gnnv_trainer* t, const int32_t* seeds, int32_t n_seeds, in
       if (tm) GNNV_TRY_CUDA(cudaEventRecord(t->ev[1], s));
       if (tl) tl->mark(s, "gather");
       launch_gather(t->c, t->b, t->H[0], t->d_stats, s, t->rowidx[t->cur]);
-      if (t->c->dynamic) launch_cache_update(t->c, t->b, t->H[0], s);  // NEXT-3 admission
+      if (t->c->dynamic) {  // NEXT-3 admission (Eq.5's t_replace)
+        if (tl) tl->mark(s, "replace");
+        launch_cache_update(t->c, t->b, t->H[0], s);
+      }
       if (tm) GNNV_TRY_CUDA(cudaEventRecord(t->ev[2], s));
     }
     gnnv_blocks* b = t->b;
