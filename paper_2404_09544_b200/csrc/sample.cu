@@ -13,7 +13,10 @@
 //                     a fixed-stride slot array ell[r*k + i]; each id not yet
 //                     in F_h is "claimed" with atomicMax(tag[u], -(2+slot)),
 //                     i.e. the smallest (row, position) slot wins -- exactly
-//                     the first appearance in the (dst, position) scan.
+//                     the first appearance in the (dst, position) scan.  The
+//                     atomic is skipped when a read already shows an earlier
+//                     claim (hub vertices draw thousands of claimants; the
+//                     max is monotone, so a stale read only costs an atomic).
 //   k_sample_hop_tpr: the same for k <= 8 with one thread per row (more rows
 //                     in flight per warp); bit-identical.
 //   k_winners       : slot-parallel over the hop: slot e won iff tag[u] still
@@ -168,7 +171,7 @@ __global__ void __launch_bounds__(256) k_sample_hop(const int64_t* __restrict__ 
       const int e = r * k + slot;
       ell[e] = u;
       if ((uint32_t)u < (uint64_t)N) {
-        if (tag[u] < 0) atomicMax(&tag[u], -(2 + e));
+        if (tag[u] < -(2 + e)) atomicMax(&tag[u], -(2 + e));  // skip if an earlier slot already claimed u
       }
     }
     if (active && gl == 0) {
@@ -241,7 +244,7 @@ __global__ void __launch_bounds__(256) k_sample_hop_tpr(const int64_t* __restric
     if (i < c) {
       const int e = r * k + i;
       ell[e] = u[i];
-      if ((uint32_t)u[i] < (uint64_t)N && tag[u[i]] < 0) atomicMax(&tag[u[i]], -(2 + e));
+      if ((uint32_t)u[i] < (uint64_t)N && tag[u[i]] < -(2 + e)) atomicMax(&tag[u[i]], -(2 + e));
     }
   }
   cnt[r] = c;
@@ -384,7 +387,7 @@ __global__ void __launch_bounds__(256) k_sample_hop_biased(const int64_t* __rest
       const int u = __ldg(&indices[beg + pos]);
       const int e = r * k + lane;
       ell[e] = u;
-      if ((uint32_t)u < (uint64_t)N && tag[u] < 0) atomicMax(&tag[u], -(2 + e));
+      if ((uint32_t)u < (uint64_t)N && tag[u] < -(2 + e)) atomicMax(&tag[u], -(2 + e));
     }
     if (lane == 0) {
       cnt[r] = c;
