@@ -558,3 +558,27 @@ def test_dynamic_cache_trainer_pipelined(mini):
     tr.free()
     torch.cuda.synchronize()
     assert cache.counters().tolist()[:3] == [ref.hits, ref.misses, ref.replaced]
+
+
+def test_nccl_comm_world1(mini):
+    """The NCCL plumbing of the data-parallel path on one rank: the library
+    loads NCCL, creates a communicator from a unique id, runs the trainer's
+    all-reduce (identity for one rank) and builds a SHARDED cache with it."""
+    gd, g = mini
+    comm = gnnv.Comm(0, 1, gnnv.Comm.unique_id(), 0)
+    t = torch.arange(10, dtype=torch.float32, device="cuda")
+    comm.allreduce_sum(t)
+    torch.cuda.synchronize()
+    assert t.tolist() == list(range(10))
+    cache = gnnv.Cache(g, 0.3, placement=gnnv.PLACE_SHARDED, comm=comm)
+    cfg = CONFIGS["mini"]
+    dims = [gd.d, cfg["hidden"], cfg["hidden"], gd.C]
+    tr = gnnv.Trainer(g, cache, dims, cfg["fanouts"], cfg["batch"], init_weights(dims), prec=2, comm=comm)
+    seeds = epoch_seeds(gd.n, 0)[: cfg["batch"]]
+    loss, _ = tr.step(seeds, len(seeds), len(seeds), 3, 0.01)
+    ref = train_step(gd.indptr, gd.indices, gd.feats, gd.d, gd.labels, seeds, cfg["fanouts"], 3, init_weights(dims),
+                     0.01)
+    assert abs(loss - ref["loss"]) <= 5e-3 * abs(ref["loss"])
+    tr.free()
+    cache.free()
+    comm.free()
