@@ -384,7 +384,9 @@ def main():
             s2, n2 = batch(t + 1, host)
             tr.prefetch(s2, n2, BASE_RNG_SEED + t + 1, on_host=host, stream=pf_stream)
             pending["t"] = t + 1
-        return tr.read_loss(stream=stream) if want_loss else None
+        # the step's loss is read back asynchronously: a ticket now, the value
+        # once its copy has landed (one step later), no stream synchronisation
+        return tr.loss_async(stream=stream) if want_loss else None
 
     def drain():
         if pending["t"] is not None:  # consume the trailing prefetch (untimed)
@@ -446,8 +448,13 @@ def main():
     t_e2e0 = time.perf_counter()
     e0.record(stream)
     loss = None
+    prev = None
     for t in range(t0_steps, t0_steps + args.steps):
-        loss = run(t, host=True, want_loss=True)
+        ticket = run(t, host=True, want_loss=True)
+        if prev is not None:
+            loss = tr.loss_result(prev)  # step t-1's loss on the host (device -> host read every step)
+        prev = ticket
+    loss = tr.loss_result(prev)
     e1.record(stream)
     barrier()
     wall_e2e = time.perf_counter() - t_e2e0

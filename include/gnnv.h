@@ -406,6 +406,14 @@ gnnv_status gnnv_trainer_prefetch(gnnv_trainer* t, const int32_t* seeds, int32_t
  * and reports a pending seed error.  Lets a pipelined loop enqueue the next
  * prefetch before blocking on the loss. */
 gnnv_status gnnv_trainer_read_loss(gnnv_trainer* t, float* loss_out, gnnv_stream s);
+/* Asynchronous loss read-back (the e2e loop's per-step result without a
+ * per-step stream synchronisation): _loss_async enqueues on `s` the copy of
+ * the last step's loss (and the seed-error flag) into a pinned ring slot and
+ * returns a ticket; _loss_result waits for that copy only and returns the
+ * loss (PARAM if the step saw a bad seed).  The ring holds 8 tickets; a
+ * ticket older than 8 issues is STATE. */
+gnnv_status gnnv_trainer_loss_async(gnnv_trainer* t, int64_t* ticket, gnnv_stream s);
+gnnv_status gnnv_trainer_loss_result(gnnv_trainer* t, int64_t ticket, float* loss_out);
 /* Device counters of the last step's gather: int64[4] (see gnnv_gather). */
 gnnv_status gnnv_trainer_stats(gnnv_trainer* t, int64_t* host_stats4);
 

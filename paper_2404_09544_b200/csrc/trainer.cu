@@ -36,6 +36,13 @@ struct gnnv_trainer {
   int32_t* h_seeds = nullptr;  // pinned staging
   float* h_out = nullptr;      // pinned: loss
   int32_t* h_err = nullptr;    // pinned: sample error flag
+  // asynchronous loss read-back: a ring of pinned (loss, error flag) slots,
+  // each completed by an event (gnnv_trainer_loss_async / _loss_result)
+  static constexpr int kLossRing = 8;
+  float* h_lossr = nullptr;       // [kLossRing]
+  int32_t* h_errr = nullptr;      // [kLossRing]
+  cudaEvent_t ev_loss[kLossRing] = {nullptr};
+  int64_t loss_tickets = 0;
   float* H[GNNV_MAX_LAYERS + 1] = {nullptr};
   int32_t Hs[GNNV_MAX_LAYERS + 1] = {0};
   float* A[GNNV_MAX_LAYERS + 1] = {nullptr};
@@ -155,6 +162,10 @@ gnnv_status gnnv_trainer_free(gnnv_trainer* t) {
   dfree(t->d_params);
   dfree(t->d_grads);
   if (t->h_out) cudaFreeHost(t->h_out);
+  if (t->h_lossr) cudaFreeHost(t->h_lossr);
+  if (t->h_errr) cudaFreeHost(t->h_errr);
+  for (auto& e : t->ev_loss)
+    if (e) cudaEventDestroy(e);
   if (t->h_err) cudaFreeHost(t->h_err);
   for (int i = 1; i <= GNNV_MAX_LAYERS; ++i) {
     dfree(t->H[i]);
@@ -209,6 +220,9 @@ gnnv_status gnnv_trainer_create(gnnv_graph* g, gnnv_cache* c, const gnnv_model_d
       t->d_seeds = (int32_t*)dmalloc(md->max_seeds * sizeof(int32_t), "seeds");
       GNNV_TRY_CUDA(cudaMallocHost(&t->h_seeds, md->max_seeds * sizeof(int32_t)));
       GNNV_TRY_CUDA(cudaMallocHost(&t->h_out, 4 * sizeof(float)));
+      GNNV_TRY_CUDA(cudaMallocHost(&t->h_lossr, gnnv_trainer::kLossRing * sizeof(float)));
+      GNNV_TRY_CUDA(cudaMallocHost(&t->h_errr, gnnv_trainer::kLossRing * sizeof(int32_t)));
+      for (auto& e : t->ev_loss) GNNV_TRY_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
       GNNV_TRY_CUDA(cudaMallocHost(&t->h_err, 4 * sizeof(int32_t)));
       gnnv_blocks* b = t->b;
       t->Hs[0] = g->stride;
@@ -358,6 +372,35 @@ gnnv_status gnnv_trainer_read_loss(gnnv_trainer* t, float* loss_out, gnnv_stream
       GNNV_TRY_CUDA(cudaMemsetAsync(t->b->d_sizes + 2 * L + 1, 0, sizeof(int32_t), s));
       throw Error{GNNV_ERR_PARAM, "step: repeated or out-of-range seed id"};
     }
+  });
+}
+
+gnnv_status gnnv_trainer_loss_async(gnnv_trainer* t, int64_t* ticket, gnnv_stream stream) {
+  return guarded([&] {
+    GNNV_REQUIRE(t && ticket, GNNV_ERR_PARAM, "loss_async: null");
+    cudaStream_t s = (cudaStream_t)stream;
+    const int L = t->md.L;
+    const int k = (int)(t->loss_tickets % gnnv_trainer::kLossRing);
+    // the slot's previous copy must have landed before it is reused
+    if (t->loss_tickets >= gnnv_trainer::kLossRing) GNNV_TRY_CUDA(cudaEventSynchronize(t->ev_loss[k]));
+    GNNV_TRY_CUDA(
+        cudaMemcpyAsync(t->h_lossr + k, t->d_grads + t->nparams, sizeof(float), cudaMemcpyDeviceToHost, s));
+    GNNV_TRY_CUDA(
+        cudaMemcpyAsync(t->h_errr + k, t->b->d_sizes + 2 * L + 1, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    GNNV_TRY_CUDA(cudaEventRecord(t->ev_loss[k], s));
+    *ticket = t->loss_tickets++;
+  });
+}
+
+gnnv_status gnnv_trainer_loss_result(gnnv_trainer* t, int64_t ticket, float* loss_out) {
+  return guarded([&] {
+    GNNV_REQUIRE(t && loss_out, GNNV_ERR_PARAM, "loss_result: null");
+    GNNV_REQUIRE(ticket >= 0 && ticket < t->loss_tickets && ticket >= t->loss_tickets - gnnv_trainer::kLossRing,
+                 GNNV_ERR_STATE, "loss_result: ticket not issued or already recycled (ring of 8)");
+    const int k = (int)(ticket % gnnv_trainer::kLossRing);
+    GNNV_TRY_CUDA(cudaEventSynchronize(t->ev_loss[k]));
+    *loss_out = t->h_lossr[k];
+    GNNV_REQUIRE(!t->h_errr[k], GNNV_ERR_PARAM, "step: repeated or out-of-range seed id");
   });
 }
 

@@ -119,6 +119,8 @@ _SIGS = {
     "gnnv_trainer_set_params": (I32, [VP, VP]),
     "gnnv_trainer_blocks": (VP, [VP]),
     "gnnv_trainer_x_level": (I32, [VP]),
+    "gnnv_trainer_loss_async": (I32, [VP, VP, VP]),
+    "gnnv_trainer_loss_result": (I32, [VP, C.c_int64, VP]),
     "gnnv_trainer_set_locality": (I32, [VP, I32]),
     "gnnv_blocks_set_locality": (I32, [VP, VP, I32]),
     "gnnv_trainer_activation": (I32, [VP, I32, PP, C.POINTER(I32)]),
@@ -485,6 +487,17 @@ class Trainer:
     def read_loss(self, stream=None) -> float:
         out = C.c_float(0.0)
         _check(load().gnnv_trainer_read_loss(self.h, C.byref(out), stream_ptr(stream)))
+        return float(out.value)
+
+    def loss_async(self, stream=None) -> int:
+        """Enqueue the last step's loss read-back; returns a ticket."""
+        t = C.c_int64(0)
+        _check(load().gnnv_trainer_loss_async(self.h, C.byref(t), stream_ptr(stream)))
+        return int(t.value)
+
+    def loss_result(self, ticket: int) -> float:
+        out = C.c_float(0.0)
+        _check(load().gnnv_trainer_loss_result(self.h, int(ticket), C.byref(out)))
         return float(out.value)
 
     def params(self) -> np.ndarray:

@@ -582,3 +582,25 @@ def test_nccl_comm_world1(mini):
     tr.free()
     cache.free()
     comm.free()
+
+
+def test_async_loss_readback(mini):
+    """gnnv_trainer_loss_async / _loss_result return the same losses as the
+    synchronous read, with several steps in flight."""
+    gd, g = mini
+    cfg = CONFIGS["mini"]
+    dims = [gd.d, cfg["hidden"], cfg["hidden"], gd.C]
+    B = cfg["batch"]
+    perm = epoch_seeds(gd.n, 0)
+    cache = gnnv.Cache(g, 0.3)
+    a = gnnv.Trainer(g, cache, dims, cfg["fanouts"], B, init_weights(dims), prec=2)
+    b = gnnv.Trainer(g, cache, dims, cfg["fanouts"], B, init_weights(dims), prec=2)
+    sync = [a.step(perm[i * B:(i + 1) * B], B, B, 50 + i, 0.01)[0] for i in range(10)]
+    tickets = []
+    for i in range(10):
+        b.step(perm[i * B:(i + 1) * B], B, B, 50 + i, 0.01, want_loss=False)
+        tickets.append(b.loss_async())
+    got = [b.loss_result(t) for t in tickets[-8:]]
+    assert got == sync[-8:]
+    with pytest.raises(gnnv.GnnvError):
+        b.loss_result(tickets[0])  # recycled (ring of 8)
