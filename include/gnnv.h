@@ -36,6 +36,10 @@
  *    up to a multiple of 4 floats (16-byte rows); padding columns are written
  *    as 0 by every kernel that produces them.  The graph feature table may
  *    use any stride >= d that is a multiple of 4.
+ *  - Concurrency.  The GEMM launches (gnnv_layer_*, gnnv_dense_*, gnnv_step)
+ *    share per-process workspaces (weight images): on one device they must
+ *    not run concurrently on different streams.  Sampling and gathering on
+ *    separate blocks/buffers may (the trainer's Eq.4 prefetch does).
  *  - Determinism.  gnnv_sample output is a pure function of (graph, seeds,
  *    fanouts, rng_seed): independent of device, stream, rank and world size.
  *    gnnv_gather rows are bit-exact copies.

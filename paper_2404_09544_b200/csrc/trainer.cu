@@ -69,6 +69,7 @@ struct gnnv_trainer {
   int pend_n = 0;
   uint64_t pend_rng = 0;
   cudaStream_t side = nullptr;
+  void* green = nullptr;  // CUgreenCtx of the side stream (GNNV_PF_SMS), or null
   cudaEvent_t ev_ready[2] = {nullptr, nullptr}, ev_free[2] = {nullptr, nullptr}, ev_in = nullptr;
   cudaEvent_t ev_h2d[2] = {nullptr, nullptr};  // last copy out of h_seedsb[k]
   bool h2d_used[2] = {false, false};
@@ -108,7 +109,7 @@ static F drv(const char* name) {
   return reinterpret_cast<F>(p);
 }
 
-static cudaStream_t make_side_stream(int device) {
+static cudaStream_t make_side_stream(int device, void** green_ctx) {
   int lo = 0, hi = 0;
   GNNV_TRY_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
   const char* e = getenv("GNNV_PF_SMS");
@@ -133,6 +134,7 @@ static cudaStream_t make_side_stream(int device) {
                      create(&gc, desc, dev, CU_GREEN_CTX_DEFAULT_STREAM) == CUDA_SUCCESS &&
                      mkstream(&st, gc, CU_STREAM_NON_BLOCKING, lo) == CUDA_SUCCESS,
                  GNNV_ERR_CUDA, "green context for the prefetch stream");
+    *green_ctx = (void*)gc;
     return (cudaStream_t)st;
   }
   cudaStream_t st;
@@ -159,6 +161,12 @@ gnnv_status gnnv_trainer_free(gnnv_trainer* t) {
   }
   if (t->ev_in) cudaEventDestroy(t->ev_in);
   if (t->side) cudaStreamDestroy(t->side);
+  if (t->green) {
+    try {
+      drv<CUresult (*)(CUgreenCtx)>("cuGreenCtxDestroy")((CUgreenCtx)t->green);
+    } catch (...) {
+    }
+  }
   dfree(t->d_params);
   dfree(t->d_grads);
   if (t->h_out) cudaFreeHost(t->h_out);
@@ -462,7 +470,7 @@ gnnv_status gnnv_trainer_prefetch(gnnv_trainer* t, const int32_t* seeds, int32_t
       t->d_seedsb[k] = (int32_t*)dmalloc(t->md.max_seeds * sizeof(int32_t), "seeds (prefetch)");
       GNNV_TRY_CUDA(cudaMallocHost(&t->h_seedsb[k], t->md.max_seeds * sizeof(int32_t)));
       t->d_statsb[k] = (int64_t*)dmalloc(4 * sizeof(int64_t), "gather stats (prefetch)");
-      if (!t->side) t->side = make_side_stream(g->device);
+      if (!t->side) t->side = make_side_stream(g->device, &t->green);
     }
     cudaStream_t s = (cudaStream_t)stream;
     // order after the step that last computed on buffer set k and, for
@@ -482,8 +490,17 @@ gnnv_status gnnv_trainer_prefetch(gnnv_trainer* t, const int32_t* seeds, int32_t
       const char* e = getenv("GNNV_PF_BLOCKS");
       return e ? atoi(e) : 0;
     }();
-    set_grid_cap(pf_cap);
-    set_pdl(false);
+    // launch settings of the overlapped batch, restored on every exit path
+    struct PrefetchLaunch {
+      explicit PrefetchLaunch(int cap) {
+        set_grid_cap(cap);
+        set_pdl(false);
+      }
+      ~PrefetchLaunch() {
+        set_grid_cap(0);
+        set_pdl(true);
+      }
+    } pf_launch(pf_cap);
     launch_sample(g, t->bb[k], d_seeds, n_seeds, rng_seed, t->side);
     t->bb[k]->sampled = true;
     GNNV_TRY_CUDA(cudaMemsetAsync(t->d_statsb[k], 0, 4 * sizeof(int64_t), t->side));
@@ -493,8 +510,7 @@ gnnv_status gnnv_trainer_prefetch(gnnv_trainer* t, const int32_t* seeds, int32_t
       if (tl) tl->mark(t->side, "pf_replace");
       launch_cache_update(t->c, t->bb[k], t->X[k], t->side);
     }
-    set_grid_cap(0);
-    set_pdl(true);
+
     if (tl) tl->mark(t->side, "end");
     GNNV_TRY_CUDA(cudaEventRecord(t->ev_ready[k], t->side));
     t->pending = true;
