@@ -604,3 +604,29 @@ def test_async_loss_readback(mini):
     assert got == sync[-8:]
     with pytest.raises(gnnv.GnnvError):
         b.loss_result(tickets[0])  # recycled (ring of 8)
+
+
+@pytest.mark.parametrize("kind", ["sage", "gcn"])
+@pytest.mark.parametrize("prec", [0, 2])
+def test_step_degenerate_graph(kind, prec):
+    """A whole training step on a graph with an isolated seed (zero sampled
+    neighbours: mean aggregate 0 for SAGE, the vertex itself for GCN --
+    reading Q15) and rows with fewer neighbours than the fanout, as fp32 and
+    as tf32 with the whole table cached (the layer-1 table-reading path)."""
+    lib()
+    gd = tiny_graph("isolated", d=6, C=3)
+    g = gnnv.Graph.from_data(gd)
+    dims = [gd.d, 8, gd.C]
+    kid = gnnv.KIND_SAGE if kind == "sage" else gnnv.KIND_GCN
+    w = init_weights(dims, kind=kind)
+    cache = gnnv.Cache(g, 1.0)
+    tr = gnnv.Trainer(g, cache, dims, [3, 2], 4, w, kind=kid, prec=prec)
+    seeds = np.array([5, 0, 2, 4])  # 5 is isolated
+    loss, _ = tr.step(seeds, 4, 4, 17, 0.1)
+    ref = train_step(gd.indptr, gd.indices, gd.feats, gd.d, gd.labels, seeds, [3, 2], 17, w, 0.1, kind=kind)
+    tol = 1e-4 if prec == 0 else 5e-3
+    assert abs(loss - ref["loss"]) <= tol * abs(ref["loss"])
+    grads = gnnv.unflat_params(tr.grads(), dims, kid)
+    for (gW, gb), (rW, rb) in zip(grads, ref["grads"]):
+        assert normwise(gW, rW) < (1e-4 if prec == 0 else 2e-2)
+        assert normwise(gb, rb) < (1e-4 if prec == 0 else 2e-2)
