@@ -411,11 +411,13 @@ gnnv_status gnnv_trainer_prefetch(gnnv_trainer* t, const int32_t* seeds, int32_t
  * prefetch before blocking on the loss. */
 gnnv_status gnnv_trainer_read_loss(gnnv_trainer* t, float* loss_out, gnnv_stream s);
 /* Asynchronous loss read-back (the e2e loop's per-step result without a
- * per-step stream synchronisation): _loss_async enqueues on `s` the copy of
- * the last step's loss (and the seed-error flag) into a pinned ring slot and
- * returns a ticket; _loss_result waits for that copy only and returns the
- * loss (PARAM if the step saw a bad seed).  The ring holds 8 tickets; a
- * ticket older than 8 issues is STATE. */
+ * per-step stream synchronisation): every step's SGD kernel writes the
+ * step's all-reduced loss and seed-error flag into a mapped pinned ring
+ * slot (zero-copy, no copy on the stream); _loss_async records an event on
+ * `s` after the last enqueued step and returns its ticket (the step index);
+ * _loss_result waits for that event only and returns the loss (PARAM if the
+ * step saw a bad seed).  The ring holds the last 8 steps; an older ticket
+ * is STATE.  STATE before the first step. */
 gnnv_status gnnv_trainer_loss_async(gnnv_trainer* t, int64_t* ticket, gnnv_stream s);
 gnnv_status gnnv_trainer_loss_result(gnnv_trainer* t, int64_t ticket, float* loss_out);
 /* Device counters of the last step's gather: int64[4] (see gnnv_gather). */

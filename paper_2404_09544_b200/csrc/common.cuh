@@ -294,6 +294,7 @@ void launch_relu_mask(const float* G, const float* H, float* Gp, int32_t ld, int
 void launch_ce_loss(const float* z, int32_t ldz, int32_t C, const int32_t* d_rows, const int32_t* d_F,
                     const int32_t* d_labels, int32_t n_global, float* d_loss, float* dz, float* partial,
                     unsigned int* counter, int64_t max_rows, cudaStream_t s);
-void launch_sgd(float* p, const float* g, int64_t n, float lr, cudaStream_t s);
+void launch_sgd(float* p, const float* g, int64_t n, float lr, cudaStream_t s, float* out_loss = nullptr,
+                int32_t* out_err = nullptr, const int32_t* err = nullptr);
 
 }  // namespace gnnv

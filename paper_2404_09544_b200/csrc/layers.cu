@@ -207,16 +207,25 @@ void launch_ce_loss(const float* z, int32_t ldz, int32_t C, const int32_t* d_row
   GNNV_CHECK_LAUNCH();
 }
 
-__global__ void k_sgd(float* __restrict__ p, const float* __restrict__ g, int64_t n, float lr) {
+// p -= lr g; with `out_loss` (the trainer's mapped host ring slot) thread 0
+// also publishes the step's all-reduced loss g[n] and the seed-error flag,
+// so the host reads the step's result without a copy on the stream.
+__global__ void k_sgd(float* __restrict__ p, const float* __restrict__ g, int64_t n, float lr, float* out_loss,
+                      int32_t* out_err, const int32_t* err) {
   GNNV_PDL_ENTRY();
+  if (out_loss && blockIdx.x == 0 && threadIdx.x == 0) {
+    *out_loss = g[n];
+    *out_err = *err;
+    __threadfence_system();
+  }
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     p[i] -= lr * g[i];
 }
-
-void launch_sgd(float* p, const float* g, int64_t n, float lr, cudaStream_t s) {
+void launch_sgd(float* p, const float* g, int64_t n, float lr, cudaStream_t s, float* out_loss, int32_t* out_err,
+                const int32_t* err) {
   if (n <= 0) return;
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, 256), (int64_t)num_sms() * 4));
-  launch_k(k_sgd, grid, 256, 0, s, p, g, n, lr);
+  launch_k(k_sgd, grid, 256, 0, s, p, g, n, lr, out_loss, out_err, err);
   GNNV_CHECK_LAUNCH();
 }
 

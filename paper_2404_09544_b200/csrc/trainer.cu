@@ -39,9 +39,12 @@ struct gnnv_trainer {
   // asynchronous loss read-back: a ring of pinned (loss, error flag) slots,
   // each completed by an event (gnnv_trainer_loss_async / _loss_result)
   static constexpr int kLossRing = 8;
-  float* h_lossr = nullptr;       // [kLossRing]
-  int32_t* h_errr = nullptr;      // [kLossRing]
+  float* h_lossr = nullptr;       // [kLossRing] mapped pinned: the SGD kernel writes step s's loss at s % ring
+  int32_t* h_errr = nullptr;      // [kLossRing] mapped pinned: its seed-error flag
+  float* d_lossr = nullptr;       // device aliases of the two rings
+  int32_t* d_errr = nullptr;
   cudaEvent_t ev_loss[kLossRing] = {nullptr};
+  int64_t steps_done = 0;         // steps enqueued (the ring position)
   int64_t loss_tickets = 0;
   float* H[GNNV_MAX_LAYERS + 1] = {nullptr};
   int32_t Hs[GNNV_MAX_LAYERS + 1] = {0};
@@ -228,8 +231,10 @@ gnnv_status gnnv_trainer_create(gnnv_graph* g, gnnv_cache* c, const gnnv_model_d
       t->d_seeds = (int32_t*)dmalloc(md->max_seeds * sizeof(int32_t), "seeds");
       GNNV_TRY_CUDA(cudaMallocHost(&t->h_seeds, md->max_seeds * sizeof(int32_t)));
       GNNV_TRY_CUDA(cudaMallocHost(&t->h_out, 4 * sizeof(float)));
-      GNNV_TRY_CUDA(cudaMallocHost(&t->h_lossr, gnnv_trainer::kLossRing * sizeof(float)));
-      GNNV_TRY_CUDA(cudaMallocHost(&t->h_errr, gnnv_trainer::kLossRing * sizeof(int32_t)));
+      GNNV_TRY_CUDA(cudaHostAlloc(&t->h_lossr, gnnv_trainer::kLossRing * sizeof(float), cudaHostAllocMapped));
+      GNNV_TRY_CUDA(cudaHostAlloc(&t->h_errr, gnnv_trainer::kLossRing * sizeof(int32_t), cudaHostAllocMapped));
+      GNNV_TRY_CUDA(cudaHostGetDevicePointer((void**)&t->d_lossr, t->h_lossr, 0));
+      GNNV_TRY_CUDA(cudaHostGetDevicePointer((void**)&t->d_errr, t->h_errr, 0));
       for (auto& e : t->ev_loss) GNNV_TRY_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
       GNNV_TRY_CUDA(cudaMallocHost(&t->h_err, 4 * sizeof(int32_t)));
       gnnv_blocks* b = t->b;
@@ -388,27 +393,27 @@ gnnv_status gnnv_trainer_loss_async(gnnv_trainer* t, int64_t* ticket, gnnv_strea
     GNNV_REQUIRE(t && ticket, GNNV_ERR_PARAM, "loss_async: null");
     cudaStream_t s = (cudaStream_t)stream;
     const int L = t->md.L;
-    const int k = (int)(t->loss_tickets % gnnv_trainer::kLossRing);
-    // the slot's previous copy must have landed before it is reused
-    if (t->loss_tickets >= gnnv_trainer::kLossRing) GNNV_TRY_CUDA(cudaEventSynchronize(t->ev_loss[k]));
-    GNNV_TRY_CUDA(
-        cudaMemcpyAsync(t->h_lossr + k, t->d_grads + t->nparams, sizeof(float), cudaMemcpyDeviceToHost, s));
-    GNNV_TRY_CUDA(
-        cudaMemcpyAsync(t->h_errr + k, t->b->d_sizes + 2 * L + 1, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    (void)L;
+    GNNV_REQUIRE(t->steps_done > 0, GNNV_ERR_STATE, "loss_async: no step has run");
+    // the last step's SGD kernel writes its loss into the mapped ring slot;
+    // an event marks when that write is complete (no copy on the stream)
+    const int64_t step = t->steps_done - 1;
+    const int k = (int)(step % gnnv_trainer::kLossRing);
     GNNV_TRY_CUDA(cudaEventRecord(t->ev_loss[k], s));
-    *ticket = t->loss_tickets++;
+    *ticket = step;
+    t->loss_tickets = t->steps_done;
   });
 }
 
 gnnv_status gnnv_trainer_loss_result(gnnv_trainer* t, int64_t ticket, float* loss_out) {
   return guarded([&] {
     GNNV_REQUIRE(t && loss_out, GNNV_ERR_PARAM, "loss_result: null");
-    GNNV_REQUIRE(ticket >= 0 && ticket < t->loss_tickets && ticket >= t->loss_tickets - gnnv_trainer::kLossRing,
+    GNNV_REQUIRE(ticket >= 0 && ticket < t->loss_tickets && ticket >= t->steps_done - gnnv_trainer::kLossRing,
                  GNNV_ERR_STATE, "loss_result: ticket not issued or already recycled (ring of 8)");
     const int k = (int)(ticket % gnnv_trainer::kLossRing);
     GNNV_TRY_CUDA(cudaEventSynchronize(t->ev_loss[k]));
-    *loss_out = t->h_lossr[k];
-    GNNV_REQUIRE(!t->h_errr[k], GNNV_ERR_PARAM, "step: repeated or out-of-range seed id");
+    *loss_out = ((volatile float*)t->h_lossr)[k];
+    GNNV_REQUIRE(!((volatile int32_t*)t->h_errr)[k], GNNV_ERR_PARAM, "step: repeated or out-of-range seed id");
   });
 }
 
@@ -581,7 +586,12 @@ gnnv_status gnnv_step(gnnv_trainer* t, const int32_t* seeds, int32_t n_seeds, in
     }
     if (tm) GNNV_TRY_CUDA(cudaEventRecord(t->ev[6], s));
     if (tl) tl->mark(s, "sgd");
-    launch_sgd(t->d_params, t->d_grads, t->nparams, lr, s);
+    {
+      const int slot = (int)(t->steps_done % gnnv_trainer::kLossRing);
+      launch_sgd(t->d_params, t->d_grads, t->nparams, lr, s, t->d_lossr + slot, t->d_errr + slot,
+                 b->d_sizes + 2 * L + 1);
+      ++t->steps_done;
+    }
     if (tl) tl->mark(s, "end");
     GNNV_TRY_CUDA(cudaEventRecord(t->ev_free[t->cur], s));  // buffer set may be refilled
     if (tm) GNNV_TRY_CUDA(cudaEventRecord(t->ev[7], s));
