@@ -534,6 +534,13 @@ gnnv_status gnnv_step(gnnv_trainer* t, const int32_t* seeds, int32_t n_seeds, in
     gnnv_graph* g = t->g;
     const int L = t->md.L;
     Timeline* tl = t->tl.on ? &t->tl : nullptr;
+    // Programmatic dependent launch only for a serial step: with the Eq.4
+    // prefetch in flight the next kernel's early-resident CTAs take SM slots
+    // the overlapped batch needs (measured: 1.49 vs 1.41 ms per products step)
+    struct StepPdl {
+      explicit StepPdl(bool on) { set_pdl(on); }
+      ~StepPdl() { set_pdl(true); }
+    } step_pdl(!t->pending);
     if (tm) GNNV_TRY_CUDA(cudaEventRecord(t->ev[0], s));
     if (t->pending) {
       // the batch was sampled and gathered by gnnv_trainer_prefetch
