@@ -255,7 +255,9 @@ def algorithmic(seg: str, sizes, cfg, dims, stride, prec, peaks):
     if name == "gather":
         rowb = stride * 4
         lvl = int(sizes.get("x_level", L))
-        if lvl < L:  # whole table cached: rows of F_{L-1} copied, every F_L row resolved to its cache row
+        if lvl < 0:  # whole table cached, layer-1 GEMMs gather H_dst from it: F_L rows resolved, none copied
+            by = n[L] * 12
+        elif lvl < L:  # whole table cached: rows of F_{L-1} copied, every F_L row resolved to its cache row
             by = 2 * n[lvl] * rowb + n[L] * 12
         else:
             by = sizes["hits"] * rowb + n[L] * rowb + n[L] * 8

@@ -352,13 +352,24 @@ gnnv_status gnnv_trainer_set_params(gnnv_trainer* t, const float* host_params);
  * step. */
 gnnv_blocks* gnnv_trainer_blocks(gnnv_trainer* t);
 /* Which rows of X (activation 0) the trainer materialises: F_level, i.e.
- * L (every row of F_L) or L-1 (the dst prefix F_{L-1} only).  L-1 when the
- * cache holds the whole table on this device (capacity N, one shard): the
- * gather then writes only the rows the layer-1 GEMMs read and the layer-1
- * aggregation reads its source rows from the cache table directly (the
- * retrieval still goes through the cache's slot map; hit counters still
- * cover every row of F_L).  GNNV_NO_XFUSE=1 in the environment disables it. */
+ * L (every row of F_L), L-1 (the dst prefix F_{L-1} only) or -1 (none).
+ * L-1 when the cache holds the whole table on this device (capacity N, one
+ * shard): the gather then writes only the rows the layer-1 GEMMs read and
+ * the layer-1 aggregation reads its source rows from the cache table
+ * directly (the retrieval still goes through the cache's slot map; hit
+ * counters still cover every row of F_L).  -1 when in addition the model is
+ * SAGE with TF32 GEMMs and GNNV_XROWS=1 was set when the trainer was
+ * created: the layer-1 GEMMs (forward and dW) then read the H_dst rows from
+ * the table as well (TMA gather4 through the same row indices) and X is
+ * never written (off by default: slower on products).
+ * GNNV_NO_XFUSE=1 in the environment disables both. */
 int32_t gnnv_trainer_x_level(const gnnv_trainer* t);
+/* Whole-table mode (x_level < L): *d_rowidx = int32[n_L] cache-table row of
+ * every F_L row of the last step (row u of layer 1's input is row
+ * (*d_rowidx)[u] of *d_table, a [N x stride] fp32 table in degree-rank
+ * order); both NULL otherwise.  Borrowed device pointers, valid until the
+ * trainer's next step on that buffer set.  Errors: GNNV_ERR_PARAM (null). */
+gnnv_status gnnv_trainer_rowidx(const gnnv_trainer* t, const int32_t** d_rowidx, const float** d_table);
 /* Device pointers of the trainer's activations for layer i (0 = X) of the
  * last step (same buffer-set caveat; X holds the rows of gnnv_trainer_x_level). */
 gnnv_status gnnv_trainer_activation(gnnv_trainer* t, int32_t i, const float** d_H, int32_t* stride);

@@ -14,7 +14,9 @@
 // With d_rowidx (trainer, whole table resident on this device) only the dst
 // prefix F_{L-1} of X is materialised -- the rows the layer-1 GEMMs read --
 // and rowidx[u] = cache row of every F_L row, through which the layer-1
-// aggregation reads the cache directly (spmm.cu, k_spmm_fwd<LPR, true>).
+// aggregation reads the cache directly (spmm.cu, k_spmm_fwd<LPR, true>);
+// with materialize = false not even that (the TF32 layer-1 GEMMs gather the
+// H_dst rows from the table with TMA gather4, gemm_tma.cu).
 #include <string.h>
 
 #include <cub/device/device_radix_sort.cuh>
@@ -72,7 +74,7 @@ __global__ void __launch_bounds__(256) k_gather(const int32_t* __restrict__ F, c
                                                 int32_t* __restrict__ rowidx) {
   GNNV_PDL_ENTRY();
   const int n = sizes[L];
-  const int n_mat = sizes[mat_level];  // rows materialised in X (all, or the dst prefix)
+  const int n_mat = mat_level < 0 ? 0 : sizes[mat_level];  // rows materialised in X (all, the dst prefix, none)
   const int vec = stride >> 2;
   const int lane = threadIdx.x & 31;
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -124,7 +126,7 @@ __global__ void __launch_bounds__(256) k_gather(const int32_t* __restrict__ F, c
 }
 
 void launch_gather(const gnnv_cache* c, const gnnv_blocks* b, float* d_X, int64_t* d_stats, cudaStream_t s,
-                   int32_t* d_rowidx) {
+                   int32_t* d_rowidx, bool materialize) {
   const gnnv_graph* g = c->g;
   constexpr int RU = 8;
   const int64_t rows_ub = b->max_n[b->L];
@@ -134,7 +136,7 @@ void launch_gather(const gnnv_cache* c, const gnnv_blocks* b, float* d_X, int64_
   launch_k(k_gather<RU>, std::max(blocks, 1), 256, 0, s, b->d_F, b->d_sizes, b->L, c->d_slot, c->d_shard_ptrs, c->world,
                                                    c->rank, g->d_feats, g->stride, d_X,
                                                    reinterpret_cast<unsigned long long*>(d_stats),
-                                                   d_rowidx ? b->L - 1 : b->L, d_rowidx);
+                                                   !materialize ? -1 : d_rowidx ? b->L - 1 : b->L, d_rowidx);
   GNNV_CHECK_LAUNCH();
 }
 

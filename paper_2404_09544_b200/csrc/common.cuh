@@ -222,7 +222,7 @@ void launch_sample(gnnv_graph* g, gnnv_blocks* b, const int32_t* d_seeds, int32_
 // cache.cu
 void launch_cache_update(gnnv_cache* c, const gnnv_blocks* b, const float* d_X, cudaStream_t s);
 void launch_gather(const gnnv_cache* c, const gnnv_blocks* b, float* d_X, int64_t* d_stats, cudaStream_t s,
-                   int32_t* d_rowidx = nullptr);
+                   int32_t* d_rowidx = nullptr, bool materialize = true);
 // Cap on the grid of the sampling / gather kernels (0 = none); the trainer
 // sets it around a prefetch so the overlapped batch occupies few SMs.
 void set_grid_cap(int blocks);
@@ -251,8 +251,20 @@ struct GemmFwdArgs {
   // bit n%32 = (Y[m][n] > 0), for a later fused dW (NULL: none)
   uint32_t* mask_bits = nullptr;
   int32_t mask_ld = 0;
+  // TF32 only: X1 row m is row x1_rows[m] of X1, a [x1_table_rows x ld1]
+  // table (layer 1 reading H_dst from the whole-table cache; NULL: row m)
+  const int32_t* x1_rows = nullptr;
+  int64_t x1_table_rows = 0;
 };
 void gemm_fwd(const GemmFwdArgs& a, int prec, cudaStream_t s);
+// Layer 1 of the trainer with the whole feature table on the device: H_dst
+// (X's dst prefix) is read by the TF32 GEMMs straight from the table through
+// the gather's row indices, so X is never materialised.
+struct XRows {
+  const float* table;
+  const int32_t* rows;
+  int64_t table_rows;
+};
 // words per row of a ReLU bit mask over N columns (16-byte rows for TMA)
 inline int32_t mask_words(int32_t N) { return ((N + 31) / 32 + 3) / 4 * 4; }
 void launch_relu_bits(const float* H, int32_t ldh, int32_t N, const int32_t* d_M, int64_t max_M, uint32_t* bits,
@@ -272,6 +284,8 @@ struct GemmDwArgs {  // dW = [X1|X2]^T G (+ bias row = colsum G) : deterministic
   const uint32_t* mask_bits = nullptr;
   int32_t mask_ld = 0;
   bool db_fused = false;  // TF32 only: db = colsum(G) computed by the dW kernel (G final)
+  const int32_t* x1_rows = nullptr;  // as GemmFwdArgs::x1_rows
+  int64_t x1_table_rows = 0;
 };
 void gemm_dw(const GemmDwArgs& a, int prec, cudaStream_t s);
 size_t gemm_dw_partial_floats(int32_t rows_plus_bias, int32_t N, int32_t* splits_out, int64_t max_M);

@@ -247,6 +247,7 @@ bool gemm_dw_tma(const GemmDwArgs& a, cudaStream_t s);
 // Precision dispatch.  A tensor-core path that does not handle a shape is an
 // error, never a silent fall back to another precision.
 void gemm_fwd(const GemmFwdArgs& a, int prec, cudaStream_t s) {
+  GNNV_REQUIRE(!a.x1_rows || prec == GNNV_PREC_TF32, GNNV_ERR_UNSUPPORTED, "fwd: indexed X1 rows need the tf32 path");
   if (prec == GNNV_PREC_FP32) return gemm_fwd_simt(a, s);
   const bool ok = prec == GNNV_PREC_TF32 ? gemm_fwd_tma(a, s) : gemm_fwd_tc(a, s);
   GNNV_REQUIRE(ok, GNNV_ERR_UNSUPPORTED, "tensor-core fwd GEMM: d_out > 252 is not supported");
@@ -258,6 +259,7 @@ void gemm_dx(const GemmDxArgs& a, int prec, cudaStream_t s) {
 }
 // For TF32 this computes dW only; db comes from k_mask_colsum (layers.cu).
 void gemm_dw(const GemmDwArgs& a, int prec, cudaStream_t s) {
+  GNNV_REQUIRE(!a.x1_rows || prec == GNNV_PREC_TF32, GNNV_ERR_UNSUPPORTED, "dW: indexed X1 rows need the tf32 path");
   if (prec == GNNV_PREC_FP32) return gemm_dw_simt(a, s);
   const bool ok = prec == GNNV_PREC_TF32 ? gemm_dw_tma(a, s) : gemm_dw_tc(a, s);
   GNNV_REQUIRE(ok, GNNV_ERR_UNSUPPORTED, "tensor-core dW GEMM: d_out > 256 is not supported");

@@ -74,6 +74,17 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, i
       "l"(map), "r"(c0), "r"(c1), "r"(smem_u32(bar))
       : "memory");
 }
+// TMA gather4 (sm_100a): rows r0..r3 of a 2-D tensor, columns [c0, c0 + box
+// width), into 4 consecutive box rows at dst (the tensor map's box is
+// {width, 1}); the swizzle follows the shared-memory address as for tiles.
+__device__ __forceinline__ void tma_gather4(void* dst, const CUtensorMap* map, int c0, int r0, int r1, int r2, int r3,
+                                            uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, "
+      "%4, %5, %6}], [%7];" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(c0), "r"(r0), "r"(r1), "r"(r2), "r"(r3), "r"(smem_u32(bar))
+      : "memory");
+}
 __device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void* src, int c0, int c1) {
   asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(map), "r"(c0),
                "r"(c1), "r"(smem_u32(src))
@@ -178,6 +189,11 @@ struct Params {
   // dW: also the column sums of G (db) without a mask (G already masked)
   int dbsum;
   int dbg;        // micro-benchmark switches (GNNV_DEBUG_GEMM): 1 = no epilogue stores, 2 = no MMA
+  // fwd / dW: X1 row m is row x1_rows[m] of the tensor behind ta1 (layer 1
+  // reading H_dst straight from the degree-ordered cache table): ta1 then
+  // has a {width, 1} box and X1 tiles arrive by TMA gather4, 4 rows per
+  // instruction, one instruction per producer lane (NULL: plain tiles)
+  const int32_t* x1_rows;
 };
 
 static int debug_flags() {
@@ -271,20 +287,39 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_tma_gemm(const __grid_constant_
   if (MODE != MODE_DW) {
     // ======================= persistent fwd / dX =======================
     if (warp == 0) {
-      if (lane == 0) {
+      const bool g4 = MODE == MODE_FWD && p.x1_rows != nullptr;
+      if (lane == 0 || g4) {
         int it = 0;
         for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
           const int mt = MODE == MODE_DX ? tile / p.n_ntiles : tile;
           const int nt = MODE == MODE_DX ? tile % p.n_ntiles : 0;
+          // gather4: lane l loads rows 4l..4l+3 of the tile; rows >= M read
+          // table row 0 (their outputs are never stored)
+          int r4[4] = {0, 0, 0, 0};
+          if (g4) {
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              const int m = mt * BM + 4 * lane + j;
+              r4[j] = m < M ? __ldg(p.x1_rows + m) : 0;
+            }
+          }
           for (int kb = 0; kb < p.nkb; ++kb, ++it) {
             const int s = it % S;
-            if (it >= S) mbar_wait(&empty[s], ((it / S) & 1) ^ 1);
             uint8_t* sa = smem + (size_t)s * stage_bytes;
             uint8_t* sb = sa + a_bytes;
-            mbar_arrive_tx(&full[s], (uint32_t)stage_bytes);
-            if (MODE == MODE_FWD && kb >= p.nkb1) tma_load_2d(sa, &p.ta2, (kb - p.nkb1) * BK, mt * BM, &full[s]);
-            else tma_load_2d(sa, &p.ta1, kb * BK, mt * BM, &full[s]);
-            tma_load_2d(sb, &p.tb, kb * BK, nt * BN, &full[s]);
+            if (lane == 0) {
+              if (it >= S) mbar_wait(&empty[s], ((it / S) & 1) ^ 1);
+              mbar_arrive_tx(&full[s], (uint32_t)stage_bytes);
+            }
+            if (g4) __syncwarp();
+            if (MODE == MODE_FWD && kb >= p.nkb1) {
+              if (lane == 0) tma_load_2d(sa, &p.ta2, (kb - p.nkb1) * BK, mt * BM, &full[s]);
+            } else if (g4) {
+              tma_gather4(sa + lane * 4 * BKB, &p.ta1, kb * BK, r4[0], r4[1], r4[2], r4[3], &full[s]);
+            } else {
+              tma_load_2d(sa, &p.ta1, kb * BK, mt * BM, &full[s]);
+            }
+            if (lane == 0) tma_load_2d(sb, &p.tb, kb * BK, nt * BN, &full[s]);
           }
         }
       }
@@ -413,25 +448,50 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_tma_gemm(const __grid_constant_
     const int ig = blockIdx.y;  // i-tile group
     const int ngroups = MT * 4 + BN / 32;  // 32-column transposer work units
     if (warp == 0) {
-      if (lane == 0) {
+      // gather4 (p.x1_rows): lanes 0..3 load graph rows 4l..4l+3 of each
+      // k-block's X1 tiles, their indices fetched one k-block ahead; rows
+      // >= M read table row 0 (the transposers zero them)
+      const bool g4 = p.x1_rows != nullptr;
+      auto rows4 = [&](int i, int (&r4)[4]) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int m = (kb0 + i) * DW_KR + 4 * lane + j;
+          r4[j] = (i < nkb && m < M) ? __ldg(p.x1_rows + m) : 0;
+        }
+      };
+      int rc[4] = {0, 0, 0, 0}, rn[4] = {0, 0, 0, 0};
+      if (g4 && lane < 4) rows4(0, rc);
+      if (lane == 0 || (g4 && lane < 4)) {
         for (int i = 0; i < nkb; ++i) {
           const int s = i % S;
-          if (i >= S) mbar_wait(&empty[s], ((i / S) & 1) ^ 1);
+          if (g4) rows4(i + 1, rn);
           uint8_t* sa = smem + (size_t)s * stage_bytes;
           const int row = (kb0 + i) * DW_KR;
-          uint32_t bytes = (uint32_t)b_bytes;
-          for (int mt = 0; mt < MT; ++mt)
-            if ((ig * MT + mt) * 4 < p.ablocks) bytes += DW_KR * BM * 4;
-          mbar_arrive_tx(&full[s], bytes);
+          if (lane == 0) {
+            if (i >= S) mbar_wait(&empty[s], ((i / S) & 1) ^ 1);
+            uint32_t bytes = (uint32_t)b_bytes;
+            for (int mt = 0; mt < MT; ++mt)
+              if ((ig * MT + mt) * 4 < p.ablocks) bytes += DW_KR * BM * 4;
+            mbar_arrive_tx(&full[s], bytes);
+          }
+          if (g4) __syncwarp(0xfu);
           for (int mt = 0; mt < MT; ++mt) {
             const int blk = (ig * MT + mt) * 4;  // first 32-wide i block of this 128-row tile
             if (blk >= p.ablocks) continue;
             uint8_t* dst = sa + mt * (DW_KR * BM * 4);
-            if (blk < p.nkb1) tma_load_2d(dst, &p.ta1, blk * 32, row, &full[s]);
-            else tma_load_2d(dst, &p.ta2, (blk - p.nkb1) * 32, row, &full[s]);
+            if (blk < p.nkb1) {
+              if (g4) tma_gather4(dst + lane * 4 * BM * 4, &p.ta1, blk * 32, rc[0], rc[1], rc[2], rc[3], &full[s]);
+              else tma_load_2d(dst, &p.ta1, blk * 32, row, &full[s]);
+            } else if (lane == 0) {
+              tma_load_2d(dst, &p.ta2, (blk - p.nkb1) * 32, row, &full[s]);
+            }
           }
-          tma_load_2d(sa + a_bytes, &p.tb, 0, row, &full[s]);
-          if (p.mask) tma_load_2d(sa + a_bytes + g_bytes, &p.th, 0, row, &full[s]);
+          if (lane == 0) {
+            tma_load_2d(sa + a_bytes, &p.tb, 0, row, &full[s]);
+            if (p.mask) tma_load_2d(sa + a_bytes + g_bytes, &p.th, 0, row, &full[s]);
+          }
+#pragma unroll
+          for (int j = 0; j < 4; ++j) rc[j] = rn[j];
         }
       }
     } else if (warp == 1) {
@@ -726,7 +786,8 @@ bool gemm_fwd_tma(const GemmFwdArgs& a, cudaStream_t s) {
   launch_k(k_bt_fwd, std::min(1024, (BN * Kp + 255) / 256), 256, 0, s, a.W, a.K1, nkb1, a.X2 ? 1 : 0, a.N, BN, Kp, Bt);
   GNNV_CHECK_LAUNCH();
   Params p{};
-  p.ta1 = make_map(a.X1, a.max_M, a.K1, a.ld1, BM);
+  p.x1_rows = a.x1_rows;
+  p.ta1 = a.x1_rows ? make_map(a.X1, a.x1_table_rows, a.K1, a.ld1, 1) : make_map(a.X1, a.max_M, a.K1, a.ld1, BM);
   p.ta2 = a.X2 ? make_map(a.X2, a.max_M, a.K1, a.ld2, BM) : p.ta1;
   p.tb = make_map(Bt, BN, Kp, Kp, BN);
   p.two = a.X2 ? 1 : 0;
@@ -817,7 +878,9 @@ bool gemm_dw_tma(const GemmDwArgs& a, cudaStream_t s) {
     GNNV_TRY_CUDA(cudaMemsetAsync(a.db, 0, (size_t)a.N * sizeof(float), s));
     p.db = a.db;
   }
-  p.ta1 = make_map(a.X1, a.max_M, a.K1, a.ld1, DW_KR, BM, false);
+  p.x1_rows = a.x1_rows;
+  p.ta1 = a.x1_rows ? make_map(a.X1, a.x1_table_rows, a.K1, a.ld1, 1, BM, false)
+                    : make_map(a.X1, a.max_M, a.K1, a.ld1, DW_KR, BM, false);
   p.ta2 = a.X2 ? make_map(a.X2, a.max_M, a.K1, a.ld2, DW_KR, BM, false) : p.ta1;
   p.tb = make_map(a.G, a.max_M, a.N, a.ldg, DW_KR, BN, false);
   p.two = a.X2 ? 1 : 0;

@@ -245,7 +245,7 @@ static void check_layer(const gnnv_blocks* b, int32_t layer, const gnnv_layer_de
 
 void layer_fwd_impl(gnnv_blocks* b, int32_t layer, const gnnv_layer_desc* ld, const float* Hsrc, const float* W,
                     const float* bias, float* Hdst, float* A, cudaStream_t s, Timeline* tl, uint32_t* mask_bits,
-                    const float* agg_table, const int32_t* rowidx) {
+                    const float* agg_table, const int32_t* rowidx, const XRows* xr) {
   const std::string sfx = ".l" + std::to_string(layer);
   if (tl) tl->mark(s, "spmm_fwd" + sfx);
   const int h = b->L - layer;
@@ -257,10 +257,11 @@ void layer_fwd_impl(gnnv_blocks* b, int32_t layer, const gnnv_layer_desc* ld, co
                   lda, ld->d_in, ld->kind, ld->aggr, s, rowidx);
   GemmFwdArgs g{};
   if (ld->kind == GNNV_KIND_SAGE) {
-    g.X1 = Hsrc;
+    g.X1 = xr ? xr->table : Hsrc;
     g.ld1 = ld->in_stride;
     g.X2 = A;
     g.ld2 = lda;
+    if (xr) g.x1_rows = xr->rows, g.x1_table_rows = xr->table_rows;
   } else {
     g.X1 = A;
     g.ld1 = lda;
@@ -287,7 +288,7 @@ void layer_fwd_impl(gnnv_blocks* b, int32_t layer, const gnnv_layer_desc* ld, co
 void layer_bwd_impl(gnnv_blocks* b, int32_t layer, const gnnv_layer_desc* ld, const float* Gdst, const float* Hdst,
                     const float* Hsrc, const float* A, const float* W, float* Gsrc, float* dW, float* db,
                     cudaStream_t s, Timeline* tl, const uint32_t* mask_bits, bool g_masked,
-                    const uint32_t* src_bits, int32_t src_bits_ld) {
+                    const uint32_t* src_bits, int32_t src_bits_ld, const XRows* xr) {
   const std::string sfx = ".l" + std::to_string(layer);
   const int h = b->L - layer;
   const int32_t* d_ndst = b->d_sizes + h;
@@ -340,10 +341,11 @@ void layer_bwd_impl(gnnv_blocks* b, int32_t layer, const gnnv_layer_desc* ld, co
   }
   GemmDwArgs w{};
   if (sage) {
-    w.X1 = Hsrc;
+    w.X1 = xr ? xr->table : Hsrc;
     w.ld1 = ld->in_stride;
     w.X2 = A;
     w.ld2 = lda;
+    if (xr) w.x1_rows = xr->rows, w.x1_table_rows = xr->table_rows;
   } else {
     w.X1 = A;
     w.ld1 = lda;
@@ -410,7 +412,8 @@ gnnv_status gnnv_layer_fwd(gnnv_blocks* b, int32_t layer, const gnnv_layer_desc*
   return guarded([&] {
     check_layer(b, layer, ld);
     GNNV_REQUIRE(d_Hsrc && d_W && d_b && d_Hdst && d_saveA, GNNV_ERR_PARAM, "layer_fwd: null buffer");
-    layer_fwd_impl(b, layer, ld, d_Hsrc, d_W, d_b, d_Hdst, d_saveA, (cudaStream_t)s, nullptr, nullptr, nullptr, nullptr);
+    layer_fwd_impl(b, layer, ld, d_Hsrc, d_W, d_b, d_Hdst, d_saveA, (cudaStream_t)s, nullptr, nullptr, nullptr, nullptr,
+                   nullptr);
   });
 }
 
@@ -422,7 +425,7 @@ gnnv_status gnnv_layer_bwd(gnnv_blocks* b, int32_t layer, const gnnv_layer_desc*
     GNNV_REQUIRE(d_Gdst && d_Hdst && d_Hsrc && d_saveA && d_W && d_dW && d_db, GNNV_ERR_PARAM,
                  "layer_bwd: null buffer");
     layer_bwd_impl(b, layer, ld, d_Gdst, d_Hdst, d_Hsrc, d_saveA, d_W, d_Gsrc, d_dW, d_db, (cudaStream_t)s, nullptr,
-                   nullptr, false, nullptr, 0);
+                   nullptr, false, nullptr, 0, nullptr);
   });
 }
 

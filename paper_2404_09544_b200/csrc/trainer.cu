@@ -13,11 +13,11 @@
 namespace gnnv {
 void layer_fwd_impl(gnnv_blocks* b, int32_t layer, const gnnv_layer_desc* ld, const float* Hsrc, const float* W,
                     const float* bias, float* Hdst, float* A, cudaStream_t s, Timeline* tl, uint32_t* mask_bits,
-                    const float* agg_table, const int32_t* rowidx);
+                    const float* agg_table, const int32_t* rowidx, const XRows* xr);
 void layer_bwd_impl(gnnv_blocks* b, int32_t layer, const gnnv_layer_desc* ld, const float* Gdst, const float* Hdst,
                     const float* Hsrc, const float* A, const float* W, float* Gsrc, float* dW, float* db,
                     cudaStream_t s, Timeline* tl, const uint32_t* mask_bits, bool g_masked,
-                    const uint32_t* src_bits, int32_t src_bits_ld);
+                    const uint32_t* src_bits, int32_t src_bits_ld, const XRows* xr);
 }  // namespace gnnv
 
 using namespace gnnv;
@@ -82,6 +82,13 @@ struct gnnv_trainer {
   // every F_L row's cache row in rowidx; layer 1 aggregates from the table.
   int32_t loc_w = 1;  // NEXT-2 locality weight for both buffer sets
   bool x_fused = false;
+  // x_fused with TF32 SAGE and GNNV_XROWS=1: the layer-1 GEMMs also read
+  // H_dst from the table (TMA gather4 through rowidx), so the gather copies
+  // no rows at all.  Off by default: measured on products, the gather4 loads
+  // (a 400-byte row fetched as four 128-byte pieces, one per k-block) cost
+  // the layer-1 GEMMs more (fwd 180 -> 257 us, dW 215 -> 230 us) than the
+  // dst-prefix copy they save (92 -> 25 us).
+  bool x_rows = false;
   const float* table = nullptr;
   int32_t* rowidx[2] = {nullptr, nullptr};
 };
@@ -242,7 +249,8 @@ gnnv_status gnnv_trainer_create(gnnv_graph* g, gnnv_cache* c, const gnnv_model_d
       t->x_fused = L > 1 && !c->dynamic && c->capacity == g->n && c->world == 1 && c->shards.size() == 1 &&
                    c->shards[0] && !getenv("GNNV_NO_XFUSE");
       t->table = t->x_fused ? c->shards[0] : nullptr;
-      const int64_t xrows = t->x_fused ? b->max_n[L - 1] : b->max_n[L];
+      t->x_rows = t->x_fused && md->prec == GNNV_PREC_TF32 && md->kind == GNNV_KIND_SAGE && getenv("GNNV_XROWS");
+      const int64_t xrows = t->x_rows ? 1 : t->x_fused ? b->max_n[L - 1] : b->max_n[L];
       t->H[0] = (float*)dmalloc((size_t)xrows * g->stride * sizeof(float), "X (gathered features)");
       if (t->x_fused) t->rowidx[0] = (int32_t*)dmalloc(b->max_n[L] * sizeof(int32_t), "cache rows of F_L");
       for (int i = 1; i <= L; ++i) {
@@ -287,7 +295,15 @@ int64_t gnnv_trainer_num_params(const gnnv_trainer* t) { return t ? t->nparams :
 gnnv_blocks* gnnv_trainer_blocks(gnnv_trainer* t) { return t ? t->b : nullptr; }
 
 int32_t gnnv_trainer_x_level(const gnnv_trainer* t) {
-  return t ? (t->x_fused ? t->md.L - 1 : t->md.L) : -1;
+  return t ? (t->x_rows ? -1 : t->x_fused ? t->md.L - 1 : t->md.L) : -1;
+}
+
+gnnv_status gnnv_trainer_rowidx(const gnnv_trainer* t, const int32_t** d_rowidx, const float** d_table) {
+  return guarded([&] {
+    GNNV_REQUIRE(t && d_rowidx && d_table, GNNV_ERR_PARAM, "trainer_rowidx: null");
+    *d_rowidx = t->x_fused ? t->rowidx[t->cur] : nullptr;
+    *d_table = t->x_fused ? t->table : nullptr;
+  });
 }
 
 gnnv_status gnnv_trainer_get(gnnv_trainer* t, float* host_params, float* host_grads) {
@@ -468,7 +484,7 @@ gnnv_status gnnv_trainer_prefetch(gnnv_trainer* t, const int32_t* seeds, int32_t
       if (st != GNNV_OK) throw Error{st, get_error()};
       st = gnnv_blocks_set_locality(t->bb[k], t->c, t->loc_w);
       if (st != GNNV_OK) throw Error{st, get_error()};
-      const int64_t xrows = t->bb[k]->max_n[t->x_fused ? t->md.L - 1 : t->md.L];
+      const int64_t xrows = t->x_rows ? 1 : t->bb[k]->max_n[t->x_fused ? t->md.L - 1 : t->md.L];
       t->X[k] = (float*)dmalloc((size_t)xrows * g->stride * sizeof(float), "X (prefetch)");
       if (t->x_fused)
         t->rowidx[k] = (int32_t*)dmalloc(t->bb[k]->max_n[t->md.L] * sizeof(int32_t), "cache rows of F_L (prefetch)");
@@ -510,7 +526,7 @@ gnnv_status gnnv_trainer_prefetch(gnnv_trainer* t, const int32_t* seeds, int32_t
     t->bb[k]->sampled = true;
     GNNV_TRY_CUDA(cudaMemsetAsync(t->d_statsb[k], 0, 4 * sizeof(int64_t), t->side));
     if (tl) tl->mark(t->side, "pf_gather");
-    launch_gather(t->c, t->bb[k], t->X[k], t->d_statsb[k], t->side, t->rowidx[k]);
+    launch_gather(t->c, t->bb[k], t->X[k], t->d_statsb[k], t->side, t->rowidx[k], !t->x_rows);
     if (t->c->dynamic) {  // NEXT-3 admission
       if (tl) tl->mark(t->side, "pf_replace");
       launch_cache_update(t->c, t->bb[k], t->X[k], t->side);
@@ -560,7 +576,7 @@ gnnv_status gnnv_step(gnnv_trainer* t, const int32_t* seeds, int32_t n_seeds, in
       GNNV_TRY_CUDA(cudaMemsetAsync(t->d_stats, 0, 4 * sizeof(int64_t), s));
       if (tm) GNNV_TRY_CUDA(cudaEventRecord(t->ev[1], s));
       if (tl) tl->mark(s, "gather");
-      launch_gather(t->c, t->b, t->H[0], t->d_stats, s, t->rowidx[t->cur]);
+      launch_gather(t->c, t->b, t->H[0], t->d_stats, s, t->rowidx[t->cur], !t->x_rows);
       if (t->c->dynamic) {  // NEXT-3 admission (Eq.5's t_replace)
         if (tl) tl->mark(s, "replace");
         launch_cache_update(t->c, t->b, t->H[0], s);
@@ -568,10 +584,13 @@ gnnv_status gnnv_step(gnnv_trainer* t, const int32_t* seeds, int32_t n_seeds, in
       if (tm) GNNV_TRY_CUDA(cudaEventRecord(t->ev[2], s));
     }
     gnnv_blocks* b = t->b;
+    const XRows xr{t->table, t->rowidx[t->cur], g->n};
+    const XRows* xr1 = t->x_rows ? &xr : nullptr;
     for (int i = 1; i <= L; ++i) {
       const gnnv_layer_desc ld = layer_desc(t, i);
       layer_fwd_impl(b, i, &ld, t->H[i - 1], t->d_params + t->w_off[i - 1], t->d_params + t->b_off[i - 1], t->H[i],
-                     t->A[i], s, tl, t->mbits[i], t->table, i == 1 ? t->rowidx[t->cur] : nullptr);
+                     t->A[i], s, tl, t->mbits[i], t->table, i == 1 ? t->rowidx[t->cur] : nullptr,
+                     i == 1 ? xr1 : nullptr);
     }
     if (tm) GNNV_TRY_CUDA(cudaEventRecord(t->ev[3], s));
     float* d_loss = t->d_grads + t->nparams;
@@ -583,7 +602,8 @@ gnnv_status gnnv_step(gnnv_trainer* t, const int32_t* seeds, int32_t n_seeds, in
       const gnnv_layer_desc ld = layer_desc(t, i);
       layer_bwd_impl(b, i, &ld, t->G[i], t->H[i], t->H[i - 1], t->A[i], t->d_params + t->w_off[i - 1],
                      i > 1 ? t->G[i - 1] : nullptr, t->d_grads + t->w_off[i - 1], t->d_grads + t->b_off[i - 1], s, tl,
-                     t->mbits[i], t->mbits[i] != nullptr, t->mbits[i - 1], mask_words(t->md.dims[i - 1]));
+                     t->mbits[i], t->mbits[i] != nullptr, t->mbits[i - 1], mask_words(t->md.dims[i - 1]),
+                     i == 1 ? xr1 : nullptr);
     }
     if (tm) GNNV_TRY_CUDA(cudaEventRecord(t->ev[5], s));
     if (tl) tl->mark(s, "allreduce");

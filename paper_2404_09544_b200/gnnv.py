@@ -15,7 +15,8 @@ from typing import List, Optional, Sequence
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libgnnv.so")
+# GNNV_LIB: an alternative build of the same library (A/B timing of two builds)
+LIB_PATH = os.environ.get("GNNV_LIB") or os.path.join(_HERE, "libgnnv.so")
 MAX_LAYERS = 8
 
 OK, ERR_PARAM, ERR_STATE, ERR_OOM, ERR_CUDA, ERR_COMM, ERR_UNSUPPORTED = range(7)
@@ -119,6 +120,7 @@ _SIGS = {
     "gnnv_trainer_set_params": (I32, [VP, VP]),
     "gnnv_trainer_blocks": (VP, [VP]),
     "gnnv_trainer_x_level": (I32, [VP]),
+    "gnnv_trainer_rowidx": (I32, [VP, C.POINTER(C.c_void_p), C.POINTER(C.c_void_p)]),
     "gnnv_trainer_loss_async": (I32, [VP, VP, VP]),
     "gnnv_trainer_loss_result": (I32, [VP, C.c_int64, VP]),
     "gnnv_trainer_set_locality": (I32, [VP, I32]),
@@ -519,8 +521,14 @@ class Trainer:
         _check(load().gnnv_trainer_set_locality(self.h, locality_weight(bias)))
 
     def x_level(self) -> int:
-        """Frontier level whose rows X holds: L (all of F_L) or L-1 (dst prefix)."""
+        """Frontier level whose rows X holds: L (all of F_L), L-1 (dst prefix) or -1 (none)."""
         return int(load().gnnv_trainer_x_level(self.h))
+
+    def rowidx(self):
+        """(device ptr of int32[n_L] cache rows of F_L, device ptr of the table) or (None, None)."""
+        r, t = C.c_void_p(), C.c_void_p()
+        _check(load().gnnv_trainer_rowidx(self.h, C.byref(r), C.byref(t)))
+        return r.value, t.value
 
     def activation(self, i: int):
         p = C.c_void_p()

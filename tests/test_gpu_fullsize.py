@@ -25,7 +25,7 @@ from oracle.sampler import Block, sample_blocks
 from paper_2404_09544_b200 import gnnv
 from synth import BASE_RNG_SEED, CONFIGS, epoch_seeds, init_weights, make_graph
 
-from gpu_util import assert_close_cond, blocks_to_host, lib, normwise, read_f32
+from gpu_util import assert_close_cond, blocks_to_host, lib, normwise, read_f32, read_i32
 
 pytestmark = pytest.mark.gpu
 
@@ -74,15 +74,29 @@ def check_blocks_and_gather(gd, tr, ref_frontiers, ref_blocks, ratio):
         np.testing.assert_array_equal(ptr, ob.indptr, err_msg=f"indptr hop {h}")
         np.testing.assert_array_equal(idx, ob.indices, err_msg=f"indices hop {h}")
     FL = ref_frontiers[-1]
-    # X holds F_L, or only the dst prefix F_{L-1} when the whole table is
-    # cached (the layer-1 aggregation then reads the cache table directly)
-    lvl = tr.x_level()
-    assert lvl == (len(ref_blocks) - 1 if ratio == 1.0 else len(ref_blocks))
-    Fx = ref_frontiers[lvl]
-    p0, s0 = tr.activation(0)
-    X = read_f32(p0, len(Fx), s0)
-    assert X.tobytes() == oracle.gather_rows(gd.feats, Fx).tobytes(), "gathered rows"
     slot, owner, _ = cache_slots(gd.indptr, ratio)
+    # X holds F_L; or only the dst prefix F_{L-1} when the whole table is
+    # cached (the layer-1 aggregation then reads the cache table directly);
+    # or nothing (-1) when the tf32 layer-1 GEMMs gather H_dst from the table
+    # too.  With the whole table, the rows layer 1 reads are table rows
+    # rowidx[u]: rowidx must be the oracle's slot of every F_L row and those
+    # table rows the feature rows, bit for bit.
+    lvl = tr.x_level()
+    L = len(ref_blocks)
+    assert lvl in ((L - 1, -1) if ratio == 1.0 else (L,))
+    if lvl >= 0:
+        Fx = ref_frontiers[lvl]
+        p0, s0 = tr.activation(0)
+        X = read_f32(p0, len(Fx), s0)
+        assert X.tobytes() == oracle.gather_rows(gd.feats, Fx).tobytes(), "gathered rows"
+    if ratio == 1.0:
+        pr, pt = tr.rowidx()
+        ridx = read_i32(pr, len(FL))
+        np.testing.assert_array_equal(ridx, slot[FL], err_msg="cache rows of F_L")
+        pick = np.random.default_rng(1).choice(len(FL), min(len(FL), 4096), replace=False)
+        for u in pick[:64]:  # the table rows themselves (cache build), a sample
+            row = read_f32(pt + int(ridx[u]) * gd.stride * 4, 1, gd.stride)
+            assert row.tobytes() == oracle.gather_rows(gd.feats, FL[u:u + 1]).tobytes(), ("table row", u)
     cnt = access_counts(slot, owner, FL)
     assert tr.stats().tolist() == [cnt["rows"], cnt["hits_local"], cnt["hits_peer"], cnt["misses_host"]]
     return hb
@@ -123,7 +137,7 @@ def test_products_full_step(products, prec):
         ob = blks[i] = _blk(hb, L - i)
         p_in, s_in = tr.activation(i - 1)
         p_out, s_out = tr.activation(i)
-        if i == 1 and tr.x_level() < L:  # layer 1 read the cache table: the exact feature rows
+        if i == 1 and tr.x_level() < L:  # layer 1 read the cache table (checked above): the exact feature rows
             Hin = oracle.gather_rows(gd.feats, hb[L - 1][4])[:, : dims[0]]
         else:
             Hin = read_f32(p_in, ob.n_src, s_in)[:, : dims[i - 1]]

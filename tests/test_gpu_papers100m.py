@@ -22,7 +22,7 @@ from oracle.sampler import sample_blocks
 from paper_2404_09544_b200 import gnnv
 from synth import BASE_RNG_SEED, CONFIGS, epoch_seeds, init_weights, make_graph
 
-from gpu_util import blocks_to_host, lib, read_f32
+from gpu_util import blocks_to_host, lib, read_f32, read_i32
 
 pytestmark = [
     pytest.mark.gpu,
@@ -56,11 +56,15 @@ def test_papers100m_batch_bit_exact():
         np.testing.assert_array_equal(ptr, ob.indptr)
         np.testing.assert_array_equal(idx, ob.indices)
     FL = F[-1]
-    Fx = F[tr.x_level()]  # whole table cached: X holds the dst prefix F_{L-1}
-    p0, s0 = tr.activation(0)
-    X = read_f32(p0, len(Fx), s0)
-    assert X.tobytes() == oracle.gather_rows(gd.feats, Fx).tobytes()
     slot, owner, _ = cache_slots(gd.indptr, cfg["ratio"])
+    lvl = tr.x_level()  # whole table cached: X holds the dst prefix F_{L-1}, or nothing (-1)
+    if lvl >= 0:
+        Fx = F[lvl]
+        p0, s0 = tr.activation(0)
+        X = read_f32(p0, len(Fx), s0)
+        assert X.tobytes() == oracle.gather_rows(gd.feats, Fx).tobytes()
+    pr, pt = tr.rowidx()  # the rows layer 1 reads: table rows rowidx[u] = slot of F_L[u]
+    np.testing.assert_array_equal(read_i32(pr, len(FL)), slot[FL])
     cnt = access_counts(slot, owner, FL)
     assert tr.stats().tolist() == [cnt["rows"], cnt["hits_local"], cnt["hits_peer"], cnt["misses_host"]]
     print(f"papers100m: frontiers {[len(f) for f in F]}, edges {[b.nnz for b in blocks]}, loss {loss:.5f}")

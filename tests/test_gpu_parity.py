@@ -13,7 +13,7 @@ from oracle.sampler import Block, sample_blocks
 from paper_2404_09544_b200 import gnnv
 from synth import CONFIGS, epoch_seeds, init_weights, make_graph, row_stride, tiny_graph
 
-from gpu_util import assert_close_cond, blocks_to_host, dev_f32, dev_i32, lib, normwise, read_f32
+from gpu_util import assert_close_cond, blocks_to_host, dev_f32, dev_i32, lib, normwise, read_f32, read_i32
 
 pytestmark = pytest.mark.gpu
 
@@ -630,3 +630,44 @@ def test_step_degenerate_graph(kind, prec):
     for (gW, gb), (rW, rb) in zip(grads, ref["grads"]):
         assert normwise(gW, rW) < (1e-4 if prec == 0 else 2e-2)
         assert normwise(gb, rb) < (1e-4 if prec == 0 else 2e-2)
+
+
+def test_step_whole_table_gather4(mini, monkeypatch):
+    """Whole table cached, tf32 SAGE: the layer-1 GEMMs (forward and dW) read
+    H_dst straight from the degree-ordered table with TMA gather4 through the
+    gather's row indices and X is never written (x_level -1).  The forward
+    reads exactly the values the materialised path reads, in the same order,
+    (GNNV_XROWS=1), so the loss equals bit for bit that of the same step with X materialised
+    (a cache one row short of the table: ratio (N-1)/N); the gradients match
+    it to the dW kernel's atomic summation order.  Both match the oracle."""
+    gd, g = mini
+    cfg = CONFIGS["mini"]
+    dims = [gd.d, cfg["hidden"], cfg["hidden"], gd.C]
+    w = init_weights(dims)
+    L = len(cfg["fanouts"])
+    seeds = epoch_seeds(gd.n, 0)[: cfg["batch"]]
+    out = {}
+    monkeypatch.setenv("GNNV_XROWS", "1")  # read when a trainer is created
+    for name, ratio in (("rows", 1.0), ("copy", (gd.n - 1) / gd.n)):
+        tr = gnnv.Trainer(g, gnnv.Cache(g, ratio), dims, cfg["fanouts"], cfg["batch"], w, prec=gnnv.PREC_TF32)
+        loss, _ = tr.step(seeds, len(seeds), len(seeds), 0x5EED, 0.05)
+        out[name] = (loss, tr.grads(), tr.x_level(), tr)
+    assert out["rows"][2] == -1 and out["copy"][2] == L
+    assert out["rows"][0] == out["copy"][0], (out["rows"][0], out["copy"][0])
+    assert normwise(out["rows"][1], out["copy"][1]) < 1e-6
+    ref = train_step(gd.indptr, gd.indices, gd.feats, gd.d, gd.labels, seeds, cfg["fanouts"], 0x5EED, w, 0.05)
+    assert abs(out["rows"][0] - ref["loss"]) <= 5e-3 * abs(ref["loss"])
+    tr = out["rows"][3]
+    pr, _ = tr.rowidx()
+    slot, _, _ = cache_slots(gd.indptr, 1.0)
+    FL = ref["frontiers"][-1]
+    np.testing.assert_array_equal(read_i32(pr, len(FL)), slot[FL])
+    # layer 1's output vs the oracle fed the exact feature rows
+    hb = blocks_to_host(tr.blocks)
+    ob = _oracle_block(hb, L - 1)
+    Hin = oracle.gather_rows(gd.feats, FL)[:, : dims[0]]
+    p_out, s_out = tr.activation(1)
+    Hout = read_f32(p_out, ob.n_dst, s_out)[:, : dims[1]]
+    Ho, _ = layer_fwd(ob, Hin, w[0][0], w[0][1], True)
+    Hm, _ = layer_fwd(ob, Hin, w[0][0], w[0][1], True, absval=True)
+    assert_close_cond(Hout, Ho, Hm, RTOL[2], "layer 1 (gather4 H_dst)")
