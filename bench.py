@@ -347,7 +347,7 @@ def main():
     tr.set_locality(args.locality_bias)
     # the step runs on a high-priority stream; the trainer's prefetch stream
     # has the lowest priority (Eq.4 overlap without delaying the step)
-    stream = torch.cuda.Stream(priority=-1)
+    stream = torch.cuda.Stream(priority=int(os.environ.get("GNNV_STEP_PRIO", "-1")))
     torch.cuda.set_stream(stream)
     lr = 0.01
     # seeds of global iteration t: perm[t*G*B:(t+1)*G*B], rank r takes the r-th B-slice

@@ -74,6 +74,10 @@ struct gnnv_trainer {
   cudaStream_t side = nullptr;
   void* green = nullptr;  // CUgreenCtx of the side stream (GNNV_PF_SMS), or null
   cudaEvent_t ev_ready[2] = {nullptr, nullptr}, ev_free[2] = {nullptr, nullptr}, ev_in = nullptr;
+  // GNNV_PF_GATHER_AFTER=i: the step records ev_mid after layer i's forward
+  // and a prefetch enqueued after that step starts its gather only then
+  cudaEvent_t ev_mid = nullptr;
+  bool mid_pending = false;
   cudaEvent_t ev_h2d[2] = {nullptr, nullptr};  // last copy out of h_seedsb[k]
   bool h2d_used[2] = {false, false};
   Timeline tl_side;
@@ -147,8 +151,13 @@ static cudaStream_t make_side_stream(int device, void** green_ctx) {
     *green_ctx = (void*)gc;
     return (cudaStream_t)st;
   }
+  // GNNV_PF_PRIO=high: the prefetch stream takes the highest priority
+  // instead of the lowest (its latency-bound sampler then runs early in the
+  // step instead of filling gaps until the end)
+  const char* pe = getenv("GNNV_PF_PRIO");
+  const int prio = (pe && pe[0] == 'h') ? hi : lo;
   cudaStream_t st;
-  GNNV_TRY_CUDA(cudaStreamCreateWithPriority(&st, cudaStreamNonBlocking, lo));
+  GNNV_TRY_CUDA(cudaStreamCreateWithPriority(&st, cudaStreamNonBlocking, prio));
   return st;
 }
 
@@ -170,6 +179,7 @@ gnnv_status gnnv_trainer_free(gnnv_trainer* t) {
     if (t->ev_h2d[k]) cudaEventDestroy(t->ev_h2d[k]);
   }
   if (t->ev_in) cudaEventDestroy(t->ev_in);
+  if (t->ev_mid) cudaEventDestroy(t->ev_mid);
   if (t->side) cudaStreamDestroy(t->side);
   if (t->green) {
     try {
@@ -282,6 +292,7 @@ gnnv_status gnnv_trainer_create(gnnv_graph* g, gnnv_cache* c, const gnnv_model_d
         GNNV_TRY_CUDA(cudaEventCreateWithFlags(&t->ev_h2d[k], cudaEventDisableTiming));
       }
       GNNV_TRY_CUDA(cudaEventCreateWithFlags(&t->ev_in, cudaEventDisableTiming));
+      GNNV_TRY_CUDA(cudaEventCreateWithFlags(&t->ev_mid, cudaEventDisableTiming));
       GNNV_TRY_CUDA(cudaDeviceSynchronize());
     } catch (...) {
       gnnv_trainer_free(t);
@@ -525,6 +536,10 @@ gnnv_status gnnv_trainer_prefetch(gnnv_trainer* t, const int32_t* seeds, int32_t
     launch_sample(g, t->bb[k], d_seeds, n_seeds, rng_seed, t->side);
     t->bb[k]->sampled = true;
     GNNV_TRY_CUDA(cudaMemsetAsync(t->d_statsb[k], 0, 4 * sizeof(int64_t), t->side));
+    if (t->mid_pending) {
+      GNNV_TRY_CUDA(cudaStreamWaitEvent(t->side, t->ev_mid, 0));
+      t->mid_pending = false;
+    }
     if (tl) tl->mark(t->side, "pf_gather");
     launch_gather(t->c, t->bb[k], t->X[k], t->d_statsb[k], t->side, t->rowidx[k], !t->x_rows);
     if (t->c->dynamic) {  // NEXT-3 admission
@@ -591,6 +606,14 @@ gnnv_status gnnv_step(gnnv_trainer* t, const int32_t* seeds, int32_t n_seeds, in
       layer_fwd_impl(b, i, &ld, t->H[i - 1], t->d_params + t->w_off[i - 1], t->d_params + t->b_off[i - 1], t->H[i],
                      t->A[i], s, tl, t->mbits[i], t->table, i == 1 ? t->rowidx[t->cur] : nullptr,
                      i == 1 ? xr1 : nullptr);
+      static const int gate = [] {
+        const char* e = getenv("GNNV_PF_GATHER_AFTER");
+        return e ? atoi(e) : 0;
+      }();
+      if (i == gate) {
+        GNNV_TRY_CUDA(cudaEventRecord(t->ev_mid, s));
+        t->mid_pending = true;
+      }
     }
     if (tm) GNNV_TRY_CUDA(cudaEventRecord(t->ev[3], s));
     float* d_loss = t->d_grads + t->nparams;
