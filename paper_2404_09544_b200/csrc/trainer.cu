@@ -74,8 +74,11 @@ struct gnnv_trainer {
   cudaStream_t side = nullptr;
   void* green = nullptr;  // CUgreenCtx of the side stream (GNNV_PF_SMS), or null
   cudaEvent_t ev_ready[2] = {nullptr, nullptr}, ev_free[2] = {nullptr, nullptr}, ev_in = nullptr;
-  // GNNV_PF_GATHER_AFTER=i: the step records ev_mid after layer i's forward
-  // and a prefetch enqueued after that step starts its gather only then
+  // Prefetch gating (experiments on the Eq.4 overlap): GNNV_PF_GATE=fI or bI
+  // makes the step record ev_mid after layer I's forward (f) or backward (b);
+  // a prefetch enqueued after that step starts its sampling
+  // (GNNV_PF_GATE_SAMPLE=1) or its gather only then.  GNNV_PF_GATHER_AFTER=I
+  // is fI for the gather.
   cudaEvent_t ev_mid = nullptr;
   bool mid_pending = false;
   cudaEvent_t ev_h2d[2] = {nullptr, nullptr};  // last copy out of h_seedsb[k]
@@ -121,6 +124,25 @@ static F drv(const char* name) {
   GNNV_TRY_CUDA(cudaGetDriverEntryPoint(name, &p, cudaEnableDefault, &q));
   GNNV_REQUIRE(p && q == cudaDriverEntryPointSuccess, GNNV_ERR_CUDA, std::string("driver entry point ") + name);
   return reinterpret_cast<F>(p);
+}
+
+struct PfGate {
+  char phase = 0;  // 'f', 'b' or 0 (none)
+  int layer = 0;
+  bool sample = false;
+};
+static const PfGate& pf_gate() {
+  static const PfGate g = [] {
+    PfGate r;
+    if (const char* e = getenv("GNNV_PF_GATE")) {
+      if ((e[0] == 'f' || e[0] == 'b') && e[1]) r.phase = e[0], r.layer = atoi(e + 1);
+    } else if (const char* a = getenv("GNNV_PF_GATHER_AFTER")) {
+      r.phase = 'f', r.layer = atoi(a);
+    }
+    r.sample = getenv("GNNV_PF_GATE_SAMPLE") != nullptr;
+    return r;
+  }();
+  return g;
 }
 
 static cudaStream_t make_side_stream(int device, void** green_ctx) {
@@ -517,6 +539,10 @@ gnnv_status gnnv_trainer_prefetch(gnnv_trainer* t, const int32_t* seeds, int32_t
     GNNV_TRY_CUDA(cudaStreamWaitEvent(t->side, t->ev_free[k], 0));
     Timeline* tl = t->tl.on ? &t->tl_side : nullptr;
     const int32_t* d_seeds = stage_seeds(t, k, seeds, n_seeds, seeds_on_host, t->side, tl);
+    if (t->mid_pending && pf_gate().sample) {
+      GNNV_TRY_CUDA(cudaStreamWaitEvent(t->side, t->ev_mid, 0));
+      t->mid_pending = false;
+    }
     if (tl) tl->mark(t->side, "pf_sample");
     static const int pf_cap = [] {
       const char* e = getenv("GNNV_PF_BLOCKS");
@@ -536,7 +562,7 @@ gnnv_status gnnv_trainer_prefetch(gnnv_trainer* t, const int32_t* seeds, int32_t
     launch_sample(g, t->bb[k], d_seeds, n_seeds, rng_seed, t->side);
     t->bb[k]->sampled = true;
     GNNV_TRY_CUDA(cudaMemsetAsync(t->d_statsb[k], 0, 4 * sizeof(int64_t), t->side));
-    if (t->mid_pending) {
+    if (t->mid_pending && !pf_gate().sample) {
       GNNV_TRY_CUDA(cudaStreamWaitEvent(t->side, t->ev_mid, 0));
       t->mid_pending = false;
     }
@@ -606,11 +632,7 @@ gnnv_status gnnv_step(gnnv_trainer* t, const int32_t* seeds, int32_t n_seeds, in
       layer_fwd_impl(b, i, &ld, t->H[i - 1], t->d_params + t->w_off[i - 1], t->d_params + t->b_off[i - 1], t->H[i],
                      t->A[i], s, tl, t->mbits[i], t->table, i == 1 ? t->rowidx[t->cur] : nullptr,
                      i == 1 ? xr1 : nullptr);
-      static const int gate = [] {
-        const char* e = getenv("GNNV_PF_GATHER_AFTER");
-        return e ? atoi(e) : 0;
-      }();
-      if (i == gate) {
+      if (pf_gate().phase == 'f' && i == pf_gate().layer) {
         GNNV_TRY_CUDA(cudaEventRecord(t->ev_mid, s));
         t->mid_pending = true;
       }
@@ -627,6 +649,10 @@ gnnv_status gnnv_step(gnnv_trainer* t, const int32_t* seeds, int32_t n_seeds, in
                      i > 1 ? t->G[i - 1] : nullptr, t->d_grads + t->w_off[i - 1], t->d_grads + t->b_off[i - 1], s, tl,
                      t->mbits[i], t->mbits[i] != nullptr, t->mbits[i - 1], mask_words(t->md.dims[i - 1]),
                      i == 1 ? xr1 : nullptr);
+      if (pf_gate().phase == 'b' && i == pf_gate().layer) {
+        GNNV_TRY_CUDA(cudaEventRecord(t->ev_mid, s));
+        t->mid_pending = true;
+      }
     }
     if (tm) GNNV_TRY_CUDA(cudaEventRecord(t->ev[5], s));
     if (tl) tl->mark(s, "allreduce");
