@@ -281,6 +281,20 @@ def algorithmic(seg: str, sizes, cfg, dims, stride, prec, peaks):
         ld = (d_in + 3) & ~3
         by = n[h] * d_in * 4 + nnz[h] * 4 + (n[h] + 1) * 8 + n[h + 1] * ld * 4 + n[h] * ld * 4
         return "hbm", by, "GB/s", peaks["hbm"]
+    if name in ("tail_a", "tail_b"):
+        # fused output layer (tail.cu).  a: self + sampled neighbour rows of
+        # H^{L-1} read, aggregates, logits and dlogits written, the dH rows
+        # of the seeds and of every owner edge written, dA saved.  b: dA and
+        # the non-owner edges' dH rows read-modify-written, [H | A] and dz
+        # read for dW.
+        ld = (d_in + 3) & ~3
+        if name == "tail_a":
+            by = (U[h] + n[h]) * d_in * 4 + n[h] * ld * 4 + 2 * n[h] * ((d_out + 3) & ~3) * 4 \
+                + n[h + 1] * ld * 4 + n[h] * d_in * 4 + nnz[h] * 4
+        else:
+            rep = max(0, nnz[h] - (n[h + 1] - n[h]))
+            by = n[h] * d_in * 4 + rep * ld * 8 + n[h] * (2 * d_in + d_out) * 4
+        return "hbm", by, "GB/s", peaks["hbm"]
     if name == "relu_mask":
         return "hbm", 3 * n[h] * ((d_out + 3) & ~3) * 4, "GB/s", peaks["hbm"]
     ld_in, ld_out = (d_in + 3) & ~3, (d_out + 3) & ~3

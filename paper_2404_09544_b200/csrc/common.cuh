@@ -302,6 +302,29 @@ struct GemmDxArgs {  // [Y1 | Y2] = G W^T  (Y1 = first K1 cols, Y2 = the rest)
   int32_t y1_bits_ld = 0;
 };
 void gemm_dx(const GemmDxArgs& a, int prec, cudaStream_t s);
+// tail.cu: the trainer's output layer (forward, loss, backward) fused
+struct TailArgs {
+  const int32_t *indptr, *indices;  // hop-0 block (dst = seeds)
+  const uint32_t* own;              // owner-edge masks of the hop-0 rows
+  const int32_t* d_ndst;            // n_0 on the device
+  int64_t max_dst;
+  const float* H; int32_t ldh;      // H^{L-1} [n_1 x ldh]
+  const uint32_t* hbits; int32_t hbits_ld;  // its ReLU bits
+  const float *W, *bias;            // [W_s; W_n] (2d x C), b (C)
+  int32_t d, C, aggr;
+  float* A; int32_t lda;            // aggregates out [n_0 x lda]
+  float *Z, *dZ; int32_t ldz;       // logits and dlogits [n_0 x ldz]
+  const int32_t *F, *labels;
+  int32_t n_global;
+  float* dH; int32_t ldg;           // dL/dH^{L-1} [n_1 x ldg] (ReLU derivative applied)
+  float* dA;                        // scratch [n_0 x d]
+  float* loss_partial;              // >= ceil(max_dst / 32) floats
+  float* part;                      // tail_partial_floats(max_dst, d, C): per-CTA dW/db partials
+  float *dW, *db, *d_loss;
+};
+bool tail_supported(int kind, int d, int C, int fanout0);
+size_t tail_partial_floats(int64_t max_dst, int d, int C);
+void launch_tail(const TailArgs& a, cudaStream_t s, Timeline* tl, const std::string& sfx);
 // layers.cu
 void launch_relu_mask(const float* G, const float* H, float* Gp, int32_t ld, int32_t N, const int32_t* d_M,
                       int64_t max_M, cudaStream_t s);

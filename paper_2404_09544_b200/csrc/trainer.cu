@@ -54,6 +54,11 @@ struct gnnv_trainer {
   // epilogue; the backward masks dH where it is produced)
   uint32_t* mbits[GNNV_MAX_LAYERS + 1] = {nullptr};
   float* loss_partial = nullptr;
+  // fused output layer (tail.cu): TF32 SAGE with L >= 2 and the shapes
+  // tail_supported() accepts; GNNV_NO_TAIL=1 keeps the per-kernel path
+  bool tail = false;
+  float* tail_dA = nullptr;    // [max_n[0] x dims[L-1]]
+  float* tail_part = nullptr;  // per-CTA dW/db partials
   unsigned int* loss_counter = nullptr;
   int64_t* d_stats = nullptr;
   cudaEvent_t ev[8] = {nullptr};
@@ -224,6 +229,8 @@ gnnv_status gnnv_trainer_free(gnnv_trainer* t) {
   }
   for (auto* m : t->mbits) dfree(m);
   dfree(t->loss_partial);
+  dfree(t->tail_dA);
+  dfree(t->tail_part);
   dfree(t->loss_counter);
   for (auto& e : t->ev)
     if (e) cudaEventDestroy(e);
@@ -296,7 +303,15 @@ gnnv_status gnnv_trainer_create(gnnv_graph* g, gnnv_cache* c, const gnnv_model_d
         for (int i = 1; i < L; ++i)
           t->mbits[i] = (uint32_t*)dmalloc((size_t)b->max_n[L - i] * mask_words(md->dims[i]) * sizeof(uint32_t),
                                            "ReLU bits");
-      t->loss_partial = (float*)dmalloc(256 * sizeof(float), "loss partials");
+      t->loss_partial =
+          (float*)dmalloc(std::max<int64_t>(256, ceil_div(b->max_n[0], 32)) * sizeof(float), "loss partials");
+      t->tail = md->prec == GNNV_PREC_TF32 && L >= 2 &&
+                tail_supported(md->kind, md->dims[L - 1], md->dims[L], md->fanouts[0]) && !getenv("GNNV_NO_TAIL");
+      if (t->tail) {
+        t->tail_dA = (float*)dmalloc((size_t)b->max_n[0] * md->dims[L - 1] * sizeof(float), "output-layer dA");
+        t->tail_part = (float*)dmalloc(tail_partial_floats(b->max_n[0], md->dims[L - 1], md->dims[L]) * sizeof(float),
+                                       "output-layer dW partials");
+      }
       t->loss_counter = (unsigned int*)dmalloc(sizeof(unsigned int), "loss counter");
       GNNV_TRY_CUDA(cudaMemset(t->loss_counter, 0, sizeof(unsigned int)));
       t->d_stats = (int64_t*)dmalloc(4 * sizeof(int64_t), "gather stats");
@@ -628,6 +643,7 @@ gnnv_status gnnv_step(gnnv_trainer* t, const int32_t* seeds, int32_t n_seeds, in
     const XRows xr{t->table, t->rowidx[t->cur], g->n};
     const XRows* xr1 = t->x_rows ? &xr : nullptr;
     for (int i = 1; i <= L; ++i) {
+      if (t->tail && i == L) break;  // the fused output layer below
       const gnnv_layer_desc ld = layer_desc(t, i);
       layer_fwd_impl(b, i, &ld, t->H[i - 1], t->d_params + t->w_off[i - 1], t->d_params + t->b_off[i - 1], t->H[i],
                      t->A[i], s, tl, t->mbits[i], t->table, i == 1 ? t->rowidx[t->cur] : nullptr,
@@ -639,11 +655,49 @@ gnnv_status gnnv_step(gnnv_trainer* t, const int32_t* seeds, int32_t n_seeds, in
     }
     if (tm) GNNV_TRY_CUDA(cudaEventRecord(t->ev[3], s));
     float* d_loss = t->d_grads + t->nparams;
-    if (tl) tl->mark(s, "loss");
-    launch_ce_loss(t->H[L], t->Hs[L], t->md.dims[L], b->d_sizes, b->d_F, g->d_labels, n_global, d_loss, t->G[L],
-                   t->loss_partial, t->loss_counter, b->max_n[0], s);
+    if (t->tail) {
+      // output layer forward + loss + backward (tail.cu); the per-phase
+      // timing puts all of it in "loss"
+      TailArgs a{};
+      a.indptr = b->d_indptr[0];
+      a.indices = b->d_indices[0];
+      a.own = b->d_own[0];
+      a.d_ndst = b->d_sizes;
+      a.max_dst = b->max_n[0];
+      a.H = t->H[L - 1];
+      a.ldh = t->Hs[L - 1];
+      a.hbits = t->mbits[L - 1];
+      a.hbits_ld = mask_words(t->md.dims[L - 1]);
+      a.W = t->d_params + t->w_off[L - 1];
+      a.bias = t->d_params + t->b_off[L - 1];
+      a.d = t->md.dims[L - 1];
+      a.C = t->md.dims[L];
+      a.aggr = t->md.aggr;
+      a.A = t->A[L];
+      a.lda = row_stride(t->md.dims[L - 1]);
+      a.Z = t->H[L];
+      a.dZ = t->G[L];
+      a.ldz = t->Hs[L];
+      a.F = b->d_F;
+      a.labels = g->d_labels;
+      a.n_global = n_global;
+      a.dH = t->G[L - 1];
+      a.ldg = t->Hs[L - 1];
+      a.dA = t->tail_dA;
+      a.loss_partial = t->loss_partial;
+      a.part = t->tail_part;
+      a.dW = t->d_grads + t->w_off[L - 1];
+      a.db = t->d_grads + t->b_off[L - 1];
+      a.d_loss = d_loss;
+      launch_tail(a, s, tl, ".l" + std::to_string(L));
+    } else {
+      if (tl) tl->mark(s, "loss");
+      launch_ce_loss(t->H[L], t->Hs[L], t->md.dims[L], b->d_sizes, b->d_F, g->d_labels, n_global, d_loss, t->G[L],
+                     t->loss_partial, t->loss_counter, b->max_n[0], s);
+    }
     if (tm) GNNV_TRY_CUDA(cudaEventRecord(t->ev[4], s));
     for (int i = L; i >= 1; --i) {
+      if (t->tail && i == L) continue;
       const gnnv_layer_desc ld = layer_desc(t, i);
       layer_bwd_impl(b, i, &ld, t->G[i], t->H[i], t->H[i - 1], t->A[i], t->d_params + t->w_off[i - 1],
                      i > 1 ? t->G[i - 1] : nullptr, t->d_grads + t->w_off[i - 1], t->d_grads + t->b_off[i - 1], s, tl,

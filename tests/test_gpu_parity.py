@@ -671,3 +671,41 @@ def test_step_whole_table_gather4(mini, monkeypatch):
     Ho, _ = layer_fwd(ob, Hin, w[0][0], w[0][1], True)
     Hm, _ = layer_fwd(ob, Hin, w[0][0], w[0][1], True, absval=True)
     assert_close_cond(Hout, Ho, Hm, RTOL[2], "layer 1 (gather4 H_dst)")
+
+
+def test_fused_output_layer_matches_per_kernel_path(mini, monkeypatch):
+    """The tf32 trainer runs its output layer (layer-L forward, CE loss,
+    layer-L backward) as the two fused kernels of tail.cu; GNNV_NO_TAIL=1
+    (read when a trainer is created) keeps the seven per-kernel launches.
+    Same step, same inputs: the loss, the logits, dH of layer L-1 and every
+    gradient agree to the tf32 GEMM rounding, and both match the oracle."""
+    gd, g = mini
+    cfg = CONFIGS["mini"]
+    dims = [gd.d, cfg["hidden"], cfg["hidden"], gd.C]
+    L = len(cfg["fanouts"])
+    w = init_weights(dims)
+    seeds = epoch_seeds(gd.n, 0)[: cfg["batch"]]
+    out = {}
+    for name in ("fused", "split"):
+        if name == "split":
+            monkeypatch.setenv("GNNV_NO_TAIL", "1")
+        tr = gnnv.Trainer(g, gnnv.Cache(g, cfg["ratio"]), dims, cfg["fanouts"], cfg["batch"], w, prec=gnnv.PREC_TF32)
+        tr.timeline(True)
+        loss, _ = tr.step(seeds, len(seeds), len(seeds), 0x5EED, 0.05)
+        segs = tr.timeline_read()
+        hb = blocks_to_host(tr.blocks)
+        pz, sz = tr.activation(L)
+        pg, sg = tr.activation(L - 1)
+        out[name] = dict(loss=loss, segs=segs, grads=tr.grads(), Z=read_f32(pz, hb[0][0], sz)[:, : gd.C])
+    assert f"tail_a.l{L}" in out["fused"]["segs"] and "loss" not in out["fused"]["segs"]
+    assert "loss" in out["split"]["segs"] and f"tail_a.l{L}" not in out["split"]["segs"]
+    f, s = out["fused"], out["split"]
+    assert abs(f["loss"] - s["loss"]) <= 2e-3 * abs(s["loss"])
+    assert normwise(f["Z"], s["Z"]) < 4e-3
+    assert normwise(f["grads"], s["grads"]) < 1e-2
+    ref = train_step(gd.indptr, gd.indices, gd.feats, gd.d, gd.labels, seeds, cfg["fanouts"], 0x5EED, w, 0.05)
+    assert abs(f["loss"] - ref["loss"]) <= 5e-3 * abs(ref["loss"])
+    for (gW, gb), (rW, rb) in zip(gnnv.unflat_params(f["grads"], dims), ref["grads"]):
+        for a_, b_ in ((gW, rW), (gb, rb)):
+            cos = float(np.dot(a_.ravel(), b_.ravel()) / (np.linalg.norm(a_) * np.linalg.norm(b_) + 1e-30))
+            assert cos > 0.98, cos
