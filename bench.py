@@ -539,6 +539,16 @@ def main():
         rooflines[name] = r
         if roofline is None and not name.startswith("pf_"):
             roofline = r
+    # north_star's "per-iteration gather+SpMM" against HBM: algorithmic bytes
+    # of the gather and every aggregation segment over their summed times
+    gs = [k for k in rooflines if k.split(".")[0] in ("gather", "pf_gather", "spmm_fwd", "spmm_bwd")]
+    gather_spmm = None
+    if gs:
+        by = sum(rooflines[k]["algorithmic_per_launch"] for k in gs)
+        ms = sum(rooflines[k]["avg_ms"] for k in gs)
+        gather_spmm = {"segments": gs, "bytes": by, "ms": ms, "achieved": by / ms / 1e6, "peak": peaks["hbm"],
+                       "unit": "GB/s", "frac": by / ms / 1e6 / peaks["hbm"],
+                       "note": "pf_gather, when present, is timed while overlapped with the step"}
     # -------------------------------------------------------- CPU baseline
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -568,6 +578,7 @@ def main():
             "gpu_launches": int(launches),
             "roofline": roofline,
             "rooflines": rooflines,
+            "gather_spmm": gather_spmm,
             "phases_ms_per_step": {k: v[0] / args.steps for k, v in sorted(segs.items(), key=lambda kv: -kv[1][0])},
             "sizes_per_step": {"frontier": [round(x) for x in sizes["n"]], "edges": [round(x) for x in sizes["nnz"]],
                                "distinct_src": [round(x) for x in sizes["U"]], "cache_hits": sizes["hits"],

@@ -9,7 +9,8 @@ usage:
 The step's launches are assigned to the bench timeline's segments by the
 trainer's fixed launch order (gnnv_step): sampler kernels -> "sample",
 k_gather -> "gather", per layer k_spmm_fwd -> "spmm_fwd.l<i>", the forward
-GEMM (+ its weight image) -> "gemm_fwd.l<i>", k_ce_loss -> "loss", per layer
+GEMM (+ its weight image) -> "gemm_fwd.l<i>", k_ce_loss -> "loss" (or the
+fused output layer k_tail_a / k_tail_b -> "tail_a.l<L>" / "tail_b.l<L>"), per layer
 from L down: mask pass -> "relu_mask.l<i>", dW GEMM + reductions ->
 "gemm_dw.l<i>", dX GEMM (+ image) -> "gemm_dx.l<i>", the two aggregation
 push passes -> "spmm_bwd.l<i>", k_sgd -> "sgd".  Traffic = dram__bytes_read
@@ -85,6 +86,11 @@ def main() -> None:
             cur = f"gemm_fwd.l{f}"
         elif n.startswith("k_ce_loss"):
             cur = "loss"
+        elif n.startswith("k_tail_a"):  # fused output layer (tail.cu): layer L fwd + loss + bwd
+            cur = f"tail_a.l{f + 1}"
+        elif n.startswith("k_tail_b"):
+            cur = f"tail_b.l{L}"
+            b = L
         elif n.startswith(("k_mask_colsum", "k_relu_mask", "k_relu_bits")):
             b -= 1
             pending_dw = True
