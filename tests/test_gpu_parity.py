@@ -673,7 +673,8 @@ def test_step_whole_table_gather4(mini, monkeypatch):
     assert_close_cond(Hout, Ho, Hm, RTOL[2], "layer 1 (gather4 H_dst)")
 
 
-def test_fused_output_layer_matches_per_kernel_path(mini, monkeypatch):
+@pytest.mark.parametrize("aggr", [gnnv.AGGR_MEAN, gnnv.AGGR_SUM])
+def test_fused_output_layer_matches_per_kernel_path(mini, monkeypatch, aggr):
     """The tf32 trainer runs its output layer (layer-L forward, CE loss,
     layer-L backward) as the two fused kernels of tail.cu; GNNV_NO_TAIL=1
     (read when a trainer is created) keeps the seven per-kernel launches.
@@ -689,7 +690,8 @@ def test_fused_output_layer_matches_per_kernel_path(mini, monkeypatch):
     for name in ("fused", "split"):
         if name == "split":
             monkeypatch.setenv("GNNV_NO_TAIL", "1")
-        tr = gnnv.Trainer(g, gnnv.Cache(g, cfg["ratio"]), dims, cfg["fanouts"], cfg["batch"], w, prec=gnnv.PREC_TF32)
+        tr = gnnv.Trainer(g, gnnv.Cache(g, cfg["ratio"]), dims, cfg["fanouts"], cfg["batch"], w, aggr=aggr,
+                          prec=gnnv.PREC_TF32)
         tr.timeline(True)
         loss, _ = tr.step(seeds, len(seeds), len(seeds), 0x5EED, 0.05)
         segs = tr.timeline_read()
@@ -703,7 +705,8 @@ def test_fused_output_layer_matches_per_kernel_path(mini, monkeypatch):
     assert abs(f["loss"] - s["loss"]) <= 2e-3 * abs(s["loss"])
     assert normwise(f["Z"], s["Z"]) < 4e-3
     assert normwise(f["grads"], s["grads"]) < 1e-2
-    ref = train_step(gd.indptr, gd.indices, gd.feats, gd.d, gd.labels, seeds, cfg["fanouts"], 0x5EED, w, 0.05)
+    ref = train_step(gd.indptr, gd.indices, gd.feats, gd.d, gd.labels, seeds, cfg["fanouts"], 0x5EED, w, 0.05,
+                     aggr="mean" if aggr == gnnv.AGGR_MEAN else "sum")
     assert abs(f["loss"] - ref["loss"]) <= 5e-3 * abs(ref["loss"])
     for (gW, gb), (rW, rb) in zip(gnnv.unflat_params(f["grads"], dims), ref["grads"]):
         for a_, b_ in ((gW, rW), (gb, rb)):
