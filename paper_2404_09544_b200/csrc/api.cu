@@ -324,6 +324,8 @@ gnnv_status gnnv_blocks_create(gnnv_graph* g, int32_t max_seeds, const int32_t* 
       GNNV_TRY_CUDA(cudaMemset(b->d_sizes, 0, (2 * L + 2) * sizeof(int32_t)));
       b->scan_words = tiles_max + 1;
       b->d_scan = (unsigned long long*)dmalloc(b->scan_words * sizeof(unsigned long long), "scan status");
+      // zero once: every hop's k_map clears the words its scan used (sample.cu)
+      GNNV_TRY_CUDA(cudaMemset(b->d_scan, 0, b->scan_words * sizeof(unsigned long long)));
       GNNV_TRY_CUDA(cudaDeviceSynchronize());
     } catch (...) {
       gnnv_blocks_free(b);

@@ -286,6 +286,7 @@ struct GemmDwArgs {  // dW = [X1|X2]^T G (+ bias row = colsum G) : deterministic
   bool db_fused = false;  // TF32 only: db = colsum(G) computed by the dW kernel (G final)
   const int32_t* x1_rows = nullptr;  // as GemmFwdArgs::x1_rows
   int64_t x1_table_rows = 0;
+  bool zeroed = false;  // TF32: dW (and db) already zero (the trainer clears them in-kernel)
 };
 void gemm_dw(const GemmDwArgs& a, int prec, cudaStream_t s);
 size_t gemm_dw_partial_floats(int32_t rows_plus_bias, int32_t N, int32_t* splits_out, int64_t max_M);
@@ -321,6 +322,7 @@ struct TailArgs {
   float* loss_partial;              // >= ceil(max_dst / 32) floats
   float* part;                      // tail_partial_floats(max_dst, d, C): per-CTA dW/db partials
   float *dW, *db, *d_loss;
+  float* zero; int64_t zero_n;      // cleared by k_tail_a (the other layers' dW/db), may be NULL
 };
 bool tail_supported(int kind, int d, int C, int fanout0);
 size_t tail_partial_floats(int64_t max_dst, int d, int C);

@@ -862,7 +862,7 @@ bool gemm_dw_tma(const GemmDwArgs& a, cudaStream_t s) {
   const int splits =
       (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(nkbm, 8), (int64_t)num_sms() / igroups));
   const int Ktot = a.X2 ? 2 * a.K1 : a.K1;
-  GNNV_TRY_CUDA(cudaMemsetAsync(a.dW, 0, (size_t)Ktot * a.N * sizeof(float), s));
+  if (!a.zeroed) GNNV_TRY_CUDA(cudaMemsetAsync(a.dW, 0, (size_t)Ktot * a.N * sizeof(float), s));
   Params p{};
   if (a.mask_bits) {
     GNNV_REQUIRE(a.mask_ld == mask_words(a.N), GNNV_ERR_PARAM, "dW: mask bits row stride");
@@ -875,7 +875,7 @@ bool gemm_dw_tma(const GemmDwArgs& a, cudaStream_t s) {
   }
   if (p.mask || p.dbsum) {
     GNNV_REQUIRE(a.db, GNNV_ERR_PARAM, "dW: db output required");
-    GNNV_TRY_CUDA(cudaMemsetAsync(a.db, 0, (size_t)a.N * sizeof(float), s));
+    if (!a.zeroed) GNNV_TRY_CUDA(cudaMemsetAsync(a.db, 0, (size_t)a.N * sizeof(float), s));
     p.db = a.db;
   }
   p.x1_rows = a.x1_rows;

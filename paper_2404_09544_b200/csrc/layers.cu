@@ -288,7 +288,7 @@ void layer_fwd_impl(gnnv_blocks* b, int32_t layer, const gnnv_layer_desc* ld, co
 void layer_bwd_impl(gnnv_blocks* b, int32_t layer, const gnnv_layer_desc* ld, const float* Gdst, const float* Hdst,
                     const float* Hsrc, const float* A, const float* W, float* Gsrc, float* dW, float* db,
                     cudaStream_t s, Timeline* tl, const uint32_t* mask_bits, bool g_masked,
-                    const uint32_t* src_bits, int32_t src_bits_ld, const XRows* xr) {
+                    const uint32_t* src_bits, int32_t src_bits_ld, const XRows* xr, bool grads_zeroed) {
   const std::string sfx = ".l" + std::to_string(layer);
   const int h = b->L - layer;
   const int32_t* d_ndst = b->d_sizes + h;
@@ -365,6 +365,7 @@ void layer_bwd_impl(gnnv_blocks* b, int32_t layer, const gnnv_layer_desc* ld, co
     w.mask_ld = mwords;
   }
   w.db_fused = tf32 && !need_mask;
+  w.zeroed = tf32 && grads_zeroed;
   if (tl) tl->mark(s, "gemm_dw" + sfx);
   gemm_dw(w, ld->prec, s);
   if (Gsrc) {
@@ -425,7 +426,7 @@ gnnv_status gnnv_layer_bwd(gnnv_blocks* b, int32_t layer, const gnnv_layer_desc*
     GNNV_REQUIRE(d_Gdst && d_Hdst && d_Hsrc && d_saveA && d_W && d_dW && d_db, GNNV_ERR_PARAM,
                  "layer_bwd: null buffer");
     layer_bwd_impl(b, layer, ld, d_Gdst, d_Hdst, d_Hsrc, d_saveA, d_W, d_Gsrc, d_dW, d_db, (cudaStream_t)s, nullptr,
-                   nullptr, false, nullptr, 0, nullptr);
+                   nullptr, false, nullptr, 0, nullptr, false);
   });
 }
 

@@ -550,12 +550,17 @@ __global__ void __launch_bounds__(kScanTile) k_relabel_scan(int64_t N, int h, in
   }
 }
 
+// Also clears the scan status words hop hp's k_relabel_scan used (its
+// ticket counter and one word per tile), so the next hop's -- or the next
+// batch's -- scan starts from zero without a memset node in the stream.
 __global__ void k_map(int hp, int kp, const int32_t* sizes, const int32_t* __restrict__ ellp,
                       const int32_t* __restrict__ cntp, const int32_t* __restrict__ indptrp, const int32_t* tag,
-                      int32_t* __restrict__ indicesp) {
+                      int32_t* __restrict__ indicesp, unsigned long long* scan, int64_t scan_words) {
   GNNV_PDL_ENTRY();
-  map_slots(blockIdx.x * (int64_t)blockDim.x + threadIdx.x, (int64_t)gridDim.x * blockDim.x, hp, kp, sizes, ellp, cntp,
-            indptrp, tag, indicesp);
+  const int64_t t0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x, stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t used = std::min<int64_t>(scan_words, 1 + ((int64_t)sizes[hp] + kScanTile - 1) / kScanTile);
+  for (int64_t i = t0; i < used; i += stride) scan[i] = 0ull;
+  map_slots(t0, stride, hp, kp, sizes, ellp, cntp, indptrp, tag, indicesp);
 }
 
 __global__ void k_reset(const int32_t* __restrict__ F, const int32_t* sizes, int L, int64_t N, int32_t* tag) {
@@ -599,7 +604,7 @@ void launch_sample(gnnv_graph* g, gnnv_blocks* b, const int32_t* d_seeds, int32_
       const int64_t slots_ub = b->max_n[h - 1] * (int64_t)b->fanouts[h - 1];
       launch_k(k_map, grid_for(slots_ub, 1024, sms * 8), 256, 0, s, h - 1, b->fanouts[h - 1], b->d_sizes, b->d_ell,
                                                               b->d_cnt, b->d_indptr[h - 1], b->d_tag,
-                                                              b->d_indices[h - 1]);
+                                                              b->d_indices[h - 1], b->d_scan, b->scan_words);
       GNNV_CHECK_LAUNCH();
     }
     const int threads = 256;
@@ -625,7 +630,6 @@ void launch_sample(gnnv_graph* g, gnnv_blocks* b, const int32_t* d_seeds, int32_
     }
 #undef GNNV_SAMPLE_LAUNCH
     GNNV_CHECK_LAUNCH();
-    GNNV_TRY_CUDA(cudaMemsetAsync(b->d_scan, 0, b->scan_words * sizeof(unsigned long long), s));
     const int tiles_ub = (int)ceil_div(rows_ub, kScanTile);
     launch_k(k_winners, grid_for(rows_ub * k, 1024, 0), 256, 0, s, g->n, h, k, b->d_sizes, b->d_ell, b->d_cnt, b->d_tag,
                                                              b->d_own[h]);
@@ -636,7 +640,8 @@ void launch_sample(gnnv_graph* g, gnnv_blocks* b, const int32_t* d_seeds, int32_
   }
   const int64_t slots_ub = b->max_n[L - 1] * (int64_t)b->fanouts[L - 1];
   launch_k(k_map, grid_for(slots_ub, 1024, sms * 8), 256, 0, s, L - 1, b->fanouts[L - 1], b->d_sizes, b->d_ell, b->d_cnt,
-                                                          b->d_indptr[L - 1], b->d_tag, b->d_indices[L - 1]);
+                                                          b->d_indptr[L - 1], b->d_tag, b->d_indices[L - 1], b->d_scan,
+                                                          b->scan_words);
   GNNV_CHECK_LAUNCH();
   launch_k(k_reset, grid_for(b->max_n[L], 1024, sms * 8), 256, 0, s, b->d_F, b->d_sizes, L, g->n, b->d_tag);
   GNNV_CHECK_LAUNCH();

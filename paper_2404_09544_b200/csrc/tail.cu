@@ -83,8 +83,12 @@ __global__ void __launch_bounds__(TA_WARPS * 32, 1) k_tail_a(
     const float* __restrict__ W, const float* __restrict__ bias, int d, int C, int aggr, float* __restrict__ A,
     int lda, float* __restrict__ Z, float* __restrict__ dZ, int ldz, const int32_t* __restrict__ F,
     const int32_t* __restrict__ labels, int n_global, float* dH, int ldg, float* dAs, float* __restrict__ part,
-    float* __restrict__ loss_partial) {
+    float* __restrict__ loss_partial, float* __restrict__ zero, int64_t zero_n) {
   GNNV_PDL_ENTRY();
+  // the earlier layers' dW / db, accumulated atomically by their dW GEMMs
+  // later in the step: cleared here instead of by memset nodes
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < zero_n; i += (int64_t)gridDim.x * blockDim.x)
+    zero[i] = 0.f;
   extern __shared__ __align__(16) float sm[];
   const TailSmem L(d, C);
   const int K = L.K, C8 = L.C8;
@@ -434,7 +438,7 @@ static void launch_tail_cpl(const TailArgs& a, cudaStream_t s, Timeline* tl, con
   if (tl) tl->mark(s, "tail_a" + sfx);
   launch_k(k_tail_a<CPL>, ga, TA_WARPS * 32, smem, s, a.indptr, a.indices, a.own, a.d_ndst, a.H, a.ldh, a.hbits,
            a.hbits_ld, a.W, a.bias, a.d, a.C, a.aggr, a.A, a.lda, a.Z, a.dZ, a.ldz, a.F, a.labels, a.n_global, a.dH,
-           a.ldg, a.dA, a.part, a.loss_partial);
+           a.ldg, a.dA, a.part, a.loss_partial, a.zero, a.zero ? a.zero_n : (int64_t)0);
   GNNV_CHECK_LAUNCH();
   const int push_blocks = (int)ceil_div(std::max<int64_t>(a.max_dst, 1), 8);
   const int K = 2 * a.d;

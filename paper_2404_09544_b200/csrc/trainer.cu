@@ -17,7 +17,7 @@ void layer_fwd_impl(gnnv_blocks* b, int32_t layer, const gnnv_layer_desc* ld, co
 void layer_bwd_impl(gnnv_blocks* b, int32_t layer, const gnnv_layer_desc* ld, const float* Gdst, const float* Hdst,
                     const float* Hsrc, const float* A, const float* W, float* Gsrc, float* dW, float* db,
                     cudaStream_t s, Timeline* tl, const uint32_t* mask_bits, bool g_masked,
-                    const uint32_t* src_bits, int32_t src_bits_ld, const XRows* xr);
+                    const uint32_t* src_bits, int32_t src_bits_ld, const XRows* xr, bool grads_zeroed);
 }  // namespace gnnv
 
 using namespace gnnv;
@@ -686,6 +686,8 @@ gnnv_status gnnv_step(gnnv_trainer* t, const int32_t* seeds, int32_t n_seeds, in
       a.dA = t->tail_dA;
       a.loss_partial = t->loss_partial;
       a.part = t->tail_part;
+      a.zero = t->d_grads;  // layers 1..L-1: [0, w_off[L-1])
+      a.zero_n = t->w_off[L - 1];
       a.dW = t->d_grads + t->w_off[L - 1];
       a.db = t->d_grads + t->b_off[L - 1];
       a.d_loss = d_loss;
@@ -702,7 +704,7 @@ gnnv_status gnnv_step(gnnv_trainer* t, const int32_t* seeds, int32_t n_seeds, in
       layer_bwd_impl(b, i, &ld, t->G[i], t->H[i], t->H[i - 1], t->A[i], t->d_params + t->w_off[i - 1],
                      i > 1 ? t->G[i - 1] : nullptr, t->d_grads + t->w_off[i - 1], t->d_grads + t->b_off[i - 1], s, tl,
                      t->mbits[i], t->mbits[i] != nullptr, t->mbits[i - 1], mask_words(t->md.dims[i - 1]),
-                     i == 1 ? xr1 : nullptr);
+                     i == 1 ? xr1 : nullptr, t->tail);
       if (pf_gate().phase == 'b' && i == pf_gate().layer) {
         GNNV_TRY_CUDA(cudaEventRecord(t->ev_mid, s));
         t->mid_pending = true;
