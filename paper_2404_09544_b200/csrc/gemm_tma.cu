@@ -585,17 +585,29 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_tma_gemm(const __grid_constant_
           }
           const int krow0 = (is_a ? gx * 32 : MT * BM + (gx - MT * 4) * 32) + 4 * cq;
           const uint32_t kt_u32 = smem_u32(kt);
-#define GNNV_KROW_STORE(ci, comp)                                                                        \
-  {                                                                                                      \
-    const int krow = krow0 + (ci);                                                                       \
-    st_shared_v4(kt_u32 + (uint32_t)krow * 64 + ((rq ^ ((krow >> 1) & 3)) << 4), x[0].comp, x[1].comp, \
-                 x[2].comp, x[3].comp);                                                                  \
-  }
-          GNNV_KROW_STORE(0, x)
-          GNNV_KROW_STORE(1, y)
-          GNNV_KROW_STORE(2, z)
-          GNNV_KROW_STORE(3, w)
-#undef GNNV_KROW_STORE
+          // Store q writes feature (K-major row) krow0 + ((q + cq/2) & 3): the
+          // per-lane rotation spreads each 8-lane phase of the STS.128 over
+          // both row parities and all four SW64 chunks, i.e. all 32 banks
+          // (one wavefront per phase; without it 8 lanes of a phase share 8
+          // banks -- 4x the store wavefronts, measured 57% of the shared pipe)
+          const int rot = cq >> 1;
+          const bool r1 = rot & 1, r2 = rot & 2;
+          float y[4][4];  // y[j][q] = component (q + rot) & 3 of x[j] (branch-free selects)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const float a = r1 ? x[j].y : x[j].x, b = r1 ? x[j].z : x[j].y;
+            const float c = r1 ? x[j].w : x[j].z, e = r1 ? x[j].x : x[j].w;
+            y[j][0] = r2 ? c : a;
+            y[j][1] = r2 ? e : b;
+            y[j][2] = r2 ? a : c;
+            y[j][3] = r2 ? b : e;
+          }
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int krow = krow0 + ((q + rot) & 3);
+            st_shared_v4(kt_u32 + (uint32_t)krow * 64 + ((rq ^ ((krow >> 1) & 3)) << 4), y[0][q], y[1][q], y[2][q],
+                         y[3][q]);
+          }
         }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // every writer, then one arrive per warp
         __syncwarp();
