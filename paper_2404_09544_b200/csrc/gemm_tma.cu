@@ -42,6 +42,8 @@ constexpr int BK = 32;      // fp32 elements of K per stage
 constexpr int NE = 8;       // epilogue / transposer warps
 constexpr int NTHREADS = 64 + 32 * NE;
 constexpr int FWD_STAGES = 4;
+constexpr int PAIR_STAGES = 5;  // CTA-pair fwd: a stage is A 16 KB + half of B 16 KB
+constexpr int PAIR_OB = 2;      // CTA-pair fwd: double-buffered 4 KB epilogue staging per warp
 constexpr int DW_STAGES = 4;
 constexpr int DW_MT = 2;    // 128-row i-tiles per dW CTA
 constexpr int DW_KR = 16;   // graph rows per dW k-block
@@ -110,15 +112,62 @@ __device__ __forceinline__ uint64_t desc_sw(uint32_t saddr, uint32_t sbo, uint32
   return d;
 }
 // kind::tf32 instruction descriptor: D=f32, A=B=tf32, M=128, N, majors.
-__device__ __forceinline__ uint32_t idesc_tf32(uint32_t n, bool a_mn, bool b_mn) {
+__device__ __forceinline__ uint32_t idesc_tf32(uint32_t n, bool a_mn, bool b_mn, uint32_t m = BM) {
   return (1u << 4) | (2u << 7) | (2u << 10) | ((a_mn ? 1u : 0u) << 15) | ((b_mn ? 1u : 0u) << 16) | ((n >> 3) << 17) |
-         ((uint32_t)(BM >> 4) << 24);
+         ((m >> 4) << 24);
 }
 __device__ __forceinline__ void mma_tf32(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
   asm volatile(
       "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\ntcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(
           d),
       "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+// ---- CTA pair (cluster of 2, tcgen05 cta_group::2) helpers
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// shared::cluster address of the same offset in CTA `rank` of the cluster
+__device__ __forceinline__ uint32_t map_rank(const void* p, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(p)), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void mbar_arrive_remote(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* b, uint32_t parity) {
+  asm volatile(
+      "{\n.reg .pred p;\nW_%=:\nmbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1, 1000000;\n@!p bra "
+      "W_%=;\n}\n" ::"r"(smem_u32(b)),
+      "r"(parity)
+      : "memory");
+}
+// TMA into this CTA's shared memory, completing bytes on the pair leader's
+// mbarrier (rank 0: the barrier address with the peer bit cleared)
+__device__ __forceinline__ void tma_load_2d_pair(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], "
+      "[%4];" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(c0), "r"(c1), "r"(smem_u32(bar) & 0xFEFFFFFFu)
+      : "memory");
+}
+__device__ __forceinline__ void mma_tf32_pair(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\ntcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(d),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+// arrive on the barrier at this offset in both CTAs of the pair when the
+// leader's MMAs issued so far complete
+__device__ __forceinline__ void mma_commit_pair(uint64_t* bar) {
+  asm volatile(
+      "{\n.reg .b16 m;\nmov.b16 m, 3;\ntcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 "
+      "[%0], m;\n}\n" ::"r"(smem_u32(bar))
+      : "memory");
 }
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
@@ -205,20 +254,29 @@ static int debug_flags() {
   return f;
 }
 
-template <int MODE>
+// PAIR (MODE_FWD only): a cluster of 2 CTAs computes 256-row tiles with
+// tcgen05.mma.cta_group::2 (M = 256): each CTA stages its own 128 rows of A
+// and half of the W^T tile's N columns, the leader (rank 0) issues the MMAs,
+// each CTA's TMEM receives its 128 rows; the W^T bytes each CTA pulls from L2
+// per k-block halve, and the smaller stage affords 6 stages.
+template <int MODE, bool PAIR = false>
 __global__ void __launch_bounds__(NTHREADS, 1) k_tma_gemm(const __grid_constant__ Params p) {
   GNNV_PDL_ENTRY();
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   __shared__ float s_bias[256];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
-  constexpr int S = MODE == MODE_DW ? DW_STAGES : FWD_STAGES;
+  constexpr int S = MODE == MODE_DW ? DW_STAGES : PAIR ? PAIR_STAGES : FWD_STAGES;
   constexpr int MT = MODE == MODE_DW ? DW_MT : 1;
   const int BN = p.BN;
-  // fwd/dX stage: A [128 rows x 128B] + B [BN rows x 128B] (K-major SW128 boxes).
+  const uint32_t crank = PAIR ? cluster_rank() : 0u;
+  const int pid = PAIR ? (int)blockIdx.x / 2 : (int)blockIdx.x;   // tile-loop index of this CTA (pair)
+  const int npid = PAIR ? (int)gridDim.x / 2 : (int)gridDim.x;
+  // fwd/dX stage: A [128 rows x 128B] + B [BN rows x 128B] (K-major SW128 boxes;
+  // PAIR: B [BN/2 rows x 128B], this CTA's half of N).
   // dW stage (unswizzled row-major boxes of DW_KR graph rows): MT A tiles of
   // [16 x 128] fp32, then G [16 x BN], then (fused mask) H [16 x BN].
   const int a_bytes = MODE == MODE_DW ? MT * DW_KR * BM * 4 : BM * BKB;
-  const int g_bytes = MODE == MODE_DW ? DW_KR * BN * 4 : BN * BKB;
+  const int g_bytes = MODE == MODE_DW ? DW_KR * BN * 4 : (PAIR ? BN / 2 : BN) * BKB;
   const int b_bytes = MODE == MODE_DW ? g_bytes + (p.mask ? DW_KR * p.nwp * 4 : 0) : g_bytes;
   const int stage_bytes = a_bytes + b_bytes;
   // dW: two K-major SW64 tiles (64B rows = 16 tf32 of K) built by the transposers;
@@ -226,7 +284,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_tma_gemm(const __grid_constant_
   const int kt_bytes = MODE == MODE_DW ? (MT * BM + BN) * 64 : 0;
   uint8_t* kbuf = smem + (((size_t)S * stage_bytes + 1023) & ~(size_t)1023);  // swizzle-atom aligned
   uint8_t* obuf = kbuf;
-  const int extra = MODE == MODE_DW ? 2 * kt_bytes : NE * 4096;
+  const int extra = MODE == MODE_DW ? 2 * kt_bytes : NE * 4096 * (PAIR ? PAIR_OB : 1);
   uint64_t* bars = reinterpret_cast<uint64_t*>(kbuf + extra);
   uint64_t* full = bars;
   uint64_t* empty = bars + S;
@@ -246,7 +304,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_tma_gemm(const __grid_constant_
     kb1 = min(nkbm, kb0 + per);
   } else {
     ntiles = ((M + BM - 1) / BM) * (MODE == MODE_DX ? p.n_ntiles : 1);
-    if ((int)blockIdx.x >= ntiles) return;  // block-uniform
+    if (PAIR) ntiles = (ntiles + 1) / 2;  // 256-row pair tiles
+    if (pid >= ntiles) return;  // block-uniform (pair-uniform)
   }
   uint32_t ncols = 32;
   const uint32_t need = (uint32_t)(MT * BN) * (MODE == MODE_DW ? 1u : 2u);
@@ -261,20 +320,28 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_tma_gemm(const __grid_constant_
       mbar_init(&kready[b], NE);
       mbar_init(&kfree[b], 1);
       mbar_init(&tfull[b], 1);
-      mbar_init(&tempty[b], NE);
+      mbar_init(&tempty[b], PAIR ? 2 * NE : NE);  // PAIR: the leader's, both CTAs' epilogue warps
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
+  if (PAIR) cluster_sync_all();  // the peer's barriers exist before any remote arrive / TMA
   if (warp == 0 && lane == 0) {
     tma_prefetch(&p.ta1);
     if (p.two) tma_prefetch(&p.ta2);
     tma_prefetch(&p.tb);
   }
   if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(s_tmem)),
-                 "r"(ncols)
-                 : "memory");
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    if (PAIR) {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(s_tmem)),
+                   "r"(ncols)
+                   : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(s_tmem)),
+                   "r"(ncols)
+                   : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
   }
   if (MODE == MODE_FWD && warp >= 2) {
     for (int i = threadIdx.x - 64; i < BN; i += NE * 32) s_bias[i] = i < p.N ? __ldg(p.bias + i) : 0.f;
@@ -287,8 +354,28 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_tma_gemm(const __grid_constant_
   if (MODE != MODE_DW) {
     // ======================= persistent fwd / dX =======================
     if (warp == 0) {
-      const bool g4 = MODE == MODE_FWD && p.x1_rows != nullptr;
-      if (lane == 0 || g4) {
+      const bool g4 = MODE == MODE_FWD && !PAIR && p.x1_rows != nullptr;
+      if (PAIR) {
+        if (lane == 0) {
+          // both CTAs: wait for the local stage to be free (the leader's MMA
+          // commit arrives on it in both CTAs), load this CTA's A rows and
+          // half of B, completing bytes on the leader's full barrier
+          int it = 0;
+          for (int tile = pid; tile < ntiles; tile += npid) {
+            const int mt = 2 * tile + (int)crank;
+            for (int kb = 0; kb < p.nkb; ++kb, ++it) {
+              const int s = it % S;
+              uint8_t* sa = smem + (size_t)s * stage_bytes;
+              uint8_t* sb = sa + a_bytes;
+              if (it >= S) mbar_wait(&empty[s], ((it / S) & 1) ^ 1);
+              if (crank == 0) mbar_arrive_tx(&full[s], (uint32_t)(2 * stage_bytes));
+              if (kb >= p.nkb1) tma_load_2d_pair(sa, &p.ta2, (kb - p.nkb1) * BK, mt * BM, &full[s]);
+              else tma_load_2d_pair(sa, &p.ta1, kb * BK, mt * BM, &full[s]);
+              tma_load_2d_pair(sb, &p.tb, kb * BK, (int)crank * (BN / 2), &full[s]);
+            }
+          }
+        }
+      } else if (lane == 0 || g4) {
         int it = 0;
         for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
           const int mt = MODE == MODE_DX ? tile / p.n_ntiles : tile;
@@ -324,7 +411,31 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_tma_gemm(const __grid_constant_
         }
       }
     } else if (warp == 1) {
-      if (lane == 0) {
+      if (PAIR) {
+        if (lane == 0 && crank == 0) {
+          const uint32_t idesc = idesc_tf32((uint32_t)BN, false, false, 2 * BM);
+          int it = 0, lt = 0;
+          for (int tile = pid; tile < ntiles; tile += npid, ++lt) {
+            const int acc = lt & 1;
+            if (lt >= 2) mbar_wait_cluster(&tempty[acc], ((lt >> 1) & 1) ^ 1);
+            tc_after();
+            for (int kb = 0; kb < p.nkb; ++kb, ++it) {
+              const int s = it % S;
+              mbar_wait(&full[s], (it / S) & 1);
+              tc_after();
+              const uint32_t a0 = smem_u32(smem + (size_t)s * stage_bytes);
+              const uint32_t b0 = a0 + a_bytes;
+#pragma unroll
+              for (int k = 0; k < BK / 8; ++k)
+                mma_tf32_pair(tmem + (uint32_t)(acc * BN), desc_sw(a0 + k * 32, 1024, 2),
+                              desc_sw(b0 + k * 32, 1024, 2), idesc, (kb > 0 || k > 0) ? 1u : 0u);
+              mma_commit_pair(&empty[s]);
+            }
+            mma_commit_pair(&tfull[acc]);
+          }
+        }
+        __syncwarp();
+      } else if (lane == 0) {
         const uint32_t idesc = idesc_tf32((uint32_t)BN, false, false);
         int it = 0, lt = 0;
         for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++lt) {
@@ -356,14 +467,16 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_tma_gemm(const __grid_constant_
       // 4 KB smem buffer and one TMA store: coalesced full-line writes.
       const int q = warp & 3;
       const int half = (warp - 2) >> 2;
-      uint8_t* ob = obuf + (warp - 2) * 4096;
-      const uint32_t ob_u32 = smem_u32(ob);
+      constexpr int OBN = PAIR ? PAIR_OB : 1;
+      uint8_t* ob0 = obuf + (warp - 2) * 4096 * OBN;
+      int obi = 0;
       int lt = 0;
-      for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++lt) {
+      for (int tile = pid; tile < ntiles; tile += npid, ++lt) {
         const int acc = lt & 1;
-        const int mt = MODE == MODE_DX ? tile / p.n_ntiles : tile;
+        const int mt = PAIR ? 2 * tile + (int)crank : MODE == MODE_DX ? tile / p.n_ntiles : tile;
         const int nt = MODE == MODE_DX ? tile % p.n_ntiles : 0;
-        mbar_wait(&tfull[acc], (lt >> 1) & 1);
+        if (PAIR) mbar_wait_cluster(&tfull[acc], (lt >> 1) & 1);
+        else mbar_wait(&tfull[acc], (lt >> 1) & 1);
         tc_after();
         const int row0 = mt * BM + q * 32;
         const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN);
@@ -416,8 +529,12 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_tma_gemm(const __grid_constant_
             }
             continue;
           }
-          // the previous TMA store from this buffer must have read it
-          if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+          // the TMA store that last used this buffer (OBN chunks ago) must
+          // have read it; the OBN - 1 most recent ones may still be reading
+          uint8_t* ob = ob0 + obi * 4096;
+          const uint32_t ob_u32 = smem_u32(ob);
+          obi = (obi + 1) % OBN;
+          if (lane == 0) asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(OBN - 1) : "memory");
           __syncwarp();
 #pragma unroll
           for (int j = 0; j < 8; ++j)
@@ -438,7 +555,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_tma_gemm(const __grid_constant_
         }
         tc_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&tempty[acc]);  // one arrive per epilogue warp
+        if (lane == 0) {  // one arrive per epilogue warp (PAIR: on the leader's barrier)
+          if (PAIR) mbar_arrive_remote(map_rank(&tempty[acc], 0));
+          else mbar_arrive(&tempty[acc]);
+        }
       }
       if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
     }
@@ -673,10 +793,14 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_tma_gemm(const __grid_constant_
   }
   tc_before();
   __syncthreads();
+  if (PAIR) cluster_sync_all();  // both CTAs done with the pair's TMEM and barriers
   if (warp == 1) {
     __syncwarp();
     tc_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(ncols) : "memory");
+    if (PAIR)
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(ncols) : "memory");
+    else
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(ncols) : "memory");
   }
 }
 
@@ -763,11 +887,11 @@ struct Arena {
 };
 static Arena g_img;
 
-static size_t smem_bytes(int mode, int BN, int mask, int nwp) {
-  const int S = mode == MODE_DW ? DW_STAGES : FWD_STAGES;
+static size_t smem_bytes(int mode, int BN, int mask, int nwp, bool pair = false) {
+  const int S = mode == MODE_DW ? DW_STAGES : pair ? PAIR_STAGES : FWD_STAGES;
   const int a = mode == MODE_DW ? DW_MT * DW_KR * BM * 4 : BM * BKB;
-  const int b = mode == MODE_DW ? DW_KR * BN * 4 + (mask ? DW_KR * nwp * 4 : 0) : BN * BKB;
-  const int k = mode == MODE_DW ? 2 * (DW_MT * BM + BN) * 64 : NE * 4096;
+  const int b = mode == MODE_DW ? DW_KR * BN * 4 + (mask ? DW_KR * nwp * 4 : 0) : (pair ? BN / 2 : BN) * BKB;
+  const int k = mode == MODE_DW ? 2 * (DW_MT * BM + BN) * 64 : NE * 4096 * (pair ? PAIR_OB : 1);
   return (((size_t)S * (a + b) + 1023) & ~(size_t)1023) + k + 8 * (2 * S + 8) + 16 + 1024;
 }
 
@@ -780,6 +904,37 @@ static void launch(const Params& p, dim3 grid, cudaStream_t s) {
     attr = bytes;
   }
   launch_k(k_tma_gemm<MODE>, grid, NTHREADS, bytes, s, p);
+  GNNV_CHECK_LAUNCH();
+}
+
+// the CTA-pair forward GEMM: clusters of 2 along x
+static void launch_pair(const Params& p, int pairs, cudaStream_t s) {
+  static size_t attr = 0;
+  const size_t bytes = smem_bytes(MODE_FWD, p.BN, p.mask, p.nwp, true);
+  if (bytes > attr) {
+    GNNV_TRY_CUDA(cudaFuncSetAttribute(k_tma_gemm<MODE_FWD, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)bytes));
+    attr = bytes;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(2 * pairs));
+  cfg.blockDim = dim3(NTHREADS);
+  cfg.dynamicSmemBytes = bytes;
+  cfg.stream = s;
+  cudaLaunchAttribute attrs[2];
+  attrs[0].id = cudaLaunchAttributeClusterDimension;
+  attrs[0].val.clusterDim.x = 2;
+  attrs[0].val.clusterDim.y = 1;
+  attrs[0].val.clusterDim.z = 1;
+  int na = 1;
+  if (pdl_enabled()) {
+    attrs[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attrs[1].val.programmaticStreamSerializationAllowed = 1;
+    na = 2;
+  }
+  cfg.attrs = attrs;
+  cfg.numAttrs = na;
+  GNNV_TRY_CUDA(cudaLaunchKernelEx(&cfg, k_tma_gemm<MODE_FWD, true>, p));
   GNNV_CHECK_LAUNCH();
 }
 
@@ -799,9 +954,15 @@ bool gemm_fwd_tma(const GemmFwdArgs& a, cudaStream_t s) {
   GNNV_CHECK_LAUNCH();
   Params p{};
   p.x1_rows = a.x1_rows;
+  // CTA pairs (cta_group::2) with GNNV_GEMM_PAIR=1 (read per call).  Off by
+  // default: measured on products, layer 1 179 -> 189-192 us (its tiles are
+  // bound by the A operand's DRAM reads and the epilogue, not by the W^T
+  // traffic the pair halves), layer 2 49 -> 46 us
+  const char* pe = getenv("GNNV_GEMM_PAIR");
+  const bool pair = pe && pe[0] == '1' && !a.x1_rows && BN % 32 == 0;
   p.ta1 = a.x1_rows ? make_map(a.X1, a.x1_table_rows, a.K1, a.ld1, 1) : make_map(a.X1, a.max_M, a.K1, a.ld1, BM);
   p.ta2 = a.X2 ? make_map(a.X2, a.max_M, a.K1, a.ld2, BM) : p.ta1;
-  p.tb = make_map(Bt, BN, Kp, Kp, BN);
+  p.tb = make_map(Bt, BN, Kp, Kp, pair ? BN / 2 : BN);
   p.two = a.X2 ? 1 : 0;
   p.nkb1 = nkb1;
   p.nkb = nkb;
@@ -818,6 +979,10 @@ bool gemm_fwd_tma(const GemmFwdArgs& a, cudaStream_t s) {
   p.bits_ld = a.mask_ld;
   const int64_t tiles = ceil_div(std::max<int64_t>(a.max_M, 1), BM);
   p.dbg = debug_flags();
+  if (pair) {
+    launch_pair(p, (int)std::min<int64_t>(ceil_div(tiles, 2), num_sms() / 2), s);
+    return true;
+  }
   launch<MODE_FWD>(p, dim3((unsigned)std::min<int64_t>(tiles, num_sms())), s);
   return true;
 }

@@ -712,3 +712,40 @@ def test_fused_output_layer_matches_per_kernel_path(mini, monkeypatch, aggr):
         for a_, b_ in ((gW, rW), (gb, rb)):
             cos = float(np.dot(a_.ravel(), b_.ravel()) / (np.linalg.norm(a_) * np.linalg.norm(b_) + 1e-30))
             assert cos > 0.98, cos
+
+
+@pytest.mark.parametrize("d_in,d_out", [(100, 256), (64, 64), (64, 96)])
+def test_layer_fwd_cta_pair_gemm(mini, monkeypatch, d_in, d_out):
+    """The CTA-pair (tcgen05 cta_group::2, M = 256) forward GEMM, GNNV_GEMM_PAIR=1:
+    a tf32 SAGE layer forward equals the single-CTA GEMM's bit for bit (the
+    same tf32 products accumulated in the same K order per output element)
+    and the oracle within the tf32 bound -- with a ragged last pair (rows
+    beyond n_dst in the peer CTA, never stored) and rows >= n_dst untouched."""
+    gd, g = mini
+    fan = CONFIGS["mini"]["fanouts"]
+    seeds = epoch_seeds(gd.n, 0)[:300]
+    blocks, hb = gpu_sample(g, seeds, fan, 11, max_seeds=512)
+    layer, h = 2, 1
+    ob = _oracle_block(hb, h)
+    rng = np.random.default_rng(7)
+    s_in = row_stride(d_in)
+    Hsrc = np.zeros((ob.n_src, s_in), np.float32)
+    Hsrc[:, :d_in] = rng.standard_normal((ob.n_src, d_in)).astype(np.float32)
+    W = (rng.standard_normal((2 * d_in, d_out)) / np.sqrt(2 * d_in)).astype(np.float32)
+    b = rng.standard_normal(d_out).astype(np.float32)
+    ld = gnnv.layer_desc(d_in, d_out, s_in, 0, 0, 1, gnnv.PREC_TF32)
+    view = blocks.info(sync=False)[h]
+    cap_dst, cap_src = view.max_dst, view.max_src
+    out = {}
+    for pair in ("0", "1"):
+        monkeypatch.setenv("GNNV_GEMM_PAIR", pair)
+        Hdst = torch.full((cap_dst, row_stride(d_out)), float("nan"), device="cuda")
+        A = torch.full((cap_dst, s_in), float("nan"), device="cuda")
+        gnnv.layer_fwd(blocks, layer, ld, padded(Hsrc, cap_src), dev_f32(W), dev_f32(b), Hdst, A)
+        torch.cuda.synchronize()
+        assert torch.isnan(Hdst[ob.n_dst:]).all()
+        out[pair] = Hdst[: ob.n_dst].cpu().numpy()[:, :d_out]
+    assert np.array_equal(out["0"], out["1"])
+    Ho, _ = layer_fwd(ob, Hsrc[:, :d_in], W, b, True)
+    Hm, _ = layer_fwd(ob, Hsrc[:, :d_in], W, b, True, absval=True)
+    assert_close_cond(out["1"], Ho, Hm, RTOL[2], "pair GEMM layer")
