@@ -52,6 +52,10 @@ CONFIGS: Dict[str, dict] = {
                      fanouts=[15, 10, 5], batch=4096, ratio=1.0, beta=0.5, hidden=256),
     "papers100m": dict(name="papers100m", n=111059956, nnz=1615685872, d=128, C=172,
                        fanouts=[15, 10, 5], batch=8192, ratio=1.0, beta=0.5, hidden=256),
+    # products with 128-d features (512-byte rows): a layout experiment
+    # (DESIGN.md §9), not a BASELINE config
+    "products_d128": dict(name="products_d128", n=2449029, nnz=61859140, d=128, C=47,
+                          fanouts=[15, 10, 5], batch=4096, ratio=1.0, beta=0.5, hidden=256),
     # small config used by unit/parity tests: several tiles and a ragged tail
     "mini": dict(name="mini", n=20000, nnz=200000, d=100, C=47, fanouts=[15, 10, 5],
                  batch=512, ratio=0.3, beta=0.5, hidden=64),
