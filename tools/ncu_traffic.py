@@ -82,7 +82,7 @@ def main() -> None:
         elif n.startswith("k_spmm_fwd"):
             f += 1
             cur = f"spmm_fwd.l{f}"
-        elif n.startswith(("k_bt_fwd", "k_wimg_fwd")) or n in ("k_tma_gemm<0>", "k_tc_gemm<0>"):
+        elif n.startswith(("k_bt_fwd", "k_wimg_fwd", "k_tma_gemm<0", "k_tc_gemm<0")):
             cur = f"gemm_fwd.l{f}"
         elif n.startswith("k_ce_loss"):
             cur = "loss"
@@ -95,13 +95,13 @@ def main() -> None:
             b -= 1
             pending_dw = True
             cur = f"relu_mask.l{b}"
-        elif n in ("k_tma_gemm<2>", "k_tc_gemm<2>") or n.startswith("k_gemm_simt"):
+        elif n.startswith(("k_tma_gemm<2", "k_tc_gemm<2", "k_gemm_simt")):
             if pending_dw:
                 pending_dw = False
             else:
                 b -= 1
             cur = f"gemm_dw.l{b}"
-        elif n.startswith(("k_bt_dx", "k_wimg_dx")) or n in ("k_tma_gemm<1>", "k_tc_gemm<1>"):
+        elif n.startswith(("k_bt_dx", "k_wimg_dx", "k_tma_gemm<1", "k_tc_gemm<1")):
             cur = f"gemm_dx.l{b}"
         elif n.startswith("k_spmm_bwd"):
             cur = f"spmm_bwd.l{b}"
