@@ -539,6 +539,11 @@ gnnv_status gnnv_trainer_prefetch(gnnv_trainer* t, const int32_t* seeds, int32_t
       t->d_seedsb[k] = (int32_t*)dmalloc(t->md.max_seeds * sizeof(int32_t), "seeds (prefetch)");
       GNNV_TRY_CUDA(cudaMallocHost(&t->h_seedsb[k], t->md.max_seeds * sizeof(int32_t)));
       t->d_statsb[k] = (int64_t*)dmalloc(4 * sizeof(int64_t), "gather stats (prefetch)");
+      // the layer backward's scratch arena, sized like the first buffer set's
+      // (grown by its steps so far): growing it at this set's first step
+      // would put a device synchronisation and a cudaMalloc inside the step
+      if (t->bb[k ^ 1] && t->bb[k ^ 1]->scratch_bytes)
+        t->bb[k]->ensure_scratch(t->bb[k ^ 1]->scratch_bytes, (cudaStream_t)stream);
       if (!t->side) t->side = make_side_stream(g->device, &t->green);
     }
     cudaStream_t s = (cudaStream_t)stream;

@@ -86,6 +86,10 @@ def run(gd, g, name, B, fan, ratio, bias, policy, steps=12, warm=3):
     main = torch.cuda.Stream(priority=-1)  # as bench.py: non-default, high priority
     t0 = warm + steps
     tr.prefetch(seeds(t0), B, BASE_RNG_SEED + t0, on_host=False, stream=pf)
+    for t in range(t0, t0 + 2):  # untimed pipelined warm-up (both buffer sets in use)
+        tr.step(seeds(t), B, B, BASE_RNG_SEED + t, 0.01, on_host=False, want_loss=False, stream=main)
+        tr.prefetch(seeds(t + 1), B, BASE_RNG_SEED + t + 1, on_host=False, stream=pf)
+    t0 += 2
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(main)
