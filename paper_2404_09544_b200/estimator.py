@@ -127,6 +127,10 @@ def features(c: Candidate, hit: float, sizes: Sequence[float]) -> Dict[str, floa
     return {
         "sample_edges": float(sum(edges)),                      # Eq.7: |V_i| - |B0| and the edges behind it
         "sample_rows": float(VL - c.batch),
+        # NEXT-2's locality-biased sampler sweeps each frontier row's whole
+        # adjacency (two ballot passes over the neighbours' cache flags),
+        # not only its k picks
+        "sample_adj": float(sum(sizes[h] for h in range(L)) * c.nnz / c.n_nodes) if c.locality_bias > 0 else 0.0,
         "transfer_host_bytes": float(VL * (1 - hit) * 4 * c.n_attr),  # Eq.6: n_attr |V_i| (1-hit)
         "transfer_hbm_bytes": float(VL * hit * row),            # the hits' copy out of the device cache
         "replace_rows": float(VL * (1 - hit)) if c.policy in ("fifo", "lru") else 0.0,  # Eq.5
@@ -136,7 +140,7 @@ def features(c: Candidate, hit: float, sizes: Sequence[float]) -> Dict[str, floa
 
 
 PHASES = {
-    "sample": ["sample_edges", "sample_rows"],
+    "sample": ["sample_edges", "sample_rows", "sample_adj"],
     "transfer": ["transfer_host_bytes", "transfer_hbm_bytes"],
     "replace": ["replace_rows"],
     "compute": ["compute_flops", "compute_bytes"],
