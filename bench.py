@@ -550,6 +550,16 @@ def main():
              "algorithmic_per_launch": amount}
         if name.startswith("pf_"):
             r["overlapped"] = True
+        if name.startswith("spmm_fwd."):
+            # the edge-visit view -- every sampled edge reads a
+            # whole source row (re-reads of rows shared by several dst rows
+            # included) plus the output rows -- next to the distinct-row one
+            i = int(name.split(".l")[1])
+            h = len(cfg["fanouts"]) - i
+            d_in = dims[i - 1]
+            ev = sizes["nnz"][h] * d_in * 4 + sizes["n"][h] * ((d_in + 3) & ~3) * 4
+            r["edge_visit_bytes"] = ev
+            r["edge_visit_frac"] = ev / (avg_ms / 1000.0) / 1e9 / peaks["hbm"]
         rooflines[name] = r
         if roofline is None and not name.startswith("pf_"):
             roofline = r
