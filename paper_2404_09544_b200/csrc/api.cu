@@ -320,6 +320,22 @@ gnnv_status gnnv_blocks_create(gnnv_graph* g, int32_t max_seeds, const int32_t* 
         b->d_indices[h] = (int32_t*)dmalloc(std::max<int64_t>(b->max_nnz[h], 1) * sizeof(int32_t), "block indices");
         b->d_own[h] = (uint32_t*)dmalloc(b->max_n[h] * sizeof(uint32_t), "block owner masks");
       }
+      // GNNV_BWD_PULL=1: CSC of the hops whose layer has a dX (h <= L-2),
+      // for the pulled backward aggregation (measured slower than the
+      // two-pass push on products; opt-in)
+      b->csc_hops = getenv("GNNV_BWD_PULL") ? L - 1 : 0;
+      if (b->csc_hops > 0) {
+        int64_t n_max = 1;
+        for (int h = 0; h < b->csc_hops; ++h) {
+          b->d_colptr[h] = (int32_t*)dmalloc((b->max_n[h + 1] + 1) * sizeof(int32_t), "block CSC colptr");
+          b->d_csc[h] = (int32_t*)dmalloc(std::max<int64_t>(b->max_nnz[h], 1) * sizeof(int32_t), "block CSC rows");
+          n_max = std::max(n_max, b->max_n[h + 1] + 1);
+        }
+        b->d_csc_cnt = (int32_t*)dmalloc(n_max * sizeof(int32_t), "CSC counts");
+        GNNV_TRY_CUDA(cudaMemset(b->d_csc_cnt, 0, n_max * sizeof(int32_t)));
+        b->csc_tmp_bytes = csc_scan_tmp_bytes(n_max);
+        b->d_csc_tmp = dmalloc(b->csc_tmp_bytes, "CSC scan temporary");
+      }
       b->d_sizes = (int32_t*)dmalloc((2 * L + 2) * sizeof(int32_t), "sizes");
       GNNV_TRY_CUDA(cudaMemset(b->d_sizes, 0, (2 * L + 2) * sizeof(int32_t)));
       b->scan_words = tiles_max + 1;
@@ -356,7 +372,11 @@ gnnv_status gnnv_blocks_free(gnnv_blocks* b) {
     dfree(b->d_indptr[h]);
     dfree(b->d_indices[h]);
     dfree(b->d_own[h]);
+    dfree(b->d_colptr[h]);
+    dfree(b->d_csc[h]);
   }
+  dfree(b->d_csc_cnt);
+  dfree(b->d_csc_tmp);
   dfree(b->d_sizes);
   dfree(b->d_scan);
   dfree(b->scratch);

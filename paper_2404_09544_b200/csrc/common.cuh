@@ -174,6 +174,17 @@ struct gnnv_blocks {
   unsigned long long* d_scan = nullptr;  // chained-scan status [1 + max tiles]
   int64_t scan_words = 0;
   uint32_t* d_own[GNNV_MAX_LAYERS] = {nullptr};  // [max_n[h]] owner-edge bit mask per dst row
+  // transposed block (CSC) of the hops whose layer has a dX (h <= L-2): the
+  // in-edges of src row u are csc_dst[h][colptr[h][u] .. colptr[h][u+1]),
+  // their dst rows (counting sort) -- the backward aggregation
+  // pulls through it (k_spmm_bwd_pull, GNNV_BWD_PULL=1).  csc_hops = 0 (default)
+  // keeps the two-pass push.
+  int32_t csc_hops = 0;
+  int32_t* d_colptr[GNNV_MAX_LAYERS] = {nullptr};  // [max_n[h+1] + 1]
+  int32_t* d_csc[GNNV_MAX_LAYERS] = {nullptr};     // [max_nnz[h]]
+  int32_t* d_csc_cnt = nullptr;    // [max n_src + 1] in-edge counts (zero between batches)
+  void* d_csc_tmp = nullptr;       // cub scan temporary storage
+  size_t csc_tmp_bytes = 0;
   bool sampled = false;
   // NEXT-2 locality bias: cached neighbours (slot[u] >= 0) weigh loc_w
   // (= 1 + 4b, 1 = unbiased); see gnnv_blocks_set_locality
@@ -219,6 +230,8 @@ struct Timeline {
 // sample.cu
 void launch_sample(gnnv_graph* g, gnnv_blocks* b, const int32_t* d_seeds, int32_t n_seeds, uint64_t rng_seed,
                    cudaStream_t s);
+// cub scan temporary bytes for the CSC column pointers of max_items columns
+size_t csc_scan_tmp_bytes(int64_t max_items);
 // cache.cu
 void launch_cache_update(gnnv_cache* c, const gnnv_blocks* b, const float* d_X, cudaStream_t s);
 void launch_gather(const gnnv_cache* c, const gnnv_blocks* b, float* d_X, int64_t* d_stats, cudaStream_t s,
@@ -235,6 +248,14 @@ void launch_spmm_fwd(const int32_t* d_indptr, const int32_t* d_indices, const in
 void launch_spmm_bwd(const int32_t* d_indptr, const int32_t* d_indices, const uint32_t* d_own, const int32_t* d_ndst,
                      int64_t max_dst, const float* dA, int32_t lda, float* dH, int32_t ldh, int32_t d, int32_t kind,
                      int32_t aggr, const uint32_t* bits, int32_t bits_ld, cudaStream_t s);
+// the same transposed aggregation pulled per src row (rows up to
+// kPullMaxLd floats; wider ones keep the push) through the block's
+// CSC (one coalesced store per dH row, no atomics; see k_spmm_bwd_pull)
+constexpr int kPullMaxLd = 512;
+void launch_spmm_bwd_pull(const int32_t* d_colptr, const int32_t* d_csc, const int32_t* d_indptr,
+                          const int32_t* d_ndst, const int32_t* d_nsrc, int64_t max_src, const float* dA, int32_t lda,
+                          float* dH, int32_t ldh, int32_t d, int32_t kind, int32_t aggr, const uint32_t* bits,
+                          int32_t bits_ld, cudaStream_t s);
 void launch_colsum_reduce(const float* partial, int blocks, int ld, int N, float* out, cudaStream_t s);
 // gemm
 struct GemmFwdArgs {

@@ -395,10 +395,18 @@ void layer_bwd_impl(gnnv_blocks* b, int32_t layer, const gnnv_layer_desc* ld, co
     if (tl) tl->mark(s, "gemm_dx" + sfx);
     gemm_dx(x, ld->prec, s);
     if (tl) tl->mark(s, "spmm_bwd" + sfx);
-    // transposed aggregation pushed from the dst rows: owner edges store,
-    // the rest add atomically -- no zeroing pass over dH_src
-    launch_spmm_bwd(b->d_indptr[h], b->d_indices[h], b->d_own[h], d_ndst, max_dst, dA, lda, Gsrc, ld->in_stride,
-                    ld->d_in, ld->kind, ld->aggr, tf32 ? src_bits : nullptr, src_bits_ld, s);
+    if (h < b->csc_hops && ld->in_stride <= kPullMaxLd) {
+      // transposed aggregation pulled per src row through the block's CSC:
+      // one coalesced store per dH_src row, no atomics
+      launch_spmm_bwd_pull(b->d_colptr[h], b->d_csc[h], b->d_indptr[h], d_ndst, b->d_sizes + h + 1, b->max_n[h + 1],
+                           dA, lda, Gsrc, ld->in_stride, ld->d_in, ld->kind, ld->aggr, tf32 ? src_bits : nullptr,
+                           src_bits_ld, s);
+    } else {
+      // transposed aggregation pushed from the dst rows: owner edges store,
+      // the rest add atomically -- no zeroing pass over dH_src
+      launch_spmm_bwd(b->d_indptr[h], b->d_indices[h], b->d_own[h], d_ndst, max_dst, dA, lda, Gsrc, ld->in_stride,
+                      ld->d_in, ld->kind, ld->aggr, tf32 ? src_bits : nullptr, src_bits_ld, s);
+    }
   }
 }
 

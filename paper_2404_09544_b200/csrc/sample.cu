@@ -32,9 +32,18 @@
 //   k_reset         : tag[F_L[i]] = INT_MIN, ready for the next call.
 #include <limits.h>
 
+#include <cub/device/device_scan.cuh>
+
 #include "common.cuh"
 
 namespace gnnv {
+
+size_t csc_scan_tmp_bytes(int64_t max_items) {
+  size_t bytes = 0;
+  GNNV_TRY_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, bytes, (const int32_t*)nullptr, (int32_t*)nullptr,
+                                              (int)max_items));
+  return bytes;
+}
 
 constexpr int kScanTile = 256;
 
@@ -94,7 +103,7 @@ __device__ __forceinline__ void load4(const int32_t* __restrict__ a, int64_t e0,
 __device__ __forceinline__ void map_slots(int64_t t0, int64_t stride, int hp, int kp, const int32_t* sizes,
                                           const int32_t* __restrict__ ellp, const int32_t* __restrict__ cntp,
                                           const int32_t* __restrict__ indptrp, const int32_t* tag,
-                                          int32_t* __restrict__ indicesp) {
+                                          int32_t* __restrict__ indicesp, int32_t* __restrict__ csc_cnt = nullptr) {
   const int64_t nslots = (int64_t)sizes[hp] * kp;
   for (int64_t e0 = 4 * t0; e0 < nslots; e0 += 4 * stride) {
     int u[4], t[4], dst[4];
@@ -114,7 +123,10 @@ __device__ __forceinline__ void map_slots(int64_t t0, int64_t stride, int hp, in
     }
 #pragma unroll
     for (int j = 0; j < 4; ++j)
-      if (dst[j] >= 0) indicesp[dst[j]] = t[j];
+      if (dst[j] >= 0) {
+        indicesp[dst[j]] = t[j];
+        if (csc_cnt) atomicAdd(csc_cnt + t[j], 1);
+      }
   }
 }
 
@@ -553,14 +565,35 @@ __global__ void __launch_bounds__(kScanTile) k_relabel_scan(int64_t N, int h, in
 // Also clears the scan status words hop hp's k_relabel_scan used (its
 // ticket counter and one word per tile), so the next hop's -- or the next
 // batch's -- scan starts from zero without a memset node in the stream.
+// With csc_cnt (hops that get a CSC): also counts each src id's in-edges.
 __global__ void k_map(int hp, int kp, const int32_t* sizes, const int32_t* __restrict__ ellp,
                       const int32_t* __restrict__ cntp, const int32_t* __restrict__ indptrp, const int32_t* tag,
-                      int32_t* __restrict__ indicesp, unsigned long long* scan, int64_t scan_words) {
+                      int32_t* __restrict__ indicesp, unsigned long long* scan, int64_t scan_words,
+                      int32_t* __restrict__ csc_cnt) {
   GNNV_PDL_ENTRY();
   const int64_t t0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x, stride = (int64_t)gridDim.x * blockDim.x;
   const int64_t used = std::min<int64_t>(scan_words, 1 + ((int64_t)sizes[hp] + kScanTile - 1) / kScanTile);
   for (int64_t i = t0; i < used; i += stride) scan[i] = 0ull;
-  map_slots(t0, stride, hp, kp, sizes, ellp, cntp, indptrp, tag, indicesp);
+  map_slots(t0, stride, hp, kp, sizes, ellp, cntp, indptrp, tag, indicesp, csc_cnt);
+}
+
+// CSC fill of hop hp (counting sort): colptr = exclusive scan of the in-edge
+// counts; edge (r, u) takes slot colptr[u] + (--cnt[u]), which also leaves
+// the counts zeroed for the next batch.  The order of a column's entries
+// follows the atomics; the pulled sum is exact up to that order.
+__global__ void k_csc_fill(int hp, int kp, const int32_t* sizes, const int32_t* __restrict__ indptrp,
+                           const int32_t* __restrict__ indicesp, int32_t* __restrict__ csc_cnt,
+                           const int32_t* __restrict__ colptr, int32_t* __restrict__ csc) {
+  GNNV_PDL_ENTRY();
+  const int64_t nslots = (int64_t)sizes[hp] * kp;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < nslots; e += (int64_t)gridDim.x * blockDim.x) {
+    const int r = (int)(e / kp), i = (int)(e - (int64_t)r * kp);
+    const int beg = __ldg(indptrp + r);
+    if (i < __ldg(indptrp + r + 1) - beg) {
+      const int u = __ldg(indicesp + beg + i);
+      csc[__ldg(colptr + u) + atomicSub(csc_cnt + u, 1) - 1] = r;
+    }
+  }
 }
 
 __global__ void k_reset(const int32_t* __restrict__ F, const int32_t* sizes, int L, int64_t N, int32_t* tag) {
@@ -596,17 +629,29 @@ void launch_sample(gnnv_graph* g, gnnv_blocks* b, const int32_t* d_seeds, int32_
                                                                 err_index);
   GNNV_CHECK_LAUNCH();
   // Hop h's slots reuse d_ell / d_cnt, so hop h-1 is mapped to local ids
-  // (its tags are final after its scan) before hop h samples.
+  // (its tags are final after its scan) before hop h samples.  Hops with a
+  // CSC (hp < csc_hops) then sort their edges by src id (stable: dst order
+  // within a column) and derive the column pointers.
+  auto map_hop = [&](int hp) {
+    const int64_t slots_ub = b->max_nnz[hp];
+    const bool csc = hp < b->csc_hops;
+    launch_k(k_map, grid_for(slots_ub, 1024, sms * 8), 256, 0, s, hp, b->fanouts[hp], b->d_sizes, b->d_ell, b->d_cnt,
+             b->d_indptr[hp], b->d_tag, b->d_indices[hp], b->d_scan, b->scan_words,
+             csc ? b->d_csc_cnt : (int32_t*)nullptr);
+    GNNV_CHECK_LAUNCH();
+    if (!csc) return;
+    size_t tmp = b->csc_tmp_bytes;
+    GNNV_TRY_CUDA(cub::DeviceScan::ExclusiveSum(b->d_csc_tmp, tmp, b->d_csc_cnt, b->d_colptr[hp],
+                                                (int)(b->max_n[hp + 1] + 1), s));
+    GNNV_CHECK_LAUNCH();
+    launch_k(k_csc_fill, grid_for(slots_ub, 256, 0), 256, 0, s, hp, b->fanouts[hp], b->d_sizes, b->d_indptr[hp],
+             b->d_indices[hp], b->d_csc_cnt, b->d_colptr[hp], b->d_csc[hp]);
+    GNNV_CHECK_LAUNCH();
+  };
   for (int h = 0; h < L; ++h) {
     const int k = b->fanouts[h];
     const int64_t rows_ub = b->max_n[h];
-    if (h > 0) {
-      const int64_t slots_ub = b->max_n[h - 1] * (int64_t)b->fanouts[h - 1];
-      launch_k(k_map, grid_for(slots_ub, 1024, sms * 8), 256, 0, s, h - 1, b->fanouts[h - 1], b->d_sizes, b->d_ell,
-                                                              b->d_cnt, b->d_indptr[h - 1], b->d_tag,
-                                                              b->d_indices[h - 1], b->d_scan, b->scan_words);
-      GNNV_CHECK_LAUNCH();
-    }
+    if (h > 0) map_hop(h - 1);
     const int threads = 256;
 #define GNNV_SAMPLE_LAUNCH(G)                                                                              \
   launch_k(k_sample_hop<G>, grid_for(rows_ub, threads / 32 * (32 / G), sms * 8), threads, 0, s,                  \
@@ -638,11 +683,7 @@ void launch_sample(gnnv_graph* g, gnnv_blocks* b, const int32_t* d_seeds, int32_
                                                   b->d_indptr[h], b->d_own[h], b->d_sizes, b->d_scan);
     GNNV_CHECK_LAUNCH();
   }
-  const int64_t slots_ub = b->max_n[L - 1] * (int64_t)b->fanouts[L - 1];
-  launch_k(k_map, grid_for(slots_ub, 1024, sms * 8), 256, 0, s, L - 1, b->fanouts[L - 1], b->d_sizes, b->d_ell, b->d_cnt,
-                                                          b->d_indptr[L - 1], b->d_tag, b->d_indices[L - 1], b->d_scan,
-                                                          b->scan_words);
-  GNNV_CHECK_LAUNCH();
+  map_hop(L - 1);
   launch_k(k_reset, grid_for(b->max_n[L], 1024, sms * 8), 256, 0, s, b->d_F, b->d_sizes, L, g->n, b->d_tag);
   GNNV_CHECK_LAUNCH();
 }

@@ -172,6 +172,147 @@ __global__ void __launch_bounds__(256) k_spmm_bwd(const int32_t* __restrict__ in
   }
 }
 
+// w_v of the mean (1/c_v, 1/(c_v+1) for GCN, 0 for an empty row) or 1 (sum)
+__device__ __forceinline__ float pull_weight(const int32_t* __restrict__ indptr, int v, bool mean, bool gcn) {
+  if (!mean) return 1.f;
+  const int denom = __ldg(indptr + v + 1) - __ldg(indptr + v) + (gcn ? 1 : 0);
+  return denom ? 1.f / (float)denom : 0.f;
+}
+
+// The same transposed aggregation pulled per SRC row through the block's CSC
+// (sampler: k_map counts, scan, k_csc_fill):
+//   dH[u] = base[u] + relu'(H[u]) * sum_{(v,u)} w_v dA[v]   (+ the GCN self
+// term w_u dA[u] for u < n_dst), base = the dX GEMM's dH_dst rows (SAGE,
+// u < n_dst) or 0.  Every dH row is written once with coalesced stores, no
+// atomics; dA (n_dst rows) is small and read from L2.  A warp takes 32 src
+// rows: lane i first fetches row i's column range, first in-edge and its
+// weight (independent loads, one round trip), then the warp's LPR-lane
+// groups load U rows' first dA rows before storing any (most src rows have a
+// single in-edge; further in-edges are added in column order).
+template <int LPR, int NC, int U>
+__global__ void __launch_bounds__(256) k_spmm_bwd_pull(const int32_t* __restrict__ colptr,
+                                                       const int32_t* __restrict__ csc,
+                                                       const int32_t* __restrict__ indptr, const int32_t* d_ndst,
+                                                       const int32_t* d_nsrc, const float* __restrict__ dA,
+                                                       int32_t lda, float* dH, int32_t ldh, int32_t d, int32_t kind,
+                                                       int32_t aggr, const uint32_t* __restrict__ bits,
+                                                       int32_t bits_ld) {
+  GNNV_PDL_ENTRY();
+  constexpr int RPW = 32 / LPR;
+  static_assert(RPW * U <= 32 && 32 % (RPW * U) == 0, "row groups must tile the warp's 32 rows");
+  const int n_dst = *d_ndst, n_src = *d_nsrc;
+  const int vec = (d + 3) >> 2;
+  const int lane = threadIdx.x & 31, sub = lane / LPR, sl = lane % LPR;
+  const unsigned smask = (LPR == 32) ? 0xffffffffu : (((1u << LPR) - 1u) << (sub * LPR));
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  const int ldh4 = ldh >> 2, lda4 = lda >> 2;
+  const float4* dA4 = reinterpret_cast<const float4*>(dA);
+  float4* dH4 = reinterpret_cast<float4*>(dH);
+  const bool gcn = kind == GNNV_KIND_GCN, mean = aggr == GNNV_AGGR_MEAN;
+  for (int base = warp * 32; base < n_src; base += nwarps * 32) {
+    // lane-parallel row metadata
+    const int mu = base + lane;
+    int mbeg = 0, mcnt = 0, mv = 0;
+    float mw = 0.f;
+    if (mu < n_src) {
+      mbeg = __ldg(colptr + mu);
+      mcnt = __ldg(colptr + mu + 1) - mbeg;
+      if (mcnt) {
+        mv = __ldg(csc + mbeg);
+        mw = pull_weight(indptr, mv, mean, gcn);
+      }
+    }
+    const float mws = (gcn && mu < n_dst) ? pull_weight(indptr, mu, mean, gcn) : 0.f;
+#pragma unroll 1
+    for (int j0 = 0; j0 < 32; j0 += RPW * U) {
+      float4 acc[U][NC];
+      int cnt[U], beg[U];
+#pragma unroll
+      for (int q = 0; q < U; ++q) {
+        const int j = j0 + q * RPW + sub;
+        const int u = base + j;
+        beg[q] = __shfl_sync(0xffffffffu, mbeg, j);
+        cnt[q] = __shfl_sync(0xffffffffu, mcnt, j);
+        const int v = __shfl_sync(0xffffffffu, mv, j);
+        const float w = __shfl_sync(0xffffffffu, mw, j);
+        const float ws = __shfl_sync(0xffffffffu, mws, j);
+#pragma unroll
+        for (int k = 0; k < NC; ++k) {
+          const int c = k * LPR + sl;
+          acc[q][k] = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (u < n_src && c < vec) {
+            if (cnt[q]) acc[q][k] = f4scale(__ldg(dA4 + (int64_t)v * lda4 + c), w);
+            if (gcn && u < n_dst) acc[q][k] = f4add(acc[q][k], f4scale(__ldg(dA4 + (int64_t)u * lda4 + c), ws));
+          }
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < U; ++q) {
+        const int u = base + j0 + q * RPW + sub;
+        if (u >= n_src) continue;  // subgroup-uniform (one row per LPR lanes)
+        // further in-edges (repeated src ids; hubs of the dst prefix collect
+        // hundreds): fetched lane-parallel, broadcast, 4 dA rows in flight
+        for (int e0 = 1; e0 < cnt[q]; e0 += LPR) {
+          int my = 0;
+          float myw = 0.f;
+          if (e0 + sl < cnt[q]) {
+            my = __ldg(csc + beg[q] + e0 + sl);
+            myw = pull_weight(indptr, my, mean, gcn);
+          }
+          const int m = min(LPR, cnt[q] - e0);
+          int jj = 0;
+          for (; jj + 4 <= m; jj += 4) {
+            int v4[4];
+            float w4[4];
+#pragma unroll
+            for (int t = 0; t < 4; ++t) {
+              v4[t] = __shfl_sync(smask, my, jj + t, LPR);
+              w4[t] = __shfl_sync(smask, myw, jj + t, LPR);
+            }
+#pragma unroll
+            for (int k = 0; k < NC; ++k) {
+              const int c = k * LPR + sl;
+              if (c < vec) {
+                float4 a[4];
+#pragma unroll
+                for (int t = 0; t < 4; ++t) a[t] = __ldg(dA4 + (int64_t)v4[t] * lda4 + c);
+#pragma unroll
+                for (int t = 0; t < 4; ++t) acc[q][k] = f4add(acc[q][k], f4scale(a[t], w4[t]));
+              }
+            }
+          }
+          for (; jj < m; ++jj) {
+            const int v = __shfl_sync(smask, my, jj, LPR);
+            const float w = __shfl_sync(smask, myw, jj, LPR);
+#pragma unroll
+            for (int k = 0; k < NC; ++k) {
+              const int c = k * LPR + sl;
+              if (c < vec) acc[q][k] = f4add(acc[q][k], f4scale(__ldg(dA4 + (int64_t)v * lda4 + c), w));
+            }
+          }
+        }
+        const bool keep = !gcn && u < n_dst;  // the dX GEMM wrote dH_dst[u] (masked)
+#pragma unroll
+        for (int k = 0; k < NC; ++k) {
+          const int c = k * LPR + sl;
+          if (c >= ldh4 || (keep && c >= vec)) continue;
+          float4 g = acc[q][k];
+          if (c < vec) {
+            g = mask_tail(g, c, d);
+            if (bits) {
+              const uint32_t m = __ldg(bits + (int64_t)u * bits_ld + (c >> 3)) >> ((c & 7) * 4);
+              g = make_float4(m & 1u ? g.x : 0.f, m & 2u ? g.y : 0.f, m & 4u ? g.z : 0.f, m & 8u ? g.w : 0.f);
+            }
+            if (keep) g = f4add(dH4[(int64_t)u * ldh4 + c], g);
+          }
+          __stcs(dH4 + (int64_t)u * ldh4 + c, g);  // streaming: keep dA in L2; padding columns of whole rows: 0
+        }
+      }
+    }
+  }
+}
+
 static int spmm_grid(int64_t max_rows, int rows_per_warp) {
   const int64_t warps = ceil_div(std::max<int64_t>(max_rows, 1), rows_per_warp);
   return (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(warps, 8), (int64_t)num_sms() * 16));
@@ -218,6 +359,31 @@ void launch_spmm_bwd(const int32_t* d_indptr, const int32_t* d_indices, const ui
     }
     GNNV_CHECK_LAUNCH();
   }
+}
+
+void launch_spmm_bwd_pull(const int32_t* d_colptr, const int32_t* d_csc, const int32_t* d_indptr,
+                          const int32_t* d_ndst, const int32_t* d_nsrc, int64_t max_src, const float* dA, int32_t lda,
+                          float* dH, int32_t ldh, int32_t d, int32_t kind, int32_t aggr, const uint32_t* bits,
+                          int32_t bits_ld, cudaStream_t s) {
+  const int ldh4 = ldh / 4;
+  const int64_t rows = ceil_div(std::max<int64_t>(max_src, 1), 32) * 32;  // a warp per 32 rows
+#define GNNV_PULL(LPR, NC, U)                                                                                     \
+  launch_k(k_spmm_bwd_pull<LPR, NC, U>, spmm_grid(rows, 32), 256, 0, s, d_colptr, d_csc, d_indptr, d_ndst, d_nsrc, \
+           dA, lda, dH, ldh, d, kind, aggr, bits, bits_ld)
+  GNNV_REQUIRE(ldh4 <= kPullMaxLd / 4, GNNV_ERR_UNSUPPORTED, "spmm_bwd_pull: rows wider than 512 floats");
+  if (ldh4 <= 8) {
+    GNNV_PULL(8, 1, 4);
+  } else if (ldh4 <= 16) {
+    GNNV_PULL(16, 1, 4);
+  } else if (ldh4 <= 32) {
+    GNNV_PULL(32, 1, 4);
+  } else if (ldh4 <= 64) {
+    GNNV_PULL(32, 2, 2);
+  } else {
+    GNNV_PULL(32, 4, 1);
+  }
+#undef GNNV_PULL
+  GNNV_CHECK_LAUNCH();
 }
 
 

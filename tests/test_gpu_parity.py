@@ -749,3 +749,40 @@ def test_layer_fwd_cta_pair_gemm(mini, monkeypatch, d_in, d_out):
     Ho, _ = layer_fwd(ob, Hsrc[:, :d_in], W, b, True)
     Hm, _ = layer_fwd(ob, Hsrc[:, :d_in], W, b, True, absval=True)
     assert_close_cond(out["1"], Ho, Hm, RTOL[2], "pair GEMM layer")
+
+
+@pytest.mark.parametrize("kind,prec", [(gnnv.KIND_SAGE, gnnv.PREC_FP32), (gnnv.KIND_GCN, gnnv.PREC_FP32),
+                                       (gnnv.KIND_SAGE, gnnv.PREC_TF32)])
+def test_backward_pull_matches_push(mini, monkeypatch, kind, prec):
+    """The backward aggregation of the layers with a dX (blocks h <= L-2)
+    pulls per src row through the block's CSC (sampler: k_map counts, scan,
+    k_csc_fill; k_spmm_bwd_pull) with GNNV_BWD_PULL=1 (read when the blocks
+    handle is created); the default is the two-pass push (owner stores +
+    atomic adds).
+    Same step, same inputs: losses equal, gradients equal up to the
+    summation order of repeated src ids (fp32) or the tf32 GEMM rounding,
+    and both match the oracle's step (fp32: 1e-4 normwise)."""
+    gd, g = mini
+    cfg = CONFIGS["mini"]
+    dims = [gd.d, cfg["hidden"], cfg["hidden"], gd.C]
+    kname = "sage" if kind == gnnv.KIND_SAGE else "gcn"
+    w = init_weights(dims, kind=kname)
+    seeds = epoch_seeds(gd.n, 0)[: cfg["batch"]]
+    out = {}
+    for name in ("push", "pull"):
+        if name == "pull":
+            monkeypatch.setenv("GNNV_BWD_PULL", "1")
+        tr = gnnv.Trainer(g, gnnv.Cache(g, cfg["ratio"]), dims, cfg["fanouts"], cfg["batch"], w, kind=kind,
+                          prec=prec)
+        tr.timeline(True)
+        loss, _ = tr.step(seeds, len(seeds), len(seeds), 0x5EED, 0.05)
+        out[name] = dict(loss=loss, grads=tr.grads(), segs=tr.timeline_read())
+    p, q = out["pull"], out["push"]
+    assert p["loss"] == q["loss"]  # the forward is untouched
+    tol = 1e-5 if prec == gnnv.PREC_FP32 else 1e-2
+    assert normwise(p["grads"], q["grads"]) < tol
+    if prec == gnnv.PREC_FP32:
+        ref = train_step(gd.indptr, gd.indices, gd.feats, gd.d, gd.labels, seeds, cfg["fanouts"], 0x5EED, w, 0.05,
+                         kind=kname)
+        for (gW, gb), (rW, rb) in zip(gnnv.unflat_params(p["grads"], dims, kind), ref["grads"]):
+            assert normwise(gW, rW) < 1e-4 and normwise(gb, rb) < 1e-4
