@@ -108,9 +108,15 @@ __global__ void __launch_bounds__(256) k_spmm_fwd(const int32_t* __restrict__ in
 // dependent memory round trips per row; here each row costs one, with the
 // three metadata loads of later rows overlapped with it.  Summation order
 // (ascending edges, four loads per add group) is the plain kernel's, so the
-// two are bitwise identical.  GNNV_SPMM_NOPF=1 selects the plain kernel.
+// two are bitwise identical.  Opt-in (GNNV_SPMM_PF=1): measured slower on
+// products layer 1 (338 vs 250 us) -- its 48 registers
+// leave 40 resident warps per SM instead of 64, and the plain kernel's
+// dependent round trips were already hidden by the other warps.
+#ifndef GNNV_PF_MINB
+#define GNNV_PF_MINB 1  // min resident CTAs (A/B builds: 8 forces 32 registers)
+#endif
 template <int LPR, bool IND>
-__global__ void __launch_bounds__(256) k_spmm_fwd_pf(const int32_t* __restrict__ indptr,
+__global__ void __launch_bounds__(256, GNNV_PF_MINB) k_spmm_fwd_pf(const int32_t* __restrict__ indptr,
                                                      const int32_t* __restrict__ indices, const int32_t* d_ndst,
                                                      const float* __restrict__ H, int32_t ldh, float* __restrict__ A,
                                                      int32_t lda, int32_t d, int32_t kind, int32_t aggr,
@@ -427,7 +433,7 @@ void launch_spmm_fwd(const int32_t* d_indptr, const int32_t* d_indices, const in
                      const float* H, int32_t ldh, float* A, int32_t lda, int32_t d, int32_t kind, int32_t aggr,
                      cudaStream_t s, const int32_t* rowidx) {
   const int vec = (d + 3) / 4;
-  const bool plain = getenv("GNNV_SPMM_NOPF") != nullptr;  // read per launch (A/B tests toggle it)
+  const bool plain = getenv("GNNV_SPMM_PF") == nullptr;  // read per launch (A/B tests toggle it)
 #define GNNV_SPMM_FWD(LPR, RPWv)                                                                                  \
   do {                                                                                                            \
     const int grid = spmm_grid(max_dst, RPWv);                                                                    \

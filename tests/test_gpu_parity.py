@@ -792,11 +792,12 @@ def test_backward_pull_matches_push(mini, monkeypatch, kind, prec):
 @pytest.mark.parametrize("ratio", [0.3, 1.0])
 @pytest.mark.parametrize("hidden", [64, 256, 600])
 def test_spmm_fwd_pipelined_matches_plain(mini, monkeypatch, kind, ratio, hidden):
-    """k_spmm_fwd_pf (the default forward aggregation: indptr, neighbour ids
+    """k_spmm_fwd_pf (opt-in GNNV_SPMM_PF=1, read per launch: indptr, neighbour ids
     and cache-row mapping of the rows S, 2S, 3S ahead in flight while the
     current row's neighbour rows load) sums in the plain kernel's order, so a
-    whole fp32 step -- loss, every activation level, every gradient -- is
-    bitwise identical to the step with GNNV_SPMM_NOPF=1 (read per launch).
+    whole fp32 forward -- loss and every activation level -- is bitwise
+    identical to the step with the plain kernel (the default); the gradients
+    agree up to the backward's atomic summation order.
     ratio 1.0 runs layer 1 through the table (rowidx) path, 0.3 through X;
     hidden 64/256/600 covers LPR 16, 32 and rows wider than one warp pass
     (d > 128 floats), and both match the oracle's step."""
@@ -807,9 +808,9 @@ def test_spmm_fwd_pipelined_matches_plain(mini, monkeypatch, kind, ratio, hidden
     w = init_weights(dims, kind=kname)
     seeds = epoch_seeds(gd.n, 0)[: cfg["batch"]]
     out = {}
-    for name in ("pf", "plain"):
-        if name == "plain":
-            monkeypatch.setenv("GNNV_SPMM_NOPF", "1")
+    for name in ("plain", "pf"):
+        if name == "pf":
+            monkeypatch.setenv("GNNV_SPMM_PF", "1")
         tr = gnnv.Trainer(g, gnnv.Cache(g, ratio), dims, cfg["fanouts"], cfg["batch"], w, kind=kind,
                           prec=gnnv.PREC_FP32)
         loss, _ = tr.step(seeds, len(seeds), len(seeds), 0x5EED, 0.05)
@@ -817,13 +818,15 @@ def test_spmm_fwd_pipelined_matches_plain(mini, monkeypatch, kind, ratio, hidden
         acts = []
         for lvl in range(1, len(dims)):
             p, s = tr.activation(lvl)
-            acts.append(read_f32(p, hb[len(dims) - 1 - lvl][0], s)[:, : dims[lvl]].cpu())
+            acts.append(read_f32(p, hb[len(dims) - 1 - lvl][0], s)[:, : dims[lvl]])
         out[name] = dict(loss=loss, grads=tr.grads(), acts=acts)
     p, q = out["pf"], out["plain"]
     assert p["loss"] == q["loss"]
     for a_, b_ in zip(p["acts"], q["acts"]):
-        assert torch.equal(a_, b_)
-    assert np.array_equal(np.asarray(p["grads"]), np.asarray(q["grads"]))
+        assert np.array_equal(a_, b_)
+    # the backward's atomic adds of repeated src ids (k_spmm_bwd phase 2) fix
+    # no summation order, so the gradients agree to fp32 rounding, not bitwise
+    assert normwise(p["grads"], q["grads"]) < 1e-5
     ref = train_step(gd.indptr, gd.indices, gd.feats, gd.d, gd.labels, seeds, cfg["fanouts"], 0x5EED, w, 0.05,
                      kind=kname)
     assert abs(p["loss"] - ref["loss"]) <= 1e-4 * abs(ref["loss"])
