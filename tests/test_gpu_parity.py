@@ -830,4 +830,8 @@ def test_spmm_fwd_pipelined_matches_plain(mini, monkeypatch, kind, ratio, hidden
     ref = train_step(gd.indptr, gd.indices, gd.feats, gd.d, gd.labels, seeds, cfg["fanouts"], 0x5EED, w, 0.05,
                      kind=kname)
     assert abs(p["loss"] - ref["loss"]) <= 1e-4 * abs(ref["loss"])
-    assert normwise(np.asarray(p["grads"]), gnnv.flat_params(ref["grads"])) < 1e-4
+    # the whole-step fp32 bound of test_step_* (1e-4 at hidden 64) scaled by
+    # sqrt(hidden / 64): the forward (2*d_in) and dX (d_out) reduction lengths
+    # grow with the hidden width and fp32 rounding error grows as their sqrt
+    tol = 1e-4 * max(1.0, (hidden / 64) ** 0.5)
+    assert normwise(np.asarray(p["grads"]), gnnv.flat_params(ref["grads"])) < tol
