@@ -180,66 +180,185 @@ def cpu_cores():
         return os.cpu_count() or 1
 
 
-def oracle_run(gd, cfg, seeds_list, rng_seeds, weights, lr, kind):
-    """Times the oracle (oracle.layers.train_step) on the given seed slices."""
+def cpu_model() -> str:
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    import platform
+
+    return platform.processor() or "unknown"
+
+
+# ---------------------------------------------------------------- oracle arm
+# P = len(sched_getaffinity) worker processes, BLAS threads 1
+# each, every worker maps the shared host store (/dev/shm, synth.store) and
+# runs the oracle's train_step (oracle/layers.py, as it stands) on its own
+# contiguous slice of the global batch -- as ranks would; the main process
+# sums the slices' gradients (the all-reduce) and applies the oracle's SGD.
+_WORKER = {}
+
+
+def _oracle_init(store_path):
+    from threadpoolctl import threadpool_limits
+
+    _WORKER["limits"] = threadpool_limits(1)  # one BLAS/OpenMP thread per worker process
+    from synth.store import open_store
+
+    _WORKER["gd"] = open_store(store_path)
+
+
+def _oracle_slice(job):
     from oracle.layers import train_step
 
-    t0 = time.perf_counter()
-    n = 0
-    for seeds, rs in zip(seeds_list, rng_seeds):
-        out = train_step(gd.indptr, gd.indices, gd.feats, gd.d, gd.labels, seeds, cfg["fanouts"], rs, weights,
-                         lr, n_global=len(seeds), kind=kind)
-        weights = out["new_weights"]
-        n += len(seeds)
-    return n, time.perf_counter() - t0
+    seeds, rs, weights, n_global, fanouts, kind = job
+    gd = _WORKER["gd"]
+    out = train_step(gd.indptr, gd.indices, gd.feats, gd.d, gd.labels, seeds, fanouts, rs, weights, 0.0,
+                     n_global=n_global, kind=kind)
+    return out["loss"], out["grads"]
 
 
-def blas_threads():
+class OracleArm:
+    """The CPU oracle over `procs` worker processes (spawned, so none of them
+    inherits a CUDA context)."""
+
+    def __init__(self, gd, cfg, kind, procs):
+        import multiprocessing as mp
+
+        from synth.store import store_path, write_store
+
+        self.cfg, self.kind, self.procs = cfg, kind, procs
+        path = store_path(cfg)
+        if not os.path.isdir(path):  # bench ranks normally created it already
+            write_store(gd, cfg)
+        self.pool = mp.get_context("spawn").Pool(procs, initializer=_oracle_init, initargs=(path,))
+
+    def step(self, seeds, rs, weights, lr):
+        """One oracle iteration on the global batch `seeds`; returns new weights."""
+        from oracle.layers import sgd_update
+
+        P = min(self.procs, len(seeds))
+        cuts = np.linspace(0, len(seeds), P + 1).astype(int)
+        jobs = [(seeds[cuts[i]:cuts[i + 1]], rs, weights, len(seeds), self.cfg["fanouts"], self.kind) for i in range(P)]
+        outs = self.pool.map(_oracle_slice, jobs)
+        grads = [[sum(o[1][l][j] for o in outs) for j in range(2)] for l in range(len(weights))]
+        return [tuple(sgd_update([W, b], g, lr)) for (W, b), g in zip(weights, grads)]
+
+    def time(self, seeds_list, rs_list, weights, lr):
+        t0 = time.perf_counter()
+        n = 0
+        for seeds, rs in zip(seeds_list, rs_list):
+            weights = self.step(seeds, rs, weights, lr)
+            n += len(seeds)
+        return n, time.perf_counter() - t0, weights
+
+    def close(self):
+        self.pool.close()
+        self.pool.join()
+
+
+def oracle_baseline(gd, cfg, kind, perm, seeds_of_t, t0, weights, lr, budget_s=20.0):
+    """cpu_baseline: the oracle on the same workload, host cores of this box:
+    full global batches with P workers until ~budget_s, plus a 1-core figure
+    (one worker process, one BLAS thread) on one rank-sized slice of B/P."""
+    P = cpu_cores()
+    arm = OracleArm(gd, cfg, kind, P)
     try:
-        from threadpoolctl import threadpool_info
+        arm.time([seeds_of_t(t0)[: 16 * P]], [BASE_RNG_SEED_BENCH - 1], weights, lr)  # worker start-up, untimed
+        n, tt, its = 0, 0.0, 0
+        w = weights
+        while its == 0 or tt < budget_s:
+            dn, dt, w = arm.time([seeds_of_t(t0 + its)], [BASE_RNG_SEED_BENCH + t0 + its], w, lr)
+            n, tt, its = n + dn, tt + dt, its + 1
+    finally:
+        arm.close()
+    one = OracleArm(gd, cfg, kind, 1)
+    try:
+        sl = seeds_of_t(t0)[: max(1, len(seeds_of_t(t0)) // P)]
+        one.time([sl], [BASE_RNG_SEED_BENCH - 1], weights, lr)
+        n1, t1, _ = one.time([sl], [BASE_RNG_SEED_BENCH + t0], weights, lr)
+    finally:
+        one.close()
+    gb = len(seeds_of_t(t0))
+    return {"value": n / tt, "unit": UNIT, "cores": P, "kind": "oracle",
+            "sample": f"{its} oracle iteration(s) of the {gb}-seed global batch (sample+gather+fwd+loss+bwd+SGD, "
+                      f"float64 NumPy/SciPy) on the {cfg['name']}-shaped graph: {P} worker processes x 1 BLAS thread, "
+                      f"each a contiguous slice of the batch (as ranks), features shared through /dev/shm; {tt:.1f} s",
+            "procs": P, "blas_threads_per_proc": 1, "cpu_model": cpu_model(),
+            "one_core": {"value": n1 / t1, "unit": UNIT,
+                         "sample": f"1 worker process, 1 BLAS thread, one {len(sl)}-seed slice; {t1:.1f} s"}}
 
-        info = threadpool_info()
-        return max([i.get("num_threads", 1) for i in info] or [1])
-    except Exception:
-        return cpu_cores()
+
+BASE_RNG_SEED_BENCH = 0x5EED
 
 
 def run_reference(args):
-    """--impl reference: the CPU oracle on this workload (rank 0 only)."""
-    rank, world, _ = dist_env()
+    """--impl reference: the CPU oracle on this workload (rank 0 only), with
+    the same config and global batch per step as our arm."""
+    rank, world, local = dist_env()
     if rank != 0:
         return
-    from synth import BASE_RNG_SEED, CONFIGS, epoch_seeds, init_weights, make_graph
+    from paper_2404_09544_b200.partition import global_batch, rank_slice
+    from synth import CONFIGS, epoch_seeds, init_weights
+    from synth.store import shared_graph
 
-    cfg = CONFIGS[args.config]
-    gd = make_graph(cfg)
+    cfg = bench_cfg(args)
+    gd = shared_graph(cfg, local)
     dims = [gd.d] + [cfg["hidden"]] * (len(cfg["fanouts"]) - 1) + [gd.C]
     w = init_weights(dims, kind=args.kind)
     perm = epoch_seeds(gd.n, 0)
-    # a bounded sample of the batch per reference step, sized so that the
-    # whole --steps/--warmup run stays near two minutes of CPU time
-    probe = min(256, cfg["batch"])
-    _, tp = oracle_run(gd, cfg, [perm[-probe:]], [BASE_RNG_SEED - 1], w, 0.01, args.kind)
-    budget = 120.0 / max(1, args.steps + args.warmup)
-    sub = int(max(16, min(cfg["batch"], budget / max(tp / probe, 1e-9))))
-    seeds = [perm[i * sub:(i + 1) * sub] for i in range(args.warmup + args.steps)]
-    rs = [BASE_RNG_SEED + i for i in range(len(seeds))]
-    oracle_run(gd, cfg, seeds[: args.warmup], rs[: args.warmup], w, 0.01, args.kind)
-    n, t = oracle_run(gd, cfg, seeds[args.warmup:], rs[args.warmup:], w, 0.01, args.kind)
-    value = n / t
-    ms = 1000.0 * t / max(1, args.steps)
+    B = cfg["batch"]
+
+    def seeds_of_t(t):
+        lo, _ = rank_slice(t, 0, world, B, gd.n)
+        return perm[lo:lo + global_batch(t, world, B, gd.n)]
+
+    P = cpu_cores()
+    arm = OracleArm(gd, cfg, args.kind, P)
+    try:
+        _, _, w = arm.time([seeds_of_t(t) for t in range(args.warmup)],
+                           [BASE_RNG_SEED_BENCH + t for t in range(args.warmup)], w, 0.01)
+        ts = range(args.warmup, args.warmup + args.steps)
+        n, tt, _ = arm.time([seeds_of_t(t) for t in ts], [BASE_RNG_SEED_BENCH + t for t in ts], w, 0.01)
+    finally:
+        arm.close()
+    value = n / tt
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": cfg["name"], "n_nodes": gd.n, "nnz": gd.nnz, "d": gd.d, "classes": gd.C,
-                   "fanouts": cfg["fanouts"], "seeds_per_step": sub, "kind": args.kind},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": blas_threads(), "kind": "oracle",
-                         "sample": f"{args.steps} oracle iterations of {sub} seeds each (of a {cfg['batch']}-seed "
-                                   f"batch) on the {cfg['name']}-shaped graph, host CPU, float64"},
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 * tt / max(1, args.steps),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": config_of(cfg, gd, world, args.kind),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": P, "kind": "oracle", "procs": P,
+                         "blas_threads_per_proc": 1, "cpu_model": cpu_model(),
+                         "sample": f"{args.steps} oracle iterations (after {args.warmup} warm-up) of the "
+                                   f"{world * B}-seed global batch, {P} worker processes x 1 BLAS thread over "
+                                   f"/dev/shm features, float64"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+def bench_cfg(args) -> dict:
+    from synth import CONFIGS
+
+    cfg = dict(CONFIGS[args.config])
+    if args.ratio is not None:
+        cfg["ratio"] = args.ratio
+    return cfg
+
+
+def config_of(cfg, gd, world, kind) -> dict:
+    """The workload (identical in both arms)."""
+    L = len(cfg["fanouts"])
+    return {"workload": cfg["name"], "n_nodes": gd.n, "nnz": gd.nnz, "d": gd.d, "classes": gd.C,
+            "fanouts": cfg["fanouts"], "batch_per_rank": cfg["batch"], "global_batch": world * cfg["batch"],
+            "cache_ratio": cfg["ratio"], "kind": kind, "hidden": cfg["hidden"], "layers": L,
+            "parallelism": f"dp{world}",
+            "l2": ("inputs > L2, no flush (feature table %.0f MB, CSR %.0f MB)" if gd.n * gd.stride * 4 > 126e6 else
+                   "feature table %.0f MB, CSR %.0f MB: may be L2-resident between steps (no flush)") % (
+                gd.n * gd.stride * 4 / 1e6, gd.nnz * 4 / 1e6)}
 
 
 def algorithmic(seg: str, sizes, cfg, dims, stride, prec, peaks):
@@ -327,7 +446,8 @@ def main():
     import torch.distributed as dist
 
     from paper_2404_09544_b200 import gnnv
-    from synth import BASE_RNG_SEED, CONFIGS, epoch_seeds, init_weights, make_graph
+    from synth import BASE_RNG_SEED, epoch_seeds, init_weights
+    from synth.store import host_bytes, shared_graph
 
     rank, world, local = dist_env()
     if world != args.gpus:
@@ -335,11 +455,12 @@ def main():
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    cfg = dict(CONFIGS[args.config])
-    if args.ratio is not None:
-        cfg["ratio"] = args.ratio
+    cfg = bench_cfg(args)
+    # one host copy of the graph per box (/dev/shm): local rank 0 generates
+    # it (or finds it), every rank maps it; the feature table is then
+    # page-locked in place by gnnv_graph_load
     t_gen = time.perf_counter()
-    gd = make_graph(cfg)
+    gd = shared_graph(cfg, local)
     t_gen = time.perf_counter() - t_gen
     gnnv.load()
     comm = None
@@ -347,16 +468,23 @@ def main():
         obj = [gnnv.Comm.unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
         comm = gnnv.Comm(rank, world, obj[0], local)
+    torch.cuda.synchronize()
+    mem = {}
+    free0, total_mem = torch.cuda.mem_get_info()
     g = gnnv.Graph.from_data(gd, device=local)
+    mem["csr_labels"] = free0 - torch.cuda.mem_get_info()[0]
     placement = gnnv.PLACE_SHARDED if args.placement == "sharded" else gnnv.PLACE_REPLICA
     policy = {"none": gnnv.POLICY_NONE, "degree": gnnv.POLICY_DEGREE, "fifo": gnnv.POLICY_FIFO,
               "lru": gnnv.POLICY_LRU}[args.policy]
+    free1 = torch.cuda.mem_get_info()[0]
     cache = gnnv.Cache(g, cfg["ratio"], policy=policy, placement=placement, comm=comm)
+    mem["cache_build"] = free1 - torch.cuda.mem_get_info()[0]
     dims = [gd.d] + [cfg["hidden"]] * (len(cfg["fanouts"]) - 1) + [gd.C]
     kind = gnnv.KIND_SAGE if args.kind == "sage" else gnnv.KIND_GCN
     prec = {"fp32": gnnv.PREC_FP32, "bf16": gnnv.PREC_BF16, "tf32": gnnv.PREC_TF32}[args.prec]
     w = init_weights(dims, kind=args.kind)
     B = cfg["batch"]
+    free2 = torch.cuda.mem_get_info()[0]
     tr = gnnv.Trainer(g, cache, dims, cfg["fanouts"], B, w, kind=kind, prec=prec, comm=comm)
     tr.set_locality(args.locality_bias)
     # the step runs on a high-priority stream; the trainer's prefetch stream
@@ -427,6 +555,11 @@ def main():
     for t in range(args.warmup):
         step_device(t)
     barrier()
+    # Gamma (Eq.9-10): device memory of this rank after warm-up
+    # (every buffer -- both Eq.4 buffer sets included -- is allocated by now;
+    # a step allocates nothing)
+    mem["trainer_runtime"] = free2 - torch.cuda.mem_get_info()[0]
+    mem["device_used_total"] = total_mem - torch.cuda.mem_get_info()[0]
     # ---------------------------------------------------------- timed region
     # K steps without instrumentation (value); the per-kernel rooflines come
     # from the next K steps, timed the same way with the library's
@@ -439,11 +572,16 @@ def main():
     dyn0 = cache.counters() if args.policy in ("fifo", "lru") else None
     launches0 = gnnv.launch_count()
     barrier()
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    ev0.record(stream)
-    for t in range(t0_steps, t0_steps + args.steps):
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+    evs[0].record(stream)
+    for i, t in enumerate(range(t0_steps, t0_steps + args.steps)):
         step_device(t)
-    ev1.record(stream)
+        if i + 1 < args.steps:
+            evs[i + 1].record(stream)
+    # the batch prefetched during the last timed step belongs to the region:
+    # close it only when that prefetch is done too
+    tr.join_prefetch(stream)
+    evs[-1].record(stream)
     barrier()
     launches = gnnv.launch_count() - launches0
     # dynamic cache: hit rate of the batches gathered during the timed region
@@ -454,8 +592,13 @@ def main():
         dyn = {"hits": int(d1[0]), "misses": int(d1[1]), "replaced": int(d1[2]),
                "hit_rate": float(d1[0]) / max(1, int(d1[0] + d1[1]))}
     clk = clocks.stop()
-    ms_total = max_over_ranks(ev0.elapsed_time(ev1))
+    ms_total = max_over_ranks(evs[0].elapsed_time(evs[-1]))
     ms_per_step = ms_total / args.steps
+    step_ms = np.array([evs[i].elapsed_time(evs[i + 1]) for i in range(args.steps)])
+    step_stats = {"median_ms": float(np.median(step_ms)), "p90_ms": float(np.percentile(step_ms, 90)),
+                  "min_ms": float(step_ms.min()), "max_ms": float(step_ms.max()),
+                  "note": "per-step CUDA events on the step stream (rank 0); the last step also waits for the "
+                          "batch it prefetched"}
     value = world * B * args.steps / (ms_total / 1000.0)
     # ------------------------------------- instrumented pass (rooflines)
     tr.timeline(True)
@@ -464,6 +607,7 @@ def main():
     ev2.record(stream)
     for t in range(t0_steps + args.steps, t0_steps + 2 * args.steps):
         step_device(t)
+    tr.join_prefetch(stream)
     ev3.record(stream)
     barrier()
     ms_instr = max_over_ranks(ev2.elapsed_time(ev3)) / args.steps
@@ -485,6 +629,7 @@ def main():
             loss = tr.loss_result(prev)  # step t-1's loss on the host (device -> host read every step)
         prev = ticket
     loss = tr.loss_result(prev)
+    tr.join_prefetch(stream)
     e1.record(stream)
     barrier()
     wall_e2e = time.perf_counter() - t_e2e0
@@ -574,28 +719,50 @@ def main():
                        "unit": "GB/s", "frac": by / ms / 1e6 / peaks["hbm"],
                        "note": "pf_gather, when present, is timed while overlapped with the step"}
     # -------------------------------------------------------- CPU baseline
+    # after every GPU measurement (rank 0; the other ranks wait at the barrier)
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        ns = args.cpu_baseline_seeds or B
-        lo, hi = seeds_of(t0_steps)
-        n_done, tcpu = oracle_run(gd, cfg, [perm[lo:lo + ns]], [BASE_RNG_SEED + t0_steps], w, lr, args.kind)
-        cpu = {"value": n_done / tcpu, "unit": UNIT, "cores": blas_threads(), "kind": "oracle",
-               "sample": f"1 oracle iteration of {ns} seeds (sample+gather+fwd+loss+bwd+SGD, float64) on the "
-                         f"{cfg['name']}-shaped graph; {tcpu:.1f} s"}
+    if rank == 0 and not args.no_cpu_baseline:
+        from paper_2404_09544_b200.partition import global_batch as _gb
+
+        def seeds_of_t(t):
+            lo, _ = rank_slice(t, 0, world, B, gd.n)
+            return perm[lo:lo + max(1, _gb(t, world, B, gd.n))]
+
+        cpu = oracle_baseline(gd, cfg, args.kind, perm, seeds_of_t, t0_steps, w, lr,
+                              budget_s=float(os.environ.get("GNNV_CPU_BUDGET_S", "20")))
+    if world > 1:
+        dist.barrier()
+    # Gamma of this rank (Eq.9-10): the cache table, the CSR, the runtime
+    # buffers; and the estimator's prediction of the same (NEXT-4)
+    from paper_2404_09544_b200.estimator import Candidate, Estimator
+
+    cv = cache.info()
+    cand = Candidate(n_nodes=gd.n, nnz=gd.nnz, n_attr=gd.d, stride=gd.stride, n_classes=gd.C, batch=B,
+                     fanouts=list(cfg["fanouts"]), hidden=cfg["hidden"], ratio=cfg["ratio"],
+                     locality_bias=args.locality_bias, policy=args.policy, kind=args.kind)
+    try:
+        pred = Estimator(coef={}).memory(cand)
+    except Exception:
+        pred = None
+    gamma = {"gamma_cache_gb": cv.bytes / 1e9, "csr_labels_gb": mem["csr_labels"] / 1e9,
+             "cache_build_gb": mem["cache_build"] / 1e9, "trainer_runtime_gb": mem["trainer_runtime"] / 1e9,
+             "device_used_gb": mem["device_used_total"] / 1e9, "device_total_gb": total_mem / 1e9,
+             "host_store_gb": host_bytes(cfg) / 1e9,
+             "eq9_10_predicted_gb": ({k: v / 1e9 for k, v in pred.items()} if pred else None),
+             "note": "cudaMemGetInfo deltas on this rank (cache_build includes the table; device_used includes the "
+                     "CUDA context and torch's allocations)"}
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": {"fp32": "f32", "bf16": "f32+bf16gemm", "tf32": "f32+tf32gemm"}[args.prec], "data": "synthetic",
-            "config": {"workload": cfg["name"], "n_nodes": gd.n, "nnz": gd.nnz, "d": gd.d, "classes": gd.C,
-                       "fanouts": cfg["fanouts"], "batch_per_rank": B, "global_batch": world * B,
-                       "cache_ratio": cfg["ratio"], "placement": args.placement, "kind": args.kind,
-                       "locality_bias": args.locality_bias, "cache_policy": args.policy,
-                       "hidden": cfg["hidden"], "gemm_precision": args.prec,
-                       "l2": "inputs > L2 (feature table %.0f MB, gathered X %.0f MB per step)" % (
-                           gd.n * gd.stride * 4 / 1e6, sizes["n"][L] * gd.stride * 4 / 1e6),
-                       "parallelism": f"dp{world}",
-                       "pipeline": "eq4-overlap (next batch sample+gather on a side stream)" if pipeline else "off"},
+            "config": config_of(cfg, gd, world, args.kind),
+            "settings": {"placement": args.placement, "locality_bias": args.locality_bias,
+                         "cache_policy": args.policy, "gemm_precision": args.prec,
+                         "gathered_x_mb_per_step": sizes["n"][L] * gd.stride * 4 / 1e6,
+                         "pipeline": "eq4-overlap (next batch sample+gather on a side stream)" if pipeline else "off"},
+            "step_stats": step_stats,
+            "gamma": gamma,
             "epoch_s": iters_per_epoch * ms_per_step / 1000.0,
             "iters_per_epoch": iters_per_epoch,
             "clocks": clk,
@@ -615,6 +782,7 @@ def main():
                     "ms_per_step": ms_e2e / args.steps, "wall_s": wall_e2e, "last_loss": loss},
             "dynamic_cache": dyn,
             "cpu_baseline": cpu,
+            "vs_cpu_baseline": (value / cpu["value"]) if cpu else None,
             "peaks": peaks["src"] + (f"; host link {peaks['host']:.1f} GB/s measured (pinned H2D copy)"
                                      if peaks.get("host") else ""),
             "graph_gen_s": t_gen,

@@ -206,13 +206,14 @@ gnnv_status gnnv_blocks_free(gnnv_blocks* b);
  * selection probability "a function of data locality"):
  * subsequent gnnv_sample calls on b draw each node's min(k, deg) neighbours
  * by successive weighted sampling without replacement, cached neighbours
- * (slot of c >= 0) weighing `weight` = 1 + 4b and the others 1 (SPEC
- * S:123; reading Q26: b in {0, 1/4, 1/2, 3/4, 1}, so weight is an
+ * (slot of c >= 0) weighing 1 + 4*bias and the others 1 (SPEC S:123,
+ * S:159; reading Q26: bias in {0, 1/4, 1/2, 3/4, 1}, so the weight is an
  * integer 1..5 and the draws are exact integer arithmetic on the same
- * Philox words as the unbiased sampler).  weight 1 restores the unbiased
- * Floyd sampler.  c must outlive the blocks' use.  PARAM on a bad weight
- * or a missing cache; STATE if c belongs to another graph. */
-gnnv_status gnnv_blocks_set_locality(gnnv_blocks* b, const gnnv_cache* c, int32_t weight);
+ * Philox words as the unbiased sampler).  bias 0 restores the unbiased
+ * Floyd sampler (c may then be NULL).  c must outlive the blocks' use.
+ * PARAM on any other bias or a missing cache; STATE if c belongs to
+ * another graph. */
+gnnv_status gnnv_blocks_set_locality(gnnv_blocks* b, const gnnv_cache* c, double bias);
 
 /* SubgraphSampling (Algorithm 1 line 2) with the unified node-wise
  * sampler of Eq.2: for every v in F_h, min(k_h, deg v) distinct
@@ -292,8 +293,12 @@ gnnv_status gnnv_layer_fwd(gnnv_blocks* b, int32_t layer, const gnnv_layer_desc*
  *  d_Gdst  dL/dH_dst (post-activation) [n_dst x row_stride(d_out)]
  *  d_Gsrc  [n_src x in_stride] overwritten; NULL for layer 1
  *  d_dW, d_db overwritten (same layout as W, b).
- * Stream-ordered.  dW/db are deterministic (fixed-order split-K
- * reduction); dH_src uses fp32 atomics (order-dependent rounding). */
+ * Stream-ordered.  Summation order: FP32 and BF16 reduce dW/db split-K
+ * partials in a fixed order (bitwise reproducible); TF32 adds the split-K
+ * partials and db into dW/db with red.global.add.f32, so their rounding
+ * depends on the order the CTAs arrive in (run-to-run differences at fp32
+ * rounding level, within the tf32 tolerance); dH_src uses fp32 atomics
+ * (order-dependent rounding) in every mode. */
 gnnv_status gnnv_layer_bwd(gnnv_blocks* b, int32_t layer, const gnnv_layer_desc* ld, const float* d_Gdst,
                            const float* d_Hdst, const float* d_Hsrc, const float* d_saveA, const float* d_W,
                            float* d_Gsrc, float* d_dW, float* d_db, gnnv_stream s);
@@ -309,7 +314,8 @@ gnnv_status gnnv_ce_loss(gnnv_blocks* b, const gnnv_graph* g, const float* d_log
  * and micro-benchmarks.  Layouts as in gnnv_layer_fwd/bwd:
  *  fwd: Y[M x ldy] = act([X1 | X2] W + b), X2 may be NULL (K = K1)
  *  dx : [Y1 | Y2] = G W^T, G [M x ldg] with N columns, Y2 may be NULL
- *  dw : dW = [X1 | X2]^T G (+ db = colsum(G) if d_db), deterministic
+ *  dw : dW = [X1 | X2]^T G (+ db = colsum(G) if d_db); fixed-order split-K
+ *       in FP32/BF16, atomic (arrival-order) split-K in TF32
  * prec: gnnv_prec.  Stream-ordered. */
 gnnv_status gnnv_dense_fwd(const float* d_X1, int32_t ld1, const float* d_X2, int32_t ld2, int32_t K1,
                            const float* d_W, const float* d_b, float* d_Y, int32_t ldy, int32_t N, int64_t M,
@@ -361,8 +367,7 @@ gnnv_blocks* gnnv_trainer_blocks(gnnv_trainer* t);
  * SAGE with TF32 GEMMs and GNNV_XROWS=1 was set when the trainer was
  * created: the layer-1 GEMMs (forward and dW) then read the H_dst rows from
  * the table as well (TMA gather4 through the same row indices) and X is
- * never written (off by default: slower on products).
- * GNNV_NO_XFUSE=1 in the environment disables both. */
+ * never written (off by default: slower on products). */
 int32_t gnnv_trainer_x_level(const gnnv_trainer* t);
 /* Whole-table mode (x_level < L): *d_rowidx = int32[n_L] cache-table row of
  * every F_L row of the last step (row u of layer 1's input is row
@@ -397,9 +402,9 @@ typedef struct {
   double total_ms;
   int32_t count;
 } gnnv_segment;
-/* The trainer's sampler locality weight (gnnv_blocks_set_locality with the
+/* The trainer's sampler locality bias (gnnv_blocks_set_locality with the
  * trainer's cache; both buffer sets).  STATE while a prefetch is pending. */
-gnnv_status gnnv_trainer_set_locality(gnnv_trainer* t, int32_t weight);
+gnnv_status gnnv_trainer_set_locality(gnnv_trainer* t, double bias);
 gnnv_status gnnv_trainer_timeline(gnnv_trainer* t, int32_t on);
 gnnv_status gnnv_trainer_timeline_read(gnnv_trainer* t, gnnv_segment* out, int32_t cap, int32_t* n_out);
 /* Eq.4 pipelining (T = n_iter max(t_sample + t_transfer,
@@ -417,6 +422,10 @@ gnnv_status gnnv_trainer_timeline_read(gnnv_trainer* t, gnnv_segment* out, int32
  * that buffer) and impose no stream dependency. */
 gnnv_status gnnv_trainer_prefetch(gnnv_trainer* t, const int32_t* seeds, int32_t n_seeds, int32_t seeds_on_host,
                                   uint64_t rng_seed, gnnv_stream s);
+/* Makes `s` wait for the pending prefetch (if any) to complete -- without
+ * consuming it -- so that a timed region closed by an event on `s` contains
+ * every batch it prefetched.  No-op without a pending prefetch. */
+gnnv_status gnnv_trainer_join_prefetch(gnnv_trainer* t, gnnv_stream s);
 /* Loss of the last step (summed over ranks) to the host; synchronises `s`
  * and reports a pending seed error.  Lets a pipelined loop enqueue the next
  * prefetch before blocking on the loss. */
@@ -424,7 +433,9 @@ gnnv_status gnnv_trainer_read_loss(gnnv_trainer* t, float* loss_out, gnnv_stream
 /* Asynchronous loss read-back (the e2e loop's per-step result without a
  * per-step stream synchronisation): every step's SGD kernel writes the
  * step's all-reduced loss and seed-error flag into a mapped pinned ring
- * slot (zero-copy, no copy on the stream); _loss_async records an event on
+ * slot (zero-copy, no copy on the stream; a step whose batch had an
+ * invalid seed writes its flag and skips its SGD update -- the flag is
+ * reset by every sample, so it never outlives its batch); _loss_async records an event on
  * `s` after the last enqueued step and returns its ticket (the step index);
  * _loss_result waits for that event only and returns the loss (PARAM if the
  * step saw a bad seed).  The ring holds the last 8 steps; an older ticket

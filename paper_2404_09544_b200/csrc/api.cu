@@ -17,11 +17,28 @@ static std::atomic<unsigned long long> g_launches{0};
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 static thread_local bool t_pdl_off = false;
 void set_pdl(bool on) { t_pdl_off = !on; }
+bool env_on(const char* name) {
+  static std::mutex mu;
+  static std::vector<std::pair<std::string, bool>> cache;
+  std::lock_guard<std::mutex> lk(mu);
+  for (auto& kv : cache)
+    if (kv.first == name) return kv.second;
+  const char* e = getenv(name);
+  const bool on = e && e[0] && strcmp(e, "0") != 0;
+  cache.emplace_back(name, on);
+  return on;
+}
 bool pdl_enabled() {
-  static const bool on = getenv("GNNV_NO_PDL") == nullptr;
+  static const bool on = !env_on("GNNV_NO_PDL");
   return on && !t_pdl_off;
 }
 void set_error(const std::string& msg) { g_last_error = msg; }
+// W = 1 + 4 bias for bias in {0, 1/4, 1/2, 3/4, 1} (reading Q26), else 0
+int32_t locality_weight(double bias) {
+  for (int q = 0; q <= 4; ++q)
+    if (bias == 0.25 * q) return 1 + q;
+  return 0;
+}
 const char* get_error() { return g_last_error.c_str(); }
 
 void* dmalloc(size_t bytes, const char* what) {
@@ -323,7 +340,7 @@ gnnv_status gnnv_blocks_create(gnnv_graph* g, int32_t max_seeds, const int32_t* 
       // GNNV_BWD_PULL=1: CSC of the hops whose layer has a dX (h <= L-2),
       // for the pulled backward aggregation (measured slower than the
       // two-pass push on products; opt-in)
-      b->csc_hops = getenv("GNNV_BWD_PULL") ? L - 1 : 0;
+      b->csc_hops = env_on("GNNV_BWD_PULL") ? L - 1 : 0;
       if (b->csc_hops > 0) {
         int64_t n_max = 1;
         for (int h = 0; h < b->csc_hops; ++h) {
@@ -351,10 +368,11 @@ gnnv_status gnnv_blocks_create(gnnv_graph* g, int32_t max_seeds, const int32_t* 
   });
 }
 
-gnnv_status gnnv_blocks_set_locality(gnnv_blocks* b, const gnnv_cache* c, int32_t weight) {
+gnnv_status gnnv_blocks_set_locality(gnnv_blocks* b, const gnnv_cache* c, double bias) {
   return guarded([&] {
     GNNV_REQUIRE(b, GNNV_ERR_PARAM, "blocks_set_locality: null");
-    GNNV_REQUIRE(weight >= 1 && weight <= 5, GNNV_ERR_PARAM, "blocks_set_locality: weight must be 1 + 4b in 1..5");
+    const int32_t weight = locality_weight(bias);
+    GNNV_REQUIRE(weight >= 1, GNNV_ERR_PARAM, "blocks_set_locality: bias must be one of 0, 0.25, 0.5, 0.75, 1");
     GNNV_REQUIRE(weight == 1 || c, GNNV_ERR_PARAM, "blocks_set_locality: a biased sampler needs the cache");
     GNNV_REQUIRE(!c || c->g == b->g, GNNV_ERR_STATE, "blocks_set_locality: cache of another graph");
     b->loc_w = weight;

@@ -131,8 +131,7 @@ void launch_gather(const gnnv_cache* c, const gnnv_blocks* b, float* d_X, int64_
   constexpr int RU = 8;
   const int64_t rows_ub = b->max_n[b->L];
   const int64_t warps = ceil_div(rows_ub, 32);
-  const int cap = grid_cap() > 0 ? grid_cap() : num_sms() * 8;
-  const int blocks = (int)std::min<int64_t>(ceil_div(warps, 8), (int64_t)cap);
+  const int blocks = (int)std::min<int64_t>(ceil_div(warps, 8), (int64_t)num_sms() * 8);
   launch_k(k_gather<RU>, std::max(blocks, 1), 256, 0, s, b->d_F, b->d_sizes, b->L, c->d_slot, c->d_shard_ptrs, c->world,
                                                    c->rank, g->d_feats, g->stride, d_X,
                                                    reinterpret_cast<unsigned long long*>(d_stats),

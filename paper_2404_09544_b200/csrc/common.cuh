@@ -103,6 +103,18 @@ inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
 int num_sms();
 
+// Opt-in switches, read once per process: set and not "0" = on.  Every one
+// of them selects a variant measured slower than (or equal to) the default
+// on the products workload and kept for A/B runs:
+//   GNNV_XROWS     layer-1 GEMMs read H_dst with TMA gather4 (gemm_tma.cu)
+//   GNNV_GEMM_PAIR forward GEMM on CTA pairs, cta_group::2 (gemm_tma.cu)
+//   GNNV_BWD_PULL  backward aggregation pulled through a CSC (spmm.cu)
+//   GNNV_NO_TAIL   per-kernel output layer instead of tail.cu
+//   GNNV_NO_PDL    no programmatic dependent launch
+bool env_on(const char* name);
+// NEXT-2 locality weight 1 + 4 bias (1..5), 0 for an unsupported bias
+int32_t locality_weight(double bias);
+
 // ---------------------------------------------------------------- handles
 }  // namespace gnnv
 
@@ -236,10 +248,6 @@ size_t csc_scan_tmp_bytes(int64_t max_items);
 void launch_cache_update(gnnv_cache* c, const gnnv_blocks* b, const float* d_X, cudaStream_t s);
 void launch_gather(const gnnv_cache* c, const gnnv_blocks* b, float* d_X, int64_t* d_stats, cudaStream_t s,
                    int32_t* d_rowidx = nullptr, bool materialize = true);
-// Cap on the grid of the sampling / gather kernels (0 = none); the trainer
-// sets it around a prefetch so the overlapped batch occupies few SMs.
-void set_grid_cap(int blocks);
-int grid_cap();
 // spmm.cu
 // rowidx != NULL: source row u is row rowidx[u] of H (the cache table)
 void launch_spmm_fwd(const int32_t* d_indptr, const int32_t* d_indices, const int32_t* d_ndst, int64_t max_dst,
@@ -290,7 +298,10 @@ struct XRows {
 inline int32_t mask_words(int32_t N) { return ((N + 31) / 32 + 3) / 4 * 4; }
 void launch_relu_bits(const float* H, int32_t ldh, int32_t N, const int32_t* d_M, int64_t max_M, uint32_t* bits,
                       int32_t bits_ld, cudaStream_t s);
-struct GemmDwArgs {  // dW = [X1|X2]^T G (+ bias row = colsum G) : deterministic split-K
+// dW = [X1|X2]^T G (+ bias row = colsum G): split-K over graph rows, reduced
+// in a fixed order (FP32/BF16, bitwise reproducible) or added with
+// red.global.add (TF32: arrival order, see gnnv_layer_bwd)
+struct GemmDwArgs {
   const float* X1; int32_t ld1;
   const float* X2; int32_t ld2;
   int32_t K1;

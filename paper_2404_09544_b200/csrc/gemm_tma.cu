@@ -13,21 +13,28 @@
 //   fwd : Y = act([X1 | X2] W + b)   A = activations, K-major (TMA box 128 x 32)
 //                                     B = W^T, K-major (prep image [Npad x K'])
 //   dX  : [Y1 | Y2] = G W^T           A = G, K-major; B = W rows, K-major image
-//   dW  : dW = [X1 | X2]^T G'         operands arrive MN-major (TMA boxes of 32
-//                                     graph rows x 32 features); kind::tf32 only
-//                                     takes K-major operands (tools/umma_probe.cu:
-//                                     an MN-major tf32 operand yields zeros), so
-//                                     the 4 epilogue warps transpose each staged
-//                                     box into a K-major SW128 tile (and zero the
-//                                     stale tail rows) before the MMA.  Reduction
-//                                     over graph rows is split across CTAs;
-//                                     db = colsum(G') is a separate kernel
+//   dW  : dW = [X1 | X2]^T G'         operands arrive MN-major (TMA boxes of 16
+//                                     graph rows x 128/256 columns, unswizzled);
+//                                     kind::tf32 only takes K-major operands (an
+//                                     MN-major tf32 operand yields zeros on
+//                                     sm_100a), so the NE transposer warps turn
+//                                     each staged box into double-buffered
+//                                     K-major SW64 tiles (conflict-free rotated
+//                                     STS.128) and, on the way, apply the ReLU
+//                                     bits to G and sum db = colsum(G').  The
+//                                     reduction over graph rows is split across
+//                                     CTAs; split-K partials and db are added
+//                                     into dW/db with red.global.add.f32
+//                                     (arrival order, see include/gnnv.h).
 //
-// Warp roles (192 threads): warp 0 = TMA producer (one elected thread),
-// warp 1 = TMEM owner + MMA issuer (one elected thread), warps 2-5 = epilogue
-// (tcgen05.ld lanes 32*(warp%4) .. +31).  fwd/dX are persistent over output
-// tiles with two TMEM accumulators (epilogue of tile t overlaps the mainloop
-// of tile t+1); dW owns one (i-tile group, row split) per CTA.
+// Warp roles (NTHREADS = 64 + 32*NE = 320): warp 0 = TMA producer (one
+// elected thread), warp 1 = TMEM owner + MMA issuer (one elected thread),
+// warps 2..2+NE-1 = epilogue (fwd/dX: tcgen05.ld of TMEM lanes
+// 32*(warp%4) .. +31, two warps per lane quadrant splitting the columns;
+// bias, ReLU, ReLU bits, TMA store through a 128B-swizzled smem buffer) or
+// transposers (dW).  fwd/dX are persistent over output tiles with two TMEM
+// accumulators (epilogue of tile t overlaps the mainloop of tile t+1); dW
+// owns one (i-tile group, row split) per CTA.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -237,7 +244,6 @@ struct Params {
   int ybits_ld;
   // dW: also the column sums of G (db) without a mask (G already masked)
   int dbsum;
-  int dbg;        // micro-benchmark switches (GNNV_DEBUG_GEMM): 1 = no epilogue stores, 2 = no MMA
   // fwd / dW: X1 row m is row x1_rows[m] of the tensor behind ta1 (layer 1
   // reading H_dst straight from the degree-ordered cache table): ta1 then
   // has a {width, 1} box and X1 tiles arrive by TMA gather4, 4 rows per
@@ -245,14 +251,6 @@ struct Params {
   const int32_t* x1_rows;
 };
 
-static int debug_flags() {
-  static int f = -1;
-  if (f < 0) {
-    const char* e = getenv("GNNV_DEBUG_GEMM");
-    f = e ? atoi(e) : 0;
-  }
-  return f;
-}
 
 // PAIR (MODE_FWD only): a cluster of 2 CTAs computes 256-row tiles with
 // tcgen05.mma.cta_group::2 (M = 256): each CTA stages its own 128 rows of A
@@ -450,8 +448,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_tma_gemm(const __grid_constant_
             const uint32_t b0 = a0 + a_bytes;
 #pragma unroll
             for (int k = 0; k < BK / 8; ++k) {
-              if (!(p.dbg & 2))
-                mma_tf32(tmem + (uint32_t)(acc * BN), desc_sw(a0 + k * 32, 1024, 2), desc_sw(b0 + k * 32, 1024, 2),
+              mma_tf32(tmem + (uint32_t)(acc * BN), desc_sw(a0 + k * 32, 1024, 2), desc_sw(b0 + k * 32, 1024, 2),
                          idesc, (kb > 0 || k > 0) ? 1u : 0u);
             }
             mma_commit(&empty[s]);
@@ -498,7 +495,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_tma_gemm(const __grid_constant_
               v[j] = n < p.N ? x : 0.f;
               bits |= (v[j] > 0.f ? 1u : 0u) << j;
             }
-            if (p.bits && row0 + lane < M && !(p.dbg & 1)) p.bits[(int64_t)(row0 + lane) * p.bits_ld + (c >> 5)] = bits;
+            if (p.bits && row0 + lane < M) p.bits[(int64_t)(row0 + lane) * p.bits_ld + (c >> 5)] = bits;
           }
           const int j0 = nt * BN + c;  // dX: column in the [Y1 | Y2] space
           if (MODE == MODE_DX && p.ybits && j0 < p.ld1) {
@@ -514,7 +511,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_tma_gemm(const __grid_constant_
             // map spans the row capacity, which may exceed the caller's rows);
             // a dX chunk straddling Y1 | Y2 also takes this path
             const int64_t m = (int64_t)row0 + lane;
-            if (m < M && !(p.dbg & 1)) {
+            if (m < M) {
 #pragma unroll
               for (int j = 0; j < 32; j += 4) {
                 const float4 o = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
@@ -542,7 +539,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_tma_gemm(const __grid_constant_
                          v[4 * j + 3]);
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
           __syncwarp();
-          if (lane == 0 && !(p.dbg & 1)) {
+          if (lane == 0) {
             if (MODE == MODE_FWD) {
               tma_store_2d(&p.ty1, ob, c, row0);
             } else if (j0 < p.ld1) {
@@ -629,8 +626,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_tma_gemm(const __grid_constant_
           for (int mt = 0; mt < MT; ++mt) {
 #pragma unroll
             for (int k = 0; k < DW_KR / 8; ++k) {
-              if (!(p.dbg & 2))
-                mma_tf32(tmem + (uint32_t)(mt * BN), desc_sw(ka + mt * BM * 64 + k * 32, 512, 4),
+              mma_tf32(tmem + (uint32_t)(mt * BN), desc_sw(ka + mt * BM * 64 + k * 32, 512, 4),
                          desc_sw(kbb + k * 32, 512, 4), idesc, (i > 0 || k > 0) ? 1u : 0u);
             }
           }
@@ -958,8 +954,7 @@ bool gemm_fwd_tma(const GemmFwdArgs& a, cudaStream_t s) {
   // default: measured on products, layer 1 179 -> 189-192 us (its tiles are
   // bound by the A operand's DRAM reads and the epilogue, not by the W^T
   // traffic the pair halves), layer 2 49 -> 46 us
-  const char* pe = getenv("GNNV_GEMM_PAIR");
-  const bool pair = pe && pe[0] == '1' && !a.x1_rows && BN % 32 == 0;
+  const bool pair = env_on("GNNV_GEMM_PAIR") && !a.x1_rows && BN % 32 == 0;
   p.ta1 = a.x1_rows ? make_map(a.X1, a.x1_table_rows, a.K1, a.ld1, 1) : make_map(a.X1, a.max_M, a.K1, a.ld1, BM);
   p.ta2 = a.X2 ? make_map(a.X2, a.max_M, a.K1, a.ld2, BM) : p.ta1;
   p.tb = make_map(Bt, BN, Kp, Kp, pair ? BN / 2 : BN);
@@ -978,7 +973,6 @@ bool gemm_fwd_tma(const GemmFwdArgs& a, cudaStream_t s) {
   p.bits = a.relu ? a.mask_bits : nullptr;
   p.bits_ld = a.mask_ld;
   const int64_t tiles = ceil_div(std::max<int64_t>(a.max_M, 1), BM);
-  p.dbg = debug_flags();
   if (pair) {
     launch_pair(p, (int)std::min<int64_t>(ceil_div(tiles, 2), num_sms() / 2), s);
     return true;
@@ -1017,7 +1011,6 @@ bool gemm_dx_tma(const GemmDxArgs& a, cudaStream_t s) {
   p.ybits = a.y1_bits;
   p.ybits_ld = a.y1_bits_ld;
   const int64_t tiles = ceil_div(std::max<int64_t>(a.max_M, 1), BM) * ntl;
-  p.dbg = debug_flags();
   launch<MODE_DX>(p, dim3((unsigned)std::min<int64_t>(tiles, num_sms())), s);
   return true;
 }
@@ -1069,7 +1062,6 @@ bool gemm_dw_tma(const GemmDwArgs& a, cudaStream_t s) {
   p.N = a.N;
   p.splits = splits;
   p.ablocks = ablocks;
-  p.dbg = debug_flags();
   launch<MODE_DW>(p, dim3((unsigned)splits, (unsigned)igroups), s);
   return true;
 }

@@ -213,11 +213,15 @@ void launch_ce_loss(const float* z, int32_t ldz, int32_t C, const int32_t* d_row
 __global__ void k_sgd(float* __restrict__ p, const float* __restrict__ g, int64_t n, float lr, float* out_loss,
                       int32_t* out_err, const int32_t* err) {
   GNNV_PDL_ENTRY();
+  const int32_t bad = err ? *err : 0;
   if (out_loss && blockIdx.x == 0 && threadIdx.x == 0) {
     *out_loss = g[n];
-    *out_err = *err;
+    *out_err = bad;
     __threadfence_system();
   }
+  // a batch with an invalid seed (sample.cu k_init_seeds) is not applied:
+  // the step reports GNNV_ERR_PARAM and the parameters stay as they were
+  if (bad) return;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     p[i] -= lr * g[i];
 }

@@ -68,19 +68,31 @@ __device__ __forceinline__ uint32_t philox_draw(uint64_t seed, uint32_t h, uint3
   return w == 0 ? o.x : (w == 1 ? o.y : (w == 2 ? o.z : o.w));
 }
 
-__global__ void k_init_seeds(const int32_t* __restrict__ seeds, int32_t n_seeds, int64_t N, int32_t* tag, int32_t* F,
-                             int32_t* sizes, int32_t err_index) {
+// One CTA (seeds <= max_seeds, a few thousand): it first clears this
+// handle's error flag -- so every sample reports only its own seeds, and a
+// bad batch does not poison later steps -- then validates and places the
+// seeds.  A seed outside [0, N) is replaced by vertex 0 in F (bit 1 of the
+// flag), a repeated seed sets bit 2: every later kernel then indexes only
+// valid vertices, and the step reports GNNV_ERR_PARAM at its next sync point
+// (its SGD skips the update).
+__global__ void __launch_bounds__(1024) k_init_seeds(const int32_t* __restrict__ seeds, int32_t n_seeds, int64_t N,
+                                                     int32_t* tag, int32_t* F, int32_t* sizes, int32_t err_index) {
   GNNV_PDL_ENTRY();
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n_seeds; i += gridDim.x * blockDim.x) {
+  if (threadIdx.x == 0) {
+    sizes[err_index] = 0;
+    sizes[0] = n_seeds;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < n_seeds; i += blockDim.x) {
     const int32_t v = seeds[i];
-    F[i] = v;
     if ((uint32_t)v >= (uint64_t)N) {
+      F[i] = 0;
       atomicOr(&sizes[err_index], 1);
       continue;
     }
+    F[i] = v;
     if (atomicCAS(&tag[v], INT_MIN, i) != INT_MIN) atomicOr(&sizes[err_index], 2);
   }
-  if (blockIdx.x == 0 && threadIdx.x == 0) sizes[0] = n_seeds;
 }
 
 // Four consecutive slots per thread: one 16-byte load of their sampled ids,
@@ -609,24 +621,17 @@ __global__ void k_reset(const int32_t* __restrict__ F, const int32_t* sizes, int
   }
 }
 
-// One work item per thread / row group (no grid-stride caps): short-lived
-// blocks let the step's higher-priority kernels interleave with a prefetch.
-static int g_grid_cap = 0;  // 0: none (set around a prefetch, see set_grid_cap)
-static int grid_for(int64_t work, int per_block, int /*max_blocks*/) {
-  int64_t g = ceil_div(std::max<int64_t>(work, 1), per_block);
-  return (int)std::min<int64_t>(g, g_grid_cap > 0 ? g_grid_cap : INT32_MAX);
-}
-
-void set_grid_cap(int blocks) { g_grid_cap = blocks; }
-int grid_cap() { return g_grid_cap; }
+// One work item per thread / row group (no grid-stride loops over a capped
+// grid): short-lived blocks let the step's higher-priority kernels
+// interleave with a prefetch.  Grids are sized by the Eq.12 capacity of the
+// hop (the realised size is on the device); surplus blocks exit at once.
+static int grid_for(int64_t work, int per_block) { return (int)ceil_div(std::max<int64_t>(work, 1), per_block); }
 
 void launch_sample(gnnv_graph* g, gnnv_blocks* b, const int32_t* d_seeds, int32_t n_seeds, uint64_t rng_seed,
                    cudaStream_t s) {
   const int L = b->L;
-  const int sms = num_sms();
   const int err_index = 2 * L + 1;
-  launch_k(k_init_seeds, grid_for(n_seeds, 256, sms * 4), 256, 0, s, d_seeds, n_seeds, g->n, b->d_tag, b->d_F, b->d_sizes,
-                                                                err_index);
+  launch_k(k_init_seeds, 1, 1024, 0, s, d_seeds, n_seeds, g->n, b->d_tag, b->d_F, b->d_sizes, err_index);
   GNNV_CHECK_LAUNCH();
   // Hop h's slots reuse d_ell / d_cnt, so hop h-1 is mapped to local ids
   // (its tags are final after its scan) before hop h samples.  Hops with a
@@ -635,7 +640,7 @@ void launch_sample(gnnv_graph* g, gnnv_blocks* b, const int32_t* d_seeds, int32_
   auto map_hop = [&](int hp) {
     const int64_t slots_ub = b->max_nnz[hp];
     const bool csc = hp < b->csc_hops;
-    launch_k(k_map, grid_for(slots_ub, 1024, sms * 8), 256, 0, s, hp, b->fanouts[hp], b->d_sizes, b->d_ell, b->d_cnt,
+    launch_k(k_map, grid_for(slots_ub, 1024), 256, 0, s, hp, b->fanouts[hp], b->d_sizes, b->d_ell, b->d_cnt,
              b->d_indptr[hp], b->d_tag, b->d_indices[hp], b->d_scan, b->scan_words,
              csc ? b->d_csc_cnt : (int32_t*)nullptr);
     GNNV_CHECK_LAUNCH();
@@ -644,7 +649,7 @@ void launch_sample(gnnv_graph* g, gnnv_blocks* b, const int32_t* d_seeds, int32_
     GNNV_TRY_CUDA(cub::DeviceScan::ExclusiveSum(b->d_csc_tmp, tmp, b->d_csc_cnt, b->d_colptr[hp],
                                                 (int)(b->max_n[hp + 1] + 1), s));
     GNNV_CHECK_LAUNCH();
-    launch_k(k_csc_fill, grid_for(slots_ub, 256, 0), 256, 0, s, hp, b->fanouts[hp], b->d_sizes, b->d_indptr[hp],
+    launch_k(k_csc_fill, grid_for(slots_ub, 256), 256, 0, s, hp, b->fanouts[hp], b->d_sizes, b->d_indptr[hp],
              b->d_indices[hp], b->d_csc_cnt, b->d_colptr[hp], b->d_csc[hp]);
     GNNV_CHECK_LAUNCH();
   };
@@ -654,21 +659,21 @@ void launch_sample(gnnv_graph* g, gnnv_blocks* b, const int32_t* d_seeds, int32_
     if (h > 0) map_hop(h - 1);
     const int threads = 256;
 #define GNNV_SAMPLE_LAUNCH(G)                                                                              \
-  launch_k(k_sample_hop<G>, grid_for(rows_ub, threads / 32 * (32 / G), sms * 8), threads, 0, s,                  \
+  launch_k(k_sample_hop<G>, grid_for(rows_ub, threads / 32 * (32 / G)), threads, 0, s,                  \
       g->d_indptr, g->d_indices, g->n, b->d_F, b->d_sizes, h, k, rng_seed, b->d_ell, b->d_cnt, b->d_tag, b->d_own[h])
     if (b->loc_w > 1) {
-      launch_k(k_sample_hop_biased, grid_for(rows_ub, 8, 0), 256, 0, s, g->d_indptr, g->d_indices, g->n, b->d_F,
+      launch_k(k_sample_hop_biased, grid_for(rows_ub, 8), 256, 0, s, g->d_indptr, g->d_indices, g->n, b->d_F,
                b->d_sizes, h, k, rng_seed, b->loc_slot, (int)b->loc_w, b->d_ell, b->d_cnt, b->d_tag, b->d_own[h]);
     } else if (k <= 4) {
-      launch_k(k_sample_hop_tpr<4>, grid_for(rows_ub, threads, 0), threads, 0, s, 
+      launch_k(k_sample_hop_tpr<4>, grid_for(rows_ub, threads), threads, 0, s, 
           g->d_indptr, g->d_indices, g->n, b->d_F, b->d_sizes, h, k, rng_seed, b->d_ell, b->d_cnt, b->d_tag, b->d_own[h]);
     } else if (k <= 8) {
-      launch_k(k_sample_hop_tpr<8>, grid_for(rows_ub, threads, 0), threads, 0, s, 
+      launch_k(k_sample_hop_tpr<8>, grid_for(rows_ub, threads), threads, 0, s, 
           g->d_indptr, g->d_indices, g->n, b->d_F, b->d_sizes, h, k, rng_seed, b->d_ell, b->d_cnt, b->d_tag, b->d_own[h]);
     } else if (k <= 16 && rows_ub < 16384) {
       GNNV_SAMPLE_LAUNCH(16);  // few rows: lanes per row beat rows per thread
     } else if (k <= 16) {
-      launch_k(k_sample_hop_tpr<16>, grid_for(rows_ub, threads, 0), threads, 0, s, 
+      launch_k(k_sample_hop_tpr<16>, grid_for(rows_ub, threads), threads, 0, s, 
           g->d_indptr, g->d_indices, g->n, b->d_F, b->d_sizes, h, k, rng_seed, b->d_ell, b->d_cnt, b->d_tag, b->d_own[h]);
     } else {
       GNNV_SAMPLE_LAUNCH(32);
@@ -676,15 +681,15 @@ void launch_sample(gnnv_graph* g, gnnv_blocks* b, const int32_t* d_seeds, int32_
 #undef GNNV_SAMPLE_LAUNCH
     GNNV_CHECK_LAUNCH();
     const int tiles_ub = (int)ceil_div(rows_ub, kScanTile);
-    launch_k(k_winners, grid_for(rows_ub * k, 1024, 0), 256, 0, s, g->n, h, k, b->d_sizes, b->d_ell, b->d_cnt, b->d_tag,
+    launch_k(k_winners, grid_for(rows_ub * k, 1024), 256, 0, s, g->n, h, k, b->d_sizes, b->d_ell, b->d_cnt, b->d_tag,
                                                              b->d_own[h]);
     GNNV_CHECK_LAUNCH();
-    launch_k(k_relabel_scan, g_grid_cap > 0 ? std::min<int>(tiles_ub, g_grid_cap) : tiles_ub, kScanTile, 0, s, g->n, h, k, L, b->d_ell, b->d_cnt, b->d_tag, b->d_F,
+    launch_k(k_relabel_scan, tiles_ub, kScanTile, 0, s, g->n, h, k, L, b->d_ell, b->d_cnt, b->d_tag, b->d_F,
                                                   b->d_indptr[h], b->d_own[h], b->d_sizes, b->d_scan);
     GNNV_CHECK_LAUNCH();
   }
   map_hop(L - 1);
-  launch_k(k_reset, grid_for(b->max_n[L], 1024, sms * 8), 256, 0, s, b->d_F, b->d_sizes, L, g->n, b->d_tag);
+  launch_k(k_reset, grid_for(b->max_n[L], 1024), 256, 0, s, b->d_F, b->d_sizes, L, g->n, b->d_tag);
   GNNV_CHECK_LAUNCH();
 }
 

@@ -15,8 +15,6 @@
 // shuffles; four neighbour rows are loaded before they are added, in
 // ascending edge order (a fixed summation order).  HBM-bound: compulsory
 // bytes are the distinct source rows + the output rows + the indices.
-#include <cstdlib>
-
 #include "common.cuh"
 
 namespace gnnv {
@@ -98,115 +96,6 @@ __global__ void __launch_bounds__(256) k_spmm_fwd(const int32_t* __restrict__ in
         reinterpret_cast<float4*>(A)[(int64_t)row * lda4 + c] = make_float4(0.f, 0.f, 0.f, 0.f);
     }
   }
-}
-
-// The same aggregation with the row metadata software-pipelined: while a
-// warp loads the neighbour rows of its current dst row r, it already has
-// in flight the cache-row mapping of row r+S's neighbour ids, the neighbour
-// ids of row r+2S and the indptr pair of row r+3S (S = the grid's row
-// stride).  The plain kernel runs indptr -> indices -> rowidx -> H as four
-// dependent memory round trips per row; here each row costs one, with the
-// three metadata loads of later rows overlapped with it.  Summation order
-// (ascending edges, four loads per add group) is the plain kernel's, so the
-// two are bitwise identical.  Opt-in (GNNV_SPMM_PF=1): measured slower on
-// products layer 1 (338 vs 250 us) -- its 48 registers
-// leave 40 resident warps per SM instead of 64, and the plain kernel's
-// dependent round trips were already hidden by the other warps.
-#ifndef GNNV_PF_MINB
-#define GNNV_PF_MINB 1  // min resident CTAs (A/B builds: 8 forces 32 registers)
-#endif
-template <int LPR, bool IND>
-__global__ void __launch_bounds__(256, GNNV_PF_MINB) k_spmm_fwd_pf(const int32_t* __restrict__ indptr,
-                                                     const int32_t* __restrict__ indices, const int32_t* d_ndst,
-                                                     const float* __restrict__ H, int32_t ldh, float* __restrict__ A,
-                                                     int32_t lda, int32_t d, int32_t kind, int32_t aggr,
-                                                     const int32_t* __restrict__ rowidx) {
-  GNNV_PDL_ENTRY();
-  constexpr int RPW = 32 / LPR;
-  const int n = *d_ndst;
-  const int vec = (d + 3) >> 2;
-  const int lane = threadIdx.x & 31, sub = lane / LPR, sl = lane % LPR;
-  const unsigned smask = (LPR == 32) ? 0xffffffffu : (((1u << LPR) - 1u) << (sub * LPR));
-  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int nwarps = (gridDim.x * blockDim.x) >> 5;
-  const int stride = nwarps * RPW;
-  const float4* H4 = reinterpret_cast<const float4*>(H);
-  const int ldh4 = ldh >> 2, lda4 = lda >> 2;
-#define GNNV_LD_PTR(r, b, c)                            \
-  do {                                                  \
-    const bool ok_ = (r) < n;                           \
-    b = ok_ ? __ldg(indptr + (r)) : 0;                  \
-    c = ok_ ? __ldg(indptr + (r) + 1) - b : 0;          \
-  } while (0)
-  const int row0 = warp * RPW + sub;
-  int b0, n0, b1, n1, b2, n2;
-  GNNV_LD_PTR(row0, b0, n0);
-  GNNV_LD_PTR(row0 + stride, b1, n1);
-  GNNV_LD_PTR(row0 + 2 * stride, b2, n2);
-  int my0 = sl < n0 ? __ldg(indices + b0 + sl) : 0;
-  int raw1 = sl < n1 ? __ldg(indices + b1 + sl) : 0;
-  if (IND) my0 = __ldg(rowidx + my0);
-  for (int base = warp * RPW; base < n; base += stride) {
-    const int row = base + sub;
-    const bool active = row < n;
-    // metadata of the next three rows, independent of this row's loads
-    const int my1 = IND ? __ldg(rowidx + raw1) : raw1;
-    const int raw2 = sl < n2 ? __ldg(indices + b2 + sl) : 0;
-    int b3, n3;
-    GNNV_LD_PTR(row + 3 * stride, b3, n3);
-    const int beg = b0, cnt = n0;
-    for (int cb = 0; cb < vec; cb += LPR) {
-      const int c = cb + sl;
-      const bool cok = active && c < vec;
-      float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (kind == GNNV_KIND_GCN && cok) acc = __ldg(H4 + (int64_t)(IND ? __ldg(rowidx + row) : row) * ldh4 + c);
-      for (int e0 = 0; e0 < cnt; e0 += LPR) {
-        int my = my0;
-        if (e0) {
-          my = (e0 + sl < cnt) ? __ldg(indices + beg + e0 + sl) : 0;
-          if (IND) my = __ldg(rowidx + my);
-        }
-        const int m = min(LPR, cnt - e0);
-        int j = 0;
-        for (; j + 4 <= m; j += 4) {
-          const int u0 = __shfl_sync(smask, my, j, LPR), u1 = __shfl_sync(smask, my, j + 1, LPR);
-          const int u2 = __shfl_sync(smask, my, j + 2, LPR), u3 = __shfl_sync(smask, my, j + 3, LPR);
-          if (cok) {
-            const float4 h0 = __ldg(H4 + (int64_t)u0 * ldh4 + c), h1 = __ldg(H4 + (int64_t)u1 * ldh4 + c);
-            const float4 h2 = __ldg(H4 + (int64_t)u2 * ldh4 + c), h3 = __ldg(H4 + (int64_t)u3 * ldh4 + c);
-            acc = f4add(acc, h0);
-            acc = f4add(acc, h1);
-            acc = f4add(acc, h2);
-            acc = f4add(acc, h3);
-          }
-        }
-        for (; j < m; ++j) {
-          const int u = __shfl_sync(smask, my, j, LPR);
-          if (cok) acc = f4add(acc, __ldg(H4 + (int64_t)u * ldh4 + c));
-        }
-      }
-      if (cok) {
-        if (aggr == GNNV_AGGR_MEAN) {
-          const int denom = cnt + (kind == GNNV_KIND_GCN ? 1 : 0);
-          acc = denom ? f4div(acc, (float)denom) : make_float4(0.f, 0.f, 0.f, 0.f);
-        }
-        reinterpret_cast<float4*>(A)[(int64_t)row * lda4 + c] = mask_tail(acc, c, d);
-      }
-    }
-    if (active) {
-      for (int c = vec + sl; c < lda4; c += LPR)
-        reinterpret_cast<float4*>(A)[(int64_t)row * lda4 + c] = make_float4(0.f, 0.f, 0.f, 0.f);
-    }
-    b0 = b1;
-    n0 = n1;
-    my0 = my1;
-    b1 = b2;
-    n1 = n2;
-    raw1 = raw2;
-    b2 = b3;
-    n2 = n3;
-  }
-#undef GNNV_LD_PTR
 }
 
 // Transposed aggregation dH[u] += w_v dA[v] over the block's edges (v, u),
@@ -433,22 +322,15 @@ void launch_spmm_fwd(const int32_t* d_indptr, const int32_t* d_indices, const in
                      const float* H, int32_t ldh, float* A, int32_t lda, int32_t d, int32_t kind, int32_t aggr,
                      cudaStream_t s, const int32_t* rowidx) {
   const int vec = (d + 3) / 4;
-  const bool plain = getenv("GNNV_SPMM_PF") == nullptr;  // read per launch (A/B tests toggle it)
 #define GNNV_SPMM_FWD(LPR, RPWv)                                                                                  \
   do {                                                                                                            \
     const int grid = spmm_grid(max_dst, RPWv);                                                                    \
-    if (rowidx && plain)                                                                                          \
+    if (rowidx)                                                                                                   \
       launch_k(k_spmm_fwd<LPR, true>, grid, 256, 0, s, d_indptr, d_indices, d_ndst, H, ldh, A, lda, d, kind, aggr,  \
                rowidx);                                                                                           \
-    else if (rowidx)                                                                                              \
-      launch_k(k_spmm_fwd_pf<LPR, true>, grid, 256, 0, s, d_indptr, d_indices, d_ndst, H, ldh, A, lda, d, kind,     \
-               aggr, rowidx);                                                                                     \
-    else if (plain)                                                                                               \
+    else                                                                                                          \
       launch_k(k_spmm_fwd<LPR, false>, grid, 256, 0, s, d_indptr, d_indices, d_ndst, H, ldh, A, lda, d, kind, aggr, \
                nullptr);                                                                                          \
-    else                                                                                                          \
-      launch_k(k_spmm_fwd_pf<LPR, false>, grid, 256, 0, s, d_indptr, d_indices, d_ndst, H, ldh, A, lda, d, kind,    \
-               aggr, nullptr);                                                                                    \
   } while (0)
   if (vec <= 8) {
     GNNV_SPMM_FWD(8, 4);

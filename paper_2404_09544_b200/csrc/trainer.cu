@@ -77,22 +77,20 @@ struct gnnv_trainer {
   int pend_n = 0;
   uint64_t pend_rng = 0;
   cudaStream_t side = nullptr;
-  void* green = nullptr;  // CUgreenCtx of the side stream (GNNV_PF_SMS), or null
   cudaEvent_t ev_ready[2] = {nullptr, nullptr}, ev_free[2] = {nullptr, nullptr}, ev_in = nullptr;
-  // Prefetch gating (experiments on the Eq.4 overlap): GNNV_PF_GATE=fI or bI
-  // makes the step record ev_mid after layer I's forward (f) or backward (b);
-  // a prefetch enqueued after that step starts its sampling
-  // (GNNV_PF_GATE_SAMPLE=1) or its gather only then.  GNNV_PF_GATHER_AFTER=I
-  // is fI for the gather.
-  cudaEvent_t ev_mid = nullptr;
-  bool mid_pending = false;
+  // NEXT-3 dynamic cache: the last admission (serial step or prefetch, on
+  // whichever stream ran it); every later gather + admission waits on it, so
+  // the slot map, the table and the shared miss buffers are never touched by
+  // two batches at once
+  cudaEvent_t ev_cache = nullptr;
+  bool cache_pending = false;
   cudaEvent_t ev_h2d[2] = {nullptr, nullptr};  // last copy out of h_seedsb[k]
   bool h2d_used[2] = {false, false};
   Timeline tl_side;
   // Whole feature table resident on this device (capacity N, one shard):
   // the gather materialises only the dst prefix F_{L-1} of X and records
   // every F_L row's cache row in rowidx; layer 1 aggregates from the table.
-  int32_t loc_w = 1;  // NEXT-2 locality weight for both buffer sets
+  double loc_bias = 0.0;  // NEXT-2 locality bias for both buffer sets
   bool x_fused = false;
   // x_fused with TF32 SAGE and GNNV_XROWS=1: the layer-1 GEMMs also read
   // H_dst from the table (TMA gather4 through rowidx), so the gather copies
@@ -117,74 +115,14 @@ static gnnv_layer_desc layer_desc(const gnnv_trainer* t, int i) {
   return ld;
 }
 
-// The prefetch (side) stream.  Lowest priority, so that the prefetch fills
-// the SMs the step leaves idle.  With GNNV_PF_SMS=n (n > 0) the stream
-// belongs to a green context confined to n SMs (driver API, CUDA 12.4+):
-// the prefetch then never occupies more than n SMs, and the step's
-// persistent GEMM CTAs do not wait for SMs drained of prefetch blocks.
-template <typename F>
-static F drv(const char* name) {
-  void* p = nullptr;
-  cudaDriverEntryPointQueryResult q;
-  GNNV_TRY_CUDA(cudaGetDriverEntryPoint(name, &p, cudaEnableDefault, &q));
-  GNNV_REQUIRE(p && q == cudaDriverEntryPointSuccess, GNNV_ERR_CUDA, std::string("driver entry point ") + name);
-  return reinterpret_cast<F>(p);
-}
-
-struct PfGate {
-  char phase = 0;  // 'f', 'b' or 0 (none)
-  int layer = 0;
-  bool sample = false;
-};
-static const PfGate& pf_gate() {
-  static const PfGate g = [] {
-    PfGate r;
-    if (const char* e = getenv("GNNV_PF_GATE")) {
-      if ((e[0] == 'f' || e[0] == 'b') && e[1]) r.phase = e[0], r.layer = atoi(e + 1);
-    } else if (const char* a = getenv("GNNV_PF_GATHER_AFTER")) {
-      r.phase = 'f', r.layer = atoi(a);
-    }
-    r.sample = getenv("GNNV_PF_GATE_SAMPLE") != nullptr;
-    return r;
-  }();
-  return g;
-}
-
-static cudaStream_t make_side_stream(int device, void** green_ctx) {
+// The prefetch (side) stream: lowest priority, so that the prefetch fills
+// the SMs the step leaves idle (DESIGN.md §9 lists the placements measured:
+// green contexts, grid caps, high priority, event gates -- none was faster).
+static cudaStream_t make_side_stream() {
   int lo = 0, hi = 0;
   GNNV_TRY_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
-  const char* e = getenv("GNNV_PF_SMS");
-  const int sms = e ? atoi(e) : 0;
-  if (sms > 0) {
-    auto getdev = drv<CUresult (*)(CUdevice*, int)>("cuDeviceGet");
-    auto getres = drv<CUresult (*)(CUdevice, CUdevResource*, CUdevResourceType)>("cuDeviceGetDevResource");
-    auto split = drv<CUresult (*)(CUdevResource*, unsigned*, const CUdevResource*, CUdevResource*, unsigned, unsigned)>(
-        "cuDevSmResourceSplitByCount");
-    auto gendesc = drv<CUresult (*)(CUdevResourceDesc*, CUdevResource*, unsigned)>("cuDevResourceGenerateDesc");
-    auto create = drv<CUresult (*)(CUgreenCtx*, CUdevResourceDesc, CUdevice, unsigned)>("cuGreenCtxCreate");
-    auto mkstream = drv<CUresult (*)(CUstream*, CUgreenCtx, unsigned, int)>("cuGreenCtxStreamCreate");
-    CUdevice dev;
-    CUdevResource all, part, rest;
-    unsigned n = 1;
-    CUdevResourceDesc desc;
-    CUgreenCtx gc;
-    CUstream st;
-    GNNV_REQUIRE(getdev(&dev, device) == CUDA_SUCCESS && getres(dev, &all, CU_DEV_RESOURCE_TYPE_SM) == CUDA_SUCCESS &&
-                     split(&part, &n, &all, &rest, 0, (unsigned)sms) == CUDA_SUCCESS && n == 1 &&
-                     gendesc(&desc, &part, 1) == CUDA_SUCCESS &&
-                     create(&gc, desc, dev, CU_GREEN_CTX_DEFAULT_STREAM) == CUDA_SUCCESS &&
-                     mkstream(&st, gc, CU_STREAM_NON_BLOCKING, lo) == CUDA_SUCCESS,
-                 GNNV_ERR_CUDA, "green context for the prefetch stream");
-    *green_ctx = (void*)gc;
-    return (cudaStream_t)st;
-  }
-  // GNNV_PF_PRIO=high: the prefetch stream takes the highest priority
-  // instead of the lowest (its latency-bound sampler then runs early in the
-  // step instead of filling gaps until the end)
-  const char* pe = getenv("GNNV_PF_PRIO");
-  const int prio = (pe && pe[0] == 'h') ? hi : lo;
   cudaStream_t st;
-  GNNV_TRY_CUDA(cudaStreamCreateWithPriority(&st, cudaStreamNonBlocking, prio));
+  GNNV_TRY_CUDA(cudaStreamCreateWithPriority(&st, cudaStreamNonBlocking, lo));
   return st;
 }
 
@@ -206,14 +144,8 @@ gnnv_status gnnv_trainer_free(gnnv_trainer* t) {
     if (t->ev_h2d[k]) cudaEventDestroy(t->ev_h2d[k]);
   }
   if (t->ev_in) cudaEventDestroy(t->ev_in);
-  if (t->ev_mid) cudaEventDestroy(t->ev_mid);
+  if (t->ev_cache) cudaEventDestroy(t->ev_cache);
   if (t->side) cudaStreamDestroy(t->side);
-  if (t->green) {
-    try {
-      drv<CUresult (*)(CUgreenCtx)>("cuGreenCtxDestroy")((CUgreenCtx)t->green);
-    } catch (...) {
-    }
-  }
   dfree(t->d_params);
   dfree(t->d_grads);
   if (t->h_out) cudaFreeHost(t->h_out);
@@ -286,9 +218,9 @@ gnnv_status gnnv_trainer_create(gnnv_graph* g, gnnv_cache* c, const gnnv_model_d
       gnnv_blocks* b = t->b;
       t->Hs[0] = g->stride;
       t->x_fused = L > 1 && !c->dynamic && c->capacity == g->n && c->world == 1 && c->shards.size() == 1 &&
-                   c->shards[0] && !getenv("GNNV_NO_XFUSE");
+                   c->shards[0];
       t->table = t->x_fused ? c->shards[0] : nullptr;
-      t->x_rows = t->x_fused && md->prec == GNNV_PREC_TF32 && md->kind == GNNV_KIND_SAGE && getenv("GNNV_XROWS");
+      t->x_rows = t->x_fused && md->prec == GNNV_PREC_TF32 && md->kind == GNNV_KIND_SAGE && env_on("GNNV_XROWS");
       const int64_t xrows = t->x_rows ? 1 : t->x_fused ? b->max_n[L - 1] : b->max_n[L];
       t->H[0] = (float*)dmalloc((size_t)xrows * g->stride * sizeof(float), "X (gathered features)");
       if (t->x_fused) t->rowidx[0] = (int32_t*)dmalloc(b->max_n[L] * sizeof(int32_t), "cache rows of F_L");
@@ -306,7 +238,7 @@ gnnv_status gnnv_trainer_create(gnnv_graph* g, gnnv_cache* c, const gnnv_model_d
       t->loss_partial =
           (float*)dmalloc(std::max<int64_t>(256, ceil_div(b->max_n[0], 32)) * sizeof(float), "loss partials");
       t->tail = md->prec == GNNV_PREC_TF32 && L >= 2 &&
-                tail_supported(md->kind, md->dims[L - 1], md->dims[L], md->fanouts[0]) && !getenv("GNNV_NO_TAIL");
+                tail_supported(md->kind, md->dims[L - 1], md->dims[L], md->fanouts[0]) && !env_on("GNNV_NO_TAIL");
       if (t->tail) {
         t->tail_dA = (float*)dmalloc((size_t)b->max_n[0] * md->dims[L - 1] * sizeof(float), "output-layer dA");
         t->tail_part = (float*)dmalloc(tail_partial_floats(b->max_n[0], md->dims[L - 1], md->dims[L]) * sizeof(float),
@@ -329,7 +261,7 @@ gnnv_status gnnv_trainer_create(gnnv_graph* g, gnnv_cache* c, const gnnv_model_d
         GNNV_TRY_CUDA(cudaEventCreateWithFlags(&t->ev_h2d[k], cudaEventDisableTiming));
       }
       GNNV_TRY_CUDA(cudaEventCreateWithFlags(&t->ev_in, cudaEventDisableTiming));
-      GNNV_TRY_CUDA(cudaEventCreateWithFlags(&t->ev_mid, cudaEventDisableTiming));
+      GNNV_TRY_CUDA(cudaEventCreateWithFlags(&t->ev_cache, cudaEventDisableTiming));
       GNNV_TRY_CUDA(cudaDeviceSynchronize());
     } catch (...) {
       gnnv_trainer_free(t);
@@ -381,16 +313,16 @@ gnnv_status gnnv_trainer_activation(gnnv_trainer* t, int32_t i, const float** d_
   });
 }
 
-gnnv_status gnnv_trainer_set_locality(gnnv_trainer* t, int32_t weight) {
+gnnv_status gnnv_trainer_set_locality(gnnv_trainer* t, double bias) {
   return guarded([&] {
     GNNV_REQUIRE(t, GNNV_ERR_PARAM, "trainer_set_locality: null");
     GNNV_REQUIRE(!t->pending, GNNV_ERR_STATE, "trainer_set_locality: a prefetched batch is pending");
     for (int k = 0; k < 2; ++k) {
       if (!t->bb[k]) continue;
-      gnnv_status st = gnnv_blocks_set_locality(t->bb[k], t->c, weight);
+      gnnv_status st = gnnv_blocks_set_locality(t->bb[k], t->c, bias);
       if (st != GNNV_OK) throw Error{st, get_error()};
     }
-    t->loc_w = weight;
+    t->loc_bias = bias;
   });
 }
 
@@ -530,7 +462,7 @@ gnnv_status gnnv_trainer_prefetch(gnnv_trainer* t, const int32_t* seeds, int32_t
       GNNV_TRY_CUDA(cudaDeviceSynchronize());
       gnnv_status st = gnnv_blocks_create(g, t->md.max_seeds, t->md.fanouts, t->md.L, &t->bb[k]);
       if (st != GNNV_OK) throw Error{st, get_error()};
-      st = gnnv_blocks_set_locality(t->bb[k], t->c, t->loc_w);
+      st = gnnv_blocks_set_locality(t->bb[k], t->c, t->loc_bias);
       if (st != GNNV_OK) throw Error{st, get_error()};
       const int64_t xrows = t->x_rows ? 1 : t->bb[k]->max_n[t->x_fused ? t->md.L - 1 : t->md.L];
       t->X[k] = (float*)dmalloc((size_t)xrows * g->stride * sizeof(float), "X (prefetch)");
@@ -544,7 +476,7 @@ gnnv_status gnnv_trainer_prefetch(gnnv_trainer* t, const int32_t* seeds, int32_t
       // would put a device synchronisation and a cudaMalloc inside the step
       if (t->bb[k ^ 1] && t->bb[k ^ 1]->scratch_bytes)
         t->bb[k]->ensure_scratch(t->bb[k ^ 1]->scratch_bytes, (cudaStream_t)stream);
-      if (!t->side) t->side = make_side_stream(g->device, &t->green);
+      if (!t->side) t->side = make_side_stream();
     }
     cudaStream_t s = (cudaStream_t)stream;
     // order after the step that last computed on buffer set k and, for
@@ -559,38 +491,24 @@ gnnv_status gnnv_trainer_prefetch(gnnv_trainer* t, const int32_t* seeds, int32_t
     GNNV_TRY_CUDA(cudaStreamWaitEvent(t->side, t->ev_free[k], 0));
     Timeline* tl = t->tl.on ? &t->tl_side : nullptr;
     const int32_t* d_seeds = stage_seeds(t, k, seeds, n_seeds, seeds_on_host, t->side, tl);
-    if (t->mid_pending && pf_gate().sample) {
-      GNNV_TRY_CUDA(cudaStreamWaitEvent(t->side, t->ev_mid, 0));
-      t->mid_pending = false;
-    }
     if (tl) tl->mark(t->side, "pf_sample");
-    static const int pf_cap = [] {
-      const char* e = getenv("GNNV_PF_BLOCKS");
-      return e ? atoi(e) : 0;
-    }();
-    // launch settings of the overlapped batch, restored on every exit path
+    // the overlapped batch launches without programmatic dependent launch
+    // (its waiting CTAs would park on SMs the concurrent step needs)
     struct PrefetchLaunch {
-      explicit PrefetchLaunch(int cap) {
-        set_grid_cap(cap);
-        set_pdl(false);
-      }
-      ~PrefetchLaunch() {
-        set_grid_cap(0);
-        set_pdl(true);
-      }
-    } pf_launch(pf_cap);
+      PrefetchLaunch() { set_pdl(false); }
+      ~PrefetchLaunch() { set_pdl(true); }
+    } pf_launch;
     launch_sample(g, t->bb[k], d_seeds, n_seeds, rng_seed, t->side);
     t->bb[k]->sampled = true;
     GNNV_TRY_CUDA(cudaMemsetAsync(t->d_statsb[k], 0, 4 * sizeof(int64_t), t->side));
-    if (t->mid_pending && !pf_gate().sample) {
-      GNNV_TRY_CUDA(cudaStreamWaitEvent(t->side, t->ev_mid, 0));
-      t->mid_pending = false;
-    }
     if (tl) tl->mark(t->side, "pf_gather");
+    if (t->c->dynamic && t->cache_pending) GNNV_TRY_CUDA(cudaStreamWaitEvent(t->side, t->ev_cache, 0));
     launch_gather(t->c, t->bb[k], t->X[k], t->d_statsb[k], t->side, t->rowidx[k], !t->x_rows);
     if (t->c->dynamic) {  // NEXT-3 admission
       if (tl) tl->mark(t->side, "pf_replace");
       launch_cache_update(t->c, t->bb[k], t->X[k], t->side);
+      GNNV_TRY_CUDA(cudaEventRecord(t->ev_cache, t->side));
+      t->cache_pending = true;
     }
 
     if (tl) tl->mark(t->side, "end");
@@ -598,6 +516,13 @@ gnnv_status gnnv_trainer_prefetch(gnnv_trainer* t, const int32_t* seeds, int32_t
     t->pending = true;
     t->pend_n = n_seeds;
     t->pend_rng = rng_seed;
+  });
+}
+
+gnnv_status gnnv_trainer_join_prefetch(gnnv_trainer* t, gnnv_stream stream) {
+  return guarded([&] {
+    GNNV_REQUIRE(t, GNNV_ERR_PARAM, "join_prefetch: null");
+    if (t->pending) GNNV_TRY_CUDA(cudaStreamWaitEvent((cudaStream_t)stream, t->ev_ready[t->cur ^ 1], 0));
   });
 }
 
@@ -637,10 +562,13 @@ gnnv_status gnnv_step(gnnv_trainer* t, const int32_t* seeds, int32_t n_seeds, in
       GNNV_TRY_CUDA(cudaMemsetAsync(t->d_stats, 0, 4 * sizeof(int64_t), s));
       if (tm) GNNV_TRY_CUDA(cudaEventRecord(t->ev[1], s));
       if (tl) tl->mark(s, "gather");
+      if (t->c->dynamic && t->cache_pending) GNNV_TRY_CUDA(cudaStreamWaitEvent(s, t->ev_cache, 0));
       launch_gather(t->c, t->b, t->H[0], t->d_stats, s, t->rowidx[t->cur], !t->x_rows);
       if (t->c->dynamic) {  // NEXT-3 admission (Eq.5's t_replace)
         if (tl) tl->mark(s, "replace");
         launch_cache_update(t->c, t->b, t->H[0], s);
+        GNNV_TRY_CUDA(cudaEventRecord(t->ev_cache, s));
+        t->cache_pending = true;
       }
       if (tm) GNNV_TRY_CUDA(cudaEventRecord(t->ev[2], s));
     }
@@ -653,10 +581,6 @@ gnnv_status gnnv_step(gnnv_trainer* t, const int32_t* seeds, int32_t n_seeds, in
       layer_fwd_impl(b, i, &ld, t->H[i - 1], t->d_params + t->w_off[i - 1], t->d_params + t->b_off[i - 1], t->H[i],
                      t->A[i], s, tl, t->mbits[i], t->table, i == 1 ? t->rowidx[t->cur] : nullptr,
                      i == 1 ? xr1 : nullptr);
-      if (pf_gate().phase == 'f' && i == pf_gate().layer) {
-        GNNV_TRY_CUDA(cudaEventRecord(t->ev_mid, s));
-        t->mid_pending = true;
-      }
     }
     if (tm) GNNV_TRY_CUDA(cudaEventRecord(t->ev[3], s));
     float* d_loss = t->d_grads + t->nparams;
@@ -710,10 +634,6 @@ gnnv_status gnnv_step(gnnv_trainer* t, const int32_t* seeds, int32_t n_seeds, in
                      i > 1 ? t->G[i - 1] : nullptr, t->d_grads + t->w_off[i - 1], t->d_grads + t->b_off[i - 1], s, tl,
                      t->mbits[i], t->mbits[i] != nullptr, t->mbits[i - 1], mask_words(t->md.dims[i - 1]),
                      i == 1 ? xr1 : nullptr, t->tail);
-      if (pf_gate().phase == 'b' && i == pf_gate().layer) {
-        GNNV_TRY_CUDA(cudaEventRecord(t->ev_mid, s));
-        t->mid_pending = true;
-      }
     }
     if (tm) GNNV_TRY_CUDA(cudaEventRecord(t->ev[5], s));
     if (tl) tl->mark(s, "allreduce");

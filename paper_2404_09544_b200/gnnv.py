@@ -123,12 +123,13 @@ _SIGS = {
     "gnnv_trainer_rowidx": (I32, [VP, C.POINTER(C.c_void_p), C.POINTER(C.c_void_p)]),
     "gnnv_trainer_loss_async": (I32, [VP, VP, VP]),
     "gnnv_trainer_loss_result": (I32, [VP, C.c_int64, VP]),
-    "gnnv_trainer_set_locality": (I32, [VP, I32]),
-    "gnnv_blocks_set_locality": (I32, [VP, VP, I32]),
+    "gnnv_trainer_set_locality": (I32, [VP, F64]),
+    "gnnv_blocks_set_locality": (I32, [VP, VP, F64]),
     "gnnv_trainer_activation": (I32, [VP, I32, PP, C.POINTER(I32)]),
     "gnnv_step": (I32, [VP, VP, I32, I32, I32, U64, F32, C.POINTER(F32), C.POINTER(StepTiming), VP]),
     "gnnv_trainer_stats": (I32, [VP, VP]),
     "gnnv_trainer_prefetch": (I32, [VP, VP, I32, I32, U64, VP]),
+    "gnnv_trainer_join_prefetch": (I32, [VP, VP]),
     "gnnv_trainer_read_loss": (I32, [VP, C.POINTER(F32), VP]),
     "gnnv_trainer_timeline": (I32, [VP, I32]),
     "gnnv_trainer_timeline_read": (I32, [VP, C.POINTER(Segment), I32, C.POINTER(I32)]),
@@ -185,14 +186,6 @@ def version() -> str:
 
 def launch_count() -> int:
     return int(load().gnnv_launch_count())
-
-
-def locality_weight(bias: float) -> int:
-    """1 + 4 bias for bias in {0, 0.25, 0.5, 0.75, 1} (reading Q26)."""
-    w = 1.0 + 4.0 * float(bias)
-    if not (0.0 <= bias <= 1.0) or abs(w - round(w)) > 1e-12:
-        raise GnnvError(ERR_PARAM, "locality bias must be in {0, 0.25, 0.5, 0.75, 1}")
-    return int(round(w))
 
 
 def row_stride(d: int) -> int:
@@ -358,7 +351,7 @@ class Blocks:
 
     def set_locality(self, cache: Optional["Cache"], bias: float):
         """Locality-biased sampling (NEXT-2): cached neighbours weigh 1 + 4 bias."""
-        _check(load().gnnv_blocks_set_locality(self.h, cache.h if cache else None, locality_weight(bias)))
+        _check(load().gnnv_blocks_set_locality(self.h, cache.h if cache else None, float(bias)))
 
     def info(self, sync: bool = True, stream=None) -> List[BlockView]:
         arr = (BlockView * self.L)()
@@ -486,6 +479,10 @@ class Trainer:
         _check(load().gnnv_trainer_prefetch(self.h, ptr(seeds), int(n_seeds), 1 if on_host else 0,
                                             int(rng_seed) & 0xFFFFFFFFFFFFFFFF, stream_ptr(stream)))
 
+    def join_prefetch(self, stream=None):
+        """`stream` waits for the pending prefetch (not consumed)."""
+        _check(load().gnnv_trainer_join_prefetch(self.h, stream_ptr(stream)))
+
     def read_loss(self, stream=None) -> float:
         out = C.c_float(0.0)
         _check(load().gnnv_trainer_read_loss(self.h, C.byref(out), stream_ptr(stream)))
@@ -518,7 +515,7 @@ class Trainer:
 
     def set_locality(self, bias: float):
         """Locality-biased sampling (NEXT-2) for the trainer's batches."""
-        _check(load().gnnv_trainer_set_locality(self.h, locality_weight(bias)))
+        _check(load().gnnv_trainer_set_locality(self.h, float(bias)))
 
     def x_level(self) -> int:
         """Frontier level whose rows X holds: L (all of F_L), L-1 (dst prefix) or -1 (none)."""

@@ -1,18 +1,19 @@
 """-m gpu parity at BASELINE.json's full sizes, in the launch configuration
 bench.py times (Trainer, Eq.4 prefetch of device seeds on its own stream,
-step on a high-priority stream, tf32 tensor-core GEMMs), against the oracle
-on the same seeded inputs.
+step on a high-priority stream), against the oracle on the same seeded
+inputs, for configs[0..3] -- Cora (ratio 0.2, d = 1433), arxiv (3 layers,
+ratio 0.5), Reddit (fanout 25, d = 602, ratio 0.1 and 1.0: misses read
+zero-copy from pinned host memory / the whole table in HBM), products (the
+bench workload) -- each in tf32 (the bench's GEMMs) and fp32 (parity mode);
+configs[4] (papers100M) is tests/test_gpu_papers100m.py.
 
-* products (configs[3], the bench workload): the whole step.  Sampling,
-  relabelling, gather and hit counters bit-exact over EVERY row; layer 1 on a
-  sample of 2048 dst rows (a row-restricted block -- rows are independent
-  problems), layers 2-3 on all rows, each fed the GPU's own input; loss;
-  every weight/bias gradient elementwise against the oracle's backward chain
-  run on the GPU's forward values (condition-aware, one rtol per GEMM stage
-  from the loss); every gradient's direction vs the oracle's own fp64 step.
-  Both tf32 (bench) and fp32 (parity mode).
-* arxiv (ratio 0.5) and Reddit (ratio 0.1): misses read zero-copy from
-  pinned host memory -- blocks, gathered rows and counters bit-exact.
+Per case, the whole step (full_step_check): sampling, relabelling, gather
+and hit counters bit-exact over EVERY row; each layer elementwise on the
+GPU's own input (a large layer on 2048 sampled dst rows as a row-restricted
+block -- rows are independent problems); loss; every weight/bias gradient
+elementwise against the oracle's backward chain run on the GPU's forward
+values (condition-aware, one rtol per GEMM stage from the loss); every
+gradient's direction vs the oracle's own fp64 step.
 """
 import numpy as np
 import pytest
@@ -23,20 +24,14 @@ from oracle.cache import access_counts, cache_slots
 from oracle.layers import agg_matrix, ce_loss, layer_bwd, layer_fwd, train_step
 from oracle.sampler import Block, sample_blocks
 from paper_2404_09544_b200 import gnnv
-from synth import BASE_RNG_SEED, CONFIGS, epoch_seeds, init_weights, make_graph
+from synth import BASE_RNG_SEED, CONFIGS, epoch_seeds, init_weights
+from synth.store import shared_graph
 
 from gpu_util import assert_close_cond, blocks_to_host, lib, normwise, read_f32, read_i32
 
 pytestmark = pytest.mark.gpu
 
 RTOL = {0: 1e-5, 2: 4e-3}  # fp32 / tf32, as test_gpu_parity (reading Q17, Q22)
-
-
-@pytest.fixture(scope="module")
-def products():
-    lib()
-    gd = make_graph("products")
-    return gd, gnnv.Graph.from_data(gd)
 
 
 def sub_block(ob: Block, H_src: np.ndarray, rows: np.ndarray):
@@ -107,99 +102,125 @@ def _blk(hb, h):
     return Block(n_dst=nd, n_src=ns, indptr=ptr.astype(np.int64), indices=idx.astype(np.int64), src_global=F)
 
 
-@pytest.mark.parametrize("prec", [2, 0])
-def test_products_full_step(products, prec):
-    gd, g = products
-    cfg = CONFIGS["products"]
-    dims = [gd.d, cfg["hidden"], cfg["hidden"], gd.C]
-    L = len(cfg["fanouts"])
-    w = init_weights(dims)
-    cache = gnnv.Cache(g, cfg["ratio"])
-    B = cfg["batch"]
-    tr = gnnv.Trainer(g, cache, dims, cfg["fanouts"], B, w, prec=prec)
-    perm = epoch_seeds(gd.n, 0)
-    t = 10  # a bench-timed iteration index (after the warm-up)
-    seeds = perm[t * B:(t + 1) * B]
-    rs = BASE_RNG_SEED + t
-    lr = 0.01
-    d_seeds = torch.as_tensor(seeds.astype(np.int32)).cuda()
-    loss = pipelined_step(tr, d_seeds, B, B, rs, lr)
-    ref = train_step(gd.indptr, gd.indices, gd.feats, gd.d, gd.labels, seeds, cfg["fanouts"], rs, w, lr)
-    hb = check_blocks_and_gather(gd, tr, ref["frontiers"], ref["blocks"], cfg["ratio"])
-    grads = gnnv.unflat_params(tr.grads(), dims)
-    rtol = RTOL[prec]
-    assert abs(loss - ref["loss"]) <= (1e-4 if prec == 0 else 5e-3) * abs(ref["loss"])
-    # forward chain, each layer fed the GPU's own input (reading Q24)
-    rng = np.random.default_rng(0)
-    H = [None] * (L + 1)
-    blks = [None] * (L + 1)
-    for i in range(1, L + 1):
-        ob = blks[i] = _blk(hb, L - i)
-        p_in, s_in = tr.activation(i - 1)
-        p_out, s_out = tr.activation(i)
-        if i == 1 and tr.x_level() < L:  # layer 1 read the cache table (checked above): the exact feature rows
-            Hin = oracle.gather_rows(gd.feats, hb[L - 1][4])[:, : dims[0]]
-        else:
-            Hin = read_f32(p_in, ob.n_src, s_in)[:, : dims[i - 1]]
-        Hout = read_f32(p_out, ob.n_dst, s_out)[:, : dims[i]]
-        H[i - 1], H[i] = Hin, Hout
-        Wi, bi = w[i - 1]
-        if i == 1:  # 2048 sampled dst rows of the 0.5M-row layer
-            rows = np.sort(rng.choice(ob.n_dst, 2048, replace=False))
-            blk, Hs = sub_block(ob, Hin, rows)
-            Ho, _ = layer_fwd(blk, Hs, Wi, bi, True)
-            Hm, _ = layer_fwd(blk, Hs, Wi, bi, True, absval=True)
-            assert_close_cond(Hout[rows], Ho, Hm, rtol, "layer 1 (sampled rows)")
-        else:
-            Ho, _ = layer_fwd(ob, Hin, Wi, bi, i < L)
-            Hm, _ = layer_fwd(ob, Hin, Wi, bi, i < L, absval=True)
-            assert_close_cond(Hout, Ho, Hm, rtol, f"layer {i}")
-    # backward chain on the GPU's forward values (its logits, its ReLU masks):
-    # every gradient elementwise against the condition-aware bound, the
-    # magnitude propagated by the same chain on |.|; each GEMM stage between
-    # the loss and layer i adds at most rtol of that magnitude.
-    _, G = ce_loss(H[L], gd.labels[seeds], B)
-    M = np.abs(G)
-    for i in range(L, 0, -1):
-        ob = blks[i]
-        A = agg_matrix(ob) @ H[i - 1].astype(np.float64)
-        Wi = w[i - 1][0]
-        rW, rb, rX = layer_bwd(ob, H[i - 1], A, H[i], Wi, G, relu=(i < L), need_dx=(i > 1))
-        mW, mb, mX = layer_bwd(ob, np.abs(H[i - 1]), np.abs(A), H[i], np.abs(Wi), M, relu=(i < L),
-                               need_dx=(i > 1))
-        stages = L - i + 1
-        assert_close_cond(grads[i - 1][0], rW, mW, rtol * stages, f"dW layer {i}")
-        assert_close_cond(grads[i - 1][1], rb, mb, rtol * stages, f"db layer {i}")
-        G, M = rX, mX
-    # and the direction of every gradient vs the oracle's own fp64 step
-    for i, ((gW, gb), (rW_, rb_)) in enumerate(zip(grads, ref["grads"])):
-        for a_, b_ in ((gW, rW_), (gb, rb_)):
-            cos = float(np.dot(a_.ravel(), b_.ravel()) / (np.linalg.norm(a_) * np.linalg.norm(b_) + 1e-30))
-            assert cos > 0.98, (i, cos)
+_GRAPHS = {}
+_REFS = {}
 
 
-@pytest.mark.parametrize("name", ["arxiv", "reddit"])
-def test_host_miss_configs_full_size(name):
-    """configs[1] (arxiv, ratio 0.5) and configs[2] (Reddit, ratio 0.1, and
-    the full-cache end of the sweep): the whole batch's blocks, gathered
-    rows (misses zero-copy from pinned host) and counters, bit-exact."""
-    lib()
+def graph_of(name):
+    """(GraphData, gnnv.Graph) of a config, generated once per session
+    (through the box's shared host store, synth.store)."""
+    if name not in _GRAPHS:
+        lib()
+        gd = shared_graph(name)
+        _GRAPHS[name] = (gd, gnnv.Graph.from_data(gd))
+    return _GRAPHS[name]
+
+
+def dims_of(name, gd):
     cfg = CONFIGS[name]
-    gd = make_graph(name)
-    g = gnnv.Graph.from_data(gd)
-    dims = [gd.d] + [cfg["hidden"]] * (len(cfg["fanouts"]) - 1) + [gd.C]
-    w = init_weights(dims)
+    return [gd.d] + [cfg["hidden"]] * (len(cfg["fanouts"]) - 1) + [gd.C]
+
+
+T_BENCH = 10  # a bench-timed iteration index (after the warm-up)
+
+
+def oracle_ref(name):
+    """The oracle's own fp64 step on iteration T_BENCH's batch (independent of
+    the cache ratio and the GEMM precision, so computed once per config)."""
+    if name not in _REFS:
+        gd, _ = graph_of(name)
+        cfg = CONFIGS[name]
+        B = cfg["batch"]
+        seeds = epoch_seeds(gd.n, 0)[T_BENCH * B:(T_BENCH + 1) * B]
+        w = init_weights(dims_of(name, gd))
+        ref = train_step(gd.indptr, gd.indices, gd.feats, gd.d, gd.labels, seeds, cfg["fanouts"],
+                         BASE_RNG_SEED + T_BENCH, w, 0.01)
+        _REFS[name] = (seeds, w, ref)
+    return _REFS[name]
+
+
+def full_step_check(name, ratio, prec, max_rows=2048):
+    """One step of config `name` as bench.py runs it (Trainer, Eq.4 prefetch
+    of device seeds, step on a high-priority stream) against the oracle:
+    blocks, frontiers, gathered rows and counters bit-exact over every row;
+    every layer of the forward chain elementwise on the GPU's own input (at
+    most max_rows sampled dst rows of a large layer, as row-restricted
+    blocks); the loss; every dW/db elementwise through the oracle's backward
+    chain on the GPU's forward values (condition-aware, one rtol per GEMM
+    stage from the loss); every gradient's direction vs the oracle's own
+    fp64 step."""
+    gd, g = graph_of(name)
+    cfg = CONFIGS[name]
+    dims = dims_of(name, gd)
+    L = len(cfg["fanouts"])
+    seeds, w, ref = oracle_ref(name)
     B = cfg["batch"]
-    perm = epoch_seeds(gd.n, 0)
-    seeds = perm[:B]
-    rs = BASE_RNG_SEED + 3
-    F, blocks = sample_blocks(gd.indptr, gd.indices, seeds, cfg["fanouts"], rs)
-    d_seeds = torch.as_tensor(seeds.astype(np.int32)).cuda()
-    for ratio in sorted({cfg["ratio"], 1.0}):
-        cache = gnnv.Cache(g, ratio)
-        tr = gnnv.Trainer(g, cache, dims, cfg["fanouts"], B, w, prec=gnnv.PREC_TF32)
-        loss = pipelined_step(tr, d_seeds, B, B, rs, 0.01)
-        assert np.isfinite(loss)
-        check_blocks_and_gather(gd, tr, F, blocks, ratio)
+    cache = gnnv.Cache(g, ratio)
+    tr = gnnv.Trainer(g, cache, dims, cfg["fanouts"], B, w, prec=prec)
+    try:
+        d_seeds = torch.as_tensor(seeds.astype(np.int32)).cuda()
+        loss = pipelined_step(tr, d_seeds, B, B, BASE_RNG_SEED + T_BENCH, 0.01)
+        hb = check_blocks_and_gather(gd, tr, ref["frontiers"], ref["blocks"], ratio)
+        grads = gnnv.unflat_params(tr.grads(), dims)
+        rtol = RTOL[prec]
+        assert abs(loss - ref["loss"]) <= (1e-4 if prec == 0 else 5e-3) * abs(ref["loss"]), (loss, ref["loss"])
+        # forward chain, each layer fed the GPU's own input (reading Q24)
+        rng = np.random.default_rng(0)
+        H = [None] * (L + 1)
+        blks = [None] * (L + 1)
+        for i in range(1, L + 1):
+            ob = blks[i] = _blk(hb, L - i)
+            p_in, s_in = tr.activation(i - 1)
+            p_out, s_out = tr.activation(i)
+            if i == 1 and tr.x_level() < L:  # layer 1 read the cache table (checked above): the exact feature rows
+                Hin = oracle.gather_rows(gd.feats, hb[L - 1][4])[:, : dims[0]]
+            else:
+                Hin = read_f32(p_in, ob.n_src, s_in)[:, : dims[i - 1]]
+            Hout = read_f32(p_out, ob.n_dst, s_out)[:, : dims[i]]
+            H[i - 1], H[i] = Hin, Hout
+            Wi, bi = w[i - 1]
+            if ob.n_dst > max_rows:
+                rows = np.sort(rng.choice(ob.n_dst, max_rows, replace=False))
+                blk, Hs = sub_block(ob, Hin, rows)
+                Ho, _ = layer_fwd(blk, Hs, Wi, bi, i < L)
+                Hm, _ = layer_fwd(blk, Hs, Wi, bi, i < L, absval=True)
+                assert_close_cond(Hout[rows], Ho, Hm, rtol, f"{name} layer {i} (sampled rows)")
+            else:
+                Ho, _ = layer_fwd(ob, Hin, Wi, bi, i < L)
+                Hm, _ = layer_fwd(ob, Hin, Wi, bi, i < L, absval=True)
+                assert_close_cond(Hout, Ho, Hm, rtol, f"{name} layer {i}")
+        # backward chain on the GPU's forward values (its logits, its ReLU
+        # masks): each GEMM stage between the loss and layer i adds at most
+        # rtol of the magnitude propagated by the same chain on |.|
+        _, G = ce_loss(H[L], gd.labels[seeds], B)
+        M = np.abs(G)
+        for i in range(L, 0, -1):
+            ob = blks[i]
+            A = agg_matrix(ob) @ H[i - 1].astype(np.float64)
+            Wi = w[i - 1][0]
+            rW, rb, rX = layer_bwd(ob, H[i - 1], A, H[i], Wi, G, relu=(i < L), need_dx=(i > 1))
+            mW, mb, mX = layer_bwd(ob, np.abs(H[i - 1]), np.abs(A), H[i], np.abs(Wi), M, relu=(i < L),
+                                   need_dx=(i > 1))
+            stages = L - i + 1
+            assert_close_cond(grads[i - 1][0], rW, mW, rtol * stages, f"{name} dW layer {i}")
+            assert_close_cond(grads[i - 1][1], rb, mb, rtol * stages, f"{name} db layer {i}")
+            G, M = rX, mX
+        # and the direction of every gradient vs the oracle's own fp64 step
+        for i, ((gW, gb), (rW_, rb_)) in enumerate(zip(grads, ref["grads"])):
+            for a_, b_ in ((gW, rW_), (gb, rb_)):
+                cos = float(np.dot(a_.ravel(), b_.ravel()) / (np.linalg.norm(a_) * np.linalg.norm(b_) + 1e-30))
+                assert cos > 0.98, (name, i, cos)
+    finally:
         tr.free()
         cache.free()
+
+
+# BASELINE.json configs[0..3] at their own cache ratios (and the full-cache
+# end of configs[2]'s sweep); tf32 = the bench's precision, fp32 = parity mode
+CASES = [("cora", 0.2), ("arxiv", 0.5), ("reddit", 0.1), ("reddit", 1.0), ("products", 1.0)]
+
+
+@pytest.mark.parametrize("prec", [2, 0], ids=["tf32", "fp32"])
+@pytest.mark.parametrize("name,ratio", CASES, ids=[f"{n}@{r}" for n, r in CASES])
+def test_full_step(name, ratio, prec):
+    full_step_check(name, ratio, prec)

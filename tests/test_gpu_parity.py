@@ -348,6 +348,40 @@ def test_step_device_seeds_and_errors(mini):
     assert l3 == l1
 
 
+def test_device_seed_out_of_range(mini):
+    """DEVICE seeds are range-checked on the device (host seeds on the host):
+    an id outside [0, N) makes the step report PARAM at its sync point, no
+    kernel reads out of bounds (the id is replaced by vertex 0), the SGD
+    update of that step is skipped, and the flag does not outlive the batch
+    -- the next valid step (also through the asynchronous loss ring)
+    succeeds."""
+    gd, g = mini
+    dims = [gd.d, 32, gd.C]
+    cache = gnnv.Cache(g, 0.5)
+    tr = gnnv.Trainer(g, cache, dims, [5, 5], 128, init_weights(dims))
+    seeds = epoch_seeds(gd.n, 3)[:128]
+    p0 = tr.params().copy()
+    for bad_id in (gd.n, -7, 2**31 - 1):
+        bad = seeds.copy()
+        bad[17] = bad_id
+        with pytest.raises(gnnv.GnnvError) as e:
+            tr.step(dev_i32(bad), 128, 128, 9, 0.1, on_host=False)
+        assert e.value.status == gnnv.ERR_PARAM
+        np.testing.assert_array_equal(tr.params(), p0)  # the bad batch was not applied
+    # asynchronous path: the bad step's ticket reports PARAM, the next one is clean
+    tr.step(dev_i32(bad), 128, 128, 9, 0.1, on_host=False, want_loss=False)
+    t_bad = tr.loss_async()
+    tr.step(dev_i32(seeds), 128, 128, 9, 0.0, on_host=False, want_loss=False)
+    t_ok = tr.loss_async()
+    with pytest.raises(gnnv.GnnvError):
+        tr.loss_result(t_bad)
+    assert np.isfinite(tr.loss_result(t_ok))
+    l_ok, _ = tr.step(dev_i32(seeds), 128, 128, 9, 0.0, on_host=False)
+    assert np.isfinite(l_ok)
+    np.testing.assert_array_equal(tr.params(), p0)
+    tr.free()
+
+
 @pytest.mark.parametrize("prec", [0, 1, 2])
 @pytest.mark.parametrize("d_in,d_out,kind", [(1433, 256, 0), (256, 256, 0), (256, 47, 0), (602, 41, 0),
                                              (128, 40, 1), (100, 256, 0), (7, 13, 0), (256, 172, 1)])
@@ -488,8 +522,11 @@ def test_biased_trainer_raises_hit_rate(mini):
         misses.append(st[3] / st[0])
         tr.free()
     assert misses[0] > misses[1] > misses[2], misses
-    with pytest.raises(gnnv.GnnvError):
-        gnnv.locality_weight(0.3)
+    tr = gnnv.Trainer(g, cache, dims, cfg["fanouts"], cfg["batch"], init_weights(dims), prec=2)
+    for bad in (0.3, -0.25, 1.25):  # the library validates the bias itself (1 + 4b must be an integer in 1..5)
+        with pytest.raises(gnnv.GnnvError):
+            tr.set_locality(bad)
+    tr.free()
 
 
 # ------------------------------------------------- dynamic cache (NEXT-3)
@@ -555,6 +592,37 @@ def test_dynamic_cache_trainer_pipelined(mini):
         oF, _ = sample_blocks(gd.indptr, gd.indices, batches[i], cfg["fanouts"], 200 + i)
         out = ref.access_batch(oF[-1])
         assert st == [out["rows"], out["hits"], 0, out["misses"]], (i, st, out)
+    tr.free()
+    torch.cuda.synchronize()
+    assert cache.counters().tolist()[:3] == [ref.hits, ref.misses, ref.replaced]
+
+
+def test_dynamic_cache_serial_then_prefetch(mini):
+    """a serial step's admission must be ordered before a
+    following prefetch's gather + admission (the prefetch runs on the
+    trainer's side stream).  step, prefetch, step, step(serial), prefetch,
+    step with an LRU cache: per-step counters equal the oracle's sequence."""
+    from oracle.cache import DynamicCache
+
+    gd, g = mini
+    cfg = CONFIGS["mini"]
+    dims = [gd.d, cfg["hidden"], cfg["hidden"], gd.C]
+    B = cfg["batch"]
+    cache = gnnv.Cache(g, 0.1, policy=3)
+    ref = DynamicCache(gd.n, int(np.floor(0.1 * gd.n)), 3)
+    tr = gnnv.Trainer(g, cache, dims, cfg["fanouts"], B, init_weights(dims), prec=2)
+    perm = epoch_seeds(gd.n, 0)
+    batches = [perm[(i % 3) * B:(i % 3 + 1) * B] for i in range(5)]
+    other = torch.cuda.Stream()  # host seeds: no stream dependency at all
+    plan = ["serial", "prefetched", "serial", "serial", "prefetched"]
+    for i, how in enumerate(plan):
+        if how == "prefetched":
+            tr.prefetch(batches[i], B, 300 + i, on_host=True, stream=other)
+        tr.step(batches[i], B, B, 300 + i, 0.01, want_loss=False)
+        st = tr.stats().tolist()
+        oF, _ = sample_blocks(gd.indptr, gd.indices, batches[i], cfg["fanouts"], 300 + i)
+        out = ref.access_batch(oF[-1])
+        assert st == [out["rows"], out["hits"], 0, out["misses"]], (i, how, st, out)
     tr.free()
     torch.cuda.synchronize()
     assert cache.counters().tolist()[:3] == [ref.hits, ref.misses, ref.replaced]
