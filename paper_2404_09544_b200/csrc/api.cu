@@ -17,15 +17,18 @@ static std::atomic<unsigned long long> g_launches{0};
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 static thread_local bool t_pdl_off = false;
 void set_pdl(bool on) { t_pdl_off = !on; }
+static std::mutex g_opt_mu;
+static std::vector<std::pair<std::string, int>> g_opt_override;  // gnnv_set_option
+static std::vector<std::pair<std::string, bool>> g_opt_env;      // environment, read once
 bool env_on(const char* name) {
-  static std::mutex mu;
-  static std::vector<std::pair<std::string, bool>> cache;
-  std::lock_guard<std::mutex> lk(mu);
-  for (auto& kv : cache)
+  std::lock_guard<std::mutex> lk(g_opt_mu);
+  for (auto& kv : g_opt_override)
+    if (kv.first == name && kv.second >= 0) return kv.second != 0;
+  for (auto& kv : g_opt_env)
     if (kv.first == name) return kv.second;
   const char* e = getenv(name);
   const bool on = e && e[0] && strcmp(e, "0") != 0;
-  cache.emplace_back(name, on);
+  g_opt_env.emplace_back(name, on);
   return on;
 }
 bool pdl_enabled() {
@@ -138,6 +141,24 @@ void* gnnv_blocks::ensure_scratch(size_t bytes, cudaStream_t s) {
 extern "C" {
 
 const char* gnnv_last_error(void) { return get_error(); }
+
+gnnv_status gnnv_set_option(const char* name, int32_t value) {
+  return guarded([&] {
+    static const char* known[] = {"GNNV_XROWS", "GNNV_GEMM_PAIR", "GNNV_BWD_PULL", "GNNV_NO_TAIL", "GNNV_NO_PDL",
+                                  "GNNV_NO_L2PUSH"};
+    GNNV_REQUIRE(name, GNNV_ERR_PARAM, "set_option: null name");
+    bool ok = false;
+    for (const char* k : known) ok |= strcmp(k, name) == 0;
+    GNNV_REQUIRE(ok, GNNV_ERR_PARAM, std::string("set_option: unknown option ") + name);
+    std::lock_guard<std::mutex> lk(g_opt_mu);
+    for (auto& kv : g_opt_override)
+      if (kv.first == name) {
+        kv.second = value;
+        return;
+      }
+    g_opt_override.emplace_back(name, value);
+  });
+}
 const char* gnnv_version(void) { return GNNV_VERSION " sm_100a"; }
 uint64_t gnnv_launch_count(void) { return g_launches.load(); }
 int32_t gnnv_row_stride(int32_t d) { return row_stride(d); }

@@ -82,6 +82,7 @@ PP = C.POINTER(C.c_void_p)
 _SIGS = {
     "gnnv_last_error": (C.c_char_p, []),
     "gnnv_version": (C.c_char_p, []),
+    "gnnv_set_option": (I32, [C.c_char_p, I32]),
     "gnnv_row_stride": (I32, [I32]),
     "gnnv_launch_count": (U64, []),
     "gnnv_graph_load": (I32, [VP, VP, I64, I64, VP, I32, I32, VP, I32, I32, PP]),
@@ -182,6 +183,11 @@ def stream_ptr(s=None) -> Optional[int]:
 
 def version() -> str:
     return load().gnnv_version().decode()
+
+
+def set_option(name: str, value: int):
+    """gnnv_set_option: opt-in variant switches (1 on, 0 off, -1 environment)."""
+    _check(load().gnnv_set_option(name.encode(), int(value)))
 
 
 def launch_count() -> int:

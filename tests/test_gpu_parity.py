@@ -33,6 +33,20 @@ def mini():
     return gd, g
 
 
+@pytest.fixture
+def option():
+    """gnnv.set_option(name, value) for one test; back to the environment after."""
+    names = []
+
+    def set_(name, value):
+        gnnv.set_option(name, value)
+        names.append(name)
+
+    yield set_
+    for n in names:
+        gnnv.set_option(n, -1)
+
+
 @pytest.fixture(scope="module")
 def cora():
     lib()
@@ -700,7 +714,7 @@ def test_step_degenerate_graph(kind, prec):
         assert normwise(gb, rb) < (1e-4 if prec == 0 else 2e-2)
 
 
-def test_step_whole_table_gather4(mini, monkeypatch):
+def test_step_whole_table_gather4(mini, option):
     """Whole table cached, tf32 SAGE: the layer-1 GEMMs (forward and dW) read
     H_dst straight from the degree-ordered table with TMA gather4 through the
     gather's row indices and X is never written (x_level -1).  The forward
@@ -715,7 +729,7 @@ def test_step_whole_table_gather4(mini, monkeypatch):
     L = len(cfg["fanouts"])
     seeds = epoch_seeds(gd.n, 0)[: cfg["batch"]]
     out = {}
-    monkeypatch.setenv("GNNV_XROWS", "1")  # read when a trainer is created
+    option("GNNV_XROWS", 1)  # read when a trainer is created
     for name, ratio in (("rows", 1.0), ("copy", (gd.n - 1) / gd.n)):
         tr = gnnv.Trainer(g, gnnv.Cache(g, ratio), dims, cfg["fanouts"], cfg["batch"], w, prec=gnnv.PREC_TF32)
         loss, _ = tr.step(seeds, len(seeds), len(seeds), 0x5EED, 0.05)
@@ -742,9 +756,9 @@ def test_step_whole_table_gather4(mini, monkeypatch):
 
 
 @pytest.mark.parametrize("aggr", [gnnv.AGGR_MEAN, gnnv.AGGR_SUM])
-def test_fused_output_layer_matches_per_kernel_path(mini, monkeypatch, aggr):
+def test_fused_output_layer_matches_per_kernel_path(mini, option, aggr):
     """The tf32 trainer runs its output layer (layer-L forward, CE loss,
-    layer-L backward) as the two fused kernels of tail.cu; GNNV_NO_TAIL=1
+    layer-L backward) as the two fused kernels of tail.cu; gnnv_set_option("GNNV_NO_TAIL", 1)
     (read when a trainer is created) keeps the seven per-kernel launches.
     Same step, same inputs: the loss, the logits, dH of layer L-1 and every
     gradient agree to the tf32 GEMM rounding, and both match the oracle."""
@@ -756,8 +770,7 @@ def test_fused_output_layer_matches_per_kernel_path(mini, monkeypatch, aggr):
     seeds = epoch_seeds(gd.n, 0)[: cfg["batch"]]
     out = {}
     for name in ("fused", "split"):
-        if name == "split":
-            monkeypatch.setenv("GNNV_NO_TAIL", "1")
+        option("GNNV_NO_TAIL", 1 if name == "split" else 0)
         tr = gnnv.Trainer(g, gnnv.Cache(g, cfg["ratio"]), dims, cfg["fanouts"], cfg["batch"], w, aggr=aggr,
                           prec=gnnv.PREC_TF32)
         tr.timeline(True)
@@ -783,7 +796,7 @@ def test_fused_output_layer_matches_per_kernel_path(mini, monkeypatch, aggr):
 
 
 @pytest.mark.parametrize("d_in,d_out", [(100, 256), (64, 64), (64, 96)])
-def test_layer_fwd_cta_pair_gemm(mini, monkeypatch, d_in, d_out):
+def test_layer_fwd_cta_pair_gemm(mini, option, d_in, d_out):
     """The CTA-pair (tcgen05 cta_group::2, M = 256) forward GEMM, GNNV_GEMM_PAIR=1:
     a tf32 SAGE layer forward equals the single-CTA GEMM's bit for bit (the
     same tf32 products accumulated in the same K order per output element)
@@ -806,7 +819,7 @@ def test_layer_fwd_cta_pair_gemm(mini, monkeypatch, d_in, d_out):
     cap_dst, cap_src = view.max_dst, view.max_src
     out = {}
     for pair in ("0", "1"):
-        monkeypatch.setenv("GNNV_GEMM_PAIR", pair)
+        option("GNNV_GEMM_PAIR", int(pair))
         Hdst = torch.full((cap_dst, row_stride(d_out)), float("nan"), device="cuda")
         A = torch.full((cap_dst, s_in), float("nan"), device="cuda")
         gnnv.layer_fwd(blocks, layer, ld, padded(Hsrc, cap_src), dev_f32(W), dev_f32(b), Hdst, A)
@@ -821,7 +834,7 @@ def test_layer_fwd_cta_pair_gemm(mini, monkeypatch, d_in, d_out):
 
 @pytest.mark.parametrize("kind,prec", [(gnnv.KIND_SAGE, gnnv.PREC_FP32), (gnnv.KIND_GCN, gnnv.PREC_FP32),
                                        (gnnv.KIND_SAGE, gnnv.PREC_TF32)])
-def test_backward_pull_matches_push(mini, monkeypatch, kind, prec):
+def test_backward_pull_matches_push(mini, option, kind, prec):
     """The backward aggregation of the layers with a dX (blocks h <= L-2)
     pulls per src row through the block's CSC (sampler: k_map counts, scan,
     k_csc_fill; k_spmm_bwd_pull) with GNNV_BWD_PULL=1 (read when the blocks
@@ -838,8 +851,7 @@ def test_backward_pull_matches_push(mini, monkeypatch, kind, prec):
     seeds = epoch_seeds(gd.n, 0)[: cfg["batch"]]
     out = {}
     for name in ("push", "pull"):
-        if name == "pull":
-            monkeypatch.setenv("GNNV_BWD_PULL", "1")
+        option("GNNV_BWD_PULL", 1 if name == "pull" else 0)
         tr = gnnv.Trainer(g, gnnv.Cache(g, cfg["ratio"]), dims, cfg["fanouts"], cfg["batch"], w, kind=kind,
                           prec=prec)
         tr.timeline(True)
@@ -854,52 +866,3 @@ def test_backward_pull_matches_push(mini, monkeypatch, kind, prec):
                          kind=kname)
         for (gW, gb), (rW, rb) in zip(gnnv.unflat_params(p["grads"], dims, kind), ref["grads"]):
             assert normwise(gW, rW) < 1e-4 and normwise(gb, rb) < 1e-4
-
-
-@pytest.mark.parametrize("kind", [gnnv.KIND_SAGE, gnnv.KIND_GCN])
-@pytest.mark.parametrize("ratio", [0.3, 1.0])
-@pytest.mark.parametrize("hidden", [64, 256, 600])
-def test_spmm_fwd_pipelined_matches_plain(mini, monkeypatch, kind, ratio, hidden):
-    """k_spmm_fwd_pf (opt-in GNNV_SPMM_PF=1, read per launch: indptr, neighbour ids
-    and cache-row mapping of the rows S, 2S, 3S ahead in flight while the
-    current row's neighbour rows load) sums in the plain kernel's order, so a
-    whole fp32 forward -- loss and every activation level -- is bitwise
-    identical to the step with the plain kernel (the default); the gradients
-    agree up to the backward's atomic summation order.
-    ratio 1.0 runs layer 1 through the table (rowidx) path, 0.3 through X;
-    hidden 64/256/600 covers LPR 16, 32 and rows wider than one warp pass
-    (d > 128 floats), and both match the oracle's step."""
-    gd, g = mini
-    cfg = CONFIGS["mini"]
-    dims = [gd.d, hidden, hidden, gd.C]
-    kname = "sage" if kind == gnnv.KIND_SAGE else "gcn"
-    w = init_weights(dims, kind=kname)
-    seeds = epoch_seeds(gd.n, 0)[: cfg["batch"]]
-    out = {}
-    for name in ("plain", "pf"):
-        if name == "pf":
-            monkeypatch.setenv("GNNV_SPMM_PF", "1")
-        tr = gnnv.Trainer(g, gnnv.Cache(g, ratio), dims, cfg["fanouts"], cfg["batch"], w, kind=kind,
-                          prec=gnnv.PREC_FP32)
-        loss, _ = tr.step(seeds, len(seeds), len(seeds), 0x5EED, 0.05)
-        hb = blocks_to_host(tr.blocks)
-        acts = []
-        for lvl in range(1, len(dims)):
-            p, s = tr.activation(lvl)
-            acts.append(read_f32(p, hb[len(dims) - 1 - lvl][0], s)[:, : dims[lvl]])
-        out[name] = dict(loss=loss, grads=tr.grads(), acts=acts)
-    p, q = out["pf"], out["plain"]
-    assert p["loss"] == q["loss"]
-    for a_, b_ in zip(p["acts"], q["acts"]):
-        assert np.array_equal(a_, b_)
-    # the backward's atomic adds of repeated src ids (k_spmm_bwd phase 2) fix
-    # no summation order, so the gradients agree to fp32 rounding, not bitwise
-    assert normwise(p["grads"], q["grads"]) < 1e-5
-    ref = train_step(gd.indptr, gd.indices, gd.feats, gd.d, gd.labels, seeds, cfg["fanouts"], 0x5EED, w, 0.05,
-                     kind=kname)
-    assert abs(p["loss"] - ref["loss"]) <= 1e-4 * abs(ref["loss"])
-    # the whole-step fp32 bound of test_step_* (1e-4 at hidden 64) scaled by
-    # sqrt(hidden / 64): the forward (2*d_in) and dX (d_out) reduction lengths
-    # grow with the hidden width and fp32 rounding error grows as their sqrt
-    tol = 1e-4 * max(1.0, (hidden / 64) ** 0.5)
-    assert normwise(np.asarray(p["grads"]), gnnv.flat_params(ref["grads"])) < tol
