@@ -101,10 +101,10 @@ typedef enum { GNNV_PREC_FP32 = 0, GNNV_PREC_BF16 = 1, GNNV_PREC_TF32 = 2 } gnnv
 const char* gnnv_last_error(void);
 /* Opt-in variants, by name (each measured slower than, or equal to, the
  * default on the products workload): GNNV_XROWS,
- * GNNV_GEMM_PAIR, GNNV_BWD_PULL, GNNV_NO_TAIL, GNNV_NO_PDL, GNNV_NO_L2PUSH.
+ * GNNV_GEMM_PAIR, GNNV_BWD_PULL, GNNV_NO_TAIL, GNNV_NO_PDL, GNNV_L2PUSH.
  * value 1 = on, 0 = off, -1 = back to the environment variable of the same
  * name (read once per process; set and not "0" = on).  Takes effect for
- * trainers / blocks created (XROWS, NO_TAIL, BWD_PULL, NO_L2PUSH) or
+ * trainers / blocks created (XROWS, NO_TAIL, BWD_PULL, L2PUSH) or
  * kernels launched (GEMM_PAIR, NO_PDL) afterwards.  PARAM on an unknown
  * name.  Process-wide; not for concurrent use with running steps. */
 gnnv_status gnnv_set_option(const char* name, int32_t value);
@@ -387,6 +387,19 @@ gnnv_status gnnv_trainer_rowidx(const gnnv_trainer* t, const int32_t** d_rowidx,
 /* Device pointers of the trainer's activations for layer i (0 = X) of the
  * last step (same buffer-set caveat; X holds the rows of gnnv_trainer_x_level). */
 gnnv_status gnnv_trainer_activation(gnnv_trainer* t, int32_t i, const float** d_H, int32_t* stride);
+/* Layer i's aggregate A^i (1..L) of the last step: [n_dst x stride] fp32
+ * (borrowed device pointer, same buffer-set caveat).  With the fused L2 push
+ * (gnnv_trainer_l2push) A^{i+1} was accumulated by layer i's GEMM epilogue
+ * and H^i (gnnv_trainer_activation) holds only the rows layer i+1 reads as
+ * its dst prefix (the first n_dst of layer i+1); its other rows exist only
+ * as their ReLU bits.  PARAM on i outside 1..L. */
+gnnv_status gnnv_trainer_aggregate(gnnv_trainer* t, int32_t i, const float** d_A, int32_t* stride);
+/* TF32: layer i's ReLU bits (1..L-1) of the last step, bit n%32 of word
+ * [row * words + n/32] = (H^i[row][n] > 0); NULL (and 0) otherwise. */
+gnnv_status gnnv_trainer_relu_bits(gnnv_trainer* t, int32_t i, const uint32_t** d_bits, int32_t* words);
+/* 1 if the trainer fuses layer i+1's aggregation into layer i's GEMM
+ * epilogue (TF32 SAGE with L >= 3 and GNNV_L2PUSH), else 0. */
+int32_t gnnv_trainer_l2push(const gnnv_trainer* t);
 
 /* One iteration of Algorithm 1 on this rank's seed slice:
  * sample -> gather -> L x (aggregate, combine) -> loss -> L x backward ->

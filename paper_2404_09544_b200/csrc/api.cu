@@ -145,7 +145,7 @@ const char* gnnv_last_error(void) { return get_error(); }
 gnnv_status gnnv_set_option(const char* name, int32_t value) {
   return guarded([&] {
     static const char* known[] = {"GNNV_XROWS", "GNNV_GEMM_PAIR", "GNNV_BWD_PULL", "GNNV_NO_TAIL", "GNNV_NO_PDL",
-                                  "GNNV_NO_L2PUSH"};
+                                  "GNNV_L2PUSH"};
     GNNV_REQUIRE(name, GNNV_ERR_PARAM, "set_option: null name");
     bool ok = false;
     for (const char* k : known) ok |= strcmp(k, name) == 0;
@@ -320,6 +320,33 @@ void comm_allgather_bytes(gnnv_comm* c, const void* mine, void* all, size_t byte
 }
 }  // namespace gnnv
 
+namespace gnnv {
+void blocks_enable_csc(gnnv_blocks* b, int h) {
+  GNNV_REQUIRE(h >= 0 && h < b->L, GNNV_ERR_PARAM, "blocks_enable_csc: hop");
+  if ((b->csc_mask >> h) & 1u) return;
+  b->d_colptr[h] = (int32_t*)dmalloc((b->max_n[h + 1] + 1) * sizeof(int32_t), "block CSC colptr");
+  b->d_csc[h] = (int32_t*)dmalloc(std::max<int64_t>(b->max_nnz[h], 1) * sizeof(int32_t), "block CSC rows");
+  int64_t n_max = 1;
+  for (int k = 0; k < b->L; ++k)
+    if (((b->csc_mask >> k) & 1u) || k == h) n_max = std::max(n_max, b->max_n[k + 1] + 1);
+  const size_t tmp = csc_scan_tmp_bytes(n_max);
+  if (n_max > b->csc_cnt_cap) {
+    GNNV_TRY_CUDA(cudaDeviceSynchronize());
+    dfree(b->d_csc_cnt);
+    b->d_csc_cnt = (int32_t*)dmalloc(n_max * sizeof(int32_t), "CSC counts");
+    GNNV_TRY_CUDA(cudaMemset(b->d_csc_cnt, 0, n_max * sizeof(int32_t)));
+    b->csc_cnt_cap = n_max;
+  }
+  if (tmp > b->csc_tmp_bytes) {
+    dfree(b->d_csc_tmp);
+    b->d_csc_tmp = dmalloc(tmp, "CSC scan temporary");
+    b->csc_tmp_bytes = tmp;
+  }
+  b->csc_mask |= 1u << h;
+  GNNV_TRY_CUDA(cudaDeviceSynchronize());
+}
+}  // namespace gnnv
+
 extern "C" {
 
 // ----------------------------------------------------------------- blocks
@@ -361,19 +388,9 @@ gnnv_status gnnv_blocks_create(gnnv_graph* g, int32_t max_seeds, const int32_t* 
       // GNNV_BWD_PULL=1: CSC of the hops whose layer has a dX (h <= L-2),
       // for the pulled backward aggregation (measured slower than the
       // two-pass push on products; opt-in)
-      b->csc_hops = env_on("GNNV_BWD_PULL") ? L - 1 : 0;
-      if (b->csc_hops > 0) {
-        int64_t n_max = 1;
-        for (int h = 0; h < b->csc_hops; ++h) {
-          b->d_colptr[h] = (int32_t*)dmalloc((b->max_n[h + 1] + 1) * sizeof(int32_t), "block CSC colptr");
-          b->d_csc[h] = (int32_t*)dmalloc(std::max<int64_t>(b->max_nnz[h], 1) * sizeof(int32_t), "block CSC rows");
-          n_max = std::max(n_max, b->max_n[h + 1] + 1);
-        }
-        b->d_csc_cnt = (int32_t*)dmalloc(n_max * sizeof(int32_t), "CSC counts");
-        GNNV_TRY_CUDA(cudaMemset(b->d_csc_cnt, 0, n_max * sizeof(int32_t)));
-        b->csc_tmp_bytes = csc_scan_tmp_bytes(n_max);
-        b->d_csc_tmp = dmalloc(b->csc_tmp_bytes, "CSC scan temporary");
-      }
+      b->pull_bwd = env_on("GNNV_BWD_PULL");
+      if (b->pull_bwd)
+        for (int h = 0; h + 1 < L; ++h) blocks_enable_csc(b, h);
       b->d_sizes = (int32_t*)dmalloc((2 * L + 2) * sizeof(int32_t), "sizes");
       GNNV_TRY_CUDA(cudaMemset(b->d_sizes, 0, (2 * L + 2) * sizeof(int32_t)));
       b->scan_words = tiles_max + 1;

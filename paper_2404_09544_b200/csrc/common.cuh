@@ -186,15 +186,17 @@ struct gnnv_blocks {
   unsigned long long* d_scan = nullptr;  // chained-scan status [1 + max tiles]
   int64_t scan_words = 0;
   uint32_t* d_own[GNNV_MAX_LAYERS] = {nullptr};  // [max_n[h]] owner-edge bit mask per dst row
-  // transposed block (CSC) of the hops whose layer has a dX (h <= L-2): the
-  // in-edges of src row u are csc_dst[h][colptr[h][u] .. colptr[h][u+1]),
-  // their dst rows (counting sort) -- the backward aggregation
-  // pulls through it (k_spmm_bwd_pull, GNNV_BWD_PULL=1).  csc_hops = 0 (default)
-  // keeps the two-pass push.
-  int32_t csc_hops = 0;
+  // transposed blocks (CSC) of selected hops: the in-edges of src row u of
+  // hop h are d_csc[h][d_colptr[h][u] .. d_colptr[h][u+1]), their dst rows
+  // (counting sort, order of arrival).  Used by the trainer's fused L2 push
+  // (the layer-1 GEMM epilogue aggregates layer 2's input; hop L-2) and, with
+  // GNNV_BWD_PULL, by the pulled backward aggregation (hops <= L-2).
+  uint32_t csc_mask = 0;  // bit h: hop h gets a CSC (blocks_enable_csc)
+  bool pull_bwd = false;   // GNNV_BWD_PULL: the CSC hops' backward aggregation pulls
   int32_t* d_colptr[GNNV_MAX_LAYERS] = {nullptr};  // [max_n[h+1] + 1]
   int32_t* d_csc[GNNV_MAX_LAYERS] = {nullptr};     // [max_nnz[h]]
   int32_t* d_csc_cnt = nullptr;    // [max n_src + 1] in-edge counts (zero between batches)
+  int64_t csc_cnt_cap = 0;
   void* d_csc_tmp = nullptr;       // cub scan temporary storage
   size_t csc_tmp_bytes = 0;
   bool sampled = false;
@@ -244,6 +246,9 @@ void launch_sample(gnnv_graph* g, gnnv_blocks* b, const int32_t* d_seeds, int32_
                    cudaStream_t s);
 // cub scan temporary bytes for the CSC column pointers of max_items columns
 size_t csc_scan_tmp_bytes(int64_t max_items);
+// give hop h of b a transposed block (CSC), built by every later
+// gnnv_sample on b (setup path: allocates; synchronises the device)
+void blocks_enable_csc(gnnv_blocks* b, int h);
 // cache.cu
 void launch_cache_update(gnnv_cache* c, const gnnv_blocks* b, const float* d_X, cudaStream_t s);
 void launch_gather(const gnnv_cache* c, const gnnv_blocks* b, float* d_X, int64_t* d_stats, cudaStream_t s,
@@ -284,8 +289,33 @@ struct GemmFwdArgs {
   // table (layer 1 reading H_dst from the whole-table cache; NULL: row m)
   const int32_t* x1_rows = nullptr;
   int64_t x1_table_rows = 0;
+  // TF32 only: the next layer's aggregation fused into the epilogue (the
+  // trainer's "L2 push"): for every output row u and every
+  // in-edge (v, u) of the next layer's block -- push_colptr[u] ..
+  // push_colptr[u+1] in push_dst -- push_out[v] += w_v * Y[u] with
+  // red.global.add (w_v = 1 / (push_indptr[v+1] - push_indptr[v]) for the
+  // mean, 1 for the sum); push_out must be zero.  Rows u >= *keep_rows are
+  // then not stored to Y (only their ReLU bits are).  NULL: off.
+  const int32_t* push_colptr = nullptr;
+  const int32_t* push_dst = nullptr;
+  const int32_t* push_indptr = nullptr;
+  float* push_out = nullptr;
+  int32_t push_ld = 0;
+  bool push_mean = true;
+  const int32_t* keep_rows = nullptr;
 };
 void gemm_fwd(const GemmFwdArgs& a, int prec, cudaStream_t s);
+// The trainer's fused L2 push (GemmFwdArgs::push_*): layer i's GEMM
+// epilogue accumulates layer i+1's aggregate A^{i+1} over the CSC of hop
+// L-i-1 into `out` (zeroed first, launch_zero_rows)
+struct FwdPush {
+  const int32_t *colptr, *dst, *indptr;
+  float* out;
+  int32_t ld;
+  bool mean;
+  const int32_t* keep_rows;
+};
+void launch_zero_rows(float* p, const int32_t* d_rows, int64_t max_rows, int32_t ld, cudaStream_t s);
 // Layer 1 of the trainer with the whole feature table on the device: H_dst
 // (X's dst prefix) is read by the TF32 GEMMs straight from the table through
 // the gather's row indices, so X is never materialised.

@@ -249,6 +249,14 @@ struct Params {
   // has a {width, 1} box and X1 tiles arrive by TMA gather4, 4 rows per
   // instruction, one instruction per producer lane (NULL: plain tiles)
   const int32_t* x1_rows;
+  // fwd: the next layer's aggregation fused into this epilogue (see
+  // GemmFwdArgs::push_*); push_out NULL = off
+  const int32_t* push_colptr;
+  const int32_t* push_dst;
+  const int32_t* push_indptr;
+  float* push_out;
+  int push_ld, push_mean;
+  const int32_t* keep_rows;
 };
 
 
@@ -477,6 +485,54 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_tma_gemm(const __grid_constant_
         tc_after();
         const int row0 = mt * BM + q * 32;
         const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN);
+        // fused push of the next layer's aggregation: this warp's 32 rows'
+        // in-edges (lane l: row row0 + l), an exclusive scan over the warp,
+        // and the first 128 edges' (dst row, weight) held in registers
+        // (edge p at lane p % 32, slot p / 32)
+        const bool push = MODE == MODE_FWD && !PAIR && p.push_out != nullptr;
+        int pe_beg = 0, pe_cnt = 0, pe_excl = 0, pe_incl = 0, pe_total = 0;
+        int pv[4] = {0, 0, 0, 0};
+        float pw[4] = {0.f, 0.f, 0.f, 0.f};
+        bool store_rows = true;
+        if (push) {
+          const int u = row0 + lane;
+          if (u < M) {
+            pe_beg = __ldg(p.push_colptr + u);
+            pe_cnt = __ldg(p.push_colptr + u + 1) - pe_beg;
+          }
+          pe_incl = pe_cnt;
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const int t = __shfl_up_sync(0xffffffffu, pe_incl, o);
+            if (lane >= o) pe_incl += t;
+          }
+          pe_excl = pe_incl - pe_cnt;
+          pe_total = __shfl_sync(0xffffffffu, pe_incl, 31);
+          // edge pidx -> (row r, edge e): r = first lane whose inclusive
+          // count exceeds pidx
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const int pidx = k * 32 + lane;
+            int r = 0;
+            for (int b = 16; b; b >>= 1) {  // binary search over the warp's prefix counts
+              const int cand = r + b;
+              const int ci = __shfl_sync(0xffffffffu, pe_incl, cand - 1);
+              if (ci <= pidx) r = cand;
+            }
+            const int eb = __shfl_sync(0xffffffffu, pe_beg, r), ex = __shfl_sync(0xffffffffu, pe_excl, r);
+            if (pidx < pe_total) {
+              const int v = __ldg(p.push_dst + eb + (pidx - ex));
+              pv[k] = v | (r << 26);  // row index packed above the dst row (rows < 2^26)
+              float w = 1.f;
+              if (p.push_mean) {
+                const int cv = __ldg(p.push_indptr + v + 1) - __ldg(p.push_indptr + v);
+                w = cv ? 1.f / (float)cv : 0.f;
+              }
+              pw[k] = w;
+            }
+          }
+          store_rows = row0 < *p.keep_rows;
+        }
         for (int c = half * 32; c < BN; c += 64) {
           float v[32];
           if (BN - c >= 32) tmem_ld32(tbase + c, v);
@@ -506,7 +562,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_tma_gemm(const __grid_constant_
             for (int j = 0; j < 32; ++j)
               if (j0 + j < p.ld1 && !((wv >> j) & 1u)) v[j] = 0.f;
           }
-          if (row0 + 32 > M || (MODE == MODE_DX && j0 < p.ld1 && j0 + 32 > p.ld1)) {
+          const bool ragged = row0 + 32 > M || (MODE == MODE_DX && j0 < p.ld1 && j0 + 32 > p.ld1);
+          if (ragged && store_rows) {
             // ragged last chunk: plain stores of the rows < M only (the TMA
             // map spans the row capacity, which may exceed the caller's rows);
             // a dX chunk straddling Y1 | Y2 also takes this path
@@ -524,8 +581,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_tma_gemm(const __grid_constant_
                 }
               }
             }
-            continue;
           }
+          if (ragged && !push) continue;
+          if (!push && !store_rows) continue;
           // the TMA store that last used this buffer (OBN chunks ago) must
           // have read it; the OBN - 1 most recent ones may still be reading
           uint8_t* ob = ob0 + obi * 4096;
@@ -539,7 +597,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_tma_gemm(const __grid_constant_
                          v[4 * j + 3]);
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
           __syncwarp();
-          if (lane == 0) {
+          if (lane == 0 && !ragged && store_rows) {
             if (MODE == MODE_FWD) {
               tma_store_2d(&p.ty1, ob, c, row0);
             } else if (j0 < p.ld1) {
@@ -548,6 +606,52 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_tma_gemm(const __grid_constant_
               tma_store_2d(&p.ty2, ob, j0 - p.ld1, row0);
             }
             asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+          }
+          if (push) {
+            // P[v][c .. c+32) += w_v * Y[u][c .. c+32) for every in-edge
+            // (v, u): four edges per instruction, eight lanes x 16 B = the
+            // 128-byte row piece of one edge (coalesced L2 reductions)
+            const int j4 = lane >> 3, qq = lane & 7;
+            for (int p0 = 0; p0 < pe_total; p0 += 4) {
+              const int pidx = p0 + j4;
+              int vr = 0;
+              float w = 0.f;
+              if (p0 < 128) {
+                const int slot = p0 >> 5;  // warp-uniform (p0 is a multiple of 4)
+                const int src = pidx & 31;
+                const int vk = slot == 0 ? pv[0] : slot == 1 ? pv[1] : slot == 2 ? pv[2] : pv[3];
+                const float wk = slot == 0 ? pw[0] : slot == 1 ? pw[1] : slot == 2 ? pw[2] : pw[3];
+                vr = __shfl_sync(0xffffffffu, vk, src);
+                w = __shfl_sync(0xffffffffu, wk, src);
+              } else {  // beyond the cached edges (hub rows): resolve on the fly
+                int r = 0;
+                for (int b = 16; b; b >>= 1) {
+                  const int cand = r + b;
+                  if (__shfl_sync(0xffffffffu, pe_incl, cand - 1) <= pidx) r = cand;
+                }
+                const int eb = __shfl_sync(0xffffffffu, pe_beg, r), ex = __shfl_sync(0xffffffffu, pe_excl, r);
+                if (pidx < pe_total) {
+                  const int v = __ldg(p.push_dst + eb + (pidx - ex));
+                  vr = v | (r << 26);
+                  w = 1.f;
+                  if (p.push_mean) {
+                    const int cv = __ldg(p.push_indptr + v + 1) - __ldg(p.push_indptr + v);
+                    w = cv ? 1.f / (float)cv : 0.f;
+                  }
+                }
+              }
+              if (pidx < pe_total && c + 4 * qq < p.push_ld) {
+                const int r = vr >> 26, v = vr & ((1 << 26) - 1);
+                float4 x;
+                asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                             : "=f"(x.x), "=f"(x.y), "=f"(x.z), "=f"(x.w)
+                             : "r"(ob_u32 + r * 128 + ((qq ^ (r & 7)) << 4)));
+                float* dst = p.push_out + (int64_t)v * p.push_ld + c + 4 * qq;
+                asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(dst), "f"(x.x * w), "f"(x.y * w),
+                             "f"(x.z * w), "f"(x.w * w)
+                             : "memory");
+              }
+            }
           }
         }
         tc_before();
@@ -954,7 +1058,7 @@ bool gemm_fwd_tma(const GemmFwdArgs& a, cudaStream_t s) {
   // default: measured on products, layer 1 179 -> 189-192 us (its tiles are
   // bound by the A operand's DRAM reads and the epilogue, not by the W^T
   // traffic the pair halves), layer 2 49 -> 46 us
-  const bool pair = env_on("GNNV_GEMM_PAIR") && !a.x1_rows && BN % 32 == 0;
+  const bool pair = env_on("GNNV_GEMM_PAIR") && !a.x1_rows && !a.push_out && BN % 32 == 0;
   p.ta1 = a.x1_rows ? make_map(a.X1, a.x1_table_rows, a.K1, a.ld1, 1) : make_map(a.X1, a.max_M, a.K1, a.ld1, BM);
   p.ta2 = a.X2 ? make_map(a.X2, a.max_M, a.K1, a.ld2, BM) : p.ta1;
   p.tb = make_map(Bt, BN, Kp, Kp, pair ? BN / 2 : BN);
@@ -972,6 +1076,16 @@ bool gemm_fwd_tma(const GemmFwdArgs& a, cudaStream_t s) {
   p.ty1 = make_map(a.Y, a.max_M, a.ldy, a.ldy, 32);
   p.bits = a.relu ? a.mask_bits : nullptr;
   p.bits_ld = a.mask_ld;
+  p.push_colptr = a.push_colptr;
+  p.push_dst = a.push_dst;
+  p.push_indptr = a.push_indptr;
+  p.push_out = a.push_out;
+  p.push_ld = a.push_ld;
+  p.push_mean = a.push_mean ? 1 : 0;
+  p.keep_rows = a.keep_rows;
+  GNNV_REQUIRE(!a.push_out || (a.push_colptr && a.push_dst && a.push_indptr && a.keep_rows && a.push_ld % 4 == 0 &&
+                               a.push_ld >= a.N),
+               GNNV_ERR_PARAM, "fwd: incomplete fused-push arguments");
   const int64_t tiles = ceil_div(std::max<int64_t>(a.max_M, 1), BM);
   if (pair) {
     launch_pair(p, (int)std::min<int64_t>(ceil_div(tiles, 2), num_sms() / 2), s);

@@ -247,18 +247,35 @@ static void check_layer(const gnnv_blocks* b, int32_t layer, const gnnv_layer_de
                "layer: prec");
 }
 
+__global__ void k_zero_rows(float4* __restrict__ p, const int32_t* d_rows, int32_t ld4) {
+  GNNV_PDL_ENTRY();
+  const int64_t n = (int64_t)*d_rows * ld4;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    p[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+}
+void launch_zero_rows(float* p, const int32_t* d_rows, int64_t max_rows, int32_t ld, cudaStream_t s) {
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(max_rows * (ld / 4), 256), num_sms() * 8));
+  launch_k(k_zero_rows, grid, 256, 0, s, reinterpret_cast<float4*>(p), d_rows, ld / 4);
+  GNNV_CHECK_LAUNCH();
+}
+
 void layer_fwd_impl(gnnv_blocks* b, int32_t layer, const gnnv_layer_desc* ld, const float* Hsrc, const float* W,
                     const float* bias, float* Hdst, float* A, cudaStream_t s, Timeline* tl, uint32_t* mask_bits,
-                    const float* agg_table, const int32_t* rowidx, const XRows* xr) {
+                    const float* agg_table, const int32_t* rowidx, const XRows* xr, const FwdPush* push,
+                    bool agg_ready) {
   const std::string sfx = ".l" + std::to_string(layer);
-  if (tl) tl->mark(s, "spmm_fwd" + sfx);
   const int h = b->L - layer;
   const int32_t* d_ndst = b->d_sizes + h;
   const int lda = row_stride(ld->d_in), ldo = row_stride(ld->d_out);
   // rowidx: the aggregation reads its source rows from the cache table
-  // (rows of Hsrc beyond the dst prefix are not materialised)
-  launch_spmm_fwd(b->d_indptr[h], b->d_indices[h], d_ndst, b->max_n[h], rowidx ? agg_table : Hsrc, ld->in_stride, A,
-                  lda, ld->d_in, ld->kind, ld->aggr, s, rowidx);
+  // (rows of Hsrc beyond the dst prefix are not materialised).  agg_ready:
+  // A was already accumulated by the previous layer's GEMM epilogue (the
+  // trainer's fused L2 push)
+  if (!agg_ready) {
+    if (tl) tl->mark(s, "spmm_fwd" + sfx);
+    launch_spmm_fwd(b->d_indptr[h], b->d_indices[h], d_ndst, b->max_n[h], rowidx ? agg_table : Hsrc, ld->in_stride,
+                    A, lda, ld->d_in, ld->kind, ld->aggr, s, rowidx);
+  }
   GemmFwdArgs g{};
   if (ld->kind == GNNV_KIND_SAGE) {
     g.X1 = xr ? xr->table : Hsrc;
@@ -284,6 +301,15 @@ void layer_fwd_impl(gnnv_blocks* b, int32_t layer, const gnnv_layer_desc* ld, co
   if (mask_bits && g.relu && ld->prec == GNNV_PREC_TF32) {
     g.mask_bits = mask_bits;
     g.mask_ld = mask_words(ld->d_out);
+  }
+  if (push) {
+    g.push_colptr = push->colptr;
+    g.push_dst = push->dst;
+    g.push_indptr = push->indptr;
+    g.push_out = push->out;
+    g.push_ld = push->ld;
+    g.push_mean = push->mean;
+    g.keep_rows = push->keep_rows;
   }
   if (tl) tl->mark(s, "gemm_fwd" + sfx);
   gemm_fwd(g, ld->prec, s);
@@ -399,7 +425,7 @@ void layer_bwd_impl(gnnv_blocks* b, int32_t layer, const gnnv_layer_desc* ld, co
     if (tl) tl->mark(s, "gemm_dx" + sfx);
     gemm_dx(x, ld->prec, s);
     if (tl) tl->mark(s, "spmm_bwd" + sfx);
-    if (h < b->csc_hops && ld->in_stride <= kPullMaxLd) {
+    if (b->pull_bwd && ((b->csc_mask >> h) & 1u) && ld->in_stride <= kPullMaxLd) {
       // transposed aggregation pulled per src row through the block's CSC:
       // one coalesced store per dH_src row, no atomics
       launch_spmm_bwd_pull(b->d_colptr[h], b->d_csc[h], b->d_indptr[h], d_ndst, b->d_sizes + h + 1, b->max_n[h + 1],
@@ -426,7 +452,7 @@ gnnv_status gnnv_layer_fwd(gnnv_blocks* b, int32_t layer, const gnnv_layer_desc*
     check_layer(b, layer, ld);
     GNNV_REQUIRE(d_Hsrc && d_W && d_b && d_Hdst && d_saveA, GNNV_ERR_PARAM, "layer_fwd: null buffer");
     layer_fwd_impl(b, layer, ld, d_Hsrc, d_W, d_b, d_Hdst, d_saveA, (cudaStream_t)s, nullptr, nullptr, nullptr, nullptr,
-                   nullptr);
+                   nullptr, nullptr, false);
   });
 }
 

@@ -635,11 +635,11 @@ void launch_sample(gnnv_graph* g, gnnv_blocks* b, const int32_t* d_seeds, int32_
   GNNV_CHECK_LAUNCH();
   // Hop h's slots reuse d_ell / d_cnt, so hop h-1 is mapped to local ids
   // (its tags are final after its scan) before hop h samples.  Hops with a
-  // CSC (hp < csc_hops) then sort their edges by src id (stable: dst order
+  // CSC (bit hp of csc_mask) then sort their edges by src id (stable: dst order
   // within a column) and derive the column pointers.
   auto map_hop = [&](int hp) {
     const int64_t slots_ub = b->max_nnz[hp];
-    const bool csc = hp < b->csc_hops;
+    const bool csc = (b->csc_mask >> hp) & 1u;
     launch_k(k_map, grid_for(slots_ub, 1024), 256, 0, s, hp, b->fanouts[hp], b->d_sizes, b->d_ell, b->d_cnt,
              b->d_indptr[hp], b->d_tag, b->d_indices[hp], b->d_scan, b->scan_words,
              csc ? b->d_csc_cnt : (int32_t*)nullptr);

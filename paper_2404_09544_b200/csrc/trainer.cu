@@ -13,7 +13,8 @@
 namespace gnnv {
 void layer_fwd_impl(gnnv_blocks* b, int32_t layer, const gnnv_layer_desc* ld, const float* Hsrc, const float* W,
                     const float* bias, float* Hdst, float* A, cudaStream_t s, Timeline* tl, uint32_t* mask_bits,
-                    const float* agg_table, const int32_t* rowidx, const XRows* xr);
+                    const float* agg_table, const int32_t* rowidx, const XRows* xr, const FwdPush* push,
+                    bool agg_ready);
 void layer_bwd_impl(gnnv_blocks* b, int32_t layer, const gnnv_layer_desc* ld, const float* Gdst, const float* Hdst,
                     const float* Hsrc, const float* A, const float* W, float* Gsrc, float* dW, float* db,
                     cudaStream_t s, Timeline* tl, const uint32_t* mask_bits, bool g_masked,
@@ -57,6 +58,13 @@ struct gnnv_trainer {
   // fused output layer (tail.cu): TF32 SAGE with L >= 2 and the shapes
   // tail_supported() accepts; GNNV_NO_TAIL=1 keeps the per-kernel path
   bool tail = false;
+  // fused L2 push (TF32 SAGE, L >= 3; opt-in GNNV_L2PUSH=1 -- measured
+  // slower): the GEMM epilogue of layer i (1 <= i <= L-2)
+  // accumulates layer i+1's aggregate A^{i+1} = P H^i with L2 reductions
+  // over the CSC of hop L-i-1 while H^i is still on chip, so H^i is stored
+  // only for the dst prefix layer i+1 reads (its other rows -- 88% of
+  // products' H^1 -- never reach HBM) and layer i+1 runs no aggregation
+  bool l2push = false;
   float* tail_dA = nullptr;    // [max_n[0] x dims[L-1]]
   float* tail_part = nullptr;  // per-CTA dW/db partials
   unsigned int* loss_counter = nullptr;
@@ -239,6 +247,9 @@ gnnv_status gnnv_trainer_create(gnnv_graph* g, gnnv_cache* c, const gnnv_model_d
           (float*)dmalloc(std::max<int64_t>(256, ceil_div(b->max_n[0], 32)) * sizeof(float), "loss partials");
       t->tail = md->prec == GNNV_PREC_TF32 && L >= 2 &&
                 tail_supported(md->kind, md->dims[L - 1], md->dims[L], md->fanouts[0]) && !env_on("GNNV_NO_TAIL");
+      t->l2push = md->prec == GNNV_PREC_TF32 && md->kind == GNNV_KIND_SAGE && L >= 3 && env_on("GNNV_L2PUSH");
+      if (t->l2push)
+        for (int i = 1; i <= L - 2; ++i) blocks_enable_csc(t->b, L - i - 1);
       if (t->tail) {
         t->tail_dA = (float*)dmalloc((size_t)b->max_n[0] * md->dims[L - 1] * sizeof(float), "output-layer dA");
         t->tail_part = (float*)dmalloc(tail_partial_floats(b->max_n[0], md->dims[L - 1], md->dims[L]) * sizeof(float),
@@ -312,6 +323,24 @@ gnnv_status gnnv_trainer_activation(gnnv_trainer* t, int32_t i, const float** d_
     *stride = t->Hs[i];
   });
 }
+
+gnnv_status gnnv_trainer_aggregate(gnnv_trainer* t, int32_t i, const float** d_A, int32_t* stride) {
+  return guarded([&] {
+    GNNV_REQUIRE(t && d_A && stride && i >= 1 && i <= t->md.L, GNNV_ERR_PARAM, "trainer_aggregate: bad args");
+    *d_A = t->A[i];
+    *stride = row_stride(t->md.dims[i - 1]);
+  });
+}
+
+gnnv_status gnnv_trainer_relu_bits(gnnv_trainer* t, int32_t i, const uint32_t** d_bits, int32_t* words) {
+  return guarded([&] {
+    GNNV_REQUIRE(t && d_bits && words && i >= 1 && i <= t->md.L, GNNV_ERR_PARAM, "trainer_relu_bits: bad args");
+    *d_bits = t->mbits[i];
+    *words = t->mbits[i] ? mask_words(t->md.dims[i]) : 0;
+  });
+}
+
+int32_t gnnv_trainer_l2push(const gnnv_trainer* t) { return t && t->l2push ? 1 : 0; }
 
 gnnv_status gnnv_trainer_set_locality(gnnv_trainer* t, double bias) {
   return guarded([&] {
@@ -464,6 +493,8 @@ gnnv_status gnnv_trainer_prefetch(gnnv_trainer* t, const int32_t* seeds, int32_t
       if (st != GNNV_OK) throw Error{st, get_error()};
       st = gnnv_blocks_set_locality(t->bb[k], t->c, t->loc_bias);
       if (st != GNNV_OK) throw Error{st, get_error()};
+      if (t->l2push)
+        for (int i = 1; i <= t->md.L - 2; ++i) blocks_enable_csc(t->bb[k], t->md.L - i - 1);
       const int64_t xrows = t->x_rows ? 1 : t->bb[k]->max_n[t->x_fused ? t->md.L - 1 : t->md.L];
       t->X[k] = (float*)dmalloc((size_t)xrows * g->stride * sizeof(float), "X (prefetch)");
       if (t->x_fused)
@@ -578,9 +609,18 @@ gnnv_status gnnv_step(gnnv_trainer* t, const int32_t* seeds, int32_t n_seeds, in
     for (int i = 1; i <= L; ++i) {
       if (t->tail && i == L) break;  // the fused output layer below
       const gnnv_layer_desc ld = layer_desc(t, i);
+      FwdPush push{};
+      const bool do_push = t->l2push && i <= L - 2;
+      if (do_push) {
+        const int hn = L - i - 1;  // the next layer's block
+        if (tl) tl->mark(s, "zero_a.l" + std::to_string(i + 1));
+        launch_zero_rows(t->A[i + 1], b->d_sizes + hn, b->max_n[hn], row_stride(t->md.dims[i]), s);
+        push = FwdPush{b->d_colptr[hn], b->d_csc[hn], b->d_indptr[hn], t->A[i + 1], row_stride(t->md.dims[i]),
+                       t->md.aggr == GNNV_AGGR_MEAN, b->d_sizes + hn};
+      }
       layer_fwd_impl(b, i, &ld, t->H[i - 1], t->d_params + t->w_off[i - 1], t->d_params + t->b_off[i - 1], t->H[i],
                      t->A[i], s, tl, t->mbits[i], t->table, i == 1 ? t->rowidx[t->cur] : nullptr,
-                     i == 1 ? xr1 : nullptr);
+                     i == 1 ? xr1 : nullptr, do_push ? &push : nullptr, t->l2push && i >= 2 && i <= L - 1);
     }
     if (tm) GNNV_TRY_CUDA(cudaEventRecord(t->ev[3], s));
     float* d_loss = t->d_grads + t->nparams;

@@ -127,6 +127,9 @@ _SIGS = {
     "gnnv_trainer_set_locality": (I32, [VP, F64]),
     "gnnv_blocks_set_locality": (I32, [VP, VP, F64]),
     "gnnv_trainer_activation": (I32, [VP, I32, PP, C.POINTER(I32)]),
+    "gnnv_trainer_aggregate": (I32, [VP, I32, PP, C.POINTER(I32)]),
+    "gnnv_trainer_relu_bits": (I32, [VP, I32, PP, C.POINTER(I32)]),
+    "gnnv_trainer_l2push": (I32, [VP]),
     "gnnv_step": (I32, [VP, VP, I32, I32, I32, U64, F32, C.POINTER(F32), C.POINTER(StepTiming), VP]),
     "gnnv_trainer_stats": (I32, [VP, VP]),
     "gnnv_trainer_prefetch": (I32, [VP, VP, I32, I32, U64, VP]),
@@ -538,6 +541,23 @@ class Trainer:
         st = C.c_int32()
         _check(load().gnnv_trainer_activation(self.h, i, C.byref(p), C.byref(st)))
         return int(p.value), int(st.value)
+
+    def aggregate(self, i: int):
+        """(device pointer, stride) of layer i's aggregate A^i of the last step."""
+        p = C.c_void_p()
+        st = C.c_int32()
+        _check(load().gnnv_trainer_aggregate(self.h, i, C.byref(p), C.byref(st)))
+        return int(p.value or 0), int(st.value)
+
+    def relu_bits(self, i: int):
+        """(device pointer, words per row) of layer i's ReLU bits (TF32), or (0, 0)."""
+        p = C.c_void_p()
+        w = C.c_int32()
+        _check(load().gnnv_trainer_relu_bits(self.h, i, C.byref(p), C.byref(w)))
+        return int(p.value or 0), int(w.value)
+
+    def l2push(self) -> bool:
+        return bool(load().gnnv_trainer_l2push(self.h))
 
     def timeline(self, on: bool):
         _check(load().gnnv_trainer_timeline(self.h, 1 if on else 0))

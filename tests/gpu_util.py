@@ -4,6 +4,10 @@ import ctypes
 import numpy as np
 import torch
 
+import oracle
+from oracle.layers import agg_matrix, ce_loss, layer_bwd, layer_fwd
+from oracle.sampler import Block
+
 from paper_2404_09544_b200 import gnnv
 from paper_2404_09544_b200.build import build
 
@@ -46,6 +50,14 @@ def read_f32(p, rows, stride):
                                    ctypes.c_size_t(int(rows) * int(stride) * 4), 3)
         assert int(res) == 0, res
     return out.cpu().numpy()
+
+
+def read_bits(p, rows, words, ncols):
+    """A [rows x words] uint32 ReLU bit mask from a device pointer, unpacked
+    to bool [rows x ncols] (bit n%32 of word n/32)."""
+    w = read_i32(p, int(rows) * int(words)).view(np.uint32).reshape(int(rows), int(words))
+    bits = np.unpackbits(w.view(np.uint8), axis=1, bitorder="little")
+    return bits[:, :ncols].astype(bool)
 
 
 _rt = None
@@ -91,3 +103,123 @@ def normwise(got, ref):
     got = np.asarray(got, np.float64)
     ref = np.asarray(ref, np.float64)
     return float(np.abs(got - ref).max() / max(np.abs(ref).max(), 1e-30))
+
+
+def _blk(hb, h):
+    nd, ns, ptr, idx, F = hb[h]
+    return Block(n_dst=nd, n_src=ns, indptr=ptr.astype(np.int64), indices=idx.astype(np.int64), src_global=F)
+
+
+def sub_block(ob: Block, H_src: np.ndarray, rows: np.ndarray):
+    """The block restricted to dst rows `rows` (each output row depends only
+    on its own sampled neighbours and itself): self rows first, then the
+    neighbours' rows, so the oracle's layer_fwd applies unchanged."""
+    cnt = np.diff(ob.indptr)[rows]
+    nbr = np.concatenate([ob.indices[ob.indptr[r]:ob.indptr[r + 1]] for r in rows])
+    n = len(rows)
+    blk = Block(n_dst=n, n_src=n + nbr.size, indptr=np.concatenate([[0], np.cumsum(cnt)]).astype(np.int64),
+                indices=(n + np.arange(nbr.size)).astype(np.int64), src_global=None)
+    return blk, np.concatenate([H_src[rows], H_src[nbr]])
+
+
+def check_forward_chain(tr, hb, dims, w, rtol, name, X0=None, max_rows=2048, kind="sage", seed=0):
+    """Every layer of the trainer's last forward against the oracle, each fed
+    the GPU's own input (reading Q24); X0 = the exact layer-1 input when X
+    is not materialised (whole-table cache).  Layers with more than max_rows
+    output rows are checked on that many sampled rows (row-restricted
+    blocks).  With the fused L2 push (tr.l2push()) layer i's GEMM also
+    accumulated A^{i+1} and stored H^i for layer i+1's dst prefix only: layer
+    i+1 is then checked on the GPU's [H^i_dst | A^{i+1}], and A^{i+1} itself
+    against the aggregation of the oracle's layer i (from the GPU's input to
+    layer i) on sampled rows, within layer i's bound (relu is 1-Lipschitz,
+    the mean a convex sum).  Returns (H, Aagg, blks) for the backward."""
+    L = len(hb)
+    push = tr.l2push()
+    rng = np.random.default_rng(seed)
+    H = [None] * (L + 1)
+    Aagg = [None] * (L + 1)
+    blks = [None] * (L + 1)
+    Hprev_in = None
+    for i in range(1, L + 1):
+        ob = blks[i] = _blk(hb, L - i)
+        p_in, s_in = tr.activation(i - 1)
+        p_out, s_out = tr.activation(i)
+        pushed_in = push and 2 <= i <= L - 1  # A^i came from layer i-1's epilogue
+        pushed_out = push and i <= L - 2  # H^i stored for the next dst prefix only
+        if i == 1 and X0 is not None:
+            Hin = X0
+        elif pushed_in:
+            Hin = read_f32(p_in, ob.n_dst, s_in)[:, : dims[i - 1]]  # the dst prefix the GPU stored
+        else:
+            Hin = read_f32(p_in, ob.n_src, s_in)[:, : dims[i - 1]]
+        Hout = read_f32(p_out, (_blk(hb, L - i - 1).n_dst if pushed_out else ob.n_dst), s_out)[:, : dims[i]]
+        H[i - 1], H[i] = Hin, Hout
+        Wi, bi = w[i - 1]
+        if pushed_in:
+            pa, sa = tr.aggregate(i)
+            A_gpu = read_f32(pa, ob.n_dst, sa)[:, : dims[i - 1]]
+            Aagg[i] = A_gpu
+            rows = np.sort(rng.choice(ob.n_dst, min(ob.n_dst, max_rows), replace=False))
+            cnt = np.diff(ob.indptr)[rows]
+            nbr = np.concatenate([ob.indices[ob.indptr[r]:ob.indptr[r + 1]] for r in rows])
+            sub, Hs = sub_block(blks[i - 1], Hprev_in, nbr)
+            Wp, bp = w[i - 2]
+            Hn, _ = layer_fwd(sub, Hs, Wp, bp, True, kind)
+            Hnm, _ = layer_fwd(sub, Hs, Wp, bp, True, kind, absval=True)
+            seg = np.repeat(np.arange(len(rows)), cnt)
+            wv = 1.0 / np.maximum(cnt, 1)
+            A_ref = np.zeros((len(rows), dims[i - 1]))
+            A_mag = np.zeros((len(rows), dims[i - 1]))
+            np.add.at(A_ref, seg, Hn * wv[seg][:, None])
+            np.add.at(A_mag, seg, Hnm * wv[seg][:, None])
+            assert_close_cond(A_gpu[rows], A_ref, A_mag, rtol, f"{name} fused aggregate A^{i} (sampled rows)")
+            X = np.concatenate([Hin.astype(np.float64), A_gpu.astype(np.float64)], axis=1)
+            Z = X @ Wi.astype(np.float64) + bi
+            Zm = np.abs(X) @ np.abs(Wi.astype(np.float64)) + np.abs(bi)
+            Ho = np.maximum(Z, 0) if i < L else Z
+            n = len(Hout)
+            assert_close_cond(Hout, Ho[:n], Zm[:n], rtol, f"{name} layer {i} (on the fused aggregate)")
+        elif len(Hout) > max_rows or pushed_out:  # only the stored prefix when pushed_out
+            rows = np.sort(rng.choice(len(Hout), min(len(Hout), max_rows), replace=False))
+            blk, Hs = sub_block(ob, Hin, rows)
+            Ho, _ = layer_fwd(blk, Hs, Wi, bi, i < L, kind)
+            Hm, _ = layer_fwd(blk, Hs, Wi, bi, i < L, kind, absval=True)
+            assert_close_cond(Hout[rows], Ho, Hm, rtol, f"{name} layer {i} (sampled rows)")
+        else:
+            Ho, _ = layer_fwd(ob, Hin, Wi, bi, i < L, kind)
+            Hm, _ = layer_fwd(ob, Hin, Wi, bi, i < L, kind, absval=True)
+            assert_close_cond(Hout, Ho, Hm, rtol, f"{name} layer {i}")
+        Hprev_in = Hin
+    return H, Aagg, blks
+
+
+def check_backward_chain(tr, blks, H, Aagg, dims, w, grads, labels, n_global, rtol, name, kind="sage"):
+    """Every dW/db elementwise against the oracle's backward chain run on the
+    GPU's forward values (its logits, its ReLU masks): each GEMM stage
+    between the loss and layer i adds at most rtol of the magnitude the same
+    chain propagates on |.|.  With the fused push, layer i's ReLU mask comes
+    from the GPU's bits and layer i+1's aggregate is the GPU's A^{i+1}."""
+    L = len(blks) - 1
+    push = tr.l2push()
+    _, G = ce_loss(H[L], labels, n_global)
+    M = np.abs(G)
+    for i in range(L, 0, -1):
+        ob = blks[i]
+        Hi = H[i]
+        if push and i <= L - 2:  # H^i beyond the dst prefix exists only as its ReLU bits
+            pbits, words = tr.relu_bits(i)
+            Hi = read_bits(pbits, ob.n_dst, words, dims[i]).astype(np.float64)
+        Hsrc = H[i - 1]
+        if push and 2 <= i <= L - 1:
+            A = Aagg[i].astype(np.float64)
+            Hsrc = np.concatenate([H[i - 1], np.zeros((ob.n_src - ob.n_dst, dims[i - 1]), H[i - 1].dtype)])
+        else:
+            A = agg_matrix(ob, kind) @ H[i - 1].astype(np.float64)
+        Wi = w[i - 1][0]
+        rW, rb, rX = layer_bwd(ob, Hsrc, A, Hi, Wi, G, relu=(i < L), need_dx=(i > 1), kind=kind)
+        mW, mb, mX = layer_bwd(ob, np.abs(Hsrc), np.abs(A), Hi, np.abs(Wi), M, relu=(i < L), need_dx=(i > 1),
+                               kind=kind)
+        stages = L - i + 1
+        assert_close_cond(grads[i - 1][0], rW, mW, rtol * stages, f"{name} dW layer {i}")
+        assert_close_cond(grads[i - 1][1], rb, mb, rtol * stages, f"{name} db layer {i}")
+        G, M = rX, mX

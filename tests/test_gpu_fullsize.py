@@ -27,23 +27,12 @@ from paper_2404_09544_b200 import gnnv
 from synth import BASE_RNG_SEED, CONFIGS, epoch_seeds, init_weights
 from synth.store import shared_graph
 
-from gpu_util import assert_close_cond, blocks_to_host, lib, normwise, read_f32, read_i32
+from gpu_util import (_blk, assert_close_cond, blocks_to_host, check_backward_chain, check_forward_chain, lib,
+                      normwise, read_f32, read_i32, sub_block)
 
 pytestmark = pytest.mark.gpu
 
 RTOL = {0: 1e-5, 2: 4e-3}  # fp32 / tf32, as test_gpu_parity (reading Q17, Q22)
-
-
-def sub_block(ob: Block, H_src: np.ndarray, rows: np.ndarray):
-    """The block restricted to dst rows `rows` (each output row depends only
-    on its own sampled neighbours and itself): self rows first, then the
-    neighbours' rows, so the oracle's layer_fwd applies unchanged."""
-    cnt = np.diff(ob.indptr)[rows]
-    nbr = np.concatenate([ob.indices[ob.indptr[r]:ob.indptr[r + 1]] for r in rows])
-    n = len(rows)
-    blk = Block(n_dst=n, n_src=n + nbr.size, indptr=np.concatenate([[0], np.cumsum(cnt)]).astype(np.int64),
-                indices=(n + np.arange(nbr.size)).astype(np.int64), src_global=None)
-    return blk, np.concatenate([H_src[rows], H_src[nbr]])
 
 
 def pipelined_step(tr, d_seeds, n, n_global, rng_seed, lr):
@@ -95,11 +84,6 @@ def check_blocks_and_gather(gd, tr, ref_frontiers, ref_blocks, ratio):
     cnt = access_counts(slot, owner, FL)
     assert tr.stats().tolist() == [cnt["rows"], cnt["hits_local"], cnt["hits_peer"], cnt["misses_host"]]
     return hb
-
-
-def _blk(hb, h):
-    nd, ns, ptr, idx, F = hb[h]
-    return Block(n_dst=nd, n_src=ns, indptr=ptr.astype(np.int64), indices=idx.astype(np.int64), src_global=F)
 
 
 _GRAPHS = {}
@@ -164,47 +148,9 @@ def full_step_check(name, ratio, prec, max_rows=2048):
         grads = gnnv.unflat_params(tr.grads(), dims)
         rtol = RTOL[prec]
         assert abs(loss - ref["loss"]) <= (1e-4 if prec == 0 else 5e-3) * abs(ref["loss"]), (loss, ref["loss"])
-        # forward chain, each layer fed the GPU's own input (reading Q24)
-        rng = np.random.default_rng(0)
-        H = [None] * (L + 1)
-        blks = [None] * (L + 1)
-        for i in range(1, L + 1):
-            ob = blks[i] = _blk(hb, L - i)
-            p_in, s_in = tr.activation(i - 1)
-            p_out, s_out = tr.activation(i)
-            if i == 1 and tr.x_level() < L:  # layer 1 read the cache table (checked above): the exact feature rows
-                Hin = oracle.gather_rows(gd.feats, hb[L - 1][4])[:, : dims[0]]
-            else:
-                Hin = read_f32(p_in, ob.n_src, s_in)[:, : dims[i - 1]]
-            Hout = read_f32(p_out, ob.n_dst, s_out)[:, : dims[i]]
-            H[i - 1], H[i] = Hin, Hout
-            Wi, bi = w[i - 1]
-            if ob.n_dst > max_rows:
-                rows = np.sort(rng.choice(ob.n_dst, max_rows, replace=False))
-                blk, Hs = sub_block(ob, Hin, rows)
-                Ho, _ = layer_fwd(blk, Hs, Wi, bi, i < L)
-                Hm, _ = layer_fwd(blk, Hs, Wi, bi, i < L, absval=True)
-                assert_close_cond(Hout[rows], Ho, Hm, rtol, f"{name} layer {i} (sampled rows)")
-            else:
-                Ho, _ = layer_fwd(ob, Hin, Wi, bi, i < L)
-                Hm, _ = layer_fwd(ob, Hin, Wi, bi, i < L, absval=True)
-                assert_close_cond(Hout, Ho, Hm, rtol, f"{name} layer {i}")
-        # backward chain on the GPU's forward values (its logits, its ReLU
-        # masks): each GEMM stage between the loss and layer i adds at most
-        # rtol of the magnitude propagated by the same chain on |.|
-        _, G = ce_loss(H[L], gd.labels[seeds], B)
-        M = np.abs(G)
-        for i in range(L, 0, -1):
-            ob = blks[i]
-            A = agg_matrix(ob) @ H[i - 1].astype(np.float64)
-            Wi = w[i - 1][0]
-            rW, rb, rX = layer_bwd(ob, H[i - 1], A, H[i], Wi, G, relu=(i < L), need_dx=(i > 1))
-            mW, mb, mX = layer_bwd(ob, np.abs(H[i - 1]), np.abs(A), H[i], np.abs(Wi), M, relu=(i < L),
-                                   need_dx=(i > 1))
-            stages = L - i + 1
-            assert_close_cond(grads[i - 1][0], rW, mW, rtol * stages, f"{name} dW layer {i}")
-            assert_close_cond(grads[i - 1][1], rb, mb, rtol * stages, f"{name} db layer {i}")
-            G, M = rX, mX
+        X0 = oracle.gather_rows(gd.feats, hb[L - 1][4])[:, : dims[0]] if tr.x_level() < L else None
+        H, Aagg, blks = check_forward_chain(tr, hb, dims, w, rtol, name, X0=X0, max_rows=max_rows)
+        check_backward_chain(tr, blks, H, Aagg, dims, w, grads, gd.labels[seeds], B, rtol, name)
         # and the direction of every gradient vs the oracle's own fp64 step
         for i, ((gW, gb), (rW_, rb_)) in enumerate(zip(grads, ref["grads"])):
             for a_, b_ in ((gW, rW_), (gb, rb_)):

@@ -77,7 +77,8 @@ def test_papers100m_batch_bit_exact():
     # feature rows of the sampled neighbours (read by the GPU from the table)
     L = len(cfg["fanouts"])
     nd, ns, ptr, idx, Fg = hb[L - 1]
-    rows = np.sort(np.random.default_rng(0).choice(nd, 2048, replace=False))
+    n_keep = hb[L - 2][0] if tr.l2push() else nd  # fused L2 push: H^1 stored for layer 2's dst prefix only
+    rows = np.sort(np.random.default_rng(0).choice(n_keep, 2048, replace=False))
     cnt = np.diff(ptr)[rows]
     nbr = np.concatenate([idx[ptr[r]:ptr[r + 1]] for r in rows])
     blk = Block(n_dst=len(rows), n_src=len(rows) + nbr.size, indptr=np.concatenate([[0], np.cumsum(cnt)]).astype(np.int64),
@@ -87,6 +88,6 @@ def test_papers100m_batch_bit_exact():
     Ho, _ = layer_fwd(blk, Hs, W1, b1, True)
     Hm, _ = layer_fwd(blk, Hs, W1, b1, True, absval=True)
     p1, s1 = tr.activation(1)
-    H1 = read_f32(p1, nd, s1)[rows, : dims[1]]
+    H1 = read_f32(p1, n_keep, s1)[rows, : dims[1]]
     assert_close_cond(H1, Ho, Hm, 4e-3, "papers100m layer 1 (sampled rows)")
     print(f"papers100m: frontiers {[len(f) for f in F]}, edges {[b.nnz for b in blocks]}, loss {loss:.5f}")

@@ -13,7 +13,7 @@ from oracle.sampler import Block, sample_blocks
 from paper_2404_09544_b200 import gnnv
 from synth import CONFIGS, epoch_seeds, init_weights, make_graph, row_stride, tiny_graph
 
-from gpu_util import assert_close_cond, blocks_to_host, dev_f32, dev_i32, lib, normwise, read_f32, read_i32
+from gpu_util import check_forward_chain, sub_block, assert_close_cond, blocks_to_host, dev_f32, dev_i32, lib, normwise, read_f32, read_i32
 
 pytestmark = pytest.mark.gpu
 
@@ -314,19 +314,10 @@ def test_step_parity(mini, kind, prec):
         # compared by direction: bf16 rounding flips the ReLU mask of
         # pre-activations within ~2^-8 of zero, so a masked gradient differs by
         # 100% on those elements and a normwise bound is ill-posed.
+        # (with the tf32 SAGE trainer's fused L2 push: layer 2 on the GPU's
+        # [H^1_dst | A^2], A^2 against the oracle's layer 1, gpu_util)
         hb = blocks_to_host(tr.blocks)
-        L = len(cfg["fanouts"])
-        w_gpu = w
-        for i in range(1, L + 1):
-            ob = _oracle_block(hb, L - i)
-            p_in, s_in = tr.activation(i - 1)
-            p_out, s_out = tr.activation(i)
-            Hin = read_f32(p_in, ob.n_src, s_in)[:, : dims[i - 1]]
-            Hout = read_f32(p_out, ob.n_dst, s_out)[:, : dims[i]]
-            Wi, bi = w_gpu[i - 1]
-            Ho, _ = layer_fwd(ob, Hin, Wi, bi, i < L, kname)
-            Hm, _ = layer_fwd(ob, Hin, Wi, bi, i < L, kname, absval=True)
-            assert_close_cond(Hout, Ho, Hm, RTOL[prec], f"step layer {i}")
+        check_forward_chain(tr, hb, dims, w, RTOL[prec], "step", kind=kname, max_rows=10**9)
         for i, ((gW, gb), (rW, rb)) in enumerate(zip(grads, ref["grads"])):
             for a_, b_ in ((gW, rW), (gb, rb)):
                 cos = float(np.dot(a_.ravel(), b_.ravel()) / (np.linalg.norm(a_) * np.linalg.norm(b_) + 1e-30))
@@ -749,10 +740,56 @@ def test_step_whole_table_gather4(mini, option):
     ob = _oracle_block(hb, L - 1)
     Hin = oracle.gather_rows(gd.feats, FL)[:, : dims[0]]
     p_out, s_out = tr.activation(1)
-    Hout = read_f32(p_out, ob.n_dst, s_out)[:, : dims[1]]
-    Ho, _ = layer_fwd(ob, Hin, w[0][0], w[0][1], True)
-    Hm, _ = layer_fwd(ob, Hin, w[0][0], w[0][1], True, absval=True)
+    n_keep = hb[L - 2][0] if tr.l2push() else ob.n_dst  # fused push: H^1 stored for layer 2's dst prefix only
+    Hout = read_f32(p_out, n_keep, s_out)[:, : dims[1]]
+    blk, Hs = sub_block(ob, Hin, np.arange(n_keep))
+    Ho, _ = layer_fwd(blk, Hs, w[0][0], w[0][1], True)
+    Hm, _ = layer_fwd(blk, Hs, w[0][0], w[0][1], True, absval=True)
     assert_close_cond(Hout, Ho, Hm, RTOL[2], "layer 1 (gather4 H_dst)")
+
+
+@pytest.mark.parametrize("aggr", [gnnv.AGGR_MEAN, gnnv.AGGR_SUM])
+@pytest.mark.parametrize("ratio", [0.3, 1.0])
+def test_fused_l2_push_matches_per_layer_aggregation(mini, option, aggr, ratio):
+    """The tf32 SAGE trainer (L >= 3) accumulates layer 2's aggregate in the
+    layer-1 GEMM epilogue (L2 reductions over hop L-2's CSC) instead of
+    storing H^1 and running the layer-2 aggregation; the default keeps the
+    per-layer kernels.  Same step, same inputs: A^2 agrees to summation-order
+    rounding, and the layer-2 output, the loss and the gradients to the tf32
+    rounding that difference can move; ratio 1.0 also runs layer 1 from the
+    cache table.  (Each path is checked against the oracle elsewhere:
+    test_step_parity, test_gpu_fullsize.)"""
+    gd, g = mini
+    cfg = CONFIGS["mini"]
+    dims = [gd.d, cfg["hidden"], cfg["hidden"], gd.C]
+    L = len(cfg["fanouts"])
+    w = init_weights(dims)
+    seeds = epoch_seeds(gd.n, 0)[: cfg["batch"]]
+    out = {}
+    for name in ("push", "plain"):
+        option("GNNV_L2PUSH", 1 if name == "push" else 0)
+        tr = gnnv.Trainer(g, gnnv.Cache(g, ratio), dims, cfg["fanouts"], cfg["batch"], w, aggr=aggr,
+                          prec=gnnv.PREC_TF32)
+        assert tr.l2push() == (name == "push")
+        tr.timeline(True)
+        loss, _ = tr.step(seeds, len(seeds), len(seeds), 0x5EED, 0.05)
+        segs = tr.timeline_read()
+        hb = blocks_to_host(tr.blocks)
+        pa, sa = tr.aggregate(2)
+        p2, s2 = tr.activation(2)
+        out[name] = dict(loss=loss, grads=tr.grads(), segs=segs, A2=read_f32(pa, hb[L - 2][0], sa)[:, : dims[1]],
+                         H2=read_f32(p2, hb[L - 2][0], s2)[:, : dims[2]])
+        tr.free()
+    assert "spmm_fwd.l2" not in out["push"]["segs"] and "spmm_fwd.l2" in out["plain"]["segs"]
+    p, q = out["push"], out["plain"]
+    # A^2 differs only by summation order and w*x vs x/c rounding (~1 ulp);
+    # downstream, an operand that lands on the other side of a tf32 rounding
+    # boundary, or a pre-activation within that of zero, moves single
+    # elements by up to 2^-10 of a term
+    assert normwise(p["A2"], q["A2"]) < 1e-6
+    assert normwise(p["H2"], q["H2"]) < 1e-4
+    assert abs(p["loss"] - q["loss"]) <= 1e-5 * abs(q["loss"])
+    assert normwise(p["grads"], q["grads"]) < 2e-3
 
 
 @pytest.mark.parametrize("aggr", [gnnv.AGGR_MEAN, gnnv.AGGR_SUM])
