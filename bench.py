@@ -96,15 +96,18 @@ def measure_host_link() -> float:
 
 
 def load_traffic(workload: str):
-    """Per-segment DRAM bytes of one step from the committed ncu capture
-    (tools/ncu_traffic.py -> profiles/r01_ncu_traffic.json), or {}."""
-    path = os.path.join(ROOT, "profiles", "r01_ncu_traffic.json")
-    try:
-        d = json.load(open(path))
-        if d.get("workload") == workload:
-            return {k: v["dram_bytes"] for k, v in d["segments"].items()}
-    except Exception:
-        pass
+    """Per-segment DRAM bytes of one step from the committed ncu captures
+    (tools/ncu_traffic.py -> profiles/r*_ncu_traffic*.json, newest round
+    first) for this workload ("<config>/<prec>"), or {}."""
+    import glob
+
+    for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_ncu_traffic*.json")), reverse=True):
+        try:
+            d = json.load(open(path))
+            if d.get("workload") == workload:
+                return {k: v["dram_bytes"] for k, v in d["segments"].items()}
+        except Exception:
+            pass
     return {}
 
 
@@ -668,10 +671,11 @@ def main():
     peaks = load_peaks()
     if sizes["misses"] > 0:
         peaks["host"] = measure_host_link()
-    # the committed capture is of the default configuration only
-    default_cfg = (args.ratio is None and args.locality_bias == 0 and args.placement == "replica"
-                   and args.kind == "sage" and args.policy == "degree")
-    traffic = load_traffic(f"{cfg['name']}/{args.prec}") if default_cfg else {}
+    # the committed captures are of the default knobs (degree cache, no
+    # locality bias, replicated, SAGE) at a given config, ratio and precision
+    default_cfg = (args.locality_bias == 0 and args.placement == "replica" and args.kind == "sage"
+                   and args.policy == "degree")
+    traffic = load_traffic(f"{cfg['name']}@{cfg['ratio']:g}/{args.prec}") if default_cfg else {}
     # dominant kernel segment of the timed region
     seg_ms = {k: v[0] / max(1, v[1]) for k, v in segs.items()}
     seg_tot = {k: v[0] for k, v in segs.items()}

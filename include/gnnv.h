@@ -101,10 +101,11 @@ typedef enum { GNNV_PREC_FP32 = 0, GNNV_PREC_BF16 = 1, GNNV_PREC_TF32 = 2 } gnnv
 const char* gnnv_last_error(void);
 /* Opt-in variants, by name (each measured slower than, or equal to, the
  * default on the products workload): GNNV_XROWS,
- * GNNV_GEMM_PAIR, GNNV_BWD_PULL, GNNV_NO_TAIL, GNNV_NO_PDL, GNNV_L2PUSH.
+ * GNNV_GEMM_PAIR, GNNV_BWD_PULL, GNNV_NO_TAIL, GNNV_NO_PDL, GNNV_L2PUSH,
+ * GNNV_NO_LASTUSE.
  * value 1 = on, 0 = off, -1 = back to the environment variable of the same
  * name (read once per process; set and not "0" = on).  Takes effect for
- * trainers / blocks created (XROWS, NO_TAIL, BWD_PULL, L2PUSH) or
+ * trainers / blocks created (XROWS, NO_TAIL, BWD_PULL, L2PUSH, NO_LASTUSE) or
  * kernels launched (GEMM_PAIR, NO_PDL) afterwards.  PARAM on an unknown
  * name.  Process-wide; not for concurrent use with running steps. */
 gnnv_status gnnv_set_option(const char* name, int32_t value);

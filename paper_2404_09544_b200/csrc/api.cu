@@ -145,7 +145,7 @@ const char* gnnv_last_error(void) { return get_error(); }
 gnnv_status gnnv_set_option(const char* name, int32_t value) {
   return guarded([&] {
     static const char* known[] = {"GNNV_XROWS", "GNNV_GEMM_PAIR", "GNNV_BWD_PULL", "GNNV_NO_TAIL", "GNNV_NO_PDL",
-                                  "GNNV_L2PUSH"};
+                                  "GNNV_L2PUSH", "GNNV_NO_LASTUSE"};
     GNNV_REQUIRE(name, GNNV_ERR_PARAM, "set_option: null name");
     bool ok = false;
     for (const char* k : known) ok |= strcmp(k, name) == 0;
@@ -345,6 +345,11 @@ void blocks_enable_csc(gnnv_blocks* b, int h) {
   b->csc_mask |= 1u << h;
   GNNV_TRY_CUDA(cudaDeviceSynchronize());
 }
+void blocks_enable_lastuse(gnnv_blocks* b) {
+  if (b->d_lastv) return;
+  b->d_lastv = (uint32_t*)dmalloc(b->max_n[b->L] * sizeof(uint32_t), "last-use slots");
+  GNNV_TRY_CUDA(cudaMemset(b->d_lastv, 0, b->max_n[b->L] * sizeof(uint32_t)));
+}
 }  // namespace gnnv
 
 extern "C" {
@@ -433,6 +438,7 @@ gnnv_status gnnv_blocks_free(gnnv_blocks* b) {
   }
   dfree(b->d_csc_cnt);
   dfree(b->d_csc_tmp);
+  dfree(b->d_lastv);
   dfree(b->d_sizes);
   dfree(b->d_scan);
   dfree(b->scratch);

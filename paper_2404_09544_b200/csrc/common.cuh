@@ -197,6 +197,11 @@ struct gnnv_blocks {
   int32_t* d_csc[GNNV_MAX_LAYERS] = {nullptr};     // [max_nnz[h]]
   int32_t* d_csc_cnt = nullptr;    // [max n_src + 1] in-edge counts (zero between batches)
   int64_t csc_cnt_cap = 0;
+  // last-use slots of hop L-1 (the layer-1 block): lastv[u] = 1 + the CSR
+  // position of src id u's last edge (0: no edge); the layer-1 aggregation
+  // loads a row for the last time with an L2 evict_first hint
+  // (blocks_enable_lastuse; NULL: off)
+  uint32_t* d_lastv = nullptr;
   void* d_csc_tmp = nullptr;       // cub scan temporary storage
   size_t csc_tmp_bytes = 0;
   bool sampled = false;
@@ -249,6 +254,7 @@ size_t csc_scan_tmp_bytes(int64_t max_items);
 // give hop h of b a transposed block (CSC), built by every later
 // gnnv_sample on b (setup path: allocates; synchronises the device)
 void blocks_enable_csc(gnnv_blocks* b, int h);
+void blocks_enable_lastuse(gnnv_blocks* b);
 // cache.cu
 void launch_cache_update(gnnv_cache* c, const gnnv_blocks* b, const float* d_X, cudaStream_t s);
 void launch_gather(const gnnv_cache* c, const gnnv_blocks* b, float* d_X, int64_t* d_stats, cudaStream_t s,
@@ -257,7 +263,7 @@ void launch_gather(const gnnv_cache* c, const gnnv_blocks* b, float* d_X, int64_
 // rowidx != NULL: source row u is row rowidx[u] of H (the cache table)
 void launch_spmm_fwd(const int32_t* d_indptr, const int32_t* d_indices, const int32_t* d_ndst, int64_t max_dst,
                      const float* H, int32_t ldh, float* A, int32_t lda, int32_t d, int32_t kind, int32_t aggr,
-                     cudaStream_t s, const int32_t* rowidx = nullptr);
+                     cudaStream_t s, const int32_t* rowidx = nullptr, const uint32_t* lastv = nullptr);
 void launch_spmm_bwd(const int32_t* d_indptr, const int32_t* d_indices, const uint32_t* d_own, const int32_t* d_ndst,
                      int64_t max_dst, const float* dA, int32_t lda, float* dH, int32_t ldh, int32_t d, int32_t kind,
                      int32_t aggr, const uint32_t* bits, int32_t bits_ld, cudaStream_t s);

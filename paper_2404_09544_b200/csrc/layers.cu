@@ -274,7 +274,7 @@ void layer_fwd_impl(gnnv_blocks* b, int32_t layer, const gnnv_layer_desc* ld, co
   if (!agg_ready) {
     if (tl) tl->mark(s, "spmm_fwd" + sfx);
     launch_spmm_fwd(b->d_indptr[h], b->d_indices[h], d_ndst, b->max_n[h], rowidx ? agg_table : Hsrc, ld->in_stride,
-                    A, lda, ld->d_in, ld->kind, ld->aggr, s, rowidx);
+                    A, lda, ld->d_in, ld->kind, ld->aggr, s, rowidx, h == b->L - 1 ? b->d_lastv : nullptr);
   }
   GemmFwdArgs g{};
   if (ld->kind == GNNV_KIND_SAGE) {

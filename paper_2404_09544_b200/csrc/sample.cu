@@ -115,7 +115,8 @@ __device__ __forceinline__ void load4(const int32_t* __restrict__ a, int64_t e0,
 __device__ __forceinline__ void map_slots(int64_t t0, int64_t stride, int hp, int kp, const int32_t* sizes,
                                           const int32_t* __restrict__ ellp, const int32_t* __restrict__ cntp,
                                           const int32_t* __restrict__ indptrp, const int32_t* tag,
-                                          int32_t* __restrict__ indicesp, int32_t* __restrict__ csc_cnt = nullptr) {
+                                          int32_t* __restrict__ indicesp, int32_t* __restrict__ csc_cnt = nullptr,
+                                          uint32_t* __restrict__ lastv = nullptr) {
   const int64_t nslots = (int64_t)sizes[hp] * kp;
   for (int64_t e0 = 4 * t0; e0 < nslots; e0 += 4 * stride) {
     int u[4], t[4], dst[4];
@@ -138,6 +139,7 @@ __device__ __forceinline__ void map_slots(int64_t t0, int64_t stride, int hp, in
       if (dst[j] >= 0) {
         indicesp[dst[j]] = t[j];
         if (csc_cnt) atomicAdd(csc_cnt + t[j], 1);
+        if (lastv) atomicMax(lastv + t[j], (uint32_t)dst[j] + 1u);  // the src id's last visit (CSR order)
       }
   }
 }
@@ -442,7 +444,8 @@ __global__ void __launch_bounds__(kScanTile) k_relabel_scan(int64_t N, int h, in
                                                             const int32_t* __restrict__ cnt, int32_t* tag,
                                                             int32_t* __restrict__ F, int32_t* __restrict__ indptr,
                                                             uint32_t* __restrict__ own, int32_t* sizes,
-                                                            unsigned long long* status) {
+                                                            unsigned long long* status,
+                                                            uint32_t* __restrict__ lastv) {
   GNNV_PDL_ENTRY();
   __shared__ int s_tile;
   __shared__ uint32_t s_wa[kScanTile / 32], s_wb[kScanTile / 32];
@@ -545,7 +548,10 @@ __global__ void __launch_bounds__(kScanTile) k_relabel_scan(int64_t N, int h, in
   }
   __syncthreads();
   const uint32_t new_off = s_pa + excl_a, edge_off = s_pb + excl_b;
-  if (r < n) indptr[r] = (int32_t)edge_off;
+  if (r < n) {
+    indptr[r] = (int32_t)edge_off;
+    if (lastv) lastv[r] = 0u;  // last-use slots of this hop's src ids, set by k_map
+  }
   __shared__ uint32_t s_off[kScanTile];
   s_off[threadIdx.x] = new_off;
   __syncthreads();
@@ -561,6 +567,7 @@ __global__ void __launch_bounds__(kScanTile) k_relabel_scan(int64_t N, int h, in
         const int nid = n + (int)s_off[rl] + __popc(m & ((1u << i) - 1u));
         tag[u] = nid;
         F[nid] = u;
+        if (lastv) lastv[nid] = 0u;
       }
     }
   }
@@ -581,12 +588,12 @@ __global__ void __launch_bounds__(kScanTile) k_relabel_scan(int64_t N, int h, in
 __global__ void k_map(int hp, int kp, const int32_t* sizes, const int32_t* __restrict__ ellp,
                       const int32_t* __restrict__ cntp, const int32_t* __restrict__ indptrp, const int32_t* tag,
                       int32_t* __restrict__ indicesp, unsigned long long* scan, int64_t scan_words,
-                      int32_t* __restrict__ csc_cnt) {
+                      int32_t* __restrict__ csc_cnt, uint32_t* __restrict__ lastv) {
   GNNV_PDL_ENTRY();
   const int64_t t0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x, stride = (int64_t)gridDim.x * blockDim.x;
   const int64_t used = std::min<int64_t>(scan_words, 1 + ((int64_t)sizes[hp] + kScanTile - 1) / kScanTile);
   for (int64_t i = t0; i < used; i += stride) scan[i] = 0ull;
-  map_slots(t0, stride, hp, kp, sizes, ellp, cntp, indptrp, tag, indicesp, csc_cnt);
+  map_slots(t0, stride, hp, kp, sizes, ellp, cntp, indptrp, tag, indicesp, csc_cnt, lastv);
 }
 
 // CSC fill of hop hp (counting sort): colptr = exclusive scan of the in-edge
@@ -642,7 +649,7 @@ void launch_sample(gnnv_graph* g, gnnv_blocks* b, const int32_t* d_seeds, int32_
     const bool csc = (b->csc_mask >> hp) & 1u;
     launch_k(k_map, grid_for(slots_ub, 1024), 256, 0, s, hp, b->fanouts[hp], b->d_sizes, b->d_ell, b->d_cnt,
              b->d_indptr[hp], b->d_tag, b->d_indices[hp], b->d_scan, b->scan_words,
-             csc ? b->d_csc_cnt : (int32_t*)nullptr);
+             csc ? b->d_csc_cnt : (int32_t*)nullptr, hp == L - 1 ? b->d_lastv : (uint32_t*)nullptr);
     GNNV_CHECK_LAUNCH();
     if (!csc) return;
     size_t tmp = b->csc_tmp_bytes;
@@ -685,7 +692,8 @@ void launch_sample(gnnv_graph* g, gnnv_blocks* b, const int32_t* d_seeds, int32_
                                                              b->d_own[h]);
     GNNV_CHECK_LAUNCH();
     launch_k(k_relabel_scan, tiles_ub, kScanTile, 0, s, g->n, h, k, L, b->d_ell, b->d_cnt, b->d_tag, b->d_F,
-                                                  b->d_indptr[h], b->d_own[h], b->d_sizes, b->d_scan);
+                                                  b->d_indptr[h], b->d_own[h], b->d_sizes, b->d_scan,
+             h == L - 1 ? b->d_lastv : (uint32_t*)nullptr);
     GNNV_CHECK_LAUNCH();
   }
   map_hop(L - 1);

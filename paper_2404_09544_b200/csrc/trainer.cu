@@ -65,6 +65,9 @@ struct gnnv_trainer {
   // only for the dst prefix layer i+1 reads (its other rows -- 88% of
   // products' H^1 -- never reach HBM) and layer i+1 runs no aggregation
   bool l2push = false;
+  // layer-1 aggregation loads a source row for the last time with an L2
+  // evict_first hint (sampler: last-use slot per src id; GNNV_NO_LASTUSE=1: off)
+  bool lastuse = false;
   float* tail_dA = nullptr;    // [max_n[0] x dims[L-1]]
   float* tail_part = nullptr;  // per-CTA dW/db partials
   unsigned int* loss_counter = nullptr;
@@ -250,6 +253,9 @@ gnnv_status gnnv_trainer_create(gnnv_graph* g, gnnv_cache* c, const gnnv_model_d
       t->l2push = md->prec == GNNV_PREC_TF32 && md->kind == GNNV_KIND_SAGE && L >= 3 && env_on("GNNV_L2PUSH");
       if (t->l2push)
         for (int i = 1; i <= L - 2; ++i) blocks_enable_csc(t->b, L - i - 1);
+      // dead-row L2 hints for the layer-1 aggregation (spmm.cu HINT)
+      t->lastuse = !env_on("GNNV_NO_LASTUSE");
+      if (t->lastuse) blocks_enable_lastuse(t->b);
       if (t->tail) {
         t->tail_dA = (float*)dmalloc((size_t)b->max_n[0] * md->dims[L - 1] * sizeof(float), "output-layer dA");
         t->tail_part = (float*)dmalloc(tail_partial_floats(b->max_n[0], md->dims[L - 1], md->dims[L]) * sizeof(float),
@@ -495,6 +501,7 @@ gnnv_status gnnv_trainer_prefetch(gnnv_trainer* t, const int32_t* seeds, int32_t
       if (st != GNNV_OK) throw Error{st, get_error()};
       if (t->l2push)
         for (int i = 1; i <= t->md.L - 2; ++i) blocks_enable_csc(t->bb[k], t->md.L - i - 1);
+      if (t->lastuse) blocks_enable_lastuse(t->bb[k]);
       const int64_t xrows = t->x_rows ? 1 : t->bb[k]->max_n[t->x_fused ? t->md.L - 1 : t->md.L];
       t->X[k] = (float*)dmalloc((size_t)xrows * g->stride * sizeof(float), "X (prefetch)");
       if (t->x_fused)

@@ -748,6 +748,38 @@ def test_step_whole_table_gather4(mini, option):
     assert_close_cond(Hout, Ho, Hm, RTOL[2], "layer 1 (gather4 H_dst)")
 
 
+@pytest.mark.parametrize("prec", [gnnv.PREC_FP32, gnnv.PREC_TF32])
+@pytest.mark.parametrize("ratio", [0.3, 1.0])
+def test_lastuse_l2_hints_bitwise_neutral(mini, option, prec, ratio):
+    """The layer-1 aggregation's dead-row L2 hints (sampler: last-use slot
+    per src id; evict_first on a row's last visit) change only cache
+    priorities: the whole step -- loss, every activation level, the
+    aggregates -- is bitwise identical with and without them
+    (GNNV_NO_LASTUSE); ratio 1.0 reads the cache table (rowidx), 0.3 reads X."""
+    gd, g = mini
+    cfg = CONFIGS["mini"]
+    dims = [gd.d, cfg["hidden"], cfg["hidden"], gd.C]
+    L = len(cfg["fanouts"])
+    w = init_weights(dims)
+    seeds = epoch_seeds(gd.n, 0)[: cfg["batch"]]
+    out = {}
+    for name in ("hints", "plain"):
+        option("GNNV_NO_LASTUSE", 1 if name == "plain" else 0)
+        tr = gnnv.Trainer(g, gnnv.Cache(g, ratio), dims, cfg["fanouts"], cfg["batch"], w, prec=prec)
+        loss, _ = tr.step(seeds, len(seeds), len(seeds), 0x5EED, 0.0)
+        hb = blocks_to_host(tr.blocks)
+        pa, sa = tr.aggregate(1)
+        acts = [read_f32(pa, hb[L - 1][0], sa)]
+        for lvl in range(1, L):
+            p_, s_ = tr.activation(lvl)
+            acts.append(read_f32(p_, hb[L - 1 - lvl][0], s_))
+        out[name] = (loss, acts)
+        tr.free()
+    assert out["hints"][0] == out["plain"][0]
+    for a_, b_ in zip(out["hints"][1], out["plain"][1]):
+        assert a_.tobytes() == b_.tobytes()
+
+
 @pytest.mark.parametrize("aggr", [gnnv.AGGR_MEAN, gnnv.AGGR_SUM])
 @pytest.mark.parametrize("ratio", [0.3, 1.0])
 def test_fused_l2_push_matches_per_layer_aggregation(mini, option, aggr, ratio):

@@ -48,10 +48,14 @@ def main() -> None:
     ap.add_argument("raw_csv")
     ap.add_argument("--layers", type=int, default=3)
     ap.add_argument("--workload", default="products/tf32")
+    ap.add_argument("--step", type=int, default=-1,
+                    help="keep only the launches of the step-th gnnv_step (0-based; steps start at k_init_seeds)")
+    ap.add_argument("--note", default="ncu --set full, one step (--no-pipeline), caches flushed per kernel replay")
     a = ap.parse_args()
     with open(a.raw_csv) as f:
         rows = [r for r in csv.reader(f)]
-    hdr, units, data = rows[0], rows[1], rows[2:]
+    h0 = next(i for i, r in enumerate(rows) if r and r[0] == "ID")  # skip ncu's log lines
+    hdr, units, data = rows[h0], rows[h0 + 1], rows[h0 + 2:]
     ix = {h: i for i, h in enumerate(hdr)}
     launches = []
     for r in data:
@@ -60,7 +64,19 @@ def main() -> None:
         rd = to_bytes(r[ix["dram__bytes_read.sum"]], units[ix["dram__bytes_read.sum"]])
         wr = to_bytes(r[ix["dram__bytes_write.sum"]], units[ix["dram__bytes_write.sum"]])
         t = to_us(r[ix["gpu__time_duration.sum"]], units[ix["gpu__time_duration.sum"]])
-        launches.append((short(r[ix["Kernel Name"]]), rd, wr, t))
+        extra = {}
+        for col, key in (("pcie__read_bytes.sum", "pcie_read"), ("pcie__write_bytes.sum", "pcie_write")):
+            if col in ix and r[ix[col]] not in ("", "n/a"):
+                extra[key] = to_bytes(r[ix[col]], units[ix[col]])
+        col = "sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed"
+        if col in ix and r[ix[col]] not in ("", "n/a"):
+            extra["tensor_pct"] = float(r[ix[col]].replace(",", ""))
+        launches.append((short(r[ix["Kernel Name"]]), rd, wr, t, extra))
+    if a.step >= 0:  # the launches of one step: from its k_init_seeds to the next one
+        starts = [i for i, k in enumerate(launches) if k[0].startswith("k_init_seeds")]
+        lo = starts[a.step]
+        hi = starts[a.step + 1] if a.step + 1 < len(starts) else len(launches)
+        launches = launches[lo:hi]
     L = a.layers
     seg = OrderedDict()
     f, b, pending_dw, cur = 0, L + 1, False, None
@@ -72,6 +88,11 @@ def main() -> None:
         s["write"] += k[2]
         s["ncu_us"] += k[3]
         s["kernels"].append(k[0])
+        for key in ("pcie_read", "pcie_write"):
+            if key in k[4]:
+                s[key] = s.get(key, 0.0) + k[4][key]
+        if "tensor_pct" in k[4]:  # per kernel (a time-weighted figure is meaningless across kernels)
+            s.setdefault("tensor_pipe_pct", []).append(round(k[4]["tensor_pct"], 2))
 
     for k in launches:
         n = k[0]
@@ -107,13 +128,11 @@ def main() -> None:
             cur = f"spmm_bwd.l{b}"
         elif n.startswith("k_sgd"):
             cur = "sgd"
-        # reductions (k_dw_reduce*, k_colsum_reduce) stay in the current segment
+        # reductions (k_dw_reduce*, k_colsum_reduce), k_zero_rows stay in the current segment
         if cur is None:
             sys.exit(f"unassigned launch {n}")
         add(cur, k)
-    out = {"workload": a.workload, "source": a.raw_csv.split("/")[-1],
-           "note": "ncu --set full, one step (--no-pipeline), caches flushed per kernel replay",
-           "segments": seg}
+    out = {"workload": a.workload, "source": a.raw_csv.split("/")[-1], "note": a.note, "segments": seg}
     json.dump(out, sys.stdout, indent=1)
     print()
 
