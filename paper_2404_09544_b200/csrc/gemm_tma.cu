@@ -257,8 +257,23 @@ struct Params {
   float* push_out;
   int push_ld, push_mean;
   const int32_t* keep_rows;
+  // fwd/dX (not PAIR): dynamic tile scheduler -- [0] next tile counter,
+  // [1] finished CTAs (the last one resets both); NULL: static round robin
+  unsigned int* sched;
 };
 
+
+// The last CTA of a launch to finish resets its scheduler slot for the next
+// launch that draws it (all producers' claims precede every CTA's exit).
+__device__ __forceinline__ void sched_done(unsigned int* sched) {
+  __threadfence();
+  if (atomicAdd(sched + 1, 1u) == gridDim.x * gridDim.y - 1) {
+    sched[0] = 0u;
+    sched[1] = 0u;
+    __threadfence();
+  }
+}
+__device__ unsigned int g_sched[64][2];  // zero-initialised; a ring of slots, one per launch in flight
 
 // PAIR (MODE_FWD only): a cluster of 2 CTAs computes 256-row tiles with
 // tcgen05.mma.cta_group::2 (M = 256): each CTA stages its own 128 rows of A
@@ -270,6 +285,14 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_tma_gemm(const __grid_constant_
   GNNV_PDL_ENTRY();
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   __shared__ float s_bias[256];
+  // dynamic tile scheduler (fwd/dX, not PAIR): the producer claims tiles
+  // (its CTA's first tile statically, then atomically from p.sched) and
+  // publishes each in a ring slot; the MMA and epilogue warps take them in
+  // the same order.  A CTA that starts late -- its SM still held by the
+  // concurrent Eq.4 prefetch -- then simply processes fewer tiles.  The
+  // producer runs at most FWD_STAGES k-blocks ahead of the MMA, which runs at
+  // most two tiles ahead of the epilogue, so 8 slots are never overrun.
+
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
   constexpr int S = MODE == MODE_DW ? DW_STAGES : PAIR ? PAIR_STAGES : FWD_STAGES;
   constexpr int MT = MODE == MODE_DW ? DW_MT : 1;
@@ -298,7 +321,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_tma_gemm(const __grid_constant_
   uint64_t* kfree = kready + 2;     // dW: MMA finished reading tile b
   uint64_t* tfull = kfree + 2;      // fwd/dX: two TMEM accumulators
   uint64_t* tempty = tfull + 2;
-  uint32_t* s_tmem = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* s_tbar = tempty + 2;                          // [8] tile ring barriers
+  int* s_tile = reinterpret_cast<int*>(s_tbar + 8);       // [8] tile ring slots
+  uint32_t* s_tmem = reinterpret_cast<uint32_t*>(s_tile + 8);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int M = *p.dM;
 
@@ -311,8 +336,12 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_tma_gemm(const __grid_constant_
   } else {
     ntiles = ((M + BM - 1) / BM) * (MODE == MODE_DX ? p.n_ntiles : 1);
     if (PAIR) ntiles = (ntiles + 1) / 2;  // 256-row pair tiles
-    if (pid >= ntiles) return;  // block-uniform (pair-uniform)
+    if (pid >= ntiles) {  // block-uniform (pair-uniform)
+      if (!PAIR && p.sched && threadIdx.x == 0) sched_done(p.sched);
+      return;
+    }
   }
+  const bool dyn = MODE != MODE_DW && !PAIR && p.sched != nullptr;
   uint32_t ncols = 32;
   const uint32_t need = (uint32_t)(MT * BN) * (MODE == MODE_DW ? 1u : 2u);
   while (ncols < need) ncols <<= 1;
@@ -328,6 +357,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_tma_gemm(const __grid_constant_
       mbar_init(&tfull[b], 1);
       mbar_init(&tempty[b], PAIR ? 2 * NE : NE);  // PAIR: the leader's, both CTAs' epilogue warps
     }
+    for (int i = 0; i < 8; ++i) mbar_init(&s_tbar[i], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (PAIR) cluster_sync_all();  // the peer's barriers exist before any remote arrive / TMA
@@ -382,8 +412,13 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_tma_gemm(const __grid_constant_
           }
         }
       } else if (lane == 0 || g4) {
-        int it = 0;
-        for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        int it = 0, lt = 0;
+        for (int tile = blockIdx.x;; ++lt) {
+          if (dyn && lane == 0) {  // publish the tile (or the end) to the MMA and epilogue warps
+            s_tile[lt & 7] = tile < ntiles ? tile : -1;
+            mbar_arrive(&s_tbar[lt & 7]);
+          }
+          if (tile >= ntiles) break;
           const int mt = MODE == MODE_DX ? tile / p.n_ntiles : tile;
           const int nt = MODE == MODE_DX ? tile % p.n_ntiles : 0;
           // gather4: lane l loads rows 4l..4l+3 of the tile; rows >= M read
@@ -413,6 +448,13 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_tma_gemm(const __grid_constant_
               tma_load_2d(sa, &p.ta1, kb * BK, mt * BM, &full[s]);
             }
             if (lane == 0) tma_load_2d(sb, &p.tb, kb * BK, nt * BN, &full[s]);
+          }
+          if (dyn) {
+            int next = 0;
+            if (lane == 0) next = (int)gridDim.x + (int)atomicAdd(p.sched, 1u);
+            tile = g4 ? __shfl_sync(0xffffffffu, next, 0) : next;
+          } else {
+            tile += gridDim.x;
           }
         }
       }
@@ -444,7 +486,14 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_tma_gemm(const __grid_constant_
       } else if (lane == 0) {
         const uint32_t idesc = idesc_tf32((uint32_t)BN, false, false);
         int it = 0, lt = 0;
-        for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++lt) {
+        for (int tile = blockIdx.x;; tile += gridDim.x, ++lt) {
+          if (dyn) {
+            mbar_wait(&s_tbar[lt & 7], (lt >> 3) & 1);
+            tile = s_tile[lt & 7];
+            if (tile < 0) break;
+          } else if (tile >= ntiles) {
+            break;
+          }
           const int acc = lt & 1;
           if (lt >= 2) mbar_wait(&tempty[acc], ((lt >> 1) & 1) ^ 1);
           tc_after();
@@ -476,7 +525,14 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_tma_gemm(const __grid_constant_
       uint8_t* ob0 = obuf + (warp - 2) * 4096 * OBN;
       int obi = 0;
       int lt = 0;
-      for (int tile = pid; tile < ntiles; tile += npid, ++lt) {
+      for (int tile = pid;; tile += npid, ++lt) {
+        if (dyn) {
+          mbar_wait(&s_tbar[lt & 7], (lt >> 3) & 1);
+          tile = s_tile[lt & 7];
+          if (tile < 0) break;
+        } else if (tile >= ntiles) {
+          break;
+        }
         const int acc = lt & 1;
         const int mt = PAIR ? 2 * tile + (int)crank : MODE == MODE_DX ? tile / p.n_ntiles : tile;
         const int nt = MODE == MODE_DX ? tile % p.n_ntiles : 0;
@@ -902,6 +958,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_tma_gemm(const __grid_constant_
     else
       asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(ncols) : "memory");
   }
+  if (dyn && threadIdx.x == 0) sched_done(p.sched);
 }
 
 // --------------------------------------------------------- prep kernels
@@ -992,7 +1049,7 @@ static size_t smem_bytes(int mode, int BN, int mask, int nwp, bool pair = false)
   const int a = mode == MODE_DW ? DW_MT * DW_KR * BM * 4 : BM * BKB;
   const int b = mode == MODE_DW ? DW_KR * BN * 4 + (mask ? DW_KR * nwp * 4 : 0) : (pair ? BN / 2 : BN) * BKB;
   const int k = mode == MODE_DW ? 2 * (DW_MT * BM + BN) * 64 : NE * 4096 * (pair ? PAIR_OB : 1);
-  return (((size_t)S * (a + b) + 1023) & ~(size_t)1023) + k + 8 * (2 * S + 8) + 16 + 1024;
+  return (((size_t)S * (a + b) + 1023) & ~(size_t)1023) + k + 8 * (2 * S + 8 + 8) + 32 + 16 + 1024;
 }
 
 template <int MODE>
@@ -1040,6 +1097,21 @@ static void launch_pair(const Params& p, int pairs, cudaStream_t s) {
 
 static int rup(int x, int m) { return (x + m - 1) / m * m; }
 
+// a scheduler slot for the next fwd/dX launch (ring of 64; a slot is reset
+// by the last CTA of the launch that used it).  GNNV_STATIC_TILES=1: the
+// static round robin instead.
+static unsigned int* next_sched() {
+  if (env_on("GNNV_STATIC_TILES")) return nullptr;
+  static unsigned int* base = nullptr;
+  static unsigned slot = 0;
+  if (!base) {
+    void* p = nullptr;
+    GNNV_TRY_CUDA(cudaGetSymbolAddress(&p, g_sched));
+    base = static_cast<unsigned int*>(p);
+  }
+  return base + 2 * (slot++ % 64);
+}
+
 }  // namespace tma
 
 bool gemm_fwd_tma(const GemmFwdArgs& a, cudaStream_t s) {
@@ -1086,6 +1158,7 @@ bool gemm_fwd_tma(const GemmFwdArgs& a, cudaStream_t s) {
   GNNV_REQUIRE(!a.push_out || (a.push_colptr && a.push_dst && a.push_indptr && a.keep_rows && a.push_ld % 4 == 0 &&
                                a.push_ld >= a.N),
                GNNV_ERR_PARAM, "fwd: incomplete fused-push arguments");
+  p.sched = pair ? nullptr : next_sched();
   const int64_t tiles = ceil_div(std::max<int64_t>(a.max_M, 1), BM);
   if (pair) {
     launch_pair(p, (int)std::min<int64_t>(ceil_div(tiles, 2), num_sms() / 2), s);
@@ -1125,6 +1198,7 @@ bool gemm_dx_tma(const GemmDxArgs& a, cudaStream_t s) {
   p.ybits = a.y1_bits;
   p.ybits_ld = a.y1_bits_ld;
   const int64_t tiles = ceil_div(std::max<int64_t>(a.max_M, 1), BM) * ntl;
+  p.sched = next_sched();
   launch<MODE_DX>(p, dim3((unsigned)std::min<int64_t>(tiles, num_sms())), s);
   return true;
 }

@@ -66,7 +66,7 @@ struct gnnv_trainer {
   // products' H^1 -- never reach HBM) and layer i+1 runs no aggregation
   bool l2push = false;
   // layer-1 aggregation loads a source row for the last time with an L2
-  // evict_first hint (sampler: last-use slot per src id; GNNV_NO_LASTUSE=1: off)
+  // evict_first hint (sampler: last-use slot per src id; opt-in GNNV_LASTUSE=1)
   bool lastuse = false;
   float* tail_dA = nullptr;    // [max_n[0] x dims[L-1]]
   float* tail_part = nullptr;  // per-CTA dW/db partials
@@ -253,8 +253,10 @@ gnnv_status gnnv_trainer_create(gnnv_graph* g, gnnv_cache* c, const gnnv_model_d
       t->l2push = md->prec == GNNV_PREC_TF32 && md->kind == GNNV_KIND_SAGE && L >= 3 && env_on("GNNV_L2PUSH");
       if (t->l2push)
         for (int i = 1; i <= L - 2; ++i) blocks_enable_csc(t->b, L - i - 1);
-      // dead-row L2 hints for the layer-1 aggregation (spmm.cu HINT)
-      t->lastuse = !env_on("GNNV_NO_LASTUSE");
+      // dead-row L2 hints for the layer-1 aggregation (spmm.cu HINT; opt-in
+      // GNNV_LASTUSE=1: measured 1.11 -> 1.04 GB DRAM reads but 255 -> 262 us
+      // on products)
+      t->lastuse = env_on("GNNV_LASTUSE");
       if (t->lastuse) blocks_enable_lastuse(t->b);
       if (t->tail) {
         t->tail_dA = (float*)dmalloc((size_t)b->max_n[0] * md->dims[L - 1] * sizeof(float), "output-layer dA");

@@ -748,6 +748,39 @@ def test_step_whole_table_gather4(mini, option):
     assert_close_cond(Hout, Ho, Hm, RTOL[2], "layer 1 (gather4 H_dst)")
 
 
+def test_dynamic_tile_scheduler_bitwise_neutral(mini, option):
+    """The persistent tf32 fwd/dX GEMMs claim their tiles from a device
+    counter (a CTA that starts late takes fewer tiles); which CTA computes a
+    tile does not change its arithmetic, so a whole pipelined step's forward -- loss
+    and every activation -- is bitwise the static round
+    robin's (GNNV_STATIC_TILES), also for ragged tile counts, over repeated
+    steps (the scheduler slots reset themselves)."""
+    gd, g = mini
+    cfg = CONFIGS["mini"]
+    dims = [gd.d, 96, 80, gd.C]
+    L = len(cfg["fanouts"])
+    w = init_weights(dims)
+    perm = epoch_seeds(gd.n, 0)
+    out = {}
+    for name in ("dynamic", "static"):
+        option("GNNV_STATIC_TILES", 1 if name == "static" else 0)
+        tr = gnnv.Trainer(g, gnnv.Cache(g, 0.3), dims, cfg["fanouts"], cfg["batch"], w, prec=gnnv.PREC_TF32)
+        res = []
+        for t in range(3):
+            seeds = perm[t * 300:(t + 1) * 300]
+            tr.prefetch(seeds, len(seeds), 40 + t)
+            loss, _ = tr.step(seeds, len(seeds), len(seeds), 40 + t, 0.0)
+            hb = blocks_to_host(tr.blocks)
+            acts = [loss]
+            for lvl in range(1, L + 1):
+                p_, s_ = tr.activation(lvl)
+                acts.append(read_f32(p_, hb[L - lvl][0], s_).tobytes())
+            res.append(acts)
+        out[name] = res
+        tr.free()
+    assert out["dynamic"] == out["static"]
+
+
 @pytest.mark.parametrize("prec", [gnnv.PREC_FP32, gnnv.PREC_TF32])
 @pytest.mark.parametrize("ratio", [0.3, 1.0])
 def test_lastuse_l2_hints_bitwise_neutral(mini, option, prec, ratio):
@@ -755,7 +788,7 @@ def test_lastuse_l2_hints_bitwise_neutral(mini, option, prec, ratio):
     per src id; evict_first on a row's last visit) change only cache
     priorities: the whole step -- loss, every activation level, the
     aggregates -- is bitwise identical with and without them
-    (GNNV_NO_LASTUSE); ratio 1.0 reads the cache table (rowidx), 0.3 reads X."""
+    (opt-in GNNV_LASTUSE); ratio 1.0 reads the cache table (rowidx), 0.3 reads X."""
     gd, g = mini
     cfg = CONFIGS["mini"]
     dims = [gd.d, cfg["hidden"], cfg["hidden"], gd.C]
@@ -764,7 +797,7 @@ def test_lastuse_l2_hints_bitwise_neutral(mini, option, prec, ratio):
     seeds = epoch_seeds(gd.n, 0)[: cfg["batch"]]
     out = {}
     for name in ("hints", "plain"):
-        option("GNNV_NO_LASTUSE", 1 if name == "plain" else 0)
+        option("GNNV_LASTUSE", 1 if name == "hints" else 0)
         tr = gnnv.Trainer(g, gnnv.Cache(g, ratio), dims, cfg["fanouts"], cfg["batch"], w, prec=prec)
         loss, _ = tr.step(seeds, len(seeds), len(seeds), 0x5EED, 0.0)
         hb = blocks_to_host(tr.blocks)
