@@ -675,7 +675,7 @@ def main():
     # locality bias, replicated, SAGE) at a given config, ratio and precision
     default_cfg = (args.locality_bias == 0 and args.placement == "replica" and args.kind == "sage"
                    and args.policy == "degree")
-    traffic = load_traffic(f"{cfg['name']}@{cfg['ratio']:g}/{args.prec}") if default_cfg else {}
+    traffic = load_traffic(f"{cfg['name']}@{float(cfg['ratio'])}/{args.prec}") if default_cfg else {}
     # dominant kernel segment of the timed region
     seg_ms = {k: v[0] / max(1, v[1]) for k, v in segs.items()}
     seg_tot = {k: v[0] for k, v in segs.items()}
@@ -710,8 +710,25 @@ def main():
             r["edge_visit_bytes"] = ev
             r["edge_visit_frac"] = ev / (avg_ms / 1000.0) / 1e9 / peaks["hbm"]
         rooflines[name] = r
-        if roofline is None and not name.startswith("pf_"):
-            roofline = r
+    # the dominant kernel of the critical path: the largest step-stream
+    # segment -- unless the step stream spends a quarter of its time waiting
+    # for the Eq.4 prefetch (host-miss-bound configs: the zero-copy gather
+    # over PCIe is then the critical path), in which case the prefetch's
+    # larger segment
+    wait = seg_tot.get("wait_prefetch", 0.0)
+    pf_bound = wait > 0.25 * main_tot or (
+        "pf_gather" in rooflines and rooflines["pf_gather"]["bound"] == "host-link"
+        and rooflines["pf_gather"]["avg_ms"] > 0.5 * (main_tot / max(1, args.steps)))
+    for name, tot in ranked:
+        if name not in rooflines:
+            continue
+        if name.startswith("pf_") != pf_bound:
+            continue
+        if pf_bound and name == "pf_sample" and "pf_gather" in rooflines and \
+                seg_tot["pf_gather"] >= 0.5 * seg_tot["pf_sample"]:
+            continue  # the sampler's overlapped time is stretched by its low priority
+        roofline = dict(rooflines[name], critical_path="prefetch" if pf_bound else "step")
+        break
     # north_star's "per-iteration gather+SpMM" against HBM: algorithmic bytes
     # of the gather and every aggregation segment over their summed times
     gs = [k for k in rooflines if k.split(".")[0] in ("gather", "pf_gather", "spmm_fwd", "spmm_bwd")]

@@ -109,6 +109,12 @@ const char* gnnv_last_error(void);
  * kernels launched (GEMM_PAIR, NO_PDL, STATIC_TILES) afterwards.  PARAM on an unknown
  * name.  Process-wide; not for concurrent use with running steps. */
 gnnv_status gnnv_set_option(const char* name, int32_t value);
+/* Debug (GNNV_GUARD_ALLOC=1 in the environment when the first allocation is
+ * made): every library allocation carries 64 KB guard regions before and
+ * after it; this call synchronises the device and sets *n_bad to the number
+ * of guard regions whose bytes changed (out-of-bounds writes), naming them
+ * in gnnv_last_error().  0 when guards are off. */
+gnnv_status gnnv_debug_check_guards(int32_t* n_bad);
 const char* gnnv_version(void);
 /* Number of kernels libgnnv has launched in this process (monotonic). */
 uint64_t gnnv_launch_count(void);

@@ -44,10 +44,28 @@ int32_t locality_weight(double bias) {
 }
 const char* get_error() { return g_last_error.c_str(); }
 
+// Guarded allocations (GNNV_GUARD_ALLOC=1; the pool's compute-sanitizer is
+// closed): every library allocation gets a 64 KB guard region on each side,
+// filled with 0xA5; gnnv_debug_check_guards() reports any allocation whose
+// guard bytes changed, i.e. an out-of-bounds write by any kernel.
+constexpr size_t kGuard = 1 << 16;
+struct GuardRec {
+  char* base;
+  size_t bytes;
+  std::string what;
+};
+static std::mutex g_guard_mu;
+static std::vector<std::pair<void*, GuardRec>> g_guard;
+static bool guard_on() {
+  static const bool on = env_on("GNNV_GUARD_ALLOC");
+  return on;
+}
+
 void* dmalloc(size_t bytes, const char* what) {
   if (bytes == 0) bytes = 16;
   void* p = nullptr;
-  cudaError_t e = cudaMalloc(&p, bytes);
+  const bool guard = guard_on();
+  cudaError_t e = cudaMalloc(&p, guard ? bytes + 2 * kGuard : bytes);
   if (e != cudaSuccess) {
     cudaGetLastError();
     char buf[256];
@@ -55,11 +73,49 @@ void* dmalloc(size_t bytes, const char* what) {
              cudaGetErrorString(e));
     throw Error{e == cudaErrorMemoryAllocation ? GNNV_ERR_OOM : GNNV_ERR_CUDA, buf};
   }
-  return p;
+  if (!guard) return p;
+  char* base = static_cast<char*>(p);
+  GNNV_TRY_CUDA(cudaMemset(base, 0xA5, kGuard));
+  GNNV_TRY_CUDA(cudaMemset(base + kGuard + bytes, 0xA5, kGuard));
+  GNNV_TRY_CUDA(cudaDeviceSynchronize());
+  std::lock_guard<std::mutex> lk(g_guard_mu);
+  g_guard.emplace_back(base + kGuard, GuardRec{base, bytes, what});
+  return base + kGuard;
+}
+
+static int g_guard_freed_bad = 0;  // violations found when an allocation was freed
+static std::string g_guard_freed_msg;
+
+// index of the first modified guard byte of side 0 (before) / 1 (after), or kGuard
+static size_t guard_first_bad(const GuardRec& r, int side) {
+  std::vector<unsigned char> h(kGuard);
+  const char* g = side ? r.base + kGuard + r.bytes : r.base;
+  if (cudaMemcpy(h.data(), g, kGuard, cudaMemcpyDeviceToHost) != cudaSuccess) return 0;
+  for (size_t i = 0; i < kGuard; ++i)
+    if (h[i] != 0xA5) return i;
+  return kGuard;
 }
 
 void dfree(void* p) {
-  if (p) cudaFree(p);
+  if (!p) return;
+  if (guard_on()) {
+    std::lock_guard<std::mutex> lk(g_guard_mu);
+    for (size_t i = 0; i < g_guard.size(); ++i)
+      if (g_guard[i].first == p) {
+        const GuardRec& r = g_guard[i].second;
+        cudaDeviceSynchronize();
+        for (int side = 0; side < 2; ++side)
+          if (guard_first_bad(r, side) < kGuard) {
+            ++g_guard_freed_bad;
+            g_guard_freed_msg += (g_guard_freed_msg.empty() ? "" : "; ") + r.what + " (freed): guard " +
+                                 (side ? "after the end" : "before the start") + " modified";
+          }
+        cudaFree(r.base);
+        g_guard.erase(g_guard.begin() + (long)i);
+        return;
+      }
+  }
+  cudaFree(p);
 }
 
 int num_sms() {
@@ -141,6 +197,34 @@ void* gnnv_blocks::ensure_scratch(size_t bytes, cudaStream_t s) {
 extern "C" {
 
 const char* gnnv_last_error(void) { return get_error(); }
+
+gnnv_status gnnv_debug_check_guards(int32_t* n_bad) {
+  return guarded([&] {
+    GNNV_REQUIRE(n_bad, GNNV_ERR_PARAM, "debug_check_guards: null");
+    *n_bad = 0;
+    if (!guard_on()) return;
+    GNNV_TRY_CUDA(cudaDeviceSynchronize());
+    std::lock_guard<std::mutex> lk(g_guard_mu);
+    std::string bad = g_guard_freed_msg;
+    *n_bad = g_guard_freed_bad;
+    g_guard_freed_bad = 0;
+    g_guard_freed_msg.clear();
+    for (auto& kv : g_guard) {
+      const GuardRec& r = kv.second;
+      for (int side = 0; side < 2; ++side) {
+        const size_t first = guard_first_bad(r, side);
+        if (first < kGuard) {
+          ++*n_bad;
+          char buf[256];
+          snprintf(buf, sizeof(buf), "%s%s (%zu bytes): guard %s modified at byte %zu", bad.empty() ? "" : "; ",
+                   r.what.c_str(), r.bytes, side ? "after the end" : "before the start", first);
+          bad += buf;
+        }
+      }
+    }
+    if (*n_bad) set_error(bad);
+  });
+}
 
 gnnv_status gnnv_set_option(const char* name, int32_t value) {
   return guarded([&] {

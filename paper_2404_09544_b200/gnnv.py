@@ -83,6 +83,7 @@ _SIGS = {
     "gnnv_last_error": (C.c_char_p, []),
     "gnnv_version": (C.c_char_p, []),
     "gnnv_set_option": (I32, [C.c_char_p, I32]),
+    "gnnv_debug_check_guards": (I32, [C.POINTER(I32)]),
     "gnnv_row_stride": (I32, [I32]),
     "gnnv_launch_count": (U64, []),
     "gnnv_graph_load": (I32, [VP, VP, I64, I64, VP, I32, I32, VP, I32, I32, PP]),
@@ -191,6 +192,13 @@ def version() -> str:
 def set_option(name: str, value: int):
     """gnnv_set_option: opt-in variant switches (1 on, 0 off, -1 environment)."""
     _check(load().gnnv_set_option(name.encode(), int(value)))
+
+
+def check_guards() -> str:
+    """gnnv_debug_check_guards: '' if no guard region changed, else the report."""
+    n = C.c_int32(0)
+    _check(load().gnnv_debug_check_guards(C.byref(n)))
+    return load().gnnv_last_error().decode(errors="replace") if n.value else ""
 
 
 def launch_count() -> int:

@@ -25,3 +25,16 @@ def pytest_collection_modifyitems(config, items):
     for it in items:
         if "gpu" in it.keywords:
             it.add_marker(skip)
+
+
+@pytest.fixture(autouse=True)
+def _guard_check(request):
+    """With GNNV_GUARD_ALLOC=1: after every GPU test, no library allocation's
+    guard region may have changed (out-of-bounds writes; the pool's
+    compute-sanitizer is closed)."""
+    yield
+    if os.environ.get("GNNV_GUARD_ALLOC") == "1" and "gpu" in request.keywords:
+        from paper_2404_09544_b200 import gnnv
+
+        report = gnnv.check_guards()
+        assert report == "", report

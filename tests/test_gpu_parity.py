@@ -2,6 +2,8 @@
 the same seeded inputs.  Integer work (sampling, relabelling, cache slots,
 hit counters) and gathered rows are bit-exact; floating point within the
 condition-aware tolerance of reading Q17 (1e-5 fp32, 2e-2 bf16)."""
+import os
+
 import numpy as np
 import pytest
 import torch
@@ -968,3 +970,33 @@ def test_backward_pull_matches_push(mini, option, kind, prec):
                          kind=kname)
         for (gW, gb), (rW, rb) in zip(gnnv.unflat_params(p["grads"], dims, kind), ref["grads"]):
             assert normwise(gW, rW) < 1e-4 and normwise(gb, rb) < 1e-4
+
+
+@pytest.mark.skipif(os.environ.get("GNNV_GUARD_ALLOC") != "1", reason="guarded allocations off (GNNV_GUARD_ALLOC=1)")
+def test_guard_alloc_detects_out_of_bounds_write(mini):
+    """Negative control of the guarded-allocation check that stands in for
+    compute-sanitizer (closed on this pool): a kernel writing 12 floats past
+    the end of a library allocation (gnnv_sgd over a range that ends beyond
+    the trainer's H^1 buffer) is reported; the guard is then restored."""
+    import ctypes
+
+    gd, g = mini
+    cfg = CONFIGS["mini"]
+    dims = [gd.d, cfg["hidden"], cfg["hidden"], gd.C]
+    L = len(cfg["fanouts"])
+    tr = gnnv.Trainer(g, gnnv.Cache(g, cfg["ratio"]), dims, cfg["fanouts"], cfg["batch"], init_weights(dims))
+    tr.step(epoch_seeds(gd.n, 0)[: cfg["batch"]], cfg["batch"], cfg["batch"], 1, 0.0)
+    assert gnnv.check_guards() == ""
+    p1, s1 = tr.activation(1)
+    rows = tr.blocks.info(sync=False)[L - 1].max_dst
+    end = p1 + rows * s1 * 4
+    ones = torch.ones(16, dtype=torch.float32, device="cuda")
+    gnnv.sgd(end - 16, ones.data_ptr(), 16, -1.0)  # 4 floats inside, 12 past the end
+    torch.cuda.synchronize()
+    report = gnnv.check_guards()
+    assert "H activations" in report and "after the end" in report, report
+    rt = ctypes.CDLL("libcudart.so.12")
+    assert rt.cudaMemset(ctypes.c_void_p(end), 0xA5, ctypes.c_size_t(48)) == 0
+    torch.cuda.synchronize()
+    assert gnnv.check_guards() == ""
+    tr.free()
