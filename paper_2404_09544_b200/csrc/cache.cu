@@ -147,7 +147,7 @@ static void open_peers(gnnv_cache* c, const cudaIpcMemHandle_t* handles) {
     if (o == c->rank || c->shards[o]) continue;
     void* p = nullptr;
     GNNV_TRY_CUDA(cudaIpcOpenMemHandle(&p, handles[o], cudaIpcMemLazyEnablePeerAccess));
-    c->shards[o] = (float*)p;
+    c->shards[o] = (float*)((char*)p + ipc_offset());
     c->shard_ipc[o] = true;
   }
   GNNV_TRY_CUDA(cudaMemcpy((void*)c->d_shard_ptrs, c->shards.data(), c->world * sizeof(float*),
@@ -431,7 +431,7 @@ gnnv_status gnnv_cache_free(gnnv_cache* c) {
   dfree(c->d_order);
   for (size_t o = 0; o < c->shards.size(); ++o) {
     if (c->shard_owned[o]) dfree(c->shards[o]);
-    if (c->shard_ipc[o]) cudaIpcCloseMemHandle(c->shards[o]);
+    if (c->shard_ipc[o]) cudaIpcCloseMemHandle((char*)c->shards[o] - ipc_offset());
   }
   dfree((void*)c->d_shard_ptrs);
   dfree(c->d_owner);

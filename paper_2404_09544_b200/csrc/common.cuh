@@ -96,6 +96,9 @@ gnnv_status guarded(F&& body) {
 }
 
 void* dmalloc(size_t bytes, const char* what);  // throws OOM with the byte count
+// offset of a dmalloc pointer from its allocation's base (a CUDA IPC handle
+// maps the base): 0, or the guard region's size with GNNV_GUARD_ALLOC
+size_t ipc_offset();
 void dfree(void* p);
 
 inline int32_t row_stride(int32_t d) { return (d + 3) & ~3; }

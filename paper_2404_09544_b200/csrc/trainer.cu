@@ -68,6 +68,13 @@ struct gnnv_trainer {
   // layer-1 aggregation loads a source row for the last time with an L2
   // evict_first hint (sampler: last-use slot per src id; opt-in GNNV_LASTUSE=1)
   bool lastuse = false;
+  // Layer 1's aggregation depends on the sampled block and the features
+  // only (no weight), so the Eq.4 prefetch also computes it for the batch it
+  // prepares (on the side stream, into that buffer set's A^1), and a step
+  // consuming a prefetch starts at the layer-1 GEMM.  GNNV_NO_PF_AGG=1: in the
+  // step.  A^1 per buffer set: A1b[k] (t->A[1] follows the current set).
+  bool pf_agg = false;
+  float* A1b[2] = {nullptr, nullptr};
   float* tail_dA = nullptr;    // [max_n[0] x dims[L-1]]
   float* tail_part = nullptr;  // per-CTA dW/db partials
   unsigned int* loss_counter = nullptr;
@@ -147,6 +154,7 @@ gnnv_status gnnv_trainer_free(gnnv_trainer* t) {
     gnnv_blocks_free(t->bb[k]);
     dfree(t->X[k]);
     dfree(t->rowidx[k]);
+    if (k == 1) dfree(t->A1b[1]);  // A1b[0] is A[1], freed with the layers
     dfree(t->d_seedsb[k]);
     if (t->h_seedsb[k]) cudaFreeHost(t->h_seedsb[k]);
     dfree(t->d_statsb[k]);
@@ -165,6 +173,7 @@ gnnv_status gnnv_trainer_free(gnnv_trainer* t) {
   for (auto& e : t->ev_loss)
     if (e) cudaEventDestroy(e);
   if (t->h_err) cudaFreeHost(t->h_err);
+  if (t->A1b[0]) t->A[1] = t->A1b[0];  // the set-0 buffer is the one the layer loop allocated
   for (int i = 1; i <= GNNV_MAX_LAYERS; ++i) {
     dfree(t->H[i]);
     dfree(t->A[i]);
@@ -235,6 +244,7 @@ gnnv_status gnnv_trainer_create(gnnv_graph* g, gnnv_cache* c, const gnnv_model_d
       const int64_t xrows = t->x_rows ? 1 : t->x_fused ? b->max_n[L - 1] : b->max_n[L];
       t->H[0] = (float*)dmalloc((size_t)xrows * g->stride * sizeof(float), "X (gathered features)");
       if (t->x_fused) t->rowidx[0] = (int32_t*)dmalloc(b->max_n[L] * sizeof(int32_t), "cache rows of F_L");
+      t->pf_agg = !env_on("GNNV_NO_PF_AGG");
       for (int i = 1; i <= L; ++i) {
         t->Hs[i] = row_stride(md->dims[i]);
         const int64_t rows = b->max_n[L - i];
@@ -274,6 +284,7 @@ gnnv_status gnnv_trainer_create(gnnv_graph* g, gnnv_cache* c, const gnnv_model_d
       t->d_seedsb[0] = t->d_seeds;
       t->h_seedsb[0] = t->h_seeds;
       t->d_statsb[0] = t->d_stats;
+      t->A1b[0] = t->A[1];
       for (int k = 0; k < 2; ++k) {
         GNNV_TRY_CUDA(cudaEventCreateWithFlags(&t->ev_ready[k], cudaEventDisableTiming));
         GNNV_TRY_CUDA(cudaEventCreateWithFlags(&t->ev_free[k], cudaEventDisableTiming));
@@ -465,6 +476,7 @@ static void select_buffers(gnnv_trainer* t, int k) {
   t->d_seeds = t->d_seedsb[k];
   t->h_seeds = t->h_seedsb[k];
   t->d_stats = t->d_statsb[k];
+  if (t->A1b[k]) t->A[1] = t->A1b[k];
 }
 
 // Stage host seeds (validated) or take device seeds; returns device pointer.
@@ -511,6 +523,9 @@ gnnv_status gnnv_trainer_prefetch(gnnv_trainer* t, const int32_t* seeds, int32_t
       t->d_seedsb[k] = (int32_t*)dmalloc(t->md.max_seeds * sizeof(int32_t), "seeds (prefetch)");
       GNNV_TRY_CUDA(cudaMallocHost(&t->h_seedsb[k], t->md.max_seeds * sizeof(int32_t)));
       t->d_statsb[k] = (int64_t*)dmalloc(4 * sizeof(int64_t), "gather stats (prefetch)");
+      if (t->pf_agg)
+        t->A1b[k] = (float*)dmalloc((size_t)t->bb[k]->max_n[t->md.L - 1] * row_stride(t->md.dims[0]) * sizeof(float),
+                                    "layer-1 aggregates (prefetch)");
       // the layer backward's scratch arena, sized like the first buffer set's
       // (grown by its steps so far): growing it at this set's first step
       // would put a device synchronisation and a cudaMalloc inside the step
@@ -550,6 +565,15 @@ gnnv_status gnnv_trainer_prefetch(gnnv_trainer* t, const int32_t* seeds, int32_t
       GNNV_TRY_CUDA(cudaEventRecord(t->ev_cache, t->side));
       t->cache_pending = true;
     }
+    if (t->pf_agg) {  // layer 1's aggregation of the prefetched batch (no weight involved)
+      if (tl) tl->mark(t->side, "pf_spmm_fwd.l1");
+      const int L = t->md.L, h = L - 1;
+      gnnv_blocks* bk = t->bb[k];
+      launch_spmm_fwd(bk->d_indptr[h], bk->d_indices[h], bk->d_sizes + h, bk->max_n[h],
+                      t->x_fused ? t->table : t->X[k], g->stride, t->A1b[k], row_stride(t->md.dims[0]),
+                      t->md.dims[0], t->md.kind, t->md.aggr, t->side, t->x_fused ? t->rowidx[k] : nullptr,
+                      bk->d_lastv);
+    }
 
     if (tl) tl->mark(t->side, "end");
     GNNV_TRY_CUDA(cudaEventRecord(t->ev_ready[k], t->side));
@@ -584,12 +608,14 @@ gnnv_status gnnv_step(gnnv_trainer* t, const int32_t* seeds, int32_t n_seeds, in
       ~StepPdl() { set_pdl(true); }
     } step_pdl(!t->pending);
     if (tm) GNNV_TRY_CUDA(cudaEventRecord(t->ev[0], s));
+    bool agg1_ready = false;
     if (t->pending) {
       // the batch was sampled and gathered by gnnv_trainer_prefetch
       GNNV_REQUIRE(n_seeds == t->pend_n && rng_seed == t->pend_rng, GNNV_ERR_STATE,
                    "step: seeds/rng_seed differ from the pending prefetch");
       select_buffers(t, t->cur ^ 1);
       t->pending = false;
+      agg1_ready = t->pf_agg;
       if (tl) tl->mark(s, "wait_prefetch");
       GNNV_TRY_CUDA(cudaStreamWaitEvent(s, t->ev_ready[t->cur], 0));
       if (tm) GNNV_TRY_CUDA(cudaEventRecord(t->ev[1], s));
@@ -629,7 +655,8 @@ gnnv_status gnnv_step(gnnv_trainer* t, const int32_t* seeds, int32_t n_seeds, in
       }
       layer_fwd_impl(b, i, &ld, t->H[i - 1], t->d_params + t->w_off[i - 1], t->d_params + t->b_off[i - 1], t->H[i],
                      t->A[i], s, tl, t->mbits[i], t->table, i == 1 ? t->rowidx[t->cur] : nullptr,
-                     i == 1 ? xr1 : nullptr, do_push ? &push : nullptr, t->l2push && i >= 2 && i <= L - 1);
+                     i == 1 ? xr1 : nullptr, do_push ? &push : nullptr,
+                     (t->l2push && i >= 2 && i <= L - 1) || (i == 1 && agg1_ready));
     }
     if (tm) GNNV_TRY_CUDA(cudaEventRecord(t->ev[3], s));
     float* d_loss = t->d_grads + t->nparams;

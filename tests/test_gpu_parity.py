@@ -783,6 +783,46 @@ def test_dynamic_tile_scheduler_bitwise_neutral(mini, option):
     assert out["dynamic"] == out["static"]
 
 
+@pytest.mark.parametrize("kind", [gnnv.KIND_SAGE, gnnv.KIND_GCN])
+@pytest.mark.parametrize("ratio", [0.3, 1.0])
+def test_prefetched_layer1_aggregation_bitwise(mini, option, kind, ratio):
+    """The Eq.4 prefetch also runs layer 1's aggregation (it needs no
+    weight) for the batch it prepares, and the consuming step starts at the
+    layer-1 GEMM (GNNV_NO_PF_AGG keeps it in the step): the same kernel on
+    the same inputs, so three pipelined steps (weights updated in between)
+    give bitwise the same losses, aggregates and activations; ratio 1.0
+    aggregates from the cache table, 0.3 from X."""
+    gd, g = mini
+    cfg = CONFIGS["mini"]
+    dims = [gd.d, cfg["hidden"], cfg["hidden"], gd.C]
+    L = len(cfg["fanouts"])
+    kname = "sage" if kind == gnnv.KIND_SAGE else "gcn"
+    w = init_weights(dims, kind=kname)
+    perm = epoch_seeds(gd.n, 0)
+    out = {}
+    for name in ("prefetch", "step"):
+        option("GNNV_NO_PF_AGG", 1 if name == "step" else 0)
+        tr = gnnv.Trainer(g, gnnv.Cache(g, ratio), dims, cfg["fanouts"], cfg["batch"], w, kind=kind,
+                          prec=gnnv.PREC_FP32)
+        res = []
+        B = cfg["batch"]
+        tr.prefetch(perm[:B], B, 60)
+        for t in range(3):
+            tr.step(perm[t * B:(t + 1) * B], B, B, 60 + t, 0.05, want_loss=False)
+            if t < 2:
+                tr.prefetch(perm[(t + 1) * B:(t + 2) * B], B, 61 + t)
+            hb = blocks_to_host(tr.blocks)
+            pa, sa = tr.aggregate(1)
+            r = [tr.read_loss(), read_f32(pa, hb[L - 1][0], sa).tobytes()]
+            for lvl in range(1, L + 1):
+                p_, s_ = tr.activation(lvl)
+                r.append(read_f32(p_, hb[L - lvl][0], s_).tobytes())
+            res.append(r)
+        out[name] = res
+        tr.free()
+    assert out["prefetch"] == out["step"]
+
+
 @pytest.mark.parametrize("prec", [gnnv.PREC_FP32, gnnv.PREC_TF32])
 @pytest.mark.parametrize("ratio", [0.3, 1.0])
 def test_lastuse_l2_hints_bitwise_neutral(mini, option, prec, ratio):
