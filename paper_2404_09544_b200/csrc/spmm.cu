@@ -212,12 +212,35 @@ __global__ void __launch_bounds__(256) k_spmm_bwd(const int32_t* __restrict__ in
       for (int e0 = 0; e0 < cnt; e0 += LPR) {
         const int my = (e0 + sl < cnt) ? __ldg(indices + beg + e0 + sl) : 0;
         const int m = min(LPR, cnt - e0);
-        for (int j = 0; j < m; ++j) {
-          const int u = __shfl_sync(smask, my, j, LPR);
-          if (cok && ((todo >> (e0 + j)) & 1u)) {
-            const float4 gm = c < vec ? masked(g, u, c) : g;
-            if (phase == 1) dH4[(int64_t)u * ldh4 + c] = gm;
-            else atomicAdd(dH4 + (int64_t)u * ldh4 + c, gm);
+        // this phase's edges of the chunk, four at a time: their src ids and
+        // ReLU-bit words are all requested before any row is written, so
+        // the dependent bit loads overlap (uniform within the row's lanes)
+        uint32_t pend = (todo >> e0) & (m >= 32 ? 0xffffffffu : ((1u << m) - 1u));
+        while (pend) {
+          int u[4];
+          uint32_t wb[4];
+          int k = 0;
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int j = pend ? __ffs(pend) - 1 : 0;
+            u[q] = __shfl_sync(smask, my, j, LPR);
+            if (pend) {
+              pend &= pend - 1;
+              k = q + 1;
+            }
+          }
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            wb[q] = (bits && q < k && cok && c < vec) ? __ldg(bits + (int64_t)u[q] * bits_ld + (c >> 3)) >> ((c & 7) * 4)
+                                                       : 0xFu;
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            if (q < k && cok) {
+              const float4 gm = make_float4(wb[q] & 1u ? g.x : 0.f, wb[q] & 2u ? g.y : 0.f, wb[q] & 4u ? g.z : 0.f,
+                                            wb[q] & 8u ? g.w : 0.f);
+              if (phase == 1) dH4[(int64_t)u[q] * ldh4 + c] = gm;
+              else atomicAdd(dH4 + (int64_t)u[q] * ldh4 + c, gm);
+            }
           }
         }
       }

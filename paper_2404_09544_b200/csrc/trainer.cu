@@ -71,8 +71,10 @@ struct gnnv_trainer {
   // Layer 1's aggregation depends on the sampled block and the features
   // only (no weight), so the Eq.4 prefetch also computes it for the batch it
   // prepares (on the side stream, into that buffer set's A^1), and a step
-  // consuming a prefetch starts at the layer-1 GEMM.  GNNV_NO_PF_AGG=1: in the
-  // step.  A^1 per buffer set: A1b[k] (t->A[1] follows the current set).
+  // consuming a prefetch starts at the layer-1 GEMM.  Opt-in (GNNV_PF_AGG=1):
+  // measured neutral on products (1.325-1.329 vs 1.327-1.330 ms; the step
+  // then waits ~0.2 ms for the longer prefetch).  A^1 per
+  // buffer set: A1b[k] (t->A[1] follows the current set).
   bool pf_agg = false;
   float* A1b[2] = {nullptr, nullptr};
   float* tail_dA = nullptr;    // [max_n[0] x dims[L-1]]
@@ -244,7 +246,7 @@ gnnv_status gnnv_trainer_create(gnnv_graph* g, gnnv_cache* c, const gnnv_model_d
       const int64_t xrows = t->x_rows ? 1 : t->x_fused ? b->max_n[L - 1] : b->max_n[L];
       t->H[0] = (float*)dmalloc((size_t)xrows * g->stride * sizeof(float), "X (gathered features)");
       if (t->x_fused) t->rowidx[0] = (int32_t*)dmalloc(b->max_n[L] * sizeof(int32_t), "cache rows of F_L");
-      t->pf_agg = !env_on("GNNV_NO_PF_AGG");
+      t->pf_agg = env_on("GNNV_PF_AGG");
       for (int i = 1; i <= L; ++i) {
         t->Hs[i] = row_stride(md->dims[i]);
         const int64_t rows = b->max_n[L - i];

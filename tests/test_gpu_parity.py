@@ -788,9 +788,10 @@ def test_dynamic_tile_scheduler_bitwise_neutral(mini, option):
 def test_prefetched_layer1_aggregation_bitwise(mini, option, kind, ratio):
     """The Eq.4 prefetch also runs layer 1's aggregation (it needs no
     weight) for the batch it prepares, and the consuming step starts at the
-    layer-1 GEMM (GNNV_NO_PF_AGG keeps it in the step): the same kernel on
-    the same inputs, so three pipelined steps (weights updated in between)
-    give bitwise the same losses, aggregates and activations; ratio 1.0
+    layer-1 GEMM (opt-in GNNV_PF_AGG; the default keeps it in the step): the same kernel on
+    the same inputs, so three pipelined steps give bitwise the same losses,
+    aggregates and activations (lr 0: the backward's atomic summation order
+    would otherwise make the next weights differ at rounding level); ratio 1.0
     aggregates from the cache table, 0.3 from X."""
     gd, g = mini
     cfg = CONFIGS["mini"]
@@ -801,14 +802,14 @@ def test_prefetched_layer1_aggregation_bitwise(mini, option, kind, ratio):
     perm = epoch_seeds(gd.n, 0)
     out = {}
     for name in ("prefetch", "step"):
-        option("GNNV_NO_PF_AGG", 1 if name == "step" else 0)
+        option("GNNV_PF_AGG", 1 if name == "prefetch" else 0)
         tr = gnnv.Trainer(g, gnnv.Cache(g, ratio), dims, cfg["fanouts"], cfg["batch"], w, kind=kind,
                           prec=gnnv.PREC_FP32)
         res = []
         B = cfg["batch"]
         tr.prefetch(perm[:B], B, 60)
         for t in range(3):
-            tr.step(perm[t * B:(t + 1) * B], B, B, 60 + t, 0.05, want_loss=False)
+            tr.step(perm[t * B:(t + 1) * B], B, B, 60 + t, 0.0, want_loss=False)
             if t < 2:
                 tr.prefetch(perm[(t + 1) * B:(t + 2) * B], B, 61 + t)
             hb = blocks_to_host(tr.blocks)
