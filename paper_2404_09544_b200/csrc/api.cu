@@ -431,6 +431,16 @@ void blocks_enable_csc(gnnv_blocks* b, int h) {
   b->csc_mask |= 1u << h;
   GNNV_TRY_CUDA(cudaDeviceSynchronize());
 }
+void blocks_enable_owner_rows(gnnv_blocks* b, int h) {
+  GNNV_REQUIRE(h >= 0 && h < b->L, GNNV_ERR_PARAM, "blocks_enable_owner_rows: hop");
+  GNNV_REQUIRE(!((b->csc_mask >> h) & 1u) || ((b->csc_nonowner >> h) & 1u), GNNV_ERR_STATE,
+               "blocks_enable_owner_rows: hop already has a full CSC");
+  if (!b->d_owner_row[h])
+    b->d_owner_row[h] = (int32_t*)dmalloc(b->max_n[h + 1] * sizeof(int32_t), "owner rows");
+  b->csc_nonowner |= 1u << h;
+  blocks_enable_csc(b, h);
+}
+
 void blocks_enable_lastuse(gnnv_blocks* b) {
   if (b->d_lastv) return;
   b->d_lastv = (uint32_t*)dmalloc(b->max_n[b->L] * sizeof(uint32_t), "last-use slots");
@@ -525,6 +535,7 @@ gnnv_status gnnv_blocks_free(gnnv_blocks* b) {
   dfree(b->d_csc_cnt);
   dfree(b->d_csc_tmp);
   dfree(b->d_lastv);
+  for (int h = 0; h < GNNV_MAX_LAYERS; ++h) dfree(b->d_owner_row[h]);
   dfree(b->d_sizes);
   dfree(b->d_scan);
   dfree(b->scratch);

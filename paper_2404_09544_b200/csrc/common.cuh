@@ -205,6 +205,11 @@ struct gnnv_blocks {
   // loads a row for the last time with an L2 evict_first hint
   // (blocks_enable_lastuse; NULL: off)
   uint32_t* d_lastv = nullptr;
+  // fused L2 push (blocks_enable_owner_rows): the hop's owner row of every
+  // src id (the dst row whose edge discovered it; -1 for the dst prefix), and
+  // its CSC holding the non-owner edges only (bit h of csc_nonowner)
+  int32_t* d_owner_row[GNNV_MAX_LAYERS] = {nullptr};
+  uint32_t csc_nonowner = 0;
   void* d_csc_tmp = nullptr;       // cub scan temporary storage
   size_t csc_tmp_bytes = 0;
   bool sampled = false;
@@ -258,6 +263,7 @@ size_t csc_scan_tmp_bytes(int64_t max_items);
 // gnnv_sample on b (setup path: allocates; synchronises the device)
 void blocks_enable_csc(gnnv_blocks* b, int h);
 void blocks_enable_lastuse(gnnv_blocks* b);
+void blocks_enable_owner_rows(gnnv_blocks* b, int h);  // + CSC of hop h's non-owner edges
 // cache.cu
 void launch_cache_update(gnnv_cache* c, const gnnv_blocks* b, const float* d_X, cudaStream_t s);
 void launch_gather(const gnnv_cache* c, const gnnv_blocks* b, float* d_X, int64_t* d_stats, cudaStream_t s,
@@ -312,6 +318,10 @@ struct GemmFwdArgs {
   int32_t push_ld = 0;
   bool push_mean = true;
   const int32_t* keep_rows = nullptr;
+  // owner row of each output row (-1: none; NULL: the CSC holds every edge):
+  // the owner edges are then reduced as runs of consecutive rows and the CSC
+  // holds only the other edges
+  const int32_t* push_owner = nullptr;
 };
 void gemm_fwd(const GemmFwdArgs& a, int prec, cudaStream_t s);
 // The trainer's fused L2 push (GemmFwdArgs::push_*): layer i's GEMM
@@ -323,6 +333,7 @@ struct FwdPush {
   int32_t ld;
   bool mean;
   const int32_t* keep_rows;
+  const int32_t* owner;
 };
 void launch_zero_rows(float* p, const int32_t* d_rows, int64_t max_rows, int32_t ld, cudaStream_t s);
 // Layer 1 of the trainer with the whole feature table on the device: H_dst

@@ -257,6 +257,7 @@ struct Params {
   float* push_out;
   int push_ld, push_mean;
   const int32_t* keep_rows;
+  const int32_t* push_owner;  // owner row of each output row (-1: none); its edge is not in the CSC
   // fwd/dX (not PAIR): dynamic tile scheduler -- [0] next tile counter,
   // [1] finished CTAs (the last one resets both); NULL: static round robin
   unsigned int* sched;
@@ -589,6 +590,22 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_tma_gemm(const __grid_constant_
           }
           store_rows = row0 < *p.keep_rows;
         }
+        // owner edges: row u's owner dst row (consecutive rows share it -- the
+        // ids a dst row discovered are numbered consecutively by the relabel
+        // scan), reduced as runs below; po_w = its mean weight
+        int po = -1;
+        float po_w = 0.f;
+        if (push && p.push_owner) {
+          const int u = row0 + lane;
+          po = u < M ? __ldg(p.push_owner + u) : -1;
+          if (po >= 0) {
+            po_w = 1.f;
+            if (p.push_mean) {
+              const int cv = __ldg(p.push_indptr + po + 1) - __ldg(p.push_indptr + po);
+              po_w = cv ? 1.f / (float)cv : 0.f;
+            }
+          }
+        }
         for (int c = half * 32; c < BN; c += 64) {
           float v[32];
           if (BN - c >= 32) tmem_ld32(tbase + c, v);
@@ -662,6 +679,39 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_tma_gemm(const __grid_constant_
               tma_store_2d(&p.ty2, ob, j0 - p.ld1, row0);
             }
             asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+          }
+          if (push && p.push_owner) {
+            // owner edges as runs: lane j sums column c + j over the rows of
+            // each run of equal owner rows (conflict-free LDS: one 128-byte
+            // swizzled row per step) and adds w_v * sum into P[v] -- one
+            // coalesced 128-byte reduction per run instead of one per edge
+            float acc = 0.f;
+            int cur = __shfl_sync(0xffffffffu, po, 0);
+            float wcur = __shfl_sync(0xffffffffu, po_w, 0);
+            const bool col_ok = c + lane < p.push_ld;
+#pragma unroll 4
+            for (int r = 0; r < 32; ++r) {
+              const int v = __shfl_sync(0xffffffffu, po, r);
+              const float wv = __shfl_sync(0xffffffffu, po_w, r);
+              if (v != cur) {  // warp-uniform
+                if (cur >= 0 && col_ok)
+                  asm volatile("red.global.add.f32 [%0], %1;" ::"l"(p.push_out + (int64_t)cur * p.push_ld + c + lane),
+                               "f"(acc * wcur)
+                               : "memory");
+                acc = 0.f;
+                cur = v;
+                wcur = wv;
+              }
+              float x;
+              asm volatile("ld.shared.f32 %0, [%1];"
+                           : "=f"(x)
+                           : "r"(ob_u32 + r * 128 + ((((lane >> 2) ^ (r & 7))) << 4) + (lane & 3) * 4));
+              acc += x;
+            }
+            if (cur >= 0 && col_ok)
+              asm volatile("red.global.add.f32 [%0], %1;" ::"l"(p.push_out + (int64_t)cur * p.push_ld + c + lane),
+                           "f"(acc * wcur)
+                           : "memory");
           }
           if (push) {
             // P[v][c .. c+32) += w_v * Y[u][c .. c+32) for every in-edge
@@ -1155,6 +1205,7 @@ bool gemm_fwd_tma(const GemmFwdArgs& a, cudaStream_t s) {
   p.push_ld = a.push_ld;
   p.push_mean = a.push_mean ? 1 : 0;
   p.keep_rows = a.keep_rows;
+  p.push_owner = a.push_owner;
   GNNV_REQUIRE(!a.push_out || (a.push_colptr && a.push_dst && a.push_indptr && a.keep_rows && a.push_ld % 4 == 0 &&
                                a.push_ld >= a.N),
                GNNV_ERR_PARAM, "fwd: incomplete fused-push arguments");

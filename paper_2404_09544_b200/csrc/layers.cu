@@ -310,6 +310,7 @@ void layer_fwd_impl(gnnv_blocks* b, int32_t layer, const gnnv_layer_desc* ld, co
     g.push_ld = push->ld;
     g.push_mean = push->mean;
     g.keep_rows = push->keep_rows;
+    g.push_owner = push->owner;
   }
   if (tl) tl->mark(s, "gemm_fwd" + sfx);
   gemm_fwd(g, ld->prec, s);

@@ -116,21 +116,25 @@ __device__ __forceinline__ void map_slots(int64_t t0, int64_t stride, int hp, in
                                           const int32_t* __restrict__ ellp, const int32_t* __restrict__ cntp,
                                           const int32_t* __restrict__ indptrp, const int32_t* tag,
                                           int32_t* __restrict__ indicesp, int32_t* __restrict__ csc_cnt = nullptr,
-                                          uint32_t* __restrict__ lastv = nullptr) {
+                                          uint32_t* __restrict__ lastv = nullptr,
+                                          const uint32_t* __restrict__ csc_skip_own = nullptr) {
   const int64_t nslots = (int64_t)sizes[hp] * kp;
   for (int64_t e0 = 4 * t0; e0 < nslots; e0 += 4 * stride) {
     int u[4], t[4], dst[4];
+    bool owner[4];
     load4(ellp, e0, nslots, u);
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       const int64_t e = e0 + j;
       dst[j] = -1;
       t[j] = 0;
+      owner[j] = false;
       if (e < nslots) {
         const int r = (int)(e / kp), i = (int)(e - (int64_t)r * kp);
         if (i < __ldg(cntp + r)) {
           dst[j] = __ldg(indptrp + r) + i;
           t[j] = tag[u[j]];
+          if (csc_skip_own) owner[j] = (__ldg(csc_skip_own + r) >> i) & 1u;
         }
       }
     }
@@ -138,7 +142,7 @@ __device__ __forceinline__ void map_slots(int64_t t0, int64_t stride, int hp, in
     for (int j = 0; j < 4; ++j)
       if (dst[j] >= 0) {
         indicesp[dst[j]] = t[j];
-        if (csc_cnt) atomicAdd(csc_cnt + t[j], 1);
+        if (csc_cnt && !owner[j]) atomicAdd(csc_cnt + t[j], 1);
         if (lastv) atomicMax(lastv + t[j], (uint32_t)dst[j] + 1u);  // the src id's last visit (CSR order)
       }
   }
@@ -445,7 +449,8 @@ __global__ void __launch_bounds__(kScanTile) k_relabel_scan(int64_t N, int h, in
                                                             int32_t* __restrict__ F, int32_t* __restrict__ indptr,
                                                             uint32_t* __restrict__ own, int32_t* sizes,
                                                             unsigned long long* status,
-                                                            uint32_t* __restrict__ lastv) {
+                                                            uint32_t* __restrict__ lastv,
+                                                            int32_t* __restrict__ owner_row) {
   GNNV_PDL_ENTRY();
   __shared__ int s_tile;
   __shared__ uint32_t s_wa[kScanTile / 32], s_wb[kScanTile / 32];
@@ -550,7 +555,8 @@ __global__ void __launch_bounds__(kScanTile) k_relabel_scan(int64_t N, int h, in
   const uint32_t new_off = s_pa + excl_a, edge_off = s_pb + excl_b;
   if (r < n) {
     indptr[r] = (int32_t)edge_off;
-    if (lastv) lastv[r] = 0u;  // last-use slots of this hop's src ids, set by k_map
+    if (lastv) lastv[r] = 0u;        // last-use slots of this hop's src ids, set by k_map
+    if (owner_row) owner_row[r] = -1;  // the dst prefix has no owner edge in this hop
   }
   __shared__ uint32_t s_off[kScanTile];
   s_off[threadIdx.x] = new_off;
@@ -568,6 +574,7 @@ __global__ void __launch_bounds__(kScanTile) k_relabel_scan(int64_t N, int h, in
         tag[u] = nid;
         F[nid] = u;
         if (lastv) lastv[nid] = 0u;
+        if (owner_row) owner_row[nid] = r0 + rl;  // the dst row whose edge discovered u
       }
     }
   }
@@ -588,26 +595,31 @@ __global__ void __launch_bounds__(kScanTile) k_relabel_scan(int64_t N, int h, in
 __global__ void k_map(int hp, int kp, const int32_t* sizes, const int32_t* __restrict__ ellp,
                       const int32_t* __restrict__ cntp, const int32_t* __restrict__ indptrp, const int32_t* tag,
                       int32_t* __restrict__ indicesp, unsigned long long* scan, int64_t scan_words,
-                      int32_t* __restrict__ csc_cnt, uint32_t* __restrict__ lastv) {
+                      int32_t* __restrict__ csc_cnt, uint32_t* __restrict__ lastv,
+                      const uint32_t* __restrict__ csc_skip_own) {
   GNNV_PDL_ENTRY();
   const int64_t t0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x, stride = (int64_t)gridDim.x * blockDim.x;
   const int64_t used = std::min<int64_t>(scan_words, 1 + ((int64_t)sizes[hp] + kScanTile - 1) / kScanTile);
   for (int64_t i = t0; i < used; i += stride) scan[i] = 0ull;
-  map_slots(t0, stride, hp, kp, sizes, ellp, cntp, indptrp, tag, indicesp, csc_cnt, lastv);
+  map_slots(t0, stride, hp, kp, sizes, ellp, cntp, indptrp, tag, indicesp, csc_cnt, lastv, csc_skip_own);
 }
 
 // CSC fill of hop hp (counting sort): colptr = exclusive scan of the in-edge
 // counts; edge (r, u) takes slot colptr[u] + (--cnt[u]), which also leaves
 // the counts zeroed for the next batch.  The order of a column's entries
 // follows the atomics; the pulled sum is exact up to that order.
+// csc_skip_own != NULL: the owner edges (bit i of own[r]) are left out --
+// the fused L2 push handles them as runs (owner rows).
 __global__ void k_csc_fill(int hp, int kp, const int32_t* sizes, const int32_t* __restrict__ indptrp,
                            const int32_t* __restrict__ indicesp, int32_t* __restrict__ csc_cnt,
-                           const int32_t* __restrict__ colptr, int32_t* __restrict__ csc) {
+                           const int32_t* __restrict__ colptr, int32_t* __restrict__ csc,
+                           const uint32_t* __restrict__ csc_skip_own) {
   GNNV_PDL_ENTRY();
   const int64_t nslots = (int64_t)sizes[hp] * kp;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < nslots; e += (int64_t)gridDim.x * blockDim.x) {
     const int r = (int)(e / kp), i = (int)(e - (int64_t)r * kp);
     const int beg = __ldg(indptrp + r);
+    if (csc_skip_own && ((__ldg(csc_skip_own + r) >> i) & 1u)) continue;
     if (i < __ldg(indptrp + r + 1) - beg) {
       const int u = __ldg(indicesp + beg + i);
       csc[__ldg(colptr + u) + atomicSub(csc_cnt + u, 1) - 1] = r;
@@ -649,7 +661,8 @@ void launch_sample(gnnv_graph* g, gnnv_blocks* b, const int32_t* d_seeds, int32_
     const bool csc = (b->csc_mask >> hp) & 1u;
     launch_k(k_map, grid_for(slots_ub, 1024), 256, 0, s, hp, b->fanouts[hp], b->d_sizes, b->d_ell, b->d_cnt,
              b->d_indptr[hp], b->d_tag, b->d_indices[hp], b->d_scan, b->scan_words,
-             csc ? b->d_csc_cnt : (int32_t*)nullptr, hp == L - 1 ? b->d_lastv : (uint32_t*)nullptr);
+             csc ? b->d_csc_cnt : (int32_t*)nullptr, hp == L - 1 ? b->d_lastv : (uint32_t*)nullptr,
+             csc && ((b->csc_nonowner >> hp) & 1u) ? b->d_own[hp] : (const uint32_t*)nullptr);
     GNNV_CHECK_LAUNCH();
     if (!csc) return;
     size_t tmp = b->csc_tmp_bytes;
@@ -657,7 +670,8 @@ void launch_sample(gnnv_graph* g, gnnv_blocks* b, const int32_t* d_seeds, int32_
                                                 (int)(b->max_n[hp + 1] + 1), s));
     GNNV_CHECK_LAUNCH();
     launch_k(k_csc_fill, grid_for(slots_ub, 256), 256, 0, s, hp, b->fanouts[hp], b->d_sizes, b->d_indptr[hp],
-             b->d_indices[hp], b->d_csc_cnt, b->d_colptr[hp], b->d_csc[hp]);
+             b->d_indices[hp], b->d_csc_cnt, b->d_colptr[hp], b->d_csc[hp],
+             ((b->csc_nonowner >> hp) & 1u) ? b->d_own[hp] : (const uint32_t*)nullptr);
     GNNV_CHECK_LAUNCH();
   };
   for (int h = 0; h < L; ++h) {
@@ -693,7 +707,7 @@ void launch_sample(gnnv_graph* g, gnnv_blocks* b, const int32_t* d_seeds, int32_
     GNNV_CHECK_LAUNCH();
     launch_k(k_relabel_scan, tiles_ub, kScanTile, 0, s, g->n, h, k, L, b->d_ell, b->d_cnt, b->d_tag, b->d_F,
                                                   b->d_indptr[h], b->d_own[h], b->d_sizes, b->d_scan,
-             h == L - 1 ? b->d_lastv : (uint32_t*)nullptr);
+             h == L - 1 ? b->d_lastv : (uint32_t*)nullptr, b->d_owner_row[h]);
     GNNV_CHECK_LAUNCH();
   }
   map_hop(L - 1);

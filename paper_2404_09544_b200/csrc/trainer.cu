@@ -264,7 +264,7 @@ gnnv_status gnnv_trainer_create(gnnv_graph* g, gnnv_cache* c, const gnnv_model_d
                 tail_supported(md->kind, md->dims[L - 1], md->dims[L], md->fanouts[0]) && !env_on("GNNV_NO_TAIL");
       t->l2push = md->prec == GNNV_PREC_TF32 && md->kind == GNNV_KIND_SAGE && L >= 3 && env_on("GNNV_L2PUSH");
       if (t->l2push)
-        for (int i = 1; i <= L - 2; ++i) blocks_enable_csc(t->b, L - i - 1);
+        for (int i = 1; i <= L - 2; ++i) blocks_enable_owner_rows(t->b, L - i - 1);
       // dead-row L2 hints for the layer-1 aggregation (spmm.cu HINT; opt-in
       // GNNV_LASTUSE=1: measured 1.11 -> 1.04 GB DRAM reads but 255 -> 262 us
       // on products)
@@ -516,7 +516,7 @@ gnnv_status gnnv_trainer_prefetch(gnnv_trainer* t, const int32_t* seeds, int32_t
       st = gnnv_blocks_set_locality(t->bb[k], t->c, t->loc_bias);
       if (st != GNNV_OK) throw Error{st, get_error()};
       if (t->l2push)
-        for (int i = 1; i <= t->md.L - 2; ++i) blocks_enable_csc(t->bb[k], t->md.L - i - 1);
+        for (int i = 1; i <= t->md.L - 2; ++i) blocks_enable_owner_rows(t->bb[k], t->md.L - i - 1);
       if (t->lastuse) blocks_enable_lastuse(t->bb[k]);
       const int64_t xrows = t->x_rows ? 1 : t->bb[k]->max_n[t->x_fused ? t->md.L - 1 : t->md.L];
       t->X[k] = (float*)dmalloc((size_t)xrows * g->stride * sizeof(float), "X (prefetch)");
@@ -653,7 +653,7 @@ gnnv_status gnnv_step(gnnv_trainer* t, const int32_t* seeds, int32_t n_seeds, in
         if (tl) tl->mark(s, "zero_a.l" + std::to_string(i + 1));
         launch_zero_rows(t->A[i + 1], b->d_sizes + hn, b->max_n[hn], row_stride(t->md.dims[i]), s);
         push = FwdPush{b->d_colptr[hn], b->d_csc[hn], b->d_indptr[hn], t->A[i + 1], row_stride(t->md.dims[i]),
-                       t->md.aggr == GNNV_AGGR_MEAN, b->d_sizes + hn};
+                       t->md.aggr == GNNV_AGGR_MEAN, b->d_sizes + hn, b->d_owner_row[hn]};
       }
       layer_fwd_impl(b, i, &ld, t->H[i - 1], t->d_params + t->w_off[i - 1], t->d_params + t->b_off[i - 1], t->H[i],
                      t->A[i], s, tl, t->mbits[i], t->table, i == 1 ? t->rowidx[t->cur] : nullptr,
