@@ -1,8 +1,9 @@
 """Micro-benchmark of the dense layer products at the products-config shapes.
 
     python tools/bench_gemm.py [M] [d_in] [d_out]
-GNNV_DEBUG_GEMM=1 (no epilogue stores) / 2 (no MMA) isolates the pipeline
-parts of the tf32 TMA kernels.  Prints device time and achieved HBM GB/s.
+Prints device time and achieved HBM GB/s of the tf32 TMA kernels (the
+round-1 switches that disabled the epilogue stores / the MMA were removed
+from the product kernel).
 """
 import os
 import sys
