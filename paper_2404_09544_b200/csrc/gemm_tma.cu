@@ -274,7 +274,7 @@ __device__ __forceinline__ void sched_done(unsigned int* sched) {
     __threadfence();
   }
 }
-__device__ unsigned int g_sched[64][2];  // zero-initialised; a ring of slots, one per launch in flight
+__device__ unsigned int g_sched[4096][2];  // zero-initialised; a ring of slots, one per launch in flight (a slot is reused only 4096 launches later -- beyond any launch queue)
 
 // PAIR (MODE_FWD only): a cluster of 2 CTAs computes 256-row tiles with
 // tcgen05.mma.cta_group::2 (M = 256): each CTA stages its own 128 rows of A
@@ -1147,7 +1147,7 @@ static void launch_pair(const Params& p, int pairs, cudaStream_t s) {
 
 static int rup(int x, int m) { return (x + m - 1) / m * m; }
 
-// a scheduler slot for the next fwd/dX launch (ring of 64; a slot is reset
+// a scheduler slot for the next fwd/dX launch (ring of 4096; a slot is reset
 // by the last CTA of the launch that used it).  GNNV_STATIC_TILES=1: the
 // static round robin instead.
 static unsigned int* next_sched() {
@@ -1159,7 +1159,7 @@ static unsigned int* next_sched() {
     GNNV_TRY_CUDA(cudaGetSymbolAddress(&p, g_sched));
     base = static_cast<unsigned int*>(p);
   }
-  return base + 2 * (slot++ % 64);
+  return base + 2 * (slot++ % 4096);
 }
 
 }  // namespace tma

@@ -1013,15 +1013,38 @@ def test_backward_pull_matches_push(mini, option, kind, prec):
             assert normwise(gW, rW) < 1e-4 and normwise(gb, rb) < 1e-4
 
 
-@pytest.mark.skipif(os.environ.get("GNNV_GUARD_ALLOC") != "1", reason="guarded allocations off (GNNV_GUARD_ALLOC=1)")
-def test_guard_alloc_detects_out_of_bounds_write(mini):
+_GUARD_CHILD = r"""
+import ctypes, os, sys
+sys.path.insert(0, os.path.join(os.environ["GNNV_ROOT"], "tests"))
+sys.path.insert(0, os.environ["GNNV_ROOT"])
+import test_gpu_parity as t
+t.lib()
+from synth import make_graph
+from paper_2404_09544_b200 import gnnv
+gd = make_graph("mini")
+t._guard_negative_control(gd, gnnv.Graph.from_data(gd))
+print("GUARD_CHILD_OK")
+"""
+
+
+def test_guard_alloc_detects_out_of_bounds_write():
     """Negative control of the guarded-allocation check that stands in for
-    compute-sanitizer (closed on this pool): a kernel writing 12 floats past
-    the end of a library allocation (gnnv_sgd over a range that ends beyond
-    the trainer's H^1 buffer) is reported; the guard is then restored."""
+    compute-sanitizer (closed on this pool), in a child process with
+    GNNV_GUARD_ALLOC=1: a kernel writing 12 floats past the end of a library
+    allocation (gnnv_sgd over a range that ends beyond the trainer's H^1
+    buffer) is reported; the guard is then restored."""
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, GNNV_GUARD_ALLOC="1", GNNV_ROOT=root)
+    r = subprocess.run([sys.executable, "-c", _GUARD_CHILD], env=env, capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0 and "GUARD_CHILD_OK" in r.stdout, r.stdout[-2000:] + r.stderr[-4000:]
+
+
+def _guard_negative_control(gd, g):
     import ctypes
 
-    gd, g = mini
     cfg = CONFIGS["mini"]
     dims = [gd.d, cfg["hidden"], cfg["hidden"], gd.C]
     L = len(cfg["fanouts"])
