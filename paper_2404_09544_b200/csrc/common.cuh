@@ -274,8 +274,12 @@ void launch_spmm_fwd(const int32_t* d_indptr, const int32_t* d_indices, const in
                      const float* H, int32_t ldh, float* A, int32_t lda, int32_t d, int32_t kind, int32_t aggr,
                      cudaStream_t s, const int32_t* rowidx = nullptr, const uint32_t* lastv = nullptr);
 void launch_spmm_bwd(const int32_t* d_indptr, const int32_t* d_indices, const uint32_t* d_own, const int32_t* d_ndst,
-                     int64_t max_dst, const float* dA, int32_t lda, float* dH, int32_t ldh, int32_t d, int32_t kind,
-                     int32_t aggr, const uint32_t* bits, int32_t bits_ld, cudaStream_t s);
+                     int64_t max_dst, const float* dA, int32_t lda, void* dH, int32_t ldh, int32_t d, int32_t kind,
+                     int32_t aggr, const uint32_t* bits, int32_t bits_ld, cudaStream_t s, bool dh_bf16 = false);
+// the forward aggregation over bf16 source rows (stride ld16 elements)
+void launch_spmm_fwd_h16(const int32_t* d_indptr, const int32_t* d_indices, const int32_t* d_ndst, int64_t max_dst,
+                         const void* H16, int32_t ld16, float* A, int32_t lda, int32_t d, int32_t kind, int32_t aggr,
+                         cudaStream_t s);
 // the same transposed aggregation pulled per src row (rows up to
 // kPullMaxLd floats; wider ones keep the push) through the block's
 // CSC (one coalesced store per dH row, no atomics; see k_spmm_bwd_pull)
@@ -322,6 +326,10 @@ struct GemmFwdArgs {
   // the owner edges are then reduced as runs of consecutive rows and the CSC
   // holds only the other edges
   const int32_t* push_owner = nullptr;
+  // TF32: every output row also stored as bf16 (y16, row stride ld16, a
+  // multiple of 32); the fp32 rows then only below *keep_rows.  NULL: off
+  void* y16 = nullptr;
+  int32_t ld16 = 0;
 };
 void gemm_fwd(const GemmFwdArgs& a, int prec, cudaStream_t s);
 // The trainer's fused L2 push (GemmFwdArgs::push_*): layer i's GEMM
@@ -336,6 +344,21 @@ struct FwdPush {
   const int32_t* owner;
 };
 void launch_zero_rows(float* p, const int32_t* d_rows, int64_t max_rows, int32_t ld, cudaStream_t s);
+// The trainer's bf16 intermediates (GNNV_BF16ACT): a hidden
+// layer's output H^i is also stored as bf16 for the next layer's
+// aggregation (its fp32 rows only for the next layer's dst prefix), and
+// dL/dH^i is produced and consumed as bf16.  Per layer call:
+struct Bf16Io {
+  void* y16 = nullptr;             // fwd: bf16 copy of this layer's output
+  int32_t ld16 = 0;                //      its row stride (elements, % 32 == 0)
+  const int32_t* keep_rows = nullptr;  // fwd: fp32 output rows kept
+  const void* src16 = nullptr;     // fwd: aggregate from this bf16 copy of H_src
+  int32_t src16_ld = 0;
+  void* gsrc16 = nullptr;          // bwd: dH_src produced as bf16 (stride gsrc16_ld)
+  int32_t gsrc16_ld = 0;
+  const void* gdst16 = nullptr;    // bwd: this layer's G read as bf16 (stride gdst16_ld)
+  int32_t gdst16_ld = 0;
+};
 // Layer 1 of the trainer with the whole feature table on the device: H_dst
 // (X's dst prefix) is read by the TF32 GEMMs straight from the table through
 // the gather's row indices, so X is never materialised.
@@ -369,6 +392,7 @@ struct GemmDwArgs {
   const int32_t* x1_rows = nullptr;  // as GemmFwdArgs::x1_rows
   int64_t x1_table_rows = 0;
   bool zeroed = false;  // TF32: dW (and db) already zero (the trainer clears them in-kernel)
+  const void* G16 = nullptr;  // TF32: G as bf16 (row stride ldg elements) instead of G
 };
 void gemm_dw(const GemmDwArgs& a, int prec, cudaStream_t s);
 size_t gemm_dw_partial_floats(int32_t rows_plus_bias, int32_t N, int32_t* splits_out, int64_t max_M);
@@ -383,6 +407,7 @@ struct GemmDxArgs {  // [Y1 | Y2] = G W^T  (Y1 = first K1 cols, Y2 = the rest)
   // TF32 only: Y1 *= ReLU bits of the previous layer (NULL: none)
   const uint32_t* y1_bits = nullptr;
   int32_t y1_bits_ld = 0;
+  void* Y1_16 = nullptr;  // TF32: Y1 stored as bf16 (row stride ld1, ld1 % 32 == 0) instead of Y1
 };
 void gemm_dx(const GemmDxArgs& a, int prec, cudaStream_t s);
 // tail.cu: the trainer's output layer (forward, loss, backward) fused

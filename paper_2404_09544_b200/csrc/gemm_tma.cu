@@ -38,6 +38,8 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <cuda_bf16.h>
+
 #include "common.cuh"
 
 namespace gnnv {
@@ -258,11 +260,24 @@ struct Params {
   int push_ld, push_mean;
   const int32_t* keep_rows;
   const int32_t* push_owner;  // owner row of each output row (-1: none); its edge is not in the CSC
+  // bf16 copies (the trainer's bf16 intermediates):
+  // fwd: every output row also stored as bf16 (y16, stride ld16, a multiple
+  // of 32), the fp32 rows only below *keep_rows; dX: the Y1 part stored as
+  // bf16 (y1_16, stride ld1) instead of fp32; dW: G is bf16 (g16 = 1)
+  __nv_bfloat16* y16;
+  int ld16;
+  __nv_bfloat16* y1_16;
+  int g16;
   // fwd/dX (not PAIR): dynamic tile scheduler -- [0] next tile counter,
   // [1] finished CTAs (the last one resets both); NULL: static round robin
   unsigned int* sched;
 };
 
+
+__device__ __forceinline__ uint32_t bf16x2(float a, float b) {
+  const __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+  return *reinterpret_cast<const uint32_t*>(&h);
+}
 
 // The last CTA of a launch to finish resets its scheduler slot for the next
 // launch that draws it (all producers' claims precede every CTA's exit).
@@ -306,7 +321,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_tma_gemm(const __grid_constant_
   // dW stage (unswizzled row-major boxes of DW_KR graph rows): MT A tiles of
   // [16 x 128] fp32, then G [16 x BN], then (fused mask) H [16 x BN].
   const int a_bytes = MODE == MODE_DW ? MT * DW_KR * BM * 4 : BM * BKB;
-  const int g_bytes = MODE == MODE_DW ? DW_KR * BN * 4 : (PAIR ? BN / 2 : BN) * BKB;
+  const int g_bytes = MODE == MODE_DW ? DW_KR * BN * (p.g16 ? 2 : 4) : (PAIR ? BN / 2 : BN) * BKB;
   const int b_bytes = MODE == MODE_DW ? g_bytes + (p.mask ? DW_KR * p.nwp * 4 : 0) : g_bytes;
   const int stage_bytes = a_bytes + b_bytes;
   // dW: two K-major SW64 tiles (64B rows = 16 tf32 of K) built by the transposers;
@@ -550,7 +565,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_tma_gemm(const __grid_constant_
         int pe_beg = 0, pe_cnt = 0, pe_excl = 0, pe_incl = 0, pe_total = 0;
         int pv[4] = {0, 0, 0, 0};
         float pw[4] = {0.f, 0.f, 0.f, 0.f};
-        bool store_rows = true;
+        bool store_rows = !(MODE == MODE_FWD && p.keep_rows) || row0 < *p.keep_rows;
         if (push) {
           const int u = row0 + lane;
           if (u < M) {
@@ -588,7 +603,6 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_tma_gemm(const __grid_constant_
               pw[k] = w;
             }
           }
-          store_rows = row0 < *p.keep_rows;
         }
         // owner edges: row u's owner dst row (consecutive rows share it -- the
         // ids a dst row discovered are numbered consecutively by the relabel
@@ -634,6 +648,27 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_tma_gemm(const __grid_constant_
 #pragma unroll
             for (int j = 0; j < 32; ++j)
               if (j0 + j < p.ld1 && !((wv >> j) & 1u)) v[j] = 0.f;
+          }
+          if (MODE == MODE_FWD && p.y16 && c < p.ld16) {  // bf16 copy of the row piece (64 bytes)
+            const int64_t m = (int64_t)row0 + lane;
+            if (m < M) {
+              uint4* dst = reinterpret_cast<uint4*>(p.y16 + m * p.ld16 + c);
+#pragma unroll
+              for (int q = 0; q < 4; ++q)
+                dst[q] = make_uint4(bf16x2(v[8 * q], v[8 * q + 1]), bf16x2(v[8 * q + 2], v[8 * q + 3]),
+                                    bf16x2(v[8 * q + 4], v[8 * q + 5]), bf16x2(v[8 * q + 6], v[8 * q + 7]));
+            }
+          }
+          if (MODE == MODE_DX && p.y1_16 && j0 < p.ld1) {  // Y1 as bf16 (j0 + 32 <= ld1: checked on the host)
+            const int64_t m = (int64_t)row0 + lane;
+            if (m < M) {
+              uint4* dst = reinterpret_cast<uint4*>(p.y1_16 + m * p.ld1 + j0);
+#pragma unroll
+              for (int q = 0; q < 4; ++q)
+                dst[q] = make_uint4(bf16x2(v[8 * q], v[8 * q + 1]), bf16x2(v[8 * q + 2], v[8 * q + 3]),
+                                    bf16x2(v[8 * q + 4], v[8 * q + 5]), bf16x2(v[8 * q + 6], v[8 * q + 7]));
+            }
+            continue;
           }
           const bool ragged = row0 + 32 > M || (MODE == MODE_DX && j0 < p.ld1 && j0 + 32 > p.ld1);
           if (ragged && store_rows) {
@@ -883,11 +918,23 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_tma_gemm(const __grid_constant_
             ld = BN;
           }
           float4 x[4];
+          if (!is_a && p.g16) {  // bf16 G: four elements (8 bytes) per staged row, widened to fp32
+            const uint2* src16 = reinterpret_cast<const uint2*>(
+                reinterpret_cast<const __nv_bfloat16*>(st + a_bytes) + (gx - MT * 4) * 32 + 4 * cq);
 #pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            const int r = 4 * rq + j;
-            x[j] = (loaded && r < valid) ? *reinterpret_cast<const float4*>(src + r * ld)
-                                         : make_float4(0.f, 0.f, 0.f, 0.f);
+            for (int j = 0; j < 4; ++j) {
+              const int r = 4 * rq + j;
+              const uint2 q = (r < valid) ? src16[r * (BN / 4)] : make_uint2(0u, 0u);
+              x[j] = make_float4(__uint_as_float(q.x << 16), __uint_as_float(q.x & 0xFFFF0000u),
+                                 __uint_as_float(q.y << 16), __uint_as_float(q.y & 0xFFFF0000u));
+            }
+          } else {
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              const int r = 4 * rq + j;
+              x[j] = (loaded && r < valid) ? *reinterpret_cast<const float4*>(src + r * ld)
+                                           : make_float4(0.f, 0.f, 0.f, 0.f);
+            }
           }
           if (!is_a && p.mask) {
             const uint32_t* wb = reinterpret_cast<const uint32_t*>(st + a_bytes + g_bytes) + (gx - MT * 4);
@@ -1062,6 +1109,20 @@ static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 
 // 2-D fp32 row-major tensor [rows x cols] with row stride ld (floats); box
 // [box_rows x 32 cols], 128B swizzle, out-of-range elements read as zero.
+// bf16 2-D map, no swizzle (the dW's G operand when it is a bf16 copy)
+static CUtensorMap make_map16(const void* base, int64_t rows, int64_t cols, int64_t ld, int box_rows, int box_cols) {
+  CUtensorMap m;
+  const cuuint64_t dims[2] = {(cuuint64_t)std::max<int64_t>(cols, 1), (cuuint64_t)std::max<int64_t>(rows, 1)};
+  const cuuint64_t strides[1] = {(cuuint64_t)ld * 2};
+  const cuuint32_t box[2] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows};
+  const cuuint32_t estr[2] = {1, 1};
+  CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  GNNV_REQUIRE(r == CUDA_SUCCESS, GNNV_ERR_CUDA, "cuTensorMapEncodeTiled (bf16) failed (alignment/stride)");
+  return m;
+}
+
 static CUtensorMap make_map(const float* base, int64_t rows, int64_t cols, int64_t ld, int box_rows,
                             int box_cols = 32, bool swizzle = true) {
   CUtensorMap m;
@@ -1094,10 +1155,10 @@ struct Arena {
 };
 static Arena g_img;
 
-static size_t smem_bytes(int mode, int BN, int mask, int nwp, bool pair = false) {
+static size_t smem_bytes(int mode, int BN, int mask, int nwp, bool pair = false, int g16 = 0) {
   const int S = mode == MODE_DW ? DW_STAGES : pair ? PAIR_STAGES : FWD_STAGES;
   const int a = mode == MODE_DW ? DW_MT * DW_KR * BM * 4 : BM * BKB;
-  const int b = mode == MODE_DW ? DW_KR * BN * 4 + (mask ? DW_KR * nwp * 4 : 0) : (pair ? BN / 2 : BN) * BKB;
+  const int b = mode == MODE_DW ? DW_KR * BN * (g16 ? 2 : 4) + (mask ? DW_KR * nwp * 4 : 0) : (pair ? BN / 2 : BN) * BKB;
   const int k = mode == MODE_DW ? 2 * (DW_MT * BM + BN) * 64 : NE * 4096 * (pair ? PAIR_OB : 1);
   return (((size_t)S * (a + b) + 1023) & ~(size_t)1023) + k + 8 * (2 * S + 8 + 8) + 32 + 16 + 1024;
 }
@@ -1105,7 +1166,7 @@ static size_t smem_bytes(int mode, int BN, int mask, int nwp, bool pair = false)
 template <int MODE>
 static void launch(const Params& p, dim3 grid, cudaStream_t s) {
   static size_t attr = 0;  // dynamic smem opt-in, raised to the largest request seen
-  const size_t bytes = smem_bytes(MODE, p.BN, p.mask, p.nwp);
+  const size_t bytes = smem_bytes(MODE, p.BN, p.mask, p.nwp, false, p.g16);
   if (bytes > attr) {
     GNNV_TRY_CUDA(cudaFuncSetAttribute(k_tma_gemm<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
     attr = bytes;
@@ -1206,6 +1267,10 @@ bool gemm_fwd_tma(const GemmFwdArgs& a, cudaStream_t s) {
   p.push_mean = a.push_mean ? 1 : 0;
   p.keep_rows = a.keep_rows;
   p.push_owner = a.push_owner;
+  p.y16 = static_cast<__nv_bfloat16*>(a.y16);
+  p.ld16 = a.ld16;
+  GNNV_REQUIRE(!a.y16 || (a.ld16 % 32 == 0 && a.ld16 >= a.N && a.keep_rows), GNNV_ERR_PARAM,
+               "fwd: bf16 copy needs a row stride that is a multiple of 32 and the kept-row count");
   GNNV_REQUIRE(!a.push_out || (a.push_colptr && a.push_dst && a.push_indptr && a.keep_rows && a.push_ld % 4 == 0 &&
                                a.push_ld >= a.N),
                GNNV_ERR_PARAM, "fwd: incomplete fused-push arguments");
@@ -1244,8 +1309,15 @@ bool gemm_dx_tma(const GemmDxArgs& a, cudaStream_t s) {
   p.Y2 = a.Y2;
   p.ld1 = a.ld1;
   p.ld2 = a.ld2;
-  p.ty1 = make_map(a.Y1, a.max_M, a.ld1, a.ld1, 32);
-  p.ty2 = a.Y2 ? make_map(a.Y2, a.max_M, a.ld2, a.ld2, 32) : p.ty1;
+  p.ty2 = a.Y2 ? make_map(a.Y2, a.max_M, a.ld2, a.ld2, 32) : CUtensorMap{};
+  if (a.Y1_16) {  // Y1 as bf16 rows: plain stores from the epilogue (ty1 unused)
+    GNNV_REQUIRE(a.ld1 % 32 == 0 && a.Y2, GNNV_ERR_PARAM, "dX: a bf16 Y1 needs ld1 % 32 == 0 and Y2");
+    p.y1_16 = static_cast<__nv_bfloat16*>(a.Y1_16);
+    p.ty1 = p.ty2;
+  } else {
+    p.ty1 = make_map(a.Y1, a.max_M, a.ld1, a.ld1, 32);
+    if (!a.Y2) p.ty2 = p.ty1;
+  }
   p.ybits = a.y1_bits;
   p.ybits_ld = a.y1_bits_ld;
   const int64_t tiles = ceil_div(std::max<int64_t>(a.max_M, 1), BM) * ntl;
@@ -1291,7 +1363,13 @@ bool gemm_dw_tma(const GemmDwArgs& a, cudaStream_t s) {
   p.ta1 = a.x1_rows ? make_map(a.X1, a.x1_table_rows, a.K1, a.ld1, 1, BM, false)
                     : make_map(a.X1, a.max_M, a.K1, a.ld1, DW_KR, BM, false);
   p.ta2 = a.X2 ? make_map(a.X2, a.max_M, a.K1, a.ld2, DW_KR, BM, false) : p.ta1;
-  p.tb = make_map(a.G, a.max_M, a.N, a.ldg, DW_KR, BN, false);
+  if (a.G16) {
+    GNNV_REQUIRE(a.ldg % 8 == 0, GNNV_ERR_PARAM, "dW: bf16 G row stride must be a multiple of 8");
+    p.g16 = 1;
+    p.tb = make_map16(a.G16, a.max_M, a.N, a.ldg, DW_KR, BN);
+  } else {
+    p.tb = make_map(a.G, a.max_M, a.N, a.ldg, DW_KR, BN, false);
+  }
   p.two = a.X2 ? 1 : 0;
   p.nkb1 = nkb1;
   p.BN = BN;

@@ -262,7 +262,7 @@ void launch_zero_rows(float* p, const int32_t* d_rows, int64_t max_rows, int32_t
 void layer_fwd_impl(gnnv_blocks* b, int32_t layer, const gnnv_layer_desc* ld, const float* Hsrc, const float* W,
                     const float* bias, float* Hdst, float* A, cudaStream_t s, Timeline* tl, uint32_t* mask_bits,
                     const float* agg_table, const int32_t* rowidx, const XRows* xr, const FwdPush* push,
-                    bool agg_ready) {
+                    bool agg_ready, const Bf16Io* io) {
   const std::string sfx = ".l" + std::to_string(layer);
   const int h = b->L - layer;
   const int32_t* d_ndst = b->d_sizes + h;
@@ -273,8 +273,13 @@ void layer_fwd_impl(gnnv_blocks* b, int32_t layer, const gnnv_layer_desc* ld, co
   // trainer's fused L2 push)
   if (!agg_ready) {
     if (tl) tl->mark(s, "spmm_fwd" + sfx);
-    launch_spmm_fwd(b->d_indptr[h], b->d_indices[h], d_ndst, b->max_n[h], rowidx ? agg_table : Hsrc, ld->in_stride,
-                    A, lda, ld->d_in, ld->kind, ld->aggr, s, rowidx, h == b->L - 1 ? b->d_lastv : nullptr);
+    if (io && io->src16)
+      launch_spmm_fwd_h16(b->d_indptr[h], b->d_indices[h], d_ndst, b->max_n[h], io->src16, io->src16_ld, A, lda,
+                          ld->d_in, ld->kind, ld->aggr, s);
+    else
+      launch_spmm_fwd(b->d_indptr[h], b->d_indices[h], d_ndst, b->max_n[h], rowidx ? agg_table : Hsrc,
+                      ld->in_stride, A, lda, ld->d_in, ld->kind, ld->aggr, s, rowidx,
+                      h == b->L - 1 ? b->d_lastv : nullptr);
   }
   GemmFwdArgs g{};
   if (ld->kind == GNNV_KIND_SAGE) {
@@ -312,6 +317,11 @@ void layer_fwd_impl(gnnv_blocks* b, int32_t layer, const gnnv_layer_desc* ld, co
     g.keep_rows = push->keep_rows;
     g.push_owner = push->owner;
   }
+  if (io && io->y16) {
+    g.y16 = io->y16;
+    g.ld16 = io->ld16;
+    g.keep_rows = io->keep_rows;
+  }
   if (tl) tl->mark(s, "gemm_fwd" + sfx);
   gemm_fwd(g, ld->prec, s);
 }
@@ -319,7 +329,8 @@ void layer_fwd_impl(gnnv_blocks* b, int32_t layer, const gnnv_layer_desc* ld, co
 void layer_bwd_impl(gnnv_blocks* b, int32_t layer, const gnnv_layer_desc* ld, const float* Gdst, const float* Hdst,
                     const float* Hsrc, const float* A, const float* W, float* Gsrc, float* dW, float* db,
                     cudaStream_t s, Timeline* tl, const uint32_t* mask_bits, bool g_masked,
-                    const uint32_t* src_bits, int32_t src_bits_ld, const XRows* xr, bool grads_zeroed) {
+                    const uint32_t* src_bits, int32_t src_bits_ld, const XRows* xr, bool grads_zeroed,
+                    const Bf16Io* io) {
   const std::string sfx = ".l" + std::to_string(layer);
   const int h = b->L - layer;
   const int32_t* d_ndst = b->d_sizes + h;
@@ -384,6 +395,11 @@ void layer_bwd_impl(gnnv_blocks* b, int32_t layer, const gnnv_layer_desc* ld, co
   w.K1 = ld->d_in;
   w.G = G;
   w.ldg = ldo;
+  if (io && io->gdst16) {
+    GNNV_REQUIRE(tf32 && !need_mask, GNNV_ERR_UNSUPPORTED, "layer_bwd: a bf16 G needs TF32 and a pre-masked G");
+    w.G16 = io->gdst16;
+    w.ldg = io->gdst16_ld;
+  }
   w.N = ld->d_out;
   w.d_M = d_ndst;
   w.max_M = max_dst;
@@ -408,7 +424,15 @@ void layer_bwd_impl(gnnv_blocks* b, int32_t layer, const gnnv_layer_desc* ld, co
     x.K1 = ld->d_in;
     x.d_M = d_ndst;
     x.max_M = max_dst;
-    if (sage) {
+    const bool g16 = io && io->gsrc16;
+    if (sage && g16) {  // dH_src (and its dst-prefix rows from the GEMM) as bf16
+      x.Y1_16 = io->gsrc16;
+      x.ld1 = io->gsrc16_ld;
+      x.y1_bits = src_bits;
+      x.y1_bits_ld = src_bits_ld;
+      x.Y2 = dA;
+      x.ld2 = lda;
+    } else if (sage) {
       x.Y1 = Gsrc;  // dH_dst lands directly in rows [0, n_dst) of dH_src
       x.ld1 = ld->in_stride;
       if (tf32) {
@@ -426,7 +450,7 @@ void layer_bwd_impl(gnnv_blocks* b, int32_t layer, const gnnv_layer_desc* ld, co
     if (tl) tl->mark(s, "gemm_dx" + sfx);
     gemm_dx(x, ld->prec, s);
     if (tl) tl->mark(s, "spmm_bwd" + sfx);
-    if (b->pull_bwd && ((b->csc_mask >> h) & 1u) && ld->in_stride <= kPullMaxLd) {
+    if (!g16 && b->pull_bwd && ((b->csc_mask >> h) & 1u) && ld->in_stride <= kPullMaxLd) {
       // transposed aggregation pulled per src row through the block's CSC:
       // one coalesced store per dH_src row, no atomics
       launch_spmm_bwd_pull(b->d_colptr[h], b->d_csc[h], b->d_indptr[h], d_ndst, b->d_sizes + h + 1, b->max_n[h + 1],
@@ -435,8 +459,12 @@ void layer_bwd_impl(gnnv_blocks* b, int32_t layer, const gnnv_layer_desc* ld, co
     } else {
       // transposed aggregation pushed from the dst rows: owner edges store,
       // the rest add atomically -- no zeroing pass over dH_src
-      launch_spmm_bwd(b->d_indptr[h], b->d_indices[h], b->d_own[h], d_ndst, max_dst, dA, lda, Gsrc, ld->in_stride,
-                      ld->d_in, ld->kind, ld->aggr, tf32 ? src_bits : nullptr, src_bits_ld, s);
+      if (g16)
+        launch_spmm_bwd(b->d_indptr[h], b->d_indices[h], b->d_own[h], d_ndst, max_dst, dA, lda, io->gsrc16,
+                        io->gsrc16_ld, ld->d_in, ld->kind, ld->aggr, src_bits, src_bits_ld, s, true);
+      else
+        launch_spmm_bwd(b->d_indptr[h], b->d_indices[h], b->d_own[h], d_ndst, max_dst, dA, lda, Gsrc, ld->in_stride,
+                        ld->d_in, ld->kind, ld->aggr, tf32 ? src_bits : nullptr, src_bits_ld, s);
     }
   }
 }
@@ -453,7 +481,7 @@ gnnv_status gnnv_layer_fwd(gnnv_blocks* b, int32_t layer, const gnnv_layer_desc*
     check_layer(b, layer, ld);
     GNNV_REQUIRE(d_Hsrc && d_W && d_b && d_Hdst && d_saveA, GNNV_ERR_PARAM, "layer_fwd: null buffer");
     layer_fwd_impl(b, layer, ld, d_Hsrc, d_W, d_b, d_Hdst, d_saveA, (cudaStream_t)s, nullptr, nullptr, nullptr, nullptr,
-                   nullptr, nullptr, false);
+                   nullptr, nullptr, false, nullptr);
   });
 }
 
@@ -465,7 +493,7 @@ gnnv_status gnnv_layer_bwd(gnnv_blocks* b, int32_t layer, const gnnv_layer_desc*
     GNNV_REQUIRE(d_Gdst && d_Hdst && d_Hsrc && d_saveA && d_W && d_dW && d_db, GNNV_ERR_PARAM,
                  "layer_bwd: null buffer");
     layer_bwd_impl(b, layer, ld, d_Gdst, d_Hdst, d_Hsrc, d_saveA, d_W, d_Gsrc, d_dW, d_db, (cudaStream_t)s, nullptr,
-                   nullptr, false, nullptr, 0, nullptr, false);
+                   nullptr, false, nullptr, 0, nullptr, false, nullptr);
   });
 }
 

@@ -15,6 +15,8 @@
 // shuffles; four neighbour rows are loaded before they are added, in
 // ascending edge order (a fixed summation order).  HBM-bound: compulsory
 // bytes are the distinct source rows + the output rows + the indices.
+#include <cuda_bf16.h>
+
 #include "common.cuh"
 
 namespace gnnv {
@@ -161,11 +163,33 @@ __global__ void __launch_bounds__(256) k_spmm_fwd(const int32_t* __restrict__ in
 //           by phase 1 or, for u < n_dst, by the dX GEMM (SAGE dH_dst).
 // Every dH row < n_src is therefore written before it is accumulated into;
 // phase 2 carries only the repeated ids (products layer 2: ~30% of edges).
-template <int LPR>
+// dH row pieces of 4 elements: fp32 (float4) or, with H16, bf16 (8 bytes;
+// the phase-2 additions are two red.global.add.noftz.bf16x2)
+__device__ __forceinline__ uint32_t pack_bf16x2(float a, float b) {
+  const __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+  return *reinterpret_cast<const uint32_t*>(&h);
+}
+template <bool H16>
+__device__ __forceinline__ void dh_store4(void* dH, int64_t i4, float4 v) {
+  if (!H16) reinterpret_cast<float4*>(dH)[i4] = v;
+  else reinterpret_cast<uint2*>(dH)[i4] = make_uint2(pack_bf16x2(v.x, v.y), pack_bf16x2(v.z, v.w));
+}
+template <bool H16>
+__device__ __forceinline__ void dh_add4(void* dH, int64_t i4, float4 v) {
+  if (!H16) {
+    atomicAdd(reinterpret_cast<float4*>(dH) + i4, v);
+  } else {
+    uint32_t* p = reinterpret_cast<uint32_t*>(reinterpret_cast<uint2*>(dH) + i4);
+    asm volatile("red.global.add.noftz.bf16x2 [%0], %1;" ::"l"(p), "r"(pack_bf16x2(v.x, v.y)) : "memory");
+    asm volatile("red.global.add.noftz.bf16x2 [%0], %1;" ::"l"(p + 1), "r"(pack_bf16x2(v.z, v.w)) : "memory");
+  }
+}
+
+template <int LPR, bool H16 = false>
 __global__ void __launch_bounds__(256) k_spmm_bwd(const int32_t* __restrict__ indptr,
                                                   const int32_t* __restrict__ indices,
                                                   const uint32_t* __restrict__ own, const int32_t* d_ndst,
-                                                  const float* __restrict__ dA, int32_t lda, float* dH, int32_t ldh,
+                                                  const float* __restrict__ dA, int32_t lda, void* dH, int32_t ldh,
                                                   int32_t d, int32_t kind, int32_t aggr, int32_t phase,
                                                   const uint32_t* __restrict__ bits, int32_t bits_ld) {
   GNNV_PDL_ENTRY();
@@ -178,7 +202,6 @@ __global__ void __launch_bounds__(256) k_spmm_bwd(const int32_t* __restrict__ in
   const int nwarps = (gridDim.x * blockDim.x) >> 5;
   const int ldh4 = ldh >> 2, lda4 = lda >> 2;
   const int cols = phase == 1 ? ldh4 : vec;  // phase 1 also writes the padding
-  float4* dH4 = reinterpret_cast<float4*>(dH);
   const bool gcn = kind == GNNV_KIND_GCN;
   // optional ReLU mask of dH's rows (the previous layer's output bits):
   // dH[u] = relu'(H[u]) * sum, applied to every contribution
@@ -208,7 +231,7 @@ __global__ void __launch_bounds__(256) k_spmm_bwd(const int32_t* __restrict__ in
       float4 g = make_float4(0.f, 0.f, 0.f, 0.f);
       if (cok && c < vec)
         g = mask_tail(f4scale(__ldg(reinterpret_cast<const float4*>(dA) + (int64_t)row * lda4 + c), w), c, d);
-      if (phase == 1 && gcn && cok) dH4[(int64_t)row * ldh4 + c] = c < vec ? masked(g, row, c) : g;
+      if (phase == 1 && gcn && cok) dh_store4<H16>(dH, (int64_t)row * ldh4 + c, c < vec ? masked(g, row, c) : g);
       for (int e0 = 0; e0 < cnt; e0 += LPR) {
         const int my = (e0 + sl < cnt) ? __ldg(indices + beg + e0 + sl) : 0;
         const int m = min(LPR, cnt - e0);
@@ -238,8 +261,8 @@ __global__ void __launch_bounds__(256) k_spmm_bwd(const int32_t* __restrict__ in
             if (q < k && cok) {
               const float4 gm = make_float4(wb[q] & 1u ? g.x : 0.f, wb[q] & 2u ? g.y : 0.f, wb[q] & 4u ? g.z : 0.f,
                                             wb[q] & 8u ? g.w : 0.f);
-              if (phase == 1) dH4[(int64_t)u[q] * ldh4 + c] = gm;
-              else atomicAdd(dH4 + (int64_t)u[q] * ldh4 + c, gm);
+              if (phase == 1) dh_store4<H16>(dH, (int64_t)u[q] * ldh4 + c, gm);
+              else dh_add4<H16>(dH, (int64_t)u[q] * ldh4 + c, gm);
             }
           }
         }
@@ -426,22 +449,119 @@ void launch_spmm_fwd(const int32_t* d_indptr, const int32_t* d_indices, const in
 }
 
 void launch_spmm_bwd(const int32_t* d_indptr, const int32_t* d_indices, const uint32_t* d_own, const int32_t* d_ndst,
-                     int64_t max_dst, const float* dA, int32_t lda, float* dH, int32_t ldh, int32_t d, int32_t kind,
-                     int32_t aggr, const uint32_t* bits, int32_t bits_ld, cudaStream_t s) {
+                     int64_t max_dst, const float* dA, int32_t lda, void* dH, int32_t ldh, int32_t d, int32_t kind,
+                     int32_t aggr, const uint32_t* bits, int32_t bits_ld, cudaStream_t s, bool dh_bf16) {
   const int ldh4 = ldh / 4;
   for (int phase = 1; phase <= 2; ++phase) {
-    if (ldh4 <= 8) {
-      launch_k(k_spmm_bwd<8>, spmm_grid(max_dst, 4), 256, 0, s, d_indptr, d_indices, d_own, d_ndst, dA, lda, dH, ldh, d, kind,
-                                                          aggr, phase, bits, bits_ld);
-    } else if (ldh4 <= 16) {
-      launch_k(k_spmm_bwd<16>, spmm_grid(max_dst, 2), 256, 0, s, d_indptr, d_indices, d_own, d_ndst, dA, lda, dH, ldh, d,
-                                                           kind, aggr, phase, bits, bits_ld);
-    } else {
-      launch_k(k_spmm_bwd<32>, spmm_grid(max_dst, 1), 256, 0, s, d_indptr, d_indices, d_own, d_ndst, dA, lda, dH, ldh, d,
-                                                           kind, aggr, phase, bits, bits_ld);
-    }
+#define GNNV_BWD(LPR, RPWv)                                                                                          \
+  do {                                                                                                               \
+    if (dh_bf16)                                                                                                     \
+      launch_k(k_spmm_bwd<LPR, true>, spmm_grid(max_dst, RPWv), 256, 0, s, d_indptr, d_indices, d_own, d_ndst, dA,   \
+               lda, dH, ldh, d, kind, aggr, phase, bits, bits_ld);                                                   \
+    else                                                                                                             \
+      launch_k(k_spmm_bwd<LPR, false>, spmm_grid(max_dst, RPWv), 256, 0, s, d_indptr, d_indices, d_own, d_ndst, dA,  \
+               lda, dH, ldh, d, kind, aggr, phase, bits, bits_ld);                                                   \
+  } while (0)
+    if (ldh4 <= 8) GNNV_BWD(8, 4);
+    else if (ldh4 <= 16) GNNV_BWD(16, 2);
+    else GNNV_BWD(32, 1);
+#undef GNNV_BWD
     GNNV_CHECK_LAUNCH();
   }
+}
+
+// The aggregation over bf16 source rows (the trainer's bf16 copy of a hidden
+// layer's output): eight elements (16 bytes) per lane and
+// unit, fp32 accumulation in the fp32 kernel's edge order, fp32 aggregate.
+// d % 8 == 0, row stride ld16 elements (a multiple of 8).
+__device__ __forceinline__ void add_bf16x8(float* acc, uint4 q) {
+  const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    acc[2 * k] += __uint_as_float(w[k] << 16);
+    acc[2 * k + 1] += __uint_as_float(w[k] & 0xFFFF0000u);
+  }
+}
+template <int LPR>
+__global__ void __launch_bounds__(256) k_spmm_fwd_h16(const int32_t* __restrict__ indptr,
+                                                      const int32_t* __restrict__ indices, const int32_t* d_ndst,
+                                                      const __nv_bfloat16* __restrict__ H, int32_t ld16,
+                                                      float* __restrict__ A, int32_t lda, int32_t d, int32_t kind,
+                                                      int32_t aggr) {
+  GNNV_PDL_ENTRY();
+  constexpr int RPW = 32 / LPR;
+  const int n = *d_ndst;
+  const int vec8 = d >> 3;
+  const int lane = threadIdx.x & 31, sub = lane / LPR, sl = lane % LPR;
+  const unsigned smask = (LPR == 32) ? 0xffffffffu : (((1u << LPR) - 1u) << (sub * LPR));
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  const uint4* H8 = reinterpret_cast<const uint4*>(H);
+  const int ld8 = ld16 >> 3, lda4 = lda >> 2;
+  for (int base = warp * RPW; base < n; base += nwarps * RPW) {
+    const int row = base + sub;
+    const bool active = row < n;
+    const int beg = active ? indptr[row] : 0;
+    const int cnt = active ? indptr[row + 1] - beg : 0;
+    for (int c0 = 0; c0 < vec8; c0 += LPR) {
+      const int c = c0 + sl;
+      const bool cok = active && c < vec8;
+      float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+      if (kind == GNNV_KIND_GCN && cok) add_bf16x8(acc, __ldg(H8 + (int64_t)row * ld8 + c));
+      for (int e0 = 0; e0 < cnt; e0 += LPR) {
+        const int my = (e0 + sl < cnt) ? __ldg(indices + beg + e0 + sl) : 0;
+        const int m = min(LPR, cnt - e0);
+        int j = 0;
+        for (; j + 4 <= m; j += 4) {
+          const int u0 = __shfl_sync(smask, my, j, LPR), u1 = __shfl_sync(smask, my, j + 1, LPR);
+          const int u2 = __shfl_sync(smask, my, j + 2, LPR), u3 = __shfl_sync(smask, my, j + 3, LPR);
+          if (cok) {
+            const uint4 h0 = __ldg(H8 + (int64_t)u0 * ld8 + c), h1 = __ldg(H8 + (int64_t)u1 * ld8 + c);
+            const uint4 h2 = __ldg(H8 + (int64_t)u2 * ld8 + c), h3 = __ldg(H8 + (int64_t)u3 * ld8 + c);
+            add_bf16x8(acc, h0);
+            add_bf16x8(acc, h1);
+            add_bf16x8(acc, h2);
+            add_bf16x8(acc, h3);
+          }
+        }
+        for (; j < m; ++j) {
+          const int u = __shfl_sync(smask, my, j, LPR);
+          if (cok) add_bf16x8(acc, __ldg(H8 + (int64_t)u * ld8 + c));
+        }
+      }
+      if (cok) {
+        if (aggr == GNNV_AGGR_MEAN) {
+          const int denom = cnt + (kind == GNNV_KIND_GCN ? 1 : 0);
+#pragma unroll
+          for (int k = 0; k < 8; ++k) acc[k] = denom ? acc[k] / (float)denom : 0.f;
+        }
+        float4* out = reinterpret_cast<float4*>(A) + (int64_t)row * lda4 + 2 * c;
+        out[0] = make_float4(acc[0], acc[1], acc[2], acc[3]);
+        out[1] = make_float4(acc[4], acc[5], acc[6], acc[7]);
+      }
+    }
+    if (active)  // padding float4s of the output row
+      for (int c4 = 2 * vec8 + sl; c4 < lda4; c4 += LPR)
+        reinterpret_cast<float4*>(A)[(int64_t)row * lda4 + c4] = make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+}
+
+void launch_spmm_fwd_h16(const int32_t* d_indptr, const int32_t* d_indices, const int32_t* d_ndst, int64_t max_dst,
+                         const void* H16, int32_t ld16, float* A, int32_t lda, int32_t d, int32_t kind, int32_t aggr,
+                         cudaStream_t s) {
+  GNNV_REQUIRE(d % 8 == 0 && ld16 % 8 == 0, GNNV_ERR_UNSUPPORTED, "spmm_fwd_h16: d and the row stride must be multiples of 8");
+  const int vec8 = d / 8;
+  const __nv_bfloat16* H = static_cast<const __nv_bfloat16*>(H16);
+  if (vec8 <= 8)
+    launch_k(k_spmm_fwd_h16<8>, spmm_grid(max_dst, 4), 256, 0, s, d_indptr, d_indices, d_ndst, H, ld16, A, lda, d, kind,
+             aggr);
+  else if (vec8 <= 16)
+    launch_k(k_spmm_fwd_h16<16>, spmm_grid(max_dst, 2), 256, 0, s, d_indptr, d_indices, d_ndst, H, ld16, A, lda, d, kind,
+             aggr);
+  else
+    launch_k(k_spmm_fwd_h16<32>, spmm_grid(max_dst, 1), 256, 0, s, d_indptr, d_indices, d_ndst, H, ld16, A, lda, d, kind,
+             aggr);
+  GNNV_CHECK_LAUNCH();
 }
 
 void launch_spmm_bwd_pull(const int32_t* d_colptr, const int32_t* d_csc, const int32_t* d_indptr,

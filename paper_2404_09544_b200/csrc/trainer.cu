@@ -14,11 +14,12 @@ namespace gnnv {
 void layer_fwd_impl(gnnv_blocks* b, int32_t layer, const gnnv_layer_desc* ld, const float* Hsrc, const float* W,
                     const float* bias, float* Hdst, float* A, cudaStream_t s, Timeline* tl, uint32_t* mask_bits,
                     const float* agg_table, const int32_t* rowidx, const XRows* xr, const FwdPush* push,
-                    bool agg_ready);
+                    bool agg_ready, const Bf16Io* io);
 void layer_bwd_impl(gnnv_blocks* b, int32_t layer, const gnnv_layer_desc* ld, const float* Gdst, const float* Hdst,
                     const float* Hsrc, const float* A, const float* W, float* Gsrc, float* dW, float* db,
                     cudaStream_t s, Timeline* tl, const uint32_t* mask_bits, bool g_masked,
-                    const uint32_t* src_bits, int32_t src_bits_ld, const XRows* xr, bool grads_zeroed);
+                    const uint32_t* src_bits, int32_t src_bits_ld, const XRows* xr, bool grads_zeroed,
+                    const Bf16Io* io);
 }  // namespace gnnv
 
 using namespace gnnv;
@@ -76,6 +77,14 @@ struct gnnv_trainer {
   // then waits ~0.2 ms for the longer prefetch).  A^1 per
   // buffer set: A1b[k] (t->A[1] follows the current set).
   bool pf_agg = false;
+  // bf16 intermediates (GNNV_BF16ACT; TF32 SAGE, L >= 3): H^i and dL/dH^i of
+  // the hidden layers i <= L-2 -- the widest activations, read back by the
+  // next layer's aggregation and by layer i's dW -- as bf16 (H16[i], G16[i],
+  // row stride ld16[i]); H[i] fp32 then holds only layer i+1's dst prefix
+  bool bf16act = false;
+  void* H16[GNNV_MAX_LAYERS + 1] = {nullptr};
+  void* G16[GNNV_MAX_LAYERS + 1] = {nullptr};
+  int32_t ld16[GNNV_MAX_LAYERS + 1] = {0};
   float* A1b[2] = {nullptr, nullptr};
   float* tail_dA = nullptr;    // [max_n[0] x dims[L-1]]
   float* tail_part = nullptr;  // per-CTA dW/db partials
@@ -182,6 +191,10 @@ gnnv_status gnnv_trainer_free(gnnv_trainer* t) {
     dfree(t->G[i]);
   }
   for (auto* m : t->mbits) dfree(m);
+  for (int i = 0; i <= GNNV_MAX_LAYERS; ++i) {
+    dfree(t->H16[i]);
+    dfree(t->G16[i]);
+  }
   dfree(t->loss_partial);
   dfree(t->tail_dA);
   dfree(t->tail_part);
@@ -262,7 +275,17 @@ gnnv_status gnnv_trainer_create(gnnv_graph* g, gnnv_cache* c, const gnnv_model_d
           (float*)dmalloc(std::max<int64_t>(256, ceil_div(b->max_n[0], 32)) * sizeof(float), "loss partials");
       t->tail = md->prec == GNNV_PREC_TF32 && L >= 2 &&
                 tail_supported(md->kind, md->dims[L - 1], md->dims[L], md->fanouts[0]) && !env_on("GNNV_NO_TAIL");
-      t->l2push = md->prec == GNNV_PREC_TF32 && md->kind == GNNV_KIND_SAGE && L >= 3 && env_on("GNNV_L2PUSH");
+      t->bf16act = md->prec == GNNV_PREC_TF32 && md->kind == GNNV_KIND_SAGE && L >= 3 && env_on("GNNV_BF16ACT");
+      for (int i = 1; i <= L - 2 && t->bf16act; ++i) t->bf16act = md->dims[i] % 8 == 0;
+      if (t->bf16act)
+        for (int i = 1; i <= L - 2; ++i) {
+          t->ld16[i] = (md->dims[i] + 31) / 32 * 32;
+          const size_t bytes = (size_t)b->max_n[L - i] * t->ld16[i] * 2;
+          t->H16[i] = dmalloc(bytes, "bf16 activations");
+          t->G16[i] = dmalloc(bytes, "bf16 activation gradients");
+        }
+      t->l2push = !t->bf16act && md->prec == GNNV_PREC_TF32 && md->kind == GNNV_KIND_SAGE && L >= 3 &&
+                  env_on("GNNV_L2PUSH");
       if (t->l2push)
         for (int i = 1; i <= L - 2; ++i) blocks_enable_owner_rows(t->b, L - i - 1);
       // dead-row L2 hints for the layer-1 aggregation (spmm.cu HINT; opt-in
@@ -362,6 +385,15 @@ gnnv_status gnnv_trainer_relu_bits(gnnv_trainer* t, int32_t i, const uint32_t** 
 }
 
 int32_t gnnv_trainer_l2push(const gnnv_trainer* t) { return t && t->l2push ? 1 : 0; }
+int32_t gnnv_trainer_bf16act(const gnnv_trainer* t) { return t && t->bf16act ? 1 : 0; }
+
+gnnv_status gnnv_trainer_activation16(gnnv_trainer* t, int32_t i, const void** d_H16, int32_t* ld) {
+  return guarded([&] {
+    GNNV_REQUIRE(t && d_H16 && ld && i >= 0 && i <= t->md.L, GNNV_ERR_PARAM, "trainer_activation16: bad args");
+    *d_H16 = t->H16[i];
+    *ld = t->H16[i] ? t->ld16[i] : 0;
+  });
+}
 
 gnnv_status gnnv_trainer_set_locality(gnnv_trainer* t, double bias) {
   return guarded([&] {
@@ -655,10 +687,22 @@ gnnv_status gnnv_step(gnnv_trainer* t, const int32_t* seeds, int32_t n_seeds, in
         push = FwdPush{b->d_colptr[hn], b->d_csc[hn], b->d_indptr[hn], t->A[i + 1], row_stride(t->md.dims[i]),
                        t->md.aggr == GNNV_AGGR_MEAN, b->d_sizes + hn, b->d_owner_row[hn]};
       }
+      Bf16Io io{};
+      if (t->bf16act) {
+        if (i <= L - 2) {  // this layer's output: a bf16 copy, fp32 rows for the next dst prefix
+          io.y16 = t->H16[i];
+          io.ld16 = t->ld16[i];
+          io.keep_rows = b->d_sizes + (L - i - 1);
+        }
+        if (i >= 2 && i - 1 <= L - 2) {  // aggregate the previous layer's bf16 copy
+          io.src16 = t->H16[i - 1];
+          io.src16_ld = t->ld16[i - 1];
+        }
+      }
       layer_fwd_impl(b, i, &ld, t->H[i - 1], t->d_params + t->w_off[i - 1], t->d_params + t->b_off[i - 1], t->H[i],
                      t->A[i], s, tl, t->mbits[i], t->table, i == 1 ? t->rowidx[t->cur] : nullptr,
                      i == 1 ? xr1 : nullptr, do_push ? &push : nullptr,
-                     (t->l2push && i >= 2 && i <= L - 1) || (i == 1 && agg1_ready));
+                     (t->l2push && i >= 2 && i <= L - 1) || (i == 1 && agg1_ready), t->bf16act ? &io : nullptr);
     }
     if (tm) GNNV_TRY_CUDA(cudaEventRecord(t->ev[3], s));
     float* d_loss = t->d_grads + t->nparams;
@@ -708,10 +752,21 @@ gnnv_status gnnv_step(gnnv_trainer* t, const int32_t* seeds, int32_t n_seeds, in
     for (int i = L; i >= 1; --i) {
       if (t->tail && i == L) continue;
       const gnnv_layer_desc ld = layer_desc(t, i);
+      Bf16Io io{};
+      if (t->bf16act) {
+        if (i - 1 >= 1 && i - 1 <= L - 2) {  // dL/dH^{i-1} produced as bf16
+          io.gsrc16 = t->G16[i - 1];
+          io.gsrc16_ld = t->ld16[i - 1];
+        }
+        if (i <= L - 2) {  // this layer's G read as bf16
+          io.gdst16 = t->G16[i];
+          io.gdst16_ld = t->ld16[i];
+        }
+      }
       layer_bwd_impl(b, i, &ld, t->G[i], t->H[i], t->H[i - 1], t->A[i], t->d_params + t->w_off[i - 1],
                      i > 1 ? t->G[i - 1] : nullptr, t->d_grads + t->w_off[i - 1], t->d_grads + t->b_off[i - 1], s, tl,
                      t->mbits[i], t->mbits[i] != nullptr, t->mbits[i - 1], mask_words(t->md.dims[i - 1]),
-                     i == 1 ? xr1 : nullptr, t->tail);
+                     i == 1 ? xr1 : nullptr, t->tail, t->bf16act ? &io : nullptr);
     }
     if (tm) GNNV_TRY_CUDA(cudaEventRecord(t->ev[5], s));
     if (tl) tl->mark(s, "allreduce");

@@ -131,6 +131,8 @@ _SIGS = {
     "gnnv_trainer_aggregate": (I32, [VP, I32, PP, C.POINTER(I32)]),
     "gnnv_trainer_relu_bits": (I32, [VP, I32, PP, C.POINTER(I32)]),
     "gnnv_trainer_l2push": (I32, [VP]),
+    "gnnv_trainer_bf16act": (I32, [VP]),
+    "gnnv_trainer_activation16": (I32, [VP, I32, PP, C.POINTER(I32)]),
     "gnnv_step": (I32, [VP, VP, I32, I32, I32, U64, F32, C.POINTER(F32), C.POINTER(StepTiming), VP]),
     "gnnv_trainer_stats": (I32, [VP, VP]),
     "gnnv_trainer_prefetch": (I32, [VP, VP, I32, I32, U64, VP]),
@@ -566,6 +568,16 @@ class Trainer:
 
     def l2push(self) -> bool:
         return bool(load().gnnv_trainer_l2push(self.h))
+
+    def bf16act(self) -> bool:
+        return bool(load().gnnv_trainer_bf16act(self.h))
+
+    def activation16(self, i: int):
+        """(device pointer, row stride) of the bf16 copy of H^i, or (0, 0)."""
+        p = C.c_void_p()
+        ld = C.c_int32()
+        _check(load().gnnv_trainer_activation16(self.h, i, C.byref(p), C.byref(ld)))
+        return int(p.value or 0), int(ld.value)
 
     def timeline(self, on: bool):
         _check(load().gnnv_trainer_timeline(self.h, 1 if on else 0))

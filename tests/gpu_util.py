@@ -52,6 +52,13 @@ def read_f32(p, rows, stride):
     return out.cpu().numpy()
 
 
+def read_bf16(p, rows, ld):
+    """A [rows x ld] bf16 matrix from a device pointer, as float64."""
+    n = int(rows) * int(ld)
+    w = read_i32(p, (n + 1) // 2).view(np.uint16)[:n].reshape(int(rows), int(ld))
+    return (w.astype(np.uint32) << 16).view(np.float32).astype(np.float64)
+
+
 def read_bits(p, rows, words, ncols):
     """A [rows x words] uint32 ReLU bit mask from a device pointer, unpacked
     to bool [rows x ncols] (bit n%32 of word n/32)."""
@@ -134,7 +141,8 @@ def check_forward_chain(tr, hb, dims, w, rtol, name, X0=None, max_rows=2048, kin
     layer i) on sampled rows, within layer i's bound (relu is 1-Lipschitz,
     the mean a convex sum).  Returns (H, Aagg, blks) for the backward."""
     L = len(hb)
-    push = tr.l2push()
+    bf16 = tr.bf16act()
+    push = tr.l2push() or bf16  # H^i stored in fp32 for the next dst prefix only
     rng = np.random.default_rng(seed)
     H = [None] * (L + 1)
     Aagg = [None] * (L + 1)
@@ -155,7 +163,27 @@ def check_forward_chain(tr, hb, dims, w, rtol, name, X0=None, max_rows=2048, kin
         Hout = read_f32(p_out, (_blk(hb, L - i - 1).n_dst if pushed_out else ob.n_dst), s_out)[:, : dims[i]]
         H[i - 1], H[i] = Hin, Hout
         Wi, bi = w[i - 1]
-        if pushed_in:
+        if pushed_in and bf16:
+            # layer i aggregated the bf16 copy of H^{i-1}: A^i against the
+            # fp32 accumulation of exactly those bf16 values (1e-5), and the
+            # copy against the fp32 prefix (bf16 rounding, 2^-9 relative)
+            pa, sa = tr.aggregate(i)
+            A_gpu = read_f32(pa, ob.n_dst, sa)[:, : dims[i - 1]]
+            Aagg[i] = A_gpu
+            p16, ld16 = tr.activation16(i - 1)
+            H16 = read_bf16(p16, ob.n_src, ld16)[:, : dims[i - 1]]
+            n_pre = len(Hin)
+            np.testing.assert_allclose(H16[:n_pre], Hin, rtol=2.0 ** -8, atol=1e-30)
+            A_ref = agg_matrix(ob, kind) @ H16
+            A_mag = agg_matrix(ob, kind) @ np.abs(H16)
+            assert_close_cond(A_gpu, A_ref, A_mag, 1e-5, f"{name} A^{i} over the bf16 copy of H^{i - 1}")
+            X = np.concatenate([Hin.astype(np.float64), A_gpu.astype(np.float64)], axis=1)
+            Z = X @ Wi.astype(np.float64) + bi
+            Zm = np.abs(X) @ np.abs(Wi.astype(np.float64)) + np.abs(bi)
+            Ho = np.maximum(Z, 0) if i < L else Z
+            n = len(Hout)
+            assert_close_cond(Hout, Ho[:n], Zm[:n], rtol, f"{name} layer {i} (on its bf16-fed aggregate)")
+        elif pushed_in:
             pa, sa = tr.aggregate(i)
             A_gpu = read_f32(pa, ob.n_dst, sa)[:, : dims[i - 1]]
             Aagg[i] = A_gpu
@@ -185,6 +213,15 @@ def check_forward_chain(tr, hb, dims, w, rtol, name, X0=None, max_rows=2048, kin
             Ho, _ = layer_fwd(blk, Hs, Wi, bi, i < L, kind)
             Hm, _ = layer_fwd(blk, Hs, Wi, bi, i < L, kind, absval=True)
             assert_close_cond(Hout[rows], Ho, Hm, rtol, f"{name} layer {i} (sampled rows)")
+            if bf16 and pushed_out:  # the bf16 copy beyond the prefix, on sampled rows: + bf16 rounding
+                p16, ld16 = tr.activation16(i)
+                H16 = read_bf16(p16, ob.n_dst, ld16)[:, : dims[i]]
+                rows = np.sort(rng.choice(ob.n_dst, min(ob.n_dst, max_rows), replace=False))
+                blk, Hs = sub_block(ob, Hin, rows)
+                Ho, _ = layer_fwd(blk, Hs, Wi, bi, i < L, kind)
+                Hm, _ = layer_fwd(blk, Hs, Wi, bi, i < L, kind, absval=True)
+                assert_close_cond(H16[rows], Ho, (rtol + 2.0 ** -8) / rtol * Hm, rtol,
+                                  f"{name} bf16 copy of layer {i} (sampled rows)")
         else:
             Ho, _ = layer_fwd(ob, Hin, Wi, bi, i < L, kind)
             Hm, _ = layer_fwd(ob, Hin, Wi, bi, i < L, kind, absval=True)
@@ -200,7 +237,7 @@ def check_backward_chain(tr, blks, H, Aagg, dims, w, grads, labels, n_global, rt
     chain propagates on |.|.  With the fused push, layer i's ReLU mask comes
     from the GPU's bits and layer i+1's aggregate is the GPU's A^{i+1}."""
     L = len(blks) - 1
-    push = tr.l2push()
+    push = tr.l2push() or tr.bf16act()
     _, G = ce_loss(H[L], labels, n_global)
     M = np.abs(G)
     for i in range(L, 0, -1):

@@ -15,7 +15,7 @@ from oracle.sampler import Block, sample_blocks
 from paper_2404_09544_b200 import gnnv
 from synth import CONFIGS, epoch_seeds, init_weights, make_graph, row_stride, tiny_graph
 
-from gpu_util import check_forward_chain, sub_block, assert_close_cond, blocks_to_host, dev_f32, dev_i32, lib, normwise, read_f32, read_i32
+from gpu_util import check_backward_chain, check_forward_chain, sub_block, assert_close_cond, blocks_to_host, dev_f32, dev_i32, lib, normwise, read_f32, read_i32
 
 pytestmark = pytest.mark.gpu
 
@@ -781,6 +781,45 @@ def test_dynamic_tile_scheduler_bitwise_neutral(mini, option):
         out[name] = res
         tr.free()
     assert out["dynamic"] == out["static"]
+
+
+@pytest.mark.parametrize("ratio", [0.3, 1.0])
+def test_bf16_intermediates(mini, option, ratio):
+    """GNNV_BF16ACT: the tf32 SAGE trainer keeps H^1 and dL/dH^1 (the widest
+    activations, L = 3) as bf16 -- the layer-2 aggregation reads the bf16
+    copy, layer 1's dW reads the bf16 gradient.  The step against the oracle
+    at the tf32 bounds (gpu_util chain checks: A^2 exact over the bf16
+    values, layer 2 on the GPU's own inputs, every dW/db through the
+    oracle's backward chain), and against the fp32-intermediate step: loss
+    within 2e-3, gradient directions within cos 0.999."""
+    gd, g = mini
+    cfg = CONFIGS["mini"]
+    dims = [gd.d, cfg["hidden"], cfg["hidden"], gd.C]
+    w = init_weights(dims)
+    seeds = epoch_seeds(gd.n, 0)[: cfg["batch"]]
+    B = len(seeds)
+    out = {}
+    for name in ("bf16", "fp32"):
+        option("GNNV_BF16ACT", 1 if name == "bf16" else 0)
+        tr = gnnv.Trainer(g, gnnv.Cache(g, ratio), dims, cfg["fanouts"], cfg["batch"], w, prec=gnnv.PREC_TF32)
+        assert tr.bf16act() == (name == "bf16")
+        tr.prefetch(seeds, B, 0x5EED)
+        loss, _ = tr.step(seeds, B, B, 0x5EED, 0.0)
+        grads = gnnv.unflat_params(tr.grads(), dims)
+        if name == "bf16":
+            hb = blocks_to_host(tr.blocks)
+            L = len(cfg["fanouts"])
+            X0 = oracle.gather_rows(gd.feats, hb[L - 1][4])[:, : dims[0]] if tr.x_level() < L else None
+            H, Aagg, blks = check_forward_chain(tr, hb, dims, w, RTOL[2], "bf16act", X0=X0, max_rows=10**9)
+            check_backward_chain(tr, blks, H, Aagg, dims, w, grads, gd.labels[seeds], B, RTOL[2], "bf16act")
+        out[name] = (loss, grads)
+        tr.free()
+    (lb, gb_), (lf, gf) = out["bf16"], out["fp32"]
+    assert abs(lb - lf) <= 2e-3 * abs(lf), (lb, lf)
+    for (aW, ab), (bW, bb) in zip(gb_, gf):
+        for a_, b_ in ((aW, bW), (ab, bb)):
+            cos = float(np.dot(a_.ravel(), b_.ravel()) / (np.linalg.norm(a_) * np.linalg.norm(b_) + 1e-30))
+            assert cos > 0.999, cos
 
 
 @pytest.mark.parametrize("kind", [gnnv.KIND_SAGE, gnnv.KIND_GCN])
