@@ -214,6 +214,7 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
 struct Params {
   CUtensorMap ta1, ta2, tb;
   CUtensorMap ty1, ty2;  // fwd/dX outputs (TMA stores, SW128 boxes of 32 x 32)
+  CUtensorMap ty16;      // fwd: the bf16 copy (unswizzled boxes of 32 x 32 bf16)
   int two;      // A has a second source (SAGE [H_dst | A])
   int nkb1;     // fwd: K blocks served by X1 (ceil(K1/32)); dw: 32-col blocks of X1
   int nkb;      // fwd/dx: K blocks in total
@@ -649,16 +650,6 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_tma_gemm(const __grid_constant_
             for (int j = 0; j < 32; ++j)
               if (j0 + j < p.ld1 && !((wv >> j) & 1u)) v[j] = 0.f;
           }
-          if (MODE == MODE_FWD && p.y16 && c < p.ld16) {  // bf16 copy of the row piece (64 bytes)
-            const int64_t m = (int64_t)row0 + lane;
-            if (m < M) {
-              uint4* dst = reinterpret_cast<uint4*>(p.y16 + m * p.ld16 + c);
-#pragma unroll
-              for (int q = 0; q < 4; ++q)
-                dst[q] = make_uint4(bf16x2(v[8 * q], v[8 * q + 1]), bf16x2(v[8 * q + 2], v[8 * q + 3]),
-                                    bf16x2(v[8 * q + 4], v[8 * q + 5]), bf16x2(v[8 * q + 6], v[8 * q + 7]));
-            }
-          }
           if (MODE == MODE_DX && p.y1_16 && j0 < p.ld1) {  // Y1 as bf16 (j0 + 32 <= ld1: checked on the host)
             const int64_t m = (int64_t)row0 + lane;
             if (m < M) {
@@ -689,6 +680,44 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_tma_gemm(const __grid_constant_
                 }
               }
             }
+          }
+          if (MODE == MODE_FWD && !PAIR && p.y16 && !push) {
+            // the bf16 copy (every row) -- and the fp32 dst-prefix rows
+            // first, if this chunk has any -- through the staging buffer and
+            // TMA stores (32 rows x 64 bytes for the bf16 piece)
+            uint8_t* ob = ob0;
+            const uint32_t ob_u32 = smem_u32(ob);
+            if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+            __syncwarp();
+            if (store_rows && !ragged) {
+#pragma unroll
+              for (int j = 0; j < 8; ++j)
+                st_shared_v4(ob_u32 + lane * 128 + ((j ^ (lane & 7)) << 4), v[4 * j], v[4 * j + 1], v[4 * j + 2],
+                             v[4 * j + 3]);
+              asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+              __syncwarp();
+              if (lane == 0) {
+                tma_store_2d(&p.ty1, ob, c, row0);
+                asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+                asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+              }
+              __syncwarp();
+            }
+            if (c < p.ld16) {
+#pragma unroll
+              for (int q = 0; q < 4; ++q)
+                asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(ob_u32 + lane * 64 + q * 16),
+                             "r"(bf16x2(v[8 * q], v[8 * q + 1])), "r"(bf16x2(v[8 * q + 2], v[8 * q + 3])),
+                             "r"(bf16x2(v[8 * q + 4], v[8 * q + 5])), "r"(bf16x2(v[8 * q + 6], v[8 * q + 7]))
+                             : "memory");
+              asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+              __syncwarp();
+              if (lane == 0) {
+                tma_store_2d(&p.ty16, ob, c, row0);
+                asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+              }
+            }
+            continue;
           }
           if (ragged && !push) continue;
           if (!push && !store_rows) continue;
@@ -1269,6 +1298,7 @@ bool gemm_fwd_tma(const GemmFwdArgs& a, cudaStream_t s) {
   p.push_owner = a.push_owner;
   p.y16 = static_cast<__nv_bfloat16*>(a.y16);
   p.ld16 = a.ld16;
+  if (a.y16) p.ty16 = make_map16(a.y16, a.max_M, a.ld16, a.ld16, 32, 32);
   GNNV_REQUIRE(!a.y16 || (a.ld16 % 32 == 0 && a.ld16 >= a.N && a.keep_rows), GNNV_ERR_PARAM,
                "fwd: bf16 copy needs a row stride that is a multiple of 32 and the kept-row count");
   GNNV_REQUIRE(!a.push_out || (a.push_colptr && a.push_dst && a.push_indptr && a.keep_rows && a.push_ld % 4 == 0 &&
