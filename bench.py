@@ -490,6 +490,7 @@ def main():
     free2 = torch.cuda.mem_get_info()[0]
     tr = gnnv.Trainer(g, cache, dims, cfg["fanouts"], B, w, kind=kind, prec=prec, comm=comm)
     tr.set_locality(args.locality_bias)
+    bf16act = tr.bf16act()  # TF32 SAGE, L >= 3: the hidden H^i / dL/dH^i kept as bf16 (reading Q30)
     # the step runs on a high-priority stream; the trainer's prefetch stream
     # has the lowest priority (Eq.4 overlap without delaying the step)
     stream = torch.cuda.Stream(priority=int(os.environ.get("GNNV_STEP_PRIO", "-1")))
@@ -776,10 +777,12 @@ def main():
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": {"fp32": "f32", "bf16": "f32+bf16gemm", "tf32": "f32+tf32gemm"}[args.prec], "data": "synthetic",
+            "vs_baseline": None, "dtype": {"fp32": "f32", "bf16": "f32+bf16gemm", "tf32": "f32+tf32gemm"}[args.prec] + (
+                "+bf16act" if bf16act else ""), "data": "synthetic",
             "config": config_of(cfg, gd, world, args.kind),
             "settings": {"placement": args.placement, "locality_bias": args.locality_bias,
                          "cache_policy": args.policy, "gemm_precision": args.prec,
+                         "bf16_intermediates": bf16act,
                          "gathered_x_mb_per_step": sizes["n"][L] * gd.stride * 4 / 1e6,
                          "pipeline": "eq4-overlap (next batch sample+gather on a side stream)" if pipeline else "off"},
             "step_stats": step_stats,

@@ -102,10 +102,10 @@ const char* gnnv_last_error(void);
 /* Opt-in variants, by name (each measured slower than, or equal to, the
  * default on the products workload): GNNV_XROWS,
  * GNNV_GEMM_PAIR, GNNV_BWD_PULL, GNNV_NO_TAIL, GNNV_NO_PDL, GNNV_L2PUSH,
- * GNNV_LASTUSE, GNNV_STATIC_TILES, GNNV_PF_AGG, GNNV_BF16ACT.
+ * GNNV_LASTUSE, GNNV_STATIC_TILES, GNNV_PF_AGG, GNNV_NO_BF16ACT.
  * value 1 = on, 0 = off, -1 = back to the environment variable of the same
  * name (read once per process; set and not "0" = on).  Takes effect for
- * trainers / blocks created (XROWS, NO_TAIL, BWD_PULL, L2PUSH, LASTUSE, PF_AGG, BF16ACT) or
+ * trainers / blocks created (XROWS, NO_TAIL, BWD_PULL, L2PUSH, LASTUSE, PF_AGG, NO_BF16ACT) or
  * kernels launched (GEMM_PAIR, NO_PDL, STATIC_TILES) afterwards.  PARAM on an unknown
  * name.  Process-wide; not for concurrent use with running steps. */
 gnnv_status gnnv_set_option(const char* name, int32_t value);
@@ -407,8 +407,8 @@ gnnv_status gnnv_trainer_relu_bits(gnnv_trainer* t, int32_t i, const uint32_t** 
 /* 1 if the trainer fuses layer i+1's aggregation into layer i's GEMM
  * epilogue (TF32 SAGE with L >= 3 and GNNV_L2PUSH), else 0. */
 int32_t gnnv_trainer_l2push(const gnnv_trainer* t);
-/* 1 if the trainer keeps bf16 intermediates (GNNV_BF16ACT; TF32 SAGE with
- * L >= 3): for each hidden layer i <= L-2, H^i is also stored as bf16 (all
+/* 1 if the trainer keeps bf16 intermediates (TF32 SAGE with L >= 3, unless
+ * GNNV_NO_BF16ACT): for each hidden layer i <= L-2, H^i is also stored as bf16 (all
  * rows; the next layer aggregates this copy), its fp32 rows only for the
  * next layer's dst prefix (as with gnnv_trainer_l2push), and dL/dH^i is
  * produced and consumed as bf16. */

@@ -77,7 +77,7 @@ struct gnnv_trainer {
   // then waits ~0.2 ms for the longer prefetch).  A^1 per
   // buffer set: A1b[k] (t->A[1] follows the current set).
   bool pf_agg = false;
-  // bf16 intermediates (GNNV_BF16ACT; TF32 SAGE, L >= 3): H^i and dL/dH^i of
+  // bf16 intermediates (TF32 SAGE, L >= 3; GNNV_NO_BF16ACT=1: off): H^i and dL/dH^i of
   // the hidden layers i <= L-2 -- the widest activations, read back by the
   // next layer's aggregation and by layer i's dW -- as bf16 (H16[i], G16[i],
   // row stride ld16[i]); H[i] fp32 then holds only layer i+1's dst prefix
@@ -275,7 +275,7 @@ gnnv_status gnnv_trainer_create(gnnv_graph* g, gnnv_cache* c, const gnnv_model_d
           (float*)dmalloc(std::max<int64_t>(256, ceil_div(b->max_n[0], 32)) * sizeof(float), "loss partials");
       t->tail = md->prec == GNNV_PREC_TF32 && L >= 2 &&
                 tail_supported(md->kind, md->dims[L - 1], md->dims[L], md->fanouts[0]) && !env_on("GNNV_NO_TAIL");
-      t->bf16act = md->prec == GNNV_PREC_TF32 && md->kind == GNNV_KIND_SAGE && L >= 3 && env_on("GNNV_BF16ACT");
+      t->bf16act = md->prec == GNNV_PREC_TF32 && md->kind == GNNV_KIND_SAGE && L >= 3 && !env_on("GNNV_NO_BF16ACT");
       for (int i = 1; i <= L - 2 && t->bf16act; ++i) t->bf16act = md->dims[i] % 8 == 0;
       if (t->bf16act)
         for (int i = 1; i <= L - 2; ++i) {

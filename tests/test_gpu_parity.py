@@ -785,7 +785,7 @@ def test_dynamic_tile_scheduler_bitwise_neutral(mini, option):
 
 @pytest.mark.parametrize("ratio", [0.3, 1.0])
 def test_bf16_intermediates(mini, option, ratio):
-    """GNNV_BF16ACT: the tf32 SAGE trainer keeps H^1 and dL/dH^1 (the widest
+    """The tf32 SAGE trainer (default; GNNV_NO_BF16ACT=1: off) keeps H^1 and dL/dH^1 (the widest
     activations, L = 3) as bf16 -- the layer-2 aggregation reads the bf16
     copy, layer 1's dW reads the bf16 gradient.  The step against the oracle
     at the tf32 bounds (gpu_util chain checks: A^2 exact over the bf16
@@ -800,7 +800,7 @@ def test_bf16_intermediates(mini, option, ratio):
     B = len(seeds)
     out = {}
     for name in ("bf16", "fp32"):
-        option("GNNV_BF16ACT", 1 if name == "bf16" else 0)
+        option("GNNV_NO_BF16ACT", 0 if name == "bf16" else 1)
         tr = gnnv.Trainer(g, gnnv.Cache(g, ratio), dims, cfg["fanouts"], cfg["batch"], w, prec=gnnv.PREC_TF32)
         assert tr.bf16act() == (name == "bf16")
         tr.prefetch(seeds, B, 0x5EED)
@@ -915,6 +915,7 @@ def test_fused_l2_push_matches_per_layer_aggregation(mini, option, aggr, ratio):
     out = {}
     for name in ("push", "plain"):
         option("GNNV_L2PUSH", 1 if name == "push" else 0)
+        option("GNNV_NO_BF16ACT", 1)  # the push and the bf16 intermediates are exclusive
         tr = gnnv.Trainer(g, gnnv.Cache(g, ratio), dims, cfg["fanouts"], cfg["batch"], w, aggr=aggr,
                           prec=gnnv.PREC_TF32)
         assert tr.l2push() == (name == "push")
