@@ -54,6 +54,7 @@ constexpr int FWD_STAGES = 4;
 constexpr int PAIR_STAGES = 5;  // CTA-pair fwd: a stage is A 16 KB + half of B 16 KB
 constexpr int PAIR_OB = 2;      // CTA-pair fwd: double-buffered 4 KB epilogue staging per warp
 constexpr int DW_STAGES = 4;
+constexpr int DW_STAGES16 = 6;  // dW with a bf16 G: 24 KB stages, two more in flight
 constexpr int DW_MT = 2;    // 128-row i-tiles per dW CTA
 constexpr int DW_KR = 16;   // graph rows per dW k-block
 constexpr int MODE_FWD = 0, MODE_DX = 1, MODE_DW = 2;
@@ -311,7 +312,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_tma_gemm(const __grid_constant_
   // most two tiles ahead of the epilogue, so 8 slots are never overrun.
 
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
-  constexpr int S = MODE == MODE_DW ? DW_STAGES : PAIR ? PAIR_STAGES : FWD_STAGES;
+  const int S = MODE == MODE_DW ? (p.g16 ? DW_STAGES16 : DW_STAGES) : PAIR ? PAIR_STAGES : FWD_STAGES;
   constexpr int MT = MODE == MODE_DW ? DW_MT : 1;
   const int BN = p.BN;
   const uint32_t crank = PAIR ? cluster_rank() : 0u;
@@ -1185,7 +1186,7 @@ struct Arena {
 static Arena g_img;
 
 static size_t smem_bytes(int mode, int BN, int mask, int nwp, bool pair = false, int g16 = 0) {
-  const int S = mode == MODE_DW ? DW_STAGES : pair ? PAIR_STAGES : FWD_STAGES;
+  const int S = mode == MODE_DW ? (g16 ? DW_STAGES16 : DW_STAGES) : pair ? PAIR_STAGES : FWD_STAGES;
   const int a = mode == MODE_DW ? DW_MT * DW_KR * BM * 4 : BM * BKB;
   const int b = mode == MODE_DW ? DW_KR * BN * (g16 ? 2 : 4) + (mask ? DW_KR * nwp * 4 : 0) : (pair ? BN / 2 : BN) * BKB;
   const int k = mode == MODE_DW ? 2 * (DW_MT * BM + BN) * 64 : NE * 4096 * (pair ? PAIR_OB : 1);

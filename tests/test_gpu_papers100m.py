@@ -27,7 +27,7 @@ from oracle.sampler import Block
 from synth import BASE_RNG_SEED, CONFIGS, epoch_seeds, init_weights
 from synth.store import shared_graph
 
-from gpu_util import assert_close_cond, blocks_to_host, lib, read_f32, read_i32
+from gpu_util import assert_close_cond, blocks_to_host, lib, read_bf16, read_f32, read_i32
 
 pytestmark = [
     pytest.mark.gpu,
@@ -77,7 +77,8 @@ def test_papers100m_batch_bit_exact():
     # feature rows of the sampled neighbours (read by the GPU from the table)
     L = len(cfg["fanouts"])
     nd, ns, ptr, idx, Fg = hb[L - 1]
-    n_keep = hb[L - 2][0] if tr.l2push() else nd  # fused L2 push: H^1 stored for layer 2's dst prefix only
+    # the fp32 H^1 holds layer 2's dst prefix only (bf16 intermediates, reading Q30)
+    n_keep = hb[L - 2][0] if (tr.l2push() or tr.bf16act()) else nd
     rows = np.sort(np.random.default_rng(0).choice(n_keep, 2048, replace=False))
     cnt = np.diff(ptr)[rows]
     nbr = np.concatenate([idx[ptr[r]:ptr[r + 1]] for r in rows])
@@ -90,4 +91,17 @@ def test_papers100m_batch_bit_exact():
     p1, s1 = tr.activation(1)
     H1 = read_f32(p1, n_keep, s1)[rows, : dims[1]]
     assert_close_cond(H1, Ho, Hm, 4e-3, "papers100m layer 1 (sampled rows)")
+    if tr.bf16act():  # the bf16 copy of H^1 (every row): layer 1 plus bf16 rounding, on rows beyond the prefix too
+        rows = np.sort(np.random.default_rng(1).choice(nd, 2048, replace=False))
+        cnt = np.diff(ptr)[rows]
+        nbr = np.concatenate([idx[ptr[r]:ptr[r + 1]] for r in rows])
+        blk = Block(n_dst=len(rows), n_src=len(rows) + nbr.size,
+                    indptr=np.concatenate([[0], np.cumsum(cnt)]).astype(np.int64),
+                    indices=(len(rows) + np.arange(nbr.size)).astype(np.int64), src_global=None)
+        Hs = oracle.gather_rows(gd.feats, np.concatenate([Fg[rows], Fg[nbr]]))[:, : gd.d]
+        Ho, _ = layer_fwd(blk, Hs, W1, b1, True)
+        Hm, _ = layer_fwd(blk, Hs, W1, b1, True, absval=True)
+        p16, ld16 = tr.activation16(1)
+        H16 = read_bf16(p16, nd, ld16)[rows, : dims[1]]
+        assert_close_cond(H16, Ho, (4e-3 + 2.0 ** -8) / 4e-3 * Hm, 4e-3, "papers100m bf16 copy of layer 1")
     print(f"papers100m: frontiers {[len(f) for f in F]}, edges {[b.nnz for b in blocks]}, loss {loss:.5f}")

@@ -444,8 +444,8 @@ def test_layer_shapes(mini, prec, d_in, d_out, kind):
 
 def test_pipelined_steps_match_sequential(mini):
     """Eq.4 pipeline: prefetching sample+gather of step t+1 on the side stream
-    changes nothing in the results (losses bitwise, parameters to fp32
-    rounding of the atomic backward)."""
+    changes nothing in the results (the first loss bitwise, the rest and the
+    parameters to the rounding of the atomic backward)."""
     gd, g = mini
     cfg = CONFIGS["mini"]
     dims = [gd.d, cfg["hidden"], cfg["hidden"], gd.C]
@@ -465,8 +465,12 @@ def test_pipelined_steps_match_sequential(mini):
             pip.prefetch(batches[i + 1], B, 101 + i)
         l_pip.append(pip.read_loss())
     assert l_seq[0] == l_pip[0]
-    np.testing.assert_allclose(l_pip, l_seq, rtol=1e-5)
-    assert normwise(pip.params(), seq.params()) < 1e-5
+    # later steps differ by the atomic summation order of the backward's
+    # repeated src ids: fp32 rounding, or bf16 rounding for the tf32
+    # trainer's bf16 dL/dH^1 (reading Q30)
+    bf16 = seq.bf16act()
+    np.testing.assert_allclose(l_pip, l_seq, rtol=1e-4 if bf16 else 1e-5)
+    assert normwise(pip.params(), seq.params()) < (5e-4 if bf16 else 1e-5)
     with pytest.raises(gnnv.GnnvError):  # one pending prefetch at a time
         pip.prefetch(batches[0], B, 7)
         pip.prefetch(batches[1], B, 8)
@@ -670,10 +674,12 @@ def test_async_loss_readback(mini):
     cache = gnnv.Cache(g, 0.3)
     a = gnnv.Trainer(g, cache, dims, cfg["fanouts"], B, init_weights(dims), prec=2)
     b = gnnv.Trainer(g, cache, dims, cfg["fanouts"], B, init_weights(dims), prec=2)
-    sync = [a.step(perm[i * B:(i + 1) * B], B, B, 50 + i, 0.01)[0] for i in range(10)]
+    # lr 0: every step's loss is then a deterministic function of its batch
+    # (the backward's atomic order cannot reach the next step's weights)
+    sync = [a.step(perm[i * B:(i + 1) * B], B, B, 50 + i, 0.0)[0] for i in range(10)]
     tickets = []
     for i in range(10):
-        b.step(perm[i * B:(i + 1) * B], B, B, 50 + i, 0.01, want_loss=False)
+        b.step(perm[i * B:(i + 1) * B], B, B, 50 + i, 0.0, want_loss=False)
         tickets.append(b.loss_async())
     got = [b.loss_result(t) for t in tickets[-8:]]
     assert got == sync[-8:]
@@ -723,6 +729,7 @@ def test_step_whole_table_gather4(mini, option):
     seeds = epoch_seeds(gd.n, 0)[: cfg["batch"]]
     out = {}
     option("GNNV_XROWS", 1)  # read when a trainer is created
+    option("GNNV_NO_BF16ACT", 1)  # fp32 intermediates: the two paths then agree to fp32 atomic rounding
     for name, ratio in (("rows", 1.0), ("copy", (gd.n - 1) / gd.n)):
         tr = gnnv.Trainer(g, gnnv.Cache(g, ratio), dims, cfg["fanouts"], cfg["batch"], w, prec=gnnv.PREC_TF32)
         loss, _ = tr.step(seeds, len(seeds), len(seeds), 0x5EED, 0.05)
