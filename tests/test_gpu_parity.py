@@ -491,8 +491,8 @@ def test_pipelined_steps_match_sequential(mini):
         if i + 1 < len(batches):
             dv.prefetch(dev[(i + 1) * B:(i + 2) * B].data_ptr(), B, 101 + i, on_host=False, stream=pf)
         losses.append(dv.read_loss(stream=main))
-    np.testing.assert_allclose(losses, l_seq, rtol=1e-5)
-    assert normwise(dv.params(), seq.params()) < 1e-5
+    np.testing.assert_allclose(losses, l_seq, rtol=1e-4 if bf16 else 1e-5)
+    assert normwise(dv.params(), seq.params()) < (5e-4 if bf16 else 1e-5)
 
 
 # ------------------------------------------- locality-biased sampling (NEXT-2)
@@ -720,7 +720,7 @@ def test_step_whole_table_gather4(mini, option):
     reads exactly the values the materialised path reads, in the same order,
     (GNNV_XROWS=1), so the loss equals bit for bit that of the same step with X materialised
     (a cache one row short of the table: ratio (N-1)/N); the gradients match
-    it to the dW kernel's atomic summation order.  Both match the oracle."""
+    it to the backward's atomic summation order.  Both match the oracle."""
     gd, g = mini
     cfg = CONFIGS["mini"]
     dims = [gd.d, cfg["hidden"], cfg["hidden"], gd.C]
@@ -736,7 +736,7 @@ def test_step_whole_table_gather4(mini, option):
         out[name] = (loss, tr.grads(), tr.x_level(), tr)
     assert out["rows"][2] == -1 and out["copy"][2] == L
     assert out["rows"][0] == out["copy"][0], (out["rows"][0], out["copy"][0])
-    assert normwise(out["rows"][1], out["copy"][1]) < 1e-6
+    assert normwise(out["rows"][1], out["copy"][1]) < 2e-5  # fp32 atomic-order rounding of the backward
     ref = train_step(gd.indptr, gd.indices, gd.feats, gd.d, gd.labels, seeds, cfg["fanouts"], 0x5EED, w, 0.05)
     assert abs(out["rows"][0] - ref["loss"]) <= 5e-3 * abs(ref["loss"])
     tr = out["rows"][3]
