@@ -102,10 +102,10 @@ const char* gnnv_last_error(void);
 /* Opt-in variants, by name (each measured slower than, or equal to, the
  * default on the products workload): GNNV_XROWS,
  * GNNV_GEMM_PAIR, GNNV_BWD_PULL, GNNV_NO_TAIL, GNNV_NO_PDL, GNNV_L2PUSH,
- * GNNV_LASTUSE, GNNV_STATIC_TILES, GNNV_PF_AGG, GNNV_NO_BF16ACT.
+ * GNNV_LASTUSE, GNNV_STATIC_TILES, GNNV_PF_AGG, GNNV_NO_BF16ACT, GNNV_NO_BF16TABLE.
  * value 1 = on, 0 = off, -1 = back to the environment variable of the same
  * name (read once per process; set and not "0" = on).  Takes effect for
- * trainers / blocks created (XROWS, NO_TAIL, BWD_PULL, L2PUSH, LASTUSE, PF_AGG, NO_BF16ACT) or
+ * trainers / blocks created (XROWS, NO_TAIL, BWD_PULL, L2PUSH, LASTUSE, PF_AGG, NO_BF16ACT, NO_BF16TABLE) or
  * kernels launched (GEMM_PAIR, NO_PDL, STATIC_TILES) afterwards.  PARAM on an unknown
  * name.  Process-wide; not for concurrent use with running steps. */
 gnnv_status gnnv_set_option(const char* name, int32_t value);

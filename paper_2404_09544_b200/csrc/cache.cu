@@ -23,6 +23,8 @@
 #include <cub/device/device_select.cuh>
 #include <cub/iterator/counting_input_iterator.cuh>
 
+#include <cuda_bf16.h>
+
 #include "common.cuh"
 
 namespace gnnv {
@@ -246,6 +248,31 @@ __global__ void k_dyn_close(int64_t* ctr, const int32_t* sizes, int L, int64_t C
   }
 }
 
+// bf16 copy of the local table: row r = bf16(table row r), zero-padded to ld16
+__global__ void k_table_bf16(const float* __restrict__ src, int32_t stride, int32_t d, int64_t rows,
+                             __nv_bfloat16* __restrict__ dst, int32_t ld16) {
+  const int64_t total = rows * ld16;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = t / ld16;
+    const int c = (int)(t - r * ld16);
+    dst[t] = __float2bfloat16_rn(c < d ? src[r * stride + c] : 0.f);
+  }
+}
+
+void cache_bf16_table(gnnv_cache* c) {
+  if (c->d_table16) return;
+  GNNV_REQUIRE(c->world == 1 && c->shards.size() == 1 && c->shards[0] && !c->dynamic, GNNV_ERR_STATE,
+               "cache_bf16_table: a single static local table is required");
+  const gnnv_graph* g = c->g;
+  c->table16_ld = (g->d + 7) / 8 * 8;
+  const int64_t rows = c->local_rows;
+  c->d_table16 = dmalloc((size_t)std::max<int64_t>(rows, 1) * c->table16_ld * 2, "bf16 feature table");
+  k_table_bf16<<<num_sms() * 16, 256>>>(c->shards[0], g->stride, g->d, rows, static_cast<__nv_bfloat16*>(c->d_table16),
+                                        c->table16_ld);
+  GNNV_CHECK_LAUNCH();
+  GNNV_TRY_CUDA(cudaDeviceSynchronize());
+}
+
 void launch_cache_update(gnnv_cache* c, const gnnv_blocks* b, const float* d_X, cudaStream_t s) {
   const int L = b->L;
   const int64_t cap = b->max_n[L];
@@ -444,6 +471,7 @@ gnnv_status gnnv_cache_free(gnnv_cache* c) {
   dfree(c->d_mflag);
   dfree(c->d_sel_tmp);
   dfree(c->d_ctr);
+  dfree(c->d_table16);
   delete c;
   return GNNV_OK;
 }

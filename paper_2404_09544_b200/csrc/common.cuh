@@ -152,6 +152,11 @@ struct gnnv_cache {
   std::vector<bool> shard_owned;
   std::vector<bool> shard_ipc;
   const float** d_shard_ptrs = nullptr;  // device array [world]
+  // bf16 copy of the whole local table (cache_bf16_table; the tf32 trainer's
+  // layer-1 aggregation reads it -- reading Q31), row stride table16_ld
+  // elements (d rounded up to 8, zero-padded); NULL until requested
+  void* d_table16 = nullptr;
+  int32_t table16_ld = 0;
   bool peers_ready = true;               // SHARDED: every peer's shard mapped
   // NEXT-3 dynamic cache (policy FIFO / LRU): starts empty, the misses of
   // every batch are admitted by gnnv_cache_update (cache.cu)
@@ -266,6 +271,8 @@ void blocks_enable_lastuse(gnnv_blocks* b);
 void blocks_enable_owner_rows(gnnv_blocks* b, int h);  // + CSC of hop h's non-owner edges
 // cache.cu
 void launch_cache_update(gnnv_cache* c, const gnnv_blocks* b, const float* d_X, cudaStream_t s);
+// builds c->d_table16 from the local table (setup path; synchronises)
+void cache_bf16_table(gnnv_cache* c);
 void launch_gather(const gnnv_cache* c, const gnnv_blocks* b, float* d_X, int64_t* d_stats, cudaStream_t s,
                    int32_t* d_rowidx = nullptr, bool materialize = true);
 // spmm.cu
@@ -277,9 +284,10 @@ void launch_spmm_bwd(const int32_t* d_indptr, const int32_t* d_indices, const ui
                      int64_t max_dst, const float* dA, int32_t lda, void* dH, int32_t ldh, int32_t d, int32_t kind,
                      int32_t aggr, const uint32_t* bits, int32_t bits_ld, cudaStream_t s, bool dh_bf16 = false);
 // the forward aggregation over bf16 source rows (stride ld16 elements)
+// rowidx != NULL: source row u is row rowidx[u] of H16 (the bf16 table)
 void launch_spmm_fwd_h16(const int32_t* d_indptr, const int32_t* d_indices, const int32_t* d_ndst, int64_t max_dst,
                          const void* H16, int32_t ld16, float* A, int32_t lda, int32_t d, int32_t kind, int32_t aggr,
-                         cudaStream_t s);
+                         cudaStream_t s, const int32_t* rowidx = nullptr);
 // the same transposed aggregation pulled per src row (rows up to
 // kPullMaxLd floats; wider ones keep the push) through the block's
 // CSC (one coalesced store per dH row, no atomics; see k_spmm_bwd_pull)
@@ -354,6 +362,7 @@ struct Bf16Io {
   const int32_t* keep_rows = nullptr;  // fwd: fp32 output rows kept
   const void* src16 = nullptr;     // fwd: aggregate from this bf16 copy of H_src
   int32_t src16_ld = 0;
+  const int32_t* src16_rows = nullptr;  // fwd: source row u is row src16_rows[u] of src16 (the bf16 table)
   void* gsrc16 = nullptr;          // bwd: dH_src produced as bf16 (stride gsrc16_ld)
   int32_t gsrc16_ld = 0;
   const void* gdst16 = nullptr;    // bwd: this layer's G read as bf16 (stride gdst16_ld)

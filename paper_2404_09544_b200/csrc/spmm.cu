@@ -482,16 +482,16 @@ __device__ __forceinline__ void add_bf16x8(float* acc, uint4 q) {
     acc[2 * k + 1] += __uint_as_float(w[k] & 0xFFFF0000u);
   }
 }
-template <int LPR>
+template <int LPR, bool IND>
 __global__ void __launch_bounds__(256) k_spmm_fwd_h16(const int32_t* __restrict__ indptr,
                                                       const int32_t* __restrict__ indices, const int32_t* d_ndst,
                                                       const __nv_bfloat16* __restrict__ H, int32_t ld16,
                                                       float* __restrict__ A, int32_t lda, int32_t d, int32_t kind,
-                                                      int32_t aggr) {
+                                                      int32_t aggr, const int32_t* __restrict__ rowidx) {
   GNNV_PDL_ENTRY();
   constexpr int RPW = 32 / LPR;
   const int n = *d_ndst;
-  const int vec8 = d >> 3;
+  const int vec8 = (d + 7) >> 3;  // 8-element units; elements >= d are zero in H
   const int lane = threadIdx.x & 31, sub = lane / LPR, sl = lane % LPR;
   const unsigned smask = (LPR == 32) ? 0xffffffffu : (((1u << LPR) - 1u) << (sub * LPR));
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -507,9 +507,11 @@ __global__ void __launch_bounds__(256) k_spmm_fwd_h16(const int32_t* __restrict_
       const int c = c0 + sl;
       const bool cok = active && c < vec8;
       float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-      if (kind == GNNV_KIND_GCN && cok) add_bf16x8(acc, __ldg(H8 + (int64_t)row * ld8 + c));
+      if (kind == GNNV_KIND_GCN && cok)
+        add_bf16x8(acc, __ldg(H8 + (int64_t)(IND ? __ldg(rowidx + row) : row) * ld8 + c));
       for (int e0 = 0; e0 < cnt; e0 += LPR) {
-        const int my = (e0 + sl < cnt) ? __ldg(indices + beg + e0 + sl) : 0;
+        int my = (e0 + sl < cnt) ? __ldg(indices + beg + e0 + sl) : 0;
+        if (IND) my = __ldg(rowidx + my);
         const int m = min(LPR, cnt - e0);
         int j = 0;
         for (; j + 4 <= m; j += 4) {
@@ -537,7 +539,7 @@ __global__ void __launch_bounds__(256) k_spmm_fwd_h16(const int32_t* __restrict_
         }
         float4* out = reinterpret_cast<float4*>(A) + (int64_t)row * lda4 + 2 * c;
         out[0] = make_float4(acc[0], acc[1], acc[2], acc[3]);
-        out[1] = make_float4(acc[4], acc[5], acc[6], acc[7]);
+        if (2 * c + 1 < lda4) out[1] = make_float4(acc[4], acc[5], acc[6], acc[7]);
       }
     }
     if (active)  // padding float4s of the output row
@@ -548,19 +550,24 @@ __global__ void __launch_bounds__(256) k_spmm_fwd_h16(const int32_t* __restrict_
 
 void launch_spmm_fwd_h16(const int32_t* d_indptr, const int32_t* d_indices, const int32_t* d_ndst, int64_t max_dst,
                          const void* H16, int32_t ld16, float* A, int32_t lda, int32_t d, int32_t kind, int32_t aggr,
-                         cudaStream_t s) {
-  GNNV_REQUIRE(d % 8 == 0 && ld16 % 8 == 0, GNNV_ERR_UNSUPPORTED, "spmm_fwd_h16: d and the row stride must be multiples of 8");
-  const int vec8 = d / 8;
+                         cudaStream_t s, const int32_t* rowidx) {
+  const int vec8 = (d + 7) / 8;
+  GNNV_REQUIRE(ld16 % 8 == 0 && ld16 >= 8 * vec8 && lda % 4 == 0, GNNV_ERR_UNSUPPORTED,
+               "spmm_fwd_h16: the bf16 row stride must be a multiple of 8 covering d");
   const __nv_bfloat16* H = static_cast<const __nv_bfloat16*>(H16);
-  if (vec8 <= 8)
-    launch_k(k_spmm_fwd_h16<8>, spmm_grid(max_dst, 4), 256, 0, s, d_indptr, d_indices, d_ndst, H, ld16, A, lda, d, kind,
-             aggr);
-  else if (vec8 <= 16)
-    launch_k(k_spmm_fwd_h16<16>, spmm_grid(max_dst, 2), 256, 0, s, d_indptr, d_indices, d_ndst, H, ld16, A, lda, d, kind,
-             aggr);
-  else
-    launch_k(k_spmm_fwd_h16<32>, spmm_grid(max_dst, 1), 256, 0, s, d_indptr, d_indices, d_ndst, H, ld16, A, lda, d, kind,
-             aggr);
+#define GNNV_H16(LPR, RPWv)                                                                                          \
+  do {                                                                                                               \
+    if (rowidx)                                                                                                      \
+      launch_k(k_spmm_fwd_h16<LPR, true>, spmm_grid(max_dst, RPWv), 256, 0, s, d_indptr, d_indices, d_ndst, H, ld16, \
+               A, lda, d, kind, aggr, rowidx);                                                                       \
+    else                                                                                                             \
+      launch_k(k_spmm_fwd_h16<LPR, false>, spmm_grid(max_dst, RPWv), 256, 0, s, d_indptr, d_indices, d_ndst, H,      \
+               ld16, A, lda, d, kind, aggr, (const int32_t*)nullptr);                                                \
+  } while (0)
+  if (vec8 <= 8) GNNV_H16(8, 4);
+  else if (vec8 <= 16) GNNV_H16(16, 2);
+  else GNNV_H16(32, 1);
+#undef GNNV_H16
   GNNV_CHECK_LAUNCH();
 }
 

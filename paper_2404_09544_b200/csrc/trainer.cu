@@ -82,6 +82,9 @@ struct gnnv_trainer {
   // next layer's aggregation and by layer i's dW -- as bf16 (H16[i], G16[i],
   // row stride ld16[i]); H[i] fp32 then holds only layer i+1's dst prefix
   bool bf16act = false;
+  // whole-table TF32 SAGE: the layer-1 aggregation reads the cache's bf16
+  // copy of the table (reading Q31; GNNV_NO_BF16TABLE=1: the fp32 table)
+  bool table16 = false;
   void* H16[GNNV_MAX_LAYERS + 1] = {nullptr};
   void* G16[GNNV_MAX_LAYERS + 1] = {nullptr};
   int32_t ld16[GNNV_MAX_LAYERS + 1] = {0};
@@ -284,6 +287,10 @@ gnnv_status gnnv_trainer_create(gnnv_graph* g, gnnv_cache* c, const gnnv_model_d
           t->H16[i] = dmalloc(bytes, "bf16 activations");
           t->G16[i] = dmalloc(bytes, "bf16 activation gradients");
         }
+      // layer 1 aggregates a bf16 copy of the whole-table cache (reading Q31)
+      t->table16 = t->x_fused && md->prec == GNNV_PREC_TF32 && md->kind == GNNV_KIND_SAGE &&
+                   !env_on("GNNV_NO_BF16TABLE");
+      if (t->table16) cache_bf16_table(c);
       t->l2push = !t->bf16act && md->prec == GNNV_PREC_TF32 && md->kind == GNNV_KIND_SAGE && L >= 3 &&
                   env_on("GNNV_L2PUSH");
       if (t->l2push)
@@ -603,10 +610,15 @@ gnnv_status gnnv_trainer_prefetch(gnnv_trainer* t, const int32_t* seeds, int32_t
       if (tl) tl->mark(t->side, "pf_spmm_fwd.l1");
       const int L = t->md.L, h = L - 1;
       gnnv_blocks* bk = t->bb[k];
-      launch_spmm_fwd(bk->d_indptr[h], bk->d_indices[h], bk->d_sizes + h, bk->max_n[h],
-                      t->x_fused ? t->table : t->X[k], g->stride, t->A1b[k], row_stride(t->md.dims[0]),
-                      t->md.dims[0], t->md.kind, t->md.aggr, t->side, t->x_fused ? t->rowidx[k] : nullptr,
-                      bk->d_lastv);
+      if (t->table16)
+        launch_spmm_fwd_h16(bk->d_indptr[h], bk->d_indices[h], bk->d_sizes + h, bk->max_n[h], t->c->d_table16,
+                            t->c->table16_ld, t->A1b[k], row_stride(t->md.dims[0]), t->md.dims[0], t->md.kind,
+                            t->md.aggr, t->side, t->rowidx[k]);
+      else
+        launch_spmm_fwd(bk->d_indptr[h], bk->d_indices[h], bk->d_sizes + h, bk->max_n[h],
+                        t->x_fused ? t->table : t->X[k], g->stride, t->A1b[k], row_stride(t->md.dims[0]),
+                        t->md.dims[0], t->md.kind, t->md.aggr, t->side, t->x_fused ? t->rowidx[k] : nullptr,
+                        bk->d_lastv);
     }
 
     if (tl) tl->mark(t->side, "end");
@@ -688,6 +700,11 @@ gnnv_status gnnv_step(gnnv_trainer* t, const int32_t* seeds, int32_t n_seeds, in
                        t->md.aggr == GNNV_AGGR_MEAN, b->d_sizes + hn, b->d_owner_row[hn]};
       }
       Bf16Io io{};
+      if (i == 1 && t->table16) {
+        io.src16 = t->c->d_table16;
+        io.src16_ld = t->c->table16_ld;
+        io.src16_rows = t->rowidx[t->cur];
+      }
       if (t->bf16act) {
         if (i <= L - 2) {  // this layer's output: a bf16 copy, fp32 rows for the next dst prefix
           io.y16 = t->H16[i];
@@ -702,7 +719,8 @@ gnnv_status gnnv_step(gnnv_trainer* t, const int32_t* seeds, int32_t n_seeds, in
       layer_fwd_impl(b, i, &ld, t->H[i - 1], t->d_params + t->w_off[i - 1], t->d_params + t->b_off[i - 1], t->H[i],
                      t->A[i], s, tl, t->mbits[i], t->table, i == 1 ? t->rowidx[t->cur] : nullptr,
                      i == 1 ? xr1 : nullptr, do_push ? &push : nullptr,
-                     (t->l2push && i >= 2 && i <= L - 1) || (i == 1 && agg1_ready), t->bf16act ? &io : nullptr);
+                     (t->l2push && i >= 2 && i <= L - 1) || (i == 1 && agg1_ready),
+                     (t->bf16act || t->table16) ? &io : nullptr);
     }
     if (tm) GNNV_TRY_CUDA(cudaEventRecord(t->ev[3], s));
     float* d_loss = t->d_grads + t->nparams;
