@@ -730,6 +730,7 @@ def test_step_whole_table_gather4(mini, option):
     out = {}
     option("GNNV_XROWS", 1)  # read when a trainer is created
     option("GNNV_NO_BF16ACT", 1)  # fp32 intermediates: the two paths then agree to fp32 atomic rounding
+    option("GNNV_NO_BF16TABLE", 1)  # and the whole-table path aggregates the fp32 table, as X's copy does
     for name, ratio in (("rows", 1.0), ("copy", (gd.n - 1) / gd.n)):
         tr = gnnv.Trainer(g, gnnv.Cache(g, ratio), dims, cfg["fanouts"], cfg["batch"], w, prec=gnnv.PREC_TF32)
         loss, _ = tr.step(seeds, len(seeds), len(seeds), 0x5EED, 0.05)
