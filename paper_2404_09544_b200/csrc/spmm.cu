@@ -483,7 +483,7 @@ __device__ __forceinline__ void add_bf16x8(float* acc, uint4 q) {
   }
 }
 template <int LPR, bool IND>
-__global__ void __launch_bounds__(256) k_spmm_fwd_h16(const int32_t* __restrict__ indptr,
+__global__ void __launch_bounds__(256, 8) k_spmm_fwd_h16(const int32_t* __restrict__ indptr,
                                                       const int32_t* __restrict__ indices, const int32_t* d_ndst,
                                                       const __nv_bfloat16* __restrict__ H, int32_t ld16,
                                                       float* __restrict__ A, int32_t lda, int32_t d, int32_t kind,
