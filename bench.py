@@ -394,14 +394,20 @@ def algorithmic(seg: str, sizes, cfg, dims, stride, prec, peaks):
     h = L - i
     d_in, d_out = dims[i - 1], dims[i]
     K = 2 * d_in
+    # bytes per element of what the step actually stores (reading Q30/Q31):
+    # the layer-1 aggregation reads the bf16 table, the hidden H^j / dL/dH^j
+    # (j <= L-2) are bf16
+    b16 = sizes.get("bf16act", False)
+    src_b = 2 if (i == 1 and sizes.get("table16", False)) or (b16 and 2 <= i <= L - 1) else 4
     if name == "spmm_fwd":
-        by = U[h] * d_in * 4 + n[h] * ((d_in + 3) & ~3) * 4 + nnz[h] * 4 + (n[h] + 1) * 4
+        by = U[h] * d_in * src_b + n[h] * ((d_in + 3) & ~3) * 4 + nnz[h] * 4 + (n[h] + 1) * 4
         return "hbm", by, "GB/s", peaks["hbm"]
     if name == "spmm_bwd":
         # dA read, block CSR + owner masks read, every dH_src row written once,
         # and the n_dst rows the dX GEMM wrote read back for accumulation
         ld = (d_in + 3) & ~3
-        by = n[h] * d_in * 4 + nnz[h] * 4 + (n[h] + 1) * 8 + n[h + 1] * ld * 4 + n[h] * ld * 4
+        gb = 2 if (b16 and i - 1 <= L - 2) else 4
+        by = n[h] * d_in * 4 + nnz[h] * 4 + (n[h] + 1) * 8 + n[h + 1] * ld * gb + n[h] * ld * gb
         return "hbm", by, "GB/s", peaks["hbm"]
     if name in ("tail_a", "tail_b"):
         # fused output layer (tail.cu).  a: self + sampled neighbour rows of
@@ -420,15 +426,16 @@ def algorithmic(seg: str, sizes, cfg, dims, stride, prec, peaks):
     if name == "relu_mask":
         return "hbm", 3 * n[h] * ((d_out + 3) & ~3) * 4, "GB/s", peaks["hbm"]
     ld_in, ld_out = (d_in + 3) & ~3, (d_out + 3) & ~3
+    out16 = b16 and i <= L - 2  # H^i (and dL/dH^i) kept as bf16, fp32 rows only for the next dst prefix
     if name == "gemm_fwd":
         fl = 2.0 * n[h] * K * d_out
-        by = n[h] * K * 4 + n[h] * ld_out * 4
+        by = n[h] * K * 4 + (n[h] * ld_out * 2 + n[h - 1] * ld_out * 4 if out16 else n[h] * ld_out * 4)
     elif name == "gemm_dx":
         fl = 2.0 * n[h] * K * d_out
-        by = n[h] * d_out * 4 + n[h] * 2 * ld_in * 4
+        by = n[h] * d_out * 4 + n[h] * ld_in * (2 if b16 and i - 1 <= L - 2 else 4) + n[h] * ld_in * 4
     elif name == "gemm_dw":
         fl = 2.0 * n[h] * (K + 1) * d_out
-        by = n[h] * K * 4 + n[h] * d_out * 4
+        by = n[h] * K * 4 + n[h] * d_out * (2 if out16 else 4)
     else:
         return None
     if prec == "fp32":
@@ -491,6 +498,7 @@ def main():
     tr = gnnv.Trainer(g, cache, dims, cfg["fanouts"], B, w, kind=kind, prec=prec, comm=comm)
     tr.set_locality(args.locality_bias)
     bf16act = tr.bf16act()  # TF32 SAGE, L >= 3: the hidden H^i / dL/dH^i kept as bf16 (reading Q30)
+    bf16tab = tr.table16()  # whole-table TF32 SAGE: layer 1 aggregates a bf16 copy of the table (reading Q31)
     # the step runs on a high-priority stream; the trainer's prefetch stream
     # has the lowest priority (Eq.4 overlap without delaying the step)
     stream = torch.cuda.Stream(priority=int(os.environ.get("GNNV_STEP_PRIO", "-1")))
@@ -669,6 +677,8 @@ def main():
         acc["misses"] += nL - hit
     sizes = {k: (v / nsz) for k, v in acc.items()}
     sizes["x_level"] = tr.x_level()
+    sizes["bf16act"] = tr.bf16act()
+    sizes["table16"] = tr.table16()
     peaks = load_peaks()
     if sizes["misses"] > 0:
         peaks["host"] = measure_host_link()
@@ -707,7 +717,8 @@ def main():
             i = int(name.split(".l")[1])
             h = len(cfg["fanouts"]) - i
             d_in = dims[i - 1]
-            ev = sizes["nnz"][h] * d_in * 4 + sizes["n"][h] * ((d_in + 3) & ~3) * 4
+            eb = 2 if (i == 1 and sizes["table16"]) or (sizes["bf16act"] and 2 <= i <= L - 1) else 4
+            ev = sizes["nnz"][h] * d_in * eb + sizes["n"][h] * ((d_in + 3) & ~3) * 4
             r["edge_visit_bytes"] = ev
             r["edge_visit_frac"] = ev / (avg_ms / 1000.0) / 1e9 / peaks["hbm"]
         rooflines[name] = r
@@ -778,11 +789,11 @@ def main():
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": {"fp32": "f32", "bf16": "f32+bf16gemm", "tf32": "f32+tf32gemm"}[args.prec] + (
-                "+bf16act" if bf16act else ""), "data": "synthetic",
+                "+bf16act" if bf16act else "") + ("+bf16table" if bf16tab else ""), "data": "synthetic",
             "config": config_of(cfg, gd, world, args.kind),
             "settings": {"placement": args.placement, "locality_bias": args.locality_bias,
                          "cache_policy": args.policy, "gemm_precision": args.prec,
-                         "bf16_intermediates": bf16act,
+                         "bf16_intermediates": bf16act, "bf16_table_layer1": tr.table16(),
                          "gathered_x_mb_per_step": sizes["n"][L] * gd.stride * 4 / 1e6,
                          "pipeline": "eq4-overlap (next batch sample+gather on a side stream)" if pipeline else "off"},
             "step_stats": step_stats,

@@ -413,6 +413,10 @@ int32_t gnnv_trainer_l2push(const gnnv_trainer* t);
  * next layer's dst prefix (as with gnnv_trainer_l2push), and dL/dH^i is
  * produced and consumed as bf16. */
 int32_t gnnv_trainer_bf16act(const gnnv_trainer* t);
+/* 1 if layer 1 aggregates the cache's bf16 copy of the whole table (TF32
+ * SAGE with the whole table on this device, unless GNNV_NO_BF16TABLE;
+ * reading Q31).  The exact fp32 rows are still what gnnv_gather copies. */
+int32_t gnnv_trainer_table16(const gnnv_trainer* t);
 /* The bf16 copy of H^i (1..L-2) of the last step: [rows x *ld] bf16
  * (borrowed device pointer), NULL and 0 when the trainer keeps none. */
 gnnv_status gnnv_trainer_activation16(gnnv_trainer* t, int32_t i, const void** d_H16, int32_t* ld);

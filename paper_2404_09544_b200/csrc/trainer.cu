@@ -393,6 +393,7 @@ gnnv_status gnnv_trainer_relu_bits(gnnv_trainer* t, int32_t i, const uint32_t** 
 
 int32_t gnnv_trainer_l2push(const gnnv_trainer* t) { return t && t->l2push ? 1 : 0; }
 int32_t gnnv_trainer_bf16act(const gnnv_trainer* t) { return t && t->bf16act ? 1 : 0; }
+int32_t gnnv_trainer_table16(const gnnv_trainer* t) { return t && t->table16 ? 1 : 0; }
 
 gnnv_status gnnv_trainer_activation16(gnnv_trainer* t, int32_t i, const void** d_H16, int32_t* ld) {
   return guarded([&] {

@@ -132,6 +132,7 @@ _SIGS = {
     "gnnv_trainer_relu_bits": (I32, [VP, I32, PP, C.POINTER(I32)]),
     "gnnv_trainer_l2push": (I32, [VP]),
     "gnnv_trainer_bf16act": (I32, [VP]),
+    "gnnv_trainer_table16": (I32, [VP]),
     "gnnv_trainer_activation16": (I32, [VP, I32, PP, C.POINTER(I32)]),
     "gnnv_step": (I32, [VP, VP, I32, I32, I32, U64, F32, C.POINTER(F32), C.POINTER(StepTiming), VP]),
     "gnnv_trainer_stats": (I32, [VP, VP]),
@@ -571,6 +572,9 @@ class Trainer:
 
     def bf16act(self) -> bool:
         return bool(load().gnnv_trainer_bf16act(self.h))
+
+    def table16(self) -> bool:
+        return bool(load().gnnv_trainer_table16(self.h))
 
     def activation16(self, i: int):
         """(device pointer, row stride) of the bf16 copy of H^i, or (0, 0)."""

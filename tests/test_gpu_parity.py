@@ -830,6 +830,40 @@ def test_bf16_intermediates(mini, option, ratio):
             assert cos > 0.999, cos
 
 
+def test_bf16_table_layer1_aggregation(mini, option):
+    """Whole table cached, tf32 SAGE: layer 1 aggregates the cache's bf16
+    copy of the table (reading Q31; the gathered rows stay the exact fp32
+    ones).  A^1 against the fp32 aggregation of the bf16-rounded feature
+    rows (1e-5) and of the exact rows (bf16 rounding, 2^-8 of |.|); the
+    step's loss within 1e-3 of the fp32-table step."""
+    gd, g = mini
+    cfg = CONFIGS["mini"]
+    dims = [gd.d, cfg["hidden"], cfg["hidden"], gd.C]
+    L = len(cfg["fanouts"])
+    w = init_weights(dims)
+    seeds = epoch_seeds(gd.n, 0)[: cfg["batch"]]
+    B = len(seeds)
+    losses = {}
+    for name in ("bf16", "fp32"):
+        option("GNNV_NO_BF16TABLE", 0 if name == "bf16" else 1)
+        tr = gnnv.Trainer(g, gnnv.Cache(g, 1.0), dims, cfg["fanouts"], B, w, prec=gnnv.PREC_TF32)
+        assert tr.table16() == (name == "bf16")
+        losses[name], _ = tr.step(seeds, B, B, 0x5EED, 0.0)
+        if name == "bf16":
+            hb = blocks_to_host(tr.blocks)
+            ob = _oracle_block(hb, L - 1)
+            pa, sa = tr.aggregate(1)
+            A = read_f32(pa, ob.n_dst, sa)[:, : gd.d]
+            X = oracle.gather_rows(gd.feats, hb[L - 1][4])[:, : gd.d].astype(np.float64)
+            X16 = (np.asarray(X, np.float32).view(np.uint32) + 0x7FFF + ((np.asarray(X, np.float32).view(np.uint32) >> 16) & 1)) & 0xFFFF0000
+            X16 = X16.astype(np.uint32).view(np.float32).astype(np.float64)  # round to nearest even, as the device
+            P = agg_matrix(ob)
+            assert_close_cond(A, P @ X16, P @ np.abs(X16), 1e-5, "A^1 over the bf16 rows")
+            assert_close_cond(A, P @ X, P @ np.abs(X), 2.0 ** -8, "A^1 vs the exact rows")
+        tr.free()
+    assert abs(losses["bf16"] - losses["fp32"]) <= 1e-3 * abs(losses["fp32"])
+
+
 @pytest.mark.parametrize("kind", [gnnv.KIND_SAGE, gnnv.KIND_GCN])
 @pytest.mark.parametrize("ratio", [0.3, 1.0])
 def test_prefetched_layer1_aggregation_bitwise(mini, option, kind, ratio):
