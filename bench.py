@@ -381,6 +381,8 @@ def algorithmic(seg: str, sizes, cfg, dims, stride, prec, peaks):
             by = n[L] * 12
         elif lvl < L:  # whole table cached: rows of F_{L-1} copied, every F_L row resolved to its cache row
             by = 2 * n[lvl] * rowb + n[L] * 12
+            if sizes.get("dw16"):  # + their bf16 copy with the ones column (layer-1 bf16 dW)
+                by += n[lvl] * (((dims[0] + 1 + 7) & ~7) * 2)
         else:
             by = sizes["hits"] * rowb + n[L] * rowb + n[L] * 8
         host = sizes["misses"] * rowb  # zero-copy reads of pinned host rows (Eq.6's transfer)
@@ -399,8 +401,11 @@ def algorithmic(seg: str, sizes, cfg, dims, stride, prec, peaks):
     # (j <= L-2) are bf16
     b16 = sizes.get("bf16act", False)
     src_b = 2 if (i == 1 and sizes.get("table16", False)) or (b16 and 2 <= i <= L - 1) else 4
+    dw16 = i == 1 and sizes.get("dw16", False)  # layer 1's dW over bf16 operands (reading Q32)
     if name == "spmm_fwd":
         by = U[h] * d_in * src_b + n[h] * ((d_in + 3) & ~3) * 4 + nnz[h] * 4 + (n[h] + 1) * 4
+        if dw16:  # + the bf16 copy of A^1
+            by += n[h] * ((d_in + 7) & ~7) * 2
         return "hbm", by, "GB/s", peaks["hbm"]
     if name == "spmm_bwd":
         # dA read, block CSR + owner masks read, every dH_src row written once,
@@ -435,13 +440,13 @@ def algorithmic(seg: str, sizes, cfg, dims, stride, prec, peaks):
         by = n[h] * d_out * 4 + n[h] * ld_in * (2 if b16 and i - 1 <= L - 2 else 4) + n[h] * ld_in * 4
     elif name == "gemm_dw":
         fl = 2.0 * n[h] * (K + 1) * d_out
-        by = n[h] * K * 4 + n[h] * d_out * (2 if out16 else 4)
+        by = n[h] * (K * 4 if not dw16 else (K + 1) * 2) + n[h] * d_out * (2 if out16 else 4)
     else:
         return None
     if prec == "fp32":
         return "alu", fl, "TFLOP/s", FP32_SIMT_TFLOPS
     # tensor-core modes: the binding roof is the larger of the two times
-    tpeak = peaks["bf16_sust"] * (0.5 if prec == "tf32" else 1.0)  # tf32 = 1/2 bf16 rate (guide)
+    tpeak = peaks["bf16_sust"] * (0.5 if prec == "tf32" and not (dw16 and name == "gemm_dw") else 1.0)  # tf32 = 1/2 bf16 rate (guide)
     if by / (peaks["hbm"] * 1e9) >= fl / (tpeak * 1e12):
         return "hbm", by, "GB/s", peaks["hbm"]
     return "tensor", fl, "TFLOP/s", tpeak
@@ -679,6 +684,7 @@ def main():
     sizes["x_level"] = tr.x_level()
     sizes["bf16act"] = tr.bf16act()
     sizes["table16"] = tr.table16()
+    sizes["dw16"] = tr.dw16()
     peaks = load_peaks()
     if sizes["misses"] > 0:
         peaks["host"] = measure_host_link()
@@ -789,11 +795,13 @@ def main():
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": {"fp32": "f32", "bf16": "f32+bf16gemm", "tf32": "f32+tf32gemm"}[args.prec] + (
-                "+bf16act" if bf16act else "") + ("+bf16table" if bf16tab else ""), "data": "synthetic",
+                "+bf16act" if bf16act else "") + ("+bf16table" if bf16tab else "") + (
+                "+bf16dw1" if tr.dw16() else ""), "data": "synthetic",
             "config": config_of(cfg, gd, world, args.kind),
             "settings": {"placement": args.placement, "locality_bias": args.locality_bias,
                          "cache_policy": args.policy, "gemm_precision": args.prec,
                          "bf16_intermediates": bf16act, "bf16_table_layer1": tr.table16(),
+                         "bf16_dw_layer1": tr.dw16(),
                          "gathered_x_mb_per_step": sizes["n"][L] * gd.stride * 4 / 1e6,
                          "pipeline": "eq4-overlap (next batch sample+gather on a side stream)" if pipeline else "off"},
             "step_stats": step_stats,

@@ -420,6 +420,16 @@ int32_t gnnv_trainer_table16(const gnnv_trainer* t);
 /* The bf16 copy of H^i (1..L-2) of the last step: [rows x *ld] bf16
  * (borrowed device pointer), NULL and 0 when the trainer keeps none. */
 gnnv_status gnnv_trainer_activation16(gnnv_trainer* t, int32_t i, const void** d_H16, int32_t* ld);
+/* The bf16 copy of dL/dH^i (1..L-2, after the ReLU mask) the last step's
+ * layer-i dW read: [rows x *ld] bf16, NULL and 0 when the trainer keeps none. */
+gnnv_status gnnv_trainer_gradient16(gnnv_trainer* t, int32_t i, const void** d_G16, int32_t* ld);
+/* 1 if layer 1's dW runs over bf16 operands (gemm_dw16: bf16act and
+ * table16, d_in + 1 <= 128, hidden a multiple of 64 up to 256, unless
+ * GNNV_NO_DW16; reading Q32).  Its operands of the last step: the bf16
+ * copy of X's dst prefix with 1.0 in column d_in (the db column) and the
+ * bf16 copy of A^1, both [n_dst x *ld] (borrowed device pointers). */
+int32_t gnnv_trainer_dw16(const gnnv_trainer* t);
+gnnv_status gnnv_trainer_dw16_operands(gnnv_trainer* t, const void** d_X16, const void** d_A16, int32_t* ld);
 
 /* One iteration of Algorithm 1 on this rank's seed slice:
  * sample -> gather -> L x (aggregate, combine) -> loss -> L x backward ->

@@ -31,6 +31,21 @@ bool env_on(const char* name) {
   g_opt_env.emplace_back(name, on);
   return on;
 }
+int env_int(const char* name, int def) {
+  {
+    std::lock_guard<std::mutex> lk(g_opt_mu);
+    for (auto& kv : g_opt_override)
+      if (kv.first == name && kv.second >= 0) return kv.second;
+  }
+  const char* e = getenv(name);
+  return e && e[0] ? atoi(e) : def;
+}
+static thread_local int t_grid_cap = 0;
+void set_grid_cap(int cap) { t_grid_cap = cap; }
+int capped_grid(int64_t grid) {
+  const int64_t g = std::max<int64_t>(grid, 1);
+  return (int)(t_grid_cap > 0 ? std::min<int64_t>(g, t_grid_cap) : g);
+}
 bool pdl_enabled() {
   static const bool on = !env_on("GNNV_NO_PDL");
   return on && !t_pdl_off;
@@ -231,7 +246,8 @@ gnnv_status gnnv_debug_check_guards(int32_t* n_bad) {
 gnnv_status gnnv_set_option(const char* name, int32_t value) {
   return guarded([&] {
     static const char* known[] = {"GNNV_XROWS", "GNNV_GEMM_PAIR", "GNNV_BWD_PULL", "GNNV_NO_TAIL", "GNNV_NO_PDL",
-                                  "GNNV_L2PUSH", "GNNV_LASTUSE", "GNNV_STATIC_TILES", "GNNV_PF_AGG", "GNNV_NO_BF16ACT", "GNNV_NO_BF16TABLE"};
+                                  "GNNV_L2PUSH", "GNNV_LASTUSE", "GNNV_STATIC_TILES", "GNNV_PF_AGG", "GNNV_NO_BF16ACT",
+                                  "GNNV_NO_BF16TABLE", "GNNV_NO_DW16", "GNNV_PF_CAP"};
     GNNV_REQUIRE(name, GNNV_ERR_PARAM, "set_option: null name");
     bool ok = false;
     for (const char* k : known) ok |= strcmp(k, name) == 0;

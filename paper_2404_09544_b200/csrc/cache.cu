@@ -73,7 +73,8 @@ __global__ void __launch_bounds__(256) k_gather(const int32_t* __restrict__ F, c
                                                 const float* const* __restrict__ shards, int G, int me,
                                                 const float* __restrict__ host, int32_t stride,
                                                 float* __restrict__ X, unsigned long long* stats, int mat_level,
-                                                int32_t* __restrict__ rowidx) {
+                                                int32_t* __restrict__ rowidx, __nv_bfloat16* __restrict__ X16,
+                                                int32_t ldx16, int32_t ones_col) {
   GNNV_PDL_ENTRY();
   const int n = sizes[L];
   const int n_mat = mat_level < 0 ? 0 : sizes[mat_level];  // rows materialised in X (all, the dst prefix, none)
@@ -116,7 +117,24 @@ __global__ void __launch_bounds__(256) k_gather(const int32_t* __restrict__ F, c
 #pragma unroll
         for (int j = 0; j < RU; ++j)
           if (r0 + j < nrows) __stcs(reinterpret_cast<float4*>(X) + (int64_t)(base + r0 + j) * vec + c, val[j]);
+        if (X16) {  // bf16 copy for the layer's bf16 dW: column ones_col = 1.0, columns past it 0
+          const int e = 4 * c;
+#pragma unroll
+          for (int j = 0; j < RU; ++j)
+            if (r0 + j < nrows) {
+              float4 v = val[j];
+              if (e + 0 >= ones_col) v.x = e + 0 == ones_col ? 1.f : 0.f;
+              if (e + 1 >= ones_col) v.y = e + 1 == ones_col ? 1.f : 0.f;
+              if (e + 2 >= ones_col) v.z = e + 2 == ones_col ? 1.f : 0.f;
+              if (e + 3 >= ones_col) v.w = e + 3 == ones_col ? 1.f : 0.f;
+              const __nv_bfloat162 lo = __floats2bfloat162_rn(v.x, v.y), hi = __floats2bfloat162_rn(v.z, v.w);
+              reinterpret_cast<uint2*>(X16)[((int64_t)(base + r0 + j) * ldx16 + e) >> 2] =
+                  make_uint2(*reinterpret_cast<const uint32_t*>(&lo), *reinterpret_cast<const uint32_t*>(&hi));
+            }
+        }
       }
+      if (X16 && 4 * vec <= ones_col && lane < nrows)  // the ones column lies past the row's stride
+        X16[(int64_t)(base + lane) * ldx16 + ones_col] = __float2bfloat16_rn(1.f);
     }
   }
   if (stats && lane == 0) {
@@ -128,16 +146,19 @@ __global__ void __launch_bounds__(256) k_gather(const int32_t* __restrict__ F, c
 }
 
 void launch_gather(const gnnv_cache* c, const gnnv_blocks* b, float* d_X, int64_t* d_stats, cudaStream_t s,
-                   int32_t* d_rowidx, bool materialize) {
+                   int32_t* d_rowidx, bool materialize, void* d_X16, int32_t ldx16) {
   const gnnv_graph* g = c->g;
+  GNNV_REQUIRE(!d_X16 || (materialize && ldx16 % 4 == 0 && ldx16 >= std::max(g->stride, g->d + 1)), GNNV_ERR_UNSUPPORTED,
+               "gather: the bf16 copy needs materialised rows and a stride (multiple of 4) covering the ones column");
   constexpr int RU = 8;
   const int64_t rows_ub = b->max_n[b->L];
   const int64_t warps = ceil_div(rows_ub, 32);
-  const int blocks = (int)std::min<int64_t>(ceil_div(warps, 8), (int64_t)num_sms() * 8);
-  launch_k(k_gather<RU>, std::max(blocks, 1), 256, 0, s, b->d_F, b->d_sizes, b->L, c->d_slot, c->d_shard_ptrs, c->world,
+  const int blocks = capped_grid(std::min<int64_t>(ceil_div(warps, 8), (int64_t)num_sms() * 8));
+  launch_k(k_gather<RU>, blocks, 256, 0, s, b->d_F, b->d_sizes, b->L, c->d_slot, c->d_shard_ptrs, c->world,
                                                    c->rank, g->d_feats, g->stride, d_X,
                                                    reinterpret_cast<unsigned long long*>(d_stats),
-                                                   !materialize ? -1 : d_rowidx ? b->L - 1 : b->L, d_rowidx);
+                                                   !materialize ? -1 : d_rowidx ? b->L - 1 : b->L, d_rowidx,
+                                                   static_cast<__nv_bfloat16*>(d_X16), ldx16, g->d);
   GNNV_CHECK_LAUNCH();
 }
 

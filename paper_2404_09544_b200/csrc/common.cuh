@@ -58,6 +58,13 @@ bool pdl_enabled();
 // off around the Eq.4 prefetch: its kernels would otherwise park waiting CTAs
 // on the SMs the concurrent step needs
 void set_pdl(bool on);
+// integer option (gnnv_set_option override, else the environment, else def)
+int env_int(const char* name, int def);
+// CTA cap for the grid-stride launches of this thread (0 = none): the Eq.4
+// prefetch caps its sampler / gather grids so the step's kernels keep room
+// on every SM (trainer.cu)
+void set_grid_cap(int cap);
+int capped_grid(int64_t grid);
 template <typename... KArgs, typename... Args>
 inline void launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args&&... args) {
   cudaLaunchConfig_t cfg = {};
@@ -274,7 +281,7 @@ void launch_cache_update(gnnv_cache* c, const gnnv_blocks* b, const float* d_X, 
 // builds c->d_table16 from the local table (setup path; synchronises)
 void cache_bf16_table(gnnv_cache* c);
 void launch_gather(const gnnv_cache* c, const gnnv_blocks* b, float* d_X, int64_t* d_stats, cudaStream_t s,
-                   int32_t* d_rowidx = nullptr, bool materialize = true);
+                   int32_t* d_rowidx = nullptr, bool materialize = true, void* d_X16 = nullptr, int32_t ldx16 = 0);
 // spmm.cu
 // rowidx != NULL: source row u is row rowidx[u] of H (the cache table)
 void launch_spmm_fwd(const int32_t* d_indptr, const int32_t* d_indices, const int32_t* d_ndst, int64_t max_dst,
@@ -287,7 +294,7 @@ void launch_spmm_bwd(const int32_t* d_indptr, const int32_t* d_indices, const ui
 // rowidx != NULL: source row u is row rowidx[u] of H16 (the bf16 table)
 void launch_spmm_fwd_h16(const int32_t* d_indptr, const int32_t* d_indices, const int32_t* d_ndst, int64_t max_dst,
                          const void* H16, int32_t ld16, float* A, int32_t lda, int32_t d, int32_t kind, int32_t aggr,
-                         cudaStream_t s, const int32_t* rowidx = nullptr);
+                         cudaStream_t s, const int32_t* rowidx = nullptr, void* A16 = nullptr, int32_t lda16 = 0);
 // the same transposed aggregation pulled per src row (rows up to
 // kPullMaxLd floats; wider ones keep the push) through the block's
 // CSC (one coalesced store per dH row, no atomics; see k_spmm_bwd_pull)
@@ -367,6 +374,12 @@ struct Bf16Io {
   int32_t gsrc16_ld = 0;
   const void* gdst16 = nullptr;    // bwd: this layer's G read as bf16 (stride gdst16_ld)
   int32_t gdst16_ld = 0;
+  // fwd: the aggregation also writes A as bf16 (a16, stride a16_ld); bwd
+  // with x16 (X's dst prefix as bf16, ones column at d_in, stride a16_ld)
+  // and gdst16: dW and db by gemm_dw16
+  void* a16 = nullptr;
+  int32_t a16_ld = 0;
+  const void* x16 = nullptr;
 };
 // Layer 1 of the trainer with the whole feature table on the device: H_dst
 // (X's dst prefix) is read by the TF32 GEMMs straight from the table through
@@ -405,6 +418,20 @@ struct GemmDwArgs {
 };
 void gemm_dw(const GemmDwArgs& a, int prec, cudaStream_t s);
 size_t gemm_dw_partial_floats(int32_t rows_plus_bias, int32_t N, int32_t* splits_out, int64_t max_M);
+// dW = [X16 | A16]^T G16 (+ db from X16's ones column K1) over bf16 operands,
+// MN-major on kind::f16 (gemm_tma.cu k_tma_dw16); K1 + 1 <= 128, N a
+// multiple of 64 up to 256
+struct GemmDw16Args {
+  const void *X16, *A16;  // [rows x ldx] bf16, column K1 of X16 = 1.0
+  int32_t ldx, K1;
+  const void* G16;        // [rows x ldg] bf16
+  int32_t ldg, N;
+  const int32_t* d_M;
+  int64_t max_M;
+  float *dW, *db;
+  bool zeroed = false;
+};
+void gemm_dw16(const GemmDw16Args& a, cudaStream_t s);
 struct GemmDxArgs {  // [Y1 | Y2] = G W^T  (Y1 = first K1 cols, Y2 = the rest)
   const float* G; int32_t ldg;
   int32_t N;

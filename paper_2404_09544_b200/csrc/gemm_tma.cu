@@ -1153,6 +1153,20 @@ static CUtensorMap make_map16(const void* base, int64_t rows, int64_t cols, int6
   return m;
 }
 
+// bf16 2-D map with 64 x 64 boxes and the 128-byte swizzle (MN-major UMMA operands)
+static CUtensorMap make_map16_sw(const void* base, int64_t rows, int64_t cols, int64_t ld) {
+  CUtensorMap m;
+  const cuuint64_t dims[2] = {(cuuint64_t)std::max<int64_t>(cols, 1), (cuuint64_t)std::max<int64_t>(rows, 1)};
+  const cuuint64_t strides[1] = {(cuuint64_t)ld * 2};
+  const cuuint32_t box[2] = {64, 64};
+  const cuuint32_t estr[2] = {1, 1};
+  CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  GNNV_REQUIRE(r == CUDA_SUCCESS, GNNV_ERR_CUDA, "cuTensorMapEncodeTiled (bf16 SW128) failed (alignment/stride)");
+  return m;
+}
+
 static CUtensorMap make_map(const float* base, int64_t rows, int64_t cols, int64_t ld, int box_rows,
                             int box_cols = 32, bool swizzle = true) {
   CUtensorMap m;
@@ -1241,8 +1255,12 @@ static int rup(int x, int m) { return (x + m - 1) / m * m; }
 // a scheduler slot for the next fwd/dX launch (ring of 4096; a slot is reset
 // by the last CTA of the launch that used it).  GNNV_STATIC_TILES=1: the
 // static round robin instead.
+static unsigned int* sched_slot();
 static unsigned int* next_sched() {
   if (env_on("GNNV_STATIC_TILES")) return nullptr;
+  return sched_slot();
+}
+static unsigned int* sched_slot() {
   static unsigned int* base = nullptr;
   static unsigned slot = 0;
   if (!base) {
@@ -1251,6 +1269,186 @@ static unsigned int* next_sched() {
     base = static_cast<unsigned int*>(p);
   }
   return base + 2 * (slot++ % 4096);
+}
+
+// ------------------------------------------------ dW over bf16 operands
+// The layer-1 weight gradient of the trainer with bf16 intermediates and
+// the bf16 table (readings Q30/Q31): dW = [X16 | A16]^T G16 with all three
+// operands bf16 in HBM.  kind::f16 accepts MN-major operands (measured with
+// tools/umma_probe.cu: bf16 MN/MN exact, tf32 MN-major all zeros), so the
+// TMA-staged row-major boxes feed the MMA directly -- no transposer warps:
+// A = X^T with M = features (two 64-feature SW128 boxes per 128-row tile,
+// 8 KB apart = LBO) and K = graph rows (8-row groups 1024 B apart = SBO),
+// B = G with N = output columns (BN/64 boxes).  64 graph rows per k-block
+// (four K = 16 MMAs per tile), split-K over graph rows across the grid,
+// partial sums added into dW with red.global.add.  X16's column K1 holds
+// 1.0, so row K1 of the first tile is colsum(G) = db.  The MMA warp zeroes
+// the rows of a ragged last k-block past M in shared memory (rows past the
+// buffers' max_M arrive zero-filled from TMA).
+constexpr int DW16_KR = 64;
+constexpr int DW16_STAGES = 3;
+constexpr int DW16_CHUNK = 4;  // k-blocks per scheduled chunk
+constexpr int DW16_BOX = DW16_KR * 128;  // one 64-row x 64-bf16 box, bytes
+
+__device__ __forceinline__ uint64_t desc_mn128(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFFu) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFFu) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)2 << 61;  // SWIZZLE_128B
+  return d;
+}
+__device__ __forceinline__ void mma_f16(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\ntcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(d),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+
+struct Dw16Params {
+  CUtensorMap tx, ta, tg;  // bf16: X16, A16 [rows x ldx] and G16 [rows x ldg], boxes of 64 x 64, SW128
+  const int32_t* dM;
+  unsigned int* sched;  // the launch's chunk counter (g_sched slot)
+  int K1, N, BN, splits;
+  float *dW, *db;
+};
+
+__global__ void __launch_bounds__(NTHREADS, 1) k_tma_dw16(const __grid_constant__ Dw16Params p) {
+  GNNV_PDL_ENTRY();
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+  constexpr int S = DW16_STAGES;
+  const int BN = p.BN;
+  const int nb = BN / 64;
+  const int a_bytes = 4 * DW16_BOX;  // two tiles (X, A) x two 64-feature boxes
+  const int stage_bytes = a_bytes + nb * DW16_BOX;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)S * stage_bytes);
+  uint64_t* empty = full + S;
+  uint64_t* tfull = empty + S;
+  int32_t* s_kb = reinterpret_cast<int32_t*>(tfull + 1);  // [S]: the k-block in each stage, -1 = no more
+  uint32_t* s_tmem = reinterpret_cast<uint32_t*>(s_kb + S);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int M = *p.dM;
+  const int nkbm = (M + DW16_KR - 1) / DW16_KR;
+  const int nchunks = (nkbm + DW16_CHUNK - 1) / DW16_CHUNK;
+  // chunks of DW16_CHUNK k-blocks: chunk blockIdx.x first, then claimed from
+  // the launch's counter -- a CTA slowed by a co-resident kernel (the Eq.4
+  // prefetch) takes fewer; every CTA keeps its sums in TMEM and flushes once
+  const bool any = (int)blockIdx.x < nchunks;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(tfull, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&p.tx);
+    tma_prefetch(&p.ta);
+    tma_prefetch(&p.tg);
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(s_tmem)), "r"(2 * 256)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_before();
+  __syncthreads();
+  tc_after();
+  const uint32_t tmem = *s_tmem;
+  if (warp == 0) {
+    if (lane == 0) {
+      int i = 0;
+      for (int c = blockIdx.x; c < nchunks; c = (int)gridDim.x + (int)atomicAdd(p.sched, 1u)) {
+        const int kb_end = min(nkbm, (c + 1) * DW16_CHUNK);
+        for (int kb = c * DW16_CHUNK; kb < kb_end; ++kb, ++i) {
+          const int s = i % S;
+          uint8_t* st = smem + (size_t)s * stage_bytes;
+          const int row = kb * DW16_KR;
+          if (i >= S) mbar_wait(&empty[s], ((i / S) & 1) ^ 1);
+          s_kb[s] = kb;
+          mbar_arrive_tx(&full[s], (uint32_t)stage_bytes);
+          tma_load_2d(st, &p.tx, 0, row, &full[s]);
+          tma_load_2d(st + DW16_BOX, &p.tx, 64, row, &full[s]);
+          tma_load_2d(st + 2 * DW16_BOX, &p.ta, 0, row, &full[s]);
+          tma_load_2d(st + 3 * DW16_BOX, &p.ta, 64, row, &full[s]);
+          for (int j = 0; j < nb; ++j) tma_load_2d(st + a_bytes + j * DW16_BOX, &p.tg, 64 * j, row, &full[s]);
+        }
+      }
+      const int s = i % S;  // end marker
+      if (i >= S) mbar_wait(&empty[s], ((i / S) & 1) ^ 1);
+      s_kb[s] = -1;
+      mbar_arrive(&full[s]);
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    // D f32, A = B = bf16, both MN-major, N = BN, M = 128
+    const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | (1u << 15) | (1u << 16) |
+                           ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+    int i = 0;
+    for (;; ++i) {
+      const int s = i % S;
+      mbar_wait(&full[s], (i / S) & 1);
+      const int kb = s_kb[s];
+      if (kb < 0) break;
+      const int valid = M - kb * DW16_KR;
+      if (valid < DW16_KR) {  // ragged last k-block: rows M.. of every box hold stale data -> zero them
+        uint8_t* st = smem + (size_t)s * stage_bytes;
+        const int per_box = (DW16_KR - valid) * 8;  // 16-byte chunks
+        for (int q = lane; q < (4 + nb) * per_box; q += 32) {
+          const int box = q / per_box, k = q - box * per_box;
+          *reinterpret_cast<uint4*>(st + (size_t)box * DW16_BOX + (size_t)valid * 128 + (size_t)k * 16) =
+              make_uint4(0u, 0u, 0u, 0u);
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      }
+      __syncwarp();
+      tc_after();
+      if (lane == 0) {
+        const uint32_t a0 = smem_u32(smem + (size_t)s * stage_bytes), b0 = a0 + a_bytes;
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+          for (int ks = 0; ks < DW16_KR / 16; ++ks)
+            mma_f16(tmem + (uint32_t)(mt * BN), desc_mn128(a0 + mt * 2 * DW16_BOX + ks * 2048, DW16_BOX, 1024),
+                    desc_mn128(b0 + ks * 2048, DW16_BOX, 1024), idesc, (i > 0 || ks > 0) ? 1u : 0u);
+        mma_commit(&empty[s]);
+      }
+      __syncwarp();
+    }
+    if (lane == 0) {
+      if (i > 0) mma_commit(tfull);
+      else mbar_arrive(tfull);
+    }
+    __syncwarp();
+  } else if (any) {
+    mbar_wait(tfull, 0);
+    tc_after();
+    const int q = warp & 3;
+    const int half = (warp - 2) >> 2;
+    const int r = q * 32 + lane;  // TMEM lane = row of the 128-row tile
+    for (int mt = 0; mt < 2; ++mt) {
+      float* dst = nullptr;
+      if (mt == 0 && r < p.K1) dst = p.dW + (int64_t)r * p.N;
+      else if (mt == 0 && r == p.K1) dst = p.db;  // the ones column
+      else if (mt == 1 && r < p.K1) dst = p.dW + (int64_t)(p.K1 + r) * p.N;
+      for (int c = half * 32; c < BN; c += 64) {
+        float v[32];
+        tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(mt * BN + c), v);
+        if (!dst) continue;
+#pragma unroll
+        for (int j = 0; j < 32; j += 4)
+          if (c + j < p.N)
+            atomicAdd(reinterpret_cast<float4*>(dst + c + j), make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]));
+      }
+    }
+  }
+  tc_before();
+  __syncthreads();
+  if (warp == 1)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2 * 256) : "memory");
+  if (threadIdx.x == 0) sched_done(p.sched);
 }
 
 }  // namespace tma
@@ -1360,6 +1558,38 @@ bool gemm_dx_tma(const GemmDxArgs& a, cudaStream_t s) {
 
 // dW; with a.mask_bits also the fused ReLU mask and db (else db comes from the
 // column-sum kernel in layers.cu).
+void gemm_dw16(const GemmDw16Args& a, cudaStream_t s) {
+  using namespace tma;
+  GNNV_REQUIRE(a.K1 + 1 <= 128 && a.N % 64 == 0 && a.N <= 256 && a.ldx % 8 == 0 && a.ldx >= a.K1 + 1 &&
+                   a.ldg % 8 == 0 && a.ldg >= a.N,
+               GNNV_ERR_UNSUPPORTED, "dw16: K1 + 1 <= 128, N % 64 == 0 and N <= 256, strides multiples of 8");
+  Dw16Params p{};
+  p.tx = make_map16_sw(a.X16, a.max_M, a.ldx, a.ldx);
+  p.ta = make_map16_sw(a.A16, a.max_M, a.ldx, a.ldx);
+  p.tg = make_map16_sw(a.G16, a.max_M, a.N, a.ldg);
+  p.dM = a.d_M;
+  p.K1 = a.K1;
+  p.N = a.N;
+  p.BN = a.N;
+  const int64_t nchunks = ceil_div(ceil_div(std::max<int64_t>(a.max_M, 1), DW16_KR), DW16_CHUNK);
+  p.splits = (int)std::max<int64_t>(1, std::min<int64_t>(nchunks, (int64_t)num_sms()));
+  p.sched = sched_slot();
+  p.dW = a.dW;
+  p.db = a.db;
+  if (!a.zeroed) {
+    GNNV_TRY_CUDA(cudaMemsetAsync(a.dW, 0, (size_t)2 * a.K1 * a.N * sizeof(float), s));
+    GNNV_TRY_CUDA(cudaMemsetAsync(a.db, 0, (size_t)a.N * sizeof(float), s));
+  }
+  const size_t bytes = (size_t)DW16_STAGES * (4 + a.N / 64) * DW16_BOX + 8 * (2 * DW16_STAGES + 1) + 4 * DW16_STAGES + 16 + 1024;
+  static size_t attr = 0;
+  if (bytes > attr) {
+    GNNV_TRY_CUDA(cudaFuncSetAttribute(k_tma_dw16, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+    attr = bytes;
+  }
+  launch_k(k_tma_dw16, dim3((unsigned)p.splits), NTHREADS, bytes, s, p);
+  GNNV_CHECK_LAUNCH();
+}
+
 bool gemm_dw_tma(const GemmDwArgs& a, cudaStream_t s) {
   using namespace tma;
   const int BN = rup(a.N, 32);

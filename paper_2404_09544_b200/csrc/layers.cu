@@ -275,7 +275,7 @@ void layer_fwd_impl(gnnv_blocks* b, int32_t layer, const gnnv_layer_desc* ld, co
     if (tl) tl->mark(s, "spmm_fwd" + sfx);
     if (io && io->src16)
       launch_spmm_fwd_h16(b->d_indptr[h], b->d_indices[h], d_ndst, b->max_n[h], io->src16, io->src16_ld, A, lda,
-                          ld->d_in, ld->kind, ld->aggr, s, io->src16_rows);
+                          ld->d_in, ld->kind, ld->aggr, s, io->src16_rows, io->a16, io->a16_ld);
     else
       launch_spmm_fwd(b->d_indptr[h], b->d_indices[h], d_ndst, b->max_n[h], rowidx ? agg_table : Hsrc,
                       ld->in_stride, A, lda, ld->d_in, ld->kind, ld->aggr, s, rowidx,
@@ -414,7 +414,25 @@ void layer_bwd_impl(gnnv_blocks* b, int32_t layer, const gnnv_layer_desc* ld, co
   w.db_fused = tf32 && !need_mask;
   w.zeroed = tf32 && grads_zeroed;
   if (tl) tl->mark(s, "gemm_dw" + sfx);
-  gemm_dw(w, ld->prec, s);
+  if (io && io->x16 && io->a16 && io->gdst16) {
+    GNNV_REQUIRE(sage && !xr && w.db_fused, GNNV_ERR_UNSUPPORTED, "layer_bwd: the bf16 dW needs SAGE and a final G");
+    GemmDw16Args w16{};
+    w16.X16 = io->x16;
+    w16.A16 = io->a16;
+    w16.ldx = io->a16_ld;
+    w16.K1 = ld->d_in;
+    w16.G16 = io->gdst16;
+    w16.ldg = io->gdst16_ld;
+    w16.N = ld->d_out;
+    w16.d_M = d_ndst;
+    w16.max_M = max_dst;
+    w16.dW = dW;
+    w16.db = db;
+    w16.zeroed = w.zeroed;
+    gemm_dw16(w16, s);
+  } else {
+    gemm_dw(w, ld->prec, s);
+  }
   if (Gsrc) {
     GemmDxArgs x{};
     x.G = G;

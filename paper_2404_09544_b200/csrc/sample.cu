@@ -644,7 +644,7 @@ __global__ void k_reset(const int32_t* __restrict__ F, const int32_t* sizes, int
 // grid): short-lived blocks let the step's higher-priority kernels
 // interleave with a prefetch.  Grids are sized by the Eq.12 capacity of the
 // hop (the realised size is on the device); surplus blocks exit at once.
-static int grid_for(int64_t work, int per_block) { return (int)ceil_div(std::max<int64_t>(work, 1), per_block); }
+static int grid_for(int64_t work, int per_block) { return capped_grid(ceil_div(std::max<int64_t>(work, 1), per_block)); }
 
 void launch_sample(gnnv_graph* g, gnnv_blocks* b, const int32_t* d_seeds, int32_t n_seeds, uint64_t rng_seed,
                    cudaStream_t s) {
@@ -701,7 +701,7 @@ void launch_sample(gnnv_graph* g, gnnv_blocks* b, const int32_t* d_seeds, int32_
     }
 #undef GNNV_SAMPLE_LAUNCH
     GNNV_CHECK_LAUNCH();
-    const int tiles_ub = (int)ceil_div(rows_ub, kScanTile);
+    const int tiles_ub = capped_grid(ceil_div(rows_ub, kScanTile));
     launch_k(k_winners, grid_for(rows_ub * k, 1024), 256, 0, s, g->n, h, k, b->d_sizes, b->d_ell, b->d_cnt, b->d_tag,
                                                              b->d_own[h]);
     GNNV_CHECK_LAUNCH();

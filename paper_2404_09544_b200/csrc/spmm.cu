@@ -487,7 +487,8 @@ __global__ void __launch_bounds__(256, 8) k_spmm_fwd_h16(const int32_t* __restri
                                                       const int32_t* __restrict__ indices, const int32_t* d_ndst,
                                                       const __nv_bfloat16* __restrict__ H, int32_t ld16,
                                                       float* __restrict__ A, int32_t lda, int32_t d, int32_t kind,
-                                                      int32_t aggr, const int32_t* __restrict__ rowidx) {
+                                                      int32_t aggr, const int32_t* __restrict__ rowidx,
+                                                      __nv_bfloat16* __restrict__ A16, int32_t lda16) {
   GNNV_PDL_ENTRY();
   constexpr int RPW = 32 / LPR;
   const int n = *d_ndst;
@@ -540,6 +541,10 @@ __global__ void __launch_bounds__(256, 8) k_spmm_fwd_h16(const int32_t* __restri
         float4* out = reinterpret_cast<float4*>(A) + (int64_t)row * lda4 + 2 * c;
         out[0] = make_float4(acc[0], acc[1], acc[2], acc[3]);
         if (2 * c + 1 < lda4) out[1] = make_float4(acc[4], acc[5], acc[6], acc[7]);
+        if (A16)  // the bf16 copy the layer's bf16 dW reads (gemm_dw16)
+          reinterpret_cast<uint4*>(A16)[(int64_t)row * (lda16 >> 3) + c] =
+              make_uint4(pack_bf16x2(acc[0], acc[1]), pack_bf16x2(acc[2], acc[3]), pack_bf16x2(acc[4], acc[5]),
+                         pack_bf16x2(acc[6], acc[7]));
       }
     }
     if (active)  // padding float4s of the output row
@@ -550,8 +555,11 @@ __global__ void __launch_bounds__(256, 8) k_spmm_fwd_h16(const int32_t* __restri
 
 void launch_spmm_fwd_h16(const int32_t* d_indptr, const int32_t* d_indices, const int32_t* d_ndst, int64_t max_dst,
                          const void* H16, int32_t ld16, float* A, int32_t lda, int32_t d, int32_t kind, int32_t aggr,
-                         cudaStream_t s, const int32_t* rowidx) {
+                         cudaStream_t s, const int32_t* rowidx, void* A16, int32_t lda16) {
   const int vec8 = (d + 7) / 8;
+  GNNV_REQUIRE(!A16 || (lda16 % 8 == 0 && lda16 >= 8 * vec8), GNNV_ERR_UNSUPPORTED,
+               "spmm_fwd_h16: the bf16 output stride must be a multiple of 8 covering d");
+  __nv_bfloat16* a16 = static_cast<__nv_bfloat16*>(A16);
   GNNV_REQUIRE(ld16 % 8 == 0 && ld16 >= 8 * vec8 && lda % 4 == 0, GNNV_ERR_UNSUPPORTED,
                "spmm_fwd_h16: the bf16 row stride must be a multiple of 8 covering d");
   const __nv_bfloat16* H = static_cast<const __nv_bfloat16*>(H16);
@@ -559,10 +567,10 @@ void launch_spmm_fwd_h16(const int32_t* d_indptr, const int32_t* d_indices, cons
   do {                                                                                                               \
     if (rowidx)                                                                                                      \
       launch_k(k_spmm_fwd_h16<LPR, true>, spmm_grid(max_dst, RPWv), 256, 0, s, d_indptr, d_indices, d_ndst, H, ld16, \
-               A, lda, d, kind, aggr, rowidx);                                                                       \
+               A, lda, d, kind, aggr, rowidx, a16, lda16);                                                           \
     else                                                                                                             \
       launch_k(k_spmm_fwd_h16<LPR, false>, spmm_grid(max_dst, RPWv), 256, 0, s, d_indptr, d_indices, d_ndst, H,      \
-               ld16, A, lda, d, kind, aggr, (const int32_t*)nullptr);                                                \
+               ld16, A, lda, d, kind, aggr, (const int32_t*)nullptr, a16, lda16);                                    \
   } while (0)
   if (vec8 <= 8) GNNV_H16(8, 4);
   else if (vec8 <= 16) GNNV_H16(16, 2);

@@ -85,6 +85,14 @@ struct gnnv_trainer {
   // whole-table TF32 SAGE: the layer-1 aggregation reads the cache's bf16
   // copy of the table (reading Q31; GNNV_NO_BF16TABLE=1: the fp32 table)
   bool table16 = false;
+  // with both: layer 1's dW over bf16 MN-major operands (gemm_dw16, no
+  // transposer): the gather also writes a bf16 copy of X's dst prefix with a
+  // ones column at d (X16[k]) and the layer-1 aggregation a bf16
+  // copy of A^1 (A16[k]); GNNV_NO_DW16=1: the TF32 dW
+  bool dw16 = false;
+  void* X16[2] = {nullptr, nullptr};
+  void* A16[2] = {nullptr, nullptr};
+  int32_t ld16x = 0;  // their row stride: d + 1 rounded up to 8
   void* H16[GNNV_MAX_LAYERS + 1] = {nullptr};
   void* G16[GNNV_MAX_LAYERS + 1] = {nullptr};
   int32_t ld16[GNNV_MAX_LAYERS + 1] = {0};
@@ -158,6 +166,14 @@ static cudaStream_t make_side_stream() {
   return st;
 }
 
+static void alloc_dw16(gnnv_trainer* t, int k, const gnnv_blocks* b) {
+  const size_t bytes = (size_t)b->max_n[t->md.L - 1] * t->ld16x * 2;
+  t->X16[k] = dmalloc(bytes, "bf16 X dst prefix (layer-1 dW)");
+  t->A16[k] = dmalloc(bytes, "bf16 layer-1 aggregates (layer-1 dW)");
+  GNNV_TRY_CUDA(cudaMemset(t->X16[k], 0, bytes));
+  GNNV_TRY_CUDA(cudaMemset(t->A16[k], 0, bytes));
+}
+
 extern "C" {
 
 gnnv_status gnnv_trainer_free(gnnv_trainer* t) {
@@ -167,6 +183,8 @@ gnnv_status gnnv_trainer_free(gnnv_trainer* t) {
   for (int k = 0; k < 2; ++k) {
     gnnv_blocks_free(t->bb[k]);
     dfree(t->X[k]);
+    dfree(t->X16[k]);
+    dfree(t->A16[k]);
     dfree(t->rowidx[k]);
     if (k == 1) dfree(t->A1b[1]);  // A1b[0] is A[1], freed with the layers
     dfree(t->d_seedsb[k]);
@@ -291,6 +309,10 @@ gnnv_status gnnv_trainer_create(gnnv_graph* g, gnnv_cache* c, const gnnv_model_d
       t->table16 = t->x_fused && md->prec == GNNV_PREC_TF32 && md->kind == GNNV_KIND_SAGE &&
                    !env_on("GNNV_NO_BF16TABLE");
       if (t->table16) cache_bf16_table(c);
+      t->dw16 = t->table16 && t->bf16act && !t->x_rows && md->dims[0] + 1 <= 128 && md->dims[1] % 64 == 0 &&
+                md->dims[1] <= 256 && !env_on("GNNV_NO_DW16");
+      t->ld16x = (md->dims[0] + 1 + 7) / 8 * 8;
+      if (t->dw16) alloc_dw16(t, 0, b);
       t->l2push = !t->bf16act && md->prec == GNNV_PREC_TF32 && md->kind == GNNV_KIND_SAGE && L >= 3 &&
                   env_on("GNNV_L2PUSH");
       if (t->l2push)
@@ -403,6 +425,25 @@ gnnv_status gnnv_trainer_activation16(gnnv_trainer* t, int32_t i, const void** d
   });
 }
 
+gnnv_status gnnv_trainer_gradient16(gnnv_trainer* t, int32_t i, const void** d_G16, int32_t* ld) {
+  return guarded([&] {
+    GNNV_REQUIRE(t && d_G16 && ld && i >= 0 && i <= t->md.L, GNNV_ERR_PARAM, "trainer_gradient16: bad args");
+    *d_G16 = t->G16[i];
+    *ld = t->G16[i] ? t->ld16[i] : 0;
+  });
+}
+
+int32_t gnnv_trainer_dw16(const gnnv_trainer* t) { return t && t->dw16 ? 1 : 0; }
+
+gnnv_status gnnv_trainer_dw16_operands(gnnv_trainer* t, const void** d_X16, const void** d_A16, int32_t* ld) {
+  return guarded([&] {
+    GNNV_REQUIRE(t && d_X16 && d_A16 && ld, GNNV_ERR_PARAM, "trainer_dw16_operands: null");
+    *d_X16 = t->X16[t->cur];
+    *d_A16 = t->A16[t->cur];
+    *ld = t->dw16 ? t->ld16x : 0;
+  });
+}
+
 gnnv_status gnnv_trainer_set_locality(gnnv_trainer* t, double bias) {
   return guarded([&] {
     GNNV_REQUIRE(t, GNNV_ERR_PARAM, "trainer_set_locality: null");
@@ -511,6 +552,7 @@ gnnv_status gnnv_trainer_stats(gnnv_trainer* t, int64_t* host_stats4) {
   });
 }
 
+
 static void select_buffers(gnnv_trainer* t, int k) {
   t->cur = k;
   t->b = t->bb[k];
@@ -565,6 +607,7 @@ gnnv_status gnnv_trainer_prefetch(gnnv_trainer* t, const int32_t* seeds, int32_t
       t->d_seedsb[k] = (int32_t*)dmalloc(t->md.max_seeds * sizeof(int32_t), "seeds (prefetch)");
       GNNV_TRY_CUDA(cudaMallocHost(&t->h_seedsb[k], t->md.max_seeds * sizeof(int32_t)));
       t->d_statsb[k] = (int64_t*)dmalloc(4 * sizeof(int64_t), "gather stats (prefetch)");
+      if (t->dw16) alloc_dw16(t, k, t->bb[k]);
       if (t->pf_agg)
         t->A1b[k] = (float*)dmalloc((size_t)t->bb[k]->max_n[t->md.L - 1] * row_stride(t->md.dims[0]) * sizeof(float),
                                     "layer-1 aggregates (prefetch)");
@@ -592,15 +635,22 @@ gnnv_status gnnv_trainer_prefetch(gnnv_trainer* t, const int32_t* seeds, int32_t
     // the overlapped batch launches without programmatic dependent launch
     // (its waiting CTAs would park on SMs the concurrent step needs)
     struct PrefetchLaunch {
-      PrefetchLaunch() { set_pdl(false); }
-      ~PrefetchLaunch() { set_pdl(true); }
+      PrefetchLaunch() {
+        set_pdl(false);
+        set_grid_cap(env_int("GNNV_PF_CAP", 0));
+      }
+      ~PrefetchLaunch() {
+        set_pdl(true);
+        set_grid_cap(0);
+      }
     } pf_launch;
     launch_sample(g, t->bb[k], d_seeds, n_seeds, rng_seed, t->side);
     t->bb[k]->sampled = true;
     GNNV_TRY_CUDA(cudaMemsetAsync(t->d_statsb[k], 0, 4 * sizeof(int64_t), t->side));
     if (tl) tl->mark(t->side, "pf_gather");
     if (t->c->dynamic && t->cache_pending) GNNV_TRY_CUDA(cudaStreamWaitEvent(t->side, t->ev_cache, 0));
-    launch_gather(t->c, t->bb[k], t->X[k], t->d_statsb[k], t->side, t->rowidx[k], !t->x_rows);
+    launch_gather(t->c, t->bb[k], t->X[k], t->d_statsb[k], t->side, t->rowidx[k], !t->x_rows, t->X16[k],
+                  t->ld16x);
     if (t->c->dynamic) {  // NEXT-3 admission
       if (tl) tl->mark(t->side, "pf_replace");
       launch_cache_update(t->c, t->bb[k], t->X[k], t->side);
@@ -614,7 +664,7 @@ gnnv_status gnnv_trainer_prefetch(gnnv_trainer* t, const int32_t* seeds, int32_t
       if (t->table16)
         launch_spmm_fwd_h16(bk->d_indptr[h], bk->d_indices[h], bk->d_sizes + h, bk->max_n[h], t->c->d_table16,
                             t->c->table16_ld, t->A1b[k], row_stride(t->md.dims[0]), t->md.dims[0], t->md.kind,
-                            t->md.aggr, t->side, t->rowidx[k]);
+                            t->md.aggr, t->side, t->rowidx[k], t->A16[k], t->ld16x);
       else
         launch_spmm_fwd(bk->d_indptr[h], bk->d_indices[h], bk->d_sizes + h, bk->max_n[h],
                         t->x_fused ? t->table : t->X[k], g->stride, t->A1b[k], row_stride(t->md.dims[0]),
@@ -676,7 +726,8 @@ gnnv_status gnnv_step(gnnv_trainer* t, const int32_t* seeds, int32_t n_seeds, in
       if (tm) GNNV_TRY_CUDA(cudaEventRecord(t->ev[1], s));
       if (tl) tl->mark(s, "gather");
       if (t->c->dynamic && t->cache_pending) GNNV_TRY_CUDA(cudaStreamWaitEvent(s, t->ev_cache, 0));
-      launch_gather(t->c, t->b, t->H[0], t->d_stats, s, t->rowidx[t->cur], !t->x_rows);
+      launch_gather(t->c, t->b, t->H[0], t->d_stats, s, t->rowidx[t->cur], !t->x_rows, t->X16[t->cur],
+                    t->ld16x);
       if (t->c->dynamic) {  // NEXT-3 admission (Eq.5's t_replace)
         if (tl) tl->mark(s, "replace");
         launch_cache_update(t->c, t->b, t->H[0], s);
@@ -705,6 +756,8 @@ gnnv_status gnnv_step(gnnv_trainer* t, const int32_t* seeds, int32_t n_seeds, in
         io.src16 = t->c->d_table16;
         io.src16_ld = t->c->table16_ld;
         io.src16_rows = t->rowidx[t->cur];
+        io.a16 = t->A16[t->cur];
+        io.a16_ld = t->ld16x;
       }
       if (t->bf16act) {
         if (i <= L - 2) {  // this layer's output: a bf16 copy, fp32 rows for the next dst prefix
@@ -780,6 +833,11 @@ gnnv_status gnnv_step(gnnv_trainer* t, const int32_t* seeds, int32_t n_seeds, in
         if (i <= L - 2) {  // this layer's G read as bf16
           io.gdst16 = t->G16[i];
           io.gdst16_ld = t->ld16[i];
+        }
+        if (i == 1 && t->dw16) {
+          io.x16 = t->X16[t->cur];
+          io.a16 = t->A16[t->cur];
+          io.a16_ld = t->ld16x;
         }
       }
       layer_bwd_impl(b, i, &ld, t->G[i], t->H[i], t->H[i - 1], t->A[i], t->d_params + t->w_off[i - 1],

@@ -134,6 +134,9 @@ _SIGS = {
     "gnnv_trainer_bf16act": (I32, [VP]),
     "gnnv_trainer_table16": (I32, [VP]),
     "gnnv_trainer_activation16": (I32, [VP, I32, PP, C.POINTER(I32)]),
+    "gnnv_trainer_gradient16": (I32, [VP, I32, PP, C.POINTER(I32)]),
+    "gnnv_trainer_dw16": (I32, [VP]),
+    "gnnv_trainer_dw16_operands": (I32, [VP, PP, PP, C.POINTER(I32)]),
     "gnnv_step": (I32, [VP, VP, I32, I32, I32, U64, F32, C.POINTER(F32), C.POINTER(StepTiming), VP]),
     "gnnv_trainer_stats": (I32, [VP, VP]),
     "gnnv_trainer_prefetch": (I32, [VP, VP, I32, I32, U64, VP]),
@@ -582,6 +585,24 @@ class Trainer:
         ld = C.c_int32()
         _check(load().gnnv_trainer_activation16(self.h, i, C.byref(p), C.byref(ld)))
         return int(p.value or 0), int(ld.value)
+
+    def gradient16(self, i: int):
+        """(device pointer, row stride) of the bf16 dL/dH^i layer i's dW read, or (0, 0)."""
+        p = C.c_void_p()
+        ld = C.c_int32()
+        _check(load().gnnv_trainer_gradient16(self.h, i, C.byref(p), C.byref(ld)))
+        return int(p.value or 0), int(ld.value)
+
+    def dw16(self) -> bool:
+        return bool(load().gnnv_trainer_dw16(self.h))
+
+    def dw16_operands(self):
+        """(X16, A16, row stride): layer 1's bf16 dW operands of the last step."""
+        x = C.c_void_p()
+        a = C.c_void_p()
+        ld = C.c_int32()
+        _check(load().gnnv_trainer_dw16_operands(self.h, C.byref(x), C.byref(a), C.byref(ld)))
+        return int(x.value or 0), int(a.value or 0), int(ld.value)
 
     def timeline(self, on: bool):
         _check(load().gnnv_trainer_timeline(self.h, 1 if on else 0))

@@ -15,7 +15,7 @@ from oracle.sampler import Block, sample_blocks
 from paper_2404_09544_b200 import gnnv
 from synth import CONFIGS, epoch_seeds, init_weights, make_graph, row_stride, tiny_graph
 
-from gpu_util import check_backward_chain, check_forward_chain, sub_block, assert_close_cond, blocks_to_host, dev_f32, dev_i32, lib, normwise, read_f32, read_i32
+from gpu_util import check_backward_chain, check_forward_chain, sub_block, assert_close_cond, blocks_to_host, dev_f32, dev_i32, lib, normwise, read_bf16, read_f32, read_i32
 
 pytestmark = pytest.mark.gpu
 
@@ -862,6 +862,71 @@ def test_bf16_table_layer1_aggregation(mini, option):
             assert_close_cond(A, P @ X, P @ np.abs(X), 2.0 ** -8, "A^1 vs the exact rows")
         tr.free()
     assert abs(losses["bf16"] - losses["fp32"]) <= 1e-3 * abs(losses["fp32"])
+
+
+def _bf16_round(x):
+    """fp32 -> bf16 (round to nearest even, as __float2bfloat16_rn), as float64."""
+    u = np.ascontiguousarray(x, np.float32).view(np.uint32).astype(np.uint64)
+    r = ((u + 0x7FFF + ((u >> 16) & 1)) & 0xFFFF0000).astype(np.uint32)
+    return r.view(np.float32).astype(np.float64)
+
+
+@pytest.mark.parametrize("pipelined", [False, True], ids=["serial", "pipelined"])
+def test_bf16_layer1_dw(mini, option, pipelined):
+    """Layer 1's dW over bf16 MN-major operands (gemm_dw16, reading Q32):
+    its operands are exactly the bf16 roundings of the step's own fp32 X dst
+    prefix (with 1.0 in column d: the db column) and A^1, and dW / db equal
+    [X16 | A16]^T G16 and colsum(G16) in fp64 up to fp32 accumulation
+    (rtol 1e-5 of the |.| product).  A large batch first, then a smaller
+    one: the second's ragged last k-block sits over rows the first step
+    left non-zero, so a missing tail mask would show.  Against the TF32 dW
+    (GNNV_NO_DW16=1): the same loss bitwise (the forward is unchanged), dW
+    of layer 1 within cos 0.9999 and through the oracle's backward chain."""
+    gd, g = mini
+    cfg = CONFIGS["mini"]
+    dims = [gd.d, cfg["hidden"], cfg["hidden"], gd.C]
+    L = len(cfg["fanouts"])
+    w = init_weights(dims)
+    perm = epoch_seeds(gd.n, 0)
+    B = cfg["batch"]
+    runs = {}
+    for name in ("dw16", "tf32"):
+        option("GNNV_NO_DW16", 0 if name == "dw16" else 1)
+        tr = gnnv.Trainer(g, gnnv.Cache(g, 1.0), dims, cfg["fanouts"], B, w, prec=gnnv.PREC_TF32)
+        assert tr.dw16() == (name == "dw16")
+        for t, n in ((0, B), (1, B // 3 + 7)):
+            seeds = perm[t * B:t * B + n]
+            if pipelined:
+                tr.prefetch(seeds, n, 77 + t)
+            loss, _ = tr.step(seeds, n, n, 77 + t, 0.0)
+        grads = gnnv.unflat_params(tr.grads(), dims)
+        if name == "dw16":
+            hb = blocks_to_host(tr.blocks)
+            ob = _oracle_block(hb, L - 1)
+            M, d = ob.n_dst, gd.d
+            px, pa, ld = tr.dw16_operands()
+            X16 = read_bf16(px, M, ld)
+            A16 = read_bf16(pa, M, ld)
+            X_all = oracle.gather_rows(gd.feats, hb[L - 1][4])[:, :d]
+            X = X_all[:M]
+            np.testing.assert_array_equal(X16[:, :d], _bf16_round(X))
+            np.testing.assert_array_equal(X16[:, d], 1.0)
+            p1, s1 = tr.aggregate(1)
+            np.testing.assert_array_equal(A16[:, :d], _bf16_round(read_f32(p1, M, s1)[:, :d]))
+            pg, ldg = tr.gradient16(1)
+            G16 = read_bf16(pg, M, ldg)[:, : dims[1]]
+            Z = np.concatenate([X16[:, :d], A16[:, :d]], axis=1)
+            assert_close_cond(grads[0][0], Z.T @ G16, np.abs(Z).T @ np.abs(G16), 1e-5, "dW^1 over the bf16 operands")
+            assert_close_cond(grads[0][1], G16.sum(0), np.abs(G16).sum(0), 1e-5, "db^1 = colsum(G16)")
+            H, Aagg, blks = check_forward_chain(tr, hb, dims, w, RTOL[2], "dw16",
+                                                X0=X_all if tr.x_level() < L else None, max_rows=10**9)
+            check_backward_chain(tr, blks, H, Aagg, dims, w, grads, gd.labels[seeds], n, RTOL[2], "dw16")
+        runs[name] = (loss, grads)
+        tr.free()
+    assert runs["dw16"][0] == runs["tf32"][0]
+    for a_, b_ in zip(runs["dw16"][1][0], runs["tf32"][1][0]):
+        cos = float(np.dot(a_.ravel(), b_.ravel()) / (np.linalg.norm(a_) * np.linalg.norm(b_) + 1e-30))
+        assert cos > 0.9999, cos
 
 
 @pytest.mark.parametrize("kind", [gnnv.KIND_SAGE, gnnv.KIND_GCN])
