@@ -377,12 +377,15 @@ def algorithmic(seg: str, sizes, cfg, dims, stride, prec, peaks):
     if name == "gather":
         rowb = stride * 4
         lvl = int(sizes.get("x_level", L))
-        if lvl < 0:  # whole table cached, layer-1 GEMMs gather H_dst from it: F_L rows resolved, none copied
+        ld16x = (dims[0] + 1 + 7) & ~7
+        if lvl < 0 and sizes.get("fwd16"):  # whole table cached, layer 1 on bf16 copies: F_{L-1} rows -> bf16 only
+            by = n[L - 1] * (rowb + ld16x * 2) + n[L] * 12
+        elif lvl < 0:  # whole table cached, layer-1 GEMMs gather H_dst from it: F_L rows resolved, none copied
             by = n[L] * 12
         elif lvl < L:  # whole table cached: rows of F_{L-1} copied, every F_L row resolved to its cache row
             by = 2 * n[lvl] * rowb + n[L] * 12
             if sizes.get("dw16"):  # + their bf16 copy with the ones column (layer-1 bf16 dW)
-                by += n[lvl] * (((dims[0] + 1 + 7) & ~7) * 2)
+                by += n[lvl] * ld16x * 2
         else:
             by = sizes["hits"] * rowb + n[L] * rowb + n[L] * 8
         host = sizes["misses"] * rowb  # zero-copy reads of pinned host rows (Eq.6's transfer)
@@ -402,8 +405,9 @@ def algorithmic(seg: str, sizes, cfg, dims, stride, prec, peaks):
     b16 = sizes.get("bf16act", False)
     src_b = 2 if (i == 1 and sizes.get("table16", False)) or (b16 and 2 <= i <= L - 1) else 4
     dw16 = i == 1 and sizes.get("dw16", False)  # layer 1's dW over bf16 operands (reading Q32)
+    fwd16 = i == 1 and sizes.get("fwd16", False)  # and its forward GEMM (reading Q33): A^1 kept as bf16 only
     if name == "spmm_fwd":
-        by = U[h] * d_in * src_b + n[h] * ((d_in + 3) & ~3) * 4 + nnz[h] * 4 + (n[h] + 1) * 4
+        by = U[h] * d_in * src_b + (0 if fwd16 else n[h] * ((d_in + 3) & ~3) * 4) + nnz[h] * 4 + (n[h] + 1) * 4
         if dw16:  # + the bf16 copy of A^1
             by += n[h] * ((d_in + 7) & ~7) * 2
         return "hbm", by, "GB/s", peaks["hbm"]
@@ -434,7 +438,7 @@ def algorithmic(seg: str, sizes, cfg, dims, stride, prec, peaks):
     out16 = b16 and i <= L - 2  # H^i (and dL/dH^i) kept as bf16, fp32 rows only for the next dst prefix
     if name == "gemm_fwd":
         fl = 2.0 * n[h] * K * d_out
-        by = n[h] * K * 4 + (n[h] * ld_out * 2 + n[h - 1] * ld_out * 4 if out16 else n[h] * ld_out * 4)
+        by = n[h] * (K * 4 if not fwd16 else (K + 1) * 2) + (n[h] * ld_out * 2 + n[h - 1] * ld_out * 4 if out16 else n[h] * ld_out * 4)
     elif name == "gemm_dx":
         fl = 2.0 * n[h] * K * d_out
         by = n[h] * d_out * 4 + n[h] * ld_in * (2 if b16 and i - 1 <= L - 2 else 4) + n[h] * ld_in * 4
@@ -446,7 +450,8 @@ def algorithmic(seg: str, sizes, cfg, dims, stride, prec, peaks):
     if prec == "fp32":
         return "alu", fl, "TFLOP/s", FP32_SIMT_TFLOPS
     # tensor-core modes: the binding roof is the larger of the two times
-    tpeak = peaks["bf16_sust"] * (0.5 if prec == "tf32" and not (dw16 and name == "gemm_dw") else 1.0)  # tf32 = 1/2 bf16 rate (guide)
+    bf16_op = (dw16 and name == "gemm_dw") or (fwd16 and name == "gemm_fwd")
+    tpeak = peaks["bf16_sust"] * (0.5 if prec == "tf32" and not bf16_op else 1.0)  # tf32 = 1/2 bf16 rate (guide)
     if by / (peaks["hbm"] * 1e9) >= fl / (tpeak * 1e12):
         return "hbm", by, "GB/s", peaks["hbm"]
     return "tensor", fl, "TFLOP/s", tpeak
@@ -685,6 +690,7 @@ def main():
     sizes["bf16act"] = tr.bf16act()
     sizes["table16"] = tr.table16()
     sizes["dw16"] = tr.dw16()
+    sizes["fwd16"] = tr.fwd16()
     peaks = load_peaks()
     if sizes["misses"] > 0:
         peaks["host"] = measure_host_link()
@@ -724,7 +730,9 @@ def main():
             h = len(cfg["fanouts"]) - i
             d_in = dims[i - 1]
             eb = 2 if (i == 1 and sizes["table16"]) or (sizes["bf16act"] and 2 <= i <= L - 1) else 4
-            ev = sizes["nnz"][h] * d_in * eb + sizes["n"][h] * ((d_in + 3) & ~3) * 4
+            ob = ((d_in + 3) & ~3) * 4 * (0 if (i == 1 and sizes["fwd16"]) else 1) + (
+                ((d_in + 7) & ~7) * 2 if (i == 1 and sizes["dw16"]) else 0)  # fp32 and / or bf16 A rows
+            ev = sizes["nnz"][h] * d_in * eb + sizes["n"][h] * ob
             r["edge_visit_bytes"] = ev
             r["edge_visit_frac"] = ev / (avg_ms / 1000.0) / 1e9 / peaks["hbm"]
         rooflines[name] = r
@@ -796,12 +804,12 @@ def main():
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": {"fp32": "f32", "bf16": "f32+bf16gemm", "tf32": "f32+tf32gemm"}[args.prec] + (
                 "+bf16act" if bf16act else "") + ("+bf16table" if bf16tab else "") + (
-                "+bf16dw1" if tr.dw16() else ""), "data": "synthetic",
+                "+bf16dw1" if tr.dw16() else "") + ("+bf16fwd1" if tr.fwd16() else ""), "data": "synthetic",
             "config": config_of(cfg, gd, world, args.kind),
             "settings": {"placement": args.placement, "locality_bias": args.locality_bias,
                          "cache_policy": args.policy, "gemm_precision": args.prec,
                          "bf16_intermediates": bf16act, "bf16_table_layer1": tr.table16(),
-                         "bf16_dw_layer1": tr.dw16(),
+                         "bf16_dw_layer1": tr.dw16(), "bf16_fwd_layer1": tr.fwd16(),
                          "gathered_x_mb_per_step": sizes["n"][L] * gd.stride * 4 / 1e6,
                          "pipeline": "eq4-overlap (next batch sample+gather on a side stream)" if pipeline else "off"},
             "step_stats": step_stats,

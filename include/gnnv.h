@@ -383,7 +383,9 @@ gnnv_blocks* gnnv_trainer_blocks(gnnv_trainer* t);
  * SAGE with TF32 GEMMs and GNNV_XROWS=1 was set when the trainer was
  * created: the layer-1 GEMMs (forward and dW) then read the H_dst rows from
  * the table as well (TMA gather4 through the same row indices) and X is
- * never written (off by default: slower on products). */
+ * never written (off by default: slower on products).  -1
+ * also with gnnv_trainer_fwd16: layer 1 then reads only the bf16 copies
+ * (gnnv_trainer_dw16_operands) and the fp32 X is never written. */
 int32_t gnnv_trainer_x_level(const gnnv_trainer* t);
 /* Whole-table mode (x_level < L): *d_rowidx = int32[n_L] cache-table row of
  * every F_L row of the last step (row u of layer 1's input is row
@@ -399,7 +401,8 @@ gnnv_status gnnv_trainer_activation(gnnv_trainer* t, int32_t i, const float** d_
  * (gnnv_trainer_l2push) A^{i+1} was accumulated by layer i's GEMM epilogue
  * and H^i (gnnv_trainer_activation) holds only the rows layer i+1 reads as
  * its dst prefix (the first n_dst of layer i+1); its other rows exist only
- * as their ReLU bits.  PARAM on i outside 1..L. */
+ * as their ReLU bits.  With gnnv_trainer_fwd16, A^1 exists only as its bf16
+ * copy: i = 1 then gives NULL and 0.  PARAM on i outside 1..L. */
 gnnv_status gnnv_trainer_aggregate(gnnv_trainer* t, int32_t i, const float** d_A, int32_t* stride);
 /* TF32: layer i's ReLU bits (1..L-1) of the last step, bit n%32 of word
  * [row * words + n/32] = (H^i[row][n] > 0); NULL (and 0) otherwise. */
@@ -429,6 +432,10 @@ gnnv_status gnnv_trainer_gradient16(gnnv_trainer* t, int32_t i, const void** d_G
  * copy of X's dst prefix with 1.0 in column d_in (the db column) and the
  * bf16 copy of A^1, both [n_dst x *ld] (borrowed device pointers). */
 int32_t gnnv_trainer_dw16(const gnnv_trainer* t);
+/* 1 if layer 1's forward GEMM also reads those bf16 copies (kind::f16 over
+ * [X16 | A16] and W rounded to bf16; with gnnv_trainer_dw16, unless
+ * GNNV_NO_FWD16; reading Q33). */
+int32_t gnnv_trainer_fwd16(const gnnv_trainer* t);
 gnnv_status gnnv_trainer_dw16_operands(gnnv_trainer* t, const void** d_X16, const void** d_A16, int32_t* ld);
 
 /* One iteration of Algorithm 1 on this rank's seed slice:

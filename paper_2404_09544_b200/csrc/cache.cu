@@ -114,9 +114,11 @@ __global__ void __launch_bounds__(256) k_gather(const int32_t* __restrict__ F, c
 #pragma unroll
         for (int j = 0; j < RU; ++j)
           if (r0 + j < nrows) val[j] = __ldg(ps[j] + c);
+        if (X) {
 #pragma unroll
-        for (int j = 0; j < RU; ++j)
-          if (r0 + j < nrows) __stcs(reinterpret_cast<float4*>(X) + (int64_t)(base + r0 + j) * vec + c, val[j]);
+          for (int j = 0; j < RU; ++j)
+            if (r0 + j < nrows) __stcs(reinterpret_cast<float4*>(X) + (int64_t)(base + r0 + j) * vec + c, val[j]);
+        }
         if (X16) {  // bf16 copy for the layer's bf16 dW: column ones_col = 1.0, columns past it 0
           const int e = 4 * c;
 #pragma unroll
@@ -150,6 +152,7 @@ void launch_gather(const gnnv_cache* c, const gnnv_blocks* b, float* d_X, int64_
   const gnnv_graph* g = c->g;
   GNNV_REQUIRE(!d_X16 || (materialize && ldx16 % 4 == 0 && ldx16 >= std::max(g->stride, g->d + 1)), GNNV_ERR_UNSUPPORTED,
                "gather: the bf16 copy needs materialised rows and a stride (multiple of 4) covering the ones column");
+  GNNV_REQUIRE(d_X || (d_X16 && d_rowidx), GNNV_ERR_PARAM, "gather: no output rows");
   constexpr int RU = 8;
   const int64_t rows_ub = b->max_n[b->L];
   const int64_t warps = ceil_div(rows_ub, 32);

@@ -345,6 +345,12 @@ struct GemmFwdArgs {
   // multiple of 32); the fp32 rows then only below *keep_rows.  NULL: off
   void* y16 = nullptr;
   int32_t ld16 = 0;
+  // TF32 mode, SAGE: X1 and X2 as bf16 copies ([M x ld16in], columns past
+  // K1 ignored) -- the GEMM then runs kind::f16 over bf16 operands (W
+  // rounded to bf16 per call); X1/X2 unused.  NULL: off
+  const void* X1_16 = nullptr;
+  const void* X2_16 = nullptr;
+  int32_t ld16in = 0;
 };
 void gemm_fwd(const GemmFwdArgs& a, int prec, cudaStream_t s);
 // The trainer's fused L2 push (GemmFwdArgs::push_*): layer i's GEMM
@@ -374,9 +380,10 @@ struct Bf16Io {
   int32_t gsrc16_ld = 0;
   const void* gdst16 = nullptr;    // bwd: this layer's G read as bf16 (stride gdst16_ld)
   int32_t gdst16_ld = 0;
-  // fwd: the aggregation also writes A as bf16 (a16, stride a16_ld); bwd
-  // with x16 (X's dst prefix as bf16, ones column at d_in, stride a16_ld)
-  // and gdst16: dW and db by gemm_dw16
+  // fwd: the aggregation also writes A as bf16 (a16, stride a16_ld) and,
+  // with x16 (X's dst prefix as bf16, ones column at d_in, stride a16_ld),
+  // the GEMM reads [x16 | a16] (kind::f16); bwd with x16, a16 and gdst16:
+  // dW and db by gemm_dw16
   void* a16 = nullptr;
   int32_t a16_ld = 0;
   const void* x16 = nullptr;

@@ -249,6 +249,7 @@ bool gemm_dw_tma(const GemmDwArgs& a, cudaStream_t s);
 void gemm_fwd(const GemmFwdArgs& a, int prec, cudaStream_t s) {
   GNNV_REQUIRE(!a.x1_rows || prec == GNNV_PREC_TF32, GNNV_ERR_UNSUPPORTED, "fwd: indexed X1 rows need the tf32 path");
   GNNV_REQUIRE(!a.push_out || prec == GNNV_PREC_TF32, GNNV_ERR_UNSUPPORTED, "fwd: the fused push needs the tf32 path");
+  GNNV_REQUIRE(!a.X1_16 || prec == GNNV_PREC_TF32, GNNV_ERR_UNSUPPORTED, "fwd: bf16 operand copies need the tf32 path");
   if (prec == GNNV_PREC_FP32) return gemm_fwd_simt(a, s);
   const bool ok = prec == GNNV_PREC_TF32 ? gemm_fwd_tma(a, s) : gemm_fwd_tc(a, s);
   GNNV_REQUIRE(ok, GNNV_ERR_UNSUPPORTED, "tensor-core fwd GEMM: d_out > 252 is not supported");

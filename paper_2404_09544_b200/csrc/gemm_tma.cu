@@ -179,6 +179,16 @@ __device__ __forceinline__ void mma_commit_pair(uint64_t* bar) {
       "[%0], m;\n}\n" ::"r"(smem_u32(bar))
       : "memory");
 }
+__device__ __forceinline__ void mma_f16(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\ntcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(d),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+// kind::f16 instruction descriptor: D=f32, A=B=bf16, M=128, N, majors.
+__device__ __forceinline__ uint32_t idesc_bf16(uint32_t n, bool a_mn, bool b_mn, uint32_t m = BM) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | ((a_mn ? 1u : 0u) << 15) | ((b_mn ? 1u : 0u) << 16) | ((n >> 3) << 17) |
+         ((m >> 4) << 24);
+}
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
                : "memory");
@@ -217,6 +227,7 @@ struct Params {
   CUtensorMap ty1, ty2;  // fwd/dX outputs (TMA stores, SW128 boxes of 32 x 32)
   CUtensorMap ty16;      // fwd: the bf16 copy (unswizzled boxes of 32 x 32 bf16)
   int two;      // A has a second source (SAGE [H_dst | A])
+  int f16;      // fwd: bf16 operands (kind::f16; 64-element k-blocks, same 128-byte rows)
   int nkb1;     // fwd: K blocks served by X1 (ceil(K1/32)); dw: 32-col blocks of X1
   int nkb;      // fwd/dx: K blocks in total
   int BN;       // N per tile (fwd/dx: mult of 16; dw: mult of 32)
@@ -458,14 +469,15 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_tma_gemm(const __grid_constant_
               mbar_arrive_tx(&full[s], (uint32_t)stage_bytes);
             }
             if (g4) __syncwarp();
+            const int kc = (MODE == MODE_FWD && p.f16) ? 2 * BK : BK;  // elements per 128-byte k-block
             if (MODE == MODE_FWD && kb >= p.nkb1) {
-              if (lane == 0) tma_load_2d(sa, &p.ta2, (kb - p.nkb1) * BK, mt * BM, &full[s]);
+              if (lane == 0) tma_load_2d(sa, &p.ta2, (kb - p.nkb1) * kc, mt * BM, &full[s]);
             } else if (g4) {
               tma_gather4(sa + lane * 4 * BKB, &p.ta1, kb * BK, r4[0], r4[1], r4[2], r4[3], &full[s]);
             } else {
-              tma_load_2d(sa, &p.ta1, kb * BK, mt * BM, &full[s]);
+              tma_load_2d(sa, &p.ta1, kb * kc, mt * BM, &full[s]);
             }
-            if (lane == 0) tma_load_2d(sb, &p.tb, kb * BK, nt * BN, &full[s]);
+            if (lane == 0) tma_load_2d(sb, &p.tb, kb * kc, nt * BN, &full[s]);
           }
           if (dyn) {
             int next = 0;
@@ -502,7 +514,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_tma_gemm(const __grid_constant_
         }
         __syncwarp();
       } else if (lane == 0) {
-        const uint32_t idesc = idesc_tf32((uint32_t)BN, false, false);
+        const bool f16 = MODE == MODE_FWD && p.f16;
+        const uint32_t idesc = f16 ? idesc_bf16((uint32_t)BN, false, false) : idesc_tf32((uint32_t)BN, false, false);
         int it = 0, lt = 0;
         for (int tile = blockIdx.x;; tile += gridDim.x, ++lt) {
           if (dyn) {
@@ -521,9 +534,16 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_tma_gemm(const __grid_constant_
             tc_after();
             const uint32_t a0 = smem_u32(smem + (size_t)s * stage_bytes);
             const uint32_t b0 = a0 + a_bytes;
+            // 32 bytes of K per MMA in both kinds (8 tf32 / 16 bf16)
+            if (f16) {
 #pragma unroll
-            for (int k = 0; k < BK / 8; ++k) {
-              mma_tf32(tmem + (uint32_t)(acc * BN), desc_sw(a0 + k * 32, 1024, 2), desc_sw(b0 + k * 32, 1024, 2),
+              for (int k = 0; k < BK / 8; ++k)
+                mma_f16(tmem + (uint32_t)(acc * BN), desc_sw(a0 + k * 32, 1024, 2), desc_sw(b0 + k * 32, 1024, 2),
+                        idesc, (kb > 0 || k > 0) ? 1u : 0u);
+            } else {
+#pragma unroll
+              for (int k = 0; k < BK / 8; ++k)
+                mma_tf32(tmem + (uint32_t)(acc * BN), desc_sw(a0 + k * 32, 1024, 2), desc_sw(b0 + k * 32, 1024, 2),
                          idesc, (kb > 0 || k > 0) ? 1u : 0u);
             }
             mma_commit(&empty[s]);
@@ -1107,6 +1127,25 @@ __global__ void k_bt_fwd(const float* __restrict__ W, int K1, int nkb1, int two,
     Bt[t] = (k >= 0 && n < N) ? W[(int64_t)k * N + n] : 0.f;
   }
 }
+// bf16 fwd B image: Bt16[n][kp] (Npad x Kp), 64-element k-blocks: X1's
+// nkb1 blocks then X2's; columns past K1 in each part are zero (X1's bf16
+// copy may carry a ones column there)
+__global__ void k_bt_fwd16(const float* __restrict__ W, int K1, int nkb1, int two, int N, int Npad, int Kp,
+                           __nv_bfloat16* Bt) {
+  GNNV_PDL_ENTRY();
+  const int total = Npad * Kp;
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < total; t += gridDim.x * blockDim.x) {
+    const int n = t / Kp, kp = t - n * Kp;
+    int k = -1;
+    if (kp < 64 * nkb1) {
+      if (kp < K1) k = kp;
+    } else if (two) {
+      const int kk = kp - 64 * nkb1;
+      if (kk < K1) k = K1 + kk;
+    }
+    Bt[t] = __float2bfloat16_rn((k >= 0 && n < N) ? W[(int64_t)k * N + n] : 0.f);
+  }
+}
 // dX B image: Bd[j][k] (NCpad x Kp): j over [0, ld1) -> W row j (< K1),
 // [ld1, ld1+ld2) -> W row K1 + (j - ld1); k < N.
 __global__ void k_bt_dx(const float* __restrict__ W, int K1, int ld1, int ld2, int two, int N, int NCpad, int Kp,
@@ -1153,12 +1192,12 @@ static CUtensorMap make_map16(const void* base, int64_t rows, int64_t cols, int6
   return m;
 }
 
-// bf16 2-D map with 64 x 64 boxes and the 128-byte swizzle (MN-major UMMA operands)
-static CUtensorMap make_map16_sw(const void* base, int64_t rows, int64_t cols, int64_t ld) {
+// bf16 2-D map with 64-element (128-byte) x box_rows boxes and the 128-byte swizzle (UMMA operands)
+static CUtensorMap make_map16_sw(const void* base, int64_t rows, int64_t cols, int64_t ld, int box_rows = 64) {
   CUtensorMap m;
   const cuuint64_t dims[2] = {(cuuint64_t)std::max<int64_t>(cols, 1), (cuuint64_t)std::max<int64_t>(rows, 1)};
   const cuuint64_t strides[1] = {(cuuint64_t)ld * 2};
-  const cuuint32_t box[2] = {64, 64};
+  const cuuint32_t box[2] = {64, (cuuint32_t)box_rows};
   const cuuint32_t estr[2] = {1, 1};
   CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -1298,11 +1337,6 @@ __device__ __forceinline__ uint64_t desc_mn128(uint32_t saddr, uint32_t lbo, uin
   d |= (uint64_t)1 << 46;
   d |= (uint64_t)2 << 61;  // SWIZZLE_128B
   return d;
-}
-__device__ __forceinline__ void mma_f16(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
-  asm volatile(
-      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\ntcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(d),
-      "l"(a), "l"(b), "r"(idesc), "r"(acc));
 }
 
 struct Dw16Params {
@@ -1457,23 +1491,40 @@ bool gemm_fwd_tma(const GemmFwdArgs& a, cudaStream_t s) {
   using namespace tma;
   const int BN = rup(a.ldy, 16);
   if (BN > 256) return false;
-  const int nkb1 = (a.K1 + BK - 1) / BK;
-  const int nkb = a.X2 ? 2 * nkb1 : nkb1;
-  const int Kp = nkb * BK;
-  float* Bt = (float*)g_img.get((size_t)BN * Kp * sizeof(float), s);
-  launch_k(k_bt_fwd, std::min(1024, (BN * Kp + 255) / 256), 256, 0, s, a.W, a.K1, nkb1, a.X2 ? 1 : 0, a.N, BN, Kp, Bt);
+  const bool f16 = a.X1_16 != nullptr;
+  const int kc = f16 ? 2 * BK : BK;  // elements per k-block
+  const int nkb1 = (a.K1 + kc - 1) / kc;
+  const int nkb = a.X2 || (f16 && a.X2_16) ? 2 * nkb1 : nkb1;
+  const int Kp = nkb * kc;
+  void* Bt = g_img.get((size_t)BN * Kp * (f16 ? 2 : 4), s);
+  if (f16)
+    launch_k(k_bt_fwd16, std::min(1024, (BN * Kp + 255) / 256), 256, 0, s, a.W, a.K1, nkb1, a.X2_16 ? 1 : 0, a.N, BN,
+             Kp, (__nv_bfloat16*)Bt);
+  else
+    launch_k(k_bt_fwd, std::min(1024, (BN * Kp + 255) / 256), 256, 0, s, a.W, a.K1, nkb1, a.X2 ? 1 : 0, a.N, BN, Kp,
+             (float*)Bt);
   GNNV_CHECK_LAUNCH();
   Params p{};
+  p.f16 = f16 ? 1 : 0;
   p.x1_rows = a.x1_rows;
   // CTA pairs (cta_group::2) with GNNV_GEMM_PAIR=1 (read per call).  Off by
   // default: measured on products, layer 1 179 -> 189-192 us (its tiles are
   // bound by the A operand's DRAM reads and the epilogue, not by the W^T
   // traffic the pair halves), layer 2 49 -> 46 us
-  const bool pair = env_on("GNNV_GEMM_PAIR") && !a.x1_rows && !a.push_out && BN % 32 == 0;
-  p.ta1 = a.x1_rows ? make_map(a.X1, a.x1_table_rows, a.K1, a.ld1, 1) : make_map(a.X1, a.max_M, a.K1, a.ld1, BM);
-  p.ta2 = a.X2 ? make_map(a.X2, a.max_M, a.K1, a.ld2, BM) : p.ta1;
-  p.tb = make_map(Bt, BN, Kp, Kp, pair ? BN / 2 : BN);
-  p.two = a.X2 ? 1 : 0;
+  const bool pair = env_on("GNNV_GEMM_PAIR") && !a.x1_rows && !a.push_out && BN % 32 == 0 && !f16;
+  if (f16) {
+    GNNV_REQUIRE(!a.x1_rows && a.ld16in % 8 == 0 && a.ld16in >= a.K1, GNNV_ERR_PARAM,
+                 "fwd: bf16 operands need plain rows with a stride (multiple of 8) covering K1");
+    p.ta1 = make_map16_sw(a.X1_16, a.max_M, a.ld16in, a.ld16in, BM);
+    p.ta2 = a.X2_16 ? make_map16_sw(a.X2_16, a.max_M, a.ld16in, a.ld16in, BM) : p.ta1;
+    p.tb = make_map16_sw(Bt, BN, Kp, Kp, BN);
+    p.two = a.X2_16 ? 1 : 0;
+  } else {
+    p.ta1 = a.x1_rows ? make_map(a.X1, a.x1_table_rows, a.K1, a.ld1, 1) : make_map(a.X1, a.max_M, a.K1, a.ld1, BM);
+    p.ta2 = a.X2 ? make_map(a.X2, a.max_M, a.K1, a.ld2, BM) : p.ta1;
+    p.tb = make_map((const float*)Bt, BN, Kp, Kp, pair ? BN / 2 : BN);
+    p.two = a.X2 ? 1 : 0;
+  }
   p.nkb1 = nkb1;
   p.nkb = nkb;
   p.BN = BN;

@@ -274,8 +274,9 @@ void layer_fwd_impl(gnnv_blocks* b, int32_t layer, const gnnv_layer_desc* ld, co
   if (!agg_ready) {
     if (tl) tl->mark(s, "spmm_fwd" + sfx);
     if (io && io->src16)
-      launch_spmm_fwd_h16(b->d_indptr[h], b->d_indices[h], d_ndst, b->max_n[h], io->src16, io->src16_ld, A, lda,
-                          ld->d_in, ld->kind, ld->aggr, s, io->src16_rows, io->a16, io->a16_ld);
+      launch_spmm_fwd_h16(b->d_indptr[h], b->d_indices[h], d_ndst, b->max_n[h], io->src16, io->src16_ld,
+                          io->x16 && io->a16 ? nullptr : A, lda, ld->d_in, ld->kind, ld->aggr, s, io->src16_rows,
+                          io->a16, io->a16_ld);
     else
       launch_spmm_fwd(b->d_indptr[h], b->d_indices[h], d_ndst, b->max_n[h], rowidx ? agg_table : Hsrc,
                       ld->in_stride, A, lda, ld->d_in, ld->kind, ld->aggr, s, rowidx,
@@ -293,6 +294,11 @@ void layer_fwd_impl(gnnv_blocks* b, int32_t layer, const gnnv_layer_desc* ld, co
     g.ld1 = lda;
     g.X2 = nullptr;
     g.ld2 = 0;
+  }
+  if (io && io->x16 && io->a16 && ld->kind == GNNV_KIND_SAGE) {  // bf16 operand copies (reading Q33)
+    g.X1_16 = io->x16;
+    g.X2_16 = io->a16;
+    g.ld16in = io->a16_ld;
   }
   g.K1 = ld->d_in;
   g.W = W;

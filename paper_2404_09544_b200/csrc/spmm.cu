@@ -538,16 +538,18 @@ __global__ void __launch_bounds__(256, 8) k_spmm_fwd_h16(const int32_t* __restri
 #pragma unroll
           for (int k = 0; k < 8; ++k) acc[k] = denom ? acc[k] / (float)denom : 0.f;
         }
-        float4* out = reinterpret_cast<float4*>(A) + (int64_t)row * lda4 + 2 * c;
-        out[0] = make_float4(acc[0], acc[1], acc[2], acc[3]);
-        if (2 * c + 1 < lda4) out[1] = make_float4(acc[4], acc[5], acc[6], acc[7]);
+        if (A) {
+          float4* out = reinterpret_cast<float4*>(A) + (int64_t)row * lda4 + 2 * c;
+          out[0] = make_float4(acc[0], acc[1], acc[2], acc[3]);
+          if (2 * c + 1 < lda4) out[1] = make_float4(acc[4], acc[5], acc[6], acc[7]);
+        }
         if (A16)  // the bf16 copy the layer's bf16 dW reads (gemm_dw16)
           reinterpret_cast<uint4*>(A16)[(int64_t)row * (lda16 >> 3) + c] =
               make_uint4(pack_bf16x2(acc[0], acc[1]), pack_bf16x2(acc[2], acc[3]), pack_bf16x2(acc[4], acc[5]),
                          pack_bf16x2(acc[6], acc[7]));
       }
     }
-    if (active)  // padding float4s of the output row
+    if (active && A)  // padding float4s of the output row
       for (int c4 = 2 * vec8 + sl; c4 < lda4; c4 += LPR)
         reinterpret_cast<float4*>(A)[(int64_t)row * lda4 + c4] = make_float4(0.f, 0.f, 0.f, 0.f);
   }
@@ -560,6 +562,7 @@ void launch_spmm_fwd_h16(const int32_t* d_indptr, const int32_t* d_indices, cons
   GNNV_REQUIRE(!A16 || (lda16 % 8 == 0 && lda16 >= 8 * vec8), GNNV_ERR_UNSUPPORTED,
                "spmm_fwd_h16: the bf16 output stride must be a multiple of 8 covering d");
   __nv_bfloat16* a16 = static_cast<__nv_bfloat16*>(A16);
+  GNNV_REQUIRE(A || a16, GNNV_ERR_PARAM, "spmm_fwd_h16: no output");
   GNNV_REQUIRE(ld16 % 8 == 0 && ld16 >= 8 * vec8 && lda % 4 == 0, GNNV_ERR_UNSUPPORTED,
                "spmm_fwd_h16: the bf16 row stride must be a multiple of 8 covering d");
   const __nv_bfloat16* H = static_cast<const __nv_bfloat16*>(H16);

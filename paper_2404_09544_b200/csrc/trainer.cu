@@ -90,6 +90,9 @@ struct gnnv_trainer {
   // ones column at d (X16[k]) and the layer-1 aggregation a bf16
   // copy of A^1 (A16[k]); GNNV_NO_DW16=1: the TF32 dW
   bool dw16 = false;
+  // with dw16: layer 1's forward GEMM reads the same bf16 copies (kind::f16,
+  // reading Q33); GNNV_NO_FWD16=1: the TF32 GEMM over the fp32 rows
+  bool fwd16 = false;
   void* X16[2] = {nullptr, nullptr};
   void* A16[2] = {nullptr, nullptr};
   int32_t ld16x = 0;  // their row stride: d + 1 rounded up to 8
@@ -312,6 +315,11 @@ gnnv_status gnnv_trainer_create(gnnv_graph* g, gnnv_cache* c, const gnnv_model_d
       t->dw16 = t->table16 && t->bf16act && !t->x_rows && md->dims[0] + 1 <= 128 && md->dims[1] % 64 == 0 &&
                 md->dims[1] <= 256 && !env_on("GNNV_NO_DW16");
       t->ld16x = (md->dims[0] + 1 + 7) / 8 * 8;
+      t->fwd16 = t->dw16 && !env_on("GNNV_NO_FWD16");
+      if (t->fwd16) {  // layer 1 reads only the bf16 copies: no fp32 X
+        dfree(t->H[0]);
+        t->H[0] = (float*)dmalloc((size_t)g->stride * sizeof(float), "X (unused: bf16 copies)");
+      }
       if (t->dw16) alloc_dw16(t, 0, b);
       t->l2push = !t->bf16act && md->prec == GNNV_PREC_TF32 && md->kind == GNNV_KIND_SAGE && L >= 3 &&
                   env_on("GNNV_L2PUSH");
@@ -359,7 +367,7 @@ int64_t gnnv_trainer_num_params(const gnnv_trainer* t) { return t ? t->nparams :
 gnnv_blocks* gnnv_trainer_blocks(gnnv_trainer* t) { return t ? t->b : nullptr; }
 
 int32_t gnnv_trainer_x_level(const gnnv_trainer* t) {
-  return t ? (t->x_rows ? -1 : t->x_fused ? t->md.L - 1 : t->md.L) : -1;
+  return t ? (t->x_rows || t->fwd16 ? -1 : t->x_fused ? t->md.L - 1 : t->md.L) : -1;
 }
 
 gnnv_status gnnv_trainer_rowidx(const gnnv_trainer* t, const int32_t** d_rowidx, const float** d_table) {
@@ -400,8 +408,9 @@ gnnv_status gnnv_trainer_activation(gnnv_trainer* t, int32_t i, const float** d_
 gnnv_status gnnv_trainer_aggregate(gnnv_trainer* t, int32_t i, const float** d_A, int32_t* stride) {
   return guarded([&] {
     GNNV_REQUIRE(t && d_A && stride && i >= 1 && i <= t->md.L, GNNV_ERR_PARAM, "trainer_aggregate: bad args");
-    *d_A = t->A[i];
-    *stride = row_stride(t->md.dims[i - 1]);
+    const bool none = i == 1 && t->fwd16;  // layer 1 keeps only the bf16 copy (gnnv_trainer_dw16_operands)
+    *d_A = none ? nullptr : t->A[i];
+    *stride = none ? 0 : row_stride(t->md.dims[i - 1]);
   });
 }
 
@@ -434,6 +443,7 @@ gnnv_status gnnv_trainer_gradient16(gnnv_trainer* t, int32_t i, const void** d_G
 }
 
 int32_t gnnv_trainer_dw16(const gnnv_trainer* t) { return t && t->dw16 ? 1 : 0; }
+int32_t gnnv_trainer_fwd16(const gnnv_trainer* t) { return t && t->fwd16 ? 1 : 0; }
 
 gnnv_status gnnv_trainer_dw16_operands(gnnv_trainer* t, const void** d_X16, const void** d_A16, int32_t* ld) {
   return guarded([&] {
@@ -600,7 +610,7 @@ gnnv_status gnnv_trainer_prefetch(gnnv_trainer* t, const int32_t* seeds, int32_t
       if (t->l2push)
         for (int i = 1; i <= t->md.L - 2; ++i) blocks_enable_owner_rows(t->bb[k], t->md.L - i - 1);
       if (t->lastuse) blocks_enable_lastuse(t->bb[k]);
-      const int64_t xrows = t->x_rows ? 1 : t->bb[k]->max_n[t->x_fused ? t->md.L - 1 : t->md.L];
+      const int64_t xrows = t->x_rows || t->fwd16 ? 1 : t->bb[k]->max_n[t->x_fused ? t->md.L - 1 : t->md.L];
       t->X[k] = (float*)dmalloc((size_t)xrows * g->stride * sizeof(float), "X (prefetch)");
       if (t->x_fused)
         t->rowidx[k] = (int32_t*)dmalloc(t->bb[k]->max_n[t->md.L] * sizeof(int32_t), "cache rows of F_L (prefetch)");
@@ -649,8 +659,8 @@ gnnv_status gnnv_trainer_prefetch(gnnv_trainer* t, const int32_t* seeds, int32_t
     GNNV_TRY_CUDA(cudaMemsetAsync(t->d_statsb[k], 0, 4 * sizeof(int64_t), t->side));
     if (tl) tl->mark(t->side, "pf_gather");
     if (t->c->dynamic && t->cache_pending) GNNV_TRY_CUDA(cudaStreamWaitEvent(t->side, t->ev_cache, 0));
-    launch_gather(t->c, t->bb[k], t->X[k], t->d_statsb[k], t->side, t->rowidx[k], !t->x_rows, t->X16[k],
-                  t->ld16x);
+    launch_gather(t->c, t->bb[k], t->fwd16 ? nullptr : t->X[k], t->d_statsb[k], t->side, t->rowidx[k], !t->x_rows,
+                  t->X16[k], t->ld16x);
     if (t->c->dynamic) {  // NEXT-3 admission
       if (tl) tl->mark(t->side, "pf_replace");
       launch_cache_update(t->c, t->bb[k], t->X[k], t->side);
@@ -663,8 +673,8 @@ gnnv_status gnnv_trainer_prefetch(gnnv_trainer* t, const int32_t* seeds, int32_t
       gnnv_blocks* bk = t->bb[k];
       if (t->table16)
         launch_spmm_fwd_h16(bk->d_indptr[h], bk->d_indices[h], bk->d_sizes + h, bk->max_n[h], t->c->d_table16,
-                            t->c->table16_ld, t->A1b[k], row_stride(t->md.dims[0]), t->md.dims[0], t->md.kind,
-                            t->md.aggr, t->side, t->rowidx[k], t->A16[k], t->ld16x);
+                            t->c->table16_ld, t->fwd16 ? nullptr : t->A1b[k], row_stride(t->md.dims[0]),
+                            t->md.dims[0], t->md.kind, t->md.aggr, t->side, t->rowidx[k], t->A16[k], t->ld16x);
       else
         launch_spmm_fwd(bk->d_indptr[h], bk->d_indices[h], bk->d_sizes + h, bk->max_n[h],
                         t->x_fused ? t->table : t->X[k], g->stride, t->A1b[k], row_stride(t->md.dims[0]),
@@ -726,8 +736,8 @@ gnnv_status gnnv_step(gnnv_trainer* t, const int32_t* seeds, int32_t n_seeds, in
       if (tm) GNNV_TRY_CUDA(cudaEventRecord(t->ev[1], s));
       if (tl) tl->mark(s, "gather");
       if (t->c->dynamic && t->cache_pending) GNNV_TRY_CUDA(cudaStreamWaitEvent(s, t->ev_cache, 0));
-      launch_gather(t->c, t->b, t->H[0], t->d_stats, s, t->rowidx[t->cur], !t->x_rows, t->X16[t->cur],
-                    t->ld16x);
+      launch_gather(t->c, t->b, t->fwd16 ? nullptr : t->H[0], t->d_stats, s, t->rowidx[t->cur], !t->x_rows,
+                    t->X16[t->cur], t->ld16x);
       if (t->c->dynamic) {  // NEXT-3 admission (Eq.5's t_replace)
         if (tl) tl->mark(s, "replace");
         launch_cache_update(t->c, t->b, t->H[0], s);
@@ -758,6 +768,7 @@ gnnv_status gnnv_step(gnnv_trainer* t, const int32_t* seeds, int32_t n_seeds, in
         io.src16_rows = t->rowidx[t->cur];
         io.a16 = t->A16[t->cur];
         io.a16_ld = t->ld16x;
+        if (t->fwd16) io.x16 = t->X16[t->cur];
       }
       if (t->bf16act) {
         if (i <= L - 2) {  // this layer's output: a bf16 copy, fp32 rows for the next dst prefix

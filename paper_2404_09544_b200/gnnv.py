@@ -136,6 +136,7 @@ _SIGS = {
     "gnnv_trainer_activation16": (I32, [VP, I32, PP, C.POINTER(I32)]),
     "gnnv_trainer_gradient16": (I32, [VP, I32, PP, C.POINTER(I32)]),
     "gnnv_trainer_dw16": (I32, [VP]),
+    "gnnv_trainer_fwd16": (I32, [VP]),
     "gnnv_trainer_dw16_operands": (I32, [VP, PP, PP, C.POINTER(I32)]),
     "gnnv_step": (I32, [VP, VP, I32, I32, I32, U64, F32, C.POINTER(F32), C.POINTER(StepTiming), VP]),
     "gnnv_trainer_stats": (I32, [VP, VP]),
@@ -595,6 +596,9 @@ class Trainer:
 
     def dw16(self) -> bool:
         return bool(load().gnnv_trainer_dw16(self.h))
+
+    def fwd16(self) -> bool:
+        return bool(load().gnnv_trainer_fwd16(self.h))
 
     def dw16_operands(self):
         """(X16, A16, row stride): layer 1's bf16 dW operands of the last step."""

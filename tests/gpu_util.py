@@ -59,6 +59,24 @@ def read_bf16(p, rows, ld):
     return (w.astype(np.uint32) << 16).view(np.float32).astype(np.float64)
 
 
+def bf16_round(x):
+    """fp32 -> bf16 (round to nearest even, as __float2bfloat16_rn), as float64."""
+    u = np.ascontiguousarray(x, np.float32).view(np.uint32).astype(np.uint64)
+    r = ((u + 0x7FFF + ((u >> 16) & 1)) & 0xFFFF0000).astype(np.uint32)
+    return r.view(np.float32).astype(np.float64)
+
+
+def layer1_aggregate(tr, n_dst):
+    """A^1 of the trainer's last step as stored: the fp32 rows, or -- when
+    layer 1 keeps only the bf16 copy (gnnv_trainer_fwd16, reading Q33) --
+    that copy (as float64)."""
+    pa, sa = tr.aggregate(1)
+    if pa:
+        return read_f32(pa, n_dst, sa)
+    _, p16, ld = tr.dw16_operands()
+    return read_bf16(p16, n_dst, ld)
+
+
 def read_bits(p, rows, words, ncols):
     """A [rows x words] uint32 ReLU bit mask from a device pointer, unpacked
     to bool [rows x ncols] (bit n%32 of word n/32)."""

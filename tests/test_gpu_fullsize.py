@@ -27,8 +27,8 @@ from paper_2404_09544_b200 import gnnv
 from synth import BASE_RNG_SEED, CONFIGS, epoch_seeds, init_weights
 from synth.store import shared_graph
 
-from gpu_util import (_blk, assert_close_cond, blocks_to_host, check_backward_chain, check_forward_chain, lib,
-                      normwise, read_f32, read_i32, sub_block)
+from gpu_util import (_blk, assert_close_cond, bf16_round, blocks_to_host, check_backward_chain, check_forward_chain, lib,
+                      normwise, read_bf16, read_f32, read_i32, sub_block)
 
 pytestmark = pytest.mark.gpu
 
@@ -73,6 +73,13 @@ def check_blocks_and_gather(gd, tr, ref_frontiers, ref_blocks, ratio):
         p0, s0 = tr.activation(0)
         X = read_f32(p0, len(Fx), s0)
         assert X.tobytes() == oracle.gather_rows(gd.feats, Fx).tobytes(), "gathered rows"
+    if tr.dw16():  # layer 1's bf16 operand copy of X's dst prefix: the rounded feature rows + the ones column
+        Fx = ref_frontiers[L - 1]
+        px, _, ld = tr.dw16_operands()
+        X16 = read_bf16(px, len(Fx), ld)
+        Xr = oracle.gather_rows(gd.feats, Fx)[:, : gd.d]
+        np.testing.assert_array_equal(X16[:, : gd.d], bf16_round(Xr), err_msg="bf16 copy of the gathered rows")
+        np.testing.assert_array_equal(X16[:, gd.d], 1.0)
     if ratio == 1.0:
         pr, pt = tr.rowidx()
         ridx = read_i32(pr, len(FL))
