@@ -222,6 +222,38 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
   for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+// tcgen05.ld without the wait (several loads in flight; tmem_wait_ld32
+// then waits and pins the registers after the wait)
+__device__ __forceinline__ void tmem_ld32_nw(uint32_t taddr, uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,"
+      "%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]),
+        "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+        "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr)
+      : "memory");
+}
+__device__ __forceinline__ void tmem_ld16_nw(uint32_t taddr, uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr)
+      : "memory");
+#pragma unroll
+  for (int i = 16; i < 32; ++i) r[i] = 0u;
+}
+__device__ __forceinline__ void tmem_pin32(uint32_t (&r)[32]) {
+  asm volatile(""
+               : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]), "+r"(r[7]),
+                 "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]), "+r"(r[12]), "+r"(r[13]), "+r"(r[14]), "+r"(r[15]),
+                 "+r"(r[16]), "+r"(r[17]), "+r"(r[18]), "+r"(r[19]), "+r"(r[20]), "+r"(r[21]), "+r"(r[22]),
+                 "+r"(r[23]), "+r"(r[24]), "+r"(r[25]), "+r"(r[26]), "+r"(r[27]), "+r"(r[28]), "+r"(r[29]),
+                 "+r"(r[30]), "+r"(r[31]));
+}
+
 struct Params {
   CUtensorMap ta1, ta2, tb;
   CUtensorMap ty1, ty2;  // fwd/dX outputs (TMA stores, SW128 boxes of 32 x 32)
@@ -313,7 +345,7 @@ template <int MODE, bool PAIR = false>
 __global__ void __launch_bounds__(NTHREADS, 1) k_tma_gemm(const __grid_constant__ Params p) {
   GNNV_PDL_ENTRY();
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  __shared__ float s_bias[256];
+  __shared__ __align__(16) float s_bias[256];
   // dynamic tile scheduler (fwd/dX, not PAIR): the producer claims tiles
   // (its CTA's first tile statically, then atomically from p.sched) and
   // publishes each in a ring slot; the MMA and epilogue warps take them in
@@ -642,6 +674,97 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_tma_gemm(const __grid_constant_
             }
           }
         }
+        if (MODE == MODE_FWD && !PAIR && p.y16 && !push) {
+          // forward with the bf16 copy: two 32-column pieces per pass (64
+          // contiguous columns; both TMEM loads in flight, one staging
+          // round and one proxy fence for both bf16 pieces)
+          const uint32_t ob_u32 = smem_u32(ob0);
+          for (int c0 = half * 64; c0 < BN; c0 += 128) {
+            uint32_t r[2][32];
+#pragma unroll
+            for (int h2 = 0; h2 < 2; ++h2) {
+              const int c = c0 + 32 * h2;
+              if (c >= BN) continue;
+              if (BN - c >= 32) tmem_ld32_nw(tbase + c, r[h2]);
+              else tmem_ld16_nw(tbase + c, r[h2]);
+            }
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+            tmem_pin32(r[0]);
+            tmem_pin32(r[1]);
+            const int64_t m = (int64_t)row0 + lane;
+            const bool rag = row0 + 32 > M;
+#pragma unroll
+            for (int h2 = 0; h2 < 2; ++h2) {
+              const int c = c0 + 32 * h2;
+              if (c >= BN) continue;
+              float v[32];
+              uint32_t bits = 0;
+              if (c + 32 <= p.N && p.relu) {  // whole piece inside N: vector bias loads, no column tests
+                const float4* b4 = reinterpret_cast<const float4*>(s_bias + c);
+#pragma unroll
+                for (int j4 = 0; j4 < 8; ++j4) {
+                  const float4 b = b4[j4];
+                  v[4 * j4 + 0] = fmaxf(__uint_as_float(r[h2][4 * j4 + 0]) + b.x, 0.f);
+                  v[4 * j4 + 1] = fmaxf(__uint_as_float(r[h2][4 * j4 + 1]) + b.y, 0.f);
+                  v[4 * j4 + 2] = fmaxf(__uint_as_float(r[h2][4 * j4 + 2]) + b.z, 0.f);
+                  v[4 * j4 + 3] = fmaxf(__uint_as_float(r[h2][4 * j4 + 3]) + b.w, 0.f);
+                }
+#pragma unroll
+                for (int j = 0; j < 32; ++j) bits |= (v[j] > 0.f ? 1u : 0u) << j;
+              } else {
+#pragma unroll
+                for (int j = 0; j < 32; ++j) {
+                  const int n = c + j;
+                  float x = __uint_as_float(r[h2][j]) + (n < BN ? s_bias[n] : 0.f);
+                  if (p.relu) x = fmaxf(x, 0.f);
+                  v[j] = n < p.N ? x : 0.f;
+                  bits |= (v[j] > 0.f ? 1u : 0u) << j;
+                }
+              }
+              if (p.bits && m < M) p.bits[m * p.bits_ld + (c >> 5)] = bits;
+              if (store_rows && rag) {  // ragged fp32 prefix rows: plain stores of the rows < M
+                if (m < M)
+#pragma unroll
+                  for (int j = 0; j < 32; j += 4)
+                    if (c + j < p.ldy)
+                      *reinterpret_cast<float4*>(p.Y + m * p.ldy + c + j) =
+                          make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+              } else if (store_rows) {  // fp32 prefix rows: 4 KB through the staging buffer
+                if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+                __syncwarp();
+#pragma unroll
+                for (int j = 0; j < 8; ++j)
+                  st_shared_v4(ob_u32 + lane * 128 + ((j ^ (lane & 7)) << 4), v[4 * j], v[4 * j + 1], v[4 * j + 2],
+                               v[4 * j + 3]);
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                __syncwarp();
+                if (lane == 0) {
+                  tma_store_2d(&p.ty1, ob0, c, row0);
+                  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+                }
+              }
+              // the bf16 piece: packed into r[h2][0..15] until both are staged
+#pragma unroll
+              for (int q = 0; q < 16; ++q) r[h2][q] = bf16x2(v[2 * q], v[2 * q + 1]);
+            }
+            if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+            __syncwarp();
+#pragma unroll
+            for (int h2 = 0; h2 < 2; ++h2)
+#pragma unroll
+              for (int q = 0; q < 4; ++q)
+                asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(ob_u32 + h2 * 2048 + lane * 64 + q * 16),
+                             "r"(r[h2][4 * q]), "r"(r[h2][4 * q + 1]), "r"(r[h2][4 * q + 2]), "r"(r[h2][4 * q + 3])
+                             : "memory");
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            __syncwarp();
+            if (lane == 0) {
+              for (int h2 = 0; h2 < 2; ++h2)
+                if (c0 + 32 * h2 < BN && c0 + 32 * h2 < p.ld16) tma_store_2d(&p.ty16, ob0 + h2 * 2048, c0 + 32 * h2, row0);
+              asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+            }
+          }
+        } else
         for (int c = half * 32; c < BN; c += 64) {
           float v[32];
           if (BN - c >= 32) tmem_ld32(tbase + c, v);
@@ -705,12 +828,14 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_tma_gemm(const __grid_constant_
           if (MODE == MODE_FWD && !PAIR && p.y16 && !push) {
             // the bf16 copy (every row) -- and the fp32 dst-prefix rows
             // first, if this chunk has any -- through the staging buffer and
-            // TMA stores (32 rows x 64 bytes for the bf16 piece)
+            // TMA stores.  The 2 KB bf16 pieces (32 rows x 64 bytes) alternate
+            // between the buffer's halves, so one may still be read while
+            // the next is written; the 4 KB fp32 piece waits for both
             uint8_t* ob = ob0;
             const uint32_t ob_u32 = smem_u32(ob);
-            if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-            __syncwarp();
             if (store_rows && !ragged) {
+              if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+              __syncwarp();
 #pragma unroll
               for (int j = 0; j < 8; ++j)
                 st_shared_v4(ob_u32 + lane * 128 + ((j ^ (lane & 7)) << 4), v[4 * j], v[4 * j + 1], v[4 * j + 2],
@@ -725,18 +850,22 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_tma_gemm(const __grid_constant_
               __syncwarp();
             }
             if (c < p.ld16) {
+              const uint32_t hb = ob_u32 + (uint32_t)obi * 2048u;
+              if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+              __syncwarp();
 #pragma unroll
               for (int q = 0; q < 4; ++q)
-                asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(ob_u32 + lane * 64 + q * 16),
+                asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(hb + lane * 64 + q * 16),
                              "r"(bf16x2(v[8 * q], v[8 * q + 1])), "r"(bf16x2(v[8 * q + 2], v[8 * q + 3])),
                              "r"(bf16x2(v[8 * q + 4], v[8 * q + 5])), "r"(bf16x2(v[8 * q + 6], v[8 * q + 7]))
                              : "memory");
               asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
               __syncwarp();
               if (lane == 0) {
-                tma_store_2d(&p.ty16, ob, c, row0);
+                tma_store_2d(&p.ty16, ob + obi * 2048, c, row0);
                 asm volatile("cp.async.bulk.commit_group;" ::: "memory");
               }
+              obi ^= 1;
             }
             continue;
           }
