@@ -378,8 +378,8 @@ def algorithmic(seg: str, sizes, cfg, dims, stride, prec, peaks):
         rowb = stride * 4
         lvl = int(sizes.get("x_level", L))
         ld16x = (dims[0] + 1 + 7) & ~7
-        if lvl < 0 and sizes.get("fwd16"):  # whole table cached, layer 1 on bf16 copies: F_{L-1} rows -> bf16 only
-            by = n[L - 1] * (rowb + ld16x * 2) + n[L] * 12
+        if lvl < 0 and sizes.get("fwd16"):  # whole table cached, layer 1 on bf16 copies: F_{L-1} rows
+            by = n[L - 1] * ((dims[0] + 7) & ~7) * 2 + n[L - 1] * ld16x * 2 + n[L] * 12  # of the bf16 table -> X16
         elif lvl < 0:  # whole table cached, layer-1 GEMMs gather H_dst from it: F_L rows resolved, none copied
             by = n[L] * 12
         elif lvl < L:  # whole table cached: rows of F_{L-1} copied, every F_L row resolved to its cache row
