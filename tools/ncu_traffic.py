@@ -12,7 +12,7 @@ k_gather -> "gather", per layer k_spmm_fwd -> "spmm_fwd.l<i>", the forward
 GEMM (+ its weight image) -> "gemm_fwd.l<i>", k_ce_loss -> "loss" (or the
 fused output layer k_tail_a / k_tail_b -> "tail_a.l<L>" / "tail_b.l<L>"), per layer
 from L down: mask pass -> "relu_mask.l<i>", dW GEMM + reductions ->
-"gemm_dw.l<i>", dX GEMM (+ image) -> "gemm_dx.l<i>", the two aggregation
+"gemm_dw.l<i>" (k_tma_dw16 too, with its bf16 G pass), dX GEMM (+ image) -> "gemm_dx.l<i>", the two aggregation
 push passes -> "spmm_bwd.l<i>", k_sgd -> "sgd".  Traffic = dram__bytes_read
 + dram__bytes_write summed over the segment's kernels (ncu replays each
 kernel with cold caches, so this is an upper bound on the in-step traffic).
@@ -116,6 +116,15 @@ def main() -> None:
             b -= 1
             pending_dw = True
             cur = f"relu_mask.l{b}"
+        elif n.startswith("k_tma_dw16"):  # dW over bf16 operands
+            if pending_dw:  # its G -> bf16 + db pass belongs to the same bench segment
+                pending_dw = False
+                m = seg.pop(f"relu_mask.l{b}", None)
+                if m:
+                    seg[f"gemm_dw.l{b}"] = m
+            else:
+                b -= 1
+            cur = f"gemm_dw.l{b}"
         elif n.startswith(("k_tma_gemm<2", "k_tc_gemm<2", "k_gemm_simt")):
             if pending_dw:
                 pending_dw = False
