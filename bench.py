@@ -406,10 +406,13 @@ def algorithmic(seg: str, sizes, cfg, dims, stride, prec, peaks):
     src_b = 2 if (i == 1 and sizes.get("table16", False)) or (b16 and 2 <= i <= L - 1) else 4
     dw16 = i == 1 and sizes.get("dw16", False)  # layer 1's dW over bf16 operands (reading Q32)
     fwd16 = i == 1 and sizes.get("fwd16", False)  # and its forward GEMM (reading Q33): A^1 kept as bf16 only
+    hid16 = 2 <= i <= L - 1 and sizes.get("hid16", False)  # hidden layers' forward GEMM on bf16 (reading Q34)
     if name == "spmm_fwd":
         by = U[h] * d_in * src_b + (0 if fwd16 else n[h] * ((d_in + 3) & ~3) * 4) + nnz[h] * 4 + (n[h] + 1) * 4
         if dw16:  # + the bf16 copy of A^1
             by += n[h] * ((d_in + 7) & ~7) * 2
+        if hid16:  # + the bf16 copy of A^i
+            by += n[h] * ((d_in + 31) & ~31) * 2
         return "hbm", by, "GB/s", peaks["hbm"]
     if name == "spmm_bwd":
         # dA read, block CSR + owner masks read, every dH_src row written once,
@@ -438,19 +441,23 @@ def algorithmic(seg: str, sizes, cfg, dims, stride, prec, peaks):
     out16 = b16 and i <= L - 2  # H^i (and dL/dH^i) kept as bf16, fp32 rows only for the next dst prefix
     if name == "gemm_fwd":
         fl = 2.0 * n[h] * K * d_out
-        by = n[h] * (K * 4 if not fwd16 else (K + 1) * 2) + (n[h] * ld_out * 2 + n[h - 1] * ld_out * 4 if out16 else n[h] * ld_out * 4)
+        by = n[h] * (K * 4 if not (fwd16 or hid16) else (K + 1) * 2 if fwd16 else K * 2) + (n[h] * ld_out * 2 + n[h - 1] * ld_out * 4 if out16 else n[h] * ld_out * 4)
     elif name == "gemm_dx":
         fl = 2.0 * n[h] * K * d_out
-        by = n[h] * d_out * 4 + n[h] * ld_in * (2 if b16 and i - 1 <= L - 2 else 4) + n[h] * ld_in * 4
+        by = n[h] * d_out * (2 if hid16 and sizes.get("hid16_dw") else 4) + n[h] * ld_in * (
+            2 if b16 and i - 1 <= L - 2 else 4) + n[h] * ld_in * 4
     elif name == "gemm_dw":
         fl = 2.0 * n[h] * (K + 1) * d_out
         by = n[h] * (K * 4 if not dw16 else (K + 1) * 2) + n[h] * d_out * (2 if out16 else 4)
+        if hid16 and sizes.get("hid16_dw"):  # G (fp32) -> bf16 copy + db, then dW over [H16 | A16] and G16
+            by = n[h] * K * 2 + n[h] * d_out * (4 + 2 + 2)
     else:
         return None
     if prec == "fp32":
         return "alu", fl, "TFLOP/s", FP32_SIMT_TFLOPS
     # tensor-core modes: the binding roof is the larger of the two times
-    bf16_op = (dw16 and name == "gemm_dw") or (fwd16 and name == "gemm_fwd")
+    bf16_op = ((dw16 or (hid16 and sizes.get("hid16_dw"))) and name in ("gemm_dw", "gemm_dx")) or (
+        (fwd16 or hid16) and name == "gemm_fwd")
     tpeak = peaks["bf16_sust"] * (0.5 if prec == "tf32" and not bf16_op else 1.0)  # tf32 = 1/2 bf16 rate (guide)
     if by / (peaks["hbm"] * 1e9) >= fl / (tpeak * 1e12):
         return "hbm", by, "GB/s", peaks["hbm"]
@@ -691,6 +698,8 @@ def main():
     sizes["table16"] = tr.table16()
     sizes["dw16"] = tr.dw16()
     sizes["fwd16"] = tr.fwd16()
+    sizes["hid16"] = L >= 3 and bool(tr.aggregate16(2)[0])
+    sizes["hid16_dw"] = L >= 3 and bool(tr.gradient16(L - 1)[0])
     peaks = load_peaks()
     if sizes["misses"] > 0:
         peaks["host"] = measure_host_link()
@@ -804,12 +813,14 @@ def main():
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": {"fp32": "f32", "bf16": "f32+bf16gemm", "tf32": "f32+tf32gemm"}[args.prec] + (
                 "+bf16act" if bf16act else "") + ("+bf16table" if bf16tab else "") + (
-                "+bf16dw1" if tr.dw16() else "") + ("+bf16fwd1" if tr.fwd16() else ""), "data": "synthetic",
+                "+bf16dw1" if tr.dw16() else "") + ("+bf16fwd1" if tr.fwd16() else "") + (
+                "+bf16fwd2" if sizes["hid16"] else ""), "data": "synthetic",
             "config": config_of(cfg, gd, world, args.kind),
             "settings": {"placement": args.placement, "locality_bias": args.locality_bias,
                          "cache_policy": args.policy, "gemm_precision": args.prec,
                          "bf16_intermediates": bf16act, "bf16_table_layer1": tr.table16(),
                          "bf16_dw_layer1": tr.dw16(), "bf16_fwd_layer1": tr.fwd16(),
+                         "bf16_fwd_hidden": sizes["hid16"],
                          "gathered_x_mb_per_step": sizes["n"][L] * gd.stride * 4 / 1e6,
                          "pipeline": "eq4-overlap (next batch sample+gather on a side stream)" if pipeline else "off"},
             "step_stats": step_stats,

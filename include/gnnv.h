@@ -423,8 +423,10 @@ int32_t gnnv_trainer_table16(const gnnv_trainer* t);
 /* The bf16 copy of H^i (1..L-2) of the last step: [rows x *ld] bf16
  * (borrowed device pointer), NULL and 0 when the trainer keeps none. */
 gnnv_status gnnv_trainer_activation16(gnnv_trainer* t, int32_t i, const void** d_H16, int32_t* ld);
-/* The bf16 copy of dL/dH^i (1..L-2, after the ReLU mask) the last step's
- * layer-i dW read: [rows x *ld] bf16, NULL and 0 when the trainer keeps none. */
+/* The bf16 copy of dL/dH^i (after the ReLU mask) the last step's layer-i
+ * dW read -- i <= L-2 with bf16 intermediates (reading Q30), hidden layers
+ * 2..L-1 with their bf16 dW (reading Q34): [rows x *ld] bf16, NULL and 0
+ * when the trainer keeps none. */
 gnnv_status gnnv_trainer_gradient16(gnnv_trainer* t, int32_t i, const void** d_G16, int32_t* ld);
 /* 1 if layer 1's dW runs over bf16 operands (gemm_dw16: bf16act and
  * table16, d_in + 1 <= 128, hidden a multiple of 64 up to 256, unless
@@ -436,6 +438,12 @@ int32_t gnnv_trainer_dw16(const gnnv_trainer* t);
  * [X16 | A16] and W rounded to bf16; with gnnv_trainer_dw16, unless
  * GNNV_NO_FWD16; reading Q33). */
 int32_t gnnv_trainer_fwd16(const gnnv_trainer* t);
+/* The bf16 copy of layer i's aggregate A^i the last step's kind::f16 GEMMs
+ * read: layer 1 with gnnv_trainer_dw16 (reading Q32), hidden layers
+ * 2..L-1 of a bf16-intermediate trainer unless GNNV_NO_HID16 (their forward
+ * GEMM reads [bf16 H^{i-1} dst prefix | this copy], reading Q34): [n_dst x
+ * *ld] bf16, NULL and 0 when there is none. */
+gnnv_status gnnv_trainer_aggregate16(gnnv_trainer* t, int32_t i, const void** d_A16, int32_t* ld);
 gnnv_status gnnv_trainer_dw16_operands(gnnv_trainer* t, const void** d_X16, const void** d_A16, int32_t* ld);
 
 /* One iteration of Algorithm 1 on this rank's seed slice:

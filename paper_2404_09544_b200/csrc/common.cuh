@@ -387,6 +387,11 @@ struct Bf16Io {
   void* a16 = nullptr;
   int32_t a16_ld = 0;
   const void* x16 = nullptr;
+  bool keep_a32 = false;  // fwd with x16: still write the fp32 A (a TF32 dW reads it)
+  // bwd with x16 and a16, G pre-masked fp32: write G's bf16 copy here (stride
+  // g16_ld) and run dW over bf16 (gemm_dw16; db by the conversion pass)
+  void* g16_out = nullptr;
+  int32_t g16_ld = 0;
 };
 // Layer 1 of the trainer with the whole feature table on the device: H_dst
 // (X's dst prefix) is read by the TF32 GEMMs straight from the table through
@@ -425,18 +430,29 @@ struct GemmDwArgs {
 };
 void gemm_dw(const GemmDwArgs& a, int prec, cudaStream_t s);
 size_t gemm_dw_partial_floats(int32_t rows_plus_bias, int32_t N, int32_t* splits_out, int64_t max_M);
-// dW = [X16 | A16]^T G16 (+ db from X16's ones column K1) over bf16 operands,
-// MN-major on kind::f16 (gemm_tma.cu k_tma_dw16); K1 + 1 <= 128, N a
-// multiple of 64 up to 256
+// dW = [S_0 | S_1]^T G16 over bf16 operands, MN-major on kind::f16
+// (gemm_tma.cu k_tma_dw16): source s ([rows x ld] bf16, `width` features)
+// fills dW rows out_row0 .. out_row0 + width; with `ones` its column
+// `width` holds 1.0 and the same MMAs give db = colsum(G16).  Widths up to
+// 256 (at most four 128-feature tiles), N a multiple of 64 up to 256.
+struct GemmDw16Src {
+  const void* p = nullptr;
+  int32_t ld = 0, width = 0, out_row0 = 0;
+  bool ones = false;
+};
 struct GemmDw16Args {
-  const void *X16, *A16;  // [rows x ldx] bf16, column K1 of X16 = 1.0
-  int32_t ldx, K1;
-  const void* G16;        // [rows x ldg] bf16
+  GemmDw16Src src[2];
+  const void* G16;  // [rows x ldg] bf16
   int32_t ldg, N;
   const int32_t* d_M;
   int64_t max_M;
-  float *dW, *db;
+  float* dW;  // rows: src widths summed
+  float* db;  // with a ones source or G32; else untouched (may be NULL)
   bool zeroed = false;
+  // G32 set: G16 is first written from this pre-masked fp32 G ([rows x
+  // ldg32]) by the same call, which also sums db = colsum(G32)
+  const float* G32 = nullptr;
+  int32_t ldg32 = 0;
 };
 void gemm_dw16(const GemmDw16Args& a, cudaStream_t s);
 struct GemmDxArgs {  // [Y1 | Y2] = G W^T  (Y1 = first K1 cols, Y2 = the rest)
@@ -451,6 +467,10 @@ struct GemmDxArgs {  // [Y1 | Y2] = G W^T  (Y1 = first K1 cols, Y2 = the rest)
   const uint32_t* y1_bits = nullptr;
   int32_t y1_bits_ld = 0;
   void* Y1_16 = nullptr;  // TF32: Y1 stored as bf16 (row stride ld1, ld1 % 32 == 0) instead of Y1
+  // TF32 mode: G as a bf16 copy ([M x ldg16]) -- the GEMM then runs kind::f16
+  // with W rounded to bf16 (reading Q34); G unused.  NULL: off
+  const void* G16 = nullptr;
+  int32_t ldg16 = 0;
 };
 void gemm_dx(const GemmDxArgs& a, int prec, cudaStream_t s);
 // tail.cu: the trainer's output layer (forward, loss, backward) fused

@@ -255,6 +255,7 @@ void gemm_fwd(const GemmFwdArgs& a, int prec, cudaStream_t s) {
   GNNV_REQUIRE(ok, GNNV_ERR_UNSUPPORTED, "tensor-core fwd GEMM: d_out > 252 is not supported");
 }
 void gemm_dx(const GemmDxArgs& a, int prec, cudaStream_t s) {
+  GNNV_REQUIRE(!a.G16 || prec == GNNV_PREC_TF32, GNNV_ERR_UNSUPPORTED, "dX: a bf16 G copy needs the tf32 path");
   if (prec == GNNV_PREC_FP32) return gemm_dx_simt(a, s);
   const bool ok = prec == GNNV_PREC_TF32 ? gemm_dx_tma(a, s) : gemm_dx_tc(a, s);
   GNNV_REQUIRE(ok, GNNV_ERR_UNSUPPORTED, "tensor-core dX GEMM: unsupported shape");

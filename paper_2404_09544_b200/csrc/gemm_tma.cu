@@ -501,7 +501,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_tma_gemm(const __grid_constant_
               mbar_arrive_tx(&full[s], (uint32_t)stage_bytes);
             }
             if (g4) __syncwarp();
-            const int kc = (MODE == MODE_FWD && p.f16) ? 2 * BK : BK;  // elements per 128-byte k-block
+            const int kc = p.f16 ? 2 * BK : BK;  // elements per 128-byte k-block
             if (MODE == MODE_FWD && kb >= p.nkb1) {
               if (lane == 0) tma_load_2d(sa, &p.ta2, (kb - p.nkb1) * kc, mt * BM, &full[s]);
             } else if (g4) {
@@ -546,7 +546,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_tma_gemm(const __grid_constant_
         }
         __syncwarp();
       } else if (lane == 0) {
-        const bool f16 = MODE == MODE_FWD && p.f16;
+        const bool f16 = p.f16 != 0;
         const uint32_t idesc = f16 ? idesc_bf16((uint32_t)BN, false, false) : idesc_tf32((uint32_t)BN, false, false);
         int it = 0, lt = 0;
         for (int tile = blockIdx.x;; tile += gridDim.x, ++lt) {
@@ -1275,6 +1275,22 @@ __global__ void k_bt_fwd16(const float* __restrict__ W, int K1, int nkb1, int tw
     Bt[t] = __float2bfloat16_rn((k >= 0 && n < N) ? W[(int64_t)k * N + n] : 0.f);
   }
 }
+// bf16 dX B image: as k_bt_dx, bf16 (64-element k-blocks)
+__global__ void k_bt_dx16(const float* __restrict__ W, int K1, int ld1, int ld2, int two, int N, int NCpad, int Kp,
+                          __nv_bfloat16* Bd) {
+  GNNV_PDL_ENTRY();
+  const int total = NCpad * Kp;
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < total; t += gridDim.x * blockDim.x) {
+    const int j = t / Kp, k = t - j * Kp;
+    int r = -1;
+    if (j < ld1) {
+      if (j < K1) r = j;
+    } else if (two && j - ld1 < ld2 && j - ld1 < K1) {
+      r = K1 + (j - ld1);
+    }
+    Bd[t] = __float2bfloat16_rn((r >= 0 && k < N) ? W[(int64_t)r * N + k] : 0.f);
+  }
+}
 // dX B image: Bd[j][k] (NCpad x Kp): j over [0, ld1) -> W row j (< K1),
 // [ld1, ld1+ld2) -> W row K1 + (j - ld1); k < N.
 __global__ void k_bt_dx(const float* __restrict__ W, int K1, int ld1, int ld2, int two, int N, int NCpad, int Kp,
@@ -1366,6 +1382,8 @@ struct Arena {
   }
 };
 static Arena g_img;
+static Arena g_dwpart;  // gemm_dw16's per-CTA slices
+static Arena g_dbpart;  // its G conversion's per-block column sums
 
 static size_t smem_bytes(int mode, int BN, int mask, int nwp, bool pair = false, int g16 = 0) {
   const int S = mode == MODE_DW ? (g16 ? DW_STAGES16 : DW_STAGES) : pair ? PAIR_STAGES : FWD_STAGES;
@@ -1468,12 +1486,24 @@ __device__ __forceinline__ uint64_t desc_mn128(uint32_t saddr, uint32_t lbo, uin
   return d;
 }
 
+// one 128-feature M tile: features [col0, col0 + 128) of a bf16 source
+// (two 64-feature boxes); TMEM lane r -> dW row out_row0 + r for r <
+// out_rows, lane db_row -> db (the source's ones column; -1: none)
+struct Dw16Tile {
+  CUtensorMap map;
+  int col0, out_row0, out_rows, db_row;
+};
 struct Dw16Params {
-  CUtensorMap tx, ta, tg;  // bf16: X16, A16 [rows x ldx] and G16 [rows x ldg], boxes of 64 x 64, SW128
+  Dw16Tile tile[4];      // CTA group g = blockIdx.y takes tiles 2g and 2g + 1
+  CUtensorMap tg;        // G16 [rows x ldg], boxes of 64 x 64, SW128
   const int32_t* dM;
-  unsigned int* sched;  // the launch's chunk counter (g_sched slot)
-  int K1, N, BN, splits;
+  unsigned int* sched[2];  // each group's chunk counter (g_sched slots)
+  int N, BN;
   float *dW, *db;
+  // CTA x's sums go to part[x][row][N] (row = dW row, db at prow - 1) with
+  // plain stores; k_dw16_reduce adds the CTAs' slices in a fixed order
+  float* part;
+  int prow;
 };
 
 __global__ void __launch_bounds__(NTHREADS, 1) k_tma_dw16(const __grid_constant__ Dw16Params p) {
@@ -1494,6 +1524,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_tma_dw16(const __grid_constant_
   const int M = *p.dM;
   const int nkbm = (M + DW16_KR - 1) / DW16_KR;
   const int nchunks = (nkbm + DW16_CHUNK - 1) / DW16_CHUNK;
+  const int grp = blockIdx.y;
+  const Dw16Tile& T0 = p.tile[2 * grp];
+  const Dw16Tile& T1 = p.tile[2 * grp + 1];
+  unsigned int* sched = p.sched[grp];
   // chunks of DW16_CHUNK k-blocks: chunk blockIdx.x first, then claimed from
   // the launch's counter -- a CTA slowed by a co-resident kernel (the Eq.4
   // prefetch) takes fewer; every CTA keeps its sums in TMEM and flushes once
@@ -1507,8 +1541,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_tma_dw16(const __grid_constant_
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 0 && lane == 0) {
-    tma_prefetch(&p.tx);
-    tma_prefetch(&p.ta);
+    tma_prefetch(&T0.map);
+    tma_prefetch(&T1.map);
     tma_prefetch(&p.tg);
   }
   if (warp == 1) {
@@ -1523,7 +1557,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_tma_dw16(const __grid_constant_
   if (warp == 0) {
     if (lane == 0) {
       int i = 0;
-      for (int c = blockIdx.x; c < nchunks; c = (int)gridDim.x + (int)atomicAdd(p.sched, 1u)) {
+      for (int c = blockIdx.x; c < nchunks; c = (int)gridDim.x + (int)atomicAdd(sched, 1u)) {
         const int kb_end = min(nkbm, (c + 1) * DW16_CHUNK);
         for (int kb = c * DW16_CHUNK; kb < kb_end; ++kb, ++i) {
           const int s = i % S;
@@ -1532,10 +1566,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_tma_dw16(const __grid_constant_
           if (i >= S) mbar_wait(&empty[s], ((i / S) & 1) ^ 1);
           s_kb[s] = kb;
           mbar_arrive_tx(&full[s], (uint32_t)stage_bytes);
-          tma_load_2d(st, &p.tx, 0, row, &full[s]);
-          tma_load_2d(st + DW16_BOX, &p.tx, 64, row, &full[s]);
-          tma_load_2d(st + 2 * DW16_BOX, &p.ta, 0, row, &full[s]);
-          tma_load_2d(st + 3 * DW16_BOX, &p.ta, 64, row, &full[s]);
+          tma_load_2d(st, &T0.map, T0.col0, row, &full[s]);
+          tma_load_2d(st + DW16_BOX, &T0.map, T0.col0 + 64, row, &full[s]);
+          tma_load_2d(st + 2 * DW16_BOX, &T1.map, T1.col0, row, &full[s]);
+          tma_load_2d(st + 3 * DW16_BOX, &T1.map, T1.col0 + 64, row, &full[s]);
           for (int j = 0; j < nb; ++j) tma_load_2d(st + a_bytes + j * DW16_BOX, &p.tg, 64 * j, row, &full[s]);
         }
       }
@@ -1585,25 +1619,42 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_tma_dw16(const __grid_constant_
       else mbar_arrive(tfull);
     }
     __syncwarp();
-  } else if (any) {
-    mbar_wait(tfull, 0);
-    tc_after();
+  } else if (any || p.part) {
+    if (any) {
+      mbar_wait(tfull, 0);
+      tc_after();
+    }
     const int q = warp & 3;
     const int half = (warp - 2) >> 2;
     const int r = q * 32 + lane;  // TMEM lane = row of the 128-row tile
     for (int mt = 0; mt < 2; ++mt) {
+      const Dw16Tile& T = mt ? T1 : T0;
       float* dst = nullptr;
-      if (mt == 0 && r < p.K1) dst = p.dW + (int64_t)r * p.N;
-      else if (mt == 0 && r == p.K1) dst = p.db;  // the ones column
-      else if (mt == 1 && r < p.K1) dst = p.dW + (int64_t)(p.K1 + r) * p.N;
+      if (p.part) {  // this CTA's slice (a CTA without chunks writes zeros)
+        float* slice = p.part + (int64_t)blockIdx.x * p.prow * p.N;
+        if (r < T.out_rows) dst = slice + (int64_t)(T.out_row0 + r) * p.N;
+        else if (r == T.db_row) dst = slice + (int64_t)(p.prow - 1) * p.N;
+      } else {
+        if (r < T.out_rows) dst = p.dW + (int64_t)(T.out_row0 + r) * p.N;
+        else if (r == T.db_row) dst = p.db;  // the source's ones column
+      }
       for (int c = half * 32; c < BN; c += 64) {
         float v[32];
-        tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(mt * BN + c), v);
-        if (!dst) continue;
+        if (any) tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(mt * BN + c), v);
+        else
 #pragma unroll
-        for (int j = 0; j < 32; j += 4)
-          if (c + j < p.N)
-            atomicAdd(reinterpret_cast<float4*>(dst + c + j), make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]));
+          for (int j = 0; j < 32; ++j) v[j] = 0.f;
+        if (!dst) continue;
+        if (p.part) {
+#pragma unroll
+          for (int j = 0; j < 32; j += 4)
+            if (c + j < p.N) __stcg(reinterpret_cast<float4*>(dst + c + j), make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]));
+        } else {
+#pragma unroll
+          for (int j = 0; j < 32; j += 4)
+            if (c + j < p.N)
+              atomicAdd(reinterpret_cast<float4*>(dst + c + j), make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]));
+        }
       }
     }
   }
@@ -1611,7 +1662,108 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_tma_dw16(const __grid_constant_
   __syncthreads();
   if (warp == 1)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2 * 256) : "memory");
-  if (threadIdx.x == 0) sched_done(p.sched);
+  if (threadIdx.x == 0) {  // the group's last CTA resets its counter
+    __threadfence();
+    if (atomicAdd(sched + 1, 1u) == gridDim.x - 1) {
+      sched[0] = 0u;
+      sched[1] = 0u;
+      __threadfence();
+    }
+  }
+}
+
+// G (fp32, already masked) -> its bf16 copy, and per-block column sums
+// (db's partials, summed by k_dw16_reduce in block order): 4 rows of 64
+// float4 columns per pass, four rows per thread in flight
+__global__ void __launch_bounds__(256) k_g16_colsum(const float* __restrict__ G, int ldg, const int32_t* d_M, int N,
+                                                    __nv_bfloat16* __restrict__ G16, int ld16, float* __restrict__ dbp) {
+  GNNV_PDL_ENTRY();
+  __shared__ float4 s_acc[256];
+  const int M = *d_M;
+  const int n4 = N >> 2;  // <= 64
+  const int rg = threadIdx.x >> 6, c4 = threadIdx.x & 63;
+  const int per = (M + gridDim.x - 1) / gridDim.x;
+  const int r0 = min(M, (int)blockIdx.x * per), r1 = min(M, r0 + per);
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (c4 < n4) {
+    for (int r = r0 + rg; r < r1; r += 16) {
+      float4 g[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        g[u] = r + 4 * u < r1 ? __ldg(reinterpret_cast<const float4*>(G + (int64_t)(r + 4 * u) * ldg) + c4)
+                              : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        if (r + 4 * u >= r1) continue;
+        const __nv_bfloat162 lo = __floats2bfloat162_rn(g[u].x, g[u].y), hi = __floats2bfloat162_rn(g[u].z, g[u].w);
+        reinterpret_cast<uint2*>(G16 + (int64_t)(r + 4 * u) * ld16)[c4] =
+            make_uint2(*reinterpret_cast<const uint32_t*>(&lo), *reinterpret_cast<const uint32_t*>(&hi));
+        acc.x += g[u].x; acc.y += g[u].y; acc.z += g[u].z; acc.w += g[u].w;
+      }
+    }
+  }
+  s_acc[threadIdx.x] = acc;
+  __syncthreads();
+  if (rg == 0 && c4 < n4) {
+    float4 t = s_acc[c4];
+    for (int q = 1; q < 4; ++q) {
+      const float4 u = s_acc[q * 64 + c4];
+      t.x += u.x; t.y += u.y; t.z += u.z; t.w += u.w;
+    }
+    reinterpret_cast<float4*>(dbp)[(int64_t)blockIdx.x * n4 + c4] = t;
+  }
+}
+
+// dW (and db) = the CTAs' slices summed in a fixed order (deterministic): a
+// block takes 32 float4 columns-chunks x 8 slice groups; thread (e, g) sums
+// slices g, g + 8, ... of element e (four loads in flight), then the 8 group
+// sums are added in group order through shared memory
+__global__ void __launch_bounds__(256) k_dw16_reduce(const float* __restrict__ part, int splits, int prow, int N,
+                                                     int has_db, float* __restrict__ dW, float* __restrict__ db,
+                                                     const float* __restrict__ dbp, int ndbp) {
+  GNNV_PDL_ENTRY();
+  __shared__ float4 s_acc[8][33];
+  const int n4 = N >> 2;
+  const int64_t total = (int64_t)prow * n4, slice4 = (int64_t)prow * n4;
+  const int e = threadIdx.x & 31, g = threadIdx.x >> 5;
+  for (int64_t t0 = blockIdx.x * 32ll; t0 < total; t0 += (int64_t)gridDim.x * 32) {
+    const int64_t t = t0 + e;
+    const int row = t < total ? (int)(t / n4) : 0;
+    const bool dbrow = t < total && row == prow - 1;
+    const float4* P = reinterpret_cast<const float4*>(dbrow && dbp ? dbp : part);
+    const int64_t stride = dbrow && dbp ? n4 : slice4;
+    const int64_t off = dbrow && dbp ? t - (int64_t)row * n4 : t;
+    const int cnt = dbrow && dbp ? ndbp : splits;
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (t < total && (!dbrow || has_db)) {
+      int sidx = g;
+      for (; sidx + 24 < cnt; sidx += 32) {
+        const float4 a = __ldcg(P + (int64_t)sidx * stride + off), b = __ldcg(P + (int64_t)(sidx + 8) * stride + off);
+        const float4 c = __ldcg(P + (int64_t)(sidx + 16) * stride + off), d = __ldcg(P + (int64_t)(sidx + 24) * stride + off);
+        acc.x += a.x; acc.y += a.y; acc.z += a.z; acc.w += a.w;
+        acc.x += b.x; acc.y += b.y; acc.z += b.z; acc.w += b.w;
+        acc.x += c.x; acc.y += c.y; acc.z += c.z; acc.w += c.w;
+        acc.x += d.x; acc.y += d.y; acc.z += d.z; acc.w += d.w;
+      }
+      for (; sidx < cnt; sidx += 8) {
+        const float4 a = __ldcg(P + (int64_t)sidx * stride + off);
+        acc.x += a.x; acc.y += a.y; acc.z += a.z; acc.w += a.w;
+      }
+    }
+    s_acc[g][e] = acc;
+    __syncthreads();
+    if (g == 0 && t < total && (!dbrow || has_db)) {
+      float4 r = s_acc[0][e];
+#pragma unroll
+      for (int q = 1; q < 8; ++q) {
+        const float4 u = s_acc[q][e];
+        r.x += u.x; r.y += u.y; r.z += u.z; r.w += u.w;
+      }
+      float4* out = dbrow ? reinterpret_cast<float4*>(db) + (t - (int64_t)row * n4) : reinterpret_cast<float4*>(dW) + t;
+      *out = r;
+    }
+    __syncthreads();
+  }
 }
 
 }  // namespace tma
@@ -1698,17 +1850,30 @@ bool gemm_dx_tma(const GemmDxArgs& a, cudaStream_t s) {
   const int NC = a.Y2 ? a.ld1 + a.ld2 : a.ld1;
   const int ntl = (NC + 255) / 256;
   const int BN = rup((NC + ntl - 1) / ntl, 32);  // whole 32-column epilogue chunks
-  const int nkb = (a.N + BK - 1) / BK;
-  const int Kp = nkb * BK;
+  const bool f16 = a.G16 != nullptr;
+  const int kc = f16 ? 2 * BK : BK;
+  const int nkb = (a.N + kc - 1) / kc;
+  const int Kp = nkb * kc;
   const int NCpad = ntl * BN;
-  float* Bd = (float*)g_img.get((size_t)NCpad * Kp * sizeof(float), s);
-  launch_k(k_bt_dx, std::min(1024, (NCpad * Kp + 255) / 256), 256, 0, s, a.W, a.K1, a.ld1, a.ld2, a.Y2 ? 1 : 0, a.N, NCpad,
-                                                                    Kp, Bd);
+  void* Bd = g_img.get((size_t)NCpad * Kp * (f16 ? 2 : 4), s);
+  if (f16)
+    launch_k(k_bt_dx16, std::min(1024, (NCpad * Kp + 255) / 256), 256, 0, s, a.W, a.K1, a.ld1, a.ld2, a.Y2 ? 1 : 0, a.N,
+             NCpad, Kp, (__nv_bfloat16*)Bd);
+  else
+    launch_k(k_bt_dx, std::min(1024, (NCpad * Kp + 255) / 256), 256, 0, s, a.W, a.K1, a.ld1, a.ld2, a.Y2 ? 1 : 0, a.N,
+             NCpad, Kp, (float*)Bd);
   GNNV_CHECK_LAUNCH();
   Params p{};
-  p.ta1 = make_map(a.G, a.max_M, a.N, a.ldg, BM);
+  p.f16 = f16 ? 1 : 0;
+  if (f16) {
+    GNNV_REQUIRE(a.ldg16 % 8 == 0 && a.ldg16 >= a.N, GNNV_ERR_PARAM, "dX: the bf16 G stride must be a multiple of 8 >= N");
+    p.ta1 = make_map16_sw(a.G16, a.max_M, a.N, a.ldg16, BM);
+    p.tb = make_map16_sw(Bd, NCpad, Kp, Kp, BN);
+  } else {
+    p.ta1 = make_map(a.G, a.max_M, a.N, a.ldg, BM);
+    p.tb = make_map((const float*)Bd, NCpad, Kp, Kp, BN);
+  }
   p.ta2 = p.ta1;
-  p.tb = make_map(Bd, NCpad, Kp, Kp, BN);
   p.nkb1 = nkb;
   p.nkb = nkb;
   p.BN = BN;
@@ -1740,33 +1905,74 @@ bool gemm_dx_tma(const GemmDxArgs& a, cudaStream_t s) {
 // column-sum kernel in layers.cu).
 void gemm_dw16(const GemmDw16Args& a, cudaStream_t s) {
   using namespace tma;
-  GNNV_REQUIRE(a.K1 + 1 <= 128 && a.N % 64 == 0 && a.N <= 256 && a.ldx % 8 == 0 && a.ldx >= a.K1 + 1 &&
-                   a.ldg % 8 == 0 && a.ldg >= a.N,
-               GNNV_ERR_UNSUPPORTED, "dw16: K1 + 1 <= 128, N % 64 == 0 and N <= 256, strides multiples of 8");
+  GNNV_REQUIRE(a.N % 64 == 0 && a.N <= 256 && a.ldg % 8 == 0 && a.ldg >= a.N, GNNV_ERR_UNSUPPORTED,
+               "dw16: N % 64 == 0 and N <= 256, G stride a multiple of 8");
   Dw16Params p{};
-  p.tx = make_map16_sw(a.X16, a.max_M, a.ldx, a.ldx);
-  p.ta = make_map16_sw(a.A16, a.max_M, a.ldx, a.ldx);
+  int nt = 0, rows = 0;
+  bool has_db = false;
+  for (const GemmDw16Src& sr : a.src) {
+    if (!sr.p) continue;
+    const int w1 = sr.width + (sr.ones ? 1 : 0);
+    GNNV_REQUIRE(sr.ld % 8 == 0 && sr.ld >= w1 && nt + (w1 + 127) / 128 <= 4, GNNV_ERR_UNSUPPORTED,
+                 "dw16: source strides multiples of 8 covering the width (+ ones), at most four 128-feature tiles");
+    const CUtensorMap m = make_map16_sw(sr.p, a.max_M, sr.ld, sr.ld);
+    for (int j = 0; 128 * j < w1; ++j) {
+      Dw16Tile& T = p.tile[nt++];
+      T.map = m;
+      T.col0 = 128 * j;
+      T.out_row0 = sr.out_row0 + 128 * j;
+      T.out_rows = std::max(0, std::min(128, sr.width - 128 * j));
+      T.db_row = (sr.ones && sr.width >= 128 * j && sr.width < 128 * j + 128) ? sr.width - 128 * j : -1;
+    }
+    rows += sr.width;
+    has_db = has_db || sr.ones;
+  }
+  GNNV_REQUIRE(nt > 0 && (!has_db || a.db) && (!a.G32 || (a.db && !has_db && a.ldg32 % 4 == 0)), GNNV_ERR_PARAM,
+               "dw16: no source, a ones column without db, or G32 without db / with a ones column");
+  if (nt & 1) {  // the last group's second tile: stages the same boxes, stores nothing
+    p.tile[nt] = p.tile[nt - 1];
+    p.tile[nt].out_rows = 0;
+    p.tile[nt].db_row = -1;
+    ++nt;
+  }
+  const int groups = nt / 2;
   p.tg = make_map16_sw(a.G16, a.max_M, a.N, a.ldg);
   p.dM = a.d_M;
-  p.K1 = a.K1;
   p.N = a.N;
   p.BN = a.N;
   const int64_t nchunks = ceil_div(ceil_div(std::max<int64_t>(a.max_M, 1), DW16_KR), DW16_CHUNK);
-  p.splits = (int)std::max<int64_t>(1, std::min<int64_t>(nchunks, (int64_t)num_sms()));
-  p.sched = sched_slot();
+  // at least kmin k-blocks per CTA: each CTA ends with one flush of its
+  // whole TMEM sums (2 x 128 x N atomics), which a small M cannot amortise
+  const int64_t kmin = std::max(1, env_int("GNNV_DW16_MINKB", 16));
+  const int64_t nkbm_ub = ceil_div(std::max<int64_t>(a.max_M, 1), DW16_KR);
+  const int splits = (int)std::max<int64_t>(
+      1, std::min<int64_t>(std::min<int64_t>(nchunks, (int64_t)(num_sms() / groups)), (int64_t)ceil_div(nkbm_ub, kmin)));
+  for (int g = 0; g < groups; ++g) p.sched[g] = sched_slot();
   p.dW = a.dW;
   p.db = a.db;
-  if (!a.zeroed) {
-    GNNV_TRY_CUDA(cudaMemsetAsync(a.dW, 0, (size_t)2 * a.K1 * a.N * sizeof(float), s));
-    GNNV_TRY_CUDA(cudaMemsetAsync(a.db, 0, (size_t)a.N * sizeof(float), s));
-  }
+  // every CTA stores its slice, k_dw16_reduce sums them (no atomics; dW and
+  // db are overwritten, so `zeroed` does not matter)
+  p.prow = rows + 1;
+  p.part = (float*)g_dwpart.get((size_t)splits * p.prow * a.N * sizeof(float), s);
   const size_t bytes = (size_t)DW16_STAGES * (4 + a.N / 64) * DW16_BOX + 8 * (2 * DW16_STAGES + 1) + 4 * DW16_STAGES + 16 + 1024;
   static size_t attr = 0;
   if (bytes > attr) {
     GNNV_TRY_CUDA(cudaFuncSetAttribute(k_tma_dw16, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
     attr = bytes;
   }
-  launch_k(k_tma_dw16, dim3((unsigned)p.splits), NTHREADS, bytes, s, p);
+  float* dbp = nullptr;
+  const int conv_blocks = 2 * num_sms();
+  if (a.G32) {  // G -> bf16 copy + db partials
+    dbp = (float*)g_dbpart.get((size_t)conv_blocks * a.N * sizeof(float), s);
+    launch_k(k_g16_colsum, conv_blocks, 256, 0, s, a.G32, a.ldg32, a.d_M, a.N,
+             static_cast<__nv_bfloat16*>(const_cast<void*>(a.G16)), a.ldg, dbp);
+    GNNV_CHECK_LAUNCH();
+  }
+  launch_k(k_tma_dw16, dim3((unsigned)splits, (unsigned)groups), NTHREADS, bytes, s, p);
+  GNNV_CHECK_LAUNCH();
+  const int64_t total4 = (int64_t)p.prow * (a.N / 4);
+  launch_k(k_dw16_reduce, (int)std::min<int64_t>(ceil_div(total4, 32), (int64_t)num_sms() * 8), 256, 0, s, p.part,
+           splits, p.prow, a.N, (has_db || a.G32) ? 1 : 0, a.dW, a.db, (const float*)dbp, dbp ? conv_blocks : 0);
   GNNV_CHECK_LAUNCH();
 }
 

@@ -4,6 +4,8 @@
 // S:322 (combine = linear + ReLU except the last layer; mean/sum over
 // neighbours), S:332 (softmax cross-entropy + plain gradient descent).
 // Layer i in 1..L runs on block b_{L-i} (dst = F_{L-i}, src = F_{L-i+1}).
+#include <cuda_bf16.h>
+
 #include "common.cuh"
 
 namespace gnnv {
@@ -61,7 +63,8 @@ void launch_relu_bits(const float* H, int32_t ldh, int32_t N, const int32_t* d_M
 constexpr int kColBlocks = 296;
 __global__ void __launch_bounds__(256) k_mask_colsum(const float* __restrict__ G, const float* __restrict__ H,
                                                      float* __restrict__ Gp, int ld, const int32_t* d_M,
-                                                     float* __restrict__ partial) {
+                                                     float* __restrict__ partial,
+                                                     __nv_bfloat16* __restrict__ G16, int ld16) {
   GNNV_PDL_ENTRY();
   __shared__ float4 s_acc[256];
   const int M = *d_M;
@@ -82,6 +85,11 @@ __global__ void __launch_bounds__(256) k_mask_colsum(const float* __restrict__ G
         const float4 h = __ldg(H4 + i);
         g = make_float4(h.x > 0.f ? g.x : 0.f, h.y > 0.f ? g.y : 0.f, h.z > 0.f ? g.z : 0.f, h.w > 0.f ? g.w : 0.f);
         P4[i] = g;
+      }
+      if (G16) {  // the bf16 copy a kind::f16 dW reads
+        const __nv_bfloat162 lo = __floats2bfloat162_rn(g.x, g.y), hi = __floats2bfloat162_rn(g.z, g.w);
+        reinterpret_cast<uint2*>(G16)[((int64_t)r * ld16 >> 2) + c4] =
+            make_uint2(*reinterpret_cast<const uint32_t*>(&lo), *reinterpret_cast<const uint32_t*>(&hi));
       }
       acc.x += g.x;
       acc.y += g.y;
@@ -275,7 +283,7 @@ void layer_fwd_impl(gnnv_blocks* b, int32_t layer, const gnnv_layer_desc* ld, co
     if (tl) tl->mark(s, "spmm_fwd" + sfx);
     if (io && io->src16)
       launch_spmm_fwd_h16(b->d_indptr[h], b->d_indices[h], d_ndst, b->max_n[h], io->src16, io->src16_ld,
-                          io->x16 && io->a16 ? nullptr : A, lda, ld->d_in, ld->kind, ld->aggr, s, io->src16_rows,
+                          io->x16 && io->a16 && !io->keep_a32 ? nullptr : A, lda, ld->d_in, ld->kind, ld->aggr, s, io->src16_rows,
                           io->a16, io->a16_ld);
     else
       launch_spmm_fwd(b->d_indptr[h], b->d_indices[h], d_ndst, b->max_n[h], rowidx ? agg_table : Hsrc,
@@ -378,7 +386,7 @@ void layer_bwd_impl(gnnv_blocks* b, int32_t layer, const gnnv_layer_desc* ld, co
   if (tf32 && need_mask && !fuse_mask) {
     // masked gradient + deterministic column sums (db) in one pass
     if (tl) tl->mark(s, "relu_mask" + sfx);
-    launch_k(k_mask_colsum, kColBlocks, 256, 0, s, Gdst, Hdst, Gp, ldo, d_ndst, colpart);
+    launch_k(k_mask_colsum, kColBlocks, 256, 0, s, Gdst, Hdst, Gp, ldo, d_ndst, colpart, (__nv_bfloat16*)nullptr, 0);
     GNNV_CHECK_LAUNCH();
     launch_colsum_reduce(colpart, kColBlocks, ldo, ld->d_out, db, s);
     G = Gp;
@@ -420,13 +428,29 @@ void layer_bwd_impl(gnnv_blocks* b, int32_t layer, const gnnv_layer_desc* ld, co
   w.db_fused = tf32 && !need_mask;
   w.zeroed = tf32 && grads_zeroed;
   if (tl) tl->mark(s, "gemm_dw" + sfx);
-  if (io && io->x16 && io->a16 && io->gdst16) {
+  if (io && io->x16 && io->a16 && io->g16_out && !need_mask && tf32 && sage) {
+    // hidden layer over bf16 operands (reading Q34): G (pre-masked fp32) ->
+    // its bf16 copy + db = colsum(G) in one pass, then dW = [H16_dst |
+    // A16]^T G16 by the MN-major kind::f16 kernel (four feature tiles)
+    GemmDw16Args w16{};
+    w16.G32 = Gdst;
+    w16.ldg32 = ldo;
+    w16.src[0] = GemmDw16Src{io->x16, io->a16_ld, ld->d_in, 0, false};
+    w16.src[1] = GemmDw16Src{io->a16, io->a16_ld, ld->d_in, ld->d_in, false};
+    w16.G16 = io->g16_out;
+    w16.ldg = io->g16_ld;
+    w16.N = ld->d_out;
+    w16.d_M = d_ndst;
+    w16.max_M = max_dst;
+    w16.dW = dW;
+    w16.db = db;
+    w16.zeroed = w.zeroed;
+    gemm_dw16(w16, s);
+  } else if (io && io->x16 && io->a16 && io->gdst16) {
     GNNV_REQUIRE(sage && !xr && w.db_fused, GNNV_ERR_UNSUPPORTED, "layer_bwd: the bf16 dW needs SAGE and a final G");
     GemmDw16Args w16{};
-    w16.X16 = io->x16;
-    w16.A16 = io->a16;
-    w16.ldx = io->a16_ld;
-    w16.K1 = ld->d_in;
+    w16.src[0] = GemmDw16Src{io->x16, io->a16_ld, ld->d_in, 0, true};
+    w16.src[1] = GemmDw16Src{io->a16, io->a16_ld, ld->d_in, ld->d_in, false};
     w16.G16 = io->gdst16;
     w16.ldg = io->gdst16_ld;
     w16.N = ld->d_out;
@@ -448,6 +472,10 @@ void layer_bwd_impl(gnnv_blocks* b, int32_t layer, const gnnv_layer_desc* ld, co
     x.K1 = ld->d_in;
     x.d_M = d_ndst;
     x.max_M = max_dst;
+    if (io && io->g16_out && io->x16 && io->a16 && !need_mask && tf32 && sage) {  // the copy the dW pass wrote
+      x.G16 = io->g16_out;
+      x.ldg16 = io->g16_ld;
+    }
     const bool g16 = io && io->gsrc16;
     if (sage && g16) {  // dH_src (and its dst-prefix rows from the GEMM) as bf16
       x.Y1_16 = io->gsrc16;
@@ -635,7 +663,8 @@ gnnv_status gnnv_dense_dw(const float* X1, int32_t ld1, const float* X2, int32_t
     w.splits = splits;
     if (prec == GNNV_PREC_TF32) {
       float* colpart = scratch + part_f;
-      launch_k(k_mask_colsum, kColBlocks, 256, 0, s, G, nullptr, nullptr, ldg, w.d_M, colpart);
+      launch_k(k_mask_colsum, kColBlocks, 256, 0, s, G, (const float*)nullptr, (float*)nullptr, ldg, w.d_M, colpart,
+               (__nv_bfloat16*)nullptr, 0);
       GNNV_CHECK_LAUNCH();
       launch_colsum_reduce(colpart, kColBlocks, ldg, N, db_out, s);
     }

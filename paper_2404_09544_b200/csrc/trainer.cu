@@ -93,6 +93,17 @@ struct gnnv_trainer {
   // with dw16: layer 1's forward GEMM reads the same bf16 copies (kind::f16,
   // reading Q33); GNNV_NO_FWD16=1: the TF32 GEMM over the fp32 rows
   bool fwd16 = false;
+  // bf16 intermediates: the forward GEMMs of hidden layers 2..L-1 read
+  // [H16^{i-1} dst prefix | A16^i] (kind::f16, reading Q34); the
+  // aggregation then also writes A^i as bf16 (A16h[i], stride ld16[i-1]).
+  // GNNV_NO_HID16=1: the TF32 GEMMs over fp32 rows
+  bool hid16 = false;
+  void* A16h[GNNV_MAX_LAYERS + 1] = {nullptr};
+  // opt-in GNNV_HID16_DW=1: their dW and dX run over bf16 too (G^i's bf16
+  // copy G16h[i], stride ld16[i], written by gemm_dw16's db pass).  Measured
+  // slower on products (layer 2: 60K rows, too few k-blocks per CTA to
+  // amortise the per-CTA TMEM flush)
+  void* G16h[GNNV_MAX_LAYERS + 1] = {nullptr};
   void* X16[2] = {nullptr, nullptr};
   void* A16[2] = {nullptr, nullptr};
   int32_t ld16x = 0;  // their row stride: d + 1 rounded up to 8
@@ -218,6 +229,8 @@ gnnv_status gnnv_trainer_free(gnnv_trainer* t) {
   for (int i = 0; i <= GNNV_MAX_LAYERS; ++i) {
     dfree(t->H16[i]);
     dfree(t->G16[i]);
+    dfree(t->A16h[i]);
+    dfree(t->G16h[i]);
   }
   dfree(t->loss_partial);
   dfree(t->tail_dA);
@@ -307,6 +320,16 @@ gnnv_status gnnv_trainer_create(gnnv_graph* g, gnnv_cache* c, const gnnv_model_d
           const size_t bytes = (size_t)b->max_n[L - i] * t->ld16[i] * 2;
           t->H16[i] = dmalloc(bytes, "bf16 activations");
           t->G16[i] = dmalloc(bytes, "bf16 activation gradients");
+        }
+      t->hid16 = t->bf16act && !env_on("GNNV_NO_HID16");
+      for (int i = 2; i <= L - 1 && t->hid16; ++i)
+        if (i - 1 > L - 2 || t->ld16[i - 1] % 8 != 0) t->hid16 = false;
+      if (t->hid16)
+        for (int i = 2; i <= L - 1; ++i) {
+          t->A16h[i] = dmalloc((size_t)b->max_n[L - i] * t->ld16[i - 1] * 2, "bf16 aggregates (hidden layers)");
+          if (env_on("GNNV_HID16_DW") && md->dims[i] % 64 == 0 && md->dims[i] <= 256 && md->dims[i - 1] <= 256)
+            t->G16h[i] = dmalloc((size_t)b->max_n[L - i] * ((md->dims[i] + 31) / 32 * 32) * 2,
+                                 "bf16 gradients (hidden-layer dW)");
         }
       // layer 1 aggregates a bf16 copy of the whole-table cache (reading Q31)
       t->table16 = t->x_fused && md->prec == GNNV_PREC_TF32 && md->kind == GNNV_KIND_SAGE &&
@@ -437,13 +460,27 @@ gnnv_status gnnv_trainer_activation16(gnnv_trainer* t, int32_t i, const void** d
 gnnv_status gnnv_trainer_gradient16(gnnv_trainer* t, int32_t i, const void** d_G16, int32_t* ld) {
   return guarded([&] {
     GNNV_REQUIRE(t && d_G16 && ld && i >= 0 && i <= t->md.L, GNNV_ERR_PARAM, "trainer_gradient16: bad args");
-    *d_G16 = t->G16[i];
-    *ld = t->G16[i] ? t->ld16[i] : 0;
+    if (t->G16[i]) {
+      *d_G16 = t->G16[i];
+      *ld = t->ld16[i];
+    } else {  // a hidden layer's dW operand (reading Q34)
+      *d_G16 = t->G16h[i];
+      *ld = t->G16h[i] ? (t->md.dims[i] + 31) / 32 * 32 : 0;
+    }
   });
 }
 
 int32_t gnnv_trainer_dw16(const gnnv_trainer* t) { return t && t->dw16 ? 1 : 0; }
 int32_t gnnv_trainer_fwd16(const gnnv_trainer* t) { return t && t->fwd16 ? 1 : 0; }
+
+gnnv_status gnnv_trainer_aggregate16(gnnv_trainer* t, int32_t i, const void** d_A16, int32_t* ld) {
+  return guarded([&] {
+    GNNV_REQUIRE(t && d_A16 && ld && i >= 1 && i <= t->md.L, GNNV_ERR_PARAM, "trainer_aggregate16: bad args");
+    const void* p = i == 1 ? t->A16[t->cur] : t->A16h[i];
+    *d_A16 = p;
+    *ld = !p ? 0 : i == 1 ? t->ld16x : t->ld16[i - 1];
+  });
+}
 
 gnnv_status gnnv_trainer_dw16_operands(gnnv_trainer* t, const void** d_X16, const void** d_A16, int32_t* ld) {
   return guarded([&] {
@@ -779,6 +816,12 @@ gnnv_status gnnv_step(gnnv_trainer* t, const int32_t* seeds, int32_t n_seeds, in
         if (i >= 2 && i - 1 <= L - 2) {  // aggregate the previous layer's bf16 copy
           io.src16 = t->H16[i - 1];
           io.src16_ld = t->ld16[i - 1];
+          if (t->hid16 && t->A16h[i]) {  // and run the GEMM over [H16 dst prefix | A16]
+            io.x16 = t->H16[i - 1];
+            io.a16 = t->A16h[i];
+            io.a16_ld = t->ld16[i - 1];
+            io.keep_a32 = true;  // the layer's TF32 dW reads the fp32 A
+          }
         }
       }
       layer_fwd_impl(b, i, &ld, t->H[i - 1], t->d_params + t->w_off[i - 1], t->d_params + t->b_off[i - 1], t->H[i],
@@ -849,6 +892,13 @@ gnnv_status gnnv_step(gnnv_trainer* t, const int32_t* seeds, int32_t n_seeds, in
           io.x16 = t->X16[t->cur];
           io.a16 = t->A16[t->cur];
           io.a16_ld = t->ld16x;
+        }
+        if (i >= 2 && t->G16h[i]) {  // hidden layer: dW over bf16 (reading Q34)
+          io.x16 = t->H16[i - 1];
+          io.a16 = t->A16h[i];
+          io.a16_ld = t->ld16[i - 1];
+          io.g16_out = t->G16h[i];
+          io.g16_ld = (t->md.dims[i] + 31) / 32 * 32;
         }
       }
       layer_bwd_impl(b, i, &ld, t->G[i], t->H[i], t->H[i - 1], t->A[i], t->d_params + t->w_off[i - 1],

@@ -983,6 +983,65 @@ def test_bf16_layer1_fwd(mini, option, pipelined):
     assert abs(losses["fwd16"] - losses["tf32"]) <= 2e-3 * abs(losses["tf32"]), losses
 
 
+@pytest.mark.parametrize("hdw", [0, 1], ids=["tf32dw", "bf16dw"])
+@pytest.mark.parametrize("ratio", [0.3, 1.0])
+def test_bf16_hidden_layer_fwd(mini, option, ratio, hdw):
+    """bf16 intermediates: layer 2's forward GEMM reads [bf16 H^1 dst prefix
+    | bf16 A^2] (kind::f16, reading Q34) and its dW the same operands with a
+    bf16 copy of its masked G.  A^2's bf16 copy is bit for bit the RNE
+    rounding of the fp32 A^2 the aggregation also writes; H^2 equals
+    relu([H16 | A16] bf16(W^2) + b^2) in fp64 to 1e-5 of the |.| product;
+    dW^2 equals [H16 | A16]^T G16 to 1e-5, db^2 (summed from the fp32 G) the
+    copy's column sums to its rounding;
+    the forward and backward chains hold at the tf32 bounds; the loss is
+    within 2e-3 of the TF32 layer-2 GEMM's (GNNV_NO_HID16=1)."""
+    gd, g = mini
+    cfg = CONFIGS["mini"]
+    dims = [gd.d, cfg["hidden"], cfg["hidden"], gd.C]
+    L = len(cfg["fanouts"])
+    w = init_weights(dims)
+    seeds = epoch_seeds(gd.n, 0)[: cfg["batch"]]
+    B = len(seeds)
+    losses = {}
+    option("GNNV_HID16_DW", hdw)  # opt-in: the hidden layer's dW and dX over bf16 too
+    for name in ("hid16", "tf32"):
+        option("GNNV_NO_HID16", 0 if name == "hid16" else 1)
+        tr = gnnv.Trainer(g, gnnv.Cache(g, ratio), dims, cfg["fanouts"], B, w, prec=gnnv.PREC_TF32)
+        tr.prefetch(seeds, B, 0x5EED)
+        losses[name], _ = tr.step(seeds, B, B, 0x5EED, 0.0)
+        p16, ld = tr.aggregate16(2)
+        assert bool(p16) == (name == "hid16")
+        if name == "hid16":
+            hb = blocks_to_host(tr.blocks)
+            n2 = hb[L - 2][0]
+            pa, sa = tr.aggregate(2)
+            A32 = read_f32(pa, n2, sa)[:, : dims[1]]
+            A16 = read_bf16(p16, n2, ld)[:, : dims[1]]
+            np.testing.assert_array_equal(A16, bf16_round(A32))
+            ph16, lh = tr.activation16(1)
+            H16 = read_bf16(ph16, n2, lh)[:, : dims[1]]
+            Xc = np.concatenate([H16, A16], axis=1)
+            W2, b2 = w[1]
+            W16 = bf16_round(W2)
+            Z = Xc @ W16 + b2.astype(np.float64)
+            mag = np.abs(Xc) @ np.abs(W16) + np.abs(b2)
+            p2, s2 = tr.activation(2)
+            H2 = read_f32(p2, n2, s2)[:, : dims[2]]
+            assert_close_cond(H2, np.maximum(Z, 0), mag, 1e-5, "H^2 over the bf16 operands")
+            grads = gnnv.unflat_params(tr.grads(), dims)
+            pg, lg = tr.gradient16(2)
+            assert bool(pg) == bool(hdw)
+            if pg:  # layer 2's dW over the same operands and the bf16 copy of its (masked) G
+                G16 = read_bf16(pg, n2, lg)[:, : dims[2]]
+                assert_close_cond(grads[1][0], Xc.T @ G16, np.abs(Xc).T @ np.abs(G16), 1e-5, "dW^2 over bf16")
+                assert_close_cond(grads[1][1], G16.sum(0), np.abs(G16).sum(0), 2.0 ** -8, "db^2 (fp32 G)")
+            X0 = oracle.gather_rows(gd.feats, hb[L - 1][4])[:, : dims[0]] if tr.x_level() < L else None
+            H, Aagg, blks = check_forward_chain(tr, hb, dims, w, RTOL[2], "hid16", X0=X0, max_rows=10**9)
+            check_backward_chain(tr, blks, H, Aagg, dims, w, grads, gd.labels[seeds], B, RTOL[2], "hid16")
+        tr.free()
+    assert abs(losses["hid16"] - losses["tf32"]) <= 2e-3 * abs(losses["tf32"]), losses
+
+
 @pytest.mark.parametrize("kind", [gnnv.KIND_SAGE, gnnv.KIND_GCN])
 @pytest.mark.parametrize("ratio", [0.3, 1.0])
 def test_prefetched_layer1_aggregation_bitwise(mini, option, kind, ratio):
