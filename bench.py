@@ -378,8 +378,8 @@ def algorithmic(seg: str, sizes, cfg, dims, stride, prec, peaks):
         rowb = stride * 4
         lvl = int(sizes.get("x_level", L))
         ld16x = (dims[0] + 1 + 7) & ~7
-        if lvl < 0 and sizes.get("fwd16"):  # whole table cached, layer 1 on bf16 copies: F_{L-1} rows
-            by = n[L - 1] * ((dims[0] + 7) & ~7) * 2 + n[L - 1] * ld16x * 2 + n[L] * 12  # of the bf16 table -> X16
+        if lvl < 0 and sizes.get("fwd16"):  # whole table cached, layer 1 on bf16 copies: F_L rows resolved only
+            by = n[L] * 12  # (the layer-1 aggregation copies the dst prefix's bf16 rows, spmm_fwd.l1)
         elif lvl < 0:  # whole table cached, layer-1 GEMMs gather H_dst from it: F_L rows resolved, none copied
             by = n[L] * 12
         elif lvl < L:  # whole table cached: rows of F_{L-1} copied, every F_L row resolved to its cache row
@@ -411,6 +411,8 @@ def algorithmic(seg: str, sizes, cfg, dims, stride, prec, peaks):
         by = U[h] * d_in * src_b + (0 if fwd16 else n[h] * ((d_in + 3) & ~3) * 4) + nnz[h] * 4 + (n[h] + 1) * 4
         if dw16:  # + the bf16 copy of A^1
             by += n[h] * ((d_in + 7) & ~7) * 2
+        if fwd16:  # + the dst rows' own bf16 table rows copied into X16 (with the ones column)
+            by += n[h] * ((d_in + 7) & ~7) * 2 + n[h] * ((d_in + 1 + 7) & ~7) * 2
         if hid16:  # + the bf16 copy of A^i
             by += n[h] * ((d_in + 31) & ~31) * 2
         return "hbm", by, "GB/s", peaks["hbm"]

@@ -185,7 +185,7 @@ void launch_gather(const gnnv_cache* c, const gnnv_blocks* b, float* d_X, int64_
   const gnnv_graph* g = c->g;
   GNNV_REQUIRE(!d_X16 || (materialize && ldx16 % 4 == 0 && ldx16 >= std::max(g->stride, g->d + 1)), GNNV_ERR_UNSUPPORTED,
                "gather: the bf16 copy needs materialised rows and a stride (multiple of 4) covering the ones column");
-  GNNV_REQUIRE(d_X || (d_X16 && d_rowidx), GNNV_ERR_PARAM, "gather: no output rows");
+  GNNV_REQUIRE(d_X || (d_X16 && d_rowidx) || (!materialize && d_rowidx), GNNV_ERR_PARAM, "gather: no output");
   // bf16 rows only, whole table on this device: copy them from its bf16 copy
   // (the same round-to-nearest-even values, half the bytes)
   const bool t16 = !d_X && d_X16 && c->d_table16 && c->world == 1 && c->table16_ld % 8 == 0;

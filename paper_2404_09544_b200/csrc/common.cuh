@@ -294,7 +294,8 @@ void launch_spmm_bwd(const int32_t* d_indptr, const int32_t* d_indices, const ui
 // rowidx != NULL: source row u is row rowidx[u] of H16 (the bf16 table)
 void launch_spmm_fwd_h16(const int32_t* d_indptr, const int32_t* d_indices, const int32_t* d_ndst, int64_t max_dst,
                          const void* H16, int32_t ld16, float* A, int32_t lda, int32_t d, int32_t kind, int32_t aggr,
-                         cudaStream_t s, const int32_t* rowidx = nullptr, void* A16 = nullptr, int32_t lda16 = 0);
+                         cudaStream_t s, const int32_t* rowidx = nullptr, void* A16 = nullptr, int32_t lda16 = 0,
+                         void* X16 = nullptr);
 // the same transposed aggregation pulled per src row (rows up to
 // kPullMaxLd floats; wider ones keep the push) through the block's
 // CSC (one coalesced store per dH row, no atomics; see k_spmm_bwd_pull)
@@ -388,6 +389,7 @@ struct Bf16Io {
   int32_t a16_ld = 0;
   const void* x16 = nullptr;
   bool keep_a32 = false;  // fwd with x16: still write the fp32 A (a TF32 dW reads it)
+  void* x16_out = nullptr;  // fwd, bf16 aggregation: also copy each dst row's own bf16 row here (+ ones column)
   // bwd with x16 and a16, G pre-masked fp32: write G's bf16 copy here (stride
   // g16_ld) and run dW over bf16 (gemm_dw16; db by the conversion pass)
   void* g16_out = nullptr;

@@ -488,7 +488,8 @@ __global__ void __launch_bounds__(256, 8) k_spmm_fwd_h16(const int32_t* __restri
                                                       const __nv_bfloat16* __restrict__ H, int32_t ld16,
                                                       float* __restrict__ A, int32_t lda, int32_t d, int32_t kind,
                                                       int32_t aggr, const int32_t* __restrict__ rowidx,
-                                                      __nv_bfloat16* __restrict__ A16, int32_t lda16) {
+                                                      __nv_bfloat16* __restrict__ A16, int32_t lda16,
+                                                      __nv_bfloat16* __restrict__ X16, int32_t ones_col) {
   GNNV_PDL_ENTRY();
   constexpr int RPW = 32 / LPR;
   const int n = *d_ndst;
@@ -510,6 +511,18 @@ __global__ void __launch_bounds__(256, 8) k_spmm_fwd_h16(const int32_t* __restri
       float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
       if (kind == GNNV_KIND_GCN && cok)
         add_bf16x8(acc, __ldg(H8 + (int64_t)(IND ? __ldg(rowidx + row) : row) * ld8 + c));
+      if (X16 && cok) {
+        // the dst row's own (bf16) features with the ones column at
+        // ones_col: the self operand of the layer's bf16 GEMMs (stride lda16)
+        uint4 sv = __ldg(H8 + (int64_t)(IND ? __ldg(rowidx + row) : row) * ld8 + c);
+        uint32_t* w = reinterpret_cast<uint32_t*>(&sv);
+        const int oh = ones_col & 7;
+        if (c == (ones_col >> 3))
+          w[oh >> 1] = (oh & 1) ? ((w[oh >> 1] & 0xFFFFu) | 0x3F800000u) : ((w[oh >> 1] & 0xFFFF0000u) | 0x3F80u);
+        uint4* xr = reinterpret_cast<uint4*>(X16) + (int64_t)row * (lda16 >> 3);
+        xr[c] = sv;
+        if (c == vec8 - 1 && (ones_col >> 3) == vec8) xr[vec8] = make_uint4(0x3F80u, 0u, 0u, 0u);
+      }
       for (int e0 = 0; e0 < cnt; e0 += LPR) {
         int my = (e0 + sl < cnt) ? __ldg(indices + beg + e0 + sl) : 0;
         if (IND) my = __ldg(rowidx + my);
@@ -557,12 +570,16 @@ __global__ void __launch_bounds__(256, 8) k_spmm_fwd_h16(const int32_t* __restri
 
 void launch_spmm_fwd_h16(const int32_t* d_indptr, const int32_t* d_indices, const int32_t* d_ndst, int64_t max_dst,
                          const void* H16, int32_t ld16, float* A, int32_t lda, int32_t d, int32_t kind, int32_t aggr,
-                         cudaStream_t s, const int32_t* rowidx, void* A16, int32_t lda16) {
+                         cudaStream_t s, const int32_t* rowidx, void* A16, int32_t lda16, void* X16) {
   const int vec8 = (d + 7) / 8;
   GNNV_REQUIRE(!A16 || (lda16 % 8 == 0 && lda16 >= 8 * vec8), GNNV_ERR_UNSUPPORTED,
                "spmm_fwd_h16: the bf16 output stride must be a multiple of 8 covering d");
   __nv_bfloat16* a16 = static_cast<__nv_bfloat16*>(A16);
   GNNV_REQUIRE(A || a16, GNNV_ERR_PARAM, "spmm_fwd_h16: no output");
+  __nv_bfloat16* x16 = static_cast<__nv_bfloat16*>(X16);
+  const int32_t ones_col = d;
+  GNNV_REQUIRE(!x16 || (a16 && lda16 >= d + 1), GNNV_ERR_PARAM,
+               "spmm_fwd_h16: the self copy shares the bf16 aggregate's stride, which must cover the ones column");
   GNNV_REQUIRE(ld16 % 8 == 0 && ld16 >= 8 * vec8 && lda % 4 == 0, GNNV_ERR_UNSUPPORTED,
                "spmm_fwd_h16: the bf16 row stride must be a multiple of 8 covering d");
   const __nv_bfloat16* H = static_cast<const __nv_bfloat16*>(H16);
@@ -570,10 +587,10 @@ void launch_spmm_fwd_h16(const int32_t* d_indptr, const int32_t* d_indices, cons
   do {                                                                                                               \
     if (rowidx)                                                                                                      \
       launch_k(k_spmm_fwd_h16<LPR, true>, spmm_grid(max_dst, RPWv), 256, 0, s, d_indptr, d_indices, d_ndst, H, ld16, \
-               A, lda, d, kind, aggr, rowidx, a16, lda16);                                                           \
+               A, lda, d, kind, aggr, rowidx, a16, lda16, x16, ones_col);                                            \
     else                                                                                                             \
       launch_k(k_spmm_fwd_h16<LPR, false>, spmm_grid(max_dst, RPWv), 256, 0, s, d_indptr, d_indices, d_ndst, H,      \
-               ld16, A, lda, d, kind, aggr, (const int32_t*)nullptr, a16, lda16);                                    \
+               ld16, A, lda, d, kind, aggr, (const int32_t*)nullptr, a16, lda16, x16, ones_col);                     \
   } while (0)
   if (vec8 <= 8) GNNV_H16(8, 4);
   else if (vec8 <= 16) GNNV_H16(16, 2);

@@ -696,8 +696,10 @@ gnnv_status gnnv_trainer_prefetch(gnnv_trainer* t, const int32_t* seeds, int32_t
     GNNV_TRY_CUDA(cudaMemsetAsync(t->d_statsb[k], 0, 4 * sizeof(int64_t), t->side));
     if (tl) tl->mark(t->side, "pf_gather");
     if (t->c->dynamic && t->cache_pending) GNNV_TRY_CUDA(cudaStreamWaitEvent(t->side, t->ev_cache, 0));
-    launch_gather(t->c, t->bb[k], t->fwd16 ? nullptr : t->X[k], t->d_statsb[k], t->side, t->rowidx[k], !t->x_rows,
-                  t->X16[k], t->ld16x);
+    // with fwd16 the layer-1 aggregation copies X's bf16 dst prefix itself:
+    // the gather only resolves every F_L row's cache row (and counts hits)
+    launch_gather(t->c, t->bb[k], t->fwd16 ? nullptr : t->X[k], t->d_statsb[k], t->side, t->rowidx[k],
+                  !t->x_rows && !t->fwd16, t->fwd16 ? nullptr : t->X16[k], t->ld16x);
     if (t->c->dynamic) {  // NEXT-3 admission
       if (tl) tl->mark(t->side, "pf_replace");
       launch_cache_update(t->c, t->bb[k], t->X[k], t->side);
@@ -711,7 +713,8 @@ gnnv_status gnnv_trainer_prefetch(gnnv_trainer* t, const int32_t* seeds, int32_t
       if (t->table16)
         launch_spmm_fwd_h16(bk->d_indptr[h], bk->d_indices[h], bk->d_sizes + h, bk->max_n[h], t->c->d_table16,
                             t->c->table16_ld, t->fwd16 ? nullptr : t->A1b[k], row_stride(t->md.dims[0]),
-                            t->md.dims[0], t->md.kind, t->md.aggr, t->side, t->rowidx[k], t->A16[k], t->ld16x);
+                            t->md.dims[0], t->md.kind, t->md.aggr, t->side, t->rowidx[k], t->A16[k], t->ld16x,
+                            t->fwd16 ? t->X16[k] : nullptr);
       else
         launch_spmm_fwd(bk->d_indptr[h], bk->d_indices[h], bk->d_sizes + h, bk->max_n[h],
                         t->x_fused ? t->table : t->X[k], g->stride, t->A1b[k], row_stride(t->md.dims[0]),
@@ -773,8 +776,8 @@ gnnv_status gnnv_step(gnnv_trainer* t, const int32_t* seeds, int32_t n_seeds, in
       if (tm) GNNV_TRY_CUDA(cudaEventRecord(t->ev[1], s));
       if (tl) tl->mark(s, "gather");
       if (t->c->dynamic && t->cache_pending) GNNV_TRY_CUDA(cudaStreamWaitEvent(s, t->ev_cache, 0));
-      launch_gather(t->c, t->b, t->fwd16 ? nullptr : t->H[0], t->d_stats, s, t->rowidx[t->cur], !t->x_rows,
-                    t->X16[t->cur], t->ld16x);
+      launch_gather(t->c, t->b, t->fwd16 ? nullptr : t->H[0], t->d_stats, s, t->rowidx[t->cur],
+                    !t->x_rows && !t->fwd16, t->fwd16 ? nullptr : t->X16[t->cur], t->ld16x);
       if (t->c->dynamic) {  // NEXT-3 admission (Eq.5's t_replace)
         if (tl) tl->mark(s, "replace");
         launch_cache_update(t->c, t->b, t->H[0], s);
@@ -805,7 +808,10 @@ gnnv_status gnnv_step(gnnv_trainer* t, const int32_t* seeds, int32_t n_seeds, in
         io.src16_rows = t->rowidx[t->cur];
         io.a16 = t->A16[t->cur];
         io.a16_ld = t->ld16x;
-        if (t->fwd16) io.x16 = t->X16[t->cur];
+        if (t->fwd16) {
+          io.x16 = t->X16[t->cur];
+          io.x16_out = t->X16[t->cur];  // written by the aggregation (self rows + ones column)
+        }
       }
       if (t->bf16act) {
         if (i <= L - 2) {  // this layer's output: a bf16 copy, fp32 rows for the next dst prefix
