@@ -271,6 +271,82 @@ __global__ void __launch_bounds__(256) k_spmm_bwd(const int32_t* __restrict__ in
   }
 }
 
+// The bf16-dH push with 8 columns (16 bytes of dH) per lane: a warp owns a
+// whole dst row of up to 256 columns, so every edge is one pass of 16-byte
+// stores (phase 1) or four bf16x2 reductions per lane (phase 2), and a
+// lane's ReLU bits are one byte of the edge row's mask word.  SAGE only
+// (no self term); dH row stride ldh = 8 * lanes used, dA row stride lda.
+__global__ void __launch_bounds__(256) k_spmm_bwd16w(const int32_t* __restrict__ indptr,
+                                                     const int32_t* __restrict__ indices,
+                                                     const uint32_t* __restrict__ own, const int32_t* d_ndst,
+                                                     const float* __restrict__ dA, int32_t lda,
+                                                     __nv_bfloat16* __restrict__ dH, int32_t ldh, int32_t d,
+                                                     int32_t aggr, int32_t phase, const uint32_t* __restrict__ bits,
+                                                     int32_t bits_ld) {
+  GNNV_PDL_ENTRY();
+  const int n = *d_ndst;
+  const int lane = threadIdx.x & 31;
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  const int c8 = lane, cols8 = ldh >> 3;
+  const bool cok = c8 < cols8;
+  for (int row = warp; row < n; row += nwarps) {
+    const int beg = indptr[row], cnt = indptr[row + 1] - beg;
+    const uint32_t mine = own[row];
+    const uint32_t todo = (cnt >= 32 ? 0xffffffffu : ((1u << cnt) - 1u)) & (phase == 1 ? mine : ~mine);
+    if (!todo) continue;  // warp-uniform (one row per warp)
+    const float w = (aggr == GNNV_AGGR_MEAN && cnt) ? 1.f / (float)cnt : 1.f;
+    float g[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    if (cok && 8 * c8 < d) {
+      const float4 a = __ldg(reinterpret_cast<const float4*>(dA + (int64_t)row * lda) + 2 * c8);
+      const float4 b = __ldg(reinterpret_cast<const float4*>(dA + (int64_t)row * lda) + 2 * c8 + 1);
+      g[0] = a.x * w; g[1] = a.y * w; g[2] = a.z * w; g[3] = a.w * w;
+      g[4] = b.x * w; g[5] = b.y * w; g[6] = b.z * w; g[7] = b.w * w;
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        if (8 * c8 + j >= d) g[j] = 0.f;
+    }
+    for (int e0 = 0; e0 < cnt; e0 += 32) {
+      const int my = (e0 + lane < cnt) ? __ldg(indices + beg + e0 + lane) : 0;
+      uint32_t pend = (todo >> e0) & (cnt - e0 >= 32 ? 0xffffffffu : ((1u << (cnt - e0)) - 1u));
+      while (pend) {
+        int u[4];
+        uint32_t wb[4];
+        int k = 0;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int j = pend ? __ffs(pend) - 1 : 0;
+          u[q] = __shfl_sync(0xffffffffu, my, j);
+          if (pend) {
+            pend &= pend - 1;
+            k = q + 1;
+          }
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          wb[q] = (bits && q < k && cok) ? (__ldg(bits + (int64_t)u[q] * bits_ld + (c8 >> 2)) >> ((c8 & 3) * 8)) : 0xFFu;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          if (q >= k || !cok) continue;
+          uint32_t h[4];
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            h[j] = pack_bf16x2(wb[q] & (1u << (2 * j)) ? g[2 * j] : 0.f, wb[q] & (2u << (2 * j)) ? g[2 * j + 1] : 0.f);
+          uint4* p = reinterpret_cast<uint4*>(dH + (int64_t)u[q] * ldh) + c8;
+          if (phase == 1) {
+            *p = make_uint4(h[0], h[1], h[2], h[3]);
+          } else {
+            uint32_t* p32 = reinterpret_cast<uint32_t*>(p);
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+              asm volatile("red.global.add.noftz.bf16x2 [%0], %1;" ::"l"(p32 + j), "r"(h[j]) : "memory");
+          }
+        }
+      }
+    }
+  }
+}
+
 // w_v of the mean (1/c_v, 1/(c_v+1) for GCN, 0 for an empty row) or 1 (sum)
 __device__ __forceinline__ float pull_weight(const int32_t* __restrict__ indptr, int v, bool mean, bool gcn) {
   if (!mean) return 1.f;
@@ -452,6 +528,15 @@ void launch_spmm_bwd(const int32_t* d_indptr, const int32_t* d_indices, const ui
                      int64_t max_dst, const float* dA, int32_t lda, void* dH, int32_t ldh, int32_t d, int32_t kind,
                      int32_t aggr, const uint32_t* bits, int32_t bits_ld, cudaStream_t s, bool dh_bf16) {
   const int ldh4 = ldh / 4;
+  if (dh_bf16 && kind == GNNV_KIND_SAGE && ldh % 8 == 0 && ldh / 8 <= 32 && ldh / 8 > 16 && lda % 8 == 0 &&
+      !env_on("GNNV_BWD_NARROW")) {
+    for (int phase = 1; phase <= 2; ++phase) {
+      launch_k(k_spmm_bwd16w, spmm_grid(max_dst, 1), 256, 0, s, d_indptr, d_indices, d_own, d_ndst, dA, lda,
+               static_cast<__nv_bfloat16*>(dH), ldh, d, aggr, phase, bits, bits_ld);
+      GNNV_CHECK_LAUNCH();
+    }
+    return;
+  }
   for (int phase = 1; phase <= 2; ++phase) {
 #define GNNV_BWD(LPR, RPWv)                                                                                          \
   do {                                                                                                               \

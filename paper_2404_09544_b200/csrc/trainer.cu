@@ -176,7 +176,9 @@ static cudaStream_t make_side_stream() {
   int lo = 0, hi = 0;
   GNNV_TRY_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
   cudaStream_t st;
-  GNNV_TRY_CUDA(cudaStreamCreateWithPriority(&st, cudaStreamNonBlocking, lo));
+  // GNNV_PF_PRIO: the side stream's priority (default: the lowest)
+  const int want = env_int("GNNV_PF_PRIO", lo);
+  GNNV_TRY_CUDA(cudaStreamCreateWithPriority(&st, cudaStreamNonBlocking, std::min(lo, std::max(hi, want))));
   return st;
 }
 
