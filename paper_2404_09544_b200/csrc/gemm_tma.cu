@@ -594,6 +594,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_tma_gemm(const __grid_constant_
       constexpr int OBN = PAIR ? PAIR_OB : 1;
       uint8_t* ob0 = obuf + (warp - 2) * 4096 * OBN;
       int obi = 0;
+      int y16h = 0;  // dX: the staging half of the next bf16 Y1 piece
+      bool full_pending = false;  // the last TMA store read the whole 4 KB buffer
       int lt = 0;
       for (int tile = pid;; tile += npid, ++lt) {
         if (dyn) {
@@ -794,7 +796,33 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_tma_gemm(const __grid_constant_
             for (int j = 0; j < 32; ++j)
               if (j0 + j < p.ld1 && !((wv >> j) & 1u)) v[j] = 0.f;
           }
-          if (MODE == MODE_DX && p.y1_16 && j0 < p.ld1) {  // Y1 as bf16 (j0 + 32 <= ld1: checked on the host)
+          if (MODE == MODE_DX && p.y1_16 && j0 < p.ld1 && row0 + 32 <= M) {
+            // Y1 as bf16 (j0 + 32 <= ld1: checked on the host): the 2 KB
+            // piece through a staging half and a TMA store (halves alternate,
+            // so one store may still be reading while the next is written)
+            const uint32_t hb = smem_u32(ob0) + (uint32_t)y16h * 2048u;
+            if (lane == 0) {  // a 4 KB fp32 store issued last reads both halves
+              if (full_pending) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+              else asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+            }
+            full_pending = false;
+            __syncwarp();
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+              asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(hb + lane * 64 + q * 16),
+                           "r"(bf16x2(v[8 * q], v[8 * q + 1])), "r"(bf16x2(v[8 * q + 2], v[8 * q + 3])),
+                           "r"(bf16x2(v[8 * q + 4], v[8 * q + 5])), "r"(bf16x2(v[8 * q + 6], v[8 * q + 7]))
+                           : "memory");
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            __syncwarp();
+            if (lane == 0) {
+              tma_store_2d(&p.ty16, ob0 + y16h * 2048, j0, row0);
+              asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+            }
+            y16h ^= 1;
+            continue;
+          }
+          if (MODE == MODE_DX && p.y1_16 && j0 < p.ld1) {  // ragged tile: the rows < M with plain stores
             const int64_t m = (int64_t)row0 + lane;
             if (m < M) {
               uint4* dst = reinterpret_cast<uint4*>(p.y1_16 + m * p.ld1 + j0);
@@ -892,6 +920,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_tma_gemm(const __grid_constant_
             } else if (p.Y2) {
               tma_store_2d(&p.ty2, ob, j0 - p.ld1, row0);
             }
+            full_pending = true;
             asm volatile("cp.async.bulk.commit_group;" ::: "memory");
           }
           if (push && p.push_owner) {
@@ -1887,6 +1916,7 @@ bool gemm_dx_tma(const GemmDxArgs& a, cudaStream_t s) {
   if (a.Y1_16) {  // Y1 as bf16 rows: plain stores from the epilogue (ty1 unused)
     GNNV_REQUIRE(a.ld1 % 32 == 0 && a.Y2, GNNV_ERR_PARAM, "dX: a bf16 Y1 needs ld1 % 32 == 0 and Y2");
     p.y1_16 = static_cast<__nv_bfloat16*>(a.Y1_16);
+    p.ty16 = make_map16(a.Y1_16, a.max_M, a.ld1, a.ld1, 32, 32);
     p.ty1 = p.ty2;
   } else {
     p.ty1 = make_map(a.Y1, a.max_M, a.ld1, a.ld1, 32);
