@@ -444,6 +444,11 @@ int32_t gnnv_trainer_fwd16(const gnnv_trainer* t);
  * GEMM reads [bf16 H^{i-1} dst prefix | this copy], reading Q34): [n_dst x
  * *ld] bf16, NULL and 0 when there is none. */
 gnnv_status gnnv_trainer_aggregate16(gnnv_trainer* t, int32_t i, const void** d_A16, int32_t* ld);
+/* 1 if the fused output layer writes dL/dH^{L-1} as bf16 (with db^{L-1}'s
+ * partial column sums) and layer L-1's dW / dX run over bf16 operands
+ * (bf16 intermediates with the fused output layer, unless GNNV_NO_TAIL16;
+ * reading Q34).  gnnv_trainer_gradient16(L-1) then returns that copy. */
+int32_t gnnv_trainer_tail16(const gnnv_trainer* t);
 gnnv_status gnnv_trainer_dw16_operands(gnnv_trainer* t, const void** d_X16, const void** d_A16, int32_t* ld);
 
 /* One iteration of Algorithm 1 on this rank's seed slice:

@@ -394,6 +394,11 @@ struct Bf16Io {
   // g16_ld) and run dW over bf16 (gemm_dw16; db by the conversion pass)
   void* g16_out = nullptr;
   int32_t g16_ld = 0;
+  // bwd with x16 and a16: G already as bf16 (stride g16_ld; the fused
+  // output layer wrote it) with db's partial column sums dbp[ndbp][d_out]
+  const void* g16_in = nullptr;
+  const float* dbp = nullptr;
+  int32_t ndbp = 0;
 };
 // Layer 1 of the trainer with the whole feature table on the device: H_dst
 // (X's dst prefix) is read by the TF32 GEMMs straight from the table through
@@ -455,6 +460,10 @@ struct GemmDw16Args {
   // ldg32]) by the same call, which also sums db = colsum(G32)
   const float* G32 = nullptr;
   int32_t ldg32 = 0;
+  // dbp set (no ones source, no G32): db = the sum of these partial column
+  // sums [ndbp][N] in order
+  const float* dbp = nullptr;
+  int32_t ndbp = 0;
 };
 void gemm_dw16(const GemmDw16Args& a, cudaStream_t s);
 struct GemmDxArgs {  // [Y1 | Y2] = G W^T  (Y1 = first K1 cols, Y2 = the rest)
@@ -490,6 +499,11 @@ struct TailArgs {
   const int32_t *F, *labels;
   int32_t n_global;
   float* dH; int32_t ldg;           // dL/dH^{L-1} [n_1 x ldg] (ReLU derivative applied)
+  // dH16 set: dL/dH^{L-1} written as bf16 instead ([n_1 x ldg], dH unused),
+  // and db_part[b][d] (b < tail_db_parts(max_dst)) gets each CTA's column
+  // sums of what it wrote: db^{L-1} = their sum (the layer's bf16 dW)
+  void* dH16 = nullptr;
+  float* db_part = nullptr;
   float* dA;                        // scratch [n_0 x d]
   float* loss_partial;              // >= ceil(max_dst / 32) floats
   float* part;                      // tail_partial_floats(max_dst, d, C): per-CTA dW/db partials
@@ -497,6 +511,7 @@ struct TailArgs {
   float* zero; int64_t zero_n;      // cleared by k_tail_a (the other layers' dW/db), may be NULL
 };
 bool tail_supported(int kind, int d, int C, int fanout0);
+int tail_db_parts(int64_t max_dst);
 size_t tail_partial_floats(int64_t max_dst, int d, int C);
 void launch_tail(const TailArgs& a, cudaStream_t s, Timeline* tl, const std::string& sfx);
 // layers.cu

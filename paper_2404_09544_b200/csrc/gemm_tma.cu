@@ -1957,8 +1957,9 @@ void gemm_dw16(const GemmDw16Args& a, cudaStream_t s) {
     rows += sr.width;
     has_db = has_db || sr.ones;
   }
-  GNNV_REQUIRE(nt > 0 && (!has_db || a.db) && (!a.G32 || (a.db && !has_db && a.ldg32 % 4 == 0)), GNNV_ERR_PARAM,
-               "dw16: no source, a ones column without db, or G32 without db / with a ones column");
+  GNNV_REQUIRE(nt > 0 && (!has_db || a.db) && (!a.G32 || (a.db && !has_db && a.ldg32 % 4 == 0)) &&
+                   (!a.dbp || (a.db && !has_db && !a.G32)),
+               GNNV_ERR_PARAM, "dw16: no source, or an inconsistent db source (ones column / G32 / partials)");
   if (nt & 1) {  // the last group's second tile: stages the same boxes, stores nothing
     p.tile[nt] = p.tile[nt - 1];
     p.tile[nt].out_rows = 0;
@@ -1990,19 +1991,22 @@ void gemm_dw16(const GemmDw16Args& a, cudaStream_t s) {
     GNNV_TRY_CUDA(cudaFuncSetAttribute(k_tma_dw16, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
     attr = bytes;
   }
-  float* dbp = nullptr;
+  const float* dbp = a.dbp;
+  int ndbp = a.ndbp;
   const int conv_blocks = 2 * num_sms();
   if (a.G32) {  // G -> bf16 copy + db partials
-    dbp = (float*)g_dbpart.get((size_t)conv_blocks * a.N * sizeof(float), s);
+    float* dbw = (float*)g_dbpart.get((size_t)conv_blocks * a.N * sizeof(float), s);
     launch_k(k_g16_colsum, conv_blocks, 256, 0, s, a.G32, a.ldg32, a.d_M, a.N,
-             static_cast<__nv_bfloat16*>(const_cast<void*>(a.G16)), a.ldg, dbp);
+             static_cast<__nv_bfloat16*>(const_cast<void*>(a.G16)), a.ldg, dbw);
+    dbp = dbw;
+    ndbp = conv_blocks;
     GNNV_CHECK_LAUNCH();
   }
   launch_k(k_tma_dw16, dim3((unsigned)splits, (unsigned)groups), NTHREADS, bytes, s, p);
   GNNV_CHECK_LAUNCH();
   const int64_t total4 = (int64_t)p.prow * (a.N / 4);
   launch_k(k_dw16_reduce, (int)std::min<int64_t>(ceil_div(total4, 32), (int64_t)num_sms() * 8), 256, 0, s, p.part,
-           splits, p.prow, a.N, (has_db || a.G32) ? 1 : 0, a.dW, a.db, (const float*)dbp, dbp ? conv_blocks : 0);
+           splits, p.prow, a.N, (has_db || dbp) ? 1 : 0, a.dW, a.db, dbp, dbp ? ndbp : 0);
   GNNV_CHECK_LAUNCH();
 }
 

@@ -428,16 +428,21 @@ void layer_bwd_impl(gnnv_blocks* b, int32_t layer, const gnnv_layer_desc* ld, co
   w.db_fused = tf32 && !need_mask;
   w.zeroed = tf32 && grads_zeroed;
   if (tl) tl->mark(s, "gemm_dw" + sfx);
-  if (io && io->x16 && io->a16 && io->g16_out && !need_mask && tf32 && sage) {
+  if (io && io->x16 && io->a16 && (io->g16_out || io->g16_in) && !need_mask && tf32 && sage) {
     // hidden layer over bf16 operands (reading Q34): G (pre-masked fp32) ->
     // its bf16 copy + db = colsum(G) in one pass, then dW = [H16_dst |
     // A16]^T G16 by the MN-major kind::f16 kernel (four feature tiles)
     GemmDw16Args w16{};
-    w16.G32 = Gdst;
-    w16.ldg32 = ldo;
+    if (io->g16_in) {  // G and db's partials from the fused output layer
+      w16.dbp = io->dbp;
+      w16.ndbp = io->ndbp;
+    } else {
+      w16.G32 = Gdst;
+      w16.ldg32 = ldo;
+    }
     w16.src[0] = GemmDw16Src{io->x16, io->a16_ld, ld->d_in, 0, false};
     w16.src[1] = GemmDw16Src{io->a16, io->a16_ld, ld->d_in, ld->d_in, false};
-    w16.G16 = io->g16_out;
+    w16.G16 = io->g16_in ? io->g16_in : io->g16_out;
     w16.ldg = io->g16_ld;
     w16.N = ld->d_out;
     w16.d_M = d_ndst;
@@ -472,8 +477,8 @@ void layer_bwd_impl(gnnv_blocks* b, int32_t layer, const gnnv_layer_desc* ld, co
     x.K1 = ld->d_in;
     x.d_M = d_ndst;
     x.max_M = max_dst;
-    if (io && io->g16_out && io->x16 && io->a16 && !need_mask && tf32 && sage) {  // the copy the dW pass wrote
-      x.G16 = io->g16_out;
+    if (io && (io->g16_out || io->g16_in) && io->x16 && io->a16 && !need_mask && tf32 && sage) {  // G's bf16 copy
+      x.G16 = io->g16_in ? io->g16_in : io->g16_out;
       x.ldg16 = io->g16_ld;
     }
     const bool g16 = io && io->gsrc16;

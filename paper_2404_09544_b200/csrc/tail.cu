@@ -26,6 +26,8 @@
 // k_tail_b:
 //   dH[u] += relu'(H[u]) dA_v for the other edges  (k_spmm_bwd phase 2)
 //   dW, db = sum of the CTA partials in CTA order; loss = sum of partials / B
+#include <cuda_bf16.h>
+
 #include "common.cuh"
 
 namespace gnnv {
@@ -83,8 +85,12 @@ __global__ void __launch_bounds__(TA_WARPS * 32, 1) k_tail_a(
     const float* __restrict__ W, const float* __restrict__ bias, int d, int C, int aggr, float* __restrict__ A,
     int lda, float* __restrict__ Z, float* __restrict__ dZ, int ldz, const int32_t* __restrict__ F,
     const int32_t* __restrict__ labels, int n_global, float* dH, int ldg, float* dAs, float* __restrict__ part,
-    float* __restrict__ loss_partial, float* __restrict__ zero, int64_t zero_n) {
+    float* __restrict__ loss_partial, float* __restrict__ zero, int64_t zero_n, __nv_bfloat16* __restrict__ dH16,
+    float* __restrict__ db_part) {
   GNNV_PDL_ENTRY();
+  __shared__ float s_db[512];  // dH16: this CTA's column sums of dL/dH^{L-1}
+  if (dH16)
+    for (int c = threadIdx.x; c < d; c += blockDim.x) s_db[c] = 0.f;
   // the earlier layers' dW / db, accumulated atomically by their dW GEMMs
   // later in the step: cleared here instead of by memset nodes
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < zero_n; i += (int64_t)gridDim.x * blockDim.x)
@@ -271,7 +277,15 @@ __global__ void __launch_bounds__(TA_WARPS * 32, 1) k_tail_a(
         if (col < d) {
           const uint32_t word = __ldg(hbits + (int64_t)v * hbits_ld + (col >> 5));
           const uint32_t b = word >> (col & 31);
-          *reinterpret_cast<float2*>(dH + (int64_t)v * ldg + col) = make_float2(b & 1u ? x0 : 0.f, b & 2u ? x1 : 0.f);
+          const float m0 = b & 1u ? x0 : 0.f, m1 = b & 2u ? x1 : 0.f;
+          if (dH16) {
+            const __nv_bfloat162 hv = __floats2bfloat162_rn(m0, m1);
+            *reinterpret_cast<__nv_bfloat162*>(dH16 + (int64_t)v * ldg + col) = hv;
+            atomicAdd(&s_db[col], m0);
+            atomicAdd(&s_db[col + 1], m1);
+          } else {
+            *reinterpret_cast<float2*>(dH + (int64_t)v * ldg + col) = make_float2(m0, m1);
+          }
         } else {  // scaled by w_v by the row's warp below
           *reinterpret_cast<float2*>(dAs + (int64_t)v * d + (col - d)) = make_float2(x0, x1);
         }
@@ -281,11 +295,17 @@ __global__ void __launch_bounds__(TA_WARPS * 32, 1) k_tail_a(
   __syncthreads();
   // ---- owner edges store w_v dA_v into their row (k_spmm_bwd phase 1);
   //      padding columns of the seeds' own dH rows
+  float4 dbs[CPL];
+#pragma unroll
+  for (int j = 0; j < CPL; ++j) dbs[j] = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
   for (int q = 0; q < 2; ++q) {
     const int r = 2 * wid + q, v = v0 + r;
     if (v >= n) continue;
-    for (int c = d + lane; c < ldg; c += 32) dH[(int64_t)v * ldg + c] = 0.f;
+    for (int c = d + lane; c < ldg; c += 32) {
+      if (dH16) dH16[(int64_t)v * ldg + c] = __float2bfloat16_rn(0.f);
+      else dH[(int64_t)v * ldg + c] = 0.f;
+    }
     const float w = aggr == GNNV_AGGR_MEAN ? (cnt[q] ? 1.f / (float)cnt[q] : 0.f) : 1.f;
     float4 da[CPL];
 #pragma unroll
@@ -324,11 +344,37 @@ __global__ void __launch_bounds__(TA_WARPS * 32, 1) k_tail_a(
 #pragma unroll
         for (int j = 0; j < CPL; ++j) {
           const int c4 = lane + 32 * j;
-          if (c4 < d4) reinterpret_cast<float4*>(dH + (int64_t)us[e] * ldg)[c4] = f4mask(da[j], wd[e][j], 4 * c4);
+          if (c4 >= d4) continue;
+          const float4 m = f4mask(da[j], wd[e][j], 4 * c4);
+          if (dH16) {
+            const __nv_bfloat162 lo = __floats2bfloat162_rn(m.x, m.y), hi = __floats2bfloat162_rn(m.z, m.w);
+            reinterpret_cast<uint2*>(dH16 + (int64_t)us[e] * ldg)[c4] =
+                make_uint2(*reinterpret_cast<const uint32_t*>(&lo), *reinterpret_cast<const uint32_t*>(&hi));
+            dbs[j] = f4add_(dbs[j], m);
+          } else {
+            reinterpret_cast<float4*>(dH + (int64_t)us[e] * ldg)[c4] = m;
+          }
         }
-        for (int c = d + lane; c < ldg; c += 32) dH[(int64_t)us[e] * ldg + c] = 0.f;
+        for (int c = d + lane; c < ldg; c += 32) {
+          if (dH16) dH16[(int64_t)us[e] * ldg + c] = __float2bfloat16_rn(0.f);
+          else dH[(int64_t)us[e] * ldg + c] = 0.f;
+        }
       }
     }
+  }
+  if (dH16) {  // this CTA's column sums -> db_part[blockIdx.x]
+#pragma unroll
+    for (int j = 0; j < CPL; ++j) {
+      const int c4 = lane + 32 * j;
+      if (c4 < d4) {
+        atomicAdd(&s_db[4 * c4 + 0], dbs[j].x);
+        atomicAdd(&s_db[4 * c4 + 1], dbs[j].y);
+        atomicAdd(&s_db[4 * c4 + 2], dbs[j].z);
+        atomicAdd(&s_db[4 * c4 + 3], dbs[j].w);
+      }
+    }
+    __syncthreads();
+    for (int c = threadIdx.x; c < d; c += blockDim.x) db_part[(int64_t)blockIdx.x * d + c] = s_db[c];
   }
   // ---- per-CTA partials: P = X^T dZ (2d x C8, K = 32 rows) and colsum dZ
   {
@@ -370,7 +416,8 @@ __global__ void __launch_bounds__(256) k_tail_b(const int32_t* __restrict__ indp
                                                 const float* __restrict__ dAs, float* dH, int ldg,
                                                 const float* __restrict__ part, int nparts, int K, int C, float* dW,
                                                 float* db, const float* __restrict__ loss_partial, int n_global,
-                                                float* d_loss) {
+                                                float* d_loss, __nv_bfloat16* __restrict__ dH16,
+                                                float* __restrict__ db_part, int db_base) {
   GNNV_PDL_ENTRY();
   const int n = *d_ndst;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -382,28 +429,56 @@ __global__ void __launch_bounds__(256) k_tail_b(const int32_t* __restrict__ indp
     if (lane == 0) *d_loss = s * (1.f / (float)n_global);
   }
   if ((int)blockIdx.x < push_blocks) {
+    __shared__ float4 s_dbw[8][128];  // dH16: per-warp column sums (d <= 512)
     const int v = blockIdx.x * 8 + wid;
-    if (v >= n) return;
-    const int beg = indptr[v], cnt = indptr[v + 1] - beg;
-    const uint32_t rest = ~own[v] & (cnt >= 32 ? 0xffffffffu : ((1u << cnt) - 1u));
-    if (!rest) return;
-    const int my = lane < cnt ? __ldg(indices + beg + lane) : 0;
     const int d4 = d >> 2;
-    float4 da[CPL];
+    float4 dbs[CPL];
 #pragma unroll
-    for (int j = 0; j < CPL; ++j) {
-      const int c4 = lane + 32 * j;
-      da[j] = c4 < d4 ? reinterpret_cast<const float4*>(dAs + (int64_t)v * d)[c4] : make_float4(0.f, 0.f, 0.f, 0.f);
-    }
-    for (uint32_t o = rest; o; o &= o - 1) {
-      const int u = __shfl_sync(0xffffffffu, my, __ffs(o) - 1);
+    for (int j = 0; j < CPL; ++j) dbs[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+    const int beg = v < n ? indptr[v] : 0, cnt = v < n ? indptr[v + 1] - beg : 0;
+    const uint32_t rest = v < n ? ~own[v] & (cnt >= 32 ? 0xffffffffu : ((1u << cnt) - 1u)) : 0u;
+    if (rest) {
+      const int my = lane < cnt ? __ldg(indices + beg + lane) : 0;
+      float4 da[CPL];
 #pragma unroll
       for (int j = 0; j < CPL; ++j) {
         const int c4 = lane + 32 * j;
-        if (c4 < d4)
-          atomicAdd(reinterpret_cast<float4*>(dH + (int64_t)u * ldg) + c4,
-                    f4mask(da[j], __ldg(hbits + (int64_t)u * hbits_ld + ((4 * c4) >> 5)), 4 * c4));
+        da[j] = c4 < d4 ? reinterpret_cast<const float4*>(dAs + (int64_t)v * d)[c4] : make_float4(0.f, 0.f, 0.f, 0.f);
       }
+      for (uint32_t o = rest; o; o &= o - 1) {
+        const int u = __shfl_sync(0xffffffffu, my, __ffs(o) - 1);
+#pragma unroll
+        for (int j = 0; j < CPL; ++j) {
+          const int c4 = lane + 32 * j;
+          if (c4 >= d4) continue;
+          const float4 m = f4mask(da[j], __ldg(hbits + (int64_t)u * hbits_ld + ((4 * c4) >> 5)), 4 * c4);
+          if (dH16) {
+            uint32_t* p = reinterpret_cast<uint32_t*>(reinterpret_cast<uint2*>(dH16 + (int64_t)u * ldg) + c4);
+            const __nv_bfloat162 lo = __floats2bfloat162_rn(m.x, m.y), hi = __floats2bfloat162_rn(m.z, m.w);
+            asm volatile("red.global.add.noftz.bf16x2 [%0], %1;" ::"l"(p), "r"(*reinterpret_cast<const uint32_t*>(&lo))
+                         : "memory");
+            asm volatile("red.global.add.noftz.bf16x2 [%0], %1;" ::"l"(p + 1),
+                         "r"(*reinterpret_cast<const uint32_t*>(&hi))
+                         : "memory");
+            dbs[j] = f4add_(dbs[j], m);
+          } else {
+            atomicAdd(reinterpret_cast<float4*>(dH + (int64_t)u * ldg) + c4, m);
+          }
+        }
+      }
+    }
+    if (!dH16) return;
+    // this block's column sums -> db_part[db_base + blockIdx.x], warps added in order
+#pragma unroll
+    for (int j = 0; j < CPL; ++j) {
+      const int c4 = lane + 32 * j;
+      if (c4 < d4) s_dbw[wid][c4] = dbs[j];
+    }
+    __syncthreads();
+    for (int c4 = threadIdx.x; c4 < d4; c4 += blockDim.x) {
+      float4 t = s_dbw[0][c4];
+      for (int w = 1; w < 8; ++w) t = f4add_(t, s_dbw[w][c4]);
+      reinterpret_cast<float4*>(db_part + (int64_t)(db_base + blockIdx.x) * d)[c4] = t;
     }
     return;
   }
@@ -419,6 +494,10 @@ __global__ void __launch_bounds__(256) k_tail_b(const int32_t* __restrict__ indp
 bool tail_supported(int kind, int d, int C, int fanout0) {
   return kind == GNNV_KIND_SAGE && d >= 8 && d % 8 == 0 && d <= 512 && C >= 1 && C <= 64 && fanout0 <= 32 &&
          TailSmem(d, C).floats() * sizeof(float) <= 220 * 1024;
+}
+
+int tail_db_parts(int64_t max_dst) {
+  return (int)(ceil_div(std::max<int64_t>(max_dst, 1), TA_ROWS) + ceil_div(std::max<int64_t>(max_dst, 1), 8));
 }
 
 size_t tail_partial_floats(int64_t max_dst, int d, int C) {
@@ -438,7 +517,8 @@ static void launch_tail_cpl(const TailArgs& a, cudaStream_t s, Timeline* tl, con
   if (tl) tl->mark(s, "tail_a" + sfx);
   launch_k(k_tail_a<CPL>, ga, TA_WARPS * 32, smem, s, a.indptr, a.indices, a.own, a.d_ndst, a.H, a.ldh, a.hbits,
            a.hbits_ld, a.W, a.bias, a.d, a.C, a.aggr, a.A, a.lda, a.Z, a.dZ, a.ldz, a.F, a.labels, a.n_global, a.dH,
-           a.ldg, a.dA, a.part, a.loss_partial, a.zero, a.zero ? a.zero_n : (int64_t)0);
+           a.ldg, a.dA, a.part, a.loss_partial, a.zero, a.zero ? a.zero_n : (int64_t)0,
+           static_cast<__nv_bfloat16*>(a.dH16), a.db_part);
   GNNV_CHECK_LAUNCH();
   const int push_blocks = (int)ceil_div(std::max<int64_t>(a.max_dst, 1), 8);
   const int K = 2 * a.d;
@@ -446,7 +526,7 @@ static void launch_tail_cpl(const TailArgs& a, cudaStream_t s, Timeline* tl, con
   if (tl) tl->mark(s, "tail_b" + sfx);
   launch_k(k_tail_b<CPL>, push_blocks + red_blocks, 256, 0, s, a.indptr, a.indices, a.own, a.d_ndst, push_blocks,
            a.hbits, a.hbits_ld, a.d, a.dA, a.dH, a.ldg, a.part, ga, K, a.C, a.dW, a.db, a.loss_partial, a.n_global,
-           a.d_loss);
+           a.d_loss, static_cast<__nv_bfloat16*>(a.dH16), a.db_part, ga);
   GNNV_CHECK_LAUNCH();
 }
 

@@ -104,6 +104,12 @@ struct gnnv_trainer {
   // slower on products (layer 2: 60K rows, too few k-blocks per CTA to
   // amortise the per-CTA TMEM flush)
   void* G16h[GNNV_MAX_LAYERS + 1] = {nullptr};
+  // the fused output layer writes dL/dH^{L-1} only as bf16 (G16h[L-1],
+  // stride Hs[L-1]) and db^{L-1}'s partial column sums (tail_dbp): layer
+  // L-1's dW and dX then run over bf16 with no conversion pass (reading
+  // Q34); GNNV_NO_TAIL16=1: fp32 dL/dH^{L-1}
+  bool tail16 = false;
+  float* tail_dbp = nullptr;
   void* X16[2] = {nullptr, nullptr};
   void* A16[2] = {nullptr, nullptr};
   int32_t ld16x = 0;  // their row stride: d + 1 rounded up to 8
@@ -234,6 +240,7 @@ gnnv_status gnnv_trainer_free(gnnv_trainer* t) {
     dfree(t->A16h[i]);
     dfree(t->G16h[i]);
   }
+  dfree(t->tail_dbp);
   dfree(t->loss_partial);
   dfree(t->tail_dA);
   dfree(t->tail_part);
@@ -333,6 +340,15 @@ gnnv_status gnnv_trainer_create(gnnv_graph* g, gnnv_cache* c, const gnnv_model_d
             t->G16h[i] = dmalloc((size_t)b->max_n[L - i] * ((md->dims[i] + 31) / 32 * 32) * 2,
                                  "bf16 gradients (hidden-layer dW)");
         }
+      t->tail16 = t->tail && t->hid16 && L - 1 >= 2 && t->A16h[L - 1] && md->dims[L - 1] % 64 == 0 &&
+                  md->dims[L - 1] <= 256 && md->dims[L - 2] <= 256 && t->Hs[L - 1] % 8 == 0 &&
+                  !env_on("GNNV_NO_TAIL16");
+      if (t->tail16) {
+        dfree(t->G16h[L - 1]);
+        t->G16h[L - 1] = dmalloc((size_t)b->max_n[1] * t->Hs[L - 1] * 2, "bf16 dL/dH^{L-1} (output layer)");
+        t->tail_dbp = (float*)dmalloc((size_t)tail_db_parts(b->max_n[0]) * md->dims[L - 1] * sizeof(float),
+                                      "db^{L-1} partials (output layer)");
+      }
       // layer 1 aggregates a bf16 copy of the whole-table cache (reading Q31)
       t->table16 = t->x_fused && md->prec == GNNV_PREC_TF32 && md->kind == GNNV_KIND_SAGE &&
                    !env_on("GNNV_NO_BF16TABLE");
@@ -467,13 +483,14 @@ gnnv_status gnnv_trainer_gradient16(gnnv_trainer* t, int32_t i, const void** d_G
       *ld = t->ld16[i];
     } else {  // a hidden layer's dW operand (reading Q34)
       *d_G16 = t->G16h[i];
-      *ld = t->G16h[i] ? (t->md.dims[i] + 31) / 32 * 32 : 0;
+      *ld = !t->G16h[i] ? 0 : (t->tail16 && i == t->md.L - 1) ? t->Hs[i] : (t->md.dims[i] + 31) / 32 * 32;
     }
   });
 }
 
 int32_t gnnv_trainer_dw16(const gnnv_trainer* t) { return t && t->dw16 ? 1 : 0; }
 int32_t gnnv_trainer_fwd16(const gnnv_trainer* t) { return t && t->fwd16 ? 1 : 0; }
+int32_t gnnv_trainer_tail16(const gnnv_trainer* t) { return t && t->tail16 ? 1 : 0; }
 
 gnnv_status gnnv_trainer_aggregate16(gnnv_trainer* t, int32_t i, const void** d_A16, int32_t* ld) {
   return guarded([&] {
@@ -868,6 +885,10 @@ gnnv_status gnnv_step(gnnv_trainer* t, const int32_t* seeds, int32_t n_seeds, in
       a.n_global = n_global;
       a.dH = t->G[L - 1];
       a.ldg = t->Hs[L - 1];
+      if (t->tail16) {
+        a.dH16 = t->G16h[L - 1];
+        a.db_part = t->tail_dbp;
+      }
       a.dA = t->tail_dA;
       a.loss_partial = t->loss_partial;
       a.part = t->tail_part;
@@ -907,6 +928,13 @@ gnnv_status gnnv_step(gnnv_trainer* t, const int32_t* seeds, int32_t n_seeds, in
           io.a16_ld = t->ld16[i - 1];
           io.g16_out = t->G16h[i];
           io.g16_ld = (t->md.dims[i] + 31) / 32 * 32;
+          if (t->tail16 && i == L - 1) {  // G came as bf16 from the fused output layer
+            io.g16_out = nullptr;
+            io.g16_in = t->G16h[i];
+            io.g16_ld = t->Hs[i];
+            io.dbp = t->tail_dbp;
+            io.ndbp = tail_db_parts(b->max_n[0]);
+          }
         }
       }
       layer_bwd_impl(b, i, &ld, t->G[i], t->H[i], t->H[i - 1], t->A[i], t->d_params + t->w_off[i - 1],

@@ -137,6 +137,7 @@ _SIGS = {
     "gnnv_trainer_gradient16": (I32, [VP, I32, PP, C.POINTER(I32)]),
     "gnnv_trainer_dw16": (I32, [VP]),
     "gnnv_trainer_fwd16": (I32, [VP]),
+    "gnnv_trainer_tail16": (I32, [VP]),
     "gnnv_trainer_aggregate16": (I32, [VP, I32, PP, C.POINTER(I32)]),
     "gnnv_trainer_dw16_operands": (I32, [VP, PP, PP, C.POINTER(I32)]),
     "gnnv_step": (I32, [VP, VP, I32, I32, I32, U64, F32, C.POINTER(F32), C.POINTER(StepTiming), VP]),
@@ -600,6 +601,9 @@ class Trainer:
 
     def fwd16(self) -> bool:
         return bool(load().gnnv_trainer_fwd16(self.h))
+
+    def tail16(self) -> bool:
+        return bool(load().gnnv_trainer_tail16(self.h))
 
     def aggregate16(self, i: int):
         """(device pointer, row stride) of the bf16 copy of A^i the kind::f16 GEMMs read, or (0, 0)."""

@@ -983,7 +983,7 @@ def test_bf16_layer1_fwd(mini, option, pipelined):
     assert abs(losses["fwd16"] - losses["tf32"]) <= 2e-3 * abs(losses["tf32"]), losses
 
 
-@pytest.mark.parametrize("hdw", [0, 1], ids=["tf32dw", "bf16dw"])
+@pytest.mark.parametrize("hdw", [0, 1, 2], ids=["tf32dw", "bf16dw_conv", "bf16dw_tail"])
 @pytest.mark.parametrize("ratio", [0.3, 1.0])
 def test_bf16_hidden_layer_fwd(mini, option, ratio, hdw):
     """bf16 intermediates: layer 2's forward GEMM reads [bf16 H^1 dst prefix
@@ -1003,7 +1003,11 @@ def test_bf16_hidden_layer_fwd(mini, option, ratio, hdw):
     seeds = epoch_seeds(gd.n, 0)[: cfg["batch"]]
     B = len(seeds)
     losses = {}
-    option("GNNV_HID16_DW", hdw)  # opt-in: the hidden layer's dW and dX over bf16 too
+    # layer 2's dW/dX: TF32 over fp32 G; over bf16 with G converted in the
+    # dW call (opt-in GNNV_HID16_DW); over the fused output layer's bf16 G
+    # and db partials (the default, GNNV_NO_TAIL16=0)
+    option("GNNV_HID16_DW", 1 if hdw == 1 else 0)
+    option("GNNV_NO_TAIL16", 0 if hdw == 2 else 1)
     for name in ("hid16", "tf32"):
         option("GNNV_NO_HID16", 0 if name == "hid16" else 1)
         tr = gnnv.Trainer(g, gnnv.Cache(g, ratio), dims, cfg["fanouts"], B, w, prec=gnnv.PREC_TF32)
@@ -1030,7 +1034,7 @@ def test_bf16_hidden_layer_fwd(mini, option, ratio, hdw):
             assert_close_cond(H2, np.maximum(Z, 0), mag, 1e-5, "H^2 over the bf16 operands")
             grads = gnnv.unflat_params(tr.grads(), dims)
             pg, lg = tr.gradient16(2)
-            assert bool(pg) == bool(hdw)
+            assert bool(pg) == (hdw > 0) and tr.tail16() == (hdw == 2)
             if pg:  # layer 2's dW over the same operands and the bf16 copy of its (masked) G
                 G16 = read_bf16(pg, n2, lg)[:, : dims[2]]
                 assert_close_cond(grads[1][0], Xc.T @ G16, np.abs(Xc).T @ np.abs(G16), 1e-5, "dW^2 over bf16")
