@@ -74,8 +74,7 @@ __global__ void __launch_bounds__(256) k_gather(const int32_t* __restrict__ F, c
                                                 const float* __restrict__ host, int32_t stride,
                                                 float* __restrict__ X, unsigned long long* stats, int mat_level,
                                                 int32_t* __restrict__ rowidx, __nv_bfloat16* __restrict__ X16,
-                                                int32_t ldx16, int32_t ones_col, const uint4* __restrict__ T16,
-                                                int32_t ldt16) {
+                                                int32_t ldx16, int32_t ones_col) {
   GNNV_PDL_ENTRY();
   const int n = sizes[L];
   const int n_mat = mat_level < 0 ? 0 : sizes[mat_level];  // rows materialised in X (all, the dst prefix, none)
@@ -88,11 +87,9 @@ __global__ void __launch_bounds__(256) k_gather(const int32_t* __restrict__ F, c
     const int row = base + lane;
     const float4* src = nullptr;
     int kind = -1;  // 0 local, 1 peer, 2 host
-    int my_s = 0;
     if (row < n) {
       const int v = F[row];
       const int s = slot[v];
-      my_s = s;
       if (rowidx) rowidx[row] = s;  // cache row of every F_L row (whole-table cache, one shard)
       if (s >= 0) {
         const int o = s % G;
@@ -107,36 +104,6 @@ __global__ void __launch_bounds__(256) k_gather(const int32_t* __restrict__ F, c
     c_peer += __popc(__ballot_sync(0xffffffffu, kind == 1));
     c_miss += __popc(__ballot_sync(0xffffffffu, kind == 2));
     const int nrows = min(32, n_mat - base);
-    if (T16) {
-      // bf16 rows straight from the cache's bf16 table (whole table, one
-      // shard; the fp32 rows are not wanted): (row, 16-byte piece) items
-      // spread over the lanes, four loads in flight per lane, the ones
-      // column patched in
-      const int ldx8 = ldx16 >> 3, ldt8 = ldt16 >> 3, items = max(nrows, 0) * ldx8;
-      const int oc8 = ones_col >> 3, oh = ones_col & 7;
-      for (int i0 = 0; i0 < items; i0 += 32 * 4) {
-        uint4 val[4];
-        int rr[4], cc[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int it = i0 + u * 32 + lane;
-          rr[u] = it / ldx8;
-          cc[u] = it - rr[u] * ldx8;
-          const int sr = __shfl_sync(0xffffffffu, my_s, rr[u] & 31);
-          val[u] = (it < items && cc[u] < ldt8 && sr >= 0) ? __ldg(T16 + (int64_t)sr * ldt8 + cc[u]) : make_uint4(0u, 0u, 0u, 0u);
-        }
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          if (i0 + u * 32 + lane >= items) continue;
-          if (cc[u] == oc8) {
-            uint32_t* w = reinterpret_cast<uint32_t*>(&val[u]);
-            w[oh >> 1] = (oh & 1) ? ((w[oh >> 1] & 0xFFFFu) | 0x3F800000u) : ((w[oh >> 1] & 0xFFFF0000u) | 0x3F80u);
-          }
-          reinterpret_cast<uint4*>(X16)[(int64_t)(base + rr[u]) * ldx8 + cc[u]] = val[u];
-        }
-      }
-      continue;
-    }
     const uint64_t my = reinterpret_cast<uint64_t>(src);
     for (int r0 = 0; r0 < nrows; r0 += RU) {
       const float4* ps[RU];
@@ -186,9 +153,6 @@ void launch_gather(const gnnv_cache* c, const gnnv_blocks* b, float* d_X, int64_
   GNNV_REQUIRE(!d_X16 || (materialize && ldx16 % 4 == 0 && ldx16 >= std::max(g->stride, g->d + 1)), GNNV_ERR_UNSUPPORTED,
                "gather: the bf16 copy needs materialised rows and a stride (multiple of 4) covering the ones column");
   GNNV_REQUIRE(d_X || (d_X16 && d_rowidx) || (!materialize && d_rowidx), GNNV_ERR_PARAM, "gather: no output");
-  // bf16 rows only, whole table on this device: copy them from its bf16 copy
-  // (the same round-to-nearest-even values, half the bytes)
-  const bool t16 = !d_X && d_X16 && c->d_table16 && c->world == 1 && c->table16_ld % 8 == 0;
   constexpr int RU = 8;
   const int64_t rows_ub = b->max_n[b->L];
   const int64_t warps = ceil_div(rows_ub, 32);
@@ -197,9 +161,7 @@ void launch_gather(const gnnv_cache* c, const gnnv_blocks* b, float* d_X, int64_
                                                    c->rank, g->d_feats, g->stride, d_X,
                                                    reinterpret_cast<unsigned long long*>(d_stats),
                                                    !materialize ? -1 : d_rowidx ? b->L - 1 : b->L, d_rowidx,
-                                                   static_cast<__nv_bfloat16*>(d_X16), ldx16, g->d,
-                                                   t16 ? static_cast<const uint4*>(c->d_table16) : nullptr,
-                                                   c->table16_ld);
+                                                   static_cast<__nv_bfloat16*>(d_X16), ldx16, g->d);
   GNNV_CHECK_LAUNCH();
 }
 
