@@ -460,7 +460,14 @@ gnnv_status gnnv_trainer_dw16_operands(gnnv_trainer* t, const void** d_X16, cons
  *  loss_out     host float (loss summed over ranks) or NULL (then the call
  *               does not synchronise unless tm != NULL)
  *  tm           per-phase device times or NULL
- * Stream-ordered on `s`. */
+ * Stream-ordered on `s`.  Precision (GNNV_PREC_TF32 trainer, SAGE): the
+ * layer GEMMs run on tcgen05 in tf32 or, where the trainer keeps bf16
+ * operand copies (readings Q30-Q34, gnnv_trainer_dw16 / fwd16 / tail16,
+ * aggregate16), in bf16 (kind::f16), always with fp32 accumulation; each
+ * bf16 mode has a GNNV_NO_* switch.  Summation order: the bf16 dW
+ * (gemm_dw16) adds its per-CTA slices in a fixed order; the TF32 dW and the
+ * backward pushes (fp32 and bf16x2 reductions) are order-dependent at their
+ * rounding level, so gradients are not bitwise reproducible run to run. */
 gnnv_status gnnv_step(gnnv_trainer* t, const int32_t* seeds, int32_t n_seeds, int32_t seeds_on_host,
                       int32_t n_global, uint64_t rng_seed, float lr, float* loss_out, gnnv_step_timing* tm,
                       gnnv_stream s);
