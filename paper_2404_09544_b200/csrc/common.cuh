@@ -289,7 +289,10 @@ void launch_spmm_fwd(const int32_t* d_indptr, const int32_t* d_indices, const in
                      cudaStream_t s, const int32_t* rowidx = nullptr, const uint32_t* lastv = nullptr);
 void launch_spmm_bwd(const int32_t* d_indptr, const int32_t* d_indices, const uint32_t* d_own, const int32_t* d_ndst,
                      int64_t max_dst, const float* dA, int32_t lda, void* dH, int32_t ldh, int32_t d, int32_t kind,
-                     int32_t aggr, const uint32_t* bits, int32_t bits_ld, cudaStream_t s, bool dh_bf16 = false);
+                     int32_t aggr, const uint32_t* bits, int32_t bits_ld, cudaStream_t s, bool dh_bf16 = false,
+                     bool da_bf16 = false);
+// the wide bf16 push (a warp per dst row, 8 columns per lane) applies
+bool spmm_bwd_wide(int32_t ldh, int32_t lda, int32_t kind, bool dh_bf16);
 // the forward aggregation over bf16 source rows (stride ld16 elements)
 // rowidx != NULL: source row u is row rowidx[u] of H16 (the bf16 table)
 void launch_spmm_fwd_h16(const int32_t* d_indptr, const int32_t* d_indices, const int32_t* d_ndst, int64_t max_dst,
@@ -478,6 +481,7 @@ struct GemmDxArgs {  // [Y1 | Y2] = G W^T  (Y1 = first K1 cols, Y2 = the rest)
   const uint32_t* y1_bits = nullptr;
   int32_t y1_bits_ld = 0;
   void* Y1_16 = nullptr;  // TF32: Y1 stored as bf16 (row stride ld1, ld1 % 32 == 0) instead of Y1
+  void* Y2_16 = nullptr;  // TF32 with Y1_16: Y2 stored as bf16 too (row stride ld2, ld2 % 32 == 0) instead of Y2
   // TF32 mode: G as a bf16 copy ([M x ldg16]) -- the GEMM then runs kind::f16
   // with W rounded to bf16 (reading Q34); G unused.  NULL: off
   const void* G16 = nullptr;

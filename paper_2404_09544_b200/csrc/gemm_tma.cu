@@ -312,6 +312,8 @@ struct Params {
   __nv_bfloat16* y16;
   int ld16;
   __nv_bfloat16* y1_16;
+  __nv_bfloat16* y2_16;  // dX: Y2 (dA) as bf16 too
+  CUtensorMap ty2_16;
   int g16;
   // fwd/dX (not PAIR): dynamic tile scheduler -- [0] next tile counter,
   // [1] finished CTAs (the last one resets both); NULL: static round robin
@@ -796,7 +798,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_tma_gemm(const __grid_constant_
             for (int j = 0; j < 32; ++j)
               if (j0 + j < p.ld1 && !((wv >> j) & 1u)) v[j] = 0.f;
           }
-          if (MODE == MODE_DX && p.y1_16 && j0 < p.ld1 && row0 + 32 <= M) {
+          // dX pieces stored as bf16: Y1 (dH_dst) and/or Y2 (dA)
+          const bool y16c = MODE == MODE_DX && ((p.y1_16 && j0 < p.ld1) ||
+                                                (p.y2_16 && j0 >= p.ld1 && j0 - p.ld1 + 32 <= p.ld2));
+          if (y16c && row0 + 32 <= M) {
             // Y1 as bf16 (j0 + 32 <= ld1: checked on the host): the 2 KB
             // piece through a staging half and a TMA store (halves alternate,
             // so one store may still be reading while the next is written)
@@ -816,16 +821,18 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_tma_gemm(const __grid_constant_
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             __syncwarp();
             if (lane == 0) {
-              tma_store_2d(&p.ty16, ob0 + y16h * 2048, j0, row0);
+              if (j0 < p.ld1) tma_store_2d(&p.ty16, ob0 + y16h * 2048, j0, row0);
+              else tma_store_2d(&p.ty2_16, ob0 + y16h * 2048, j0 - p.ld1, row0);
               asm volatile("cp.async.bulk.commit_group;" ::: "memory");
             }
             y16h ^= 1;
             continue;
           }
-          if (MODE == MODE_DX && p.y1_16 && j0 < p.ld1) {  // ragged tile: the rows < M with plain stores
+          if (y16c) {  // ragged tile: the rows < M with plain stores
             const int64_t m = (int64_t)row0 + lane;
             if (m < M) {
-              uint4* dst = reinterpret_cast<uint4*>(p.y1_16 + m * p.ld1 + j0);
+              uint4* dst = j0 < p.ld1 ? reinterpret_cast<uint4*>(p.y1_16 + m * p.ld1 + j0)
+                                      : reinterpret_cast<uint4*>(p.y2_16 + m * p.ld2 + (j0 - p.ld1));
 #pragma unroll
               for (int q = 0; q < 4; ++q)
                 dst[q] = make_uint4(bf16x2(v[8 * q], v[8 * q + 1]), bf16x2(v[8 * q + 2], v[8 * q + 3]),
@@ -1917,6 +1924,11 @@ bool gemm_dx_tma(const GemmDxArgs& a, cudaStream_t s) {
     GNNV_REQUIRE(a.ld1 % 32 == 0 && a.Y2, GNNV_ERR_PARAM, "dX: a bf16 Y1 needs ld1 % 32 == 0 and Y2");
     p.y1_16 = static_cast<__nv_bfloat16*>(a.Y1_16);
     p.ty16 = make_map16(a.Y1_16, a.max_M, a.ld1, a.ld1, 32, 32);
+    if (a.Y2_16) {
+      GNNV_REQUIRE(a.ld2 % 32 == 0, GNNV_ERR_PARAM, "dX: a bf16 Y2 needs ld2 % 32 == 0");
+      p.y2_16 = static_cast<__nv_bfloat16*>(a.Y2_16);
+      p.ty2_16 = make_map16(a.Y2_16, a.max_M, a.ld2, a.ld2, 32, 32);
+    }
     p.ty1 = p.ty2;
   } else {
     p.ty1 = make_map(a.Y1, a.max_M, a.ld1, a.ld1, 32);

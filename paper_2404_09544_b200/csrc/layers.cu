@@ -482,6 +482,10 @@ void layer_bwd_impl(gnnv_blocks* b, int32_t layer, const gnnv_layer_desc* ld, co
       x.ldg16 = io->g16_ld;
     }
     const bool g16 = io && io->gsrc16;
+    // with the wide bf16 push, dA itself goes through as bf16 (the pushed
+    // rows are stored as bf16 anyway); GNNV_NO_DA16=1: fp32 dA
+    const bool da16 = sage && g16 && tf32 && lda % 32 == 0 && spmm_bwd_wide(io->gsrc16_ld, lda, ld->kind, true) &&
+                      !env_on("GNNV_NO_DA16");
     if (sage && g16) {  // dH_src (and its dst-prefix rows from the GEMM) as bf16
       x.Y1_16 = io->gsrc16;
       x.ld1 = io->gsrc16_ld;
@@ -489,6 +493,7 @@ void layer_bwd_impl(gnnv_blocks* b, int32_t layer, const gnnv_layer_desc* ld, co
       x.y1_bits_ld = src_bits_ld;
       x.Y2 = dA;
       x.ld2 = lda;
+      if (da16) x.Y2_16 = dA;  // the scratch holds bf16 rows then (stride lda elements)
     } else if (sage) {
       x.Y1 = Gsrc;  // dH_dst lands directly in rows [0, n_dst) of dH_src
       x.ld1 = ld->in_stride;
@@ -518,7 +523,7 @@ void layer_bwd_impl(gnnv_blocks* b, int32_t layer, const gnnv_layer_desc* ld, co
       // the rest add atomically -- no zeroing pass over dH_src
       if (g16)
         launch_spmm_bwd(b->d_indptr[h], b->d_indices[h], b->d_own[h], d_ndst, max_dst, dA, lda, io->gsrc16,
-                        io->gsrc16_ld, ld->d_in, ld->kind, ld->aggr, src_bits, src_bits_ld, s, true);
+                        io->gsrc16_ld, ld->d_in, ld->kind, ld->aggr, src_bits, src_bits_ld, s, true, da16);
       else
         launch_spmm_bwd(b->d_indptr[h], b->d_indices[h], b->d_own[h], d_ndst, max_dst, dA, lda, Gsrc, ld->in_stride,
                         ld->d_in, ld->kind, ld->aggr, tf32 ? src_bits : nullptr, src_bits_ld, s);

@@ -276,10 +276,11 @@ __global__ void __launch_bounds__(256) k_spmm_bwd(const int32_t* __restrict__ in
 // stores (phase 1) or four bf16x2 reductions per lane (phase 2), and a
 // lane's ReLU bits are one byte of the edge row's mask word.  SAGE only
 // (no self term); dH row stride ldh = 8 * lanes used, dA row stride lda.
+template <bool DA16>  // dA as bf16 (the dX epilogue's bf16 copy) instead of fp32
 __global__ void __launch_bounds__(256) k_spmm_bwd16w(const int32_t* __restrict__ indptr,
                                                      const int32_t* __restrict__ indices,
                                                      const uint32_t* __restrict__ own, const int32_t* d_ndst,
-                                                     const float* __restrict__ dA, int32_t lda,
+                                                     const void* __restrict__ dA, int32_t lda,
                                                      __nv_bfloat16* __restrict__ dH, int32_t ldh, int32_t d,
                                                      int32_t aggr, int32_t phase, const uint32_t* __restrict__ bits,
                                                      int32_t bits_ld) {
@@ -298,10 +299,22 @@ __global__ void __launch_bounds__(256) k_spmm_bwd16w(const int32_t* __restrict__
     const float w = (aggr == GNNV_AGGR_MEAN && cnt) ? 1.f / (float)cnt : 1.f;
     float g[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
     if (cok && 8 * c8 < d) {
-      const float4 a = __ldg(reinterpret_cast<const float4*>(dA + (int64_t)row * lda) + 2 * c8);
-      const float4 b = __ldg(reinterpret_cast<const float4*>(dA + (int64_t)row * lda) + 2 * c8 + 1);
-      g[0] = a.x * w; g[1] = a.y * w; g[2] = a.z * w; g[3] = a.w * w;
-      g[4] = b.x * w; g[5] = b.y * w; g[6] = b.z * w; g[7] = b.w * w;
+      if (DA16) {
+        const uint4 q = __ldg(reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(dA) + (int64_t)row * lda) + c8);
+        const uint32_t qw[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const __nv_bfloat162 h2 = *reinterpret_cast<const __nv_bfloat162*>(&qw[j]);
+          g[2 * j] = __low2float(h2) * w;
+          g[2 * j + 1] = __high2float(h2) * w;
+        }
+      } else {
+        const float* dAf = static_cast<const float*>(dA);
+        const float4 a = __ldg(reinterpret_cast<const float4*>(dAf + (int64_t)row * lda) + 2 * c8);
+        const float4 b = __ldg(reinterpret_cast<const float4*>(dAf + (int64_t)row * lda) + 2 * c8 + 1);
+        g[0] = a.x * w; g[1] = a.y * w; g[2] = a.z * w; g[3] = a.w * w;
+        g[4] = b.x * w; g[5] = b.y * w; g[6] = b.z * w; g[7] = b.w * w;
+      }
 #pragma unroll
       for (int j = 0; j < 8; ++j)
         if (8 * c8 + j >= d) g[j] = 0.f;
@@ -524,19 +537,28 @@ void launch_spmm_fwd(const int32_t* d_indptr, const int32_t* d_indices, const in
   GNNV_CHECK_LAUNCH();
 }
 
+bool spmm_bwd_wide(int32_t ldh, int32_t lda, int32_t kind, bool dh_bf16) {
+  return dh_bf16 && kind == GNNV_KIND_SAGE && ldh % 8 == 0 && ldh / 8 <= 32 && ldh / 8 > 16 && lda % 8 == 0 &&
+         !env_on("GNNV_BWD_NARROW");
+}
+
 void launch_spmm_bwd(const int32_t* d_indptr, const int32_t* d_indices, const uint32_t* d_own, const int32_t* d_ndst,
                      int64_t max_dst, const float* dA, int32_t lda, void* dH, int32_t ldh, int32_t d, int32_t kind,
-                     int32_t aggr, const uint32_t* bits, int32_t bits_ld, cudaStream_t s, bool dh_bf16) {
+                     int32_t aggr, const uint32_t* bits, int32_t bits_ld, cudaStream_t s, bool dh_bf16, bool da_bf16) {
   const int ldh4 = ldh / 4;
-  if (dh_bf16 && kind == GNNV_KIND_SAGE && ldh % 8 == 0 && ldh / 8 <= 32 && ldh / 8 > 16 && lda % 8 == 0 &&
-      !env_on("GNNV_BWD_NARROW")) {
+  if (spmm_bwd_wide(ldh, lda, kind, dh_bf16)) {
     for (int phase = 1; phase <= 2; ++phase) {
-      launch_k(k_spmm_bwd16w, spmm_grid(max_dst, 1), 256, 0, s, d_indptr, d_indices, d_own, d_ndst, dA, lda,
-               static_cast<__nv_bfloat16*>(dH), ldh, d, aggr, phase, bits, bits_ld);
+      if (da_bf16)
+        launch_k(k_spmm_bwd16w<true>, spmm_grid(max_dst, 1), 256, 0, s, d_indptr, d_indices, d_own, d_ndst,
+                 (const void*)dA, lda, static_cast<__nv_bfloat16*>(dH), ldh, d, aggr, phase, bits, bits_ld);
+      else
+        launch_k(k_spmm_bwd16w<false>, spmm_grid(max_dst, 1), 256, 0, s, d_indptr, d_indices, d_own, d_ndst,
+                 (const void*)dA, lda, static_cast<__nv_bfloat16*>(dH), ldh, d, aggr, phase, bits, bits_ld);
       GNNV_CHECK_LAUNCH();
     }
     return;
   }
+  GNNV_REQUIRE(!da_bf16, GNNV_ERR_PARAM, "spmm_bwd: a bf16 dA needs the wide bf16 push");
   for (int phase = 1; phase <= 2; ++phase) {
 #define GNNV_BWD(LPR, RPWv)                                                                                          \
   do {                                                                                                               \

@@ -78,7 +78,7 @@ struct TailSmem {
 };
 
 // CPL = float4 columns of a d-wide row per lane (d <= 128 CPL)
-template <int CPL>
+template <int CPL, bool B16>  // B16: dL/dH^{L-1} as bf16 + db partials (TailArgs::dH16)
 __global__ void __launch_bounds__(TA_WARPS * 32, 1) k_tail_a(
     const int32_t* __restrict__ indptr, const int32_t* __restrict__ indices, const uint32_t* __restrict__ own,
     const int32_t* d_ndst, const float* __restrict__ H, int ldh, const uint32_t* __restrict__ hbits, int hbits_ld,
@@ -89,7 +89,7 @@ __global__ void __launch_bounds__(TA_WARPS * 32, 1) k_tail_a(
     float* __restrict__ db_part) {
   GNNV_PDL_ENTRY();
   __shared__ float s_db[512];  // dH16: this CTA's column sums of dL/dH^{L-1}
-  if (dH16)
+  if (B16)
     for (int c = threadIdx.x; c < d; c += blockDim.x) s_db[c] = 0.f;
   // the earlier layers' dW / db, accumulated atomically by their dW GEMMs
   // later in the step: cleared here instead of by memset nodes
@@ -269,6 +269,7 @@ __global__ void __launch_bounds__(TA_WARPS * 32, 1) k_tail_a(
                         to_tf32(za[8 * L.zs + k0 + 4]), to_tf32(wb[0]), to_tf32(wb[4 * L.ws]));
       }
       const int col = n0 + 2 * t;
+      float cs0 = 0.f, cs1 = 0.f;  // dH16: this lane's part of the tile's column sums
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const int r = m0 + g + 8 * h, v = v0 + r;
@@ -278,16 +279,27 @@ __global__ void __launch_bounds__(TA_WARPS * 32, 1) k_tail_a(
           const uint32_t word = __ldg(hbits + (int64_t)v * hbits_ld + (col >> 5));
           const uint32_t b = word >> (col & 31);
           const float m0 = b & 1u ? x0 : 0.f, m1 = b & 2u ? x1 : 0.f;
-          if (dH16) {
+          if (B16) {
             const __nv_bfloat162 hv = __floats2bfloat162_rn(m0, m1);
             *reinterpret_cast<__nv_bfloat162*>(dH16 + (int64_t)v * ldg + col) = hv;
-            atomicAdd(&s_db[col], m0);
-            atomicAdd(&s_db[col + 1], m1);
+            cs0 += m0;
+            cs1 += m1;
           } else {
             *reinterpret_cast<float2*>(dH + (int64_t)v * ldg + col) = make_float2(m0, m1);
           }
         } else {  // scaled by w_v by the row's warp below
           *reinterpret_cast<float2*>(dAs + (int64_t)v * d + (col - d)) = make_float2(x0, x1);
+        }
+      }
+      if (B16 && col < d) {  // tile-uniform: sum the 8 row groups (lane bits 2..4), one add per column
+#pragma unroll
+        for (int o = 4; o < 32; o <<= 1) {
+          cs0 += __shfl_xor_sync(0xffffffffu, cs0, o);
+          cs1 += __shfl_xor_sync(0xffffffffu, cs1, o);
+        }
+        if (g == 0) {
+          atomicAdd(&s_db[col], cs0);
+          atomicAdd(&s_db[col + 1], cs1);
         }
       }
     }
@@ -303,7 +315,7 @@ __global__ void __launch_bounds__(TA_WARPS * 32, 1) k_tail_a(
     const int r = 2 * wid + q, v = v0 + r;
     if (v >= n) continue;
     for (int c = d + lane; c < ldg; c += 32) {
-      if (dH16) dH16[(int64_t)v * ldg + c] = __float2bfloat16_rn(0.f);
+      if (B16) dH16[(int64_t)v * ldg + c] = __float2bfloat16_rn(0.f);
       else dH[(int64_t)v * ldg + c] = 0.f;
     }
     const float w = aggr == GNNV_AGGR_MEAN ? (cnt[q] ? 1.f / (float)cnt[q] : 0.f) : 1.f;
@@ -346,7 +358,7 @@ __global__ void __launch_bounds__(TA_WARPS * 32, 1) k_tail_a(
           const int c4 = lane + 32 * j;
           if (c4 >= d4) continue;
           const float4 m = f4mask(da[j], wd[e][j], 4 * c4);
-          if (dH16) {
+          if (B16) {
             const __nv_bfloat162 lo = __floats2bfloat162_rn(m.x, m.y), hi = __floats2bfloat162_rn(m.z, m.w);
             reinterpret_cast<uint2*>(dH16 + (int64_t)us[e] * ldg)[c4] =
                 make_uint2(*reinterpret_cast<const uint32_t*>(&lo), *reinterpret_cast<const uint32_t*>(&hi));
@@ -356,13 +368,13 @@ __global__ void __launch_bounds__(TA_WARPS * 32, 1) k_tail_a(
           }
         }
         for (int c = d + lane; c < ldg; c += 32) {
-          if (dH16) dH16[(int64_t)us[e] * ldg + c] = __float2bfloat16_rn(0.f);
+          if (B16) dH16[(int64_t)us[e] * ldg + c] = __float2bfloat16_rn(0.f);
           else dH[(int64_t)us[e] * ldg + c] = 0.f;
         }
       }
     }
   }
-  if (dH16) {  // this CTA's column sums -> db_part[blockIdx.x]
+  if (B16) {  // this CTA's column sums -> db_part[blockIdx.x]
 #pragma unroll
     for (int j = 0; j < CPL; ++j) {
       const int c4 = lane + 32 * j;
@@ -409,7 +421,7 @@ __global__ void __launch_bounds__(TA_WARPS * 32, 1) k_tail_a(
 // blocks [0, push_blocks): warp per seed row, its non-owner edges' pushes;
 // the rest: thread per element of [dW | db], the CTA partials summed in CTA
 // order (deterministic); block 0 warp 0 also reduces the loss
-template <int CPL>
+template <int CPL, bool B16>  // B16: dL/dH^{L-1} as bf16 + db partials (TailArgs::dH16)
 __global__ void __launch_bounds__(256) k_tail_b(const int32_t* __restrict__ indptr, const int32_t* __restrict__ indices,
                                                 const uint32_t* __restrict__ own, const int32_t* d_ndst, int push_blocks,
                                                 const uint32_t* __restrict__ hbits, int hbits_ld, int d,
@@ -452,7 +464,7 @@ __global__ void __launch_bounds__(256) k_tail_b(const int32_t* __restrict__ indp
           const int c4 = lane + 32 * j;
           if (c4 >= d4) continue;
           const float4 m = f4mask(da[j], __ldg(hbits + (int64_t)u * hbits_ld + ((4 * c4) >> 5)), 4 * c4);
-          if (dH16) {
+          if (B16) {
             uint32_t* p = reinterpret_cast<uint32_t*>(reinterpret_cast<uint2*>(dH16 + (int64_t)u * ldg) + c4);
             const __nv_bfloat162 lo = __floats2bfloat162_rn(m.x, m.y), hi = __floats2bfloat162_rn(m.z, m.w);
             asm volatile("red.global.add.noftz.bf16x2 [%0], %1;" ::"l"(p), "r"(*reinterpret_cast<const uint32_t*>(&lo))
@@ -467,7 +479,7 @@ __global__ void __launch_bounds__(256) k_tail_b(const int32_t* __restrict__ indp
         }
       }
     }
-    if (!dH16) return;
+    if (!B16) return;
     // this block's column sums -> db_part[db_base + blockIdx.x], warps added in order
 #pragma unroll
     for (int j = 0; j < CPL; ++j) {
@@ -504,18 +516,19 @@ size_t tail_partial_floats(int64_t max_dst, int d, int C) {
   return (size_t)ceil_div(std::max<int64_t>(max_dst, 1), TA_ROWS) * ((size_t)2 * d * C + C);
 }
 
-template <int CPL>
+template <int CPL, bool B16>
 static void launch_tail_cpl(const TailArgs& a, cudaStream_t s, Timeline* tl, const std::string& sfx) {
   const size_t smem = TailSmem(a.d, a.C).floats() * sizeof(float);
   static size_t attr = 0;
   if (smem > attr) {
-    GNNV_TRY_CUDA(cudaFuncSetAttribute(k_tail_a<CPL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    GNNV_TRY_CUDA(cudaFuncSetAttribute(k_tail_a<CPL, B16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     attr = smem;
   }
   const int ga = (int)ceil_div(std::max<int64_t>(a.max_dst, 1), TA_ROWS);
   GNNV_REQUIRE(ga <= 4096, GNNV_ERR_PARAM, "output layer: too many seed rows for the loss partials");
+  GNNV_REQUIRE(!B16 || (a.db_part && a.d <= 512), GNNV_ERR_PARAM, "output layer: bf16 dH needs the db partials");
   if (tl) tl->mark(s, "tail_a" + sfx);
-  launch_k(k_tail_a<CPL>, ga, TA_WARPS * 32, smem, s, a.indptr, a.indices, a.own, a.d_ndst, a.H, a.ldh, a.hbits,
+  launch_k(k_tail_a<CPL, B16>, ga, TA_WARPS * 32, smem, s, a.indptr, a.indices, a.own, a.d_ndst, a.H, a.ldh, a.hbits,
            a.hbits_ld, a.W, a.bias, a.d, a.C, a.aggr, a.A, a.lda, a.Z, a.dZ, a.ldz, a.F, a.labels, a.n_global, a.dH,
            a.ldg, a.dA, a.part, a.loss_partial, a.zero, a.zero ? a.zero_n : (int64_t)0,
            static_cast<__nv_bfloat16*>(a.dH16), a.db_part);
@@ -524,10 +537,15 @@ static void launch_tail_cpl(const TailArgs& a, cudaStream_t s, Timeline* tl, con
   const int K = 2 * a.d;
   const int red_blocks = (int)ceil_div((int64_t)K * a.C + a.C, 256);
   if (tl) tl->mark(s, "tail_b" + sfx);
-  launch_k(k_tail_b<CPL>, push_blocks + red_blocks, 256, 0, s, a.indptr, a.indices, a.own, a.d_ndst, push_blocks,
+  launch_k(k_tail_b<CPL, B16>, push_blocks + red_blocks, 256, 0, s, a.indptr, a.indices, a.own, a.d_ndst, push_blocks,
            a.hbits, a.hbits_ld, a.d, a.dA, a.dH, a.ldg, a.part, ga, K, a.C, a.dW, a.db, a.loss_partial, a.n_global,
            a.d_loss, static_cast<__nv_bfloat16*>(a.dH16), a.db_part, ga);
   GNNV_CHECK_LAUNCH();
+}
+template <int CPL>
+static void launch_tail_cpl(const TailArgs& a, cudaStream_t s, Timeline* tl, const std::string& sfx) {
+  if (a.dH16) launch_tail_cpl<CPL, true>(a, s, tl, sfx);
+  else launch_tail_cpl<CPL, false>(a, s, tl, sfx);
 }
 
 void launch_tail(const TailArgs& a, cudaStream_t s, Timeline* tl, const std::string& sfx) {
