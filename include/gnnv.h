@@ -118,6 +118,13 @@ gnnv_status gnnv_debug_check_guards(int32_t* n_bad);
 const char* gnnv_version(void);
 /* Number of kernels libgnnv has launched in this process (monotonic). */
 uint64_t gnnv_launch_count(void);
+/* Host-link probe (measurement helper, Eq.6's bound): SM zero-copy reads of
+ * `bytes` of pinned host memory `h_buf` (page-locked by the caller,
+ * device-mapped), 16 bytes per thread and load, the pattern of the gather's
+ * cache misses at full row width; *ms = device time of `reps` passes
+ * (CUDA events on `s`).  Synchronises `s`.  Errors: PARAM (null, bytes not
+ * a multiple of 16), CUDA. */
+gnnv_status gnnv_host_read_probe(const void* h_buf, int64_t bytes, int32_t reps, float* ms, gnnv_stream s);
 /* d rounded up to a multiple of 4 (floats). */
 int32_t gnnv_row_stride(int32_t d);
 

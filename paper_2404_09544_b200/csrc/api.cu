@@ -263,6 +263,43 @@ gnnv_status gnnv_set_option(const char* name, int32_t value) {
 }
 const char* gnnv_version(void) { return GNNV_VERSION " sm_100a"; }
 uint64_t gnnv_launch_count(void) { return g_launches.load(); }
+
+}  // extern "C"
+namespace gnnv {
+__global__ void k_host_read(const uint4* __restrict__ h, int64_t n16, unsigned int* sink) {
+  uint32_t acc = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n16; i += (int64_t)gridDim.x * blockDim.x) {
+    const uint4 v = h[i];
+    acc ^= v.x ^ v.y ^ v.z ^ v.w;
+  }
+  if (acc == 0x9e3779b9u) atomicAdd(sink, 1u);  // keeps the loads
+}
+}  // namespace gnnv
+extern "C" {
+
+gnnv_status gnnv_host_read_probe(const void* h_buf, int64_t bytes, int32_t reps, float* ms, gnnv_stream stream) {
+  return guarded([&] {
+    GNNV_REQUIRE(h_buf && ms && bytes > 0 && bytes % 16 == 0 && reps >= 1, GNNV_ERR_PARAM, "host_read_probe: args");
+    void* d = nullptr;
+    GNNV_TRY_CUDA(cudaHostGetDevicePointer(&d, const_cast<void*>(h_buf), 0));
+    unsigned int* sink = (unsigned int*)dmalloc(sizeof(unsigned int), "probe sink");
+    cudaStream_t s = (cudaStream_t)stream;
+    cudaEvent_t e0, e1;
+    GNNV_TRY_CUDA(cudaEventCreate(&e0));
+    GNNV_TRY_CUDA(cudaEventCreate(&e1));
+    const int grid = num_sms() * 8;
+    k_host_read<<<grid, 256, 0, s>>>(static_cast<const uint4*>(d), bytes / 16, sink);  // warm-up
+    GNNV_TRY_CUDA(cudaEventRecord(e0, s));
+    for (int r = 0; r < reps; ++r) k_host_read<<<grid, 256, 0, s>>>(static_cast<const uint4*>(d), bytes / 16, sink);
+    GNNV_TRY_CUDA(cudaEventRecord(e1, s));
+    GNNV_TRY_CUDA(cudaEventSynchronize(e1));
+    GNNV_CHECK_LAUNCH();
+    GNNV_TRY_CUDA(cudaEventElapsedTime(ms, e0, e1));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    dfree(sink);
+  });
+}
 int32_t gnnv_row_stride(int32_t d) { return row_stride(d); }
 
 // ------------------------------------------------------------------ graph

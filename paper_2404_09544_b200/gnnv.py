@@ -138,6 +138,7 @@ _SIGS = {
     "gnnv_trainer_dw16": (I32, [VP]),
     "gnnv_trainer_fwd16": (I32, [VP]),
     "gnnv_trainer_tail16": (I32, [VP]),
+    "gnnv_host_read_probe": (I32, [VP, I64, I32, C.POINTER(C.c_float), VP]),
     "gnnv_trainer_aggregate16": (I32, [VP, I32, PP, C.POINTER(I32)]),
     "gnnv_trainer_dw16_operands": (I32, [VP, PP, PP, C.POINTER(I32)]),
     "gnnv_step": (I32, [VP, VP, I32, I32, I32, U64, F32, C.POINTER(F32), C.POINTER(StepTiming), VP]),
@@ -212,6 +213,13 @@ def check_guards() -> str:
 
 def launch_count() -> int:
     return int(load().gnnv_launch_count())
+
+
+def host_read_probe(h_ptr: int, nbytes: int, reps: int = 5, stream: int = 0) -> float:
+    """Device ms of `reps` SM zero-copy read passes over pinned host memory."""
+    ms = C.c_float(0.0)
+    _check(load().gnnv_host_read_probe(C.c_void_p(h_ptr), nbytes, reps, C.byref(ms), C.c_void_p(stream)))
+    return float(ms.value)
 
 
 def row_stride(d: int) -> int:
