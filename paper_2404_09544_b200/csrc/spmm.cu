@@ -179,9 +179,10 @@ __device__ __forceinline__ void dh_add4(void* dH, int64_t i4, float4 v) {
   if (!H16) {
     atomicAdd(reinterpret_cast<float4*>(dH) + i4, v);
   } else {
-    uint32_t* p = reinterpret_cast<uint32_t*>(reinterpret_cast<uint2*>(dH) + i4);
-    asm volatile("red.global.add.noftz.bf16x2 [%0], %1;" ::"l"(p), "r"(pack_bf16x2(v.x, v.y)) : "memory");
-    asm volatile("red.global.add.noftz.bf16x2 [%0], %1;" ::"l"(p + 1), "r"(pack_bf16x2(v.z, v.w)) : "memory");
+    uint2* p = reinterpret_cast<uint2*>(dH) + i4;  // one 8-byte bf16x4 reduction
+    asm volatile("red.global.add.noftz.v2.bf16x2 [%0], {%1, %2};" ::"l"(p), "r"(pack_bf16x2(v.x, v.y)),
+                 "r"(pack_bf16x2(v.z, v.w))
+                 : "memory");
   }
 }
 
@@ -348,11 +349,10 @@ __global__ void __launch_bounds__(256) k_spmm_bwd16w(const int32_t* __restrict__
           uint4* p = reinterpret_cast<uint4*>(dH + (int64_t)u[q] * ldh) + c8;
           if (phase == 1) {
             *p = make_uint4(h[0], h[1], h[2], h[3]);
-          } else {
-            uint32_t* p32 = reinterpret_cast<uint32_t*>(p);
-#pragma unroll
-            for (int j = 0; j < 4; ++j)
-              asm volatile("red.global.add.noftz.bf16x2 [%0], %1;" ::"l"(p32 + j), "r"(h[j]) : "memory");
+          } else {  // one 16-byte bf16x8 reduction (REDG.ADD.BF16x8)
+            asm volatile("red.global.add.noftz.v4.bf16x2 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(h[0]), "r"(h[1]),
+                         "r"(h[2]), "r"(h[3])
+                         : "memory");
           }
         }
       }

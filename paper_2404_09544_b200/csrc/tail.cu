@@ -465,12 +465,10 @@ __global__ void __launch_bounds__(256) k_tail_b(const int32_t* __restrict__ indp
           if (c4 >= d4) continue;
           const float4 m = f4mask(da[j], __ldg(hbits + (int64_t)u * hbits_ld + ((4 * c4) >> 5)), 4 * c4);
           if (B16) {
-            uint32_t* p = reinterpret_cast<uint32_t*>(reinterpret_cast<uint2*>(dH16 + (int64_t)u * ldg) + c4);
+            uint2* p = reinterpret_cast<uint2*>(dH16 + (int64_t)u * ldg) + c4;  // one bf16x4 reduction
             const __nv_bfloat162 lo = __floats2bfloat162_rn(m.x, m.y), hi = __floats2bfloat162_rn(m.z, m.w);
-            asm volatile("red.global.add.noftz.bf16x2 [%0], %1;" ::"l"(p), "r"(*reinterpret_cast<const uint32_t*>(&lo))
-                         : "memory");
-            asm volatile("red.global.add.noftz.bf16x2 [%0], %1;" ::"l"(p + 1),
-                         "r"(*reinterpret_cast<const uint32_t*>(&hi))
+            asm volatile("red.global.add.noftz.v2.bf16x2 [%0], {%1, %2};" ::"l"(p),
+                         "r"(*reinterpret_cast<const uint32_t*>(&lo)), "r"(*reinterpret_cast<const uint32_t*>(&hi))
                          : "memory");
             dbs[j] = f4add_(dbs[j], m);
           } else {
