@@ -436,7 +436,7 @@ gnnv_status gnnv_trainer_activation16(gnnv_trainer* t, int32_t i, const void** d
  * when the trainer keeps none. */
 gnnv_status gnnv_trainer_gradient16(gnnv_trainer* t, int32_t i, const void** d_G16, int32_t* ld);
 /* 1 if layer 1's dW runs over bf16 operands (gemm_dw16: bf16act and
- * table16, d_in + 1 <= 128, hidden a multiple of 64 up to 256, unless
+ * table16, d_in + 1 <= 256, hidden a multiple of 64 up to 256, unless
  * GNNV_NO_DW16; reading Q32).  Its operands of the last step: the bf16
  * copy of X's dst prefix with 1.0 in column d_in (the db column) and the
  * bf16 copy of A^1, both [n_dst x *ld] (borrowed device pointers). */

@@ -353,7 +353,7 @@ gnnv_status gnnv_trainer_create(gnnv_graph* g, gnnv_cache* c, const gnnv_model_d
       t->table16 = t->x_fused && md->prec == GNNV_PREC_TF32 && md->kind == GNNV_KIND_SAGE &&
                    !env_on("GNNV_NO_BF16TABLE");
       if (t->table16) cache_bf16_table(c);
-      t->dw16 = t->table16 && t->bf16act && !t->x_rows && md->dims[0] + 1 <= 128 && md->dims[1] % 64 == 0 &&
+      t->dw16 = t->table16 && t->bf16act && !t->x_rows && md->dims[0] + 1 <= 256 && md->dims[1] % 64 == 0 &&
                 md->dims[1] <= 256 && !env_on("GNNV_NO_DW16");
       t->ld16x = (md->dims[0] + 1 + 7) / 8 * 8;
       t->fwd16 = t->dw16 && !env_on("GNNV_NO_FWD16");
