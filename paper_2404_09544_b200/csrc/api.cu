@@ -31,14 +31,17 @@ bool env_on(const char* name) {
   g_opt_env.emplace_back(name, on);
   return on;
 }
+static std::vector<std::pair<std::string, int>> g_opt_env_int;  // integer options from the environment, read once
 int env_int(const char* name, int def) {
-  {
-    std::lock_guard<std::mutex> lk(g_opt_mu);
-    for (auto& kv : g_opt_override)
-      if (kv.first == name && kv.second >= 0) return kv.second;
-  }
+  std::lock_guard<std::mutex> lk(g_opt_mu);
+  for (auto& kv : g_opt_override)
+    if (kv.first == name && kv.second >= 0) return kv.second;
+  for (auto& kv : g_opt_env_int)
+    if (kv.first == name) return kv.second == INT_MIN ? def : kv.second;
   const char* e = getenv(name);
-  return e && e[0] ? atoi(e) : def;
+  const int v = e && e[0] ? atoi(e) : INT_MIN;
+  g_opt_env_int.emplace_back(name, v);
+  return v == INT_MIN ? def : v;
 }
 static thread_local int t_grid_cap = 0;
 void set_grid_cap(int cap) { t_grid_cap = cap; }
