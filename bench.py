@@ -462,8 +462,9 @@ def algorithmic(seg: str, sizes, cfg, dims, stride, prec, peaks):
     elif name == "gemm_dw":
         fl = 2.0 * n[h] * (K + 1) * d_out
         by = n[h] * (K * 4 if not dw16 else (K + 1) * 2) + n[h] * d_out * (2 if out16 else 4)
-        if hid16 and sizes.get("hid16_dw"):  # G (fp32) -> bf16 copy + db, then dW over [H16 | A16] and G16
-            by = n[h] * K * 2 + n[h] * d_out * (4 + 2 + 2)
+        if hid16 and sizes.get("hid16_dw"):  # dW over [H16 | A16] and G16
+            # G16 from the fused output layer (tail16), or converted from the fp32 G here (+ db)
+            by = n[h] * K * 2 + n[h] * d_out * (2 if (sizes.get("tail16") and i == L - 1) else 4 + 2 + 2)
     else:
         return None
     if prec == "fp32":
@@ -713,6 +714,7 @@ def main():
     sizes["fwd16"] = tr.fwd16()
     sizes["hid16"] = L >= 3 and bool(tr.aggregate16(2)[0])
     sizes["hid16_dw"] = L >= 3 and bool(tr.gradient16(L - 1)[0])
+    sizes["tail16"] = tr.tail16()
     peaks = load_peaks()
     if sizes["misses"] > 0:
         peaks["host"] = measure_host_link()
