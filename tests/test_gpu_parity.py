@@ -1046,6 +1046,34 @@ def test_bf16_hidden_layer_fwd(mini, option, ratio, hdw):
     assert abs(losses["hid16"] - losses["tf32"]) <= 2e-3 * abs(losses["tf32"]), losses
 
 
+@pytest.mark.parametrize("n", [1, 3, 33, 130])
+def test_tiny_batches_bf16_paths(mini, n):
+    """The whole-table TF32 trainer with every bf16 operand path on
+    (readings Q30-Q34) at batch sizes that leave every tile ragged or empty
+    (one seed: one row per layer-2 tile, a single k-block in the dW16 CTAs,
+    most CTAs without chunks): the step against the oracle -- loss at the
+    tf32 bound, every layer and dW/db through the oracle's chains."""
+    gd, g = mini
+    cfg = CONFIGS["mini"]
+    dims = [gd.d, cfg["hidden"], cfg["hidden"], gd.C]
+    L = len(cfg["fanouts"])
+    w = init_weights(dims)
+    seeds = epoch_seeds(gd.n, 3)[:n]
+    tr = gnnv.Trainer(g, gnnv.Cache(g, 1.0), dims, cfg["fanouts"], cfg["batch"], w, prec=gnnv.PREC_TF32)
+    try:
+        assert tr.dw16() and tr.fwd16() and tr.tail16()
+        loss, _ = tr.step(seeds, n, n, 0xBEEF + n, 0.0)
+        ref = train_step(gd.indptr, gd.indices, gd.feats, gd.d, gd.labels, seeds, cfg["fanouts"], 0xBEEF + n, w, 0.0)
+        assert abs(loss - ref["loss"]) <= 5e-3 * abs(ref["loss"]), (loss, ref["loss"])
+        hb = blocks_to_host(tr.blocks)
+        grads = gnnv.unflat_params(tr.grads(), dims)
+        X0 = oracle.gather_rows(gd.feats, hb[L - 1][4])[:, : dims[0]]
+        H, Aagg, blks = check_forward_chain(tr, hb, dims, w, RTOL[2], f"tiny{n}", X0=X0, max_rows=10**9)
+        check_backward_chain(tr, blks, H, Aagg, dims, w, grads, gd.labels[seeds], n, RTOL[2], f"tiny{n}")
+    finally:
+        tr.free()
+
+
 @pytest.mark.parametrize("kind", [gnnv.KIND_SAGE, gnnv.KIND_GCN])
 @pytest.mark.parametrize("ratio", [0.3, 1.0])
 def test_prefetched_layer1_aggregation_bitwise(mini, option, kind, ratio):
