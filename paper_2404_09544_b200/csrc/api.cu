@@ -497,6 +497,11 @@ void blocks_enable_owner_rows(gnnv_blocks* b, int h) {
   blocks_enable_csc(b, h);
 }
 
+void blocks_set_rowidx(gnnv_blocks* b, const int32_t* d_slot, int32_t* d_rowidx, int64_t* d_stats) {
+  b->rowidx_slot = d_slot;
+  b->d_rowidx = d_rowidx;
+  b->d_rowidx_stats = d_stats;
+}
 void blocks_enable_lastuse(gnnv_blocks* b) {
   if (b->d_lastv) return;
   b->d_lastv = (uint32_t*)dmalloc(b->max_n[b->L] * sizeof(uint32_t), "last-use slots");

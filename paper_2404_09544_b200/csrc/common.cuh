@@ -217,6 +217,11 @@ struct gnnv_blocks {
   // loads a row for the last time with an L2 evict_first hint
   // (blocks_enable_lastuse; NULL: off)
   uint32_t* d_lastv = nullptr;
+  // whole-table trainer (blocks_set_rowidx; NULL: off): k_reset also writes
+  // rowidx[i] = slot[F[i]] for every F_L row and the all-hit gather counters
+  int32_t* d_rowidx = nullptr;
+  const int32_t* rowidx_slot = nullptr;
+  int64_t* d_rowidx_stats = nullptr;
   // fused L2 push (blocks_enable_owner_rows): the hop's owner row of every
   // src id (the dst row whose edge discovered it; -1 for the dst prefix), and
   // its CSC holding the non-owner edges only (bit h of csc_nonowner)
@@ -275,6 +280,7 @@ size_t csc_scan_tmp_bytes(int64_t max_items);
 // gnnv_sample on b (setup path: allocates; synchronises the device)
 void blocks_enable_csc(gnnv_blocks* b, int h);
 void blocks_enable_lastuse(gnnv_blocks* b);
+void blocks_set_rowidx(gnnv_blocks* b, const int32_t* d_slot, int32_t* d_rowidx, int64_t* d_stats);
 void blocks_enable_owner_rows(gnnv_blocks* b, int h);  // + CSC of hop h's non-owner edges
 // cache.cu
 void launch_cache_update(gnnv_cache* c, const gnnv_blocks* b, const float* d_X, cudaStream_t s);

@@ -627,16 +627,38 @@ __global__ void k_csc_fill(int hp, int kp, const int32_t* sizes, const int32_t* 
   }
 }
 
-__global__ void k_reset(const int32_t* __restrict__ F, const int32_t* sizes, int L, int64_t N, int32_t* tag) {
+// Tags of F_L back to empty.  With rowidx (whole-table trainer): also every
+// F_L row's cache row, rowidx[i] = slot[F[i]], and the gather counters of
+// a cache that holds every row (n_L local hits) -- the trainer then needs
+// no gather pass.
+__global__ void k_reset(const int32_t* __restrict__ F, const int32_t* sizes, int L, int64_t N, int32_t* tag,
+                        const int32_t* __restrict__ slot, int32_t* __restrict__ rowidx,
+                        unsigned long long* __restrict__ stats) {
   GNNV_PDL_ENTRY();
   const int64_t n = sizes[L];
+  if (stats && blockIdx.x == 0 && threadIdx.x == 0) {
+    stats[0] = (unsigned long long)n;
+    stats[1] = (unsigned long long)n;
+    stats[2] = 0ull;
+    stats[3] = 0ull;
+  }
   for (int64_t i0 = 4 * (blockIdx.x * (int64_t)blockDim.x + threadIdx.x); i0 < n;
        i0 += 4 * (int64_t)gridDim.x * blockDim.x) {
     int v[4];
     load4(F, i0, n, v);
+    int r[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) r[j] = (rowidx && (uint32_t)v[j] < (uint64_t)N) ? __ldg(slot + v[j]) : 0;
 #pragma unroll
     for (int j = 0; j < 4; ++j)
       if ((uint32_t)v[j] < (uint64_t)N) tag[v[j]] = INT_MIN;
+    if (rowidx) {
+      if (i0 + 3 < n) {
+        *reinterpret_cast<int4*>(rowidx + i0) = make_int4(r[0], r[1], r[2], r[3]);
+      } else {
+        for (int j = 0; j < 4 && i0 + j < n; ++j) rowidx[i0 + j] = r[j];
+      }
+    }
   }
 }
 
@@ -711,7 +733,8 @@ void launch_sample(gnnv_graph* g, gnnv_blocks* b, const int32_t* d_seeds, int32_
     GNNV_CHECK_LAUNCH();
   }
   map_hop(L - 1);
-  launch_k(k_reset, grid_for(b->max_n[L], 1024), 256, 0, s, b->d_F, b->d_sizes, L, g->n, b->d_tag);
+  launch_k(k_reset, grid_for(b->max_n[L], 1024), 256, 0, s, b->d_F, b->d_sizes, L, g->n, b->d_tag, b->rowidx_slot,
+           b->d_rowidx, reinterpret_cast<unsigned long long*>(b->d_rowidx_stats));
   GNNV_CHECK_LAUNCH();
 }
 

@@ -380,6 +380,7 @@ gnnv_status gnnv_trainer_create(gnnv_graph* g, gnnv_cache* c, const gnnv_model_d
       GNNV_TRY_CUDA(cudaMemset(t->loss_counter, 0, sizeof(unsigned int)));
       t->d_stats = (int64_t*)dmalloc(4 * sizeof(int64_t), "gather stats");
       GNNV_TRY_CUDA(cudaMemset(t->d_stats, 0, 4 * sizeof(int64_t)));
+      if (t->fwd16) blocks_set_rowidx(b, c->d_slot, t->rowidx[0], t->d_stats);  // k_reset writes the cache rows
       for (auto& e : t->ev) GNNV_TRY_CUDA(cudaEventCreate(&e));
       // buffer set 0; set 1 is allocated by the first gnnv_trainer_prefetch
       t->bb[0] = t->b;
@@ -673,6 +674,7 @@ gnnv_status gnnv_trainer_prefetch(gnnv_trainer* t, const int32_t* seeds, int32_t
       t->d_seedsb[k] = (int32_t*)dmalloc(t->md.max_seeds * sizeof(int32_t), "seeds (prefetch)");
       GNNV_TRY_CUDA(cudaMallocHost(&t->h_seedsb[k], t->md.max_seeds * sizeof(int32_t)));
       t->d_statsb[k] = (int64_t*)dmalloc(4 * sizeof(int64_t), "gather stats (prefetch)");
+      if (t->fwd16) blocks_set_rowidx(t->bb[k], t->c->d_slot, t->rowidx[k], t->d_statsb[k]);
       if (t->dw16) alloc_dw16(t, k, t->bb[k]);
       if (t->pf_agg)
         t->A1b[k] = (float*)dmalloc((size_t)t->bb[k]->max_n[t->md.L - 1] * row_stride(t->md.dims[0]) * sizeof(float),
@@ -712,13 +714,14 @@ gnnv_status gnnv_trainer_prefetch(gnnv_trainer* t, const int32_t* seeds, int32_t
     } pf_launch;
     launch_sample(g, t->bb[k], d_seeds, n_seeds, rng_seed, t->side);
     t->bb[k]->sampled = true;
-    GNNV_TRY_CUDA(cudaMemsetAsync(t->d_statsb[k], 0, 4 * sizeof(int64_t), t->side));
+    if (!t->fwd16) GNNV_TRY_CUDA(cudaMemsetAsync(t->d_statsb[k], 0, 4 * sizeof(int64_t), t->side));
     if (tl) tl->mark(t->side, "pf_gather");
     if (t->c->dynamic && t->cache_pending) GNNV_TRY_CUDA(cudaStreamWaitEvent(t->side, t->ev_cache, 0));
-    // with fwd16 the layer-1 aggregation copies X's bf16 dst prefix itself:
-    // the gather only resolves every F_L row's cache row (and counts hits)
-    launch_gather(t->c, t->bb[k], t->fwd16 ? nullptr : t->X[k], t->d_statsb[k], t->side, t->rowidx[k],
-                  !t->x_rows && !t->fwd16, t->fwd16 ? nullptr : t->X16[k], t->ld16x);
+    // with fwd16 the layer-1 aggregation copies X's bf16 dst prefix itself
+    // and the sampler's last kernel wrote every F_L row's cache row and the
+    // counters: no gather pass
+    if (!t->fwd16)
+      launch_gather(t->c, t->bb[k], t->X[k], t->d_statsb[k], t->side, t->rowidx[k], !t->x_rows, t->X16[k], t->ld16x);
     if (t->c->dynamic) {  // NEXT-3 admission
       if (tl) tl->mark(t->side, "pf_replace");
       launch_cache_update(t->c, t->bb[k], t->X[k], t->side);
@@ -791,12 +794,12 @@ gnnv_status gnnv_step(gnnv_trainer* t, const int32_t* seeds, int32_t n_seeds, in
       if (tl) tl->mark(s, "sample");
       launch_sample(g, t->b, d_seeds, n_seeds, rng_seed, s);
       t->b->sampled = true;
-      GNNV_TRY_CUDA(cudaMemsetAsync(t->d_stats, 0, 4 * sizeof(int64_t), s));
+      if (!t->fwd16) GNNV_TRY_CUDA(cudaMemsetAsync(t->d_stats, 0, 4 * sizeof(int64_t), s));
       if (tm) GNNV_TRY_CUDA(cudaEventRecord(t->ev[1], s));
       if (tl) tl->mark(s, "gather");
       if (t->c->dynamic && t->cache_pending) GNNV_TRY_CUDA(cudaStreamWaitEvent(s, t->ev_cache, 0));
-      launch_gather(t->c, t->b, t->fwd16 ? nullptr : t->H[0], t->d_stats, s, t->rowidx[t->cur],
-                    !t->x_rows && !t->fwd16, t->fwd16 ? nullptr : t->X16[t->cur], t->ld16x);
+      if (!t->fwd16)
+        launch_gather(t->c, t->b, t->H[0], t->d_stats, s, t->rowidx[t->cur], !t->x_rows, t->X16[t->cur], t->ld16x);
       if (t->c->dynamic) {  // NEXT-3 admission (Eq.5's t_replace)
         if (tl) tl->mark(s, "replace");
         launch_cache_update(t->c, t->b, t->H[0], s);
