@@ -99,15 +99,24 @@ typedef enum { GNNV_PREC_FP32 = 0, GNNV_PREC_BF16 = 1, GNNV_PREC_TF32 = 2 } gnnv
 
 /* ------------------------------------------------------------------ misc */
 const char* gnnv_last_error(void);
-/* Opt-in variants, by name (each measured slower than, or equal to, the
- * default on the products workload): GNNV_XROWS,
- * GNNV_GEMM_PAIR, GNNV_BWD_PULL, GNNV_NO_TAIL, GNNV_NO_PDL, GNNV_L2PUSH,
- * GNNV_LASTUSE, GNNV_STATIC_TILES, GNNV_PF_AGG, GNNV_NO_BF16ACT, GNNV_NO_BF16TABLE.
- * value 1 = on, 0 = off, -1 = back to the environment variable of the same
- * name (read once per process; set and not "0" = on).  Takes effect for
- * trainers / blocks created (XROWS, NO_TAIL, BWD_PULL, L2PUSH, LASTUSE, PF_AGG, NO_BF16ACT, NO_BF16TABLE) or
- * kernels launched (GEMM_PAIR, NO_PDL, STATIC_TILES) afterwards.  PARAM on an unknown
- * name.  Process-wide; not for concurrent use with running steps. */
+/* Named options (DESIGN.md §9 has each one's measurement on products).
+ * Opt-in variants, measured slower than or equal to the default: GNNV_XROWS,
+ * GNNV_GEMM_PAIR, GNNV_BWD_PULL, GNNV_L2PUSH, GNNV_LASTUSE,
+ * GNNV_STATIC_TILES, GNNV_PF_AGG, GNNV_HID16_DW (a hidden layer's dW/dX over
+ * a converted bf16 G), GNNV_BWD_NARROW (the 4-column bf16 push).
+ * Switches back to the fp32 / TF32 form of a default path: GNNV_NO_TAIL,
+ * GNNV_NO_PDL, GNNV_NO_BF16ACT (Q30), GNNV_NO_BF16TABLE (Q31), GNNV_NO_DW16
+ * (Q32), GNNV_NO_FWD16 (Q33), GNNV_NO_HID16 and GNNV_NO_TAIL16 (Q34),
+ * GNNV_NO_DA16 (fp32 dA in the bf16 push).  Integer options:
+ * GNNV_PF_CAP (CTA cap of the Eq.4 prefetch's launches, 0 = none),
+ * GNNV_PF_PRIO (its stream priority), GNNV_DW16_MINKB (k-blocks per CTA
+ * of the bf16 dW, default 16).
+ * value 1 = on, 0 = off (integers: the value, >= 0 here; a negative
+ * priority only through the environment), -1 = back to the environment
+ * variable of the same name (read once per process; set and not "0" = on).
+ * Options that shape a trainer or blocks take effect for those created
+ * afterwards, the rest for kernels launched afterwards.  PARAM on an
+ * unknown name.  Process-wide; not for concurrent use with running steps. */
 gnnv_status gnnv_set_option(const char* name, int32_t value);
 /* Debug (GNNV_GUARD_ALLOC=1 in the environment when the first allocation is
  * made): every library allocation carries 64 KB guard regions before and

@@ -248,9 +248,12 @@ gnnv_status gnnv_debug_check_guards(int32_t* n_bad) {
 
 gnnv_status gnnv_set_option(const char* name, int32_t value) {
   return guarded([&] {
-    static const char* known[] = {"GNNV_XROWS", "GNNV_GEMM_PAIR", "GNNV_BWD_PULL", "GNNV_NO_TAIL", "GNNV_NO_PDL",
-                                  "GNNV_L2PUSH", "GNNV_LASTUSE", "GNNV_STATIC_TILES", "GNNV_PF_AGG", "GNNV_NO_BF16ACT",
-                                  "GNNV_NO_BF16TABLE", "GNNV_NO_DW16", "GNNV_PF_CAP", "GNNV_NO_FWD16", "GNNV_NO_HID16", "GNNV_DW16_MINKB", "GNNV_HID16_DW", "GNNV_PF_PRIO", "GNNV_BWD_NARROW", "GNNV_NO_TAIL16", "GNNV_NO_DA16"};
+    static const char* known[] = {"GNNV_XROWS",      "GNNV_GEMM_PAIR",    "GNNV_BWD_PULL",   "GNNV_NO_TAIL",
+                                  "GNNV_NO_PDL",     "GNNV_L2PUSH",       "GNNV_LASTUSE",    "GNNV_STATIC_TILES",
+                                  "GNNV_PF_AGG",     "GNNV_NO_BF16ACT",   "GNNV_NO_BF16TABLE", "GNNV_NO_DW16",
+                                  "GNNV_PF_CAP",     "GNNV_NO_FWD16",     "GNNV_NO_HID16",   "GNNV_DW16_MINKB",
+                                  "GNNV_HID16_DW",   "GNNV_PF_PRIO",      "GNNV_BWD_NARROW", "GNNV_NO_TAIL16",
+                                  "GNNV_NO_DA16"};
     GNNV_REQUIRE(name, GNNV_ERR_PARAM, "set_option: null name");
     bool ok = false;
     for (const char* k : known) ok |= strcmp(k, name) == 0;
