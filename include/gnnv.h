@@ -465,6 +465,14 @@ gnnv_status gnnv_trainer_aggregate16(gnnv_trainer* t, int32_t i, const void** d_
  * (bf16 intermediates with the fused output layer, unless GNNV_NO_TAIL16;
  * reading Q34).  gnnv_trainer_gradient16(L-1) then returns that copy. */
 int32_t gnnv_trainer_tail16(const gnnv_trainer* t);
+/* 1 if the trainer's sampler leaves the last hop unrelabelled (with
+ * gnnv_trainer_fwd16, unless GNNV_NO_LASTROWS or GNNV_LASTUSE): the last
+ * hop's sampled ids claim no local id, so its block (gnnv_blocks_info of
+ * gnnv_trainer_blocks) has n_src = n_dst and F_L = F_{L-1}, and its CSR
+ * indices are the ids' cache-table rows (slot[u]; the cache's d_order maps
+ * them back); gnnv_trainer_rowidx covers F_{L-1} and the gather counters
+ * count F_{L-1}'s rows.  The same sampled edges as the relabelled form. */
+int32_t gnnv_trainer_last_rows(const gnnv_trainer* t);
 gnnv_status gnnv_trainer_dw16_operands(gnnv_trainer* t, const void** d_X16, const void** d_A16, int32_t* ld);
 
 /* One iteration of Algorithm 1 on this rank's seed slice:

@@ -253,7 +253,7 @@ gnnv_status gnnv_set_option(const char* name, int32_t value) {
                                   "GNNV_PF_AGG",     "GNNV_NO_BF16ACT",   "GNNV_NO_BF16TABLE", "GNNV_NO_DW16",
                                   "GNNV_PF_CAP",     "GNNV_NO_FWD16",     "GNNV_NO_HID16",   "GNNV_DW16_MINKB",
                                   "GNNV_HID16_DW",   "GNNV_PF_PRIO",      "GNNV_BWD_NARROW", "GNNV_NO_TAIL16",
-                                  "GNNV_NO_DA16"};
+                                  "GNNV_NO_DA16",    "GNNV_NO_LASTROWS"};
     GNNV_REQUIRE(name, GNNV_ERR_PARAM, "set_option: null name");
     bool ok = false;
     for (const char* k : known) ok |= strcmp(k, name) == 0;
@@ -505,6 +505,7 @@ void blocks_set_rowidx(gnnv_blocks* b, const int32_t* d_slot, int32_t* d_rowidx,
   b->d_rowidx = d_rowidx;
   b->d_rowidx_stats = d_stats;
 }
+void blocks_set_last_rows(gnnv_blocks* b, const int32_t* d_slot) { b->last_rows = d_slot; }
 void blocks_enable_lastuse(gnnv_blocks* b) {
   if (b->d_lastv) return;
   b->d_lastv = (uint32_t*)dmalloc(b->max_n[b->L] * sizeof(uint32_t), "last-use slots");

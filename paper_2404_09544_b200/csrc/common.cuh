@@ -222,6 +222,11 @@ struct gnnv_blocks {
   int32_t* d_rowidx = nullptr;
   const int32_t* rowidx_slot = nullptr;
   int64_t* d_rowidx_stats = nullptr;
+  // whole-table trainer (blocks_set_last_rows; NULL: off): the last hop is
+  // not relabelled -- its sampled ids claim no tag, get no local id, and its
+  // CSR indices are their cache-table rows last_rows[u] (F_L = F_{L-1});
+  // the layer-1 aggregation reads the table rows directly
+  const int32_t* last_rows = nullptr;
   // fused L2 push (blocks_enable_owner_rows): the hop's owner row of every
   // src id (the dst row whose edge discovered it; -1 for the dst prefix), and
   // its CSC holding the non-owner edges only (bit h of csc_nonowner)
@@ -281,6 +286,7 @@ size_t csc_scan_tmp_bytes(int64_t max_items);
 void blocks_enable_csc(gnnv_blocks* b, int h);
 void blocks_enable_lastuse(gnnv_blocks* b);
 void blocks_set_rowidx(gnnv_blocks* b, const int32_t* d_slot, int32_t* d_rowidx, int64_t* d_stats);
+void blocks_set_last_rows(gnnv_blocks* b, const int32_t* d_slot);
 void blocks_enable_owner_rows(gnnv_blocks* b, int h);  // + CSC of hop h's non-owner edges
 // cache.cu
 void launch_cache_update(gnnv_cache* c, const gnnv_blocks* b, const float* d_X, cudaStream_t s);
@@ -304,7 +310,7 @@ bool spmm_bwd_wide(int32_t ldh, int32_t lda, int32_t kind, bool dh_bf16);
 void launch_spmm_fwd_h16(const int32_t* d_indptr, const int32_t* d_indices, const int32_t* d_ndst, int64_t max_dst,
                          const void* H16, int32_t ld16, float* A, int32_t lda, int32_t d, int32_t kind, int32_t aggr,
                          cudaStream_t s, const int32_t* rowidx = nullptr, void* A16 = nullptr, int32_t lda16 = 0,
-                         void* X16 = nullptr);
+                         void* X16 = nullptr, bool rows_direct = false);
 // the same transposed aggregation pulled per src row (rows up to
 // kPullMaxLd floats; wider ones keep the push) through the block's
 // CSC (one coalesced store per dH row, no atomics; see k_spmm_bwd_pull)
@@ -399,6 +405,7 @@ struct Bf16Io {
   const void* x16 = nullptr;
   bool keep_a32 = false;  // fwd with x16: still write the fp32 A (a TF32 dW reads it)
   void* x16_out = nullptr;  // fwd, bf16 aggregation: also copy each dst row's own bf16 row here (+ ones column)
+  bool rows_direct = false;  // fwd, with src16_rows: the block's indices are already table rows (last_rows)
   // bwd with x16 and a16, G pre-masked fp32: write G's bf16 copy here (stride
   // g16_ld) and run dW over bf16 (gemm_dw16; db by the conversion pass)
   void* g16_out = nullptr;

@@ -284,7 +284,7 @@ void layer_fwd_impl(gnnv_blocks* b, int32_t layer, const gnnv_layer_desc* ld, co
     if (io && io->src16)
       launch_spmm_fwd_h16(b->d_indptr[h], b->d_indices[h], d_ndst, b->max_n[h], io->src16, io->src16_ld,
                           io->x16 && io->a16 && !io->keep_a32 ? nullptr : A, lda, ld->d_in, ld->kind, ld->aggr, s, io->src16_rows,
-                          io->a16, io->a16_ld, io->x16_out);
+                          io->a16, io->a16_ld, io->x16_out, io->rows_direct);
     else
       launch_spmm_fwd(b->d_indptr[h], b->d_indices[h], d_ndst, b->max_n[h], rowidx ? agg_table : Hsrc,
                       ld->in_stride, A, lda, ld->d_in, ld->kind, ld->aggr, s, rowidx,

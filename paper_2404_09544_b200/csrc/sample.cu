@@ -117,7 +117,8 @@ __device__ __forceinline__ void map_slots(int64_t t0, int64_t stride, int hp, in
                                           const int32_t* __restrict__ indptrp, const int32_t* tag,
                                           int32_t* __restrict__ indicesp, int32_t* __restrict__ csc_cnt = nullptr,
                                           uint32_t* __restrict__ lastv = nullptr,
-                                          const uint32_t* __restrict__ csc_skip_own = nullptr) {
+                                          const uint32_t* __restrict__ csc_skip_own = nullptr,
+                                          const int32_t* __restrict__ rows_of = nullptr) {
   const int64_t nslots = (int64_t)sizes[hp] * kp;
   for (int64_t e0 = 4 * t0; e0 < nslots; e0 += 4 * stride) {
     int u[4], t[4], dst[4];
@@ -133,7 +134,7 @@ __device__ __forceinline__ void map_slots(int64_t t0, int64_t stride, int hp, in
         const int r = (int)(e / kp), i = (int)(e - (int64_t)r * kp);
         if (i < __ldg(cntp + r)) {
           dst[j] = __ldg(indptrp + r) + i;
-          t[j] = tag[u[j]];
+          t[j] = rows_of ? __ldg(rows_of + u[j]) : tag[u[j]];  // rows_of: the id's cache-table row
           if (csc_skip_own) owner[j] = (__ldg(csc_skip_own + r) >> i) & 1u;
         }
       }
@@ -201,7 +202,7 @@ __global__ void __launch_bounds__(256) k_sample_hop(const int64_t* __restrict__ 
       const int e = r * k + slot;
       ell[e] = u;
       if ((uint32_t)u < (uint64_t)N) {
-        if (tag[u] < -(2 + e)) atomicMax(&tag[u], -(2 + e));  // skip if an earlier slot already claimed u
+        if (tag && tag[u] < -(2 + e)) atomicMax(&tag[u], -(2 + e));  // skip if an earlier slot already claimed u
       }
     }
     if (active && gl == 0) {
@@ -274,7 +275,7 @@ __global__ void __launch_bounds__(256) k_sample_hop_tpr(const int64_t* __restric
     if (i < c) {
       const int e = r * k + i;
       ell[e] = u[i];
-      if ((uint32_t)u[i] < (uint64_t)N && tag[u[i]] < -(2 + e)) atomicMax(&tag[u[i]], -(2 + e));
+      if (tag && (uint32_t)u[i] < (uint64_t)N && tag[u[i]] < -(2 + e)) atomicMax(&tag[u[i]], -(2 + e));
     }
   }
   cnt[r] = c;
@@ -417,7 +418,7 @@ __global__ void __launch_bounds__(256) k_sample_hop_biased(const int64_t* __rest
       const int u = __ldg(&indices[beg + pos]);
       const int e = r * k + lane;
       ell[e] = u;
-      if ((uint32_t)u < (uint64_t)N && tag[u] < -(2 + e)) atomicMax(&tag[u], -(2 + e));
+      if (tag && (uint32_t)u < (uint64_t)N && tag[u] < -(2 + e)) atomicMax(&tag[u], -(2 + e));
     }
     if (lane == 0) {
       cnt[r] = c;
@@ -596,12 +597,12 @@ __global__ void k_map(int hp, int kp, const int32_t* sizes, const int32_t* __res
                       const int32_t* __restrict__ cntp, const int32_t* __restrict__ indptrp, const int32_t* tag,
                       int32_t* __restrict__ indicesp, unsigned long long* scan, int64_t scan_words,
                       int32_t* __restrict__ csc_cnt, uint32_t* __restrict__ lastv,
-                      const uint32_t* __restrict__ csc_skip_own) {
+                      const uint32_t* __restrict__ csc_skip_own, const int32_t* __restrict__ rows_of) {
   GNNV_PDL_ENTRY();
   const int64_t t0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x, stride = (int64_t)gridDim.x * blockDim.x;
   const int64_t used = std::min<int64_t>(scan_words, 1 + ((int64_t)sizes[hp] + kScanTile - 1) / kScanTile);
   for (int64_t i = t0; i < used; i += stride) scan[i] = 0ull;
-  map_slots(t0, stride, hp, kp, sizes, ellp, cntp, indptrp, tag, indicesp, csc_cnt, lastv, csc_skip_own);
+  map_slots(t0, stride, hp, kp, sizes, ellp, cntp, indptrp, tag, indicesp, csc_cnt, lastv, csc_skip_own, rows_of);
 }
 
 // CSC fill of hop hp (counting sort): colptr = exclusive scan of the in-edge
@@ -684,7 +685,8 @@ void launch_sample(gnnv_graph* g, gnnv_blocks* b, const int32_t* d_seeds, int32_
     launch_k(k_map, grid_for(slots_ub, 1024), 256, 0, s, hp, b->fanouts[hp], b->d_sizes, b->d_ell, b->d_cnt,
              b->d_indptr[hp], b->d_tag, b->d_indices[hp], b->d_scan, b->scan_words,
              csc ? b->d_csc_cnt : (int32_t*)nullptr, hp == L - 1 ? b->d_lastv : (uint32_t*)nullptr,
-             csc && ((b->csc_nonowner >> hp) & 1u) ? b->d_own[hp] : (const uint32_t*)nullptr);
+             csc && ((b->csc_nonowner >> hp) & 1u) ? b->d_own[hp] : (const uint32_t*)nullptr,
+             hp == L - 1 ? b->last_rows : (const int32_t*)nullptr);
     GNNV_CHECK_LAUNCH();
     if (!csc) return;
     size_t tmp = b->csc_tmp_bytes;
@@ -701,32 +703,36 @@ void launch_sample(gnnv_graph* g, gnnv_blocks* b, const int32_t* d_seeds, int32_
     const int64_t rows_ub = b->max_n[h];
     if (h > 0) map_hop(h - 1);
     const int threads = 256;
+    // the whole-table trainer's last hop (b->last_rows): no claims, no local ids
+    int32_t* const tagh = (h == L - 1 && b->last_rows) ? nullptr : b->d_tag;
 #define GNNV_SAMPLE_LAUNCH(G)                                                                              \
   launch_k(k_sample_hop<G>, grid_for(rows_ub, threads / 32 * (32 / G)), threads, 0, s,                  \
-      g->d_indptr, g->d_indices, g->n, b->d_F, b->d_sizes, h, k, rng_seed, b->d_ell, b->d_cnt, b->d_tag, b->d_own[h])
+      g->d_indptr, g->d_indices, g->n, b->d_F, b->d_sizes, h, k, rng_seed, b->d_ell, b->d_cnt, tagh, b->d_own[h])
     if (b->loc_w > 1) {
       launch_k(k_sample_hop_biased, grid_for(rows_ub, 8), 256, 0, s, g->d_indptr, g->d_indices, g->n, b->d_F,
-               b->d_sizes, h, k, rng_seed, b->loc_slot, (int)b->loc_w, b->d_ell, b->d_cnt, b->d_tag, b->d_own[h]);
+               b->d_sizes, h, k, rng_seed, b->loc_slot, (int)b->loc_w, b->d_ell, b->d_cnt, tagh, b->d_own[h]);
     } else if (k <= 4) {
       launch_k(k_sample_hop_tpr<4>, grid_for(rows_ub, threads), threads, 0, s, 
-          g->d_indptr, g->d_indices, g->n, b->d_F, b->d_sizes, h, k, rng_seed, b->d_ell, b->d_cnt, b->d_tag, b->d_own[h]);
+          g->d_indptr, g->d_indices, g->n, b->d_F, b->d_sizes, h, k, rng_seed, b->d_ell, b->d_cnt, tagh, b->d_own[h]);
     } else if (k <= 8) {
       launch_k(k_sample_hop_tpr<8>, grid_for(rows_ub, threads), threads, 0, s, 
-          g->d_indptr, g->d_indices, g->n, b->d_F, b->d_sizes, h, k, rng_seed, b->d_ell, b->d_cnt, b->d_tag, b->d_own[h]);
+          g->d_indptr, g->d_indices, g->n, b->d_F, b->d_sizes, h, k, rng_seed, b->d_ell, b->d_cnt, tagh, b->d_own[h]);
     } else if (k <= 16 && rows_ub < 16384) {
       GNNV_SAMPLE_LAUNCH(16);  // few rows: lanes per row beat rows per thread
     } else if (k <= 16) {
       launch_k(k_sample_hop_tpr<16>, grid_for(rows_ub, threads), threads, 0, s, 
-          g->d_indptr, g->d_indices, g->n, b->d_F, b->d_sizes, h, k, rng_seed, b->d_ell, b->d_cnt, b->d_tag, b->d_own[h]);
+          g->d_indptr, g->d_indices, g->n, b->d_F, b->d_sizes, h, k, rng_seed, b->d_ell, b->d_cnt, tagh, b->d_own[h]);
     } else {
       GNNV_SAMPLE_LAUNCH(32);
     }
 #undef GNNV_SAMPLE_LAUNCH
     GNNV_CHECK_LAUNCH();
     const int tiles_ub = capped_grid(ceil_div(rows_ub, kScanTile));
-    launch_k(k_winners, grid_for(rows_ub * k, 1024), 256, 0, s, g->n, h, k, b->d_sizes, b->d_ell, b->d_cnt, b->d_tag,
-                                                             b->d_own[h]);
-    GNNV_CHECK_LAUNCH();
+    if (tagh) {  // no winners without claims: own[] stays zero, the scan numbers no new ids
+      launch_k(k_winners, grid_for(rows_ub * k, 1024), 256, 0, s, g->n, h, k, b->d_sizes, b->d_ell, b->d_cnt, b->d_tag,
+               b->d_own[h]);
+      GNNV_CHECK_LAUNCH();
+    }
     launch_k(k_relabel_scan, tiles_ub, kScanTile, 0, s, g->n, h, k, L, b->d_ell, b->d_cnt, b->d_tag, b->d_F,
                                                   b->d_indptr[h], b->d_own[h], b->d_sizes, b->d_scan,
              h == L - 1 ? b->d_lastv : (uint32_t*)nullptr, b->d_owner_row[h]);

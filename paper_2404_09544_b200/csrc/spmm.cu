@@ -589,7 +589,7 @@ __device__ __forceinline__ void add_bf16x8(float* acc, uint4 q) {
     acc[2 * k + 1] += __uint_as_float(w[k] & 0xFFFF0000u);
   }
 }
-template <int LPR, bool IND>
+template <int LPR, int IND>  // IND 0: rows of H; 1: rows rowidx[.] of H; 2: indices are H rows, the self row rowidx[row]
 __global__ void __launch_bounds__(256, 8) k_spmm_fwd_h16(const int32_t* __restrict__ indptr,
                                                       const int32_t* __restrict__ indices, const int32_t* d_ndst,
                                                       const __nv_bfloat16* __restrict__ H, int32_t ld16,
@@ -632,7 +632,7 @@ __global__ void __launch_bounds__(256, 8) k_spmm_fwd_h16(const int32_t* __restri
       }
       for (int e0 = 0; e0 < cnt; e0 += LPR) {
         int my = (e0 + sl < cnt) ? __ldg(indices + beg + e0 + sl) : 0;
-        if (IND) my = __ldg(rowidx + my);
+        if (IND == 1) my = __ldg(rowidx + my);
         const int m = min(LPR, cnt - e0);
         int j = 0;
         for (; j + 4 <= m; j += 4) {
@@ -677,7 +677,8 @@ __global__ void __launch_bounds__(256, 8) k_spmm_fwd_h16(const int32_t* __restri
 
 void launch_spmm_fwd_h16(const int32_t* d_indptr, const int32_t* d_indices, const int32_t* d_ndst, int64_t max_dst,
                          const void* H16, int32_t ld16, float* A, int32_t lda, int32_t d, int32_t kind, int32_t aggr,
-                         cudaStream_t s, const int32_t* rowidx, void* A16, int32_t lda16, void* X16) {
+                         cudaStream_t s, const int32_t* rowidx, void* A16, int32_t lda16, void* X16,
+                         bool rows_direct) {
   const int vec8 = (d + 7) / 8;
   GNNV_REQUIRE(!A16 || (lda16 % 8 == 0 && lda16 >= 8 * vec8), GNNV_ERR_UNSUPPORTED,
                "spmm_fwd_h16: the bf16 output stride must be a multiple of 8 covering d");
@@ -692,11 +693,14 @@ void launch_spmm_fwd_h16(const int32_t* d_indptr, const int32_t* d_indices, cons
   const __nv_bfloat16* H = static_cast<const __nv_bfloat16*>(H16);
 #define GNNV_H16(LPR, RPWv)                                                                                          \
   do {                                                                                                               \
-    if (rowidx)                                                                                                      \
-      launch_k(k_spmm_fwd_h16<LPR, true>, spmm_grid(max_dst, RPWv), 256, 0, s, d_indptr, d_indices, d_ndst, H, ld16, \
+    if (rowidx && rows_direct)                                                                                       \
+      launch_k(k_spmm_fwd_h16<LPR, 2>, spmm_grid(max_dst, RPWv), 256, 0, s, d_indptr, d_indices, d_ndst, H, ld16,    \
+               A, lda, d, kind, aggr, rowidx, a16, lda16, x16, ones_col);                                            \
+    else if (rowidx)                                                                                                 \
+      launch_k(k_spmm_fwd_h16<LPR, 1>, spmm_grid(max_dst, RPWv), 256, 0, s, d_indptr, d_indices, d_ndst, H, ld16,    \
                A, lda, d, kind, aggr, rowidx, a16, lda16, x16, ones_col);                                            \
     else                                                                                                             \
-      launch_k(k_spmm_fwd_h16<LPR, false>, spmm_grid(max_dst, RPWv), 256, 0, s, d_indptr, d_indices, d_ndst, H,      \
+      launch_k(k_spmm_fwd_h16<LPR, 0>, spmm_grid(max_dst, RPWv), 256, 0, s, d_indptr, d_indices, d_ndst, H,          \
                ld16, A, lda, d, kind, aggr, (const int32_t*)nullptr, a16, lda16, x16, ones_col);                     \
   } while (0)
   if (vec8 <= 8) GNNV_H16(8, 4);

@@ -110,6 +110,10 @@ struct gnnv_trainer {
   // Q34); GNNV_NO_TAIL16=1: fp32 dL/dH^{L-1}
   bool tail16 = false;
   float* tail_dbp = nullptr;
+  // with fwd16: the sampler does not relabel the last hop; its CSR indices
+  // are the sampled ids' cache-table rows (blocks_set_last_rows) and the
+  // layer-1 aggregation reads them directly.  GNNV_NO_LASTROWS=1: relabelled
+  bool last_rows = false;
   void* X16[2] = {nullptr, nullptr};
   void* A16[2] = {nullptr, nullptr};
   int32_t ld16x = 0;  // their row stride: d + 1 rounded up to 8
@@ -381,6 +385,8 @@ gnnv_status gnnv_trainer_create(gnnv_graph* g, gnnv_cache* c, const gnnv_model_d
       t->d_stats = (int64_t*)dmalloc(4 * sizeof(int64_t), "gather stats");
       GNNV_TRY_CUDA(cudaMemset(t->d_stats, 0, 4 * sizeof(int64_t)));
       if (t->fwd16) blocks_set_rowidx(b, c->d_slot, t->rowidx[0], t->d_stats);  // k_reset writes the cache rows
+      t->last_rows = t->fwd16 && !t->lastuse && !env_on("GNNV_NO_LASTROWS");
+      if (t->last_rows) blocks_set_last_rows(b, c->d_slot);
       for (auto& e : t->ev) GNNV_TRY_CUDA(cudaEventCreate(&e));
       // buffer set 0; set 1 is allocated by the first gnnv_trainer_prefetch
       t->bb[0] = t->b;
@@ -492,6 +498,7 @@ gnnv_status gnnv_trainer_gradient16(gnnv_trainer* t, int32_t i, const void** d_G
 int32_t gnnv_trainer_dw16(const gnnv_trainer* t) { return t && t->dw16 ? 1 : 0; }
 int32_t gnnv_trainer_fwd16(const gnnv_trainer* t) { return t && t->fwd16 ? 1 : 0; }
 int32_t gnnv_trainer_tail16(const gnnv_trainer* t) { return t && t->tail16 ? 1 : 0; }
+int32_t gnnv_trainer_last_rows(const gnnv_trainer* t) { return t && t->last_rows ? 1 : 0; }
 
 gnnv_status gnnv_trainer_aggregate16(gnnv_trainer* t, int32_t i, const void** d_A16, int32_t* ld) {
   return guarded([&] {
@@ -675,6 +682,7 @@ gnnv_status gnnv_trainer_prefetch(gnnv_trainer* t, const int32_t* seeds, int32_t
       GNNV_TRY_CUDA(cudaMallocHost(&t->h_seedsb[k], t->md.max_seeds * sizeof(int32_t)));
       t->d_statsb[k] = (int64_t*)dmalloc(4 * sizeof(int64_t), "gather stats (prefetch)");
       if (t->fwd16) blocks_set_rowidx(t->bb[k], t->c->d_slot, t->rowidx[k], t->d_statsb[k]);
+      if (t->last_rows) blocks_set_last_rows(t->bb[k], t->c->d_slot);
       if (t->dw16) alloc_dw16(t, k, t->bb[k]);
       if (t->pf_agg)
         t->A1b[k] = (float*)dmalloc((size_t)t->bb[k]->max_n[t->md.L - 1] * row_stride(t->md.dims[0]) * sizeof(float),
@@ -736,7 +744,7 @@ gnnv_status gnnv_trainer_prefetch(gnnv_trainer* t, const int32_t* seeds, int32_t
         launch_spmm_fwd_h16(bk->d_indptr[h], bk->d_indices[h], bk->d_sizes + h, bk->max_n[h], t->c->d_table16,
                             t->c->table16_ld, t->fwd16 ? nullptr : t->A1b[k], row_stride(t->md.dims[0]),
                             t->md.dims[0], t->md.kind, t->md.aggr, t->side, t->rowidx[k], t->A16[k], t->ld16x,
-                            t->fwd16 ? t->X16[k] : nullptr);
+                            t->fwd16 ? t->X16[k] : nullptr, t->last_rows);
       else
         launch_spmm_fwd(bk->d_indptr[h], bk->d_indices[h], bk->d_sizes + h, bk->max_n[h],
                         t->x_fused ? t->table : t->X[k], g->stride, t->A1b[k], row_stride(t->md.dims[0]),
@@ -833,6 +841,7 @@ gnnv_status gnnv_step(gnnv_trainer* t, const int32_t* seeds, int32_t n_seeds, in
         if (t->fwd16) {
           io.x16 = t->X16[t->cur];
           io.x16_out = t->X16[t->cur];  // written by the aggregation (self rows + ones column)
+          io.rows_direct = t->last_rows;
         }
       }
       if (t->bf16act) {

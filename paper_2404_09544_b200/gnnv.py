@@ -138,6 +138,7 @@ _SIGS = {
     "gnnv_trainer_dw16": (I32, [VP]),
     "gnnv_trainer_fwd16": (I32, [VP]),
     "gnnv_trainer_tail16": (I32, [VP]),
+    "gnnv_trainer_last_rows": (I32, [VP]),
     "gnnv_host_read_probe": (I32, [VP, I64, I32, C.POINTER(C.c_float), VP]),
     "gnnv_trainer_aggregate16": (I32, [VP, I32, PP, C.POINTER(I32)]),
     "gnnv_trainer_dw16_operands": (I32, [VP, PP, PP, C.POINTER(I32)]),
@@ -492,7 +493,11 @@ class Trainer:
     def blocks(self) -> "Blocks":
         """The blocks of the last step (borrowed; with the Eq.4 prefetch the
         trainer alternates between two buffer sets)."""
-        return Blocks(self.g, self._max_seeds, self._fanouts, h=C.c_void_p(load().gnnv_trainer_blocks(self.h)))
+        b = Blocks(self.g, self._max_seeds, self._fanouts, h=C.c_void_p(load().gnnv_trainer_blocks(self.h)))
+        # the last hop's indices are cache-table rows (gnnv_trainer_last_rows):
+        # the cache's degree order maps them back to vertex ids
+        b.last_rows_order = self.cache.info().d_order if self.last_rows() else None
+        return b
 
     def step(self, seeds, n_seeds: int, n_global: int, rng_seed: int, lr: float, on_host: bool = True,
              want_loss: bool = True, timing: bool = False, stream=None):
@@ -612,6 +617,9 @@ class Trainer:
 
     def tail16(self) -> bool:
         return bool(load().gnnv_trainer_tail16(self.h))
+
+    def last_rows(self) -> bool:
+        return bool(load().gnnv_trainer_last_rows(self.h))
 
     def aggregate16(self, i: int):
         """(device pointer, row stride) of the bf16 copy of A^i the kind::f16 GEMMs read, or (0, 0)."""

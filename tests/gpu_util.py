@@ -96,7 +96,13 @@ def _cudart():
 
 
 def blocks_to_host(blocks: gnnv.Blocks):
-    """Per hop: (n_dst, n_src, indptr, indices, src_global) on the host."""
+    """Per hop: (n_dst, n_src, indptr, indices, src_global) on the host.
+
+    A trainer that leaves its last hop unrelabelled (gnnv_trainer_last_rows:
+    indices are cache-table rows, F_L = F_{L-1}) is brought to the relabelled
+    form here: rows -> vertex ids through the cache's degree order, then new
+    local ids in first-appearance (CSR) order after F_{L-1} -- the numbering
+    the sampler's scan gives -- so every check sees the same blocks."""
     torch.cuda.synchronize()
     views = blocks.info(sync=True)
     out = []
@@ -105,6 +111,22 @@ def blocks_to_host(blocks: gnnv.Blocks):
         indices = read_i32(v.d_indices, v.nnz)
         F = read_i32(v.d_src_global, v.n_src)
         out.append((int(v.n_dst), int(v.n_src), indptr, indices, F))
+    order_ptr = getattr(blocks, "last_rows_order", None)
+    if order_ptr:
+        nd, ns, indptr, rows, F = out[-1]
+        assert ns == nd, "last_rows: the last hop adds no frontier entries"
+        order = read_i32(order_ptr, blocks.g.n)
+        ids = order[rows]
+        local = {int(u): i for i, u in enumerate(F)}
+        Fl = list(F)
+        idx = np.empty(len(ids), np.int32)
+        for e, u in enumerate(ids.tolist()):
+            j = local.get(u)
+            if j is None:
+                j = local[u] = len(Fl)
+                Fl.append(u)
+            idx[e] = j
+        out[-1] = (nd, len(Fl), indptr, idx, np.asarray(Fl, np.int32))
     return out
 
 

@@ -80,6 +80,11 @@ def check_blocks_and_gather(gd, tr, ref_frontiers, ref_blocks, ratio):
         Xr = oracle.gather_rows(gd.feats, Fx)[:, : gd.d]
         np.testing.assert_array_equal(X16[:, : gd.d], bf16_round(Xr), err_msg="bf16 copy of the gathered rows")
         np.testing.assert_array_equal(X16[:, gd.d], 1.0)
+    # a trainer that leaves its last hop unrelabelled (gnnv_trainer_last_rows)
+    # resolves and counts the rows of F_{L-1}: the last hop's edges carry
+    # their table rows themselves (checked through blocks_to_host above)
+    if tr.last_rows():
+        FL = ref_frontiers[-2]
     if ratio == 1.0:
         pr, pt = tr.rowidx()
         ridx = read_i32(pr, len(FL))

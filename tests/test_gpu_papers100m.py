@@ -69,6 +69,8 @@ def test_papers100m_batch_bit_exact():
         p0, s0 = tr.activation(0)
         X = read_f32(p0, len(Fx), s0)
         assert X.tobytes() == oracle.gather_rows(gd.feats, Fx).tobytes()
+    if tr.last_rows():  # the last hop unrelabelled: rowidx and the counters cover F_{L-1}
+        FL = F[-2]
     pr, pt = tr.rowidx()  # the rows layer 1 reads: table rows rowidx[u] = slot of F_L[u]
     np.testing.assert_array_equal(read_i32(pr, len(FL)), slot[FL])
     cnt = access_counts(slot, owner, FL)
