@@ -410,7 +410,10 @@ int32_t gnnv_trainer_x_level(const gnnv_trainer* t);
  * trainer's next step on that buffer set.  Errors: GNNV_ERR_PARAM (null). */
 gnnv_status gnnv_trainer_rowidx(const gnnv_trainer* t, const int32_t** d_rowidx, const float** d_table);
 /* Device pointers of the trainer's activations for layer i (0 = X) of the
- * last step (same buffer-set caveat; X holds the rows of gnnv_trainer_x_level). */
+ * last step (same buffer-set caveat; X holds the rows of gnnv_trainer_x_level).
+ * NULL and 0 for H^1 of a 3-layer trainer whose hidden layers and output
+ * layer run over bf16 (gnnv_trainer_tail16): only its bf16 copy exists
+ * (gnnv_trainer_activation16) unless GNNV_KEEP_H1. */
 gnnv_status gnnv_trainer_activation(gnnv_trainer* t, int32_t i, const float** d_H, int32_t* stride);
 /* Layer i's aggregate A^i (1..L) of the last step: [n_dst x stride] fp32
  * (borrowed device pointer, same buffer-set caveat).  With the fused L2 push

@@ -114,6 +114,11 @@ struct gnnv_trainer {
   // are the sampled ids' cache-table rows (blocks_set_last_rows) and the
   // layer-1 aggregation reads them directly.  GNNV_NO_LASTROWS=1: relabelled
   bool last_rows = false;
+  // with hid16 and tail16 at L = 3 nothing reads H^1's fp32 rows (layer 2's
+  // GEMMs read its bf16 copy, the output layer reads H^2): layer 1's
+  // epilogue writes none (h1_fp32 false; GNNV_KEEP_H1=1 keeps them)
+  bool h1_fp32 = true;
+  int32_t* d_zero = nullptr;
   void* X16[2] = {nullptr, nullptr};
   void* A16[2] = {nullptr, nullptr};
   int32_t ld16x = 0;  // their row stride: d + 1 rounded up to 8
@@ -245,6 +250,7 @@ gnnv_status gnnv_trainer_free(gnnv_trainer* t) {
     dfree(t->G16h[i]);
   }
   dfree(t->tail_dbp);
+  dfree(t->d_zero);
   dfree(t->loss_partial);
   dfree(t->tail_dA);
   dfree(t->tail_part);
@@ -386,6 +392,9 @@ gnnv_status gnnv_trainer_create(gnnv_graph* g, gnnv_cache* c, const gnnv_model_d
       GNNV_TRY_CUDA(cudaMemset(t->d_stats, 0, 4 * sizeof(int64_t)));
       if (t->fwd16) blocks_set_rowidx(b, c->d_slot, t->rowidx[0], t->d_stats);  // k_reset writes the cache rows
       t->last_rows = t->fwd16 && !t->lastuse && !env_on("GNNV_NO_LASTROWS");
+      t->h1_fp32 = !(t->hid16 && t->tail16 && L == 3) || env_on("GNNV_KEEP_H1");
+      t->d_zero = (int32_t*)dmalloc(sizeof(int32_t), "zero");
+      GNNV_TRY_CUDA(cudaMemset(t->d_zero, 0, sizeof(int32_t)));
       if (t->last_rows) blocks_set_last_rows(b, c->d_slot);
       for (auto& e : t->ev) GNNV_TRY_CUDA(cudaEventCreate(&e));
       // buffer set 0; set 1 is allocated by the first gnnv_trainer_prefetch
@@ -448,8 +457,9 @@ gnnv_status gnnv_trainer_set_params(gnnv_trainer* t, const float* host_params) {
 gnnv_status gnnv_trainer_activation(gnnv_trainer* t, int32_t i, const float** d_H, int32_t* stride) {
   return guarded([&] {
     GNNV_REQUIRE(t && d_H && stride && i >= 0 && i <= t->md.L, GNNV_ERR_PARAM, "trainer_activation: bad args");
-    *d_H = t->H[i];
-    *stride = t->Hs[i];
+    const bool none = i == 1 && !t->h1_fp32;  // only the bf16 copy (gnnv_trainer_activation16)
+    *d_H = none ? nullptr : t->H[i];
+    *stride = none ? 0 : t->Hs[i];
   });
 }
 
@@ -848,7 +858,7 @@ gnnv_status gnnv_step(gnnv_trainer* t, const int32_t* seeds, int32_t n_seeds, in
         if (i <= L - 2) {  // this layer's output: a bf16 copy, fp32 rows for the next dst prefix
           io.y16 = t->H16[i];
           io.ld16 = t->ld16[i];
-          io.keep_rows = b->d_sizes + (L - i - 1);
+          io.keep_rows = (i == 1 && !t->h1_fp32) ? t->d_zero : b->d_sizes + (L - i - 1);
         }
         if (i >= 2 && i - 1 <= L - 2) {  // aggregate the previous layer's bf16 copy
           io.src16 = t->H16[i - 1];

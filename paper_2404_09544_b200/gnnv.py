@@ -570,7 +570,7 @@ class Trainer:
         p = C.c_void_p()
         st = C.c_int32()
         _check(load().gnnv_trainer_activation(self.h, i, C.byref(p), C.byref(st)))
-        return int(p.value), int(st.value)
+        return int(p.value or 0), int(st.value)
 
     def aggregate(self, i: int):
         """(device pointer, stride) of layer i's aggregate A^i of the last step."""

@@ -66,6 +66,16 @@ def bf16_round(x):
     return r.view(np.float32).astype(np.float64)
 
 
+def read_activation(tr, i, rows):
+    """H^i's rows as stored: the fp32 rows, or -- when the trainer keeps none
+    (H^1 at L = 3 with the bf16 hidden-layer paths) -- its bf16 copy."""
+    p, s = tr.activation(i)
+    if p:
+        return read_f32(p, rows, s)
+    p16, ld = tr.activation16(i)
+    return read_bf16(p16, rows, ld)
+
+
 def layer1_aggregate(tr, n_dst):
     """A^1 of the trainer's last step as stored: the fp32 rows, or -- when
     layer 1 keeps only the bf16 copy (gnnv_trainer_fwd16, reading Q33) --
@@ -192,15 +202,20 @@ def check_forward_chain(tr, hb, dims, w, rtol, name, X0=None, max_rows=2048, kin
         ob = blks[i] = _blk(hb, L - i)
         p_in, s_in = tr.activation(i - 1)
         p_out, s_out = tr.activation(i)
+        # H^1 without fp32 rows (gnnv_trainer_activation NULL): its bf16 copy,
+        # which is also what layer 2 read; the output check then allows the
+        # copy's rounding on top of rtol
+        out16 = not p_out and i >= 1
+        in16 = not p_in and i >= 2
         pushed_in = push and 2 <= i <= L - 1  # A^i came from layer i-1's epilogue
         pushed_out = push and i <= L - 2  # H^i stored for the next dst prefix only
         if i == 1 and X0 is not None:
             Hin = X0
         elif pushed_in:
-            Hin = read_f32(p_in, ob.n_dst, s_in)[:, : dims[i - 1]]  # the dst prefix the GPU stored
+            Hin = read_activation(tr, i - 1, ob.n_dst)[:, : dims[i - 1]]  # the dst prefix the GPU stored
         else:
-            Hin = read_f32(p_in, ob.n_src, s_in)[:, : dims[i - 1]]
-        Hout = read_f32(p_out, (_blk(hb, L - i - 1).n_dst if pushed_out else ob.n_dst), s_out)[:, : dims[i]]
+            Hin = read_activation(tr, i - 1, ob.n_src)[:, : dims[i - 1]]
+        Hout = read_activation(tr, i, (_blk(hb, L - i - 1).n_dst if pushed_out else ob.n_dst))[:, : dims[i]]
         H[i - 1], H[i] = Hin, Hout
         Wi, bi = w[i - 1]
         if pushed_in and bf16:
@@ -252,7 +267,11 @@ def check_forward_chain(tr, hb, dims, w, rtol, name, X0=None, max_rows=2048, kin
             blk, Hs = sub_block(ob, Hin, rows)
             Ho, _ = layer_fwd(blk, Hs, Wi, bi, i < L, kind)
             Hm, _ = layer_fwd(blk, Hs, Wi, bi, i < L, kind, absval=True)
-            assert_close_cond(Hout[rows], Ho, Hm, rtol, f"{name} layer {i} (sampled rows)")
+            if out16:  # the bf16 copy stands for the fp32 rows: + its rounding
+                assert_close_cond(Hout[rows], Ho, (rtol + 2.0 ** -8) / rtol * Hm, rtol,
+                                  f"{name} layer {i} (bf16 copy, sampled rows)")
+            else:
+                assert_close_cond(Hout[rows], Ho, Hm, rtol, f"{name} layer {i} (sampled rows)")
             if bf16 and pushed_out:  # the bf16 copy beyond the prefix, on sampled rows: + bf16 rounding
                 p16, ld16 = tr.activation16(i)
                 H16 = read_bf16(p16, ob.n_dst, ld16)[:, : dims[i]]
