@@ -1,5 +1,6 @@
 // C-ABI glue: errors, graph load, NCCL comm, blocks handles (host code).
 #include <dlfcn.h>
+#include <cub/device/device_scan.cuh>
 #include <limits.h>
 #include <string.h>
 
@@ -505,7 +506,17 @@ void blocks_set_rowidx(gnnv_blocks* b, const int32_t* d_slot, int32_t* d_rowidx,
   b->d_rowidx = d_rowidx;
   b->d_rowidx_stats = d_stats;
 }
-void blocks_set_last_rows(gnnv_blocks* b, const int32_t* d_slot) { b->last_rows = d_slot; }
+void blocks_set_last_rows(gnnv_blocks* b, const int32_t* d_slot) {
+  b->last_rows = d_slot;
+  // cub temporary of the last hop's offsets scan (shared with the CSC scans)
+  size_t tmp = 0;
+  GNNV_TRY_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, b->d_cnt, b->d_indptr[b->L - 1], (int)b->max_n[b->L - 1]));
+  if (tmp > b->csc_tmp_bytes) {
+    dfree(b->d_csc_tmp);
+    b->d_csc_tmp = dmalloc(tmp, "scan temporary");
+    b->csc_tmp_bytes = tmp;
+  }
+}
 void blocks_enable_lastuse(gnnv_blocks* b) {
   if (b->d_lastv) return;
   b->d_lastv = (uint32_t*)dmalloc(b->max_n[b->L] * sizeof(uint32_t), "last-use slots");

@@ -632,6 +632,19 @@ __global__ void k_csc_fill(int hp, int kp, const int32_t* sizes, const int32_t* 
 // F_L row's cache row, rowidx[i] = slot[F[i]], and the gather counters of
 // a cache that holds every row (n_L local hits) -- the trainer then needs
 // no gather pass.
+// the last hop kept as table rows: F_L = F_{L-1}; its edge count and the
+// CSR's closing offset from the exclusive sum of the row counts
+__global__ void k_last_hop_sizes(int32_t* sizes, int L, int32_t* indptr, const int32_t* cnt) {
+  GNNV_PDL_ENTRY();
+  if (threadIdx.x == 0) {
+    const int n = sizes[L - 1];
+    const int e = n ? indptr[n - 1] + cnt[n - 1] : 0;
+    indptr[n] = e;
+    sizes[L] = n;
+    sizes[L + 1 + (L - 1)] = e;
+  }
+}
+
 __global__ void k_reset(const int32_t* __restrict__ F, const int32_t* sizes, int L, int64_t N, int32_t* tag,
                         const int32_t* __restrict__ slot, int32_t* __restrict__ rowidx,
                         unsigned long long* __restrict__ stats) {
@@ -732,6 +745,17 @@ void launch_sample(gnnv_graph* g, gnnv_blocks* b, const int32_t* d_seeds, int32_
       launch_k(k_winners, grid_for(rows_ub * k, 1024), 256, 0, s, g->n, h, k, b->d_sizes, b->d_ell, b->d_cnt, b->d_tag,
                b->d_own[h]);
       GNNV_CHECK_LAUNCH();
+    }
+    if (!tagh) {
+      // the last hop as table rows numbers no new ids: its CSR offsets are a
+      // plain exclusive sum of the row counts (cub, over the row capacity;
+      // entries past the hop's n are never read), the totals fixed up after
+      size_t tmp = b->csc_tmp_bytes;
+      GNNV_TRY_CUDA(cub::DeviceScan::ExclusiveSum(b->d_csc_tmp, tmp, b->d_cnt, b->d_indptr[h], (int)rows_ub, s));
+      GNNV_CHECK_LAUNCH();
+      launch_k(k_last_hop_sizes, 1, 32, 0, s, b->d_sizes, L, b->d_indptr[h], b->d_cnt);
+      GNNV_CHECK_LAUNCH();
+      continue;
     }
     launch_k(k_relabel_scan, tiles_ub, kScanTile, 0, s, g->n, h, k, L, b->d_ell, b->d_cnt, b->d_tag, b->d_F,
                                                   b->d_indptr[h], b->d_own[h], b->d_sizes, b->d_scan,
