@@ -1074,6 +1074,47 @@ def test_tiny_batches_bf16_paths(mini, n):
         tr.free()
 
 
+@pytest.mark.parametrize("seeds", [[5], [5, 0, 2, 4], [0, 1, 2, 3]])
+def test_last_hop_table_rows_degenerate(seeds):
+    """The whole-table TF32 trainer's unrelabelled last hop (its CSR offsets
+    a plain exclusive sum of the row counts) on a graph with an
+    isolated vertex: a batch whose every hop is empty (seed 5 alone: no edge
+    in any block, the closing offset 0), one mixing the isolated seed with
+    rows of fewer neighbours than the fanout, and one without it; L = 3 so
+    every bf16 operand path is on.  Serial and pipelined (Eq.4 prefetch)
+    steps against the oracle: loss at the tf32 bound, every layer and dW/db
+    through the oracle's chains."""
+    lib()
+    gd = tiny_graph("isolated", d=6, C=3)
+    g = gnnv.Graph.from_data(gd)
+    dims = [gd.d, 64, 64, gd.C]
+    fan = [3, 2, 2]
+    w = init_weights(dims)
+    seeds = np.array(seeds)
+    n = len(seeds)
+    for pipelined in (False, True):
+        tr = gnnv.Trainer(g, gnnv.Cache(g, 1.0), dims, fan, 4, w, prec=gnnv.PREC_TF32)
+        try:
+            assert tr.last_rows() and tr.fwd16()
+            if pipelined:
+                tr.prefetch(seeds, n, 41)
+            loss, _ = tr.step(seeds, n, n, 41, 0.0)
+            ref = train_step(gd.indptr, gd.indices, gd.feats, gd.d, gd.labels, seeds, fan, 41, w, 0.0)
+            assert abs(loss - ref["loss"]) <= 5e-3 * abs(ref["loss"]), (pipelined, loss, ref["loss"])
+            # every layer and dW/db through the oracle's chains over the
+            # operands the GPU read (a 4-row batch leaves no averaging to
+            # hide bf16 rounding in a normwise end-to-end bound)
+            L = len(fan)
+            hb = blocks_to_host(tr.blocks)
+            grads = gnnv.unflat_params(tr.grads(), dims)
+            X0 = oracle.gather_rows(gd.feats, hb[L - 1][4])[:, : dims[0]]
+            tag = f"degenerate{n}{'p' if pipelined else 's'}"
+            H, Aagg, blks = check_forward_chain(tr, hb, dims, w, RTOL[2], tag, X0=X0, max_rows=10**9)
+            check_backward_chain(tr, blks, H, Aagg, dims, w, grads, gd.labels[seeds], n, RTOL[2], tag)
+        finally:
+            tr.free()
+
+
 @pytest.mark.parametrize("kind", [gnnv.KIND_SAGE, gnnv.KIND_GCN])
 @pytest.mark.parametrize("ratio", [0.3, 1.0])
 def test_prefetched_layer1_aggregation_bitwise(mini, option, kind, ratio):
