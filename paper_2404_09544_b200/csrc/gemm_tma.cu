@@ -260,6 +260,7 @@ struct Params {
   CUtensorMap ty16;      // fwd: the bf16 copy (unswizzled boxes of 32 x 32 bf16)
   int two;      // A has a second source (SAGE [H_dst | A])
   int f16;      // fwd: bf16 operands (kind::f16; 64-element k-blocks, same 128-byte rows)
+  int bres;     // fwd: B (W^T) loaded once per CTA and kept resident; stages carry A only
   int nkb1;     // fwd: K blocks served by X1 (ceil(K1/32)); dw: 32-col blocks of X1
   int nkb;      // fwd/dx: K blocks in total
   int BN;       // N per tile (fwd/dx: mult of 16; dw: mult of 32)
@@ -369,12 +370,16 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_tma_gemm(const __grid_constant_
   // [16 x 128] fp32, then G [16 x BN], then (fused mask) H [16 x BN].
   const int a_bytes = MODE == MODE_DW ? MT * DW_KR * BM * 4 : BM * BKB;
   const int g_bytes = MODE == MODE_DW ? DW_KR * BN * (p.g16 ? 2 : 4) : (PAIR ? BN / 2 : BN) * BKB;
-  const int b_bytes = MODE == MODE_DW ? g_bytes + (p.mask ? DW_KR * p.nwp * 4 : 0) : g_bytes;
+  const bool bres = MODE == MODE_FWD && !PAIR && p.bres;
+  const int b_bytes = MODE == MODE_DW ? g_bytes + (p.mask ? DW_KR * p.nwp * 4 : 0) : bres ? 0 : g_bytes;
   const int stage_bytes = a_bytes + b_bytes;
+  // resident B (bres): the nkb k-blocks of W^T [BN rows x 128B] first, then the A stages
+  uint8_t* sres = smem;
+  uint8_t* sst = smem + (bres ? (size_t)p.nkb * g_bytes : (size_t)0);
   // dW: two K-major SW64 tiles (64B rows = 16 tf32 of K) built by the transposers;
   // fwd/dX: one 4 KB SW128 output staging buffer per epilogue warp (TMA store)
   const int kt_bytes = MODE == MODE_DW ? (MT * BM + BN) * 64 : 0;
-  uint8_t* kbuf = smem + (((size_t)S * stage_bytes + 1023) & ~(size_t)1023);  // swizzle-atom aligned
+  uint8_t* kbuf = sst + (((size_t)S * stage_bytes + 1023) & ~(size_t)1023);  // swizzle-atom aligned
   uint8_t* obuf = kbuf;
   const int extra = MODE == MODE_DW ? 2 * kt_bytes : NE * 4096 * (PAIR ? PAIR_OB : 1);
   uint64_t* bars = reinterpret_cast<uint64_t*>(kbuf + extra);
@@ -387,6 +392,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_tma_gemm(const __grid_constant_
   uint64_t* s_tbar = tempty + 2;                          // [8] tile ring barriers
   int* s_tile = reinterpret_cast<int*>(s_tbar + 8);       // [8] tile ring slots
   uint32_t* s_tmem = reinterpret_cast<uint32_t*>(s_tile + 8);
+  uint64_t* bfull = reinterpret_cast<uint64_t*>(s_tmem + 2);  // bres: W^T resident
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int M = *p.dM;
 
@@ -421,6 +427,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_tma_gemm(const __grid_constant_
       mbar_init(&tempty[b], PAIR ? 2 * NE : NE);  // PAIR: the leader's, both CTAs' epilogue warps
     }
     for (int i = 0; i < 8; ++i) mbar_init(&s_tbar[i], 1);
+    mbar_init(bfull, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (PAIR) cluster_sync_all();  // the peer's barriers exist before any remote arrive / TMA
@@ -494,9 +501,14 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_tma_gemm(const __grid_constant_
               r4[j] = m < M ? __ldg(p.x1_rows + m) : 0;
             }
           }
+          if (bres && lt == 0 && lane == 0) {  // W^T once: nkb boxes on their own barrier
+            mbar_arrive_tx(bfull, (uint32_t)(p.nkb * g_bytes));
+            for (int kb = 0; kb < p.nkb; ++kb)
+              tma_load_2d(sres + (size_t)kb * g_bytes, &p.tb, kb * (p.f16 ? 2 * BK : BK), 0, bfull);
+          }
           for (int kb = 0; kb < p.nkb; ++kb, ++it) {
             const int s = it % S;
-            uint8_t* sa = smem + (size_t)s * stage_bytes;
+            uint8_t* sa = sst + (size_t)s * stage_bytes;
             uint8_t* sb = sa + a_bytes;
             if (lane == 0) {
               if (it >= S) mbar_wait(&empty[s], ((it / S) & 1) ^ 1);
@@ -511,7 +523,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_tma_gemm(const __grid_constant_
             } else {
               tma_load_2d(sa, &p.ta1, kb * kc, mt * BM, &full[s]);
             }
-            if (lane == 0) tma_load_2d(sb, &p.tb, kb * kc, nt * BN, &full[s]);
+            if (lane == 0 && !bres) tma_load_2d(sb, &p.tb, kb * kc, nt * BN, &full[s]);
           }
           if (dyn) {
             int next = 0;
@@ -561,13 +573,14 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_tma_gemm(const __grid_constant_
           }
           const int acc = lt & 1;
           if (lt >= 2) mbar_wait(&tempty[acc], ((lt >> 1) & 1) ^ 1);
+          if (bres && lt == 0) mbar_wait(bfull, 0);
           tc_after();
           for (int kb = 0; kb < p.nkb; ++kb, ++it) {
             const int s = it % S;
             mbar_wait(&full[s], (it / S) & 1);
             tc_after();
-            const uint32_t a0 = smem_u32(smem + (size_t)s * stage_bytes);
-            const uint32_t b0 = a0 + a_bytes;
+            const uint32_t a0 = smem_u32(sst + (size_t)s * stage_bytes);
+            const uint32_t b0 = bres ? smem_u32(sres + (size_t)kb * g_bytes) : a0 + a_bytes;
             // 32 bytes of K per MMA in both kinds (8 tf32 / 16 bf16)
             if (f16) {
 #pragma unroll
@@ -1421,18 +1434,21 @@ static Arena g_img;
 static Arena g_dwpart;  // gemm_dw16's per-CTA slices
 static Arena g_dbpart;  // its G conversion's per-block column sums
 
-static size_t smem_bytes(int mode, int BN, int mask, int nwp, bool pair = false, int g16 = 0) {
+// bres_nkb > 0: the forward's W^T resident (bres_nkb k-blocks of BN x 128B), stages of A only
+static size_t smem_bytes(int mode, int BN, int mask, int nwp, bool pair = false, int g16 = 0, int bres_nkb = 0) {
   const int S = mode == MODE_DW ? (g16 ? DW_STAGES16 : DW_STAGES) : pair ? PAIR_STAGES : FWD_STAGES;
   const int a = mode == MODE_DW ? DW_MT * DW_KR * BM * 4 : BM * BKB;
-  const int b = mode == MODE_DW ? DW_KR * BN * (g16 ? 2 : 4) + (mask ? DW_KR * nwp * 4 : 0) : (pair ? BN / 2 : BN) * BKB;
+  const int b = mode == MODE_DW ? DW_KR * BN * (g16 ? 2 : 4) + (mask ? DW_KR * nwp * 4 : 0)
+                : bres_nkb ? 0 : (pair ? BN / 2 : BN) * BKB;
   const int k = mode == MODE_DW ? 2 * (DW_MT * BM + BN) * 64 : NE * 4096 * (pair ? PAIR_OB : 1);
-  return (((size_t)S * (a + b) + 1023) & ~(size_t)1023) + k + 8 * (2 * S + 8 + 8) + 32 + 16 + 1024;
+  return (size_t)bres_nkb * BN * BKB + (((size_t)S * (a + b) + 1023) & ~(size_t)1023) + k + 8 * (2 * S + 8 + 8) +
+         32 + 16 + 16 + 1024;
 }
 
 template <int MODE>
 static void launch(const Params& p, dim3 grid, cudaStream_t s) {
   static size_t attr = 0;  // dynamic smem opt-in, raised to the largest request seen
-  const size_t bytes = smem_bytes(MODE, p.BN, p.mask, p.nwp, false, p.g16);
+  const size_t bytes = smem_bytes(MODE, p.BN, p.mask, p.nwp, false, p.g16, MODE == MODE_FWD && p.bres ? p.nkb : 0);
   if (bytes > attr) {
     GNNV_TRY_CUDA(cudaFuncSetAttribute(k_tma_gemm<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
     attr = bytes;
@@ -1871,6 +1887,11 @@ bool gemm_fwd_tma(const GemmFwdArgs& a, cudaStream_t s) {
   GNNV_REQUIRE(!a.push_out || (a.push_colptr && a.push_dst && a.push_indptr && a.keep_rows && a.push_ld % 4 == 0 &&
                                a.push_ld >= a.N),
                GNNV_ERR_PARAM, "fwd: incomplete fused-push arguments");
+  // W^T resident in shared memory when it fits beside the A stages and the
+  // epilogue buffers (layer 1 over [X16 | A16]: 4 k-blocks, 128 KB): each
+  // tile then streams only its A rows instead of re-reading W^T from L2
+  p.bres = f16 && !pair && !a.x1_rows && !env_on("GNNV_NO_BRES") &&
+           smem_bytes(MODE_FWD, BN, 0, 0, false, 0, nkb) <= (size_t)227 * 1024;
   p.sched = pair ? nullptr : next_sched();
   const int64_t tiles = ceil_div(std::max<int64_t>(a.max_M, 1), BM);
   if (pair) {
