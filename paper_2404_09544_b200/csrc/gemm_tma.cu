@@ -710,6 +710,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_tma_gemm(const __grid_constant_
             tmem_pin32(r[1]);
             const int64_t m = (int64_t)row0 + lane;
             const bool rag = row0 + 32 > M;
+            uint32_t bw[2] = {0u, 0u};  // the pieces' ReLU bits, stored after the proxy fence
 #pragma unroll
             for (int h2 = 0; h2 < 2; ++h2) {
               const int c = c0 + 32 * h2;
@@ -738,7 +739,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_tma_gemm(const __grid_constant_
                   bits |= (v[j] > 0.f ? 1u : 0u) << j;
                 }
               }
-              if (p.bits && m < M) p.bits[m * p.bits_ld + (c >> 5)] = bits;
+              bw[h2] = bits;
               if (store_rows && rag) {  // ragged fp32 prefix rows: plain stores of the rows < M
                 if (m < M)
 #pragma unroll
@@ -779,6 +780,13 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_tma_gemm(const __grid_constant_
               for (int h2 = 0; h2 < 2; ++h2)
                 if (c0 + 32 * h2 < BN && c0 + 32 * h2 < p.ld16) tma_store_2d(&p.ty16, ob0 + h2 * 2048, c0 + 32 * h2, row0);
               asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+            }
+            // the ReLU bits after the fence: a global store ahead of it would
+            // hold the fence's CTA-scope membar for the store's round trip
+            if (p.bits && m < M) {
+              uint32_t* bp = p.bits + m * p.bits_ld + (c0 >> 5);
+              bp[0] = bw[0];
+              if (c0 + 32 < BN) bp[1] = bw[1];
             }
           }
         } else
