@@ -102,6 +102,7 @@ __global__ void __launch_bounds__(TA_WARPS * 32, 1) k_tail_a(
   float* s_w = s_x + TA_ROWS * L.xs;    // [C8][ws]   W^T (zero columns c >= C)
   float* s_z = s_w + (size_t)C8 * L.ws; // [32][zs]   logits, then dZ
   __shared__ float s_loss[TA_WARPS];
+  __shared__ uint32_t s_hb[TA_ROWS * 16];  // the seed rows' ReLU-bit words (d <= 512), for the dX pass
   const int n = *d_ndst;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int g = lane >> 2, t = lane & 3;
@@ -143,6 +144,7 @@ __global__ void __launch_bounds__(TA_WARPS * 32, 1) k_tail_a(
     my[q] = lane < cnt[q] ? __ldg(indices + beg + lane) : 0;
     ownm[q] = ok ? own[v] : 0u;
     yv[q] = ok ? __ldg(labels + F[v]) : 0;
+    if (lane < 16) s_hb[r * 16 + lane] = (ok && 32 * lane < d) ? __ldg(hbits + (int64_t)v * hbits_ld + lane) : 0u;
     float4 hs[CPL], ag[CPL];
 #pragma unroll
     for (int j = 0; j < CPL; ++j) {
@@ -276,7 +278,7 @@ __global__ void __launch_bounds__(TA_WARPS * 32, 1) k_tail_a(
         if (v >= n) continue;
         const float x0 = acc[2 * h], x1 = acc[2 * h + 1];
         if (col < d) {
-          const uint32_t word = __ldg(hbits + (int64_t)v * hbits_ld + (col >> 5));
+          const uint32_t word = s_hb[r * 16 + (col >> 5)];
           const uint32_t b = word >> (col & 31);
           const float m0 = b & 1u ? x0 : 0.f, m1 = b & 2u ? x1 : 0.f;
           if (B16) {
