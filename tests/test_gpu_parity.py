@@ -1186,6 +1186,36 @@ def test_lastuse_l2_hints_bitwise_neutral(mini, option, prec, ratio):
         assert a_.tobytes() == b_.tobytes()
 
 
+def test_fwd16_resident_w_bitwise(mini, option):
+    """Layer 1's bf16 forward GEMM with W^T resident in shared memory (the
+    default when it fits) against the same GEMM streaming W^T with every A
+    stage (GNNV_NO_BRES=1): the MMAs read the same operands in the same
+    order, so the loss and every activation level (layer 1's bf16 copy, the
+    later layers' rows) are bitwise identical; both forward epilogues store
+    the ReLU bits after the proxy fence."""
+    gd, g = mini
+    cfg = CONFIGS["mini"]
+    dims = [gd.d, cfg["hidden"], cfg["hidden"], gd.C]
+    L = len(cfg["fanouts"])
+    w = init_weights(dims)
+    seeds = epoch_seeds(gd.n, 1)[: cfg["batch"]]
+    out = {}
+    for name in ("resident", "streamed"):
+        option("GNNV_NO_BRES", 1 if name == "streamed" else 0)
+        tr = gnnv.Trainer(g, gnnv.Cache(g, 1.0), dims, cfg["fanouts"], cfg["batch"], w, prec=gnnv.PREC_TF32)
+        try:
+            assert tr.fwd16()
+            loss, _ = tr.step(seeds, len(seeds), len(seeds), 0xB2E5, 0.0)
+            hb = blocks_to_host(tr.blocks)
+            acts = [read_activation(tr, lvl, hb[L - 1 - lvl][0]) for lvl in range(1, L)]
+            out[name] = (loss, acts)
+        finally:
+            tr.free()
+    assert out["resident"][0] == out["streamed"][0]
+    for a_, b_ in zip(out["resident"][1], out["streamed"][1]):
+        assert a_.tobytes() == b_.tobytes()
+
+
 @pytest.mark.parametrize("aggr", [gnnv.AGGR_MEAN, gnnv.AGGR_SUM])
 @pytest.mark.parametrize("ratio", [0.3, 1.0])
 def test_fused_l2_push_matches_per_layer_aggregation(mini, option, aggr, ratio):
