@@ -1186,16 +1186,18 @@ def test_lastuse_l2_hints_bitwise_neutral(mini, option, prec, ratio):
         assert a_.tobytes() == b_.tobytes()
 
 
-def test_fwd16_resident_w_bitwise(mini, option):
+@pytest.mark.parametrize("hidden", [64, 256])
+def test_fwd16_resident_w_bitwise(mini, option, hidden):
     """Layer 1's bf16 forward GEMM with W^T resident in shared memory (the
     default when it fits) against the same GEMM streaming W^T with every A
     stage (GNNV_NO_BRES=1): the MMAs read the same operands in the same
     order, so the loss and every activation level (layer 1's bf16 copy, the
     later layers' rows) are bitwise identical; both forward epilogues store
-    the ReLU bits after the proxy fence."""
+    the ReLU bits after the proxy fence.  Hidden 64 and 256 (the resident
+    image is BN x 128 bytes per k-block: 32 KB per k-block at 256)."""
     gd, g = mini
     cfg = CONFIGS["mini"]
-    dims = [gd.d, cfg["hidden"], cfg["hidden"], gd.C]
+    dims = [gd.d, hidden, hidden, gd.C]
     L = len(cfg["fanouts"])
     w = init_weights(dims)
     seeds = epoch_seeds(gd.n, 1)[: cfg["batch"]]
