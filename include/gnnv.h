@@ -108,7 +108,9 @@ const char* gnnv_last_error(void);
  * GNNV_NO_PDL, GNNV_NO_BF16ACT (Q30), GNNV_NO_BF16TABLE (Q31), GNNV_NO_DW16
  * (Q32), GNNV_NO_FWD16 (Q33), GNNV_NO_HID16 and GNNV_NO_TAIL16 (Q34),
  * GNNV_NO_DA16 (fp32 dA in the bf16 push), GNNV_NO_BRES (the bf16 forward
- * GEMM re-reads W^T per tile instead of keeping it in shared memory).
+ * GEMM re-reads W^T per tile instead of keeping it in shared memory),
+ * GNNV_NO_EPPIPE (its epilogue loads each pass's TMEM columns at the top of
+ * the pass instead of one pass ahead).
  * Integer options:
  * GNNV_PF_CAP (CTA cap of the Eq.4 prefetch's launches, 0 = none),
  * GNNV_PF_PRIO (its stream priority), GNNV_DW16_MINKB (k-blocks per CTA

@@ -254,7 +254,7 @@ gnnv_status gnnv_set_option(const char* name, int32_t value) {
                                   "GNNV_PF_AGG",     "GNNV_NO_BF16ACT",   "GNNV_NO_BF16TABLE", "GNNV_NO_DW16",
                                   "GNNV_PF_CAP",     "GNNV_NO_FWD16",     "GNNV_NO_HID16",   "GNNV_DW16_MINKB",
                                   "GNNV_HID16_DW",   "GNNV_PF_PRIO",      "GNNV_BWD_NARROW", "GNNV_NO_TAIL16",
-                                  "GNNV_NO_DA16",    "GNNV_NO_LASTROWS", "GNNV_KEEP_H1",     "GNNV_NO_BRES"};
+                                  "GNNV_NO_DA16",    "GNNV_NO_LASTROWS", "GNNV_KEEP_H1",     "GNNV_NO_BRES",   "GNNV_NO_EPPIPE"};
     GNNV_REQUIRE(name, GNNV_ERR_PARAM, "set_option: null name");
     bool ok = false;
     for (const char* k : known) ok |= strcmp(k, name) == 0;

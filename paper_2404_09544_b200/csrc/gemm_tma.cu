@@ -261,6 +261,7 @@ struct Params {
   int two;      // A has a second source (SAGE [H_dst | A])
   int f16;      // fwd: bf16 operands (kind::f16; 64-element k-blocks, same 128-byte rows)
   int bres;     // fwd: B (W^T) loaded once per CTA and kept resident; stages carry A only
+  int eppipe;   // fwd bf16 epilogue: next pass's TMEM loads issued before this pass's fence
   int nkb1;     // fwd: K blocks served by X1 (ceil(K1/32)); dw: 32-col blocks of X1
   int nkb;      // fwd/dx: K blocks in total
   int BN;       // N per tile (fwd/dx: mult of 16; dw: mult of 32)
@@ -696,15 +697,23 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_tma_gemm(const __grid_constant_
           // contiguous columns; both TMEM loads in flight, one staging
           // round and one proxy fence for both bf16 pieces)
           const uint32_t ob_u32 = smem_u32(ob0);
-          for (int c0 = half * 64; c0 < BN; c0 += 128) {
-            uint32_t r[2][32];
+          uint32_t r[2][32];
+          // the next pass's TMEM loads are issued as soon as this pass's
+          // packed pieces are in shared memory, so their latency overlaps
+          // the proxy fence, the TMA stores and the ReLU-bit stores
+          auto ld_pass = [&](int cp) {
 #pragma unroll
             for (int h2 = 0; h2 < 2; ++h2) {
-              const int c = c0 + 32 * h2;
+              const int c = cp + 32 * h2;
               if (c >= BN) continue;
               if (BN - c >= 32) tmem_ld32_nw(tbase + c, r[h2]);
               else tmem_ld16_nw(tbase + c, r[h2]);
             }
+          };
+          const bool epp = p.eppipe != 0;
+          if (half * 64 < BN) ld_pass(half * 64);
+          for (int c0 = half * 64; c0 < BN; c0 += 128) {
+            if (!epp && c0 != half * 64) ld_pass(c0);
             asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
             tmem_pin32(r[0]);
             tmem_pin32(r[1]);
@@ -774,6 +783,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_tma_gemm(const __grid_constant_
                 asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(ob_u32 + h2 * 2048 + lane * 64 + q * 16),
                              "r"(r[h2][4 * q]), "r"(r[h2][4 * q + 1]), "r"(r[h2][4 * q + 2]), "r"(r[h2][4 * q + 3])
                              : "memory");
+            if (epp && c0 + 128 < BN) ld_pass(c0 + 128);
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             __syncwarp();
             if (lane == 0) {
@@ -1900,6 +1910,7 @@ bool gemm_fwd_tma(const GemmFwdArgs& a, cudaStream_t s) {
   // tile then streams only its A rows instead of re-reading W^T from L2
   p.bres = f16 && !pair && !a.x1_rows && !env_on("GNNV_NO_BRES") &&
            smem_bytes(MODE_FWD, BN, 0, 0, false, 0, nkb) <= (size_t)227 * 1024;
+  p.eppipe = !env_on("GNNV_NO_EPPIPE");
   p.sched = pair ? nullptr : next_sched();
   const int64_t tiles = ceil_div(std::max<int64_t>(a.max_M, 1), BM);
   if (pair) {
