@@ -19,8 +19,11 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("rep")
     ap.add_argument("--top", type=int, default=15)
+    ap.add_argument("--kernel", default="", help="substring of the kernel to summarise (default: the first)")
     a = ap.parse_args()
-    det = subprocess.run(["ncu", "-i", a.rep, "--page", "details", "--csv"], capture_output=True, text=True).stdout
+    filt = ["-k", f"regex:{a.kernel}", "-c", "1"] if a.kernel else []
+    det = subprocess.run(["ncu", "-i", a.rep, "--page", "details", "--csv"] + filt, capture_output=True,
+                         text=True).stdout
     r = list(csv.reader(io.StringIO(det)))
     h = r[0]
     ki, ni, ui, vi, ii = (h.index(x) for x in ("Kernel Name", "Metric Name", "Metric Unit", "Metric Value", "ID"))
@@ -30,7 +33,7 @@ def main():
             continue
         seen.add(x[ni])
         print(f"{x[ki][:60]} | {x[ni]}: {x[vi]} {x[ui]}")
-    src = subprocess.run(["ncu", "-i", a.rep, "--page", "source", "--csv", "--print-source", "cuda,sass"],
+    src = subprocess.run(["ncu", "-i", a.rep, "--page", "source", "--csv", "--print-source", "cuda,sass"] + filt,
                          capture_output=True, text=True).stdout
     k, f = -1, None
     by, txt = collections.Counter(), {}
